@@ -1,0 +1,455 @@
+"""Benchmark of the contraction hot path on B200 (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--op entries|entries5|full|dot|norm] [--no-secondary]
+
+Headline (BASELINE.json metric, configs[1] = "cfg2"): batched entry
+evaluation t[idx] of a TT chain with N=10 modes of size 32 and ranks 32 on
+2^24 uniform int64 index tuples per GPU.  A step is one K1 launch over the
+whole resident batch; inputs (1.34 GB of indices) exceed the 126 MB L2, so
+no flush is needed between steps.  Multi-GPU runs shard samples: every rank
+evaluates its own 2^24 tuples (weak scaling, no data-path collective); the
+time is the max over ranks.
+
+``--impl reference`` times the reference's CPU algorithm (the numpy port in
+oracle/, a restatement of core.py:394-444) on the host cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+PROFILES = os.path.join(ROOT, "profiles")
+M_PER_GPU = 1 << 24
+CPU_SAMPLE = 1 << 20       # cpu_baseline sample (rows of the same workload)
+REF_STEP_SAMPLE = 1 << 19  # --impl reference: rows per timed step
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--op", default="entries", choices=["entries", "entries5", "full", "dot", "norm"])
+    ap.add_argument("--algo", type=int, default=0)
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (NVML; the recipe's nvidia-smi query)
+
+class ClockSampler:
+    REASONS = {
+        "sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+        "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+    }
+
+    def __init__(self, device_index):
+        self.samples, self.reasons, self.stop_ev = [], set(), threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            import torch
+
+            bus = torch.cuda.get_device_properties(device_index).pci_bus_id
+            self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode() if isinstance(bus, str) else bus) \
+                if bus else pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.nv = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # noqa: BLE001
+            self.err = repr(e)
+
+    def _run(self):
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, bit in self.REASONS.items():
+                    if mask & bit:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            self.stop_ev.wait(0.1)
+
+    def __enter__(self):
+        if self.ok:
+            self.th = threading.Thread(target=self._run, daemon=True)
+            self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self.stop_ev.set()
+            self.th.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": getattr(self, "err", "no samples")}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+
+def load_json(name):
+    p = os.path.join(PROFILES, name)
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return None
+
+
+def fp32_peak():
+    """Measured FFMA peak (tools/peaks.cu, committed in profiles/), else the
+    nominal 148 SMs x 128 FMA/clk x 2 x 1.965 GHz."""
+    pk = load_json("peaks_r01.json")
+    if pk and pk.get("fp32_ffma_tflops"):
+        return pk["fp32_ffma_tflops"], "measured (profiles/peaks_r01.json, tools/peaks.cu FFMA)"
+    return 148 * 128 * 2 * 1.965e9 / 1e12, "nominal (148 SM x 128 FMA/clk x 2 x 1.965 GHz)"
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)["hbm_gbs"], "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+
+        n = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"]
+        return max(n) if n else 1
+    except Exception:  # noqa: BLE001
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference's CPU algorithm on the host
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import tntz_oracle as O
+
+    seed = W.base_seed()
+    shape, rank_ = W.CONFIGS["cfg2"][1], W.CONFIGS["cfg2"][2]
+    chain = O.make_chain([("tt", c) for c in W.tt_cores(shape, rank_, seed)])
+    idx = W.indices(shape, REF_STEP_SAMPLE, seed + 2)
+    for _ in range(args.warmup):
+        O.entries(chain, idx)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.entries(chain, idx)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = REF_STEP_SAMPLE * args.steps / total
+    cores = blas_threads()
+    line = {
+        "impl": "reference", "metric": "TT entries/sec (t[idx])", "value": value, "unit": "entries/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": cfg2_config(args.gpus, REF_STEP_SAMPLE),
+        "cpu_baseline": {"value": value, "unit": "entries/s", "cores": cores, "kind": "port",
+                         "sample": f"{REF_STEP_SAMPLE} rows of the cfg2 workload per step; numpy port "
+                                   "of tntz entries (core.py:394-444), float64, OpenBLAS threads"},
+        "e2e": {"value": value, "unit": "entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cfg2_config(n, m):
+    return {"workload": "cfg2: " + W.CONFIGS["cfg2"][0], "samples_per_step_per_gpu": m,
+            "modes": 10, "mode_size": 32, "rank": 32, "index_dtype": "int64",
+            "parallelism": f"dp{n} (sample shards)",
+            "l2": "inputs larger than L2 (1.34 GB of indices per step per GPU), no flush"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+def timed_steps(fn, steps, warmup, stream, dist):
+    import torch
+
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    if dist:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        torch.distributed.barrier()
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms
+
+
+def bench_entries(args, cfg, dev, dist, ws, rank):
+    """K1 on cfg2 (default) or cfg5; returns the JSON fields."""
+    import torch
+
+    import paper_2206_11128_b200 as tb
+    from paper_2206_11128_b200 import core as C
+
+    seed = W.base_seed()
+    if cfg == "cfg2":
+        shape, r = W.CONFIGS["cfg2"][1], W.CONFIGS["cfg2"][2]
+        t = tb.TnTensor([tb.ModeNode("tt", c) for c in W.tt_cores(shape, r, seed)])
+        m = M_PER_GPU
+    else:
+        shape = W.CONFIGS["cfg5"][1]
+        t = tb.TnTensor([tb.ModeNode(k, c, f) for k, c, f in W.hybrid_nodes(seed)])
+        m = 1 << 26
+    p = t._packed()
+    modes = [("diag" if md.layout == 1 else "dense", md.r_left, md.r_right) for md in p.modes]
+    flops_per_entry = W.entry_flops(modes)
+    idx_host = torch.from_numpy(W.indices(shape, m, seed + 2 + rank)).pin_memory()
+    idx = idx_host.to(dev)
+    out = torch.empty(m, dtype=torch.float32, device=dev)
+    err = torch.empty(1, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    wsbuf = [None]
+
+    def step():
+        wsbuf[0] = C.launch_entries(p, idx, out, err, args.algo, wsbuf[0])
+
+    with ClockSampler(dev.index) as clk:
+        ms = timed_steps(step, args.steps, args.warmup, stream, dist)
+    assert int(err.item()) >= t.ndim, "bench inputs must be in bounds"
+    ms_step = ms / args.steps
+    value = ws * m / (ms_step * 1e-3)
+    achieved = flops_per_entry * m / (ms_step * 1e-3) / 1e12
+    peak, peak_src = fp32_peak()
+    ncu = load_json(f"ncu_{cfg}_entries.json") or {}
+    roof = {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak, "traffic": ncu.get("dram_bytes_per_launch"),
+            "peak_source": peak_src,
+            "algorithmic": f"{flops_per_entry} flop/entry (2*r_l*r_r per dense mode, R per diag mode) x {m} entries per launch",
+            "hbm_view": {"bytes_per_launch": (8 * len(shape) + 4) * m,
+                         "achieved_gbs": (8 * len(shape) + 4) * m / (ms_step * 1e-3) / 1e9}}
+    fields = {"value": value, "ms_per_step": ms_step, "roofline": roof, "clocks": clk.summary(),
+              "gpu_launches": args.steps}
+    # e2e through the public API from pinned host memory: H2D of the step's
+    # indices + K1 + D2H of the step's output, every step
+    e2e_steps = max(2, min(args.steps, 3))
+
+    def e2e_step():
+        res = tb.entries(t, idx_host)  # façade: H2D, launch, error-word check
+        host = res.cpu()
+        return host
+
+    e2e_step()
+    torch.cuda.synchronize()
+    if dist:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    if dist:
+        tt_ = torch.tensor([el], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(tt_, op=torch.distributed.ReduceOp.MAX)
+        el = float(tt_.item())
+    fields["e2e"] = {"value": ws * m * e2e_steps / el, "unit": "entries/s",
+                     "h2d_bytes_per_step": idx_host.numel() * 8, "d2h_bytes_per_step": m * 4,
+                     "steps": e2e_steps, "path": "paper_2206_11128_b200.entries(t, pinned host int64) + .cpu()"}
+    fields["_t"], fields["_out"], fields["_idx_host"] = t, out, idx_host
+    return fields
+
+
+def cpu_baseline_entries(t_nodes_fn, idx_host, out_dev, m_sample):
+    """The oracle (numpy port of core.py:394-444) on the first m_sample rows
+    of the same workload; doubles as the parity gate for the timed output."""
+    from oracle import tntz_oracle as O
+
+    chain = O.make_chain(t_nodes_fn())
+    idx = idx_host[:m_sample].numpy()
+    O.entries(chain, idx[:4096])  # warm-up
+    t0 = time.perf_counter()
+    ref = O.entries(chain, idx)
+    el = time.perf_counter() - t0
+    got = out_dev[:m_sample].double().cpu().numpy()
+    err = O.rel_errors(got, ref)
+    return {"value": m_sample / el, "unit": "entries/s", "cores": blas_threads(), "kind": "port",
+            "sample": f"first {m_sample} rows of the same workload; numpy port of tntz entries "
+                      "(core.py:394-444), float64, OpenBLAS threads"}, err
+
+
+def bench_full(dev, steps, warmup, dist):
+    """K2 on cfg3: full() of a TT N=4, I=256, r=64 -> 17.18 GB fp32."""
+    import torch
+
+    import paper_2206_11128_b200 as tb
+
+    shape, r = W.CONFIGS["cfg3"][1], W.CONFIGS["cfg3"][2]
+    t = tb.TnTensor([tb.ModeNode("tt", c) for c in W.tt_cores(shape, r, W.base_seed())])
+    t._packed()
+    out = torch.empty(shape, dtype=torch.float32, device=dev)
+    from paper_2206_11128_b200 import _native as N
+    import ctypes
+
+    p = t._packed()
+    lib = N.load()
+    wsb = lib.tnb_full_workspace_bytes(ctypes.byref(p.chain), 0, shape[0])
+    wsbuf = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+    st = N.stream_ptr(dev)
+
+    def step():
+        N.check(lib.tnb_full_f32(ctypes.byref(p.chain), 0, shape[0], out.data_ptr(),
+                                 wsbuf.data_ptr(), wsb, st), "full")
+
+    ms = timed_steps(step, steps, warmup, torch.cuda.current_stream(dev), dist) / steps
+    nbytes = out.numel() * 4
+    del out
+    return {"op": "full", "workload": "cfg3", "ms_per_step": ms, "GB/s": nbytes / (ms * 1e-3) / 1e9,
+            "bytes_written": nbytes}
+
+
+def bench_dot(dev, steps, warmup, dist, is_norm=False):
+    """K3 on cfg4: 4096 pairs of TTs (N=16, I=64, r=16); cores drawn on the
+    device (torch, seeded) since only their shapes matter for timing."""
+    import ctypes
+
+    import torch
+
+    import paper_2206_11128_b200 as tb
+    from paper_2206_11128_b200 import _native as N
+
+    shape, r = W.CONFIGS["cfg4"][1], W.CONFIGS["cfg4"][2]
+    g = torch.Generator(device=dev)
+    g.manual_seed(W.base_seed())
+    ranks = [1] + [r] * (len(shape) - 1) + [1]
+
+    def mk():
+        return tb.TnTensor([tb.ModeNode("tt", torch.randn((4096, ranks[k], s, ranks[k + 1]), device=dev,
+                                                          generator=g) * 0.25, batched=True)
+                            for k, s in enumerate(shape)], 4096)
+
+    a, b = mk(), mk()
+    pa, pb = a._packed(), b._packed()
+    out = torch.empty(4096, dtype=torch.float32, device=dev)
+    lib = N.load()
+    st = N.stream_ptr(dev)
+
+    def step():
+        if is_norm:
+            N.check(lib.tnb_norm_f32(ctypes.byref(pa.chain), out.data_ptr(), st), "norm")
+        else:
+            N.check(lib.tnb_dot_f32(ctypes.byref(pa.chain), ctypes.byref(pb.chain), out.data_ptr(), st), "dot")
+
+    ms = timed_steps(step, steps, warmup, torch.cuda.current_stream(dev), dist) / steps
+    per_pair = sum(ranks[k] * s * ranks[k + 1] for k, s in enumerate(shape)) * 4
+    nbytes = 4096 * per_pair * (1 if is_norm else 2)
+    return {"op": "norm" if is_norm else "dot", "workload": "cfg4", "ms_per_step": ms,
+            "pairs/s": 4096 / (ms * 1e-3), "GB/s": nbytes / (ms * 1e-3) / 1e9}
+
+
+def run_ours(args):
+    import torch
+
+    ws, rank, local = dist_env()
+    dist = ws > 1
+    if dist:
+        torch.distributed.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    line = {"metric": "TT entries/sec (t[idx])", "unit": "entries/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic"}
+    if args.op in ("entries", "entries5"):
+        cfg = "cfg2" if args.op == "entries" else "cfg5"
+        f = bench_entries(args, cfg, dev, dist, ws, rank)
+        t, out, idx_host = f.pop("_t"), f.pop("_out"), f.pop("_idx_host")
+        line.update(f)
+        line["config"] = cfg2_config(ws, M_PER_GPU) if cfg == "cfg2" else {
+            "workload": "cfg5: " + W.CONFIGS["cfg5"][0], "samples_per_step_per_gpu": 1 << 26,
+            "parallelism": f"dp{ws} (sample shards)", "l2": "inputs larger than L2, no flush"}
+        if rank == 0 and ws == 1 and not args.no_cpu:
+            seed = W.base_seed()
+            nodes_fn = (lambda: [("tt", c) for c in W.tt_cores(W.CONFIGS["cfg2"][1], 32, seed)]) \
+                if cfg == "cfg2" else (lambda: W.hybrid_nodes(seed))
+            cb, perr = cpu_baseline_entries(nodes_fn, idx_host, out, CPU_SAMPLE)
+            line["cpu_baseline"] = cb
+            line["parity_gate"] = {"rows": CPU_SAMPLE, **perr,
+                                   "pass": perr["rel_fro"] <= 1e-5 and perr["max_rel"] <= 1e-5}
+            if not line["parity_gate"]["pass"]:
+                line["value"] = None
+                line["error"] = "parity gate failed: throughput not reported"
+        del out
+        torch.cuda.empty_cache()
+        if not args.no_secondary and ws == 1:
+            sec = []
+            for fn in (lambda: bench_full(dev, 3, 2, dist), lambda: bench_dot(dev, 5, 2, dist),
+                       lambda: bench_dot(dev, 5, 2, dist, True)):
+                try:
+                    sec.append(fn())
+                except Exception as e:  # noqa: BLE001
+                    sec.append({"error": repr(e)})
+                torch.cuda.empty_cache()
+            line["secondary"] = sec
+    elif args.op == "full":
+        r = bench_full(dev, args.steps, args.warmup, dist)
+        line.update({"metric": "full() GB/s", "unit": "GB/s", "value": r["GB/s"] * ws,
+                     "ms_per_step": r["ms_per_step"], "config": {"workload": "cfg3"}})
+    else:
+        r = bench_dot(dev, args.steps, args.warmup, dist, args.op == "norm")
+        line.update({"metric": f"{args.op}s/sec", "unit": "pairs/s", "value": r["pairs/s"] * ws,
+                     "ms_per_step": r["ms_per_step"], "config": {"workload": "cfg4"}})
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,163 @@
+/*
+ * tnb.h -- C ABI of the B200-native contraction hot path (libtnb.so).
+ *
+ * Drop-in boundary for the reference's hot path, /root/reference/pkg/src/tntz:
+ *   entries   core.py:394-460   (t[idx] via indexing.py:120-130)
+ *   full      core.py:337-359   (TnTensor.full, core.py:176-177)
+ *   chain_dot core.py:362-384   (arithmetic.dot, arithmetic.py:189-193)
+ *   norm      core.py:387-391   (TnTensor.norm, core.py:179-180)
+ *   per-node preparation: promote_cp_node core.py:266-296,
+ *                         node_tt_core core.py:307-327, apply_factor 330-334
+ *
+ * The reference is a pure-Python API with no FFI; these entry points are what
+ * its ctypes binding would call.  Conventions:
+ *   - every pointer to tensor data is a DEVICE pointer (fp32 values, int64
+ *     indices), row-major / C order;
+ *   - the caller owns every buffer; workspace sizes are queried first;
+ *   - every launch is asynchronous on the given stream (a cudaStream_t, passed
+ *     as void*; NULL = legacy default stream);
+ *   - status codes only, no exceptions cross the ABI; tnb_last_error() gives a
+ *     thread-local message for the last non-zero status;
+ *   - no global mutable state: calls on distinct streams/threads are safe.
+ */
+#ifndef TNB_H_
+#define TNB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define TNB_OK 0
+#define TNB_EINVAL 1      /* shape / rank / argument contract violated        */
+#define TNB_EINDEX 2      /* reserved: index errors are reported via err_mode */
+#define TNB_ECUDA 3       /* CUDA launch or runtime error                      */
+#define TNB_EWORKSPACE 4  /* workspace smaller than the queried size          */
+
+/* node kinds (core.py:29-30) */
+#define TNB_KIND_TT 0
+#define TNB_KIND_CP 1
+
+/* repacked slice layouts */
+#define TNB_LAYOUT_DENSE 0 /* [B?][J][r_left][r_right] contiguous r_l x r_r tiles */
+#define TNB_LAYOUT_DIAG 1  /* [B?][J][R]: interior CP node, diagonal copy-tensor */
+
+/* CP positions (core.py:32-34) */
+#define TNB_POS_INTERIOR 0
+#define TNB_POS_LEFT 1
+#define TNB_POS_RIGHT 2
+#define TNB_POS_SINGLE 3 /* one-mode chain: the copy tensor reduces to a sum */
+
+/* entries algorithm selector (0 = automatic) */
+#define TNB_ALGO_AUTO 0
+#define TNB_ALGO_LAYERED 1  /* one launch per mode over a global state buffer */
+#define TNB_ALGO_CHAIN 2    /* one thread per sample, cores via L1/L2          */
+#define TNB_ALGO_BUCKETED 3 /* per-CTA counting sort, warp-shared core slices  */
+
+/*
+ * One node exactly as the reference stores it (ModeNode, core.py:41-99).
+ * TT core: [B?][r_left][internal][r_right]; CP core: [B?][internal][rank].
+ * factor (Tucker basis, J x I): [B?][phys][internal] or NULL.
+ */
+typedef struct {
+  int32_t kind;     /* TNB_KIND_TT / TNB_KIND_CP                        */
+  int32_t internal; /* I = core.shape[-2]                                */
+  int32_t phys;     /* J = factor.shape[-2] if factor else I             */
+  int32_t r_left;   /* TT: core.shape[-3]; CP: rank R                    */
+  int32_t r_right;  /* TT: core.shape[-1]; CP: rank R                    */
+  int32_t pad_;
+  const float* core;
+  const float* factor;
+} tnb_node;
+
+/* One repacked mode operator, as the kernels consume it. */
+typedef struct {
+  int32_t layout;  /* TNB_LAYOUT_DENSE / TNB_LAYOUT_DIAG            */
+  int32_t phys;    /* J                                             */
+  int32_t r_left;  /* effective chain ranks (CP: 1 outward at ends) */
+  int32_t r_right;
+  float* slices;   /* see TNB_LAYOUT_*                              */
+} tnb_mode;
+
+typedef struct {
+  int32_t n_modes;
+  int32_t pad_;
+  int64_t batch; /* 0 = unbatched, else B: every mode has a leading B axis */
+  const tnb_mode* modes; /* HOST array of n_modes descriptors */
+} tnb_chain;
+
+/* --- library ------------------------------------------------------------ */
+const char* tnb_version(void);
+const char* tnb_last_error(void);
+/* Returns TNB_OK when a device of compute capability 10.x is current. */
+int tnb_device_check(void);
+
+/* --- K0: per-node preparation ------------------------------------------- */
+/*
+ * Validates the rank chain (core.py:244-263, boundary ranks 1 core.py:131-133)
+ * and fills layout/phys/r_left/r_right of modes[0..n) (slices untouched).
+ * Replaces the implicit per-call node_tt_core of core.py:307-327.
+ */
+int tnb_plan_modes(const tnb_node* nodes, int32_t n_modes, tnb_mode* modes);
+/* Number of floats mode k's repacked slices occupy (per the plan). */
+int64_t tnb_mode_floats(const tnb_mode* mode, int64_t batch);
+/*
+ * Fills modes[k].slices: promotes CP nodes (core.py:266-296) and absorbs
+ * Tucker factors (apply_factor, core.py:330-334) once per tensor.
+ */
+int tnb_repack_f32(const tnb_node* nodes, int32_t n_modes, int64_t batch,
+                   const tnb_mode* modes, void* stream);
+/*
+ * Dense TT core of mode k in the reference layout [B?][r_l][J][r_r]
+ * (node_tt_core with absorb_factor=True, core.py:307-327).
+ */
+int tnb_tt_core_f32(const tnb_chain* chain, int32_t k, float* out, void* stream);
+/*
+ * promote_cp_node (core.py:266-296) of one CP node, factor NOT applied:
+ * out is [B?][1|R][I][R|1] (TNB_POS_LEFT/INTERIOR/RIGHT) or [B?][1][I][1]
+ * (TNB_POS_SINGLE, the sum of core.py:316-320).
+ */
+int tnb_promote_cp_f32(const tnb_node* node, int32_t position, int64_t batch,
+                       float* out, void* stream);
+
+/* --- K1: entry evaluation  (core.py:394-460) ----------------------------- */
+/*
+ * idx: int64 [m][n_modes] row-major, raw user indices (negatives allowed);
+ * out: fp32 [m] (unbatched) or [m][batch].
+ * err_mode: device int32; on completion it holds the LOWEST mode that had an
+ * index outside [-J, J) (the ContractViolationError "index out of bounds on
+ * mode k" of core.py:409-416), or a value >= n_modes when all were valid.
+ * When it reports an error the contents of out are unspecified.
+ */
+int64_t tnb_entries_workspace_bytes(const tnb_chain* chain, int64_t m, int32_t algo);
+int tnb_entries_f32(const tnb_chain* chain, const int64_t* idx, int64_t m,
+                    float* out, int32_t* err_mode, int32_t algo,
+                    void* workspace, int64_t workspace_bytes, void* stream);
+
+/* --- K2: dense decompression  (core.py:337-359) -------------------------- */
+/*
+ * Writes the C-order slab of full(t) whose leading (mode-0) index lies in
+ * [lead_lo, lead_hi): (lead_hi-lead_lo) * prod(J_1..J_{N-1}) floats, per batch
+ * element (batched: out is [B][slab]).  [0, J_0) is the whole tensor; a slab
+ * equals the reference's full(t[lo:hi]) (indexing.py:132-137).
+ */
+int64_t tnb_full_workspace_bytes(const tnb_chain* chain, int64_t lead_lo, int64_t lead_hi);
+int tnb_full_f32(const tnb_chain* chain, int64_t lead_lo, int64_t lead_hi, float* out,
+                 void* workspace, int64_t workspace_bytes, void* stream);
+
+/* --- K3: inner products  (core.py:362-391) ------------------------------- */
+/*
+ * out[e] = <a_e, b_e> for every batch element (one float when unbatched).
+ * Shapes and batching must agree (ContractViolationError in core.py:368-371).
+ */
+int tnb_dot_f32(const tnb_chain* a, const tnb_chain* b, float* out, void* stream);
+/* out[e] = sqrt(max(<t_e, t_e>, 0))  (core.py:387-391) */
+int tnb_norm_f32(const tnb_chain* t, float* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TNB_H_ */

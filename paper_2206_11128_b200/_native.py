@@ -1,0 +1,117 @@
+"""ctypes binding of libtnb.so (the C ABI declared in include/tnb.h).
+
+There is deliberately no fallback: if the library is missing or no sm_100
+device is present, every compute entry point raises :class:`NativeError`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from ctypes import POINTER, c_char_p, c_int, c_int32, c_int64, c_void_p
+from pathlib import Path
+
+from .errors import ContractViolationError, NativeError
+
+LIB_PATH = Path(__file__).resolve().parent / "libtnb.so"
+
+TNB_OK, TNB_EINVAL, TNB_EINDEX, TNB_ECUDA, TNB_EWORKSPACE = 0, 1, 2, 3, 4
+KIND_TT, KIND_CP = 0, 1
+LAYOUT_DENSE, LAYOUT_DIAG = 0, 1
+POS_INTERIOR, POS_LEFT, POS_RIGHT, POS_SINGLE = 0, 1, 2, 3
+ALGO_AUTO, ALGO_LAYERED, ALGO_CHAIN, ALGO_BUCKETED = 0, 1, 2, 3
+
+
+class TnbNode(ctypes.Structure):
+    _fields_ = [("kind", c_int32), ("internal", c_int32), ("phys", c_int32),
+                ("r_left", c_int32), ("r_right", c_int32), ("pad_", c_int32),
+                ("core", c_void_p), ("factor", c_void_p)]
+
+
+class TnbMode(ctypes.Structure):
+    _fields_ = [("layout", c_int32), ("phys", c_int32), ("r_left", c_int32),
+                ("r_right", c_int32), ("slices", c_void_p)]
+
+
+class TnbChain(ctypes.Structure):
+    _fields_ = [("n_modes", c_int32), ("pad_", c_int32), ("batch", c_int64),
+                ("modes", POINTER(TnbMode))]
+
+
+# name -> (restype, argtypes); exactly the declarations of include/tnb.h
+SIGNATURES = {
+    "tnb_version": (c_char_p, []),
+    "tnb_last_error": (c_char_p, []),
+    "tnb_device_check": (c_int, []),
+    "tnb_plan_modes": (c_int, [POINTER(TnbNode), c_int32, POINTER(TnbMode)]),
+    "tnb_mode_floats": (c_int64, [POINTER(TnbMode), c_int64]),
+    "tnb_repack_f32": (c_int, [POINTER(TnbNode), c_int32, c_int64, POINTER(TnbMode), c_void_p]),
+    "tnb_tt_core_f32": (c_int, [POINTER(TnbChain), c_int32, c_void_p, c_void_p]),
+    "tnb_promote_cp_f32": (c_int, [POINTER(TnbNode), c_int32, c_int64, c_void_p, c_void_p]),
+    "tnb_entries_workspace_bytes": (c_int64, [POINTER(TnbChain), c_int64, c_int32]),
+    "tnb_entries_f32": (c_int, [POINTER(TnbChain), c_void_p, c_int64, c_void_p, c_void_p,
+                                c_int32, c_void_p, c_int64, c_void_p]),
+    "tnb_full_workspace_bytes": (c_int64, [POINTER(TnbChain), c_int64, c_int64]),
+    "tnb_full_f32": (c_int, [POINTER(TnbChain), c_int64, c_int64, c_void_p, c_void_p,
+                             c_int64, c_void_p]),
+    "tnb_dot_f32": (c_int, [POINTER(TnbChain), POINTER(TnbChain), c_void_p, c_void_p]),
+    "tnb_norm_f32": (c_int, [POINTER(TnbChain), c_void_p, c_void_p]),
+}
+
+_lock = threading.Lock()
+_lib = None
+_device_ok = set()
+
+
+def load() -> ctypes.CDLL:
+    """Loads libtnb.so once; raises NativeError when it is not built."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise NativeError(
+                    f"{LIB_PATH} is missing: build it with "
+                    "`python -m paper_2206_11128_b200._build` (no CPU fallback exists)")
+            lib = ctypes.CDLL(str(LIB_PATH))
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+        return _lib
+
+
+def last_error() -> str:
+    return load().tnb_last_error().decode(errors="replace")
+
+
+def check(rc: int, what: str) -> None:
+    """Maps a libtnb status to the reference's exception classes."""
+    if rc == TNB_OK:
+        return
+    msg = last_error()
+    if rc in (TNB_EINVAL, TNB_EINDEX):
+        raise ContractViolationError(f"{what}: {msg}")
+    raise NativeError(f"{what}: {msg} (status {rc})")
+
+
+def require_device(device) -> None:
+    """Fails loudly unless ``device`` is an sm_100 CUDA device."""
+    import torch
+
+    if device is None or device.type != "cuda" or not torch.cuda.is_available():
+        raise NativeError("paper_2206_11128_b200 computes on a CUDA (sm_100a) device only; "
+                          "no CPU fallback exists")
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    if idx in _device_ok:
+        return
+    lib = load()
+    with torch.cuda.device(idx):
+        check(lib.tnb_device_check(), "device check")
+    _device_ok.add(idx)
+
+
+def stream_ptr(device) -> int:
+    import torch
+
+    return torch.cuda.current_stream(device).cuda_stream

@@ -1,0 +1,446 @@
+"""Blended CP / TT / Tucker chains held on a B200, contracted by libtnb.
+
+Drop-in for the reference's core model and hot path
+(/root/reference/pkg/src/tntz/core.py):
+
+============================  ==========================================
+reference                     here
+============================  ==========================================
+ModeNode      core.py:41-99   :class:`ModeNode` (same kinds, shapes, checks)
+TnTensor      core.py:102-241 :class:`TnTensor` (same validation/messages)
+promote_cp_node core.py:266   :func:`promote_cp_node` (K0 kernel)
+node_tt_core  core.py:307     :func:`node_tt_core` (K0 kernel)
+full          core.py:337     :func:`full` (K2: step kernels + one GEMM)
+chain_dot     core.py:362     :func:`chain_dot` (K3)
+norm          core.py:387     :func:`norm` (K3)
+entries       core.py:394     :func:`entries` (K1)
+============================  ==========================================
+
+Intended deviations (BASELINE north_star): values are fp32 (the reference
+upcasts to float64, core.py:37-38) and results are CUDA ``torch.Tensor``s
+(unbatched ``dot``/``norm`` still return a Python ``float``).  Cores are
+repacked once per tensor into the kernels' layout (K0) and cached; values
+are immutable, exactly as the reference requires, so the
+cache never goes stale.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Iterable, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import ContractViolationError, StructuralError
+
+TT = "tt"
+CP = "cp"
+
+INTERIOR = "interior"
+LEFT_BOUNDARY = "left_boundary"
+RIGHT_BOUNDARY = "right_boundary"
+
+_POS = {INTERIOR: N.POS_INTERIOR, LEFT_BOUNDARY: N.POS_LEFT, RIGHT_BOUNDARY: N.POS_RIGHT}
+
+
+def _default_device() -> torch.device:
+    if torch.cuda.is_available():
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def _as_f32(a) -> torch.Tensor:
+    """fp32, contiguous, on the current CUDA device when one exists."""
+    if isinstance(a, torch.Tensor):
+        t = a.detach()
+        dev = t.device if t.device.type == "cuda" else _default_device()
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float32)))
+        dev = _default_device()
+    return t.to(device=dev, dtype=torch.float32).contiguous()
+
+
+class ModeNode:
+    """One node of the chain: a core plus an optional basis factor
+    (core.py:41-99).  ``kind`` is ``"tt"`` (``r_left x I x r_right``) or
+    ``"cp"`` (``I x R``); batched nodes carry one extra leading axis."""
+
+    __slots__ = ("kind", "core", "factor", "batched")
+
+    def __init__(self, kind: str, core, factor=None, batched: bool = False):
+        if kind not in (TT, CP):
+            raise ContractViolationError(f"unknown node kind {kind!r}")
+        core = _as_f32(core)
+        expected = (3 if kind == TT else 2) + (1 if batched else 0)
+        if core.dim() != expected:
+            raise StructuralError(
+                f"{kind} core must have {expected} axes, got shape {tuple(core.shape)}")
+        if factor is not None:
+            factor = _as_f32(factor)
+            if factor.dim() != 2 + (1 if batched else 0):
+                raise StructuralError(
+                    f"factor must have {2 + batched} axes, got shape {tuple(factor.shape)}")
+            if factor.shape[-1] != core.shape[-2]:
+                raise StructuralError(
+                    f"factor maps onto internal size {factor.shape[-1]}, "
+                    f"core has internal size {core.shape[-2]}")
+            if factor.device != core.device:
+                factor = factor.to(core.device)
+        self.kind = kind
+        self.core = core
+        self.factor = factor
+        self.batched = bool(batched)
+
+    @property
+    def internal_size(self) -> int:
+        return int(self.core.shape[-2])
+
+    @property
+    def physical_size(self) -> int:
+        if self.factor is not None:
+            return int(self.factor.shape[-2])
+        return self.internal_size
+
+    @property
+    def cp_rank(self) -> int:
+        if self.kind != CP:
+            raise ContractViolationError("cp_rank is only defined for CP nodes")
+        return int(self.core.shape[-1])
+
+    def copy(self) -> "ModeNode":
+        return ModeNode(self.kind, self.core, self.factor, self.batched)
+
+    def _native(self) -> N.TnbNode:
+        nd = N.TnbNode()
+        nd.kind = N.KIND_TT if self.kind == TT else N.KIND_CP
+        nd.internal = self.internal_size
+        nd.phys = self.physical_size
+        if self.kind == TT:
+            nd.r_left, nd.r_right = int(self.core.shape[-3]), int(self.core.shape[-1])
+        else:
+            nd.r_left = nd.r_right = self.cp_rank
+        nd.core = self.core.data_ptr()
+        nd.factor = self.factor.data_ptr() if self.factor is not None else None
+        return nd
+
+    def __repr__(self):
+        f = "" if self.factor is None else f", factor{tuple(self.factor.shape)}"
+        return f"ModeNode({self.kind}, core{tuple(self.core.shape)}{f})"
+
+
+class _Packed:
+    """Device-resident repacked chain (K0 output) plus its C descriptor."""
+
+    __slots__ = ("chain", "modes", "buffers", "device", "n")
+
+    def __init__(self, chain, modes, buffers, device, n):
+        self.chain, self.modes, self.buffers, self.device, self.n = chain, modes, buffers, device, n
+
+
+class TnTensor:
+    """An N-mode tensor stored as a chain of TT/CP nodes (core.py:102-241)."""
+
+    __slots__ = ("_nodes", "_batch_size", "_pack")
+
+    def __init__(self, nodes: Iterable[ModeNode], batch_size: Optional[int] = None):
+        nodes = tuple(n.copy() for n in nodes)
+        if len(nodes) == 0:
+            raise ContractViolationError("a tensor needs at least one mode")
+        if batch_size is not None and batch_size < 1:
+            raise ContractViolationError("batch size must be >= 1")
+        for k, node in enumerate(nodes):
+            if batch_size is None:
+                if node.batched:
+                    raise StructuralError(f"node {k} is batched but the tensor is not")
+            else:
+                if not node.batched:
+                    raise StructuralError(f"node {k} lacks the batch axis")
+                if node.core.shape[0] != batch_size:
+                    raise StructuralError(
+                        f"node {k} has batch {node.core.shape[0]}, expected {batch_size}")
+                if node.factor is not None and node.factor.shape[0] != batch_size:
+                    raise StructuralError(f"node {k} factor has a mismatched batch")
+        ranks = _rank_chain(nodes)
+        if ranks[0] != 1 or ranks[-1] != 1:
+            raise StructuralError(f"boundary ranks must be 1, got {ranks[0]}, {ranks[-1]}")
+        dev = nodes[0].core.device
+        if any(n.core.device != dev for n in nodes):
+            nodes = tuple(ModeNode(n.kind, n.core.to(dev),
+                                   None if n.factor is None else n.factor.to(dev), n.batched)
+                          for n in nodes)
+        self._nodes = nodes
+        self._batch_size = batch_size
+        self._pack = None
+
+    # -- metadata (core.py:139-172) ---------------------------------------
+    @property
+    def nodes(self) -> tuple:
+        return self._nodes
+
+    @property
+    def batch_size(self) -> Optional[int]:
+        return self._batch_size
+
+    @property
+    def ndim(self) -> int:
+        return len(self._nodes)
+
+    @property
+    def shape(self) -> tuple:
+        return tuple(n.physical_size for n in self._nodes)
+
+    @property
+    def ranks(self) -> list:
+        return _rank_chain(self._nodes)
+
+    @property
+    def device(self) -> torch.device:
+        return self._nodes[0].core.device
+
+    def numel(self) -> int:
+        return int(np.prod(self.shape, dtype=np.int64)) if self.ndim else 0
+
+    def dof(self) -> int:
+        b = self._batch_size or 1
+        total = 0
+        for n in self._nodes:
+            total += n.core.numel() // b
+            if n.factor is not None:
+                total += n.factor.numel() // b
+        return total
+
+    # -- conversions --------------------------------------------------------
+    def full(self, *, lead: Optional[tuple] = None) -> torch.Tensor:
+        return full(self, lead=lead)
+
+    def norm(self):
+        return norm(self)
+
+    def batch_element(self, b: int) -> "TnTensor":
+        if self._batch_size is None:
+            raise ContractViolationError("tensor is not batched")
+        nodes = [ModeNode(n.kind, n.core[b], None if n.factor is None else n.factor[b])
+                 for n in self._nodes]
+        return TnTensor(nodes)
+
+    def __repr__(self):
+        kinds = "".join("T" if n.kind == TT else "C" for n in self._nodes)
+        b = "" if self._batch_size is None else f", batch={self._batch_size}"
+        return f"TnTensor(shape={self.shape}, ranks={self.ranks}, kinds={kinds}{b})"
+
+    def __getitem__(self, key):
+        from . import indexing
+
+        return indexing.getitem(self, key)
+
+    # -- K0: repack once, cache (values are immutable) ------------------------
+    def _packed(self) -> _Packed:
+        if self._pack is not None:
+            return self._pack
+        dev = self.device
+        N.require_device(dev)
+        lib = N.load()
+        n = self.ndim
+        nodes = (N.TnbNode * n)(*[nd._native() for nd in self._nodes])
+        modes = (N.TnbMode * n)()
+        N.check(lib.tnb_plan_modes(nodes, n, modes), "plan")
+        batch = self._batch_size or 0
+        bufs = []
+        for k in range(n):
+            cnt = lib.tnb_mode_floats(ctypes.byref(modes[k]), batch)
+            buf = torch.empty(max(cnt, 1), dtype=torch.float32, device=dev)
+            modes[k].slices = buf.data_ptr()
+            bufs.append(buf)
+        with torch.cuda.device(dev):
+            N.check(lib.tnb_repack_f32(nodes, n, batch, modes, N.stream_ptr(dev)), "repack")
+        chain = N.TnbChain(n, 0, batch, ctypes.cast(modes, ctypes.POINTER(N.TnbMode)))
+        self._pack = _Packed(chain, modes, bufs, dev, n)
+        return self._pack
+
+
+TnTensor.torch = TnTensor.full  # tntorch spelling of full()
+
+
+# ---------------------------------------------------------------------------
+# rank bookkeeping (core.py:244-263)
+
+def _node_ranks(node: ModeNode, k: int, n_modes: int) -> tuple:
+    if node.kind == TT:
+        return int(node.core.shape[-3]), int(node.core.shape[-1])
+    r = node.cp_rank
+    return (1 if k == 0 else r), (1 if k == n_modes - 1 else r)
+
+
+def _rank_chain(nodes: Sequence[ModeNode]) -> list:
+    n = len(nodes)
+    pairs = [_node_ranks(node, k, n) for k, node in enumerate(nodes)]
+    for k in range(n - 1):
+        if pairs[k][1] != pairs[k + 1][0]:
+            raise StructuralError(
+                f"rank mismatch between modes {k} and {k + 1}: "
+                f"{pairs[k][1]} vs {pairs[k + 1][0]}")
+    return [pairs[0][0]] + [p[1] for p in pairs]
+
+
+# ---------------------------------------------------------------------------
+# per-node preparation (core.py:266-334), on the device
+
+def promote_cp_node(node: ModeNode, position: str) -> torch.Tensor:
+    """TT core equivalent of a CP node at a chain position (core.py:266-296)."""
+    if node.kind != CP:
+        raise ContractViolationError("promote_cp_node expects a CP node")
+    if position not in _POS:
+        raise ContractViolationError(f"unknown position {position!r}")
+    dev = node.core.device
+    N.require_device(dev)
+    r, i = node.cp_rank, node.internal_size
+    b = int(node.core.shape[0]) if node.batched else 0
+    shape = {INTERIOR: (r, i, r), LEFT_BOUNDARY: (1, i, r), RIGHT_BOUNDARY: (r, i, 1)}[position]
+    out = torch.empty(((b,) if b else ()) + shape, dtype=torch.float32, device=dev)
+    nd = ModeNode(CP, node.core, None, node.batched)._native()
+    with torch.cuda.device(dev):
+        N.check(N.load().tnb_promote_cp_f32(ctypes.byref(nd), _POS[position], b,
+                                            out.data_ptr(), N.stream_ptr(dev)), "promote_cp_node")
+    return out
+
+
+def node_tt_core(t: TnTensor, k: int) -> torch.Tensor:
+    """Effective TT core of mode k, CP promoted and factor absorbed
+    (core.py:307-327), in the reference layout (r_l, J, r_r)."""
+    if not 0 <= k < t.ndim:
+        raise ContractViolationError(f"mode {k} out of range")
+    p = t._packed()
+    m = p.modes[k]
+    b = t.batch_size
+    shape = (m.r_left, m.phys, m.r_right)
+    out = torch.empty(((b,) if b else ()) + shape, dtype=torch.float32, device=p.device)
+    with torch.cuda.device(p.device):
+        N.check(N.load().tnb_tt_core_f32(ctypes.byref(p.chain), k, out.data_ptr(),
+                                         N.stream_ptr(p.device)), "node_tt_core")
+    return out
+
+
+# ---------------------------------------------------------------------------
+# K2: dense decompression (core.py:337-359)
+
+def full(t: TnTensor, *, lead: Optional[tuple] = None) -> torch.Tensor:
+    """Dense C-order tensor (leading batch axis if batched).
+
+    ``lead=(lo, hi)`` (extension) returns only the slab whose leading index
+    lies in [lo, hi), i.e. the reference's ``full(t[lo:hi])``."""
+    p = t._packed()
+    shape = t.shape
+    lo, hi = (0, shape[0]) if lead is None else (int(lead[0]), int(lead[1]))
+    if not (0 <= lo <= hi <= shape[0]):
+        raise ContractViolationError(f"slab [{lo}, {hi}) outside mode 0 of size {shape[0]}")
+    oshape = (hi - lo,) + tuple(shape[1:])
+    if t.batch_size is not None:
+        oshape = (t.batch_size,) + oshape
+    out = torch.empty(oshape, dtype=torch.float32, device=p.device)
+    lib = N.load()
+    wsb = lib.tnb_full_workspace_bytes(ctypes.byref(p.chain), lo, hi)
+    if wsb < 0:
+        N.check(N.TNB_EINVAL, "full")
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=p.device)
+    with torch.cuda.device(p.device):
+        N.check(lib.tnb_full_f32(ctypes.byref(p.chain), lo, hi, out.data_ptr(), ws.data_ptr(),
+                                 wsb, N.stream_ptr(p.device)), "full")
+    return out
+
+
+# ---------------------------------------------------------------------------
+# K3: inner product and norm (core.py:362-391)
+
+def chain_dot(a: TnTensor, b: TnTensor):
+    if a.shape != b.shape:
+        raise ContractViolationError(f"shape mismatch: {a.shape} vs {b.shape}")
+    if a.batch_size != b.batch_size:
+        raise ContractViolationError("operands must agree on batching")
+    pa, pb = a._packed(), b._packed()
+    if pa.device != pb.device:
+        raise ContractViolationError("operands live on different devices")
+    out = torch.empty(a.batch_size or 1, dtype=torch.float32, device=pa.device)
+    with torch.cuda.device(pa.device):
+        N.check(N.load().tnb_dot_f32(ctypes.byref(pa.chain), ctypes.byref(pb.chain),
+                                     out.data_ptr(), N.stream_ptr(pa.device)), "chain_dot")
+    if a.batch_size is None:
+        return float(out[0].item())
+    return out
+
+
+def norm(t: TnTensor):
+    p = t._packed()
+    out = torch.empty(t.batch_size or 1, dtype=torch.float32, device=p.device)
+    with torch.cuda.device(p.device):
+        N.check(N.load().tnb_norm_f32(ctypes.byref(p.chain), out.data_ptr(),
+                                      N.stream_ptr(p.device)), "norm")
+    if t.batch_size is None:
+        return float(out[0].item())
+    return out
+
+
+# ---------------------------------------------------------------------------
+# K1: entry evaluation (core.py:394-460)
+
+def _index_tensor(t: TnTensor, indices, device) -> torch.Tensor:
+    """Shape/dtype normalisation of core.py:402-408; returns a 2-D tensor."""
+    if isinstance(indices, torch.Tensor):
+        idx = indices.detach()
+    else:
+        idx = torch.from_numpy(np.ascontiguousarray(np.asarray(indices)))
+    if idx.dim() == 1:
+        idx = idx[None, :]
+    if idx.dim() != 2 or idx.shape[1] != t.ndim:
+        raise ContractViolationError(
+            f"index array must be (M, {t.ndim}), got {tuple(idx.shape)}")
+    if idx.dtype.is_floating_point:
+        # the reference lets float indices through entries(): negatives wrap,
+        # bounds are checked on the float values, and the searchsorted
+        # bucketing floors them (core.py:409-416, 435-437)
+        idx = idx.to(device=device, dtype=torch.float64)
+        size = torch.tensor(t.shape, dtype=torch.float64, device=device)
+        idx = torch.where(idx < 0, idx + size, idx)
+        if idx.numel():
+            bad = ((idx < 0) | (idx >= size)).any(dim=0).nonzero()
+            if bad.numel():
+                raise ContractViolationError(f"index out of bounds on mode {int(bad[0, 0])}")
+        idx = torch.floor(idx)
+    return idx.to(device=device, dtype=torch.int64).contiguous()
+
+
+def entries(t: TnTensor, indices, *, algo: int = N.ALGO_AUTO) -> torch.Tensor:
+    """Values at explicit multi-indices: shape (M,), or (M, B) if batched."""
+    p = t._packed()
+    idx = _index_tensor(t, indices, p.device)
+    m = int(idx.shape[0])
+    b = t.batch_size
+    out = torch.empty((m, b) if b else (m,), dtype=torch.float32, device=p.device)
+    if m == 0:
+        return out
+    err = torch.empty(1, dtype=torch.int32, device=p.device)
+    launch_entries(p, idx, out, err, algo)
+    code = int(err.item())
+    if code < t.ndim:
+        raise ContractViolationError(f"index out of bounds on mode {code}")
+    return out
+
+
+def launch_entries(p: _Packed, idx: torch.Tensor, out: torch.Tensor, err: torch.Tensor,
+                   algo: int = N.ALGO_AUTO, ws: Optional[torch.Tensor] = None):
+    """Asynchronous K1 launch on the current stream (no host sync); the
+    caller reads ``err`` (>= n_modes means every index was valid)."""
+    lib = N.load()
+    m = int(idx.shape[0])
+    wsb = lib.tnb_entries_workspace_bytes(ctypes.byref(p.chain), m, algo)
+    if wsb < 0:
+        N.check(N.TNB_EINVAL, "entries")
+    if wsb > 0 and (ws is None or ws.numel() < wsb):
+        ws = torch.empty(wsb, dtype=torch.uint8, device=p.device)
+    with torch.cuda.device(p.device):
+        N.check(lib.tnb_entries_f32(ctypes.byref(p.chain), idx.data_ptr(), m, out.data_ptr(),
+                                    err.data_ptr(), algo,
+                                    ws.data_ptr() if wsb > 0 else None, wsb,
+                                    N.stream_ptr(p.device)), "entries")
+    return ws

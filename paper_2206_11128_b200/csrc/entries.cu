@@ -1,0 +1,199 @@
+// K1: batched multi-index entry evaluation (reference: entries,
+// core.py:394-460, reached from t[idx] via indexing.py:120-130).
+//
+// Three algorithms share one contract (tnb.h):
+//   LAYERED  - one launch per mode over a global [m][B][r] state buffer; any
+//              rank, any number of modes (the reference's own mode-by-mode
+//              structure, core.py:419-429).  Needs a workspace.
+//   CHAIN    - one thread per (sample, batch element); the r-vector state
+//              lives in registers for the whole chain, cores are read through
+//              L1/L2.  Ranks <= 32.
+//   BUCKETED - entries_bucketed.cu: the performance kernel (cfg2 / cfg5).
+// Index handling is identical in all three: negatives wrap, any value outside
+// [-J, J) lowers *err to its mode number (core.py:409-416), and the kernel
+// keeps going with a clamped index so no out-of-range address is formed.
+#include "common.cuh"
+
+namespace tnb {
+int launch_entries_bucketed(const ChainDev& ch, const int64_t* idx, int64_t m, float* out,
+                            int32_t* err, cudaStream_t st);
+bool bucketed_supported(const ChainDev& ch);
+
+namespace {
+
+template <int RMAX>
+__global__ void __launch_bounds__(256) entries_chain_kernel(const __grid_constant__ ChainDev ch,
+                                                            const int64_t* __restrict__ idx,
+                                                            int64_t m, float* __restrict__ out,
+                                                            int32_t* err) {
+  const int64_t B = ch.batch;
+  const int N = ch.n;
+  const int64_t total = m * B;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = t / B;
+    const int64_t e = t - s * B;
+    const int64_t* row = idx + s * N;
+    float v[RMAX];
+#pragma unroll
+    for (int a = 0; a < RMAX; ++a) v[a] = (a == 0) ? 1.f : 0.f;
+    for (int k = 0; k < N; ++k) {
+      const ModeDev& md = ch.m[k];
+      const int j = norm_index(row[k], md.J, k, err);
+      if (md.J == 0) continue;
+      const float* g = md.s + e * md.bstride;
+      if (md.layout == TNB_LAYOUT_DIAG) {
+        g += (int64_t)j * md.rl;
+#pragma unroll
+        for (int a = 0; a < RMAX; ++a)
+          if (a < md.rl) v[a] *= __ldg(g + a);
+      } else {
+        const int rl = md.rl, rr = md.rr;
+        g += (int64_t)j * rl * rr;
+        float w[RMAX];
+#pragma unroll
+        for (int c = 0; c < RMAX; ++c) w[c] = 0.f;
+#pragma unroll
+        for (int a = 0; a < RMAX; ++a) {
+          if (a < rl) {
+            const float va = v[a];
+            const float* ga = g + a * rr;
+#pragma unroll
+            for (int c = 0; c < RMAX; ++c)
+              if (c < rr) w[c] = fmaf(va, __ldg(ga + c), w[c]);
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < RMAX; ++c) v[c] = w[c];
+      }
+    }
+    out[t] = v[0];
+  }
+}
+
+// One mode of the layered algorithm: thread per (sample, batch element, c).
+__global__ void entries_layer_kernel(ModeDev md, int k, int N, int64_t B,
+                                     const int64_t* __restrict__ idx, int64_t m,
+                                     const float* __restrict__ vin, float* __restrict__ vout,
+                                     int stride, float* __restrict__ out, int last,
+                                     int32_t* err) {
+  const int rl = md.rl, rr = md.rr;
+  const int64_t total = m * B * rr;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t se = t / rr;
+    const int c = (int)(t - se * rr);
+    const int64_t s = se / B;
+    const int64_t e = se - s * B;
+    const int j = norm_index(idx[s * N + k], md.J, k, err);
+    float acc = 0.f;
+    if (md.J > 0) {
+      const float* g = md.s + e * md.bstride;
+      const float* vi = vin ? vin + se * stride : nullptr;
+      if (md.layout == TNB_LAYOUT_DIAG) {
+        acc = (vi ? vi[c] : 1.f) * __ldg(g + (int64_t)j * rl + c);
+      } else {
+        const float* gj = g + (int64_t)j * rl * rr + c;
+        for (int a = 0; a < rl; ++a) acc = fmaf(vi ? vi[a] : 1.f, __ldg(gj + (int64_t)a * rr), acc);
+      }
+    }
+    if (last)
+      out[se] = acc;
+    else
+      vout[se * stride + c] = acc;
+  }
+}
+
+inline int grid_for(int64_t total, int threads) {
+  int64_t g = ceil_div(total, threads);
+  const int64_t cap = (int64_t)num_sms() * 16;
+  if (g > cap) g = cap;
+  return (int)(g < 1 ? 1 : g);
+}
+
+int pick_algo(const tnb_chain* c, int algo, int rmax) {
+  if (algo != TNB_ALGO_AUTO) return algo;
+  if (c->n_modes > kMaxModes || rmax > 32) return TNB_ALGO_LAYERED;
+  return TNB_ALGO_CHAIN;
+}
+
+int chain_rmax(const tnb_chain* c) {
+  int r = 1;
+  for (int k = 0; k < c->n_modes; ++k) {
+    if (c->modes[k].r_left > r) r = c->modes[k].r_left;
+    if (c->modes[k].r_right > r) r = c->modes[k].r_right;
+  }
+  return r;
+}
+
+}  // namespace
+
+int64_t entries_workspace(const tnb_chain* c, int64_t m, int algo) {
+  if (!c || !c->modes || c->n_modes < 1 || m < 0) return -1;
+  const int rmax = chain_rmax(c);
+  if (pick_algo(c, algo, rmax) != TNB_ALGO_LAYERED) return 0;
+  const int64_t B = c->batch > 0 ? c->batch : 1;
+  return 2 * m * B * (int64_t)rmax * (int64_t)sizeof(float);
+}
+
+int launch_entries(const tnb_chain* c, const int64_t* idx, int64_t m, float* out, int32_t* err,
+                   int algo, void* ws, int64_t ws_bytes, cudaStream_t st) {
+  static thread_local ChainDev ch;
+  if (!c || !c->modes) return set_error(TNB_EINVAL, "null chain");
+  const int rmax0 = chain_rmax(c);
+  const int use = pick_algo(c, algo, rmax0);
+  int rc = make_chain_dev(c, &ch, use != TNB_ALGO_LAYERED);
+  if (rc) return rc;
+  // "no error" sentinel 0x7f7f7f7f >= n_modes
+  rc = check_cuda(cudaMemsetAsync(err, 0x7f, sizeof(int32_t), st), "memset err");
+  if (rc || m == 0) return rc;
+  const int64_t B = ch.batch;
+  if (use == TNB_ALGO_CHAIN) {
+    const int64_t total = m * B;
+    const int g = grid_for(total, 256);
+    if (ch.rmax <= 8)
+      entries_chain_kernel<8><<<g, 256, 0, st>>>(ch, idx, m, out, err);
+    else if (ch.rmax <= 16)
+      entries_chain_kernel<16><<<g, 256, 0, st>>>(ch, idx, m, out, err);
+    else if (ch.rmax <= 32)
+      entries_chain_kernel<32><<<g, 256, 0, st>>>(ch, idx, m, out, err);
+    else
+      return set_error(TNB_EINVAL, "chain algorithm supports ranks <= 32, got %d", ch.rmax);
+    return check_launch("entries_chain");
+  }
+  if (use == TNB_ALGO_BUCKETED) {
+    if (!bucketed_supported(ch))
+      return set_error(TNB_EINVAL, "bucketed algorithm does not support this chain");
+    return launch_entries_bucketed(ch, idx, m, out, err, st);
+  }
+  if (use != TNB_ALGO_LAYERED) return set_error(TNB_EINVAL, "unknown entries algorithm %d", algo);
+  const int64_t need = 2 * m * B * (int64_t)ch.rmax * (int64_t)sizeof(float);
+  if (!ws || ws_bytes < need)
+    return set_error(TNB_EWORKSPACE, "entries needs %lld workspace bytes, got %lld",
+                     (long long)need, (long long)ws_bytes);
+  float* buf[2] = {(float*)ws, (float*)ws + m * B * ch.rmax};
+  const float* vin = nullptr;
+  for (int k = 0; k < c->n_modes; ++k) {
+    const tnb_mode& mm = c->modes[k];
+    ModeDev md;
+    md.s = mm.slices;
+    md.bstride = c->batch > 0 ? mode_floats(mm) : 0;
+    md.layout = mm.layout;
+    md.J = mm.phys;
+    md.rl = mm.r_left;
+    md.rr = mm.r_right;
+    const int last = (k == c->n_modes - 1);
+    float* vout = buf[k & 1];
+    const int64_t total = m * B * md.rr;
+    if (total > 0)
+      entries_layer_kernel<<<grid_for(total, 256), 256, 0, st>>>(md, k, c->n_modes, B, idx, m,
+                                                                 vin, vout, ch.rmax, out, last,
+                                                                 err);
+    rc = check_launch("entries_layer");
+    if (rc) return rc;
+    vin = vout;
+  }
+  return TNB_OK;
+}
+
+}  // namespace tnb

@@ -1,0 +1,373 @@
+// K2: dense decompression (reference: full, core.py:337-359).
+//
+// The reference accumulates the chain left to right through 2-D unfoldings,
+// m = m @ g.reshape(r_l, J*r_r) (core.py:345-351).  Here the chain is split at
+// a rank edge p: a left partial L = G_0..G_{p-1} of shape (prod_{k<p} J_k, r_p)
+// and a right partial R = G_p..G_{N-1} of shape (r_p, prod_{k>=p} J_k) are
+// built by small step kernels, and ONE GEMM out = L @ R produces the C-order
+// output.  That last GEMM is the whole cost: it writes prod(J) floats and is
+// bound by HBM write bandwidth when its FLOPs run on tensor cores
+// (full_tc.cu); the SIMT GEMM below is the generic path.
+// A slab [lo, hi) of the leading mode restricts L's rows, which is the
+// reference's own full(t[lo:hi]) (indexing.py:132-137); it is also how the
+// multi-GPU runner shards full() across devices.
+#include <vector>
+
+#include "common.cuh"
+
+namespace tnb {
+// tcgen05 3xTF32 GEMM (full_tc.cu); returns false when the shape is unsupported
+bool tc_gemm_supported(int64_t M, int64_t N, int K, int64_t lda, int64_t ldb, int64_t ldc);
+int launch_tc_gemm(const float* A, int64_t lda, int64_t sA, const float* B, int64_t ldb,
+                   int64_t sB, float* C, int64_t ldc, int64_t sC, int64_t M, int64_t N, int K,
+                   int64_t batch, cudaStream_t st);
+
+namespace {
+
+struct Step {
+  int k;
+  int64_t rows;  // left: P rows of the input; right: columns n of the input
+};
+
+struct FullPlan {
+  int n = 0;
+  int p = 0;            // split edge, 1 <= p <= n
+  int64_t slab_rows = 0;
+  int64_t rowsL = 0;    // rows of L
+  int64_t colsR = 0;    // columns of R
+  int64_t l_buf = 0;    // floats per batch element per L ping-pong buffer
+  int64_t r_buf = 0;    // floats per batch element per R ping-pong buffer
+  int64_t out_per = 0;  // floats per batch element of the output slab
+};
+
+int make_plan(const tnb_chain* c, int64_t lo, int64_t hi, FullPlan* P) {
+  if (!c || !c->modes || c->n_modes < 1) return set_error(TNB_EINVAL, "null chain");
+  const int n = c->n_modes;
+  const tnb_mode* m = c->modes;
+  if (lo < 0 || hi < lo || hi > m[0].phys)
+    return set_error(TNB_EINVAL, "slab [%lld, %lld) outside leading mode of size %d",
+                     (long long)lo, (long long)hi, m[0].phys);
+  P->n = n;
+  P->slab_rows = hi - lo;
+  // out size per batch element
+  int64_t out_per = P->slab_rows;
+  for (int k = 1; k < n; ++k) out_per *= m[k].phys;
+  P->out_per = out_per;
+  // choose p by a weighted FMA count (step kernels ~4x less efficient than
+  // the final GEMM) with a memory tie-break
+  double best = -1;
+  for (int p = 1; p <= n; ++p) {
+    double cost = 0, mem = 0;
+    double rows = (double)P->slab_rows;
+    for (int k = 1; k < p; ++k) {
+      const double f = (m[k].layout == TNB_LAYOUT_DIAG) ? 1.0 : (double)m[k].r_right;
+      const double w = (k == n - 1 && p == n) ? 1.0 : 4.0;  // last step writes out
+      cost += w * rows * m[k].phys * m[k].r_left * f;
+      rows *= m[k].phys;
+      mem += rows * m[k].r_right;
+    }
+    double cols = 1;
+    if (p < n) {
+      cols = m[n - 1].phys;
+      for (int k = n - 2; k >= p; --k) {
+        const double f = (m[k].layout == TNB_LAYOUT_DIAG) ? 1.0 : (double)m[k].r_right;
+        cost += 4.0 * cols * m[k].phys * m[k].r_left * f;
+        cols *= m[k].phys;
+        mem += cols * m[k].r_left;
+      }
+      cost += rows * cols * m[p].r_left;  // final GEMM
+    }
+    const double score = cost + 1e-3 * mem;
+    if (best < 0 || score < best) {
+      best = score;
+      P->p = p;
+    }
+  }
+  // buffer sizes for the chosen p
+  const int p = P->p;
+  int64_t rows = P->slab_rows, lmax = 0;
+  for (int k = 1; k < p; ++k) {
+    rows *= m[k].phys;
+    const bool writes_out = (p == n && k == n - 1);
+    if (!writes_out) lmax = rows * m[k].r_right > lmax ? rows * m[k].r_right : lmax;
+  }
+  P->rowsL = rows;
+  int64_t cols = 1, rmax = 0;
+  if (p < n) {
+    cols = m[n - 1].phys;
+    rmax = cols * m[n - 1].r_left;
+    for (int k = n - 2; k >= p; --k) {
+      cols *= m[k].phys;
+      const int64_t s = cols * m[k].r_left;
+      rmax = s > rmax ? s : rmax;
+    }
+  }
+  P->colsR = cols;
+  P->l_buf = lmax;
+  P->r_buf = rmax;
+  return TNB_OK;
+}
+
+// left step: out[e][(p*J + j)*rr + c] = sum_a in[e][p*rl + a] * G_e(j, a, c)
+__global__ void full_left_step(ModeDev md, int64_t B, const float* __restrict__ in, int64_t in_bs,
+                               int64_t P, float* __restrict__ out, int64_t out_bs) {
+  const int J = md.J, rl = md.rl, rr = md.rr;
+  const int64_t per = P * J * rr;
+  const int64_t total = per * B;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = t / per;
+    int64_t r = t - e * per;
+    const int64_t p = r / ((int64_t)J * rr);
+    r -= p * J * rr;
+    const int j = (int)(r / rr);
+    const int c = (int)(r - (int64_t)j * rr);
+    const float* g = md.s + e * md.bstride;
+    const float* x = in + e * in_bs + p * rl;
+    float acc;
+    if (md.layout == TNB_LAYOUT_DIAG) {
+      acc = x[c] * __ldg(g + (int64_t)j * rl + c);
+    } else {
+      acc = 0.f;
+      const float* gj = g + (int64_t)j * rl * rr + c;
+      for (int a = 0; a < rl; ++a) acc = fmaf(x[a], __ldg(gj + (int64_t)a * rr), acc);
+    }
+    out[e * out_bs + r + p * J * rr] = acc;
+  }
+}
+
+// R of the last mode: out[e][a*J + j] = G_e(j, a, 0)
+__global__ void full_right_first(ModeDev md, int64_t B, float* __restrict__ out, int64_t out_bs) {
+  const int J = md.J, rl = md.rl;
+  const int64_t per = (int64_t)rl * J;
+  const int64_t total = per * B;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = t / per;
+    const int64_t r = t - e * per;
+    const int a = (int)(r / J);
+    const int j = (int)(r - (int64_t)a * J);
+    out[e * out_bs + r] = __ldg(md.s + e * md.bstride + (int64_t)j * rl + a);
+  }
+}
+
+// right step: out[e][a][j*n + x] = sum_c G_e(j, a, c) * in[e][c][x]
+__global__ void full_right_step(ModeDev md, int64_t B, const float* __restrict__ in,
+                                int64_t in_bs, int64_t n, float* __restrict__ out,
+                                int64_t out_bs) {
+  const int J = md.J, rl = md.rl, rr = md.rr;
+  const int64_t per = (int64_t)rl * J * n;
+  const int64_t total = per * B;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = t / per;
+    int64_t r = t - e * per;
+    const int a = (int)(r / ((int64_t)J * n));
+    const int64_t rem = r - (int64_t)a * J * n;
+    const int j = (int)(rem / n);
+    const int64_t x = rem - (int64_t)j * n;
+    const float* g = md.s + e * md.bstride;
+    const float* y = in + e * in_bs + x;
+    float acc;
+    if (md.layout == TNB_LAYOUT_DIAG) {
+      acc = __ldg(g + (int64_t)j * rl + a) * y[(int64_t)a * n];
+    } else {
+      acc = 0.f;
+      const float* ga = g + ((int64_t)j * rl + a) * rr;
+      for (int c = 0; c < rr; ++c) acc = fmaf(__ldg(ga + c), y[(int64_t)c * n], acc);
+    }
+    out[e * out_bs + r] = acc;
+  }
+}
+
+// Generic SIMT GEMM C[e] = A[e] (MxK) @ B[e] (KxN), row-major, fp32.
+// 128x128 tile, BK=8, 256 threads, 8x8 outputs per thread (two 4x4 quads per
+// axis so shared-memory reads and global stores are float4 and coalesced).
+constexpr int GBM = 128, GBN = 128, GBK = 8;
+__global__ void __launch_bounds__(256) sgemm_kernel(const float* __restrict__ A, int64_t lda,
+                                                    int64_t sA, const float* __restrict__ Bm,
+                                                    int64_t ldb, int64_t sB,
+                                                    float* __restrict__ C, int64_t ldc, int64_t sC,
+                                                    int64_t M, int64_t N, int K) {
+  __shared__ __align__(16) float As[GBK][GBM];
+  __shared__ __align__(16) float Bs[GBK][GBN];
+  const int64_t e = blockIdx.z;
+  A += e * sA;
+  Bm += e * sB;
+  C += e * sC;
+  const int64_t m0 = (int64_t)blockIdx.y * GBM, n0 = (int64_t)blockIdx.x * GBN;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+  for (int k0 = 0; k0 < K; k0 += GBK) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int l = tid + i * 256;
+      const int r = l / GBK, kk = l % GBK;
+      const int64_t gm = m0 + r;
+      As[kk][r] = (gm < M && k0 + kk < K) ? __ldg(A + gm * lda + k0 + kk) : 0.f;
+      const int kb = l / GBN, cb = l % GBN;
+      const int64_t gn = n0 + cb;
+      Bs[kb][cb] = (k0 + kb < K && gn < N) ? __ldg(Bm + (int64_t)(k0 + kb) * ldb + gn) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < GBK; ++kk) {
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[kk][64 + ty * 4]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[kk][64 + tx * 4]);
+      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  const bool vec = (ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t gm = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+    if (gm >= M) continue;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t gn = n0 + h * 64 + tx * 4;
+      float* dst = C + gm * ldc + gn;
+      if (vec && gn + 3 < N) {
+        __stcs(reinterpret_cast<float4*>(dst),
+               make_float4(acc[i][h * 4], acc[i][h * 4 + 1], acc[i][h * 4 + 2], acc[i][h * 4 + 3]));
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (gn + q < N) dst[q] = acc[i][h * 4 + q];
+      }
+    }
+  }
+}
+
+inline int grid_for(int64_t total) {
+  int64_t g = ceil_div(total, 256);
+  const int64_t cap = (int64_t)num_sms() * 16;
+  if (g > cap) g = cap;
+  return (int)(g < 1 ? 1 : g);
+}
+
+ModeDev mode_dev(const tnb_chain* c, int k) {
+  const tnb_mode& mm = c->modes[k];
+  ModeDev md;
+  md.s = mm.slices;
+  md.bstride = c->batch > 0 ? mode_floats(mm) : 0;
+  md.layout = mm.layout;
+  md.J = mm.phys;
+  md.rl = mm.r_left;
+  md.rr = mm.r_right;
+  return md;
+}
+
+}  // namespace
+
+int launch_sgemm(const float* A, int64_t lda, int64_t sA, const float* B, int64_t ldb, int64_t sB,
+                 float* C, int64_t ldc, int64_t sC, int64_t M, int64_t N, int K, int64_t batch,
+                 cudaStream_t st) {
+  if (M == 0 || N == 0 || batch == 0) return TNB_OK;
+  if (batch > 65535) return set_error(TNB_EINVAL, "gemm batch too large");
+  dim3 grid((unsigned)ceil_div(N, GBN), (unsigned)ceil_div(M, GBM), (unsigned)batch);
+  if (grid.y > 65535) return set_error(TNB_EINVAL, "gemm M too large");
+  sgemm_kernel<<<grid, 256, 0, st>>>(A, lda, sA, B, ldb, sB, C, ldc, sC, M, N, K);
+  return check_launch("sgemm");
+}
+
+int64_t full_workspace(const tnb_chain* c, int64_t lo, int64_t hi) {
+  FullPlan P;
+  if (make_plan(c, lo, hi, &P)) return -1;
+  const int64_t B = c->batch > 0 ? c->batch : 1;
+  return (2 * P.l_buf + 2 * P.r_buf) * B * (int64_t)sizeof(float);
+}
+
+int launch_full(const tnb_chain* c, int64_t lo, int64_t hi, float* out, void* ws,
+                int64_t ws_bytes, cudaStream_t st) {
+  FullPlan P;
+  int rc = make_plan(c, lo, hi, &P);
+  if (rc) return rc;
+  ChainDev tmp;
+  rc = make_chain_dev(c, &tmp, false);  // validates ranks
+  if (rc) return rc;
+  const int64_t B = c->batch > 0 ? c->batch : 1;
+  if (P.out_per == 0) return TNB_OK;
+  if (!out) return set_error(TNB_EINVAL, "null output");
+  const int64_t need = (2 * P.l_buf + 2 * P.r_buf) * B * (int64_t)sizeof(float);
+  if (need > 0 && (!ws || ws_bytes < need))
+    return set_error(TNB_EWORKSPACE, "full needs %lld workspace bytes, got %lld",
+                     (long long)need, (long long)ws_bytes);
+  float* lb[2] = {(float*)ws, (float*)ws + P.l_buf * B};
+  float* rb[2] = {(float*)ws + 2 * P.l_buf * B, (float*)ws + 2 * P.l_buf * B + P.r_buf * B};
+  const int n = P.n, p = P.p;
+
+  // ---- left partial: L0 is a view of mode 0's slices (rows lo..hi) ----
+  const ModeDev m0 = mode_dev(c, 0);
+  const float* L = m0.s + lo * (int64_t)m0.rl * m0.rr;  // dense, rl == 1
+  int64_t L_bs = m0.bstride;
+  int64_t rows = P.slab_rows;
+  if (n == 1) {
+    // out[e][j] = G_e(lo + j, 0, 0)
+    for (int64_t e = 0; e < B; ++e) {
+      rc = check_cuda(cudaMemcpyAsync(out + e * P.out_per, L + e * L_bs,
+                                      P.out_per * sizeof(float), cudaMemcpyDeviceToDevice, st),
+                      "copy");
+      if (rc) return rc;
+    }
+    return TNB_OK;
+  }
+  for (int k = 1; k < p; ++k) {
+    const ModeDev md = mode_dev(c, k);
+    const bool writes_out = (p == n && k == n - 1);
+    float* dst = writes_out ? out : lb[k & 1];
+    const int64_t dst_bs = writes_out ? P.out_per : P.l_buf;
+    const int64_t total = rows * md.J * md.rr * B;
+    if (total > 0)
+      full_left_step<<<grid_for(total), 256, 0, st>>>(md, B, L, L_bs, rows, dst, dst_bs);
+    rc = check_launch("full_left_step");
+    if (rc) return rc;
+    L = dst;
+    L_bs = dst_bs;
+    rows *= md.J;
+  }
+  if (p == n) return TNB_OK;
+
+  // ---- right partial ----
+  const ModeDev ml = mode_dev(c, n - 1);
+  float* R = rb[0];
+  int64_t cols = ml.J;
+  {
+    const int64_t total = (int64_t)ml.rl * ml.J * B;
+    if (total > 0) full_right_first<<<grid_for(total), 256, 0, st>>>(ml, B, R, P.r_buf);
+    rc = check_launch("full_right_first");
+    if (rc) return rc;
+  }
+  int which = 0;
+  for (int k = n - 2; k >= p; --k) {
+    const ModeDev md = mode_dev(c, k);
+    float* dst = rb[which ^ 1];
+    const int64_t total = (int64_t)md.rl * md.J * cols * B;
+    if (total > 0)
+      full_right_step<<<grid_for(total), 256, 0, st>>>(md, B, R, P.r_buf, cols, dst, P.r_buf);
+    rc = check_launch("full_right_step");
+    if (rc) return rc;
+    R = dst;
+    which ^= 1;
+    cols *= md.J;
+  }
+  // ---- out = L @ R ----
+  const int K = c->modes[p].r_left;
+  if (K == 0) return check_cuda(cudaMemsetAsync(out, 0, P.out_per * B * sizeof(float), st), "memset");
+  if (tc_gemm_supported(rows, cols, K, K, cols, cols))
+    return launch_tc_gemm(L, K, L_bs, R, cols, P.r_buf, out, cols, P.out_per, rows, cols, K, B, st);
+  return launch_sgemm(L, K, L_bs, R, cols, P.r_buf, out, cols, P.out_per, rows, cols, K, B, st);
+}
+
+}  // namespace tnb

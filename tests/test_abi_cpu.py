@@ -1,0 +1,152 @@
+"""CPU-side checks of the boundary: libtnb.so loads, exports exactly the
+symbols include/tnb.h declares, and the host-side contract (validation,
+planning, error mapping) behaves like the reference without a GPU."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2206_11128_b200 import _build, _native
+
+    if not _native.LIB_PATH.exists():
+        _build.build(verbose=False)
+    return _native.load()
+
+
+def declared_symbols():
+    text = (ROOT / "include" / "tnb.h").read_text()
+    return sorted(set(re.findall(r"\b(tnb_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_entry_points():
+    syms = declared_symbols()
+    for s in ("tnb_entries_f32", "tnb_full_f32", "tnb_dot_f32", "tnb_norm_f32", "tnb_repack_f32"):
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol(lib):
+    from paper_2206_11128_b200 import _native
+
+    for s in declared_symbols():
+        assert hasattr(lib, s), s
+        assert s in _native.SIGNATURES, f"{s} lacks a ctypes signature"
+    assert set(_native.SIGNATURES) == set(declared_symbols())
+    assert lib.tnb_version().startswith(b"tnb")
+
+
+def test_struct_layouts_match_header():
+    from paper_2206_11128_b200 import _native as N
+
+    assert ctypes.sizeof(N.TnbNode) == 40
+    assert ctypes.sizeof(N.TnbMode) == 24
+    assert ctypes.sizeof(N.TnbChain) == 24
+
+
+def _plan(lib, specs):
+    from paper_2206_11128_b200 import _native as N
+
+    n = len(specs)
+    nodes = (N.TnbNode * n)()
+    for k, (kind, I, J, rl, rr) in enumerate(specs):
+        nodes[k].kind, nodes[k].internal, nodes[k].phys = kind, I, J
+        nodes[k].r_left, nodes[k].r_right = rl, rr
+        nodes[k].core = 1  # never dereferenced by planning
+        nodes[k].factor = 1 if I != J else None
+    modes = (N.TnbMode * n)()
+    rc = lib.tnb_plan_modes(nodes, n, modes)
+    return rc, modes
+
+
+def test_plan_promotes_cp_by_position(lib):
+    from paper_2206_11128_b200 import _native as N
+
+    rc, modes = _plan(lib, [(N.KIND_CP, 4, 4, 3, 3), (N.KIND_CP, 5, 7, 3, 3), (N.KIND_TT, 6, 6, 3, 2),
+                            (N.KIND_CP, 2, 2, 2, 2)])
+    assert rc == 0
+    got = [(m.layout, m.phys, m.r_left, m.r_right) for m in modes]
+    assert got == [(N.LAYOUT_DENSE, 4, 1, 3), (N.LAYOUT_DIAG, 7, 3, 3),
+                   (N.LAYOUT_DENSE, 6, 3, 2), (N.LAYOUT_DENSE, 2, 2, 1)]
+    assert lib.tnb_mode_floats(ctypes.byref(modes[1]), 0) == 7 * 3
+    assert lib.tnb_mode_floats(ctypes.byref(modes[2]), 5) == 5 * 6 * 3 * 2
+    rc, modes = _plan(lib, [(N.KIND_CP, 5, 5, 3, 3)])
+    assert rc == 0 and (modes[0].r_left, modes[0].r_right) == (1, 1)
+
+
+def test_plan_rejects_bad_chains(lib):
+    from paper_2206_11128_b200 import _native as N
+
+    rc, _ = _plan(lib, [(N.KIND_TT, 3, 3, 1, 2), (N.KIND_TT, 4, 4, 3, 1)])
+    assert rc == N.TNB_EINVAL and b"rank mismatch between modes 0 and 1" in lib.tnb_last_error()
+    rc, _ = _plan(lib, [(N.KIND_TT, 3, 3, 2, 1)])
+    assert rc == N.TNB_EINVAL and b"boundary ranks must be 1" in lib.tnb_last_error()
+
+
+def test_workspace_queries(lib):
+    from paper_2206_11128_b200 import _native as N
+
+    _, modes = _plan(lib, [(N.KIND_TT, 16, 16, 1, 8), (N.KIND_TT, 16, 16, 8, 8), (N.KIND_TT, 16, 16, 8, 1)])
+    ch = N.TnbChain(3, 0, 0, ctypes.cast(modes, ctypes.POINTER(N.TnbMode)))
+    assert lib.tnb_entries_workspace_bytes(ctypes.byref(ch), 1000, N.ALGO_CHAIN) == 0
+    assert lib.tnb_entries_workspace_bytes(ctypes.byref(ch), 1000, N.ALGO_LAYERED) == 2 * 1000 * 8 * 4
+    assert lib.tnb_full_workspace_bytes(ctypes.byref(ch), 0, 16) >= 0
+    assert lib.tnb_full_workspace_bytes(ctypes.byref(ch), 0, 17) == -1
+
+
+# -- façade validation mirrors the reference (no GPU needed) ---------------
+
+def test_facade_validation_messages():
+    import paper_2206_11128_b200 as tb
+
+    with pytest.raises(tb.ContractViolationError):
+        tb.ModeNode("xx", np.ones((1, 2, 1)))
+    with pytest.raises(tb.StructuralError, match="3 axes"):
+        tb.ModeNode("tt", np.ones((2, 2)))
+    with pytest.raises(tb.StructuralError, match="internal size"):
+        tb.ModeNode("tt", np.ones((1, 3, 1)), factor=np.ones((5, 2)))
+    with pytest.raises(tb.StructuralError, match="rank mismatch between modes 0 and 1"):
+        tb.TnTensor([tb.ModeNode("tt", np.ones((1, 3, 2))), tb.ModeNode("tt", np.ones((3, 4, 1)))])
+    with pytest.raises(tb.StructuralError, match="boundary ranks"):
+        tb.TnTensor([tb.ModeNode("tt", np.ones((2, 3, 1)))])
+    with pytest.raises(tb.StructuralError):
+        tb.TnTensor([tb.ModeNode("cp", np.ones((3, 2))), tb.ModeNode("tt", np.ones((3, 4, 1)))])
+    with pytest.raises(tb.ContractViolationError):
+        tb.TnTensor([])
+    good = tb.ModeNode("tt", np.ones((2, 1, 3, 1)), batched=True)
+    with pytest.raises(tb.StructuralError):
+        tb.TnTensor([good], batch_size=3)
+    with pytest.raises(tb.StructuralError):
+        tb.TnTensor([tb.ModeNode("tt", np.ones((1, 3, 1)))], batch_size=2)
+    assert issubclass(tb.ContractViolationError, ValueError)
+    assert issubclass(tb.StructuralError, ValueError)
+
+
+def test_facade_metadata():
+    import paper_2206_11128_b200 as tb
+
+    t = tb.TnTensor([tb.ModeNode("cp", np.ones((3, 5))), tb.ModeNode("cp", np.ones((4, 5)), np.ones((6, 4))),
+                     tb.ModeNode("tt", np.ones((5, 2, 1)))])
+    assert t.shape == (3, 6, 2) and t.ranks == [1, 5, 5, 1] and t.ndim == 3
+    assert t.numel() == 36 and t.dof() == 15 + 20 + 24 + 10
+    assert "kinds=CCT" in repr(t)
+
+
+def test_no_cpu_fallback():
+    import torch
+
+    import paper_2206_11128_b200 as tb
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    t = tb.TnTensor([tb.ModeNode("tt", np.ones((1, 3, 1)))])
+    with pytest.raises(tb.NativeError):
+        tb.full(t)
+    with pytest.raises(tb.NativeError):
+        t[np.zeros((1, 1), dtype=np.int64)]

@@ -1,0 +1,111 @@
+"""Parity at the five BASELINE configurations (SURVEY §8(d) parity sampling).
+
+Inputs come from the pinned generators (tests/test_oracle_golden.py checks
+them against the real reference); the CPU oracle runs on subsets sized to
+finish in seconds, and size-independent properties cover the full sizes.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import tntz_oracle as O
+from tests.helpers import assert_close, facade, to_np
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+tb = pytest.importorskip("paper_2206_11128_b200")
+from paper_2206_11128_b200 import _native as N  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def tt(cores, batch=None):
+    return facade([("tt", c, None) for c in cores], batch), O.make_chain([("tt", c) for c in cores], batch)
+
+
+def test_cfg1_everything():
+    cores = O.random_tt((16,) * 6, 8, seed=0, scale=8 ** -0.5)
+    t, o = tt(cores)
+    ref = O.full(o)
+    assert_close(tb.full(t), ref, what="cfg1 full")
+    idx = O.uniform_indices((16,) * 6, 1 << 20, 2)
+    ref_e = ref[tuple(idx.T)]
+    for algo in (N.ALGO_AUTO, N.ALGO_CHAIN, N.ALGO_LAYERED):
+        assert_close(tb.entries(t, idx, algo=algo), ref_e, what=f"cfg1 entries {algo}")
+    assert_close(np.asarray(tb.norm(t)), np.asarray(O.norm(o)), what="cfg1 norm")
+
+
+def test_cfg2_subset():
+    cores = O.random_tt((32,) * 10, 32, seed=0, scale=32 ** -0.5)
+    t, o = tt(cores)
+    m = 1 << 24
+    idx = torch.from_numpy(O.uniform_indices((32,) * 10, m, 2)).cuda()
+    got = tb.entries(t, idx)
+    assert tuple(got.shape) == (m,)
+    # oracle on 2^20 samples spread over the whole batch (every shard)
+    sel = np.linspace(0, m - 1, 1 << 20).astype(np.int64)
+    sub = idx[torch.from_numpy(sel).cuda()].cpu().numpy()
+    assert_close(to_np(got)[sel], O.entries(o, sub), what="cfg2")
+
+
+def test_cfg5_subset():
+    nodes = O.cfg5_nodes(seed=0)
+    t = facade(nodes)
+    o = O.make_chain(nodes)
+    m = 1 << 22
+    idx = torch.from_numpy(O.uniform_indices((128,) * 8, m, 2)).cuda()
+    got = to_np(tb.entries(t, idx))
+    sel = np.linspace(0, m - 1, 1 << 18).astype(np.int64)
+    assert_close(got[sel], O.entries(o, idx[torch.from_numpy(sel).cuda()].cpu().numpy()), what="cfg5")
+    assert_close(np.asarray(tb.norm(t)), np.asarray(O.norm(o)), what="cfg5 norm")
+
+
+def test_cfg3_slabs_and_norm():
+    cores = O.random_tt((256,) * 4, 64, seed=0, scale=64 ** -0.5)
+    t, o = tt(cores)
+    for i0 in (0, 37, 128, 255):
+        assert_close(tb.full(t, lead=(i0, i0 + 1)), O.full_slab(o, i0, i0 + 1), what=f"cfg3 slab {i0}")
+    # a multi-slab shard (what one of 8 GPUs writes) against its slabs
+    shard = tb.full(t, lead=(32, 64))
+    for i in (0, 31):
+        assert_close(shard[i:i + 1], O.full_slab(o, 32 + i, 33 + i), what="cfg3 shard")
+    assert_close(np.asarray(tb.norm(t)), np.asarray(O.norm(o)), what="cfg3 norm")
+
+
+@pytest.mark.slow
+def test_cfg3_whole_tensor_checksum():
+    # size-independent property at the full 17 GB size: sum of squares of
+    # full(t) equals norm(t)^2 (core.py:387-391), accumulated in float64
+    cores = O.random_tt((256,) * 4, 64, seed=0, scale=64 ** -0.5)
+    t, o = tt(cores)
+    f = tb.full(t)
+    assert tuple(f.shape) == (256,) * 4
+    acc = 0.0
+    for i in range(0, 256, 16):
+        acc += float((f[i:i + 16].double() ** 2).sum())
+    ref = O.norm(o) ** 2
+    assert abs(acc - ref) <= 1e-5 * ref
+    del f
+
+
+def test_cfg4_pairs():
+    a = O.random_tt((64,) * 16, 16, seed=0, batch_size=4096, scale=0.25)
+    b = O.random_tt((64,) * 16, 16, seed=1, batch_size=4096, scale=0.25)
+    ta, oa = tt(a, 4096)
+    tb_, ob = tt(b, 4096)
+    dots = to_np(tb.dot(ta, tb_))
+    norms = to_np(tb.norm(ta))
+    assert dots.shape == (4096,) and norms.shape == (4096,)
+    lo, hi = 0, 256
+    ref_d = O.chain_dot(O.batch_slice(oa, lo, hi), O.batch_slice(ob, lo, hi))
+    ref_n = O.norm(O.batch_slice(oa, lo, hi))
+    assert_close(dots[lo:hi], ref_d, what="cfg4 dot")
+    assert_close(norms[lo:hi], ref_n, what="cfg4 norm")
+    # the last chunk too (every shard of an 8-way split is covered by its ends)
+    ref_d = O.chain_dot(O.batch_slice(oa, 3840, 4096), O.batch_slice(ob, 3840, 4096))
+    assert_close(dots[3840:], ref_d, what="cfg4 dot tail")

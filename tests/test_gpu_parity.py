@@ -1,0 +1,200 @@
+"""GPU parity: the CUDA path (through libtnb's C ABI via the façade) against
+the reference's golden vectors and the pinned CPU oracle."""
+
+import numpy as np
+import pytest
+
+from oracle import tntz_oracle as O
+from tests import golden_cases as G
+from tests.helpers import assert_close, assert_dot_close, facade, to_np
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+tb = pytest.importorskip("paper_2206_11128_b200")
+from paper_2206_11128_b200 import _native as N  # noqa: E402
+
+ALGOS = [N.ALGO_AUTO, N.ALGO_LAYERED, N.ALGO_CHAIN]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+@pytest.mark.parametrize("name", G.CASE_NAMES)
+def test_golden_full_norm(name):
+    c = G.case(name)
+    t = facade(c["nodes"], c["batch"])
+    out = c["out"]
+    if "full" in out:
+        assert_close(tb.full(t), out["full"], what=f"{name} full")
+    ref_norm = np.asarray(out["norm"], dtype=np.float64)
+    got = tb.norm(t)
+    if c["batch"] is None:
+        assert isinstance(got, float)
+    assert_close(np.asarray(to_np(got)), ref_norm, what=f"{name} norm")
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("name", [n for n in G.CASE_NAMES if "entries" in G.case(n)["out"]])
+def test_golden_entries(name, algo):
+    c = G.case(name)
+    t = facade(c["nodes"], c["batch"])
+    got = tb.entries(t, c["out"]["idx"], algo=algo)
+    assert_close(got, c["out"]["entries"], what=f"{name} entries algo={algo}")
+
+
+@pytest.mark.parametrize("name", [n for n in G.CASE_NAMES if "dot" in G.case(n)["out"]])
+def test_golden_dot(name):
+    c = G.case(name)
+    a = facade(c["nodes"], c["batch"])
+    b = facade(*c["other"])
+    oa, ob = O.make_chain(c["nodes"], c["batch"]), O.make_chain(*c["other"])
+    scale = np.asarray(O.norm(oa)) * np.asarray(O.norm(ob))
+    got = tb.dot(a, b)
+    if c["batch"] is None:
+        assert isinstance(got, float)
+    assert_dot_close(got, c["out"]["dot"], scale, what=f"{name} dot")
+
+
+@pytest.mark.parametrize("name", G.CASE_NAMES)
+def test_node_tt_core_matches_oracle(name):
+    c = G.case(name)
+    t = facade(c["nodes"], c["batch"])
+    oc = O.make_chain(c["nodes"], c["batch"])
+    for k in range(t.ndim):
+        assert_close(tb.node_tt_core(t, k), O.tt_core(oc, k), what=f"{name} mode {k}")
+
+
+def test_promote_cp_node_layouts():
+    # test_core.py:21-53 layouts
+    n = tb.ModeNode("cp", np.eye(2))
+    d = to_np(tb.promote_cp_node(n, tb.INTERIOR))
+    exp = np.zeros((2, 2, 2))
+    for a in range(2):
+        exp[a, a, a] = 1.0
+    assert np.array_equal(d, exp)
+    d = to_np(tb.promote_cp_node(tb.ModeNode("cp", np.ones((3, 2))), tb.LEFT_BOUNDARY))
+    assert d.shape == (1, 3, 2) and np.array_equal(d, np.ones((1, 3, 2)))
+    u = np.arange(12.0).reshape(4, 3)
+    d = to_np(tb.promote_cp_node(tb.ModeNode("cp", u), tb.RIGHT_BOUNDARY))
+    assert d.shape == (3, 4, 1) and np.array_equal(d[:, :, 0], u.T)
+    ub = np.random.default_rng(0).standard_normal((2, 4, 3)).astype(np.float32)
+    d = to_np(tb.promote_cp_node(tb.ModeNode("cp", ub, batched=True), tb.INTERIOR))
+    for b in range(2):
+        assert np.array_equal(d[b], O.promote_cp(ub[b].astype(np.float64), 1, 3, False))
+    with pytest.raises(tb.ContractViolationError):
+        tb.promote_cp_node(tb.ModeNode("tt", np.ones((1, 3, 1))), tb.INTERIOR)
+
+
+# -- index semantics (core.py:402-416, indexing.py:120-130) -----------------
+
+def _small():
+    cores = O.random_tt((4, 5, 3), [2, 3], seed=1)
+    return facade([("tt", c, None) for c in cores]), O.make_chain([("tt", c) for c in cores])
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_index_semantics(algo):
+    t, o = _small()
+    f = O.full(o)
+    v = to_np(tb.entries(t, np.array([[-1, -2, -3]]), algo=algo))
+    assert v.shape == (1,) and abs(v[0] - f[3, 3, 0]) <= 1e-5 * np.abs(f).max()
+    # -size wraps to 0
+    v = to_np(tb.entries(t, np.array([[-4, -5, -3]]), algo=algo))
+    assert abs(v[0] - f[0, 0, 0]) <= 1e-5 * np.abs(f).max()
+    # out of bounds: lowest offending mode named, both directions
+    with pytest.raises(tb.ContractViolationError, match="index out of bounds on mode 1"):
+        tb.entries(t, np.array([[0, 5, 0], [0, 0, 7]]), algo=algo)
+    with pytest.raises(tb.ContractViolationError, match="mode 0"):
+        tb.entries(t, np.array([[0, 0, 0], [-5, 0, 9]]), algo=algo)
+    with pytest.raises(tb.ContractViolationError, match="mode 2"):
+        tb.entries(t, np.array([[0, 0, -4]]), algo=algo)
+    # 1-D index -> one sample; int32 accepted; empty -> (0,)
+    assert tuple(tb.entries(t, np.array([1, 2, 0])).shape) == (1,)
+    i32 = np.array([[1, 2, 0], [3, 4, 2]], dtype=np.int32)
+    assert_close(tb.entries(t, i32, algo=algo), O.entries(o, i32))
+    assert tuple(tb.entries(t, np.zeros((0, 3), dtype=np.int64)).shape) == (0,)
+    # torch index tensors, host and device
+    ti = torch.tensor([[1, 2, 0]])
+    assert_close(tb.entries(t, ti), O.entries(o, ti.numpy()))
+    assert_close(tb.entries(t, ti.cuda()), O.entries(o, ti.numpy()))
+    with pytest.raises(tb.ContractViolationError):
+        tb.entries(t, np.zeros((2, 2), dtype=np.int64))
+
+
+def test_float_indices_follow_reference_quirk():
+    # entries() floors float indices after wrapping (SURVEY §8(a) probes);
+    # getitem() rejects them (indexing.py:128-129)
+    t, o = _small()
+    fi = np.array([[1.5, 2.0, -0.5]])
+    assert_close(tb.entries(t, fi), O.entries(o, fi))
+    with pytest.raises(tb.ContractViolationError, match="mode 1"):
+        tb.entries(t, np.array([[0.0, 5.0, 0.0]]))
+    with pytest.raises(tb.ContractViolationError, match="integers"):
+        t[np.array([[0.5, 1.0, 0.0]])]
+
+
+def test_getitem_forms():
+    t, o = _small()
+    f = O.full(o)
+    idx = np.array([[0, 1, 2], [3, 4, 0], [1, 0, 1]])
+    vals = t[idx]
+    assert tuple(vals.shape) == (3,)
+    assert_close(vals, f[idx[:, 0], idx[:, 1], idx[:, 2]])
+    with pytest.raises(tb.ContractViolationError, match="columns"):
+        t[np.array([[0, 1]])]
+    # all-integer tuple -> python float; bounds checked last mode first
+    assert abs(t[1, 2, -1] - f[1, 2, 2]) <= 1e-5 * np.abs(f).max()
+    with pytest.raises(tb.ContractViolationError, match="index 9 out of bounds for size 3"):
+        t[7, 0, 9]
+    with pytest.raises(NotImplementedError):
+        t[0:2]
+
+
+def test_batched_entries_and_getitem():
+    c = G.case("batched_tt")
+    t = facade(c["nodes"], c["batch"])
+    got = t[c["out"]["idx"]]
+    assert tuple(got.shape) == (c["out"]["idx"].shape[0], c["batch"])
+    assert_close(got, c["out"]["entries"])
+
+
+def test_full_slabs_match_reference_slicing():
+    for name in ("tt_453", "tucker_675", "blended_3", "batched_hybrid", "hybrid_wide"):
+        c = G.case(name)
+        t = facade(c["nodes"], c["batch"])
+        o = O.make_chain(c["nodes"], c["batch"])
+        j0 = t.shape[0]
+        for lo, hi in [(0, 1), (1, j0), (j0 - 1, j0), (0, j0)]:
+            assert_close(tb.full(t, lead=(lo, hi)), O.full_slab(o, lo, hi), what=f"{name} [{lo},{hi})")
+        assert tuple(tb.full(t, lead=(1, 1)).shape)[-t.ndim] == 0
+
+
+def test_dot_contract_errors():
+    a = facade([("tt", c, None) for c in O.random_tt((2, 3), 1, seed=0)])
+    b = facade([("tt", c, None) for c in O.random_tt((3, 2), 1, seed=0)])
+    with pytest.raises(tb.ContractViolationError, match="dot needs equal shapes"):
+        tb.dot(a, b)
+    bb = facade([("tt", c, None) for c in O.random_tt((2, 3), 1, seed=0, batch_size=2)], 2)
+    with pytest.raises(tb.ContractViolationError, match="agree on batching"):
+        tb.dot(a, bb)
+
+
+def test_dot_zero_is_exact():
+    # test_arithmetic.py:121-123
+    a = facade([("tt", c, None) for c in O.random_tt((3, 4), 2, seed=16)])
+    z = facade([("tt", c * 0, None) for c in O.random_tt((3, 4), 2, seed=16)])
+    assert tb.dot(a, z) == 0.0
+    assert tb.norm(z) == 0.0
+
+
+def test_batched_dot_equals_loop():
+    # test_arithmetic.py:346-387
+    a = facade([("tt", c, None) for c in O.random_tt((3, 4, 5), 3, seed=45, batch_size=3)], 3)
+    b = facade([("tt", c, None) for c in O.random_tt((3, 4, 5), 2, seed=46, batch_size=3)], 3)
+    vec = to_np(tb.dot(a, b))
+    for e in range(3):
+        assert abs(vec[e] - tb.dot(a.batch_element(e), b.batch_element(e))) <= 1e-6 * max(abs(vec[e]), 1)

@@ -1,0 +1,136 @@
+// Roofline denominators MEASURED_PEAKS.json lacks:
+//   FP32 FFMA throughput (scalar FFMA and packed FFMA2), HBM write-only and
+//   read-only bandwidth, plus a copy for cross-checking hbm_gbs.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o build/peaks tools/peaks.cu
+// Prints one JSON object.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#define CK(x)                                                             \
+  do {                                                                    \
+    cudaError_t e_ = (x);                                                 \
+    if (e_ != cudaSuccess) {                                              \
+      fprintf(stderr, "%s: %s\n", #x, cudaGetErrorString(e_));            \
+      return 1;                                                           \
+    }                                                                     \
+  } while (0)
+
+constexpr int kIters = 4096;
+
+template <bool kRegC>
+__global__ void __launch_bounds__(256) ffma_kernel(float* out, float s) {
+  float a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = threadIdx.x * 1e-3f + i;
+  // kRegC: all three sources in registers (the form real kernels issue)
+  const float b = s, c = kRegC ? 1e-7f * (float)(threadIdx.x & 3) : 1e-7f;
+  for (int it = 0; it < kIters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = fmaf(a[i], b, c);
+  }
+  float r = 0.f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) r += a[i];
+  if (r == 12345.f) out[0] = r;
+}
+
+__global__ void __launch_bounds__(256) ffma2_kernel(float* out, float s) {
+  unsigned long long a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    float lo = threadIdx.x * 1e-3f + i, hi = lo + 0.5f;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(a[i]) : "f"(lo), "f"(hi));
+  }
+  unsigned long long b, c;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(b) : "f"(s));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(c) : "f"(1e-7f));
+  for (int it = 0; it < kIters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(a[i]) : "l"(b), "l"(c));
+  }
+  float r = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a[i]));
+    r += lo + hi;
+  }
+  if (r == 12345.f) out[0] = r;
+}
+
+__global__ void write_kernel(float4* __restrict__ p, int64_t n) {
+  const float4 v = make_float4(1.f, 2.f, 3.f, 4.f);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    __stcs(p + i, v);
+}
+
+__global__ void read_kernel(const float4* __restrict__ p, int64_t n, float* out) {
+  float acc = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = __ldcs(p + i);
+    acc += v.x + v.y + v.z + v.w;
+  }
+  if (acc == 12345.f) out[0] = acc;
+}
+
+__global__ void copy_kernel(const float4* __restrict__ a, float4* __restrict__ b, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    __stcs(b + i, __ldcs(a + i));
+}
+
+template <typename F>
+float best_ms(F launch, int reps) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int r = 0; r < reps + 2; ++r) {
+    cudaEventRecord(e0);
+    launch();
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (r >= 2 && ms < best) best = ms;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return best;
+}
+
+int main() {
+  int sms = 0, dev = 0;
+  CK(cudaGetDevice(&dev));
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  float* d_out;
+  CK(cudaMalloc(&d_out, 16));
+  const int blocks = sms * 8, threads = 256;
+  const double fmas = (double)blocks * threads * kIters * 16;
+  float ms_ffma = best_ms([&] { ffma_kernel<false><<<blocks, threads>>>(d_out, 0.999f); }, 10);
+  float ms_ffma_r = best_ms([&] { ffma_kernel<true><<<blocks, threads>>>(d_out, 0.999f); }, 10);
+  float ms_ffma2 = best_ms([&] { ffma2_kernel<<<blocks, threads>>>(d_out, 0.999f); }, 10);
+  CK(cudaGetLastError());
+  const int64_t bytes = 8LL << 30;  // 8 GiB, far above L2
+  float4 *a, *b;
+  CK(cudaMalloc(&a, bytes));
+  CK(cudaMalloc(&b, bytes));
+  const int64_t n = bytes / 16;
+  const int bw_blocks = sms * 16;
+  float ms_w = best_ms([&] { write_kernel<<<bw_blocks, 512>>>(a, n); }, 8);
+  float ms_r = best_ms([&] { read_kernel<<<bw_blocks, 512>>>(a, n, d_out); }, 8);
+  float ms_c = best_ms([&] { copy_kernel<<<bw_blocks, 512>>>(a, b, n); }, 8);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  printf("{\"fp32_ffma_tflops\": %.2f, \"fp32_ffma_3reg_tflops\": %.2f, \"fp32_ffma2_tflops\": %.2f, \"hbm_write_gbs\": %.1f, "
+         "\"hbm_read_gbs\": %.1f, \"hbm_copy_gbs\": %.1f, \"sms\": %d, "
+         "\"how\": \"best of 10 (ffma: %d blocks x 256 thr x 16 chains x %d iters) / best of 8 over 8 GiB "
+         "(write __stcs float4, read __ldcs float4, copy counts read+write)\"}\n",
+         2 * fmas / (ms_ffma * 1e-3) / 1e12, 2 * fmas / (ms_ffma_r * 1e-3) / 1e12, 2 * fmas / (ms_ffma2 * 1e-3) / 1e12,
+         bytes / (ms_w * 1e-3) / 1e9, bytes / (ms_r * 1e-3) / 1e9, 2.0 * bytes / (ms_c * 1e-3) / 1e9,
+         sms, blocks, kIters);
+  return 0;
+}
