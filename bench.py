@@ -18,6 +18,7 @@ oracle/, a restatement of core.py:394-444) on the host cores, rank 0 only.
 from __future__ import annotations
 
 import argparse
+import faulthandler
 import json
 import math
 import os
@@ -70,9 +71,13 @@ class ClockSampler:
             pynvml.nvmlInit()
             import torch
 
-            bus = torch.cuda.get_device_properties(device_index).pci_bus_id
-            self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode() if isinstance(bus, str) else bus) \
-                if bus else pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            props = torch.cuda.get_device_properties(device_index)
+            ids = [getattr(props, a, None) for a in ("pci_domain_id", "pci_bus_id", "pci_device_id")]
+            if all(isinstance(v, int) for v in ids):
+                busid = "%08X:%02X:%02X.0" % tuple(ids)
+                self.h = pynvml.nvmlDeviceGetHandleByPciBusId(busid)
+            else:
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(int(device_index))
             self.nv = pynvml
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
             self.ok = True
@@ -444,6 +449,7 @@ def run_ours(args):
 
 
 def main():
+    faulthandler.enable()
     args = parse()
     if args.impl == "reference":
         run_reference(args)

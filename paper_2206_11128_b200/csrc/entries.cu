@@ -148,6 +148,8 @@ int launch_entries(const tnb_chain* c, const int64_t* idx, int64_t m, float* out
   rc = check_cuda(cudaMemsetAsync(err, 0x7f, sizeof(int32_t), st), "memset err");
   if (rc || m == 0) return rc;
   const int64_t B = ch.batch;
+  if (algo == TNB_ALGO_AUTO && m >= (1 << 16) && bucketed_supported(ch))
+    return launch_entries_bucketed(ch, idx, m, out, err, st);
   if (use == TNB_ALGO_CHAIN) {
     const int64_t total = m * B;
     const int g = grid_for(total, 256);

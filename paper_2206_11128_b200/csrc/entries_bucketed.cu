@@ -1,10 +1,333 @@
-// K1 performance kernel (placeholder until the bucketed kernel lands).
+// K1 performance kernel: bucketed entry evaluation for unbatched chains with
+// ranks <= 32 (BASELINE configs 2 and 5).
+//
+// Reference algorithm (core.py:432-444): per mode, argsort the samples by
+// their index value so every group shares one core slice and the group's
+// update is a real (n_j x r) @ (r x s) product.  A global re-sort per mode
+// would cost 2 x M x r x 4 bytes of HBM traffic per mode, so
+// here the grouping happens per CTA tile, on chip:
+//
+//   * a persistent CTA (one per SM) owns a tile of T samples; their r-vector
+//     states live in shared memory at FIXED slots (sample id), so no state
+//     ever moves between modes -- only a permutation is rebuilt;
+//   * per interior dense mode, a counting sort of the tile's indices
+//     (warp-aggregated match_any + smem atomics) yields perm, bucket starts
+//     and counts;
+//   * each warp takes an equal contiguous range of sorted positions; for each
+//     bucket in its range it loads that core slice ONCE into registers
+//     (lane group of L lanes holds all r rows x C columns), then streams its
+//     samples: a group reads a sample's state row (LDS.128 broadcast within
+//     the group), does r x C FMAs per lane, and writes its C output columns
+//     back into the same slot (__syncwarp between reads and writes);
+//   * the first mode (rank 1 on the left) is a row copy, interior CP modes
+//     are diagonal scalings, the last mode (rank 1 on the right) a dot
+//     product -- none of those need sorting;
+//   * index tuples are read once per tile (coalesced int64), validated
+//     (negative wrap, lowest OOB mode -> *err), compacted to uint8/uint16 in
+//     shared memory; the next tile's indices are prefetched into L2.
+// Each sample's arithmetic is a fixed FMA sequence, so results do not depend
+// on the sort order or the tile a sample lands in.
 #include "common.cuh"
 
 namespace tnb {
-bool bucketed_supported(const ChainDev&) { return false; }
-int launch_entries_bucketed(const ChainDev&, const int64_t*, int64_t, float*, int32_t*,
-                            cudaStream_t) {
-  return set_error(TNB_EINVAL, "bucketed entries not built");
+namespace {
+
+constexpr int kThreads = 512;
+constexpr int kMaxJ = 1024;          // bucket count limit for sorted modes
+constexpr int kSmemLimit = 232448;   // 227 KB dynamic smem per CTA on sm_100
+
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
+
+__device__ __forceinline__ int64_t ld_stream_i64(const int64_t* p) {
+  int64_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.b64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+
+template <int R>
+struct Geo {
+  static constexpr int C = (R == 24) ? 3 : 2;  // output columns per lane
+  static constexpr int L = R / C;              // lanes per sample group
+  static constexpr int G = 32 / L;             // sample groups per warp
+  static constexpr int P = 8 / G;              // passes per iteration (8 samples)
+  static constexpr int RP = R + 4;             // padded state row (bank spread)
+  static_assert(L * C == R && 32 % L == 0 && G * P == 8, "geometry");
+};
+
+template <typename IdxT>
+__host__ __device__ inline size_t smem_bytes(int T, int RP, int N, int jcap) {
+  size_t b = (size_t)T * RP * sizeof(float);      // state
+  b += (size_t)T * 2 * sizeof(uint16_t);          // perm + rank
+  b += (size_t)N * T * sizeof(IdxT);              // compact indices
+  b = (b + 15) & ~(size_t)15;
+  b += (size_t)2 * (jcap + 1) * sizeof(int);      // counts + starts
+  return b;
+}
+
+template <int R, typename IdxT>
+__global__ void __launch_bounds__(kThreads, 1)
+    entries_bucketed_kernel(const __grid_constant__ ChainDev ch, const int64_t* __restrict__ idx,
+                            int64_t m, float* __restrict__ out, int32_t* __restrict__ err, int T,
+                            int jcap) {
+  using Gm = Geo<R>;
+  constexpr int C = Gm::C, L = Gm::L, G = Gm::G, P = Gm::P, RP = Gm::RP;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int N = ch.n;
+  float* state = reinterpret_cast<float*>(smem);
+  uint16_t* perm = reinterpret_cast<uint16_t*>(state + (size_t)T * RP);
+  uint16_t* rnk = perm + T;
+  IdxT* idxs = reinterpret_cast<IdxT*>(rnk + T);
+  size_t off = (size_t)T * RP * 4 + (size_t)T * 4 + (size_t)N * T * sizeof(IdxT);
+  off = (off + 15) & ~(size_t)15;
+  int* cnt = reinterpret_cast<int*>(smem + off);
+  int* start = cnt + jcap + 1;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int nwarps = kThreads / 32;
+  const int gi = lane / L;   // sample group within the warp
+  const int q = lane % L;    // lane within the group -> columns q*C .. q*C+C-1
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int64_t ntiles = (m + T - 1) / T;
+
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t s0 = tile * T;
+    const int tn = (int)((m - s0) < T ? (m - s0) : T);
+    {  // warm L2 with the next tile's index block
+      const int64_t nt = tile + gridDim.x;
+      if (nt < ntiles) {
+        const int64_t ns0 = nt * T;
+        const int64_t nbytes = ((m - ns0) < T ? (m - ns0) : T) * N * 8;
+        const char* base = reinterpret_cast<const char*>(idx + ns0 * N);
+        for (int64_t o = (int64_t)tid * 128; o < nbytes; o += (int64_t)kThreads * 128)
+          prefetch_l2(base + o);
+      }
+    }
+    // ---- indices: coalesced int64 read, wrap/validate, compact, mode-major
+    {
+      const int64_t* src = idx + s0 * N;
+      const int total = tn * N;
+      int s = tid / N, k = tid - (tid / N) * N;
+      const int ds = kThreads / N, dk = kThreads - ds * N;
+      for (int e = tid; e < total; e += kThreads) {
+        const ModeDev& md = ch.m[k];
+        const int j = norm_index(ld_stream_i64(src + e), md.J, k, err);
+        idxs[(size_t)k * T + s] = (IdxT)j;
+        s += ds;
+        k += dk;
+        if (k >= N) {
+          k -= N;
+          ++s;
+        }
+      }
+    }
+    __syncthreads();
+
+    for (int k = 0; k < N; ++k) {
+      const ModeDev& md = ch.m[k];
+      const IdxT* col = idxs + (size_t)k * T;
+      const int rl = md.rl, rr = md.rr;
+      if (k == 0) {
+        if (N == 1) {  // [J][1][1]
+          for (int s = tid; s < tn; s += kThreads) out[s0 + s] = __ldg(md.s + col[s]);
+        } else {       // state row = G_0[j][0][:], zero padded to R
+          for (int e = tid; e < tn * R; e += kThreads) {
+            const int s = e / R, c = e - (e / R) * R;
+            state[s * RP + c] = (c < rr) ? __ldg(md.s + (int64_t)col[s] * rr + c) : 0.f;
+          }
+        }
+      } else if (md.layout == TNB_LAYOUT_DIAG) {
+        for (int e = tid; e < tn * R; e += kThreads) {
+          const int s = e / R, c = e - (e / R) * R;
+          if (c < rl) state[s * RP + c] *= __ldg(md.s + (int64_t)col[s] * rl + c);
+        }
+      } else if (k == N - 1) {  // rr == 1: out = state . G[j][:, 0]
+        for (int s = tid; s < tn; s += kThreads) {
+          const float* g = md.s + (int64_t)col[s] * rl;
+          const float* v = state + s * RP;
+          float acc = 0.f;
+#pragma unroll
+          for (int a = 0; a < R; ++a)
+            if (a < rl) acc = fmaf(v[a], __ldg(g + a), acc);
+          out[s0 + s] = acc;
+        }
+      } else {
+        // ---- counting sort of the tile by this mode's index ----
+        const int J = md.J;
+        for (int j = tid; j <= J; j += kThreads) cnt[j] = 0;
+        __syncthreads();
+        const int tn32 = (tn + 31) & ~31;
+        for (int s = tid; s < tn32; s += kThreads) {
+          const bool act = s < tn;
+          const unsigned amask = __ballot_sync(0xffffffffu, act);
+          if (act) {
+            const int key = col[s];
+            const unsigned peers = __match_any_sync(amask, key);
+            const int leader = __ffs(peers) - 1;
+            int base = 0;
+            if (lane == leader) base = atomicAdd(&cnt[key], __popc(peers));
+            base = __shfl_sync(peers, base, leader);
+            rnk[s] = (uint16_t)(base + __popc(peers & lt_mask));
+          }
+        }
+        __syncthreads();
+        if (warp == 0) {  // exclusive scan of cnt[0..J) -> start
+          const int per = (J + 31) / 32;
+          const int lo = lane * per;
+          int sum = 0;
+          for (int j = lo; j < lo + per && j < J; ++j) sum += cnt[j];
+          int incl = sum;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+          }
+          int run = incl - sum;
+          for (int j = lo; j < lo + per && j < J; ++j) {
+            start[j] = run;
+            run += cnt[j];
+          }
+        }
+        __syncthreads();
+        for (int s = tid; s < tn; s += kThreads) perm[start[col[s]] + rnk[s]] = (uint16_t)s;
+        __syncthreads();
+
+        // ---- warp ranges of sorted positions; core slice in registers ----
+        const int lo = (int)(((int64_t)warp * tn) / nwarps);
+        const int hi = (int)(((int64_t)(warp + 1) * tn) / nwarps);
+        int p = lo;
+        while (p < hi) {
+          const int key = col[perm[p]];
+          const int bend = min(start[key] + cnt[key], hi);
+          float g[R][C];
+          const float* gs = md.s + (int64_t)key * rl * rr;
+#pragma unroll
+          for (int a = 0; a < R; ++a)
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+              const int cc = q * C + c;
+              g[a][c] = (a < rl && cc < rr) ? __ldg(gs + a * rr + cc) : 0.f;
+            }
+          for (; p < bend; p += 8) {
+            const int n = min(8, bend - p);
+            int sid[P];
+#pragma unroll
+            for (int pi = 0; pi < P; ++pi) {
+              const int w = pi * G + gi;
+              sid[pi] = (w < n) ? (int)perm[p + w] : -1;
+            }
+            float acc[P][C];
+#pragma unroll
+            for (int pi = 0; pi < P; ++pi)
+#pragma unroll
+              for (int c = 0; c < C; ++c) acc[pi][c] = 0.f;
+#pragma unroll
+            for (int a4 = 0; a4 < R / 4; ++a4) {
+              float4 v[P];
+#pragma unroll
+              for (int pi = 0; pi < P; ++pi)
+                v[pi] = (sid[pi] >= 0)
+                            ? *reinterpret_cast<const float4*>(state + sid[pi] * RP + a4 * 4)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+              for (int pi = 0; pi < P; ++pi)
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                  acc[pi][c] = fmaf(v[pi].x, g[a4 * 4 + 0][c], acc[pi][c]);
+                  acc[pi][c] = fmaf(v[pi].y, g[a4 * 4 + 1][c], acc[pi][c]);
+                  acc[pi][c] = fmaf(v[pi].z, g[a4 * 4 + 2][c], acc[pi][c]);
+                  acc[pi][c] = fmaf(v[pi].w, g[a4 * 4 + 3][c], acc[pi][c]);
+                }
+            }
+            __syncwarp();  // every lane of a group has read its sample's row
+#pragma unroll
+            for (int pi = 0; pi < P; ++pi)
+              if (sid[pi] >= 0) {
+                float* dst = state + sid[pi] * RP + q * C;
+                if constexpr (C == 2) {
+                  *reinterpret_cast<float2*>(dst) = make_float2(acc[pi][0], acc[pi][1]);
+                } else {
+#pragma unroll
+                  for (int c = 0; c < C; ++c) dst[c] = acc[pi][c];
+                }
+              }
+            __syncwarp();
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+int pick_R(int rmax) {
+  if (rmax <= 8) return 8;
+  if (rmax <= 16) return 16;
+  if (rmax <= 24) return 24;
+  if (rmax <= 32) return 32;
+  return 0;
+}
+
+template <int R, typename IdxT>
+int launch_t(const ChainDev& ch, const int64_t* idx, int64_t m, float* out, int32_t* err,
+             int jcap, cudaStream_t st) {
+  constexpr int RP = Geo<R>::RP;
+  // largest tile (multiple of 32, < 65536) that fits the smem budget
+  int T = 65504;
+  while (T > 32 && smem_bytes<IdxT>(T, RP, ch.n, jcap) > (size_t)kSmemLimit) T -= 32;
+  const size_t smem = smem_bytes<IdxT>(T, RP, ch.n, jcap);
+  if (smem > (size_t)kSmemLimit) return set_error(TNB_EINVAL, "bucketed: chain too long for smem");
+  auto kern = entries_bucketed_kernel<R, IdxT>;
+  int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem),
+                      "bucketed smem attr");
+  if (rc) return rc;
+  const int64_t ntiles = (m + T - 1) / T;
+  const int grid = (int)(ntiles < num_sms() ? ntiles : num_sms());
+  kern<<<grid, kThreads, smem, st>>>(ch, idx, m, out, err, T, jcap);
+  return check_launch("entries_bucketed");
+}
+
+}  // namespace
+
+bool bucketed_supported(const ChainDev& ch) {
+  if (ch.batch != 1 || ch.n < 1 || ch.n > kMaxModes || pick_R(ch.rmax) == 0) return false;
+  for (int k = 0; k < ch.n; ++k) {
+    const ModeDev& md = ch.m[k];
+    if (md.J <= 0 || md.J > 65535) return false;
+    if (md.bstride != 0) return false;
+    const bool sorted = k > 0 && k < ch.n - 1 && md.layout == TNB_LAYOUT_DENSE;
+    if (sorted && md.J > kMaxJ) return false;
+  }
+  return true;
+}
+
+int launch_entries_bucketed(const ChainDev& ch, const int64_t* idx, int64_t m, float* out,
+                            int32_t* err, cudaStream_t st) {
+  int jmax = 1;
+  bool small = true;
+  for (int k = 0; k < ch.n; ++k) {
+    if (ch.m[k].J > 256) small = false;
+    if (k > 0 && k < ch.n - 1 && ch.m[k].layout == TNB_LAYOUT_DENSE && ch.m[k].J > jmax)
+      jmax = ch.m[k].J;
+  }
+  const int jcap = jmax;
+  switch (pick_R(ch.rmax)) {
+    case 8:
+      return small ? launch_t<8, uint8_t>(ch, idx, m, out, err, jcap, st)
+                   : launch_t<8, uint16_t>(ch, idx, m, out, err, jcap, st);
+    case 16:
+      return small ? launch_t<16, uint8_t>(ch, idx, m, out, err, jcap, st)
+                   : launch_t<16, uint16_t>(ch, idx, m, out, err, jcap, st);
+    case 24:
+      return small ? launch_t<24, uint8_t>(ch, idx, m, out, err, jcap, st)
+                   : launch_t<24, uint16_t>(ch, idx, m, out, err, jcap, st);
+    case 32:
+      return small ? launch_t<32, uint8_t>(ch, idx, m, out, err, jcap, st)
+                   : launch_t<32, uint16_t>(ch, idx, m, out, err, jcap, st);
+  }
+  return set_error(TNB_EINVAL, "bucketed: rank > 32");
+}
+
 }  // namespace tnb

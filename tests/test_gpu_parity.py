@@ -14,7 +14,7 @@ torch = pytest.importorskip("torch")
 tb = pytest.importorskip("paper_2206_11128_b200")
 from paper_2206_11128_b200 import _native as N  # noqa: E402
 
-ALGOS = [N.ALGO_AUTO, N.ALGO_LAYERED, N.ALGO_CHAIN]
+ALGOS = [N.ALGO_AUTO, N.ALGO_LAYERED, N.ALGO_CHAIN, N.ALGO_BUCKETED]
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -42,6 +42,10 @@ def test_golden_full_norm(name):
 def test_golden_entries(name, algo):
     c = G.case(name)
     t = facade(c["nodes"], c["batch"])
+    if algo == N.ALGO_BUCKETED and c["batch"] is not None:
+        with pytest.raises(tb.ContractViolationError, match="bucketed"):
+            tb.entries(t, c["out"]["idx"], algo=algo)
+        return
     got = tb.entries(t, c["out"]["idx"], algo=algo)
     assert_close(got, c["out"]["entries"], what=f"{name} entries algo={algo}")
 
@@ -198,3 +202,38 @@ def test_batched_dot_equals_loop():
     vec = to_np(tb.dot(a, b))
     for e in range(3):
         assert abs(vec[e] - tb.dot(a.batch_element(e), b.batch_element(e))) <= 1e-6 * max(abs(vec[e]), 1)
+
+
+@pytest.mark.parametrize("m", [1, 31, 1000, 5000, 70001])
+@pytest.mark.parametrize("algo", [N.ALGO_BUCKETED, N.ALGO_AUTO])
+def test_bucketed_tiles_and_tails(m, algo):
+    # ragged tile tails, ranks that are not multiples of 4, a rank-1 edge,
+    # an interior CP (diagonal) mode and Tucker factors, uint8 compaction
+    rng = np.random.default_rng(m)
+    nodes = [
+        ("tt", rng.standard_normal((1, 5, 3)).astype(np.float32), None),
+        ("cp", rng.standard_normal((7, 3)).astype(np.float32), rng.standard_normal((11, 7)).astype(np.float32)),
+        ("tt", rng.standard_normal((3, 4, 1)).astype(np.float32), None),
+        ("tt", rng.standard_normal((1, 6, 7)).astype(np.float32), rng.standard_normal((9, 6)).astype(np.float32)),
+        ("tt", rng.standard_normal((7, 13, 2)).astype(np.float32), None),
+        ("tt", rng.standard_normal((2, 3, 1)).astype(np.float32), None),
+    ]
+    t = facade(nodes)
+    o = O.make_chain(nodes)
+    idx = O.uniform_indices(t.shape, m, 5)
+    idx[::3] -= np.asarray(t.shape)
+    assert_close(tb.entries(t, idx, algo=algo), O.entries(o, idx), what=f"m={m}")
+    bad = idx.copy()
+    bad[m // 2, 4] = 13
+    with pytest.raises(tb.ContractViolationError, match="mode 4"):
+        tb.entries(t, bad, algo=algo)
+
+
+@pytest.mark.parametrize("r,J", [(8, 300), (16, 40), (24, 128), (32, 32), (32, 1024)])
+def test_bucketed_rank_classes(r, J):
+    # every register geometry (R = 8/16/24/32) and the uint16 index path
+    cores = O.random_tt((J, J, 5, J), r, seed=r + J, scale=r ** -0.5)
+    t = facade([("tt", c, None) for c in cores])
+    o = O.make_chain([("tt", c) for c in cores])
+    idx = O.uniform_indices(t.shape, 20000, 1)
+    assert_close(tb.entries(t, idx, algo=N.ALGO_BUCKETED), O.entries(o, idx), what=f"r={r} J={J}")
