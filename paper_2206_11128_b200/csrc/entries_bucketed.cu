@@ -46,6 +46,19 @@ __device__ __forceinline__ int64_t ld_stream_i64(const int64_t* p) {
   return v;
 }
 
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts64(uint32_t a, float x, float y) {
+  asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(x), "f"(y) : "memory");
+}
+__device__ __forceinline__ void sts32(uint32_t a, float x) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(x) : "memory");
+}
+
 template <int R>
 struct Geo {
   static constexpr int C = (R == 24) ? 3 : 2;  // output columns per lane
@@ -58,7 +71,7 @@ struct Geo {
 
 template <typename IdxT>
 __host__ __device__ inline size_t smem_bytes(int T, int RP, int N, int jcap) {
-  size_t b = (size_t)T * RP * sizeof(float);      // state
+  size_t b = (size_t)(T + 1) * RP * sizeof(float);  // state (+ dummy row)
   b += (size_t)T * 2 * sizeof(uint16_t);          // perm + rank
   b += (size_t)N * T * sizeof(IdxT);              // compact indices
   b = (b + 15) & ~(size_t)15;
@@ -76,14 +89,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(16) unsigned char smem[];
   const int N = ch.n;
   float* state = reinterpret_cast<float*>(smem);
-  uint16_t* perm = reinterpret_cast<uint16_t*>(state + (size_t)T * RP);
+  uint16_t* perm = reinterpret_cast<uint16_t*>(state + (size_t)(T + 1) * RP);
   uint16_t* rnk = perm + T;
   IdxT* idxs = reinterpret_cast<IdxT*>(rnk + T);
-  size_t off = (size_t)T * RP * 4 + (size_t)T * 4 + (size_t)N * T * sizeof(IdxT);
+  size_t off = (size_t)(T + 1) * RP * 4 + (size_t)T * 4 + (size_t)N * T * sizeof(IdxT);
   off = (off + 15) & ~(size_t)15;
   int* cnt = reinterpret_cast<int*>(smem + off);
   int* start = cnt + jcap + 1;
 
+  const uint32_t s_state = (uint32_t)__cvta_generic_to_shared(state);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int nwarps = kThreads / 32;
   const int gi = lane / L;   // sample group within the warp
@@ -209,13 +223,15 @@ __global__ void __launch_bounds__(kThreads, 1)
               const int cc = q * C + c;
               g[a][c] = (a < rl && cc < rr) ? __ldg(gs + a * rr + cc) : 0.f;
             }
-          for (; p < bend; p += 8) {
+          while (p < bend) {
             const int n = min(8, bend - p);
-            int sid[P];
+            // empty slots of a ragged last iteration point at the dummy row T
+            uint32_t row[P];
 #pragma unroll
             for (int pi = 0; pi < P; ++pi) {
               const int w = pi * G + gi;
-              sid[pi] = (w < n) ? (int)perm[p + w] : -1;
+              const int sidx = (w < n) ? (int)perm[p + w] : T;
+              row[pi] = s_state + (uint32_t)sidx * (RP * 4);
             }
             float acc[P][C];
 #pragma unroll
@@ -226,10 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int a4 = 0; a4 < R / 4; ++a4) {
               float4 v[P];
 #pragma unroll
-              for (int pi = 0; pi < P; ++pi)
-                v[pi] = (sid[pi] >= 0)
-                            ? *reinterpret_cast<const float4*>(state + sid[pi] * RP + a4 * 4)
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
+              for (int pi = 0; pi < P; ++pi) v[pi] = lds128(row[pi] + a4 * 16);
 #pragma unroll
               for (int pi = 0; pi < P; ++pi)
 #pragma unroll
@@ -242,17 +255,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             __syncwarp();  // every lane of a group has read its sample's row
 #pragma unroll
-            for (int pi = 0; pi < P; ++pi)
-              if (sid[pi] >= 0) {
-                float* dst = state + sid[pi] * RP + q * C;
-                if constexpr (C == 2) {
-                  *reinterpret_cast<float2*>(dst) = make_float2(acc[pi][0], acc[pi][1]);
-                } else {
+            for (int pi = 0; pi < P; ++pi) {
+              const uint32_t dst = row[pi] + q * (C * 4);
+              if constexpr (C == 2) {
+                sts64(dst, acc[pi][0], acc[pi][1]);
+              } else {
 #pragma unroll
-                  for (int c = 0; c < C; ++c) dst[c] = acc[pi][c];
-                }
+                for (int c = 0; c < C; ++c) sts32(dst + 4 * c, acc[pi][c]);
               }
+            }
             __syncwarp();
+            p += n;
           }
         }
       }
