@@ -55,10 +55,32 @@ __device__ __forceinline__ float4 lds128(uint32_t a) {
 __device__ __forceinline__ void sts64(uint32_t a, float x, float y) {
   asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(x), "f"(y) : "memory");
 }
+__device__ __forceinline__ void sts_b64(uint32_t a, uint64_t x) {
+  asm volatile("st.shared.b64 [%0], %1;" ::"r"(a), "l"(x) : "memory");
+}
+// acc.{x,y} += g.{x,y} * v  (packed fp32 FMA, one issue slot for two FMAs)
+__device__ __forceinline__ void ffma2(uint64_t& acc, uint64_t g, float v) {
+  asm("{\n\t.reg .b64 vv;\n\tmov.b64 vv, {%2, %2};\n\tfma.rn.f32x2 %0, %1, vv, %0;\n\t}"
+      : "+l"(acc)
+      : "l"(g), "f"(v));
+}
+__device__ __forceinline__ uint64_t ldg_b64(const float* p) {
+  uint64_t v;
+  asm volatile("ld.global.nc.b64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint64_t pack2(float lo, float hi) {
+  uint64_t v;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(v) : "f"(lo), "f"(hi));
+  return v;
+}
 __device__ __forceinline__ void sts32(uint32_t a, float x) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(x) : "memory");
 }
 
+// Column ownership inside a sample group of L lanes (lane q): C == 2 -> the
+// pair (2q, 2q+1); C == 3 (R = 24, L = 8) -> the pair (2q, 2q+1) plus the
+// single column 16 + q.  Pairs are updated with packed FFMA2 (fma.rn.f32x2).
 template <int R>
 struct Geo {
   static constexpr int C = (R == 24) ? 3 : 2;  // output columns per lane
@@ -118,21 +140,40 @@ __global__ void __launch_bounds__(kThreads, 1)
           prefetch_l2(base + o);
       }
     }
-    // ---- indices: coalesced int64 read, wrap/validate, compact, mode-major
+    // ---- indices: coalesced int64 read (4 loads in flight per thread),
+    //      wrap/validate, compact, mode-major
     {
       const int64_t* src = idx + s0 * N;
       const int total = tn * N;
-      int s = tid / N, k = tid - (tid / N) * N;
-      const int ds = kThreads / N, dk = kThreads - ds * N;
-      for (int e = tid; e < total; e += kThreads) {
-        const ModeDev& md = ch.m[k];
-        const int j = norm_index(ld_stream_i64(src + e), md.J, k, err);
-        idxs[(size_t)k * T + s] = (IdxT)j;
-        s += ds;
-        k += dk;
-        if (k >= N) {
-          k -= N;
-          ++s;
+      constexpr int U = 4;
+      int ss[U], kk[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = tid + u * kThreads;
+        ss[u] = e / N;
+        kk[u] = e - ss[u] * N;
+      }
+      const int ds = (U * kThreads) / N, dk = (U * kThreads) - ds * N;
+      for (int e0 = tid; e0 < total; e0 += U * kThreads) {
+        int64_t raw[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = e0 + u * kThreads;
+          raw[u] = (e < total) ? ld_stream_i64(src + e) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (e0 + u * kThreads < total) {
+            const int k = kk[u];
+            const int j = norm_index(raw[u], ch.m[k].J, k, err);
+            idxs[(size_t)k * T + ss[u]] = (IdxT)j;
+          }
+          ss[u] += ds;
+          kk[u] += dk;
+          if (kk[u] >= N) {
+            kk[u] -= N;
+            ++ss[u];
+          }
         }
       }
     }
@@ -157,14 +198,34 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (c < rl) state[s * RP + c] *= __ldg(md.s + (int64_t)col[s] * rl + c);
         }
       } else if (k == N - 1) {  // rr == 1: out = state . G[j][:, 0]
-        for (int s = tid; s < tn; s += kThreads) {
-          const float* g = md.s + (int64_t)col[s] * rl;
-          const float* v = state + s * RP;
-          float acc = 0.f;
+        if (rl == R) {  // full rank: unpredicated 16-byte loads, two FMA chains
+          for (int s = tid; s < tn; s += kThreads) {
+            const float4* g4 = reinterpret_cast<const float4*>(md.s + (int64_t)col[s] * R);
+            const uint32_t vrow = s_state + (uint32_t)s * (RP * 4);
+            float4 gv[R / 4];
 #pragma unroll
-          for (int a = 0; a < R; ++a)
-            if (a < rl) acc = fmaf(v[a], __ldg(g + a), acc);
-          out[s0 + s] = acc;
+            for (int a4 = 0; a4 < R / 4; ++a4) gv[a4] = __ldg(g4 + a4);
+            float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+            for (int a4 = 0; a4 < R / 4; ++a4) {
+              const float4 v = lds128(vrow + a4 * 16);
+              acc0 = fmaf(v.x, gv[a4].x, acc0);
+              acc1 = fmaf(v.y, gv[a4].y, acc1);
+              acc0 = fmaf(v.z, gv[a4].z, acc0);
+              acc1 = fmaf(v.w, gv[a4].w, acc1);
+            }
+            out[s0 + s] = acc0 + acc1;
+          }
+        } else {
+          for (int s = tid; s < tn; s += kThreads) {
+            const float* g = md.s + (int64_t)col[s] * rl;
+            const float* v = state + s * RP;
+            float acc = 0.f;
+#pragma unroll
+            for (int a = 0; a < R; ++a)
+              if (a < rl) acc = fmaf(v[a], __ldg(g + a), acc);
+            out[s0 + s] = acc;
+          }
         }
       } else {
         // ---- counting sort of the tile by this mode's index ----
@@ -214,15 +275,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         while (p < hi) {
           const int key = col[perm[p]];
           const int bend = min(start[key] + cnt[key], hi);
-          float g[R][C];
+          // core slice -> registers (see Geo for the column ownership)
+          constexpr int C1 = (C == 3) ? 1 : 0;
+          uint64_t g2[R];
+          float g1[C1 ? R : 1];
           const float* gs = md.s + (int64_t)key * rl * rr;
+          const int cp = 2 * q, cs = 16 + q;
+          if (rl == R && rr == R) {  // full rank: unpredicated 8-byte loads
 #pragma unroll
-          for (int a = 0; a < R; ++a)
-#pragma unroll
-            for (int c = 0; c < C; ++c) {
-              const int cc = q * C + c;
-              g[a][c] = (a < rl && cc < rr) ? __ldg(gs + a * rr + cc) : 0.f;
+            for (int a = 0; a < R; ++a) {
+              g2[a] = ldg_b64(gs + a * R + cp);
+              if constexpr (C1) g1[a] = __ldg(gs + a * R + cs);
             }
+          } else {
+#pragma unroll
+            for (int a = 0; a < R; ++a) {
+              const bool ra = a < rl;
+              const float x0 = (ra && cp < rr) ? __ldg(gs + a * rr + cp) : 0.f;
+              const float x1 = (ra && cp + 1 < rr) ? __ldg(gs + a * rr + cp + 1) : 0.f;
+              g2[a] = pack2(x0, x1);
+              if constexpr (C1) g1[a] = (ra && cs < rr) ? __ldg(gs + a * rr + cs) : 0.f;
+            }
+          }
           while (p < bend) {
             const int n = min(8, bend - p);
             // empty slots of a ragged last iteration point at the dummy row T
@@ -233,36 +307,37 @@ __global__ void __launch_bounds__(kThreads, 1)
               const int sidx = (w < n) ? (int)perm[p + w] : T;
               row[pi] = s_state + (uint32_t)sidx * (RP * 4);
             }
-            float acc[P][C];
+            uint64_t acc2[P];
+            float acc1[P];
 #pragma unroll
-            for (int pi = 0; pi < P; ++pi)
-#pragma unroll
-              for (int c = 0; c < C; ++c) acc[pi][c] = 0.f;
+            for (int pi = 0; pi < P; ++pi) {
+              acc2[pi] = 0ull;
+              acc1[pi] = 0.f;
+            }
 #pragma unroll
             for (int a4 = 0; a4 < R / 4; ++a4) {
               float4 v[P];
 #pragma unroll
               for (int pi = 0; pi < P; ++pi) v[pi] = lds128(row[pi] + a4 * 16);
 #pragma unroll
-              for (int pi = 0; pi < P; ++pi)
-#pragma unroll
-                for (int c = 0; c < C; ++c) {
-                  acc[pi][c] = fmaf(v[pi].x, g[a4 * 4 + 0][c], acc[pi][c]);
-                  acc[pi][c] = fmaf(v[pi].y, g[a4 * 4 + 1][c], acc[pi][c]);
-                  acc[pi][c] = fmaf(v[pi].z, g[a4 * 4 + 2][c], acc[pi][c]);
-                  acc[pi][c] = fmaf(v[pi].w, g[a4 * 4 + 3][c], acc[pi][c]);
+              for (int pi = 0; pi < P; ++pi) {
+                ffma2(acc2[pi], g2[a4 * 4 + 0], v[pi].x);
+                ffma2(acc2[pi], g2[a4 * 4 + 1], v[pi].y);
+                ffma2(acc2[pi], g2[a4 * 4 + 2], v[pi].z);
+                ffma2(acc2[pi], g2[a4 * 4 + 3], v[pi].w);
+                if constexpr (C1) {
+                  acc1[pi] = fmaf(v[pi].x, g1[a4 * 4 + 0], acc1[pi]);
+                  acc1[pi] = fmaf(v[pi].y, g1[a4 * 4 + 1], acc1[pi]);
+                  acc1[pi] = fmaf(v[pi].z, g1[a4 * 4 + 2], acc1[pi]);
+                  acc1[pi] = fmaf(v[pi].w, g1[a4 * 4 + 3], acc1[pi]);
                 }
+              }
             }
             __syncwarp();  // every lane of a group has read its sample's row
 #pragma unroll
             for (int pi = 0; pi < P; ++pi) {
-              const uint32_t dst = row[pi] + q * (C * 4);
-              if constexpr (C == 2) {
-                sts64(dst, acc[pi][0], acc[pi][1]);
-              } else {
-#pragma unroll
-                for (int c = 0; c < C; ++c) sts32(dst + 4 * c, acc[pi][c]);
-              }
+              sts_b64(row[pi] + cp * 4, acc2[pi]);
+              if constexpr (C1) sts32(row[pi] + cs * 4, acc1[pi]);
             }
             __syncwarp();
             p += n;
