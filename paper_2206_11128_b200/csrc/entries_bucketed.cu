@@ -32,9 +32,7 @@
 namespace tnb {
 namespace {
 
-constexpr int kThreads = 512;
 constexpr int kMaxJ = 1024;          // bucket count limit for sorted modes
-constexpr int kSmemLimit = 232448;   // 227 KB dynamic smem per CTA on sm_100
 
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
@@ -64,6 +62,11 @@ __device__ __forceinline__ void ffma2(uint64_t& acc, uint64_t g, float v) {
       : "+l"(acc)
       : "l"(g), "f"(v));
 }
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
 __device__ __forceinline__ uint64_t ldg_b64(const float* p) {
   uint64_t v;
   asm volatile("ld.global.nc.b64 %0, [%1];" : "=l"(v) : "l"(p));
@@ -91,6 +94,39 @@ struct Geo {
   static_assert(L * C == R && 32 % L == 0 && G * P == 8, "geometry");
 };
 
+
+// K-split pass group for R == 32: NP samples (one per pass) of one bucket.
+// Lane (h, qq) holds rows 16h..16h+15 of the core slice, column pair
+// (2qq, 2qq+1); the two row halves are summed with one 64-bit shuffle.
+template <int NP, int RP>
+__device__ __forceinline__ void ks_passes(const uint64_t (&g2)[16], const uint16_t* perm, int p,
+                                          uint32_t s_state, int h, int qq) {
+  uint32_t rowb[NP];
+#pragma unroll
+  for (int pi = 0; pi < NP; ++pi) rowb[pi] = s_state + (uint32_t)perm[p + pi] * (RP * 4);
+  uint64_t acc2[NP];
+#pragma unroll
+  for (int pi = 0; pi < NP; ++pi) acc2[pi] = 0ull;
+#pragma unroll
+  for (int a4 = 0; a4 < 4; ++a4) {
+#pragma unroll
+    for (int pi = 0; pi < NP; ++pi) {
+      const float4 v = lds128(rowb[pi] + h * 64 + a4 * 16);
+      ffma2(acc2[pi], g2[a4 * 4 + 0], v.x);
+      ffma2(acc2[pi], g2[a4 * 4 + 1], v.y);
+      ffma2(acc2[pi], g2[a4 * 4 + 2], v.z);
+      ffma2(acc2[pi], g2[a4 * 4 + 3], v.w);
+    }
+  }
+#pragma unroll
+  for (int pi = 0; pi < NP; ++pi) acc2[pi] = add2(acc2[pi], __shfl_xor_sync(0xffffffffu, acc2[pi], 16));
+  __syncwarp();  // every lane has read its rows
+#pragma unroll
+  for (int pi = 0; pi < NP; ++pi)
+    if ((pi & 1) == (NP > 1 ? h : 0)) sts_b64(rowb[pi] + qq * 8, acc2[pi]);
+  __syncwarp();
+}
+
 template <typename IdxT>
 __host__ __device__ inline size_t smem_bytes(int T, int RP, int N, int jcap) {
   size_t b = (size_t)(T + 1) * RP * sizeof(float);  // state (+ dummy row)
@@ -101,8 +137,8 @@ __host__ __device__ inline size_t smem_bytes(int T, int RP, int N, int jcap) {
   return b;
 }
 
-template <int R, typename IdxT>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int R, typename IdxT, int NT>
+__global__ void __launch_bounds__(NT, 512 / NT)
     entries_bucketed_kernel(const __grid_constant__ ChainDev ch, const int64_t* __restrict__ idx,
                             int64_t m, float* __restrict__ out, int32_t* __restrict__ err, int T,
                             int jcap) {
@@ -121,7 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const uint32_t s_state = (uint32_t)__cvta_generic_to_shared(state);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int nwarps = kThreads / 32;
+  constexpr int nwarps = NT / 32;
   const int gi = lane / L;   // sample group within the warp
   const int q = lane % L;    // lane within the group -> columns q*C .. q*C+C-1
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -136,7 +172,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t ns0 = nt * T;
         const int64_t nbytes = ((m - ns0) < T ? (m - ns0) : T) * N * 8;
         const char* base = reinterpret_cast<const char*>(idx + ns0 * N);
-        for (int64_t o = (int64_t)tid * 128; o < nbytes; o += (int64_t)kThreads * 128)
+        for (int64_t o = (int64_t)tid * 128; o < nbytes; o += (int64_t)NT * 128)
           prefetch_l2(base + o);
       }
     }
@@ -149,21 +185,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       int ss[U], kk[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int e = tid + u * kThreads;
+        const int e = tid + u * NT;
         ss[u] = e / N;
         kk[u] = e - ss[u] * N;
       }
-      const int ds = (U * kThreads) / N, dk = (U * kThreads) - ds * N;
-      for (int e0 = tid; e0 < total; e0 += U * kThreads) {
+      const int ds = (U * NT) / N, dk = (U * NT) - ds * N;
+      for (int e0 = tid; e0 < total; e0 += U * NT) {
         int64_t raw[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int e = e0 + u * kThreads;
+          const int e = e0 + u * NT;
           raw[u] = (e < total) ? ld_stream_i64(src + e) : 0;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          if (e0 + u * kThreads < total) {
+          if (e0 + u * NT < total) {
             const int k = kk[u];
             const int j = norm_index(raw[u], ch.m[k].J, k, err);
             idxs[(size_t)k * T + ss[u]] = (IdxT)j;
@@ -185,21 +221,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int rl = md.rl, rr = md.rr;
       if (k == 0) {
         if (N == 1) {  // [J][1][1]
-          for (int s = tid; s < tn; s += kThreads) out[s0 + s] = __ldg(md.s + col[s]);
+          for (int s = tid; s < tn; s += NT) out[s0 + s] = __ldg(md.s + col[s]);
+        } else if (rr == R) {  // state row = G_0[j][0][:] (16-byte copies)
+          for (int e = tid; e < tn * (R / 4); e += NT) {
+            const int s = e / (R / 4), c4 = e - (e / (R / 4)) * (R / 4);
+            const float4 g = __ldg(reinterpret_cast<const float4*>(md.s + (int64_t)col[s] * R) + c4);
+            *reinterpret_cast<float4*>(state + s * RP + c4 * 4) = g;
+          }
         } else {       // state row = G_0[j][0][:], zero padded to R
-          for (int e = tid; e < tn * R; e += kThreads) {
+          for (int e = tid; e < tn * R; e += NT) {
             const int s = e / R, c = e - (e / R) * R;
             state[s * RP + c] = (c < rr) ? __ldg(md.s + (int64_t)col[s] * rr + c) : 0.f;
           }
         }
       } else if (md.layout == TNB_LAYOUT_DIAG) {
-        for (int e = tid; e < tn * R; e += kThreads) {
+        for (int e = tid; e < tn * R; e += NT) {
           const int s = e / R, c = e - (e / R) * R;
           if (c < rl) state[s * RP + c] *= __ldg(md.s + (int64_t)col[s] * rl + c);
         }
       } else if (k == N - 1) {  // rr == 1: out = state . G[j][:, 0]
         if (rl == R) {  // full rank: unpredicated 16-byte loads, two FMA chains
-          for (int s = tid; s < tn; s += kThreads) {
+          for (int s = tid; s < tn; s += NT) {
             const float4* g4 = reinterpret_cast<const float4*>(md.s + (int64_t)col[s] * R);
             const uint32_t vrow = s_state + (uint32_t)s * (RP * 4);
             float4 gv[R / 4];
@@ -217,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             out[s0 + s] = acc0 + acc1;
           }
         } else {
-          for (int s = tid; s < tn; s += kThreads) {
+          for (int s = tid; s < tn; s += NT) {
             const float* g = md.s + (int64_t)col[s] * rl;
             const float* v = state + s * RP;
             float acc = 0.f;
@@ -230,15 +272,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else {
         // ---- counting sort of the tile by this mode's index ----
         const int J = md.J;
-        for (int j = tid; j <= J; j += kThreads) cnt[j] = 0;
+        const int kbits = 32 - __clz(J > 1 ? J - 1 : 1);
+        for (int j = tid; j <= J; j += NT) cnt[j] = 0;
         __syncthreads();
         const int tn32 = (tn + 31) & ~31;
-        for (int s = tid; s < tn32; s += kThreads) {
+        for (int s = tid; s < tn32; s += NT) {
           const bool act = s < tn;
           const unsigned amask = __ballot_sync(0xffffffffu, act);
           if (act) {
             const int key = col[s];
-            const unsigned peers = __match_any_sync(amask, key);
+            // lanes holding the same key: AND of per-bit ballots (cheaper
+            // than MATCH.ANY for the <= 10-bit keys of sorted modes)
+            unsigned peers = amask;
+            for (int b = 0; b < kbits; ++b) {
+              const bool bit = (key >> b) & 1;
+              const unsigned bal = __ballot_sync(amask, bit);
+              peers &= bit ? bal : ~bal;
+            }
             const int leader = __ffs(peers) - 1;
             int base = 0;
             if (lane == leader) base = atomicAdd(&cnt[key], __popc(peers));
@@ -265,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         __syncthreads();
-        for (int s = tid; s < tn; s += kThreads) perm[start[col[s]] + rnk[s]] = (uint16_t)s;
+        for (int s = tid; s < tn; s += NT) perm[start[col[s]] + rnk[s]] = (uint16_t)s;
         __syncthreads();
 
         // ---- warp ranges of sorted positions; core slice in registers ----
@@ -275,72 +325,111 @@ __global__ void __launch_bounds__(kThreads, 1)
         while (p < hi) {
           const int key = col[perm[p]];
           const int bend = min(start[key] + cnt[key], hi);
-          // core slice -> registers (see Geo for the column ownership)
-          constexpr int C1 = (C == 3) ? 1 : 0;
-          uint64_t g2[R];
-          float g1[C1 ? R : 1];
-          const float* gs = md.s + (int64_t)key * rl * rr;
-          const int cp = 2 * q, cs = 16 + q;
-          if (rl == R && rr == R) {  // full rank: unpredicated 8-byte loads
+          if constexpr (R == 32) {
+            // K-split geometry: lane (h, qq) owns rows 16h..16h+15 and the
+            // column pair (2qq, 2qq+1); one sample per pass, the two row
+            // halves are summed with one 64-bit shuffle.  Halves the core
+            // registers (32) so 8 passes stay in flight.
+            const int h = lane >> 4, qq = lane & 15;
+            uint64_t g2[16];
+            const float* gs = md.s + (int64_t)key * rl * rr;
+            if (rl == R && rr == R) {
 #pragma unroll
-            for (int a = 0; a < R; ++a) {
-              g2[a] = ldg_b64(gs + a * R + cp);
-              if constexpr (C1) g1[a] = __ldg(gs + a * R + cs);
-            }
-          } else {
+              for (int i = 0; i < 16; ++i) g2[i] = ldg_b64(gs + (16 * h + i) * R + 2 * qq);
+            } else {
 #pragma unroll
-            for (int a = 0; a < R; ++a) {
-              const bool ra = a < rl;
-              const float x0 = (ra && cp < rr) ? __ldg(gs + a * rr + cp) : 0.f;
-              const float x1 = (ra && cp + 1 < rr) ? __ldg(gs + a * rr + cp + 1) : 0.f;
-              g2[a] = pack2(x0, x1);
-              if constexpr (C1) g1[a] = (ra && cs < rr) ? __ldg(gs + a * rr + cs) : 0.f;
-            }
-          }
-          while (p < bend) {
-            const int n = min(8, bend - p);
-            // empty slots of a ragged last iteration point at the dummy row T
-            uint32_t row[P];
-#pragma unroll
-            for (int pi = 0; pi < P; ++pi) {
-              const int w = pi * G + gi;
-              const int sidx = (w < n) ? (int)perm[p + w] : T;
-              row[pi] = s_state + (uint32_t)sidx * (RP * 4);
-            }
-            uint64_t acc2[P];
-            float acc1[P];
-#pragma unroll
-            for (int pi = 0; pi < P; ++pi) {
-              acc2[pi] = 0ull;
-              acc1[pi] = 0.f;
-            }
-#pragma unroll
-            for (int a4 = 0; a4 < R / 4; ++a4) {
-              float4 v[P];
-#pragma unroll
-              for (int pi = 0; pi < P; ++pi) v[pi] = lds128(row[pi] + a4 * 16);
-#pragma unroll
-              for (int pi = 0; pi < P; ++pi) {
-                ffma2(acc2[pi], g2[a4 * 4 + 0], v[pi].x);
-                ffma2(acc2[pi], g2[a4 * 4 + 1], v[pi].y);
-                ffma2(acc2[pi], g2[a4 * 4 + 2], v[pi].z);
-                ffma2(acc2[pi], g2[a4 * 4 + 3], v[pi].w);
-                if constexpr (C1) {
-                  acc1[pi] = fmaf(v[pi].x, g1[a4 * 4 + 0], acc1[pi]);
-                  acc1[pi] = fmaf(v[pi].y, g1[a4 * 4 + 1], acc1[pi]);
-                  acc1[pi] = fmaf(v[pi].z, g1[a4 * 4 + 2], acc1[pi]);
-                  acc1[pi] = fmaf(v[pi].w, g1[a4 * 4 + 3], acc1[pi]);
-                }
+              for (int i = 0; i < 16; ++i) {
+                const int a = 16 * h + i;
+                const float x0 = (a < rl && 2 * qq < rr) ? __ldg(gs + a * rr + 2 * qq) : 0.f;
+                const float x1 = (a < rl && 2 * qq + 1 < rr) ? __ldg(gs + a * rr + 2 * qq + 1) : 0.f;
+                g2[i] = pack2(x0, x1);
               }
             }
-            __syncwarp();  // every lane of a group has read its sample's row
-#pragma unroll
-            for (int pi = 0; pi < P; ++pi) {
-              sts_b64(row[pi] + cp * 4, acc2[pi]);
-              if constexpr (C1) sts32(row[pi] + cs * 4, acc1[pi]);
+            // exact-size pass groups: no dummy rows, no wasted FMAs
+            while (bend - p >= 8) {
+              ks_passes<8, RP>(g2, perm, p, s_state, h, qq);
+              p += 8;
             }
-            __syncwarp();
-            p += n;
+            if (bend - p >= 4) {
+              ks_passes<4, RP>(g2, perm, p, s_state, h, qq);
+              p += 4;
+            }
+            if (bend - p >= 2) {
+              ks_passes<2, RP>(g2, perm, p, s_state, h, qq);
+              p += 2;
+            }
+            if (bend - p >= 1) {
+              ks_passes<1, RP>(g2, perm, p, s_state, h, qq);
+              p += 1;
+            }
+          } else {
+            // core slice -> registers (see Geo for the column ownership)
+            constexpr int C1 = (C == 3) ? 1 : 0;
+            uint64_t g2[R];
+            float g1[C1 ? R : 1];
+            const float* gs = md.s + (int64_t)key * rl * rr;
+            const int cp = 2 * q, cs = 16 + q;
+            if (rl == R && rr == R) {  // full rank: unpredicated 8-byte loads
+  #pragma unroll
+              for (int a = 0; a < R; ++a) {
+                g2[a] = ldg_b64(gs + a * R + cp);
+                if constexpr (C1) g1[a] = __ldg(gs + a * R + cs);
+              }
+            } else {
+  #pragma unroll
+              for (int a = 0; a < R; ++a) {
+                const bool ra = a < rl;
+                const float x0 = (ra && cp < rr) ? __ldg(gs + a * rr + cp) : 0.f;
+                const float x1 = (ra && cp + 1 < rr) ? __ldg(gs + a * rr + cp + 1) : 0.f;
+                g2[a] = pack2(x0, x1);
+                if constexpr (C1) g1[a] = (ra && cs < rr) ? __ldg(gs + a * rr + cs) : 0.f;
+              }
+            }
+            while (p < bend) {
+              const int n = min(8, bend - p);
+              // empty slots of a ragged last iteration point at the dummy row T
+              uint32_t row[P];
+  #pragma unroll
+              for (int pi = 0; pi < P; ++pi) {
+                const int w = pi * G + gi;
+                const int sidx = (w < n) ? (int)perm[p + w] : T;
+                row[pi] = s_state + (uint32_t)sidx * (RP * 4);
+              }
+              uint64_t acc2[P];
+              float acc1[P];
+  #pragma unroll
+              for (int pi = 0; pi < P; ++pi) {
+                acc2[pi] = 0ull;
+                acc1[pi] = 0.f;
+              }
+  #pragma unroll
+              for (int a4 = 0; a4 < R / 4; ++a4) {
+                float4 v[P];
+  #pragma unroll
+                for (int pi = 0; pi < P; ++pi) v[pi] = lds128(row[pi] + a4 * 16);
+  #pragma unroll
+                for (int pi = 0; pi < P; ++pi) {
+                  ffma2(acc2[pi], g2[a4 * 4 + 0], v[pi].x);
+                  ffma2(acc2[pi], g2[a4 * 4 + 1], v[pi].y);
+                  ffma2(acc2[pi], g2[a4 * 4 + 2], v[pi].z);
+                  ffma2(acc2[pi], g2[a4 * 4 + 3], v[pi].w);
+                  if constexpr (C1) {
+                    acc1[pi] = fmaf(v[pi].x, g1[a4 * 4 + 0], acc1[pi]);
+                    acc1[pi] = fmaf(v[pi].y, g1[a4 * 4 + 1], acc1[pi]);
+                    acc1[pi] = fmaf(v[pi].z, g1[a4 * 4 + 2], acc1[pi]);
+                    acc1[pi] = fmaf(v[pi].w, g1[a4 * 4 + 3], acc1[pi]);
+                  }
+                }
+              }
+              __syncwarp();  // every lane of a group has read its sample's row
+  #pragma unroll
+              for (int pi = 0; pi < P; ++pi) {
+                sts_b64(row[pi] + cp * 4, acc2[pi]);
+                if constexpr (C1) sts32(row[pi] + cs * 4, acc1[pi]);
+              }
+              __syncwarp();
+  p += n;
+            }
           }
         }
       }
@@ -357,24 +446,42 @@ int pick_R(int rmax) {
   return 0;
 }
 
-template <int R, typename IdxT>
-int launch_t(const ChainDev& ch, const int64_t* idx, int64_t m, float* out, int32_t* err,
-             int jcap, cudaStream_t st) {
+int bucket_threads() {
+  static int v = 0;
+  if (v == 0) {
+    const char* e = getenv("TNB_BUCKET_THREADS");
+    v = (e && atoi(e) == 512) ? 512 : 256;
+  }
+  return v;
+}
+
+template <int R, typename IdxT, int NT>
+int launch_nt(const ChainDev& ch, const int64_t* idx, int64_t m, float* out, int32_t* err,
+              int jcap, cudaStream_t st) {
   constexpr int RP = Geo<R>::RP;
-  // largest tile (multiple of 32, < 65536) that fits the smem budget
+  // 512/NT CTAs share an SM's 228 KB (1 KB reserved per CTA)
+  const size_t budget = (size_t)(233472 / (512 / NT)) - 1024;
   int T = 65504;
-  while (T > 32 && smem_bytes<IdxT>(T, RP, ch.n, jcap) > (size_t)kSmemLimit) T -= 32;
+  while (T > 32 && smem_bytes<IdxT>(T, RP, ch.n, jcap) > budget) T -= 32;
   const size_t smem = smem_bytes<IdxT>(T, RP, ch.n, jcap);
-  if (smem > (size_t)kSmemLimit) return set_error(TNB_EINVAL, "bucketed: chain too long for smem");
-  auto kern = entries_bucketed_kernel<R, IdxT>;
+  if (smem > budget) return set_error(TNB_EINVAL, "bucketed: chain too long for smem");
+  auto kern = entries_bucketed_kernel<R, IdxT, NT>;
   int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem),
                       "bucketed smem attr");
   if (rc) return rc;
   const int64_t ntiles = (m + T - 1) / T;
-  const int grid = (int)(ntiles < num_sms() ? ntiles : num_sms());
-  kern<<<grid, kThreads, smem, st>>>(ch, idx, m, out, err, T, jcap);
+  const int64_t slots = (int64_t)num_sms() * (512 / NT);
+  const int grid = (int)(ntiles < slots ? ntiles : slots);
+  kern<<<grid, NT, smem, st>>>(ch, idx, m, out, err, T, jcap);
   return check_launch("entries_bucketed");
+}
+
+template <int R, typename IdxT>
+int launch_t(const ChainDev& ch, const int64_t* idx, int64_t m, float* out, int32_t* err,
+             int jcap, cudaStream_t st) {
+  if (bucket_threads() == 512) return launch_nt<R, IdxT, 512>(ch, idx, m, out, err, jcap, st);
+  return launch_nt<R, IdxT, 256>(ch, idx, m, out, err, jcap, st);
 }
 
 }  // namespace

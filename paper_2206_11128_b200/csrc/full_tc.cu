@@ -5,20 +5,21 @@
 // hi = rna_tf32(x), lo = x - hi (exact), and C = Ahi*Bhi + Ahi*Blo + Alo*Bhi
 // accumulated in fp32 in TMEM (the dropped lo*lo term is ~2^-22 relative).
 //
-// Design (one persistent CTA per SM, 384 threads, no cluster):
+// Design (one persistent CTA per SM, 512 threads, no cluster):
 //   * B (= R^T block of BN=256 output columns, K <= 64) is RESIDENT in shared
 //     memory in the UMMA canonical K-major SWIZZLE_128B layout, hi and lo
 //     (128 KB); it is refilled only when the CTA's work moves to the next
 //     column block (cb-major tile order).
 //   * A (= 128 rows of L) never touches shared memory: loader warps (warps
-//     4-7, thread = row) read the rows from global/L2, split them into
-//     hi/lo in registers and tcgen05.st them into TMEM, where tcgen05.mma
+//     4-11; thread = row, two warps per TMEM lane quadrant, one K half each)
+//     read the rows from global/L2 one tile ahead, split them into hi/lo in
+//     registers and tcgen05.st them into TMEM, where tcgen05.mma
 //     takes its A operand (kind::tf32, A from TMEM, B from smem).  Two A
 //     buffers of 128 columns (hi 64 | lo 64).
 //   * MMA issuer (warp 0, one lane): per A tile, two 128x128 N-subtiles, each
 //     24 MMAs (8 k-steps x 3 products) into one of two 128-column TMEM
 //     accumulators; tcgen05.commit signals the epilogue and frees A.
-//   * epilogue warps (8-11, thread = row): tcgen05.ld 32 columns at a time,
+//   * epilogue warps (12-15, thread = row): tcgen05.ld 32 columns at a time,
 //     streaming st.global.cs.v4 stores.  The output write (HBM) is the roof;
 //     MMAs (~1.5k cycles per subtile) hide under it (~2.7k cycles at
 //     ~24 B/clk/SM).
@@ -28,7 +29,7 @@
 namespace tnb {
 namespace {
 
-constexpr int kThreads = 384;
+constexpr int kThreads = 512;
 constexpr int BM = 128;        // rows per A tile (UMMA M)
 constexpr int BN = 256;        // resident B columns
 constexpr int SUBN = 128;      // UMMA N
@@ -116,6 +117,14 @@ __device__ __forceinline__ uint32_t b_offset(int n, int k) {
       "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]),      \
       "r"(v[29]), "r"(v[30]), "r"(v[31]))
 
+#define TMEM_ST16(taddr, v)                                                                    \
+  asm volatile(                                                                                \
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, " \
+      "%11, %12, %13, %14, %15, %16};" ::"r"(taddr),                                          \
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),  \
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),         \
+      "r"(v[15]))
+
 #define TMEM_LD32(taddr, v)                                                                    \
   asm volatile(                                                                                \
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "   \
@@ -146,7 +155,7 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
   unsigned char* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   unsigned char* sB = smem;  // hi: [0, kBBytes/2), lo: [kBBytes/2, kBBytes)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBBytes);
-  uint64_t* a_full = bars + 0;     // [2] count 128 (loader threads)
+  uint64_t* a_full = bars + 0;     // [2] count 256 (loader threads)
   uint64_t* a_empty = bars + 2;    // [2] count 1 (tcgen05.commit)
   uint64_t* acc_full = bars + 4;   // [2] count 1 (tcgen05.commit)
   uint64_t* acc_empty = bars + 6;  // [2] count 128 (epilogue threads)
@@ -163,8 +172,8 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
   const int64_t t1 = (n_tiles * (blockIdx.x + 1)) / gridDim.x;
 
   if (tid == 0) {
-    mbar_init(&a_full[0], 128);
-    mbar_init(&a_full[1], 128);
+    mbar_init(&a_full[0], 256);
+    mbar_init(&a_full[1], 256);
     mbar_init(&a_empty[0], 1);
     mbar_init(&a_empty[1], 1);
     mbar_init(&acc_full[0], 1);
@@ -206,16 +215,45 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
         }
         named_sync(1, 128);
         // B block: rows n = output columns cb*BN .. +BN, k < K; R is [K][ldb]
+        // (n contiguous): 16-byte loads, 8 in flight per thread, each element
+        // split into hi/lo and stored at its swizzled K-major position
         const int64_t n0 = cb * BN;
-        for (int e = tid; e < BN * KMAX; e += 128) {
-          const int k = e / BN, n = e - (e / BN) * BN;  // consecutive threads: consecutive n
-          float x = 0.f;
-          if (k < K && n0 + n < N) x = __ldg(args.B + (int64_t)k * args.ldb + n0 + n);
-          const uint32_t hi = f2tf32(x);
-          const float lo = x - __uint_as_float(hi);
-          const uint32_t off = b_offset(n, k);
-          *reinterpret_cast<uint32_t*>(sB + off) = hi;
-          *reinterpret_cast<float*>(sB + kBBytes / 2 + off) = lo;
+        const bool bvec = ((args.ldb & 3) == 0) && ((reinterpret_cast<uintptr_t>(args.B) & 15) == 0) &&
+                          (n0 + BN <= N);
+        for (int e0 = tid; e0 < (BN / 4) * KMAX; e0 += 128 * 8) {
+          float4 xv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * 128;
+            const int k = e / (BN / 4), n4 = e - (e / (BN / 4)) * (BN / 4);
+            float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (e < (BN / 4) * KMAX && k < K) {
+              const float* src = args.B + (int64_t)k * args.ldb + n0 + n4 * 4;
+              if (bvec) {
+                x = __ldg(reinterpret_cast<const float4*>(src));
+              } else {
+                if (n0 + n4 * 4 + 0 < N) x.x = __ldg(src + 0);
+                if (n0 + n4 * 4 + 1 < N) x.y = __ldg(src + 1);
+                if (n0 + n4 * 4 + 2 < N) x.z = __ldg(src + 2);
+                if (n0 + n4 * 4 + 3 < N) x.w = __ldg(src + 3);
+              }
+            }
+            xv[u] = x;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * 128;
+            if (e >= (BN / 4) * KMAX) continue;
+            const int k = e / (BN / 4), n4 = e - (e / (BN / 4)) * (BN / 4);
+            const float xs[4] = {xv[u].x, xv[u].y, xv[u].z, xv[u].w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint32_t hi = f2tf32(xs[j]);
+              const uint32_t off = b_offset(n4 * 4 + j, k);
+              *reinterpret_cast<uint32_t*>(sB + off) = hi;
+              *reinterpret_cast<float*>(sB + kBBytes / 2 + off) = xs[j] - __uint_as_float(hi);
+            }
+          }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         named_sync(1, 128);
@@ -251,38 +289,50 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
         ++a_it;
       }
     }
-  } else if (warp < 8) {
-    // ================= WG1: A loaders (thread = row) =================
+  } else if (warp < 12) {
+    // ================= A loaders: thread = row, one K half per warp =========
     const int q = warp & 3;
+    const int kh = (warp - 4) >> 2;  // columns kh*32 .. kh*32+31
     const int r = q * 32 + lane;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    const bool vec = ((args.lda & 3) == 0) && ((reinterpret_cast<uintptr_t>(args.A) & 15) == 0);
+    auto load_row = [&](int64_t t, float4 (&x)[8]) {
+      const int64_t rb = t - (t / n_rb) * n_rb;
+      const int64_t row = rb * BM + r;
+      const float* src = args.A + row * args.lda + kh * 32;
+#pragma unroll
+      for (int c4 = 0; c4 < 8; ++c4) {
+        const int k = kh * 32 + c4 * 4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (t < t1 && row < M) {
+          if (vec && k + 3 < K) {
+            v = __ldg(reinterpret_cast<const float4*>(src + c4 * 4));
+          } else {
+            if (k + 0 < K) v.x = __ldg(src + c4 * 4 + 0);
+            if (k + 1 < K) v.y = __ldg(src + c4 * 4 + 1);
+            if (k + 2 < K) v.z = __ldg(src + c4 * 4 + 2);
+            if (k + 3 < K) v.w = __ldg(src + c4 * 4 + 3);
+          }
+        }
+        x[c4] = v;
+      }
+    };
+    float4 cur[8];
+    load_row(t0, cur);
     uint32_t a_it = 0;
     for (int64_t t = t0; t < t1; ++t) {
-      const int64_t rb = t - (t / n_rb) * n_rb;
+      float4 nxt[8];
+      load_row(t + 1, nxt);  // one tile ahead: the L2 latency overlaps this tile
       const int ab = a_it & 1;
       mbar_wait(&a_empty[ab], ((a_it >> 1) & 1) ^ 1);
       tc_fence_after();
-      const int64_t row = rb * BM + r;
-      const float* src = args.A + row * args.lda;
-      const bool vec = ((args.lda & 3) == 0) && ((reinterpret_cast<uintptr_t>(args.A) & 15) == 0);
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        uint32_t hi[32], lo[32];
+      for (int hh = 0; hh < 2; ++hh) {  // 16 columns at a time
+        uint32_t hi[16], lo[16];
 #pragma unroll
-        for (int c4 = 0; c4 < 8; ++c4) {
-          const int k = half * 32 + c4 * 4;
-          float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (row < M) {
-            if (vec && k + 3 < K) {
-              x = __ldg(reinterpret_cast<const float4*>(src + k));
-            } else {
-              if (k + 0 < K) x.x = __ldg(src + k + 0);
-              if (k + 1 < K) x.y = __ldg(src + k + 1);
-              if (k + 2 < K) x.z = __ldg(src + k + 2);
-              if (k + 3 < K) x.w = __ldg(src + k + 3);
-            }
-          }
-          const float xs[4] = {x.x, x.y, x.z, x.w};
+        for (int c4 = 0; c4 < 4; ++c4) {
+          const float4 v = cur[hh * 4 + c4];
+          const float xs[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const uint32_t h = f2tf32(xs[j]);
@@ -290,12 +340,15 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
             lo[c4 * 4 + j] = __float_as_uint(xs[j] - __uint_as_float(h));
           }
         }
-        TMEM_ST32(tm_a[ab] + lane_base + half * 32, hi);
-        TMEM_ST32(tm_a[ab] + lane_base + KMAX + half * 32, lo);
+        const uint32_t col = kh * 32 + hh * 16;
+        TMEM_ST16(tm_a[ab] + lane_base + col, hi);
+        TMEM_ST16(tm_a[ab] + lane_base + KMAX + col, lo);
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       mbar_arrive(&a_full[ab]);
+#pragma unroll
+      for (int c4 = 0; c4 < 8; ++c4) cur[c4] = nxt[c4];
       ++a_it;
     }
   } else {
@@ -313,26 +366,31 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
         tc_fence_after();
         const int64_t col0 = cb * BN + sub * SUBN;
         float* dst = args.C + row * args.ldc + col0;
-#pragma unroll 1
+        // chunk ch+1's TMEM load is in flight while chunk ch is stored
+        uint32_t va[32], vb[32];
+        TMEM_LD32(tm_acc[cbuf] + lane_base, va);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
         for (int ch = 0; ch < SUBN / 32; ++ch) {
-          uint32_t v[32];
-          TMEM_LD32(tm_acc[cbuf] + lane_base + ch * 32, v);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          uint32_t* cur = (ch & 1) ? vb : va;
+          uint32_t* nxt = (ch & 1) ? va : vb;
+          if (ch + 1 < SUBN / 32) TMEM_LD32(tm_acc[cbuf] + lane_base + (ch + 1) * 32, nxt);
           if (row < M) {
             const int64_t c0 = col0 + ch * 32;
             if (vec && c0 + 32 <= N) {
 #pragma unroll
               for (int j = 0; j < 8; ++j)
                 asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + ch * 32 + j * 4),
-                             "f"(__uint_as_float(v[4 * j])), "f"(__uint_as_float(v[4 * j + 1])),
-                             "f"(__uint_as_float(v[4 * j + 2])), "f"(__uint_as_float(v[4 * j + 3]))
+                             "f"(__uint_as_float(cur[4 * j])), "f"(__uint_as_float(cur[4 * j + 1])),
+                             "f"(__uint_as_float(cur[4 * j + 2])), "f"(__uint_as_float(cur[4 * j + 3]))
                              : "memory");
             } else {
 #pragma unroll
               for (int j = 0; j < 32; ++j)
-                if (c0 + j < N) dst[ch * 32 + j] = __uint_as_float(v[j]);
+                if (c0 + j < N) dst[ch * 32 + j] = __uint_as_float(cur[j]);
             }
           }
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         }
         tc_fence_before();
         mbar_arrive(&acc_empty[cbuf]);
