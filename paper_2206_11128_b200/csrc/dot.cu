@@ -9,6 +9,9 @@
 #include "common.cuh"
 
 namespace tnb {
+bool dot_fast_supported(const ChainDev& a, const ChainDev& b);
+int launch_dot_fast(const ChainDev& a, const ChainDev& b, float* out, bool is_norm, cudaStream_t st);
+
 namespace {
 
 __global__ void __launch_bounds__(256) dot_kernel(const __grid_constant__ ChainDev A,
@@ -82,6 +85,9 @@ int launch_dot(const tnb_chain* a, const tnb_chain* b, float* out, bool is_norm,
       return set_error(TNB_EINVAL, "shape mismatch on mode %d: %d vs %d", k, a->modes[k].phys,
                        b->modes[k].phys);
   if (a->batch != b->batch) return set_error(TNB_EINVAL, "operands must agree on batching");
+  const char* gen = getenv("TNB_DOT_GENERIC");
+  if (!(gen && gen[0] == '1') && dot_fast_supported(ca, cb))
+    return launch_dot_fast(ca, cb, out, is_norm, st);
   int cap = 1;
   for (int k = 0; k < a->n_modes; ++k) {
     const int ral = a->modes[k].r_left, rar = a->modes[k].r_right;

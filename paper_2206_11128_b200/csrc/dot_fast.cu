@@ -1,0 +1,308 @@
+// K3 performance kernel: batched chain inner products / norms for TT chains
+// of rank 16 (BASELINE config 4: 4096 pairs, N=16, I=64, r=16).
+//
+// Reference: chain_dot (core.py:362-384) propagates an r_a x r_b transfer
+// matrix M mode by mode, M' = sum_j A_j^T M B_j, as numpy's einsum path
+// "xaic,xab->bcix" then "bcix,xbid->xcd".  Here:
+//   * one CTA per pair at a time (persistent, 2 CTAs per SM, 8 warps);
+//   * core slices stream HBM -> shared memory with cp.async.bulk (TMA bulk
+//     copies) in chunks of 16 slices (16 KB per operand), double buffered
+//     behind an mbarrier full/empty pipeline -- each byte is read once;
+//   * warp w takes slices j = w, w+8 of every chunk:
+//       Y_j = M B_j   (lane = 2 rows x 4 columns; M rows in registers)
+//       Mw += A_j^T Y_j  (Y_j bounced through a 1 KB per-warp smem tile)
+//     with packed FFMA2 (fma.rn.f32x2) throughout;
+//   * at the end of each core the 8 per-warp partial M's are summed through
+//     shared memory and the new M is broadcast back into registers.
+// The boundary cores (rank 1 outward) use the same pipeline with rank-1
+// special cases.  norm() streams only one operand (A == B).
+#include "common.cuh"
+
+namespace tnb {
+namespace {
+
+constexpr int kWarps = 8;
+constexpr int kThreads = kWarps * 32;
+constexpr int R = 16;
+constexpr int CH = 16;                 // slices per chunk
+constexpr int kStages = 2;
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void ffma2(uint64_t& acc, uint64_t a, float s) {
+  asm("{\n\t.reg .b64 ss;\n\tmov.b64 ss, {%2, %2};\n\tfma.rn.f32x2 %0, %1, ss, %0;\n\t}"
+      : "+l"(acc)
+      : "l"(a), "f"(s));
+}
+__device__ __forceinline__ void unpack2(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t lds64(uint32_t a) {
+  uint64_t v;
+  asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void lds128x2(uint32_t a, uint64_t& p0, uint64_t& p1) {
+  asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(p0), "=l"(p1) : "r"(a));
+}
+__device__ __forceinline__ void sts128x2(uint32_t a, uint64_t p0, uint64_t p1) {
+  asm volatile("st.shared.v2.b64 [%0], {%1, %2};" ::"r"(a), "l"(p0), "l"(p1) : "memory");
+}
+
+struct DotArgs {
+  ChainDev a, b;  // a.m[k].s + e * bstride = slices of pair e
+  float* out;
+  int norm;
+};
+
+// chunk bookkeeping: the CTA walks (pair, core, chunk) in order
+struct Walk {
+  int64_t e;
+  int k, c;
+};
+
+__global__ void __launch_bounds__(kThreads, 2) dot_r16_kernel(const __grid_constant__ DotArgs args) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* stA = reinterpret_cast<float*>(smem);                      // [kStages][CH*R*R]
+  float* stB = stA + kStages * CH * R * R;                          // [kStages][CH*R*R]
+  float* ybuf = stB + (args.norm ? 0 : kStages * CH * R * R);       // [kWarps][R*R]
+  float* red = ybuf + kWarps * R * R;                               // [kWarps][R*R]
+  float* msm = red + kWarps * R * R;                                // [R*R]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(msm + R * R);        // full[kStages], empty[kStages]
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kStages;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ap = lane >> 2, dq = lane & 3;  // rows/cols 2ap,2ap+1 ; 4dq..4dq+3
+  const int N = args.a.n, J = args.a.m[0].J;
+  const int nch = (J + CH - 1) / CH;
+  const int64_t B = args.a.batch;
+  const bool same = args.norm != 0;
+
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  // producer state (thread 0): next chunk to load
+  Walk pw{(int64_t)blockIdx.x, 0, 0};
+  uint32_t p_it = 0;
+  auto produce_one = [&]() {
+    if (pw.e >= B) return;
+    const int s = p_it % kStages;
+    mbar_wait(&empty[s], ((p_it / kStages) & 1) ^ 1);
+    const ModeDev& ma = args.a.m[pw.k];
+    const ModeDev& mb = args.b.m[pw.k];
+    const int j0 = pw.c * CH, nj = min(CH, J - j0);
+    const uint32_t sz = (uint32_t)(nj * ma.rl * ma.rr * 4);
+    mbar_expect_tx(&full[s], same ? sz : 2 * sz);
+    bulk_g2s(stA + s * CH * R * R, ma.s + pw.e * ma.bstride + (int64_t)j0 * ma.rl * ma.rr, sz, &full[s]);
+    if (!same)
+      bulk_g2s(stB + s * CH * R * R, mb.s + pw.e * mb.bstride + (int64_t)j0 * mb.rl * mb.rr, sz,
+               &full[s]);
+    ++p_it;
+    if (++pw.c == nch) {
+      pw.c = 0;
+      if (++pw.k == N) {
+        pw.k = 0;
+        pw.e += gridDim.x;
+      }
+    }
+  };
+  if (tid == 0)
+    for (int s = 0; s < kStages; ++s) produce_one();
+
+  uint32_t c_it = 0;
+  for (int64_t e = blockIdx.x; e < B; e += gridDim.x) {
+    float mrow[2][R];  // M rows 2ap, 2ap+1 (registers)
+    for (int k = 0; k < N; ++k) {
+      const bool first = (k == 0), last = (k == N - 1);
+      uint64_t mn[2][2] = {{0ull, 0ull}, {0ull, 0ull}};
+      float lastacc = 0.f;
+      float4 mq0 = make_float4(0.f, 0.f, 0.f, 0.f), mq1 = mq0;  // M[2ap(+1)][4dq..]
+      if (last && !first) {
+        mq0 = *reinterpret_cast<const float4*>(msm + (2 * ap) * R + dq * 4);
+        mq1 = *reinterpret_cast<const float4*>(msm + (2 * ap + 1) * R + dq * 4);
+      }
+      for (int c = 0; c < nch; ++c) {
+        const int s = c_it % kStages;
+        mbar_wait(&full[s], (c_it / kStages) & 1);
+        const float* A = stA + s * CH * R * R;
+        const float* Bm = same ? A : stB + s * CH * R * R;
+        const int nj = min(CH, J - c * CH);
+        for (int jj = warp; jj < nj; jj += kWarps) {
+          if (first) {  // 1 x R slices: M' += A_j^T B_j
+            const uint32_t a_row = su32(A + jj * R), b_row = su32(Bm + jj * R);
+            uint64_t b0, b1;
+            lds128x2(b_row + dq * 16, b0, b1);
+            float a0, a1;
+            unpack2(lds64(a_row + ap * 8), a0, a1);
+            ffma2(mn[0][0], b0, a0);
+            ffma2(mn[0][1], b1, a0);
+            ffma2(mn[1][0], b0, a1);
+            ffma2(mn[1][1], b1, a1);
+          } else if (last) {  // R x 1 slices: s += a_j . (M b_j)
+            const float* aj = A + jj * R;
+            const float* bj = Bm + jj * R;
+            const float4 bv = *reinterpret_cast<const float4*>(bj + dq * 4);
+            const float a0 = aj[2 * ap], a1 = aj[2 * ap + 1];
+            float y0 = 0.f, y1 = 0.f;
+            y0 = fmaf(mq0.x, bv.x, y0);
+            y0 = fmaf(mq0.y, bv.y, y0);
+            y0 = fmaf(mq0.z, bv.z, y0);
+            y0 = fmaf(mq0.w, bv.w, y0);
+            y1 = fmaf(mq1.x, bv.x, y1);
+            y1 = fmaf(mq1.y, bv.y, y1);
+            y1 = fmaf(mq1.z, bv.z, y1);
+            y1 = fmaf(mq1.w, bv.w, y1);
+            lastacc = fmaf(a0, y0, lastacc);
+            lastacc = fmaf(a1, y1, lastacc);
+          } else {
+            // Y = M B_j : rows 2ap, 2ap+1, columns 4dq..4dq+3
+            const uint32_t bj = su32(Bm + jj * R * R);
+            uint64_t y[2][2] = {{0ull, 0ull}, {0ull, 0ull}};
+#pragma unroll
+            for (int b = 0; b < R; ++b) {
+              uint64_t p0, p1;
+              lds128x2(bj + b * 64 + dq * 16, p0, p1);
+              ffma2(y[0][0], p0, mrow[0][b]);
+              ffma2(y[0][1], p1, mrow[0][b]);
+              ffma2(y[1][0], p0, mrow[1][b]);
+              ffma2(y[1][1], p1, mrow[1][b]);
+            }
+            const uint32_t yw = su32(ybuf + warp * R * R);
+            sts128x2(yw + (2 * ap) * 64 + dq * 16, y[0][0], y[0][1]);
+            sts128x2(yw + (2 * ap + 1) * 64 + dq * 16, y[1][0], y[1][1]);
+            __syncwarp();
+            // Mw += A_j^T Y : rows c = 2ap, 2ap+1
+            const uint32_t aj = su32(A + jj * R * R);
+#pragma unroll
+            for (int a = 0; a < R; ++a) {
+              uint64_t q0, q1;
+              lds128x2(yw + a * 64 + dq * 16, q0, q1);
+              float a0, a1;
+              unpack2(lds64(aj + a * 64 + ap * 8), a0, a1);
+              ffma2(mn[0][0], q0, a0);
+              ffma2(mn[0][1], q1, a0);
+              ffma2(mn[1][0], q0, a1);
+              ffma2(mn[1][1], q1, a1);
+            }
+            __syncwarp();
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        ++c_it;
+        if (tid == 0) produce_one();
+      }
+      // ---- reduce the per-warp partial M over warps ----
+      if (last) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) lastacc += __shfl_xor_sync(0xffffffffu, lastacc, o);
+        if (lane == 0) red[warp] = lastacc;
+        __syncthreads();
+        if (tid == 0) {
+          float v = 0.f;
+          for (int w = 0; w < kWarps; ++w) v += red[w];
+          args.out[e] = args.norm ? sqrtf(fmaxf(v, 0.f)) : v;
+        }
+        __syncthreads();
+      } else {
+        float* rw = red + warp * R * R;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          float x0, x1, x2, x3;
+          unpack2(mn[i][0], x0, x1);
+          unpack2(mn[i][1], x2, x3);
+          *reinterpret_cast<float4*>(rw + (2 * ap + i) * R + dq * 4) = make_float4(x0, x1, x2, x3);
+        }
+        __syncthreads();
+        {
+          float v = 0.f;
+#pragma unroll
+          for (int w = 0; w < kWarps; ++w) v += red[w * R * R + tid];
+          msm[tid] = v;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int b = 0; b < R; ++b) mrow[i][b] = msm[(2 * ap + i) * R + b];
+        __syncthreads();
+      }
+    }
+  }
+}
+
+size_t dot_smem(bool norm) {
+  const size_t stage = (size_t)kStages * CH * R * R * 4;
+  return stage * (norm ? 1 : 2) + (size_t)(2 * kWarps * R * R + R * R) * 4 + 2 * kStages * 8 + 16;
+}
+
+bool chain_ok(const ChainDev& c) {
+  if (c.n < 2) return false;
+  const int J = c.m[0].J;
+  if (J < 1) return false;
+  for (int k = 0; k < c.n; ++k) {
+    const ModeDev& m = c.m[k];
+    if (m.layout != TNB_LAYOUT_DENSE || m.J != J) return false;
+    const int rl = (k == 0) ? 1 : R, rr = (k == c.n - 1) ? 1 : R;
+    if (m.rl != rl || m.rr != rr) return false;
+    // bulk copies need 16-byte aligned sources
+    if ((reinterpret_cast<uintptr_t>(m.s) & 15) || ((m.bstride * 4) & 15)) return false;
+  }
+  return true;
+}
+
+}  // namespace
+
+bool dot_fast_supported(const ChainDev& a, const ChainDev& b) {
+  return chain_ok(a) && chain_ok(b) && a.n == b.n && a.batch == b.batch;
+}
+
+int launch_dot_fast(const ChainDev& a, const ChainDev& b, float* out, bool is_norm, cudaStream_t st) {
+  DotArgs args;
+  args.a = a;
+  args.b = b;
+  args.out = out;
+  args.norm = is_norm ? 1 : 0;
+  const size_t smem = dot_smem(is_norm);
+  int rc = check_cuda(cudaFuncSetAttribute(dot_r16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem),
+                      "dot smem attr");
+  if (rc) return rc;
+  const int64_t slots = (int64_t)num_sms() * 2;
+  const int grid = (int)(a.batch < slots ? a.batch : slots);
+  dot_r16_kernel<<<grid, kThreads, smem, st>>>(args);
+  return check_launch("dot_r16");
+}
+
+}  // namespace tnb

@@ -19,8 +19,9 @@
 //   * MMA issuer (warp 0, one lane): per A tile, two 128x128 N-subtiles, each
 //     24 MMAs (8 k-steps x 3 products) into one of two 128-column TMEM
 //     accumulators; tcgen05.commit signals the epilogue and frees A.
-//   * epilogue warps (12-15, thread = row): tcgen05.ld 32 columns at a time,
-//     streaming st.global.cs.v4 stores.  The output write (HBM) is the roof;
+//   * epilogue warps (12-15): tcgen05.ld 32 columns at a time (thread = row),
+//     transposed through a per-warp smem tile so every st.global.cs.v4
+//     writes whole 128-byte lines.  The output write (HBM) is the roof;
 //     MMAs (~1.5k cycles per subtile) hide under it (~2.7k cycles at
 //     ~24 B/clk/SM).
 // TMEM: 512 columns = acc0 | acc1 | A0 | A1.
@@ -352,21 +353,23 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
       ++a_it;
     }
   } else {
-    // ================= WG2: epilogue (thread = row) =================
+    // ================= WG2: epilogue =================
+    // TMEM rows -> registers (thread = row) -> per-warp smem transpose ->
+    // coalesced stores: each st.global.v4 writes 4 rows x 128 B full lines.
     const int q = warp & 3;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     const bool vec = ((args.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(args.C) & 15) == 0);
+    float* tp = reinterpret_cast<float*>(smem + kBBytes + 1024) + q * (32 * 36);  // [32][36]
+    const uint32_t tp_s = smem_u32(tp);
     uint32_t s_it = 0;
     for (int64_t t = t0; t < t1; ++t) {
       const int64_t cb = t / n_rb, rb = t - cb * n_rb;
-      const int64_t row = rb * BM + q * 32 + lane;
+      const int64_t row0 = rb * BM + q * 32;  // this warp's 32 rows
       for (int sub = 0; sub < BN / SUBN; ++sub) {
         const int cbuf = s_it & 1;
         mbar_wait(&acc_full[cbuf], (s_it >> 1) & 1);
         tc_fence_after();
         const int64_t col0 = cb * BN + sub * SUBN;
-        float* dst = args.C + row * args.ldc + col0;
-        // chunk ch+1's TMEM load is in flight while chunk ch is stored
         uint32_t va[32], vb[32];
         TMEM_LD32(tm_acc[cbuf] + lane_base, va);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -375,21 +378,37 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
           uint32_t* cur = (ch & 1) ? vb : va;
           uint32_t* nxt = (ch & 1) ? va : vb;
           if (ch + 1 < SUBN / 32) TMEM_LD32(tm_acc[cbuf] + lane_base + (ch + 1) * 32, nxt);
-          if (row < M) {
-            const int64_t c0 = col0 + ch * 32;
-            if (vec && c0 + 32 <= N) {
+          // my row (lane) -> smem row
 #pragma unroll
-              for (int j = 0; j < 8; ++j)
-                asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + ch * 32 + j * 4),
-                             "f"(__uint_as_float(cur[4 * j])), "f"(__uint_as_float(cur[4 * j + 1])),
-                             "f"(__uint_as_float(cur[4 * j + 2])), "f"(__uint_as_float(cur[4 * j + 3]))
+          for (int j = 0; j < 8; ++j)
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(tp_s + (lane * 36 + j * 4) * 4),
+                         "r"(cur[4 * j]), "r"(cur[4 * j + 1]), "r"(cur[4 * j + 2]), "r"(cur[4 * j + 3])
+                         : "memory");
+          __syncwarp();
+          const int64_t c0 = col0 + ch * 32;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int rr = i * 4 + (lane >> 3), cq = (lane & 7) * 4;
+            const int64_t grow = row0 + rr;
+            float4 v;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                         : "r"(tp_s + (rr * 36 + cq) * 4));
+            if (grow < M) {
+              float* dst = args.C + grow * args.ldc + c0 + cq;
+              if (vec && c0 + cq + 4 <= N) {
+                asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(v.x), "f"(v.y),
+                             "f"(v.z), "f"(v.w)
                              : "memory");
-            } else {
+              } else {
+                const float vs[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (c0 + j < N) dst[ch * 32 + j] = __uint_as_float(cur[j]);
+                for (int u = 0; u < 4; ++u)
+                  if (c0 + cq + u < N) dst[u] = vs[u];
+              }
             }
           }
+          __syncwarp();
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         }
         tc_fence_before();
@@ -406,7 +425,7 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
   }
 }
 
-constexpr size_t kSmemBytes = 1024 + kBBytes + 16 * 8 + 64;
+constexpr size_t kSmemBytes = 1024 + kBBytes + 1024 + 4 * 32 * 36 * 4;
 
 bool tc_disabled() {
   static int v = -1;
