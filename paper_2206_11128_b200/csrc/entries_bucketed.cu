@@ -450,7 +450,7 @@ int bucket_threads() {
   static int v = 0;
   if (v == 0) {
     const char* e = getenv("TNB_BUCKET_THREADS");
-    v = (e && atoi(e) == 512) ? 512 : 256;
+    v = (e && atoi(e) == 256) ? 256 : 512;
   }
   return v;
 }

@@ -237,3 +237,20 @@ def test_bucketed_rank_classes(r, J):
     o = O.make_chain([("tt", c) for c in cores])
     idx = O.uniform_indices(t.shape, 20000, 1)
     assert_close(tb.entries(t, idx, algo=N.ALGO_BUCKETED), O.entries(o, idx), what=f"r={r} J={J}")
+
+
+@pytest.mark.parametrize("generic", ["0", "1"])
+def test_dot_rank16_fast_and_generic(generic, monkeypatch):
+    # the rank-16 streaming kernel (dot_fast.cu) and the generic one agree
+    # with the oracle; J=20 exercises a partial slice chunk
+    monkeypatch.setenv("TNB_DOT_GENERIC", generic)
+    a = O.random_tt((20,) * 5, 16, seed=3, batch_size=7, scale=0.25)
+    b = O.random_tt((20,) * 5, 16, seed=4, batch_size=7, scale=0.25)
+    ta, oa = facade([("tt", c, None) for c in a], 7), O.make_chain([("tt", c) for c in a], 7)
+    tb_, ob = facade([("tt", c, None) for c in b], 7), O.make_chain([("tt", c) for c in b], 7)
+    assert_close(tb.dot(ta, tb_), O.chain_dot(oa, ob), what="dot")
+    assert_close(tb.norm(ta), O.norm(oa), what="norm")
+    # unbatched rank-16 chains take the same kernel with one CTA
+    a1 = O.random_tt((16,) * 3, 16, seed=5, scale=0.25)
+    t1, o1 = facade([("tt", c, None) for c in a1]), O.make_chain([("tt", c) for c in a1])
+    assert abs(tb.norm(t1) - O.norm(o1)) <= 1e-5 * O.norm(o1)
