@@ -365,7 +365,8 @@ int launch_full(const tnb_chain* c, int64_t lo, int64_t hi, float* out, void* ws
   // ---- out = L @ R ----
   const int K = c->modes[p].r_left;
   if (K == 0) return check_cuda(cudaMemsetAsync(out, 0, P.out_per * B * sizeof(float), st), "memset");
-  if (tc_gemm_supported(rows, cols, K, K, cols, cols))
+  if (tc_gemm_supported(rows, cols, K, K, cols, cols) && (reinterpret_cast<uintptr_t>(L) & 15) == 0 &&
+      ((L_bs * 4) & 15) == 0)
     return launch_tc_gemm(L, K, L_bs, R, cols, P.r_buf, out, cols, P.out_per, rows, cols, K, B, st);
   return launch_sgemm(L, K, L_bs, R, cols, P.r_buf, out, cols, P.out_per, rows, cols, K, B, st);
 }
