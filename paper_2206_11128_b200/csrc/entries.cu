@@ -16,8 +16,9 @@
 
 namespace tnb {
 int launch_entries_bucketed(const ChainDev& ch, const int64_t* idx, int64_t m, float* out,
-                            int32_t* err, cudaStream_t st);
+                            int32_t* err, void* ws, int64_t ws_bytes, cudaStream_t st);
 bool bucketed_supported(const ChainDev& ch);
+int64_t bucketed_workspace(const ChainDev& ch, int64_t m);
 
 namespace {
 
@@ -128,9 +129,19 @@ int chain_rmax(const tnb_chain* c) {
 
 }  // namespace
 
+bool use_bucketed(const ChainDev& ch, int64_t m, int algo) {
+  if (algo == TNB_ALGO_BUCKETED) return true;
+  return algo == TNB_ALGO_AUTO && m >= (1 << 16) && bucketed_supported(ch);
+}
+
 int64_t entries_workspace(const tnb_chain* c, int64_t m, int algo) {
   if (!c || !c->modes || c->n_modes < 1 || m < 0) return -1;
   const int rmax = chain_rmax(c);
+  if (c->n_modes <= kMaxModes && (algo == TNB_ALGO_AUTO || algo == TNB_ALGO_BUCKETED)) {
+    static thread_local ChainDev ch;
+    if (make_chain_dev(c, &ch, true) == TNB_OK && use_bucketed(ch, m, algo))
+      return bucketed_supported(ch) ? bucketed_workspace(ch, m) : 0;
+  }
   if (pick_algo(c, algo, rmax) != TNB_ALGO_LAYERED) return 0;
   const int64_t B = c->batch > 0 ? c->batch : 1;
   return 2 * m * B * (int64_t)rmax * (int64_t)sizeof(float);
@@ -148,8 +159,8 @@ int launch_entries(const tnb_chain* c, const int64_t* idx, int64_t m, float* out
   rc = check_cuda(cudaMemsetAsync(err, 0x7f, sizeof(int32_t), st), "memset err");
   if (rc || m == 0) return rc;
   const int64_t B = ch.batch;
-  if (algo == TNB_ALGO_AUTO && m >= (1 << 16) && bucketed_supported(ch))
-    return launch_entries_bucketed(ch, idx, m, out, err, st);
+  if (algo == TNB_ALGO_AUTO && use_bucketed(ch, m, algo))
+    return launch_entries_bucketed(ch, idx, m, out, err, ws, ws_bytes, st);
   if (use == TNB_ALGO_CHAIN) {
     const int64_t total = m * B;
     const int g = grid_for(total, 256);
@@ -166,7 +177,7 @@ int launch_entries(const tnb_chain* c, const int64_t* idx, int64_t m, float* out
   if (use == TNB_ALGO_BUCKETED) {
     if (!bucketed_supported(ch))
       return set_error(TNB_EINVAL, "bucketed algorithm does not support this chain");
-    return launch_entries_bucketed(ch, idx, m, out, err, st);
+    return launch_entries_bucketed(ch, idx, m, out, err, ws, ws_bytes, st);
   }
   if (use != TNB_ALGO_LAYERED) return set_error(TNB_EINVAL, "unknown entries algorithm %d", algo);
   const int64_t need = 2 * m * B * (int64_t)ch.rmax * (int64_t)sizeof(float);

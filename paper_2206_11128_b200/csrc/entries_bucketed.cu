@@ -109,14 +109,18 @@ __device__ __forceinline__ void ks_passes(const uint64_t (&g2)[16], const uint16
   for (int pi = 0; pi < NP; ++pi) acc2[pi] = 0ull;
 #pragma unroll
   for (int a4 = 0; a4 < 4; ++a4) {
+    float4 v[NP];
 #pragma unroll
-    for (int pi = 0; pi < NP; ++pi) {
-      const float4 v = lds128(rowb[pi] + h * 64 + a4 * 16);
-      ffma2(acc2[pi], g2[a4 * 4 + 0], v.x);
-      ffma2(acc2[pi], g2[a4 * 4 + 1], v.y);
-      ffma2(acc2[pi], g2[a4 * 4 + 2], v.z);
-      ffma2(acc2[pi], g2[a4 * 4 + 3], v.w);
-    }
+    for (int pi = 0; pi < NP; ++pi) v[pi] = lds128(rowb[pi] + h * 64 + a4 * 16);
+    // consecutive FFMA2s hit different accumulators (no back-to-back RAW)
+#pragma unroll
+    for (int pi = 0; pi < NP; ++pi) ffma2(acc2[pi], g2[a4 * 4 + 0], v[pi].x);
+#pragma unroll
+    for (int pi = 0; pi < NP; ++pi) ffma2(acc2[pi], g2[a4 * 4 + 1], v[pi].y);
+#pragma unroll
+    for (int pi = 0; pi < NP; ++pi) ffma2(acc2[pi], g2[a4 * 4 + 2], v[pi].z);
+#pragma unroll
+    for (int pi = 0; pi < NP; ++pi) ffma2(acc2[pi], g2[a4 * 4 + 3], v[pi].w);
   }
 #pragma unroll
   for (int pi = 0; pi < NP; ++pi) acc2[pi] = add2(acc2[pi], __shfl_xor_sync(0xffffffffu, acc2[pi], 16));
@@ -127,98 +131,244 @@ __device__ __forceinline__ void ks_passes(const uint64_t (&g2)[16], const uint16
   __syncwarp();
 }
 
+// ---------------------------------------------------------------------------
+// Two kernels per call:
+//   prep    (one CTA per tile): index validation/compaction and the counting
+//           sort of every interior dense mode, written to a per-tile
+//           workspace record [cidx | perm[slot] | starts[slot]];
+//   compute (persistent): streams each tile's record into shared memory with
+//           cp.async.bulk (the next tile's rows/slots are prefetched as soon
+//           as the current tile stops needing them) and runs the modes; one
+//           CTA barrier per mode, no sorting on the critical path.
+
+struct BPlan {
+  int T;           // samples per tile
+  int nsort;       // interior dense modes (sorted)
+  int jpad;        // bucket-start row length (>= max J + 1, multiple of 8)
+  int idx_bytes;   // sizeof(IdxT)
+  int64_t ntiles;
+  int64_t tile_bytes;
+  int64_t off_perm, off_starts;
+  int8_t slot[kMaxModes];  // mode -> sorted slot or -1
+};
+
 template <typename IdxT>
-__host__ __device__ inline size_t smem_bytes(int T, int RP, int N, int jcap) {
-  size_t b = (size_t)(T + 1) * RP * sizeof(float);  // state (+ dummy row)
-  b += (size_t)T * 2 * sizeof(uint16_t);          // perm + rank
-  b += (size_t)N * T * sizeof(IdxT);              // compact indices
-  b = (b + 15) & ~(size_t)15;
-  b += (size_t)2 * (jcap + 1) * sizeof(int);      // counts + starts
-  return b;
+__global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant__ ChainDev ch,
+                                                           const __grid_constant__ BPlan bp,
+                                                           const int64_t* __restrict__ idx, int64_t m,
+                                                           int32_t* __restrict__ err,
+                                                           unsigned char* __restrict__ ws) {
+  constexpr int NT = 512;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int N = ch.n, T = bp.T;
+  IdxT* idxs = reinterpret_cast<IdxT*>(smem);                               // [N][T]
+  uint16_t* perm = reinterpret_cast<uint16_t*>(smem + (size_t)N * T * sizeof(IdxT));
+  uint16_t* rnk = perm + T;
+  int* cnt = reinterpret_cast<int*>(rnk + T);                                // [jpad]
+  int* start = cnt + bp.jpad;                                                // [jpad]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int64_t tile = blockIdx.x;
+  const int64_t s0 = tile * T;
+  const int tn = (int)((m - s0) < T ? (m - s0) : T);
+  unsigned char* rec = ws + tile * bp.tile_bytes;
+
+  // ---- indices: coalesced int64 read (4 in flight), wrap/validate, compact
+  {
+    const int64_t* src = idx + s0 * N;
+    const int total = tn * N;
+    constexpr int U = 4;
+    int ss[U], kk[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = tid + u * NT;
+      ss[u] = e / N;
+      kk[u] = e - ss[u] * N;
+    }
+    const int ds = (U * NT) / N, dk = (U * NT) - ds * N;
+    for (int e0 = tid; e0 < total; e0 += U * NT) {
+      int64_t raw[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = e0 + u * NT;
+        raw[u] = (e < total) ? ld_stream_i64(src + e) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (e0 + u * NT < total) {
+          const int k = kk[u];
+          idxs[(size_t)k * T + ss[u]] = (IdxT)norm_index(raw[u], ch.m[k].J, k, err);
+        }
+        ss[u] += ds;
+        kk[u] += dk;
+        if (kk[u] >= N) {
+          kk[u] -= N;
+          ++ss[u];
+        }
+      }
+    }
+    // tail rows of the last tile: index 0 keeps every later read in bounds
+    for (int e = tid; e < (T - tn) * N; e += NT) {
+      const int k = e / (T - tn), s = tn + (e - k * (T - tn));
+      idxs[(size_t)k * T + s] = (IdxT)0;
+    }
+  }
+  __syncthreads();
+  {  // compact block -> record (16-byte stores)
+    const int n16 = (int)(((size_t)N * T * sizeof(IdxT)) / 16);
+    for (int i = tid; i < n16; i += NT)
+      reinterpret_cast<uint4*>(rec)[i] = reinterpret_cast<const uint4*>(idxs)[i];
+  }
+  // ---- counting sort of every interior dense mode ----
+  for (int k = 1; k < N - 1; ++k) {
+    const int sl = bp.slot[k];
+    if (sl < 0) continue;
+    const IdxT* col = idxs + (size_t)k * T;
+    const int J = ch.m[k].J;
+    const int kbits = 32 - __clz(J > 1 ? J - 1 : 1);
+    for (int j = tid; j <= J; j += NT) cnt[j] = 0;
+    __syncthreads();
+    const int tn32 = (tn + 31) & ~31;
+    for (int s = tid; s < tn32; s += NT) {
+      const bool act = s < tn;
+      const unsigned amask = __ballot_sync(0xffffffffu, act);
+      if (act) {
+        const int key = col[s];
+        unsigned peers = amask;  // lanes holding the same key
+        for (int b = 0; b < kbits; ++b) {
+          const bool bit = (key >> b) & 1;
+          const unsigned bal = __ballot_sync(amask, bit);
+          peers &= bit ? bal : ~bal;
+        }
+        const int leader = __ffs(peers) - 1;
+        int base = 0;
+        if (lane == leader) base = atomicAdd(&cnt[key], __popc(peers));
+        base = __shfl_sync(peers, base, leader);
+        rnk[s] = (uint16_t)(base + __popc(peers & lt_mask));
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {  // exclusive scan cnt[0..J) -> start[0..J]
+      const int per = (J + 31) / 32;
+      const int lo = lane * per;
+      int sum = 0;
+      for (int j = lo; j < lo + per && j < J; ++j) sum += cnt[j];
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int run = incl - sum;
+      for (int j = lo; j < lo + per && j < J; ++j) {
+        start[j] = run;
+        run += cnt[j];
+      }
+      if (lane == 31) start[J] = incl;
+    }
+    __syncthreads();
+    for (int s = tid; s < tn; s += NT) perm[start[col[s]] + rnk[s]] = (uint16_t)s;
+    uint16_t* gst = reinterpret_cast<uint16_t*>(rec + bp.off_starts) + (size_t)sl * bp.jpad;
+    for (int j = tid; j < bp.jpad; j += NT) gst[j] = (uint16_t)(j <= J ? start[j] : tn);
+    __syncthreads();
+    uint4* gp = reinterpret_cast<uint4*>(rec + bp.off_perm + (size_t)sl * T * 2);
+    for (int i = tid; i < T * 2 / 16; i += NT) gp[i] = reinterpret_cast<const uint4*>(perm)[i];
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ uint32_t s32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mb_init(uint64_t* b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s32(b)), "r"(c));
+}
+__device__ __forceinline__ void mb_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(s32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          s32(dst)),
+      "l"(src), "r"(bytes), "r"(s32(bar))
+      : "memory");
 }
 
 template <int R, typename IdxT, int NT>
 __global__ void __launch_bounds__(NT, 512 / NT)
-    entries_bucketed_kernel(const __grid_constant__ ChainDev ch, const int64_t* __restrict__ idx,
-                            int64_t m, float* __restrict__ out, int32_t* __restrict__ err, int T,
-                            int jcap) {
+    entries_compute_kernel(const __grid_constant__ ChainDev ch, const __grid_constant__ BPlan bp,
+                           const unsigned char* __restrict__ ws, int64_t m, float* __restrict__ out) {
   using Gm = Geo<R>;
   constexpr int C = Gm::C, L = Gm::L, G = Gm::G, P = Gm::P, RP = Gm::RP;
   extern __shared__ __align__(16) unsigned char smem[];
-  const int N = ch.n;
-  float* state = reinterpret_cast<float*>(smem);
-  uint16_t* perm = reinterpret_cast<uint16_t*>(state + (size_t)(T + 1) * RP);
-  uint16_t* rnk = perm + T;
-  IdxT* idxs = reinterpret_cast<IdxT*>(rnk + T);
-  size_t off = (size_t)(T + 1) * RP * 4 + (size_t)T * 4 + (size_t)N * T * sizeof(IdxT);
-  off = (off + 15) & ~(size_t)15;
-  int* cnt = reinterpret_cast<int*>(smem + off);
-  int* start = cnt + jcap + 1;
+  const int N = ch.n, T = bp.T;
+  float* state = reinterpret_cast<float*>(smem);                                   // [T+1][RP]
+  IdxT* cidx = reinterpret_cast<IdxT*>(state + (size_t)(T + 1) * RP);              // [N][T]
+  uint16_t* permb = reinterpret_cast<uint16_t*>(cidx + (size_t)N * T);             // [2][T]
+  uint16_t* startb = permb + 2 * T;                                                // [2][jpad]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(
+      (reinterpret_cast<uintptr_t>(startb + 2 * bp.jpad) + 15) & ~(uintptr_t)15);  // cbar, pbar[2]
+  uint64_t* cbar = bars;
+  uint64_t* pbar = bars + 1;
 
-  const uint32_t s_state = (uint32_t)__cvta_generic_to_shared(state);
+  const uint32_t s_state = s32(state);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int nwarps = NT / 32;
-  const int gi = lane / L;   // sample group within the warp
-  const int q = lane % L;    // lane within the group -> columns q*C .. q*C+C-1
-  const unsigned lt_mask = (1u << lane) - 1u;
-  const int64_t ntiles = (m + T - 1) / T;
+  const int gi = lane / L;
+  const int q = lane % L;
+  const int64_t ntiles = bp.ntiles;
+  const uint32_t row_bytes = (uint32_t)T * sizeof(IdxT);
+  const uint32_t slot_bytes = (uint32_t)T * 2 + (uint32_t)bp.jpad * 2;
+  const int ns = bp.nsort;
 
+  // producer (tid 0): slot items in consumption order (tile-major, slot-minor)
+  auto issue_slot = [&](int64_t item) {
+    if (ns == 0) return;
+    const int64_t ti = item / ns;
+    const int sl = (int)(item - ti * ns);
+    const int64_t tile = blockIdx.x + ti * gridDim.x;
+    if (tile >= ntiles) return;
+    const int b = (int)(item & 1);
+    const unsigned char* rec = ws + tile * bp.tile_bytes;
+    mb_expect(&pbar[b], slot_bytes);
+    bulk(permb + b * T, rec + bp.off_perm + (size_t)sl * T * 2, (uint32_t)T * 2, &pbar[b]);
+    bulk(startb + b * bp.jpad, rec + bp.off_starts + (size_t)sl * bp.jpad * 2, (uint32_t)bp.jpad * 2,
+         &pbar[b]);
+  };
+  if (tid == 0) {
+    mb_init(cbar, 1);
+    mb_init(&pbar[0], 1);
+    mb_init(&pbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (blockIdx.x < ntiles) {
+      const unsigned char* rec = ws + (int64_t)blockIdx.x * bp.tile_bytes;
+      mb_expect(cbar, row_bytes * N);
+      for (int k = 0; k < N; ++k) bulk(cidx + (size_t)k * T, rec + (size_t)k * row_bytes, row_bytes, cbar);
+      issue_slot(0);
+      issue_slot(1);
+    }
+  }
+  __syncthreads();
+
+  uint32_t c_it = 0;
+  int64_t item = 0;  // slot items consumed
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t s0 = tile * T;
     const int tn = (int)((m - s0) < T ? (m - s0) : T);
-    {  // warm L2 with the next tile's index block
-      const int64_t nt = tile + gridDim.x;
-      if (nt < ntiles) {
-        const int64_t ns0 = nt * T;
-        const int64_t nbytes = ((m - ns0) < T ? (m - ns0) : T) * N * 8;
-        const char* base = reinterpret_cast<const char*>(idx + ns0 * N);
-        for (int64_t o = (int64_t)tid * 128; o < nbytes; o += (int64_t)NT * 128)
-          prefetch_l2(base + o);
-      }
-    }
-    // ---- indices: coalesced int64 read (4 loads in flight per thread),
-    //      wrap/validate, compact, mode-major
-    {
-      const int64_t* src = idx + s0 * N;
-      const int total = tn * N;
-      constexpr int U = 4;
-      int ss[U], kk[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int e = tid + u * NT;
-        ss[u] = e / N;
-        kk[u] = e - ss[u] * N;
-      }
-      const int ds = (U * NT) / N, dk = (U * NT) - ds * N;
-      for (int e0 = tid; e0 < total; e0 += U * NT) {
-        int64_t raw[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int e = e0 + u * NT;
-          raw[u] = (e < total) ? ld_stream_i64(src + e) : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (e0 + u * NT < total) {
-            const int k = kk[u];
-            const int j = norm_index(raw[u], ch.m[k].J, k, err);
-            idxs[(size_t)k * T + ss[u]] = (IdxT)j;
-          }
-          ss[u] += ds;
-          kk[u] += dk;
-          if (kk[u] >= N) {
-            kk[u] -= N;
-            ++ss[u];
-          }
-        }
-      }
-    }
-    __syncthreads();
-
+    const int64_t ntile = tile + gridDim.x;
+    mb_wait(cbar, c_it & 1);
+    ++c_it;
     for (int k = 0; k < N; ++k) {
       const ModeDev& md = ch.m[k];
-      const IdxT* col = idxs + (size_t)k * T;
+      const IdxT* col = cidx + (size_t)k * T;
       const int rl = md.rl, rr = md.rr;
+      bool sorted = false;
       if (k == 0) {
         if (N == 1) {  // [J][1][1]
           for (int s = tid; s < tn; s += NT) out[s0 + s] = __ldg(md.s + col[s]);
@@ -228,7 +378,7 @@ __global__ void __launch_bounds__(NT, 512 / NT)
             const float4 g = __ldg(reinterpret_cast<const float4*>(md.s + (int64_t)col[s] * R) + c4);
             *reinterpret_cast<float4*>(state + s * RP + c4 * 4) = g;
           }
-        } else {       // state row = G_0[j][0][:], zero padded to R
+        } else {  // zero padded to R
           for (int e = tid; e < tn * R; e += NT) {
             const int s = e / R, c = e - (e / R) * R;
             state[s * RP + c] = (c < rr) ? __ldg(md.s + (int64_t)col[s] * rr + c) : 0.f;
@@ -240,7 +390,7 @@ __global__ void __launch_bounds__(NT, 512 / NT)
           if (c < rl) state[s * RP + c] *= __ldg(md.s + (int64_t)col[s] * rl + c);
         }
       } else if (k == N - 1) {  // rr == 1: out = state . G[j][:, 0]
-        if (rl == R) {  // full rank: unpredicated 16-byte loads, two FMA chains
+        if (rl == R) {
           for (int s = tid; s < tn; s += NT) {
             const float4* g4 = reinterpret_cast<const float4*>(md.s + (int64_t)col[s] * R);
             const uint32_t vrow = s_state + (uint32_t)s * (RP * 4);
@@ -270,61 +420,18 @@ __global__ void __launch_bounds__(NT, 512 / NT)
           }
         }
       } else {
-        // ---- counting sort of the tile by this mode's index ----
-        const int J = md.J;
-        const int kbits = 32 - __clz(J > 1 ? J - 1 : 1);
-        for (int j = tid; j <= J; j += NT) cnt[j] = 0;
-        __syncthreads();
-        const int tn32 = (tn + 31) & ~31;
-        for (int s = tid; s < tn32; s += NT) {
-          const bool act = s < tn;
-          const unsigned amask = __ballot_sync(0xffffffffu, act);
-          if (act) {
-            const int key = col[s];
-            // lanes holding the same key: AND of per-bit ballots (cheaper
-            // than MATCH.ANY for the <= 10-bit keys of sorted modes)
-            unsigned peers = amask;
-            for (int b = 0; b < kbits; ++b) {
-              const bool bit = (key >> b) & 1;
-              const unsigned bal = __ballot_sync(amask, bit);
-              peers &= bit ? bal : ~bal;
-            }
-            const int leader = __ffs(peers) - 1;
-            int base = 0;
-            if (lane == leader) base = atomicAdd(&cnt[key], __popc(peers));
-            base = __shfl_sync(peers, base, leader);
-            rnk[s] = (uint16_t)(base + __popc(peers & lt_mask));
-          }
-        }
-        __syncthreads();
-        if (warp == 0) {  // exclusive scan of cnt[0..J) -> start
-          const int per = (J + 31) / 32;
-          const int lo = lane * per;
-          int sum = 0;
-          for (int j = lo; j < lo + per && j < J; ++j) sum += cnt[j];
-          int incl = sum;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-          }
-          int run = incl - sum;
-          for (int j = lo; j < lo + per && j < J; ++j) {
-            start[j] = run;
-            run += cnt[j];
-          }
-        }
-        __syncthreads();
-        for (int s = tid; s < tn; s += NT) perm[start[col[s]] + rnk[s]] = (uint16_t)s;
-        __syncthreads();
-
-        // ---- warp ranges of sorted positions; core slice in registers ----
+        // ---- sorted mode: permutation + bucket starts from the prep kernel
+        sorted = true;
+        const int b = (int)(item & 1);
+        mb_wait(&pbar[b], (uint32_t)((item >> 1) & 1));
+        const uint16_t* perm = permb + b * T;
+        const uint16_t* st = startb + b * bp.jpad;
         const int lo = (int)(((int64_t)warp * tn) / nwarps);
         const int hi = (int)(((int64_t)(warp + 1) * tn) / nwarps);
         int p = lo;
         while (p < hi) {
           const int key = col[perm[p]];
-          const int bend = min(start[key] + cnt[key], hi);
+          const int bend = min((int)st[key + 1], hi);
           if constexpr (R == 32) {
             // K-split geometry: lane (h, qq) owns rows 16h..16h+15 and the
             // column pair (2qq, 2qq+1); one sample per pass, the two row
@@ -407,19 +514,23 @@ __global__ void __launch_bounds__(NT, 512 / NT)
                 float4 v[P];
   #pragma unroll
                 for (int pi = 0; pi < P; ++pi) v[pi] = lds128(row[pi] + a4 * 16);
-  #pragma unroll
+              #pragma unroll
+              for (int pi = 0; pi < P; ++pi) ffma2(acc2[pi], g2[a4 * 4 + 0], v[pi].x);
+              #pragma unroll
+              for (int pi = 0; pi < P; ++pi) ffma2(acc2[pi], g2[a4 * 4 + 1], v[pi].y);
+              #pragma unroll
+              for (int pi = 0; pi < P; ++pi) ffma2(acc2[pi], g2[a4 * 4 + 2], v[pi].z);
+              #pragma unroll
+              for (int pi = 0; pi < P; ++pi) ffma2(acc2[pi], g2[a4 * 4 + 3], v[pi].w);
+              if constexpr (C1) {
+              #pragma unroll
                 for (int pi = 0; pi < P; ++pi) {
-                  ffma2(acc2[pi], g2[a4 * 4 + 0], v[pi].x);
-                  ffma2(acc2[pi], g2[a4 * 4 + 1], v[pi].y);
-                  ffma2(acc2[pi], g2[a4 * 4 + 2], v[pi].z);
-                  ffma2(acc2[pi], g2[a4 * 4 + 3], v[pi].w);
-                  if constexpr (C1) {
-                    acc1[pi] = fmaf(v[pi].x, g1[a4 * 4 + 0], acc1[pi]);
-                    acc1[pi] = fmaf(v[pi].y, g1[a4 * 4 + 1], acc1[pi]);
-                    acc1[pi] = fmaf(v[pi].z, g1[a4 * 4 + 2], acc1[pi]);
-                    acc1[pi] = fmaf(v[pi].w, g1[a4 * 4 + 3], acc1[pi]);
-                  }
+                  acc1[pi] = fmaf(v[pi].x, g1[a4 * 4 + 0], acc1[pi]);
+                  acc1[pi] = fmaf(v[pi].y, g1[a4 * 4 + 1], acc1[pi]);
+                  acc1[pi] = fmaf(v[pi].z, g1[a4 * 4 + 2], acc1[pi]);
+                  acc1[pi] = fmaf(v[pi].w, g1[a4 * 4 + 3], acc1[pi]);
                 }
+              }
               }
               __syncwarp();  // every lane of a group has read its sample's row
   #pragma unroll
@@ -434,6 +545,15 @@ __global__ void __launch_bounds__(NT, 512 / NT)
         }
       }
       __syncthreads();
+      if (tid == 0) {
+        // cidx row k of this tile is dead: prefetch the next tile's row k
+        if (ntile < ntiles) {
+          if (k == 0) mb_expect(cbar, row_bytes * N);
+          bulk(cidx + (size_t)k * T, ws + ntile * bp.tile_bytes + (size_t)k * row_bytes, row_bytes, cbar);
+        }
+        if (sorted) issue_slot(item + 2);  // this slot buffer is free again
+      }
+      if (sorted) ++item;
     }
   }
 }
@@ -455,33 +575,77 @@ int bucket_threads() {
   return v;
 }
 
-template <int R, typename IdxT, int NT>
-int launch_nt(const ChainDev& ch, const int64_t* idx, int64_t m, float* out, int32_t* err,
-              int jcap, cudaStream_t st) {
-  constexpr int RP = Geo<R>::RP;
-  // 512/NT CTAs share an SM's 228 KB (1 KB reserved per CTA)
+size_t compute_smem(int T, int RP, int N, int idx_bytes, int jpad) {
+  size_t b = (size_t)(T + 1) * RP * 4 + (size_t)N * T * idx_bytes + (size_t)2 * T * 2 + (size_t)2 * jpad * 2;
+  return ((b + 15) & ~(size_t)15) + 3 * 8;
+}
+
+// Shared by the workspace query and the launcher so both agree on T.
+int make_bplan(const ChainDev& ch, int64_t m, BPlan* bp, int* R_out, int* nt_out) {
+  const int R = pick_R(ch.rmax);
+  if (!R) return set_error(TNB_EINVAL, "bucketed: rank > 32");
+  int jmax = 1, nsort = 0;
+  bool small = true;
+  for (int k = 0; k < ch.n; ++k) {
+    if (ch.m[k].J > 256) small = false;
+    const bool srt = k > 0 && k < ch.n - 1 && ch.m[k].layout == TNB_LAYOUT_DENSE;
+    bp->slot[k] = srt ? (int8_t)nsort : (int8_t)-1;
+    if (srt) {
+      ++nsort;
+      jmax = ch.m[k].J > jmax ? ch.m[k].J : jmax;
+    }
+  }
+  const int NT = bucket_threads();
+  const int RP = R + 4;
+  const int idx_bytes = small ? 1 : 2;
+  const int jpad = ((jmax + 1) + 7) & ~7;
   const size_t budget = (size_t)(233472 / (512 / NT)) - 1024;
   int T = 65504;
-  while (T > 32 && smem_bytes<IdxT>(T, RP, ch.n, jcap) > budget) T -= 32;
-  const size_t smem = smem_bytes<IdxT>(T, RP, ch.n, jcap);
-  if (smem > budget) return set_error(TNB_EINVAL, "bucketed: chain too long for smem");
-  auto kern = entries_bucketed_kernel<R, IdxT, NT>;
-  int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem),
-                      "bucketed smem attr");
+  while (T > 32 && compute_smem(T, RP, ch.n, idx_bytes, jpad) > budget) T -= 32;
+  if (compute_smem(T, RP, ch.n, idx_bytes, jpad) > budget)
+    return set_error(TNB_EINVAL, "bucketed: chain too long for smem");
+  bp->T = T;
+  bp->nsort = nsort;
+  bp->jpad = jpad;
+  bp->idx_bytes = idx_bytes;
+  bp->ntiles = (m + T - 1) / T;
+  const int64_t cidx_b = (((int64_t)ch.n * T * idx_bytes) + 15) & ~(int64_t)15;
+  bp->off_perm = cidx_b;
+  bp->off_starts = cidx_b + (int64_t)nsort * T * 2;
+  bp->tile_bytes = (bp->off_starts + (int64_t)nsort * jpad * 2 + 127) & ~(int64_t)127;
+  *R_out = R;
+  *nt_out = NT;
+  return TNB_OK;
+}
+
+template <int R, typename IdxT, int NT>
+int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m, float* out,
+              int32_t* err, unsigned char* ws, cudaStream_t st) {
+  // prep: one CTA per tile
+  const size_t psmem = (size_t)ch.n * bp.T * sizeof(IdxT) + (size_t)bp.T * 4 + (size_t)2 * bp.jpad * 4;
+  auto pk = entries_prep_kernel<IdxT>;
+  int rc = check_cuda(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem),
+                      "prep smem attr");
   if (rc) return rc;
-  const int64_t ntiles = (m + T - 1) / T;
+  pk<<<(unsigned)bp.ntiles, 512, psmem, st>>>(ch, bp, idx, m, err, ws);
+  rc = check_launch("entries_prep");
+  if (rc) return rc;
+  const size_t csmem = compute_smem(bp.T, R + 4, ch.n, (int)sizeof(IdxT), bp.jpad);
+  auto ck = entries_compute_kernel<R, IdxT, NT>;
+  rc = check_cuda(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem),
+                  "compute smem attr");
+  if (rc) return rc;
   const int64_t slots = (int64_t)num_sms() * (512 / NT);
-  const int grid = (int)(ntiles < slots ? ntiles : slots);
-  kern<<<grid, NT, smem, st>>>(ch, idx, m, out, err, T, jcap);
-  return check_launch("entries_bucketed");
+  const int grid = (int)(bp.ntiles < slots ? bp.ntiles : slots);
+  ck<<<grid, NT, csmem, st>>>(ch, bp, ws, m, out);
+  return check_launch("entries_compute");
 }
 
 template <int R, typename IdxT>
-int launch_t(const ChainDev& ch, const int64_t* idx, int64_t m, float* out, int32_t* err,
-             int jcap, cudaStream_t st) {
-  if (bucket_threads() == 512) return launch_nt<R, IdxT, 512>(ch, idx, m, out, err, jcap, st);
-  return launch_nt<R, IdxT, 256>(ch, idx, m, out, err, jcap, st);
+int launch_ri(const ChainDev& ch, const BPlan& bp, int nt, const int64_t* idx, int64_t m, float* out,
+              int32_t* err, unsigned char* ws, cudaStream_t st) {
+  if (nt == 256) return launch_rt<R, IdxT, 256>(ch, bp, idx, m, out, err, ws, st);
+  return launch_rt<R, IdxT, 512>(ch, bp, idx, m, out, err, ws, st);
 }
 
 }  // namespace
@@ -498,31 +662,38 @@ bool bucketed_supported(const ChainDev& ch) {
   return true;
 }
 
+int64_t bucketed_workspace(const ChainDev& ch, int64_t m) {
+  BPlan bp;
+  int R, nt;
+  if (m <= 0 || !bucketed_supported(ch) || make_bplan(ch, m, &bp, &R, &nt)) return 0;
+  return bp.ntiles * bp.tile_bytes;
+}
+
 int launch_entries_bucketed(const ChainDev& ch, const int64_t* idx, int64_t m, float* out,
-                            int32_t* err, cudaStream_t st) {
-  int jmax = 1;
-  bool small = true;
-  for (int k = 0; k < ch.n; ++k) {
-    if (ch.m[k].J > 256) small = false;
-    if (k > 0 && k < ch.n - 1 && ch.m[k].layout == TNB_LAYOUT_DENSE && ch.m[k].J > jmax)
-      jmax = ch.m[k].J;
-  }
-  const int jcap = jmax;
-  switch (pick_R(ch.rmax)) {
+                            int32_t* err, void* ws, int64_t ws_bytes, cudaStream_t st) {
+  BPlan bp;
+  int R, nt;
+  int rc = make_bplan(ch, m, &bp, &R, &nt);
+  if (rc) return rc;
+  if (!ws || ws_bytes < bp.ntiles * bp.tile_bytes)
+    return set_error(TNB_EWORKSPACE, "bucketed entries needs %lld workspace bytes, got %lld",
+                     (long long)(bp.ntiles * bp.tile_bytes), (long long)ws_bytes);
+  unsigned char* w = static_cast<unsigned char*>(ws);
+  const bool small = bp.idx_bytes == 1;
+  switch (R) {
     case 8:
-      return small ? launch_t<8, uint8_t>(ch, idx, m, out, err, jcap, st)
-                   : launch_t<8, uint16_t>(ch, idx, m, out, err, jcap, st);
+      return small ? launch_ri<8, uint8_t>(ch, bp, nt, idx, m, out, err, w, st)
+                   : launch_ri<8, uint16_t>(ch, bp, nt, idx, m, out, err, w, st);
     case 16:
-      return small ? launch_t<16, uint8_t>(ch, idx, m, out, err, jcap, st)
-                   : launch_t<16, uint16_t>(ch, idx, m, out, err, jcap, st);
+      return small ? launch_ri<16, uint8_t>(ch, bp, nt, idx, m, out, err, w, st)
+                   : launch_ri<16, uint16_t>(ch, bp, nt, idx, m, out, err, w, st);
     case 24:
-      return small ? launch_t<24, uint8_t>(ch, idx, m, out, err, jcap, st)
-                   : launch_t<24, uint16_t>(ch, idx, m, out, err, jcap, st);
-    case 32:
-      return small ? launch_t<32, uint8_t>(ch, idx, m, out, err, jcap, st)
-                   : launch_t<32, uint16_t>(ch, idx, m, out, err, jcap, st);
+      return small ? launch_ri<24, uint8_t>(ch, bp, nt, idx, m, out, err, w, st)
+                   : launch_ri<24, uint16_t>(ch, bp, nt, idx, m, out, err, w, st);
+    default:
+      return small ? launch_ri<32, uint8_t>(ch, bp, nt, idx, m, out, err, w, st)
+                   : launch_ri<32, uint16_t>(ch, bp, nt, idx, m, out, err, w, st);
   }
-  return set_error(TNB_EINVAL, "bucketed: rank > 32");
 }
 
 }  // namespace tnb

@@ -10,9 +10,9 @@
 //     memory in the UMMA canonical K-major SWIZZLE_128B layout, hi and lo
 //     (128 KB); it is refilled only when the CTA's work moves to the next
 //     column block (cb-major tile order).
-//   * A (= 128 rows of L): one lane streams the raw fp32 rows into a 2-deep
-//     smem ring with cp.async.bulk; loader warps (4-11; thread = row, two
-//     warps per TMEM lane quadrant, one K half each) split them into hi/lo in
+//   * A (= 128 rows of L) never touches shared memory: loader warps (warps
+//     4-11; thread = row, two warps per TMEM lane quadrant, one K half each)
+//     read the rows from global/L2 one tile ahead, split them into hi/lo in
 //     registers and tcgen05.st them into TMEM, where tcgen05.mma
 //     takes its A operand (kind::tf32, A from TMEM, B from smem).  Two A
 //     buffers of 128 columns (hi 64 | lo 64).
@@ -37,9 +37,6 @@ constexpr int SUBN = 128;      // UMMA N
 constexpr int KMAX = 64;       // max contraction length
 constexpr int kBBytes = 2 * 2 * BN * 128;  // {hi,lo} x 2 K-blocks x 256 rows x 128 B
 constexpr uint32_t kTmemCols = 512;
-constexpr int kRowPitch = KMAX * 4 + 16;    // raw A row in smem (+16 B: conflict-free row reads)
-constexpr int kAStage = BM * kRowPitch;     // one raw A tile
-constexpr int kTpBytes = 4 * 32 * 36 * 4;   // epilogue transpose tiles
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -58,17 +55,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
       "@!P1 bra WAIT_%=;\n\t}" ::"r"(a),
       "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() {
@@ -176,9 +162,6 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
   uint64_t* acc_empty = bars + 6;  // [2] count 128 (epilogue threads)
   uint64_t* mma_idle = bars + 8;   // count 1
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
-  uint64_t* st_full = bars + 12;   // [2] raw A stage landed (count 1 + tx bytes)
-  uint64_t* st_empty = bars + 14;  // [2] raw A stage read (count 8 loader warps)
-  unsigned char* sA = smem + kBBytes + 1024 + kTpBytes;  // [2][BM][kRowPitch]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t M = args.M, N = args.N;
@@ -199,10 +182,6 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
     mbar_init(&acc_empty[0], 128);
     mbar_init(&acc_empty[1], 128);
     mbar_init(mma_idle, 1);
-    mbar_init(&st_full[0], 1);
-    mbar_init(&st_full[1], 1);
-    mbar_init(&st_empty[0], 8);
-    mbar_init(&st_empty[1], 8);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -225,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
     const uint32_t sB_hi = smem_u32(sB), sB_lo = sB_hi + kBBytes / 2;
     int64_t cur_cb = -1;
     uint32_t idle_phase = 0;
-    uint32_t a_it = 0, s_it = 0, p_it = 0;
+    uint32_t a_it = 0, s_it = 0;
     for (int64_t t = t0; t < t1; ++t) {
       const int64_t cb = t / n_rb;
       if (cb != cur_cb) {
@@ -281,19 +260,6 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
         named_sync(1, 128);
         cur_cb = cb;
       }
-      if (warp == 1 && lane == 0) {
-        // raw A rows of this tile -> smem stage (cp.async.bulk, 2 tiles deep)
-        const int s = p_it & 1;
-        mbar_wait(&st_empty[s], ((p_it >> 1) & 1) ^ 1);
-        const int64_t rb = t - cb * n_rb;
-        const int64_t r0 = rb * BM;
-        const int nv = (int)((M - r0) < BM ? (M - r0) : BM);
-        const uint32_t rowb = (uint32_t)K * 4;
-        mbar_expect_tx(&st_full[s], (uint32_t)nv * rowb);
-        for (int r = 0; r < nv; ++r)
-          bulk_g2s(sA + s * kAStage + r * kRowPitch, args.A + (r0 + r) * args.lda, rowb, &st_full[s]);
-        ++p_it;
-      }
       if (warp == 0) {
         const int ab = a_it & 1;
         mbar_wait(&a_full[ab], (a_it >> 1) & 1);
@@ -330,30 +296,34 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
     const int kh = (warp - 4) >> 2;  // columns kh*32 .. kh*32+31
     const int r = q * 32 + lane;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-    uint32_t a_it = 0;
-    for (int64_t t = t0; t < t1; ++t) {
+    const bool vec = ((args.lda & 3) == 0) && ((reinterpret_cast<uintptr_t>(args.A) & 15) == 0);
+    auto load_row = [&](int64_t t, float4 (&x)[8]) {
       const int64_t rb = t - (t / n_rb) * n_rb;
-      const bool live = rb * BM + r < M;
-      const int sst = a_it & 1;
-      mbar_wait(&st_full[sst], (a_it >> 1) & 1);
-      float4 cur[8];
-      const uint32_t src = smem_u32(sA + sst * kAStage + r * kRowPitch) + kh * 128;
+      const int64_t row = rb * BM + r;
+      const float* src = args.A + row * args.lda + kh * 32;
 #pragma unroll
       for (int c4 = 0; c4 < 8; ++c4) {
+        const int k = kh * 32 + c4 * 4;
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (live)
-          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                       : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                       : "r"(src + c4 * 16));
-        const int k = kh * 32 + c4 * 4;  // columns >= K hold stale bytes
-        if (k + 0 >= K) v.x = 0.f;
-        if (k + 1 >= K) v.y = 0.f;
-        if (k + 2 >= K) v.z = 0.f;
-        if (k + 3 >= K) v.w = 0.f;
-        cur[c4] = v;
+        if (t < t1 && row < M) {
+          if (vec && k + 3 < K) {
+            v = __ldg(reinterpret_cast<const float4*>(src + c4 * 4));
+          } else {
+            if (k + 0 < K) v.x = __ldg(src + c4 * 4 + 0);
+            if (k + 1 < K) v.y = __ldg(src + c4 * 4 + 1);
+            if (k + 2 < K) v.z = __ldg(src + c4 * 4 + 2);
+            if (k + 3 < K) v.w = __ldg(src + c4 * 4 + 3);
+          }
+        }
+        x[c4] = v;
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&st_empty[sst]);
+    };
+    float4 cur[8];
+    load_row(t0, cur);
+    uint32_t a_it = 0;
+    for (int64_t t = t0; t < t1; ++t) {
+      float4 nxt[8];
+      load_row(t + 1, nxt);  // one tile ahead: the L2 latency overlaps this tile
       const int ab = a_it & 1;
       mbar_wait(&a_empty[ab], ((a_it >> 1) & 1) ^ 1);
       tc_fence_after();
@@ -378,6 +348,8 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       mbar_arrive(&a_full[ab]);
+#pragma unroll
+      for (int c4 = 0; c4 < 8; ++c4) cur[c4] = nxt[c4];
       ++a_it;
     }
   } else {
@@ -453,7 +425,7 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
   }
 }
 
-constexpr size_t kSmemBytes = 1024 + kBBytes + 1024 + kTpBytes + 2 * kAStage;
+constexpr size_t kSmemBytes = 1024 + kBBytes + 1024 + 4 * 32 * 36 * 4;
 
 bool tc_disabled() {
   static int v = -1;
@@ -468,11 +440,10 @@ bool tc_disabled() {
 
 bool tc_gemm_supported(int64_t M, int64_t N, int K, int64_t lda, int64_t ldb, int64_t ldc) {
   if (tc_disabled()) return false;
+  (void)lda;
   (void)ldb;
   (void)ldc;
-  // raw A rows travel by cp.async.bulk: 16-byte multiples and alignment
-  return K >= 4 && K <= KMAX && (K % 4) == 0 && (lda % 4) == 0 && M >= BM && N >= SUBN &&
-         M * N >= (1LL << 20);
+  return K >= 1 && K <= KMAX && M >= BM && N >= SUBN && M * N >= (1LL << 20);
 }
 
 int launch_tc_gemm(const float* A, int64_t lda, int64_t sA, const float* B, int64_t ldb,
