@@ -158,14 +158,15 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
                                                            const int64_t* __restrict__ idx, int64_t m,
                                                            int32_t* __restrict__ err,
                                                            unsigned char* __restrict__ ws) {
-  constexpr int NT = 512;
+  constexpr int NT = 512, NW = NT / 32;
   extern __shared__ __align__(16) unsigned char smem[];
-  const int N = ch.n, T = bp.T;
-  IdxT* idxs = reinterpret_cast<IdxT*>(smem);                               // [N][T]
-  uint16_t* perm = reinterpret_cast<uint16_t*>(smem + (size_t)N * T * sizeof(IdxT));
-  uint16_t* rnk = perm + T;
-  int* cnt = reinterpret_cast<int*>(rnk + T);                                // [jpad]
-  int* start = cnt + bp.jpad;                                                // [jpad]
+  const int N = ch.n, T = bp.T, NS = bp.nsort, JP = bp.jpad;
+  IdxT* idxs = reinterpret_cast<IdxT*>(smem);                                          // [N][T]
+  uint16_t* perm = reinterpret_cast<uint16_t*>(smem + (size_t)N * T * sizeof(IdxT));  // [NS][T]
+  uint16_t* rnk = perm + (size_t)NS * T;                                               // [NS][T]
+  int* cnt = reinterpret_cast<int*>(rnk + (size_t)NS * T);                             // [NS][JP]
+  int* start = cnt + (size_t)NS * JP;                                                  // [NS][JP]
+  int8_t* smode = reinterpret_cast<int8_t*>(start + (size_t)NS * JP);                  // slot -> mode
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
   const int64_t tile = blockIdx.x;
@@ -173,6 +174,8 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
   const int tn = (int)((m - s0) < T ? (m - s0) : T);
   unsigned char* rec = ws + tile * bp.tile_bytes;
 
+  for (int i = tid; i < NS * JP; i += NT) cnt[i] = 0;
+  if (tid < N && bp.slot[tid] >= 0) smode[bp.slot[tid]] = (int8_t)tid;
   // ---- indices: coalesced int64 read (4 in flight), wrap/validate, compact
   {
     const int64_t* src = idx + s0 * N;
@@ -209,8 +212,8 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
     }
     // tail rows of the last tile: index 0 keeps every later read in bounds
     for (int e = tid; e < (T - tn) * N; e += NT) {
-      const int k = e / (T - tn), s = tn + (e - k * (T - tn));
-      idxs[(size_t)k * T + s] = (IdxT)0;
+      const int k = e / (T - tn), sx = tn + (e - k * (T - tn));
+      idxs[(size_t)k * T + sx] = (IdxT)0;
     }
   }
   __syncthreads();
@@ -219,61 +222,68 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
     for (int i = tid; i < n16; i += NT)
       reinterpret_cast<uint4*>(rec)[i] = reinterpret_cast<const uint4*>(idxs)[i];
   }
-  // ---- counting sort of every interior dense mode ----
-  for (int k = 1; k < N - 1; ++k) {
-    const int sl = bp.slot[k];
-    if (sl < 0) continue;
-    const IdxT* col = idxs + (size_t)k * T;
+  // ---- counting sort of every interior dense mode, all slots at once ----
+  // ranks: one warp-chunk of 32 samples of one slot per iteration
+  const int chunks = (tn + 31) >> 5;
+  for (int w = warp; w < NS * chunks; w += NW) {
+    const int sl = w / chunks, s = (w - sl * chunks) * 32 + lane;
+    const int k = smode[sl];
     const int J = ch.m[k].J;
     const int kbits = 32 - __clz(J > 1 ? J - 1 : 1);
-    for (int j = tid; j <= J; j += NT) cnt[j] = 0;
-    __syncthreads();
-    const int tn32 = (tn + 31) & ~31;
-    for (int s = tid; s < tn32; s += NT) {
-      const bool act = s < tn;
-      const unsigned amask = __ballot_sync(0xffffffffu, act);
-      if (act) {
-        const int key = col[s];
-        unsigned peers = amask;  // lanes holding the same key
-        for (int b = 0; b < kbits; ++b) {
-          const bool bit = (key >> b) & 1;
-          const unsigned bal = __ballot_sync(amask, bit);
-          peers &= bit ? bal : ~bal;
-        }
-        const int leader = __ffs(peers) - 1;
-        int base = 0;
-        if (lane == leader) base = atomicAdd(&cnt[key], __popc(peers));
-        base = __shfl_sync(peers, base, leader);
-        rnk[s] = (uint16_t)(base + __popc(peers & lt_mask));
+    const bool act = s < tn;
+    const unsigned amask = __ballot_sync(0xffffffffu, act);
+    if (act) {
+      const int key = idxs[(size_t)k * T + s];
+      unsigned peers = amask;  // lanes holding the same key
+      for (int b = 0; b < kbits; ++b) {
+        const bool bit = (key >> b) & 1;
+        const unsigned bal = __ballot_sync(amask, bit);
+        peers &= bit ? bal : ~bal;
       }
+      const int leader = __ffs(peers) - 1;
+      int base = 0;
+      if (lane == leader) base = atomicAdd(&cnt[sl * JP + key], __popc(peers));
+      base = __shfl_sync(peers, base, leader);
+      rnk[(size_t)sl * T + s] = (uint16_t)(base + __popc(peers & lt_mask));
     }
-    __syncthreads();
-    if (warp == 0) {  // exclusive scan cnt[0..J) -> start[0..J]
-      const int per = (J + 31) / 32;
-      const int lo = lane * per;
-      int sum = 0;
-      for (int j = lo; j < lo + per && j < J; ++j) sum += cnt[j];
-      int incl = sum;
+  }
+  __syncthreads();
+  for (int sl = warp; sl < NS; sl += NW) {  // exclusive scan per slot (one warp each)
+    const int J = ch.m[smode[sl]].J;
+    const int per = (J + 31) / 32;
+    const int lo = lane * per;
+    const int* c = cnt + sl * JP;
+    int* st = start + sl * JP;
+    int sum = 0;
+    for (int j = lo; j < lo + per && j < J; ++j) sum += c[j];
+    int incl = sum;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      int run = incl - sum;
-      for (int j = lo; j < lo + per && j < J; ++j) {
-        start[j] = run;
-        run += cnt[j];
-      }
-      if (lane == 31) start[J] = incl;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
     }
-    __syncthreads();
-    for (int s = tid; s < tn; s += NT) perm[start[col[s]] + rnk[s]] = (uint16_t)s;
-    uint16_t* gst = reinterpret_cast<uint16_t*>(rec + bp.off_starts) + (size_t)sl * bp.jpad;
-    for (int j = tid; j < bp.jpad; j += NT) gst[j] = (uint16_t)(j <= J ? start[j] : tn);
-    __syncthreads();
-    uint4* gp = reinterpret_cast<uint4*>(rec + bp.off_perm + (size_t)sl * T * 2);
-    for (int i = tid; i < T * 2 / 16; i += NT) gp[i] = reinterpret_cast<const uint4*>(perm)[i];
-    __syncthreads();
+    int run = incl - sum;
+    for (int j = lo; j < lo + per && j < J; ++j) {
+      st[j] = run;
+      run += c[j];
+    }
+    for (int j = J + lane; j < JP; j += 32) st[j] = tn;  // start[J] = end of the last bucket
+  }
+  __syncthreads();
+  for (int e = tid; e < NS * tn; e += NT) {  // scatter
+    const int sl = e / tn, s = e - sl * tn;
+    const int k = smode[sl];
+    perm[(size_t)sl * T + start[sl * JP + idxs[(size_t)k * T + s]] + rnk[(size_t)sl * T + s]] = (uint16_t)s;
+  }
+  {
+    uint16_t* gst = reinterpret_cast<uint16_t*>(rec + bp.off_starts);
+    for (int i = tid; i < NS * JP; i += NT) gst[i] = (uint16_t)start[i];
+  }
+  __syncthreads();
+  {
+    uint4* gp = reinterpret_cast<uint4*>(rec + bp.off_perm);
+    const int n16 = NS * T * 2 / 16;
+    for (int i = tid; i < n16; i += NT) gp[i] = reinterpret_cast<const uint4*>(perm)[i];
   }
 }
 
@@ -600,9 +610,14 @@ int make_bplan(const ChainDev& ch, int64_t m, BPlan* bp, int* R_out, int* nt_out
   const int idx_bytes = small ? 1 : 2;
   const int jpad = ((jmax + 1) + 7) & ~7;
   const size_t budget = (size_t)(233472 / (512 / NT)) - 1024;
+  // the prep kernel holds every slot's permutation and ranks at once
+  auto prep_smem = [&](int t) {
+    return (size_t)ch.n * t * idx_bytes + (size_t)nsort * t * 4 + (size_t)2 * nsort * jpad * 4 + 128;
+  };
   int T = 65504;
-  while (T > 32 && compute_smem(T, RP, ch.n, idx_bytes, jpad) > budget) T -= 32;
-  if (compute_smem(T, RP, ch.n, idx_bytes, jpad) > budget)
+  while (T > 32 && (compute_smem(T, RP, ch.n, idx_bytes, jpad) > budget || prep_smem(T) > 232448 - 1024))
+    T -= 32;
+  if (compute_smem(T, RP, ch.n, idx_bytes, jpad) > budget || prep_smem(T) > 232448 - 1024)
     return set_error(TNB_EINVAL, "bucketed: chain too long for smem");
   bp->T = T;
   bp->nsort = nsort;
@@ -622,7 +637,8 @@ template <int R, typename IdxT, int NT>
 int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m, float* out,
               int32_t* err, unsigned char* ws, cudaStream_t st) {
   // prep: one CTA per tile
-  const size_t psmem = (size_t)ch.n * bp.T * sizeof(IdxT) + (size_t)bp.T * 4 + (size_t)2 * bp.jpad * 4;
+  const size_t psmem = (size_t)ch.n * bp.T * sizeof(IdxT) + (size_t)bp.nsort * bp.T * 4 +
+                       (size_t)2 * bp.nsort * bp.jpad * 4 + 128;
   auto pk = entries_prep_kernel<IdxT>;
   int rc = check_cuda(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem),
                       "prep smem attr");
