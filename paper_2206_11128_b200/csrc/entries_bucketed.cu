@@ -50,6 +50,14 @@ __device__ __forceinline__ float4 lds128(uint32_t a) {
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
   return v;
 }
+// ld.shared.v4 with a compile-time byte offset folded into the address
+template <int OFF>
+__device__ __forceinline__ float4 lds128o(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4+%5];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a), "n"(OFF));
+  return v;
+}
 __device__ __forceinline__ void sts64(uint32_t a, float x, float y) {
   asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(x), "f"(y) : "memory");
 }
@@ -101,9 +109,12 @@ struct Geo {
 template <int NP, int RP>
 __device__ __forceinline__ void ks_passes(const uint64_t (&g2)[16], const uint16_t* perm, int p,
                                           uint32_t s_state, int h, int qq) {
-  uint32_t rowb[NP];
+  uint32_t rowb[NP], rowh[NP];
 #pragma unroll
-  for (int pi = 0; pi < NP; ++pi) rowb[pi] = s_state + (uint32_t)perm[p + pi] * (RP * 4);
+  for (int pi = 0; pi < NP; ++pi) {
+    rowb[pi] = s_state + (uint32_t)perm[p + pi] * (RP * 4);
+    rowh[pi] = rowb[pi] + h * 64;
+  }
   uint64_t acc2[NP];
 #pragma unroll
   for (int pi = 0; pi < NP; ++pi) acc2[pi] = 0ull;
@@ -111,7 +122,14 @@ __device__ __forceinline__ void ks_passes(const uint64_t (&g2)[16], const uint16
   for (int a4 = 0; a4 < 4; ++a4) {
     float4 v[NP];
 #pragma unroll
-    for (int pi = 0; pi < NP; ++pi) v[pi] = lds128(rowb[pi] + h * 64 + a4 * 16);
+    for (int pi = 0; pi < NP; ++pi) {
+      switch (a4) {  // immediate offsets: no per-load address arithmetic
+        case 0: v[pi] = lds128o<0>(rowh[pi]); break;
+        case 1: v[pi] = lds128o<16>(rowh[pi]); break;
+        case 2: v[pi] = lds128o<32>(rowh[pi]); break;
+        default: v[pi] = lds128o<48>(rowh[pi]); break;
+      }
+    }
     // consecutive FFMA2s hit different accumulators (no back-to-back RAW)
 #pragma unroll
     for (int pi = 0; pi < NP; ++pi) ffma2(acc2[pi], g2[a4 * 4 + 0], v[pi].x);

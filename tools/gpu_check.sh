@@ -17,7 +17,7 @@ if [ -n "$NCU" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
       --log-file gpurun_out/launches.csv $P > gpurun_out/ncu_launch.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:${NCU_K:-entries_compute} \
-      -s 1 -c 1 -o gpurun_out/prof_entries $P > gpurun_out/ncu_full.log 2>&1
+      -s 1 -c ${NCU_C:-1} -o gpurun_out/prof_entries $P > gpurun_out/ncu_full.log 2>&1
   echo "ncu rc=$?" >> gpurun_out/ncu_full.log
 fi
 if [ -n "$NCU_FULL" ]; then
