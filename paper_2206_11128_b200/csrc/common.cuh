@@ -52,8 +52,9 @@ __device__ __forceinline__ float ldg_f(const float* p) { return __ldg(p); }
 // Normalises one raw index (negative wrap, core.py:411-413) and reports an
 // out-of-bounds value by lowering *err to the mode number (core.py:414-415).
 __device__ __forceinline__ int32_t norm_index(int64_t raw, int32_t J, int32_t k, int32_t* err) {
-  int64_t v = raw < 0 ? raw + J : raw;
-  if (v < 0 || v >= J) {
+  // one unsigned compare covers both v < 0 and v >= J
+  uint64_t v = (uint64_t)(raw < 0 ? raw + J : raw);
+  if (v >= (uint64_t)J) {
     atomicMin(err, k);
     v = 0;
   }

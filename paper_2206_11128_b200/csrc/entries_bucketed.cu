@@ -241,28 +241,33 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
       reinterpret_cast<uint4*>(rec)[i] = reinterpret_cast<const uint4*>(idxs)[i];
   }
   // ---- counting sort of every interior dense mode, all slots at once ----
-  // ranks: one warp-chunk of 32 samples of one slot per iteration
+  // ranks: per slot (warp-uniform mode, J, key width), warps stride over
+  // 32-sample chunks
   const int chunks = (tn + 31) >> 5;
-  for (int w = warp; w < NS * chunks; w += NW) {
-    const int sl = w / chunks, s = (w - sl * chunks) * 32 + lane;
+  for (int sl = 0; sl < NS; ++sl) {
     const int k = smode[sl];
     const int J = ch.m[k].J;
     const int kbits = 32 - __clz(J > 1 ? J - 1 : 1);
-    const bool act = s < tn;
-    const unsigned amask = __ballot_sync(0xffffffffu, act);
-    if (act) {
-      const int key = idxs[(size_t)k * T + s];
+    const IdxT* col = idxs + (size_t)k * T;
+    int* c = cnt + sl * JP;
+    uint16_t* rk = rnk + (size_t)sl * T;
+    for (int ch32 = warp; ch32 < chunks; ch32 += NW) {
+      const int s = ch32 * 32 + lane;
+      const bool act = s < tn;
+      const unsigned amask = __ballot_sync(0xffffffffu, act);
+      const int key = act ? (int)col[s] : 0;
       unsigned peers = amask;  // lanes holding the same key
       for (int b = 0; b < kbits; ++b) {
-        const bool bit = (key >> b) & 1;
-        const unsigned bal = __ballot_sync(amask, bit);
-        peers &= bit ? bal : ~bal;
+        const unsigned bal = __ballot_sync(0xffffffffu, (key >> b) & 1);
+        peers &= ((key >> b) & 1) ? bal : ~bal;
       }
-      const int leader = __ffs(peers) - 1;
-      int base = 0;
-      if (lane == leader) base = atomicAdd(&cnt[sl * JP + key], __popc(peers));
-      base = __shfl_sync(peers, base, leader);
-      rnk[(size_t)sl * T + s] = (uint16_t)(base + __popc(peers & lt_mask));
+      if (act) {
+        const int leader = __ffs(peers) - 1;
+        int base = 0;
+        if (lane == leader) base = atomicAdd(&c[key], __popc(peers));
+        base = __shfl_sync(peers, base, leader);
+        rk[s] = (uint16_t)(base + __popc(peers & lt_mask));
+      }
     }
   }
   __syncthreads();
@@ -288,10 +293,12 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
     for (int j = J + lane; j < JP; j += 32) st[j] = tn;  // start[J] = end of the last bucket
   }
   __syncthreads();
-  for (int e = tid; e < NS * tn; e += NT) {  // scatter
-    const int sl = e / tn, s = e - sl * tn;
-    const int k = smode[sl];
-    perm[(size_t)sl * T + start[sl * JP + idxs[(size_t)k * T + s]] + rnk[(size_t)sl * T + s]] = (uint16_t)s;
+  for (int sl = 0; sl < NS; ++sl) {  // scatter
+    const IdxT* col = idxs + (size_t)smode[sl] * T;
+    const int* st = start + sl * JP;
+    const uint16_t* rk = rnk + (size_t)sl * T;
+    uint16_t* pm = perm + (size_t)sl * T;
+    for (int s = tid; s < tn; s += NT) pm[st[col[s]] + rk[s]] = (uint16_t)s;
   }
   {
     uint16_t* gst = reinterpret_cast<uint16_t*>(rec + bp.off_starts);
@@ -329,7 +336,7 @@ __device__ __forceinline__ void bulk(void* dst, const void* src, uint32_t bytes,
 }
 
 template <int R, typename IdxT, int NT>
-__global__ void __launch_bounds__(NT, 512 / NT)
+__global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
     entries_compute_kernel(const __grid_constant__ ChainDev ch, const __grid_constant__ BPlan bp,
                            const unsigned char* __restrict__ ws, int64_t m, float* __restrict__ out) {
   using Gm = Geo<R>;
@@ -598,7 +605,8 @@ int bucket_threads() {
   static int v = 0;
   if (v == 0) {
     const char* e = getenv("TNB_BUCKET_THREADS");
-    v = (e && atoi(e) == 256) ? 256 : 512;
+    const int x = e ? atoi(e) : 512;
+    v = (x == 256 || x == 640 || x == 768) ? x : 512;
   }
   return v;
 }
@@ -627,7 +635,7 @@ int make_bplan(const ChainDev& ch, int64_t m, BPlan* bp, int* R_out, int* nt_out
   const int RP = R + 4;
   const int idx_bytes = small ? 1 : 2;
   const int jpad = ((jmax + 1) + 7) & ~7;
-  const size_t budget = (size_t)(233472 / (512 / NT)) - 1024;
+  const size_t budget = (size_t)(233472 / (NT <= 256 ? 2 : 1)) - 1024;
   // the prep kernel holds every slot's permutation and ranks at once
   auto prep_smem = [&](int t) {
     return (size_t)ch.n * t * idx_bytes + (size_t)nsort * t * 4 + (size_t)2 * nsort * jpad * 4 + 128;
@@ -669,7 +677,7 @@ int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m
   rc = check_cuda(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem),
                   "compute smem attr");
   if (rc) return rc;
-  const int64_t slots = (int64_t)num_sms() * (512 / NT);
+  const int64_t slots = (int64_t)num_sms() * (NT <= 256 ? 2 : 1);
   const int grid = (int)(bp.ntiles < slots ? bp.ntiles : slots);
   ck<<<grid, NT, csmem, st>>>(ch, bp, ws, m, out);
   return check_launch("entries_compute");
@@ -679,6 +687,8 @@ template <int R, typename IdxT>
 int launch_ri(const ChainDev& ch, const BPlan& bp, int nt, const int64_t* idx, int64_t m, float* out,
               int32_t* err, unsigned char* ws, cudaStream_t st) {
   if (nt == 256) return launch_rt<R, IdxT, 256>(ch, bp, idx, m, out, err, ws, st);
+  if (nt == 640) return launch_rt<R, IdxT, 640>(ch, bp, idx, m, out, err, ws, st);
+  if (nt == 768) return launch_rt<R, IdxT, 768>(ch, bp, idx, m, out, err, ws, st);
   return launch_rt<R, IdxT, 512>(ch, bp, idx, m, out, err, ws, st);
 }
 
