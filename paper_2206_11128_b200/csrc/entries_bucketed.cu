@@ -34,15 +34,7 @@ namespace {
 
 constexpr int kMaxJ = 1024;          // bucket count limit for sorted modes
 
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
 
-__device__ __forceinline__ int64_t ld_stream_i64(const int64_t* p) {
-  int64_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.b64 %0, [%1];" : "=l"(v) : "l"(p));
-  return v;
-}
 
 __device__ __forceinline__ float4 lds128(uint32_t a) {
   float4 v;
@@ -57,9 +49,6 @@ __device__ __forceinline__ float4 lds128o(uint32_t a) {
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4+%5];"
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a), "n"(OFF));
   return v;
-}
-__device__ __forceinline__ void sts64(uint32_t a, float x, float y) {
-  asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(x), "f"(y) : "memory");
 }
 __device__ __forceinline__ void sts_b64(uint32_t a, uint64_t x) {
   asm volatile("st.shared.b64 [%0], %1;" ::"r"(a), "l"(x) : "memory");
@@ -194,44 +183,25 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
 
   for (int i = tid; i < NS * JP; i += NT) cnt[i] = 0;
   if (tid < N && bp.slot[tid] >= 0) smode[bp.slot[tid]] = (int8_t)tid;
-  // ---- indices: coalesced int64 read (4 in flight), wrap/validate, compact
+  // ---- indices: thread = sample row (N int64 values, 16-byte loads when the
+  //      row stride allows), wrap/validate per mode, compact to [N][T]
   {
     const int64_t* src = idx + s0 * N;
-    const int total = tn * N;
-    constexpr int U = 4;
-    int ss[U], kk[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int e = tid + u * NT;
-      ss[u] = e / N;
-      kk[u] = e - ss[u] * N;
-    }
-    const int ds = (U * NT) / N, dk = (U * NT) - ds * N;
-    for (int e0 = tid; e0 < total; e0 += U * NT) {
-      int64_t raw[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int e = e0 + u * NT;
-        raw[u] = (e < total) ? ld_stream_i64(src + e) : 0;
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (e0 + u * NT < total) {
-          const int k = kk[u];
-          idxs[(size_t)k * T + ss[u]] = (IdxT)norm_index(raw[u], ch.m[k].J, k, err);
+    const bool v2 = (N & 1) == 0 && (reinterpret_cast<uintptr_t>(idx) & 15) == 0;
+    for (int s = tid; s < T; s += NT) {
+      const int64_t* row = src + (int64_t)s * N;
+      if (s >= tn) {
+        for (int k = 0; k < N; ++k) idxs[(size_t)k * T + s] = (IdxT)0;  // tail rows: index 0
+      } else if (v2) {
+        for (int k = 0; k < N; k += 2) {
+          const longlong2 w = __ldg(reinterpret_cast<const longlong2*>(row + k));
+          idxs[(size_t)k * T + s] = (IdxT)norm_index(w.x, ch.m[k].J, k, err);
+          idxs[(size_t)(k + 1) * T + s] = (IdxT)norm_index(w.y, ch.m[k + 1].J, k + 1, err);
         }
-        ss[u] += ds;
-        kk[u] += dk;
-        if (kk[u] >= N) {
-          kk[u] -= N;
-          ++ss[u];
-        }
+      } else {
+        for (int k = 0; k < N; ++k)
+          idxs[(size_t)k * T + s] = (IdxT)norm_index(__ldg(row + k), ch.m[k].J, k, err);
       }
-    }
-    // tail rows of the last tile: index 0 keeps every later read in bounds
-    for (int e = tid; e < (T - tn) * N; e += NT) {
-      const int k = e / (T - tn), sx = tn + (e - k * (T - tn));
-      idxs[(size_t)k * T + sx] = (IdxT)0;
     }
   }
   __syncthreads();
@@ -247,7 +217,7 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
   for (int sl = 0; sl < NS; ++sl) {
     const int k = smode[sl];
     const int J = ch.m[k].J;
-    const int kbits = 32 - __clz(J > 1 ? J - 1 : 1);
+    (void)J;
     const IdxT* col = idxs + (size_t)k * T;
     int* c = cnt + sl * JP;
     uint16_t* rk = rnk + (size_t)sl * T;
@@ -256,12 +226,8 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
       const bool act = s < tn;
       const unsigned amask = __ballot_sync(0xffffffffu, act);
       const int key = act ? (int)col[s] : 0;
-      unsigned peers = amask;  // lanes holding the same key
-      for (int b = 0; b < kbits; ++b) {
-        const unsigned bal = __ballot_sync(0xffffffffu, (key >> b) & 1);
-        peers &= ((key >> b) & 1) ? bal : ~bal;
-      }
       if (act) {
+        const unsigned peers = __match_any_sync(amask, key);  // lanes holding the same key
         const int leader = __ffs(peers) - 1;
         int base = 0;
         if (lane == leader) base = atomicAdd(&c[key], __popc(peers));
