@@ -159,21 +159,31 @@ struct BPlan {
   int8_t slot[kMaxModes];  // mode -> sorted slot or -1
 };
 
-template <typename IdxT>
+// Warp-level multisplit: the lanes' keys are transposed into kbits ballots;
+// lane j owns buckets j, j+32, ... and gets each bucket's member mask from the
+// ballots alone -- no atomics, no MATCH loops.
+__device__ __forceinline__ unsigned key_mask(const unsigned (&b)[10], int kbits, int key, unsigned amask) {
+  unsigned m = amask;
+#pragma unroll
+  for (int i = 0; i < 10; ++i)
+    if (i < kbits) m &= ((key >> i) & 1) ? b[i] : ~b[i];
+  return m;
+}
+
+template <typename IdxT, int MAXBPL>
 __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant__ ChainDev ch,
                                                            const __grid_constant__ BPlan bp,
                                                            const int64_t* __restrict__ idx, int64_t m,
                                                            int32_t* __restrict__ err,
                                                            unsigned char* __restrict__ ws) {
-  constexpr int NT = 512, NW = NT / 32;
+  constexpr int NT = 512, NW = NT / 32;  // MAXBPL: buckets per lane (J <= 32 * MAXBPL)
   extern __shared__ __align__(16) unsigned char smem[];
   const int N = ch.n, T = bp.T, NS = bp.nsort, JP = bp.jpad;
   IdxT* idxs = reinterpret_cast<IdxT*>(smem);                                          // [N][T]
   uint16_t* perm = reinterpret_cast<uint16_t*>(smem + (size_t)N * T * sizeof(IdxT));  // [NS][T]
-  uint16_t* rnk = perm + (size_t)NS * T;                                               // [NS][T]
-  int* cnt = reinterpret_cast<int*>(rnk + (size_t)NS * T);                             // [NS][JP]
-  int* start = cnt + (size_t)NS * JP;                                                  // [NS][JP]
-  int8_t* smode = reinterpret_cast<int8_t*>(start + (size_t)NS * JP);                  // slot -> mode
+  int* cw = reinterpret_cast<int*>(perm + (size_t)NS * T);                             // [NS][JP][NW]
+  int* wsum = cw + (size_t)NS * JP * NW;                                               // [NW]
+  int8_t* smode = reinterpret_cast<int8_t*>(wsum + NW);                                // slot -> mode
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
   const int64_t tile = blockIdx.x;
@@ -181,7 +191,6 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
   const int tn = (int)((m - s0) < T ? (m - s0) : T);
   unsigned char* rec = ws + tile * bp.tile_bytes;
 
-  for (int i = tid; i < NS * JP; i += NT) cnt[i] = 0;
   if (tid < N && bp.slot[tid] >= 0) smode[bp.slot[tid]] = (int8_t)tid;
   // ---- indices: thread = sample row (N int64 values, 16-byte loads when the
   //      row stride allows), wrap/validate per mode, compact to [N][T]
@@ -210,65 +219,102 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
     for (int i = tid; i < n16; i += NT)
       reinterpret_cast<uint4*>(rec)[i] = reinterpret_cast<const uint4*>(idxs)[i];
   }
-  // ---- counting sort of every interior dense mode, all slots at once ----
-  // ranks: per slot (warp-uniform mode, J, key width), warps stride over
-  // 32-sample chunks
   const int chunks = (tn + 31) >> 5;
+  const int c_lo = (warp * chunks) / NW, c_hi = ((warp + 1) * chunks) / NW;
+  // ---- pass 1: per-warp bucket counts (lane j owns buckets j + 32u) ----
   for (int sl = 0; sl < NS; ++sl) {
     const int k = smode[sl];
     const int J = ch.m[k].J;
-    (void)J;
+    const int kbits = 32 - __clz(J > 1 ? J - 1 : 1);
+    const int bpl = (J + 31) >> 5;
     const IdxT* col = idxs + (size_t)k * T;
-    int* c = cnt + sl * JP;
-    uint16_t* rk = rnk + (size_t)sl * T;
-    for (int ch32 = warp; ch32 < chunks; ch32 += NW) {
-      const int s = ch32 * 32 + lane;
-      const bool act = s < tn;
-      const unsigned amask = __ballot_sync(0xffffffffu, act);
-      const int key = act ? (int)col[s] : 0;
-      if (act) {
-        const unsigned peers = __match_any_sync(amask, key);  // lanes holding the same key
-        const int leader = __ffs(peers) - 1;
-        int base = 0;
-        if (lane == leader) base = atomicAdd(&c[key], __popc(peers));
-        base = __shfl_sync(peers, base, leader);
-        rk[s] = (uint16_t)(base + __popc(peers & lt_mask));
-      }
+    int cnt[MAXBPL];
+#pragma unroll
+    for (int u = 0; u < MAXBPL; ++u) cnt[u] = 0;
+    for (int c = c_lo; c < c_hi; ++c) {
+      const int s = c * 32 + lane;
+      const unsigned amask = __ballot_sync(0xffffffffu, s < tn);
+      const int key = s < tn ? (int)col[s] : 0;
+      unsigned b[10];
+#pragma unroll
+      for (int i = 0; i < 10; ++i) b[i] = (i < kbits) ? __ballot_sync(0xffffffffu, (key >> i) & 1) : 0u;
+#pragma unroll
+      for (int u = 0; u < MAXBPL; ++u)
+        if (u < bpl) cnt[u] += __popc(key_mask(b, kbits, lane + 32 * u, amask));
     }
+    int* c_sl = cw + (size_t)sl * JP * NW;
+#pragma unroll
+    for (int u = 0; u < MAXBPL; ++u)
+      if (u < bpl && lane + 32 * u < J) c_sl[(lane + 32 * u) * NW + warp] = cnt[u];
   }
   __syncthreads();
-  for (int sl = warp; sl < NS; sl += NW) {  // exclusive scan per slot (one warp each)
+  // ---- exclusive scan of every slot's [J][NW] counts (j-major, warp-minor)
+  for (int sl = 0; sl < NS; ++sl) {
     const int J = ch.m[smode[sl]].J;
-    const int per = (J + 31) / 32;
-    const int lo = lane * per;
-    const int* c = cnt + sl * JP;
-    int* st = start + sl * JP;
+    int* c_sl = cw + (size_t)sl * JP * NW;
+    const int E = J * NW;
+    const int per = (E + NT - 1) / NT, lo = tid * per;
     int sum = 0;
-    for (int j = lo; j < lo + per && j < J; ++j) sum += c[j];
+    for (int e = lo; e < lo + per && e < E; ++e) sum += c_sl[e];
     int incl = sum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int y = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += y;
     }
-    int run = incl - sum;
-    for (int j = lo; j < lo + per && j < J; ++j) {
-      st[j] = run;
-      run += c[j];
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    int wpre = 0;
+    for (int w = 0; w < warp; ++w) wpre += wsum[w];
+    int run = wpre + incl - sum;
+    for (int e = lo; e < lo + per && e < E; ++e) {
+      const int v = c_sl[e];
+      c_sl[e] = run;
+      run += v;
     }
-    for (int j = J + lane; j < JP; j += 32) st[j] = tn;  // start[J] = end of the last bucket
+    __syncthreads();
   }
-  __syncthreads();
-  for (int sl = 0; sl < NS; ++sl) {  // scatter
-    const IdxT* col = idxs + (size_t)smode[sl] * T;
-    const int* st = start + sl * JP;
-    const uint16_t* rk = rnk + (size_t)sl * T;
+  // ---- pass 2: scatter (bucket base + running count + rank among peers) ----
+  for (int sl = 0; sl < NS; ++sl) {
+    const int k = smode[sl];
+    const int J = ch.m[k].J;
+    const int kbits = 32 - __clz(J > 1 ? J - 1 : 1);
+    const int bpl = (J + 31) >> 5;
+    const IdxT* col = idxs + (size_t)k * T;
+    const int* c_sl = cw + (size_t)sl * JP * NW;
     uint16_t* pm = perm + (size_t)sl * T;
-    for (int s = tid; s < tn; s += NT) pm[st[col[s]] + rk[s]] = (uint16_t)s;
+    int run[MAXBPL];
+#pragma unroll
+    for (int u = 0; u < MAXBPL; ++u) run[u] = (u < bpl && lane + 32 * u < J) ? c_sl[(lane + 32 * u) * NW + warp] : 0;
+    for (int c = c_lo; c < c_hi; ++c) {
+      const int s = c * 32 + lane;
+      const unsigned amask = __ballot_sync(0xffffffffu, s < tn);
+      const int key = s < tn ? (int)col[s] : 0;
+      unsigned b[10];
+#pragma unroll
+      for (int i = 0; i < 10; ++i) b[i] = (i < kbits) ? __ballot_sync(0xffffffffu, (key >> i) & 1) : 0u;
+      const unsigned peers = key_mask(b, kbits, key, amask);
+      int base = 0;
+#pragma unroll
+      for (int u = 0; u < MAXBPL; ++u) {
+        if (u < bpl) {
+          const int v = __shfl_sync(0xffffffffu, run[u], key & 31);
+          if ((key >> 5) == u) base = v;
+        }
+      }
+      if (s < tn) pm[base + __popc(peers & lt_mask)] = (uint16_t)s;
+#pragma unroll
+      for (int u = 0; u < MAXBPL; ++u)
+        if (u < bpl) run[u] += __popc(key_mask(b, kbits, lane + 32 * u, amask));
+    }
   }
-  {
+  {  // bucket starts: the scanned count of (j, warp 0); start[J..] = tn
     uint16_t* gst = reinterpret_cast<uint16_t*>(rec + bp.off_starts);
-    for (int i = tid; i < NS * JP; i += NT) gst[i] = (uint16_t)start[i];
+    for (int i = tid; i < NS * JP; i += NT) {
+      const int sl = i / JP, j = i - sl * JP;
+      const int J = ch.m[smode[sl]].J;
+      gst[i] = (uint16_t)(j < J ? cw[((size_t)sl * JP + j) * NW] : tn);
+    }
   }
   __syncthreads();
   {
@@ -577,6 +623,10 @@ int bucket_threads() {
   return v;
 }
 
+size_t prep_smem_bytes(int N, int T, int idx_bytes, int nsort, int jpad) {
+  return (size_t)N * T * idx_bytes + (size_t)nsort * T * 2 + (size_t)nsort * jpad * 16 * 4 + 16 * 4 + 256;
+}
+
 size_t compute_smem(int T, int RP, int N, int idx_bytes, int jpad) {
   size_t b = (size_t)(T + 1) * RP * 4 + (size_t)N * T * idx_bytes + (size_t)2 * T * 2 + (size_t)2 * jpad * 2;
   return ((b + 15) & ~(size_t)15) + 3 * 8;
@@ -602,10 +652,8 @@ int make_bplan(const ChainDev& ch, int64_t m, BPlan* bp, int* R_out, int* nt_out
   const int idx_bytes = small ? 1 : 2;
   const int jpad = ((jmax + 1) + 7) & ~7;
   const size_t budget = (size_t)(233472 / (NT <= 256 ? 2 : 1)) - 1024;
-  // the prep kernel holds every slot's permutation and ranks at once
-  auto prep_smem = [&](int t) {
-    return (size_t)ch.n * t * idx_bytes + (size_t)nsort * t * 4 + (size_t)2 * nsort * jpad * 4 + 128;
-  };
+  // the prep kernel holds every slot's permutation and per-warp counts at once
+  auto prep_smem = [&](int t) { return prep_smem_bytes(ch.n, t, idx_bytes, nsort, jpad); };
   int T = 65504;
   while (T > 32 && (compute_smem(T, RP, ch.n, idx_bytes, jpad) > budget || prep_smem(T) > 232448 - 1024))
     T -= 32;
@@ -629,9 +677,11 @@ template <int R, typename IdxT, int NT>
 int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m, float* out,
               int32_t* err, unsigned char* ws, cudaStream_t st) {
   // prep: one CTA per tile
-  const size_t psmem = (size_t)ch.n * bp.T * sizeof(IdxT) + (size_t)bp.nsort * bp.T * 4 +
-                       (size_t)2 * bp.nsort * bp.jpad * 4 + 128;
-  auto pk = entries_prep_kernel<IdxT>;
+  const size_t psmem = prep_smem_bytes(ch.n, bp.T, (int)sizeof(IdxT), bp.nsort, bp.jpad);
+  int jmax = 1;
+  for (int k = 0; k < ch.n; ++k)
+    if (bp.slot[k] >= 0 && ch.m[k].J > jmax) jmax = ch.m[k].J;
+  auto pk = jmax <= 128 ? entries_prep_kernel<IdxT, 4> : entries_prep_kernel<IdxT, kMaxJ / 32>;
   int rc = check_cuda(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem),
                       "prep smem attr");
   if (rc) return rc;

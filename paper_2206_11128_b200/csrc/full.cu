@@ -18,9 +18,10 @@
 namespace tnb {
 // tcgen05 3xTF32 GEMM (full_tc.cu); returns false when the shape is unsupported
 bool tc_gemm_supported(int64_t M, int64_t N, int K, int64_t lda, int64_t ldb, int64_t ldc);
+int64_t tc_gemm_workspace(int64_t M);
 int launch_tc_gemm(const float* A, int64_t lda, int64_t sA, const float* B, int64_t ldb,
                    int64_t sB, float* C, int64_t ldc, int64_t sC, int64_t M, int64_t N, int K,
-                   int64_t batch, cudaStream_t st);
+                   int64_t batch, void* ws, cudaStream_t st);
 
 namespace {
 
@@ -38,6 +39,7 @@ struct FullPlan {
   int64_t l_buf = 0;    // floats per batch element per L ping-pong buffer
   int64_t r_buf = 0;    // floats per batch element per R ping-pong buffer
   int64_t out_per = 0;  // floats per batch element of the output slab
+  int64_t tc_bytes = 0; // tensor-core GEMM workspace (split L tiles)
 };
 
 int make_plan(const tnb_chain* c, int64_t lo, int64_t hi, FullPlan* P) {
@@ -105,6 +107,9 @@ int make_plan(const tnb_chain* c, int64_t lo, int64_t hi, FullPlan* P) {
   P->colsR = cols;
   P->l_buf = lmax;
   P->r_buf = rmax;
+  P->tc_bytes = 0;
+  if (p < n && tc_gemm_supported(P->rowsL, cols, m[p].r_left, m[p].r_left, cols, cols))
+    P->tc_bytes = tc_gemm_workspace(P->rowsL);
   return TNB_OK;
 }
 
@@ -257,6 +262,11 @@ inline int grid_for(int64_t total) {
   return (int)(g < 1 ? 1 : g);
 }
 
+// byte offset of the tensor-core workspace (256-byte aligned)
+int64_t tc_offset(const FullPlan& P, int64_t B) {
+  return ((2 * P.l_buf + 2 * P.r_buf) * B * (int64_t)sizeof(float) + 255) & ~(int64_t)255;
+}
+
 ModeDev mode_dev(const tnb_chain* c, int k) {
   const tnb_mode& mm = c->modes[k];
   ModeDev md;
@@ -286,7 +296,7 @@ int64_t full_workspace(const tnb_chain* c, int64_t lo, int64_t hi) {
   FullPlan P;
   if (make_plan(c, lo, hi, &P)) return -1;
   const int64_t B = c->batch > 0 ? c->batch : 1;
-  return (2 * P.l_buf + 2 * P.r_buf) * B * (int64_t)sizeof(float);
+  return tc_offset(P, B) + P.tc_bytes;
 }
 
 int launch_full(const tnb_chain* c, int64_t lo, int64_t hi, float* out, void* ws,
@@ -300,7 +310,7 @@ int launch_full(const tnb_chain* c, int64_t lo, int64_t hi, float* out, void* ws
   const int64_t B = c->batch > 0 ? c->batch : 1;
   if (P.out_per == 0) return TNB_OK;
   if (!out) return set_error(TNB_EINVAL, "null output");
-  const int64_t need = (2 * P.l_buf + 2 * P.r_buf) * B * (int64_t)sizeof(float);
+  const int64_t need = tc_offset(P, B) + P.tc_bytes;
   if (need > 0 && (!ws || ws_bytes < need))
     return set_error(TNB_EWORKSPACE, "full needs %lld workspace bytes, got %lld",
                      (long long)need, (long long)ws_bytes);
@@ -365,9 +375,10 @@ int launch_full(const tnb_chain* c, int64_t lo, int64_t hi, float* out, void* ws
   // ---- out = L @ R ----
   const int K = c->modes[p].r_left;
   if (K == 0) return check_cuda(cudaMemsetAsync(out, 0, P.out_per * B * sizeof(float), st), "memset");
-  if (tc_gemm_supported(rows, cols, K, K, cols, cols) && (reinterpret_cast<uintptr_t>(L) & 15) == 0 &&
-      ((L_bs * 4) & 15) == 0)
-    return launch_tc_gemm(L, K, L_bs, R, cols, P.r_buf, out, cols, P.out_per, rows, cols, K, B, st);
+  if (P.tc_bytes > 0) {
+    void* tcw = (unsigned char*)ws + tc_offset(P, B);
+    return launch_tc_gemm(L, K, L_bs, R, cols, P.r_buf, out, cols, P.out_per, rows, cols, K, B, tcw, st);
+  }
   return launch_sgemm(L, K, L_bs, R, cols, P.r_buf, out, cols, P.out_per, rows, cols, K, B, st);
 }
 
