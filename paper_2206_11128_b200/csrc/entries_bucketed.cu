@@ -162,15 +162,15 @@ struct BPlan {
 // Warp-level multisplit: the lanes' keys are transposed into kbits ballots;
 // lane j owns buckets j, j+32, ... and gets each bucket's member mask from the
 // ballots alone -- no atomics, no MATCH loops.
-__device__ __forceinline__ unsigned key_mask(const unsigned (&b)[10], int kbits, int key, unsigned amask) {
+template <int KB>
+__device__ __forceinline__ unsigned key_mask(const unsigned (&b)[KB], int key, unsigned amask) {
   unsigned m = amask;
 #pragma unroll
-  for (int i = 0; i < 10; ++i)
-    if (i < kbits) m &= ((key >> i) & 1) ? b[i] : ~b[i];
+  for (int i = 0; i < KB; ++i) m &= b[i] ^ (((key >> i) & 1) ? 0u : 0xffffffffu);
   return m;
 }
 
-template <typename IdxT, int MAXBPL>
+template <typename IdxT, int MAXBPL, int KB>
 __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant__ ChainDev ch,
                                                            const __grid_constant__ BPlan bp,
                                                            const int64_t* __restrict__ idx, int64_t m,
@@ -225,7 +225,6 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
   for (int sl = 0; sl < NS; ++sl) {
     const int k = smode[sl];
     const int J = ch.m[k].J;
-    const int kbits = 32 - __clz(J > 1 ? J - 1 : 1);
     const int bpl = (J + 31) >> 5;
     const IdxT* col = idxs + (size_t)k * T;
     int cnt[MAXBPL];
@@ -235,12 +234,12 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
       const int s = c * 32 + lane;
       const unsigned amask = __ballot_sync(0xffffffffu, s < tn);
       const int key = s < tn ? (int)col[s] : 0;
-      unsigned b[10];
+      unsigned b[KB];  // KB >= bits of every slot's J: higher key bits are 0
 #pragma unroll
-      for (int i = 0; i < 10; ++i) b[i] = (i < kbits) ? __ballot_sync(0xffffffffu, (key >> i) & 1) : 0u;
+      for (int i = 0; i < KB; ++i) b[i] = __ballot_sync(0xffffffffu, (key >> i) & 1);
 #pragma unroll
       for (int u = 0; u < MAXBPL; ++u)
-        if (u < bpl) cnt[u] += __popc(key_mask(b, kbits, lane + 32 * u, amask));
+        if (u < bpl) cnt[u] += __popc(key_mask<KB>(b, lane + 32 * u, amask));
     }
     int* c_sl = cw + (size_t)sl * JP * NW;
 #pragma unroll
@@ -278,7 +277,6 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
   for (int sl = 0; sl < NS; ++sl) {
     const int k = smode[sl];
     const int J = ch.m[k].J;
-    const int kbits = 32 - __clz(J > 1 ? J - 1 : 1);
     const int bpl = (J + 31) >> 5;
     const IdxT* col = idxs + (size_t)k * T;
     const int* c_sl = cw + (size_t)sl * JP * NW;
@@ -290,10 +288,10 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
       const int s = c * 32 + lane;
       const unsigned amask = __ballot_sync(0xffffffffu, s < tn);
       const int key = s < tn ? (int)col[s] : 0;
-      unsigned b[10];
+      unsigned b[KB];  // KB >= bits of every slot's J: higher key bits are 0
 #pragma unroll
-      for (int i = 0; i < 10; ++i) b[i] = (i < kbits) ? __ballot_sync(0xffffffffu, (key >> i) & 1) : 0u;
-      const unsigned peers = key_mask(b, kbits, key, amask);
+      for (int i = 0; i < KB; ++i) b[i] = __ballot_sync(0xffffffffu, (key >> i) & 1);
+      const unsigned peers = key_mask<KB>(b, key, amask);
       int base = 0;
 #pragma unroll
       for (int u = 0; u < MAXBPL; ++u) {
@@ -305,7 +303,7 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
       if (s < tn) pm[base + __popc(peers & lt_mask)] = (uint16_t)s;
 #pragma unroll
       for (int u = 0; u < MAXBPL; ++u)
-        if (u < bpl) run[u] += __popc(key_mask(b, kbits, lane + 32 * u, amask));
+        if (u < bpl) run[u] += __popc(key_mask<KB>(b, lane + 32 * u, amask));
     }
   }
   {  // bucket starts: the scanned count of (j, warp 0); start[J..] = tn
@@ -681,7 +679,11 @@ int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m
   int jmax = 1;
   for (int k = 0; k < ch.n; ++k)
     if (bp.slot[k] >= 0 && ch.m[k].J > jmax) jmax = ch.m[k].J;
-  auto pk = jmax <= 128 ? entries_prep_kernel<IdxT, 4> : entries_prep_kernel<IdxT, kMaxJ / 32>;
+  const int kb = 32 - __builtin_clz((unsigned)(jmax > 1 ? jmax - 1 : 1));
+  auto pk = kb <= 5   ? entries_prep_kernel<IdxT, 1, 5>
+            : kb == 6 ? entries_prep_kernel<IdxT, 2, 6>
+            : kb == 7 ? entries_prep_kernel<IdxT, 4, 7>
+                      : entries_prep_kernel<IdxT, kMaxJ / 32, 10>;
   int rc = check_cuda(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem),
                       "prep smem attr");
   if (rc) return rc;

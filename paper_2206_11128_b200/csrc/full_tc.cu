@@ -292,8 +292,10 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
         tc_fence_after();
         const int64_t col = cb * NB * BNB + nb * BNB + q * 32 + lane;
         const bool cok = col < N;
-        float* dst = args.C + (mt * BMT) * args.ldc + col;
         const int64_t rows_left = M - mt * BMT;
+        const bool full_rows = rows_left >= BMT;
+        const int64_t ldc = args.ldc;
+        float* p = args.C + (mt * BMT) * ldc + col;  // row mt*128, advanced by ldc per row
         uint32_t va[32], vb[32];
         TMEM_LD32(tm_acc0 + cbuf * BMT + lane_base, va);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -302,14 +304,18 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
           uint32_t* cur = (ch & 1) ? vb : va;
           uint32_t* nxt = (ch & 1) ? va : vb;
           if (ch + 1 < BMT / 32) TMEM_LD32(tm_acc0 + cbuf * BMT + lane_base + (ch + 1) * 32, nxt);
-          if (cok) {
+          if (cok && full_rows) {
+            // one st.global per row: the warp's 32 lanes write 128 contiguous bytes
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-              const int r = ch * 32 + j;
-              if (r < rows_left)
-                asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(dst + (int64_t)r * args.ldc),
-                             "f"(__uint_as_float(cur[j]))
-                             : "memory");
+              *p = __uint_as_float(cur[j]);
+              p += ldc;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if (cok && ch * 32 + j < rows_left) *p = __uint_as_float(cur[j]);
+              p += ldc;
             }
           }
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
