@@ -181,9 +181,7 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
   const int N = ch.n, T = bp.T, NS = bp.nsort, JP = bp.jpad;
   IdxT* idxs = reinterpret_cast<IdxT*>(smem);                                          // [N][T]
   uint16_t* perm = reinterpret_cast<uint16_t*>(smem + (size_t)N * T * sizeof(IdxT));  // [NS][T]
-  int* cw = reinterpret_cast<int*>(perm + (size_t)NS * T);                             // [NS][JP][NW]
-  int* wsum = cw + (size_t)NS * JP * NW;                                               // [NW]
-  int8_t* smode = reinterpret_cast<int8_t*>(wsum + NW);                                // slot -> mode
+  int8_t* smode = reinterpret_cast<int8_t*>(perm + (size_t)NS * T);                    // slot -> mode
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
   const int64_t tile = blockIdx.x;
@@ -219,18 +217,20 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
     for (int i = tid; i < n16; i += NT)
       reinterpret_cast<uint4*>(rec)[i] = reinterpret_cast<const uint4*>(idxs)[i];
   }
+  // ---- one warp per sorted slot: count, warp scan, scatter (no block
+  //      barriers, no atomics; lane j owns buckets j, j+32, ...)
   const int chunks = (tn + 31) >> 5;
-  const int c_lo = (warp * chunks) / NW, c_hi = ((warp + 1) * chunks) / NW;
-  // ---- pass 1: per-warp bucket counts (lane j owns buckets j + 32u) ----
-  for (int sl = 0; sl < NS; ++sl) {
+  uint16_t* gst_all = reinterpret_cast<uint16_t*>(rec + bp.off_starts);
+  for (int sl = warp; sl < NS; sl += NW) {
     const int k = smode[sl];
     const int J = ch.m[k].J;
     const int bpl = (J + 31) >> 5;
     const IdxT* col = idxs + (size_t)k * T;
+    uint16_t* pm = perm + (size_t)sl * T;
     int cnt[MAXBPL];
 #pragma unroll
     for (int u = 0; u < MAXBPL; ++u) cnt[u] = 0;
-    for (int c = c_lo; c < c_hi; ++c) {
+    for (int c = 0; c < chunks; ++c) {
       const int s = c * 32 + lane;
       const unsigned amask = __ballot_sync(0xffffffffu, s < tn);
       const int key = s < tn ? (int)col[s] : 0;
@@ -241,54 +241,36 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
       for (int u = 0; u < MAXBPL; ++u)
         if (u < bpl) cnt[u] += __popc(key_mask<KB>(b, lane + 32 * u, amask));
     }
-    int* c_sl = cw + (size_t)sl * JP * NW;
-#pragma unroll
-    for (int u = 0; u < MAXBPL; ++u)
-      if (u < bpl && lane + 32 * u < J) c_sl[(lane + 32 * u) * NW + warp] = cnt[u];
-  }
-  __syncthreads();
-  // ---- exclusive scan of every slot's [J][NW] counts (j-major, warp-minor)
-  for (int sl = 0; sl < NS; ++sl) {
-    const int J = ch.m[smode[sl]].J;
-    int* c_sl = cw + (size_t)sl * JP * NW;
-    const int E = J * NW;
-    const int per = (E + NT - 1) / NT, lo = tid * per;
-    int sum = 0;
-    for (int e = lo; e < lo + per && e < E; ++e) sum += c_sl[e];
-    int incl = sum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane == 31) wsum[warp] = incl;
-    __syncthreads();
-    int wpre = 0;
-    for (int w = 0; w < warp; ++w) wpre += wsum[w];
-    int run = wpre + incl - sum;
-    for (int e = lo; e < lo + per && e < E; ++e) {
-      const int v = c_sl[e];
-      c_sl[e] = run;
-      run += v;
-    }
-    __syncthreads();
-  }
-  // ---- pass 2: scatter (bucket base + running count + rank among peers) ----
-  for (int sl = 0; sl < NS; ++sl) {
-    const int k = smode[sl];
-    const int J = ch.m[k].J;
-    const int bpl = (J + 31) >> 5;
-    const IdxT* col = idxs + (size_t)k * T;
-    const int* c_sl = cw + (size_t)sl * JP * NW;
-    uint16_t* pm = perm + (size_t)sl * T;
+    // exclusive scan over buckets j = lane + 32u (u-major, then lane)
     int run[MAXBPL];
+    int carry = 0;
 #pragma unroll
-    for (int u = 0; u < MAXBPL; ++u) run[u] = (u < bpl && lane + 32 * u < J) ? c_sl[(lane + 32 * u) * NW + warp] : 0;
-    for (int c = c_lo; c < c_hi; ++c) {
+    for (int u = 0; u < MAXBPL; ++u) {
+      if (u < bpl) {
+        int incl = cnt[u];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        run[u] = carry + incl - cnt[u];
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+      } else {
+        run[u] = 0;
+      }
+    }
+    uint16_t* gst = gst_all + (size_t)sl * JP;
+#pragma unroll
+    for (int u = 0; u < MAXBPL; ++u) {
+      const int j = lane + 32 * u;
+      if (u < bpl && j < J) gst[j] = (uint16_t)run[u];
+    }
+    for (int j = J + lane; j < JP; j += 32) gst[j] = (uint16_t)tn;
+    for (int c = 0; c < chunks; ++c) {
       const int s = c * 32 + lane;
       const unsigned amask = __ballot_sync(0xffffffffu, s < tn);
       const int key = s < tn ? (int)col[s] : 0;
-      unsigned b[KB];  // KB >= bits of every slot's J: higher key bits are 0
+      unsigned b[KB];
 #pragma unroll
       for (int i = 0; i < KB; ++i) b[i] = __ballot_sync(0xffffffffu, (key >> i) & 1);
       const unsigned peers = key_mask<KB>(b, key, amask);
@@ -304,14 +286,6 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
 #pragma unroll
       for (int u = 0; u < MAXBPL; ++u)
         if (u < bpl) run[u] += __popc(key_mask<KB>(b, lane + 32 * u, amask));
-    }
-  }
-  {  // bucket starts: the scanned count of (j, warp 0); start[J..] = tn
-    uint16_t* gst = reinterpret_cast<uint16_t*>(rec + bp.off_starts);
-    for (int i = tid; i < NS * JP; i += NT) {
-      const int sl = i / JP, j = i - sl * JP;
-      const int J = ch.m[smode[sl]].J;
-      gst[i] = (uint16_t)(j < J ? cw[((size_t)sl * JP + j) * NW] : tn);
     }
   }
   __syncthreads();
@@ -622,7 +596,8 @@ int bucket_threads() {
 }
 
 size_t prep_smem_bytes(int N, int T, int idx_bytes, int nsort, int jpad) {
-  return (size_t)N * T * idx_bytes + (size_t)nsort * T * 2 + (size_t)nsort * jpad * 16 * 4 + 16 * 4 + 256;
+  (void)jpad;
+  return (size_t)N * T * idx_bytes + (size_t)nsort * T * 2 + 256;
 }
 
 size_t compute_smem(int T, int RP, int N, int idx_bytes, int jpad) {
