@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(kThreads, 2) dot_r16_kernel(const __grid_const
   float* stA = reinterpret_cast<float*>(smem);                      // [kStages][CH*R*R]
   float* stB = stA + kStages * CH * R * R;                          // [kStages][CH*R*R]
   float* ybuf = stB + (args.norm ? 0 : kStages * CH * R * R);       // [kWarps][R*R]
-  float* red = ybuf + kWarps * R * R;                               // [kWarps][R*R]
+  float* red = ybuf + 2 * kWarps * R * R;                           // [kWarps][R*R]
   float* msm = red + kWarps * R * R;                                // [R*R]
   uint64_t* bars = reinterpret_cast<uint64_t*>(msm + R * R);        // full[kStages], empty[kStages]
   uint64_t* full = bars;
@@ -146,6 +146,7 @@ __global__ void __launch_bounds__(kThreads, 2) dot_r16_kernel(const __grid_const
     for (int k = 0; k < N; ++k) {
       const bool first = (k == 0), last = (k == N - 1);
       uint64_t mn[2][2] = {{0ull, 0ull}, {0ull, 0ull}};
+      uint64_t mn2[2][2] = {{0ull, 0ull}, {0ull, 0ull}};  // second slice of the pair
       float lastacc = 0.f;
       float4 mq0 = make_float4(0.f, 0.f, 0.f, 0.f), mq1 = mq0;  // M[2ap(+1)][4dq..]
       if (last && !first) {
@@ -185,35 +186,53 @@ __global__ void __launch_bounds__(kThreads, 2) dot_r16_kernel(const __grid_const
             y1 = fmaf(mq1.w, bv.w, y1);
             lastacc = fmaf(a0, y0, lastacc);
             lastacc = fmaf(a1, y1, lastacc);
-          } else {
-            // Y = M B_j : rows 2ap, 2ap+1, columns 4dq..4dq+3
-            const uint32_t bj = su32(Bm + jj * R * R);
-            uint64_t y[2][2] = {{0ull, 0ull}, {0ull, 0ull}};
+          } else if (jj < kWarps) {
+            // two slices per warp (jj, jj + kWarps): 8 independent FFMA2 chains
+            const int j2 = jj + kWarps;
+            const bool two = j2 < nj;
+            const uint32_t bj1 = su32(Bm + jj * R * R), bj2 = su32(Bm + (two ? j2 : jj) * R * R);
+            uint64_t y1[2][2] = {{0ull, 0ull}, {0ull, 0ull}}, y2[2][2] = {{0ull, 0ull}, {0ull, 0ull}};
 #pragma unroll
             for (int b = 0; b < R; ++b) {
-              uint64_t p0, p1;
-              lds128x2(bj + b * 64 + dq * 16, p0, p1);
-              ffma2(y[0][0], p0, mrow[0][b]);
-              ffma2(y[0][1], p1, mrow[0][b]);
-              ffma2(y[1][0], p0, mrow[1][b]);
-              ffma2(y[1][1], p1, mrow[1][b]);
+              uint64_t p0, p1, r0, r1;
+              lds128x2(bj1 + b * 64 + dq * 16, p0, p1);
+              lds128x2(bj2 + b * 64 + dq * 16, r0, r1);
+              ffma2(y1[0][0], p0, mrow[0][b]);
+              ffma2(y1[0][1], p1, mrow[0][b]);
+              ffma2(y1[1][0], p0, mrow[1][b]);
+              ffma2(y1[1][1], p1, mrow[1][b]);
+              ffma2(y2[0][0], r0, mrow[0][b]);
+              ffma2(y2[0][1], r1, mrow[0][b]);
+              ffma2(y2[1][0], r0, mrow[1][b]);
+              ffma2(y2[1][1], r1, mrow[1][b]);
             }
-            const uint32_t yw = su32(ybuf + warp * R * R);
-            sts128x2(yw + (2 * ap) * 64 + dq * 16, y[0][0], y[0][1]);
-            sts128x2(yw + (2 * ap + 1) * 64 + dq * 16, y[1][0], y[1][1]);
+            const uint32_t yw1 = su32(ybuf + (2 * warp) * R * R), yw2 = yw1 + R * R * 4;
+            sts128x2(yw1 + (2 * ap) * 64 + dq * 16, y1[0][0], y1[0][1]);
+            sts128x2(yw1 + (2 * ap + 1) * 64 + dq * 16, y1[1][0], y1[1][1]);
+            sts128x2(yw2 + (2 * ap) * 64 + dq * 16, y2[0][0], y2[0][1]);
+            sts128x2(yw2 + (2 * ap + 1) * 64 + dq * 16, y2[1][0], y2[1][1]);
             __syncwarp();
-            // Mw += A_j^T Y : rows c = 2ap, 2ap+1
-            const uint32_t aj = su32(A + jj * R * R);
+            // Mw += A_j^T Y_j for both slices (second slice masked by 'two')
+            const uint32_t aj1 = su32(A + jj * R * R), aj2 = su32(A + (two ? j2 : jj) * R * R);
+            const float w2 = two ? 1.f : 0.f;
 #pragma unroll
             for (int a = 0; a < R; ++a) {
-              uint64_t q0, q1;
-              lds128x2(yw + a * 64 + dq * 16, q0, q1);
-              float a0, a1;
-              unpack2(lds64(aj + a * 64 + ap * 8), a0, a1);
+              uint64_t q0, q1, t0, t1;
+              lds128x2(yw1 + a * 64 + dq * 16, q0, q1);
+              lds128x2(yw2 + a * 64 + dq * 16, t0, t1);
+              float a0, a1, c0, c1;
+              unpack2(lds64(aj1 + a * 64 + ap * 8), a0, a1);
+              unpack2(lds64(aj2 + a * 64 + ap * 8), c0, c1);
+              c0 *= w2;
+              c1 *= w2;
               ffma2(mn[0][0], q0, a0);
               ffma2(mn[0][1], q1, a0);
               ffma2(mn[1][0], q0, a1);
               ffma2(mn[1][1], q1, a1);
+              ffma2(mn2[0][0], t0, c0);
+              ffma2(mn2[0][1], t1, c0);
+              ffma2(mn2[1][0], t0, c1);
+              ffma2(mn2[1][1], t1, c1);
             }
             __syncwarp();
           }
@@ -239,9 +258,15 @@ __global__ void __launch_bounds__(kThreads, 2) dot_r16_kernel(const __grid_const
         float* rw = red + warp * R * R;
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-          float x0, x1, x2, x3;
+          float x0, x1, x2, x3, z0, z1, z2, z3;
           unpack2(mn[i][0], x0, x1);
           unpack2(mn[i][1], x2, x3);
+          unpack2(mn2[i][0], z0, z1);
+          unpack2(mn2[i][1], z2, z3);
+          x0 += z0;
+          x1 += z1;
+          x2 += z2;
+          x3 += z3;
           *reinterpret_cast<float4*>(rw + (2 * ap + i) * R + dq * 4) = make_float4(x0, x1, x2, x3);
         }
         __syncthreads();
@@ -264,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 2) dot_r16_kernel(const __grid_const
 
 size_t dot_smem(bool norm) {
   const size_t stage = (size_t)kStages * CH * R * R * 4;
-  return stage * (norm ? 1 : 2) + (size_t)(2 * kWarps * R * R + R * R) * 4 + 2 * kStages * 8 + 16;
+  return stage * (norm ? 1 : 2) + (size_t)(3 * kWarps * R * R + R * R) * 4 + 2 * kStages * 8 + 16;
 }
 
 bool chain_ok(const ChainDev& c) {
