@@ -392,6 +392,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
         if (N == 1) {  // [J][1][1]
           for (int s = tid; s < tn; s += NT) out[s0 + s] = __ldg(md.s + col[s]);
         } else if (rr == R) {  // state row = G_0[j][0][:] (16-byte copies)
+#pragma unroll 4
           for (int e = tid; e < tn * (R / 4); e += NT) {
             const int s = e / (R / 4), c4 = e - (e / (R / 4)) * (R / 4);
             const float4 g = __ldg(reinterpret_cast<const float4*>(md.s + (int64_t)col[s] * R) + c4);
@@ -410,22 +411,37 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
         }
       } else if (k == N - 1) {  // rr == 1: out = state . G[j][:, 0]
         if (rl == R) {
-          for (int s = tid; s < tn; s += NT) {
+          // two samples per thread per iteration: 2 x R/4 independent 16-byte
+          // loads of random core rows in flight (L2 latency bound otherwise)
+          for (int s = tid; s < tn; s += 2 * NT) {
+            const int s2 = s + NT;
+            const bool two = s2 < tn;
             const float4* g4 = reinterpret_cast<const float4*>(md.s + (int64_t)col[s] * R);
-            const uint32_t vrow = s_state + (uint32_t)s * (RP * 4);
-            float4 gv[R / 4];
+            const float4* h4 = reinterpret_cast<const float4*>(md.s + (int64_t)col[two ? s2 : s] * R);
+            float4 gv[R / 4], hv[R / 4];
 #pragma unroll
-            for (int a4 = 0; a4 < R / 4; ++a4) gv[a4] = __ldg(g4 + a4);
-            float acc0 = 0.f, acc1 = 0.f;
+            for (int a4 = 0; a4 < R / 4; ++a4) {
+              gv[a4] = __ldg(g4 + a4);
+              hv[a4] = __ldg(h4 + a4);
+            }
+            const uint32_t vrow = s_state + (uint32_t)s * (RP * 4);
+            const uint32_t wrow = s_state + (uint32_t)(two ? s2 : s) * (RP * 4);
+            float acc0 = 0.f, acc1 = 0.f, bcc0 = 0.f, bcc1 = 0.f;
 #pragma unroll
             for (int a4 = 0; a4 < R / 4; ++a4) {
               const float4 v = lds128(vrow + a4 * 16);
+              const float4 w = lds128(wrow + a4 * 16);
               acc0 = fmaf(v.x, gv[a4].x, acc0);
               acc1 = fmaf(v.y, gv[a4].y, acc1);
               acc0 = fmaf(v.z, gv[a4].z, acc0);
               acc1 = fmaf(v.w, gv[a4].w, acc1);
+              bcc0 = fmaf(w.x, hv[a4].x, bcc0);
+              bcc1 = fmaf(w.y, hv[a4].y, bcc1);
+              bcc0 = fmaf(w.z, hv[a4].z, bcc0);
+              bcc1 = fmaf(w.w, hv[a4].w, bcc1);
             }
             out[s0 + s] = acc0 + acc1;
+            if (two) out[s0 + s2] = bcc0 + bcc1;
           }
         } else {
           for (int s = tid; s < tn; s += NT) {
@@ -459,6 +475,11 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
             const int h = lane >> 4, qq = lane & 15;
             uint64_t g2[16];
             const float* gs = md.s + (int64_t)key * rl * rr;
+            if (bend < hi) {  // warm L1 with the next segment's slice (one line per lane)
+              const int nkey = col[perm[bend]];
+              const float* ngs = md.s + (int64_t)nkey * rl * rr;
+              if (lane * 32 < rl * rr) asm volatile("prefetch.global.L1 [%0];" ::"l"(ngs + lane * 32));
+            }
             if (rl == R && rr == R) {
 #pragma unroll
               for (int i = 0; i < 16; ++i) g2[i] = ldg_b64(gs + (16 * h + i) * R + 2 * qq);
