@@ -157,6 +157,7 @@ struct BPlan {
   int64_t tile_bytes;
   int64_t off_perm, off_starts;
   int8_t slot[kMaxModes];  // mode -> sorted slot or -1
+  int l1pf;                // prefetch the next segment's core slice into L1
 };
 
 // Warp-level multisplit: the lanes' keys are transposed into kbits ballots;
@@ -463,11 +464,12 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
         const uint16_t* st = startb + b * bp.jpad;
         const int lo = (int)(((int64_t)warp * tn) / nwarps);
         const int hi = (int)(((int64_t)(warp + 1) * tn) / nwarps);
+        if constexpr (R == 32) {
         int p = lo;
         while (p < hi) {
           const int key = col[perm[p]];
           const int bend = min((int)st[key + 1], hi);
-          if constexpr (R == 32) {
+          {
             // K-split geometry: lane (h, qq) owns rows 16h..16h+15 and the
             // column pair (2qq, 2qq+1); one sample per pass, the two row
             // halves are summed with one 64-bit shuffle.  Halves the core
@@ -475,7 +477,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
             const int h = lane >> 4, qq = lane & 15;
             uint64_t g2[16];
             const float* gs = md.s + (int64_t)key * rl * rr;
-            if (bend < hi) {  // warm L1 with the next segment's slice (one line per lane)
+            if (bp.l1pf && bend < hi) {  // warm L1 with the next segment's slice (one line per lane)
               const int nkey = col[perm[bend]];
               const float* ngs = md.s + (int64_t)nkey * rl * rr;
               if (lane * 32 < rl * rr) asm volatile("prefetch.global.L1 [%0];" ::"l"(ngs + lane * 32));
@@ -509,21 +511,33 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
               ks_passes<1, RP>(g2, perm, p, s_state, h, qq);
               p += 1;
             }
-          } else {
-            // core slice -> registers (see Geo for the column ownership)
-            constexpr int C1 = (C == 3) ? 1 : 0;
+          }
+        }
+        } else {
+          // Groups of L lanes work on DIFFERENT buckets (small buckets, e.g.
+          // J = 128): the warp range is split into G sub-ranges; per round
+          // every group loads one core slice (G loads share one latency) and
+          // streams that segment two samples per pass; groups that finish
+          // early idle until the round ends.
+          constexpr int C1 = (C == 3) ? 1 : 0;
+          const int glo = lo + ((hi - lo) * gi) / G, ghi = lo + ((hi - lo) * (gi + 1)) / G;
+          const int cp = 2 * q, cs = 16 + q;
+          int p = glo;
+          while (__any_sync(0xffffffffu, p < ghi)) {
+            const bool act = p < ghi;
+            const int key = act ? (int)col[perm[p]] : 0;
+            const int bend = act ? min((int)st[key + 1], ghi) : p;
             uint64_t g2[R];
             float g1[C1 ? R : 1];
             const float* gs = md.s + (int64_t)key * rl * rr;
-            const int cp = 2 * q, cs = 16 + q;
-            if (rl == R && rr == R) {  // full rank: unpredicated 8-byte loads
-  #pragma unroll
+            if (rl == R && rr == R) {
+#pragma unroll
               for (int a = 0; a < R; ++a) {
                 g2[a] = ldg_b64(gs + a * R + cp);
                 if constexpr (C1) g1[a] = __ldg(gs + a * R + cs);
               }
             } else {
-  #pragma unroll
+#pragma unroll
               for (int a = 0; a < R; ++a) {
                 const bool ra = a < rl;
                 const float x0 = (ra && cp < rr) ? __ldg(gs + a * rr + cp) : 0.f;
@@ -532,55 +546,51 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
                 if constexpr (C1) g1[a] = (ra && cs < rr) ? __ldg(gs + a * rr + cs) : 0.f;
               }
             }
-            while (p < bend) {
-              const int n = min(8, bend - p);
-              // empty slots of a ragged last iteration point at the dummy row T
-              uint32_t row[P];
-  #pragma unroll
-              for (int pi = 0; pi < P; ++pi) {
-                const int w = pi * G + gi;
-                const int sidx = (w < n) ? (int)perm[p + w] : T;
-                row[pi] = s_state + (uint32_t)sidx * (RP * 4);
+            int n = bend - p;  // this group's segment length; the round runs the warp max
+            int nmax = n;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
+            for (int it = 0; it < nmax; it += 2) {
+              uint32_t row[2];
+#pragma unroll
+              for (int pi = 0; pi < 2; ++pi) {
+                const int w = it + pi;
+                row[pi] = s_state + (uint32_t)((w < n) ? (int)perm[p + w] : T) * (RP * 4);
               }
-              uint64_t acc2[P];
-              float acc1[P];
-  #pragma unroll
-              for (int pi = 0; pi < P; ++pi) {
-                acc2[pi] = 0ull;
-                acc1[pi] = 0.f;
-              }
-  #pragma unroll
+              uint64_t acc2[2] = {0ull, 0ull};
+              float acc1[2] = {0.f, 0.f};
+#pragma unroll
               for (int a4 = 0; a4 < R / 4; ++a4) {
-                float4 v[P];
-  #pragma unroll
-                for (int pi = 0; pi < P; ++pi) v[pi] = lds128(row[pi] + a4 * 16);
-              #pragma unroll
-              for (int pi = 0; pi < P; ++pi) ffma2(acc2[pi], g2[a4 * 4 + 0], v[pi].x);
-              #pragma unroll
-              for (int pi = 0; pi < P; ++pi) ffma2(acc2[pi], g2[a4 * 4 + 1], v[pi].y);
-              #pragma unroll
-              for (int pi = 0; pi < P; ++pi) ffma2(acc2[pi], g2[a4 * 4 + 2], v[pi].z);
-              #pragma unroll
-              for (int pi = 0; pi < P; ++pi) ffma2(acc2[pi], g2[a4 * 4 + 3], v[pi].w);
-              if constexpr (C1) {
-              #pragma unroll
-                for (int pi = 0; pi < P; ++pi) {
-                  acc1[pi] = fmaf(v[pi].x, g1[a4 * 4 + 0], acc1[pi]);
-                  acc1[pi] = fmaf(v[pi].y, g1[a4 * 4 + 1], acc1[pi]);
-                  acc1[pi] = fmaf(v[pi].z, g1[a4 * 4 + 2], acc1[pi]);
-                  acc1[pi] = fmaf(v[pi].w, g1[a4 * 4 + 3], acc1[pi]);
+                float4 v[2];
+#pragma unroll
+                for (int pi = 0; pi < 2; ++pi) v[pi] = lds128(row[pi] + a4 * 16);
+#pragma unroll
+                for (int pi = 0; pi < 2; ++pi) ffma2(acc2[pi], g2[a4 * 4 + 0], v[pi].x);
+#pragma unroll
+                for (int pi = 0; pi < 2; ++pi) ffma2(acc2[pi], g2[a4 * 4 + 1], v[pi].y);
+#pragma unroll
+                for (int pi = 0; pi < 2; ++pi) ffma2(acc2[pi], g2[a4 * 4 + 2], v[pi].z);
+#pragma unroll
+                for (int pi = 0; pi < 2; ++pi) ffma2(acc2[pi], g2[a4 * 4 + 3], v[pi].w);
+                if constexpr (C1) {
+#pragma unroll
+                  for (int pi = 0; pi < 2; ++pi) {
+                    acc1[pi] = fmaf(v[pi].x, g1[a4 * 4 + 0], acc1[pi]);
+                    acc1[pi] = fmaf(v[pi].y, g1[a4 * 4 + 1], acc1[pi]);
+                    acc1[pi] = fmaf(v[pi].z, g1[a4 * 4 + 2], acc1[pi]);
+                    acc1[pi] = fmaf(v[pi].w, g1[a4 * 4 + 3], acc1[pi]);
+                  }
                 }
               }
-              }
               __syncwarp();  // every lane of a group has read its sample's row
-  #pragma unroll
-              for (int pi = 0; pi < P; ++pi) {
+#pragma unroll
+              for (int pi = 0; pi < 2; ++pi) {
                 sts_b64(row[pi] + cp * 4, acc2[pi]);
                 if constexpr (C1) sts32(row[pi] + cs * 4, acc1[pi]);
               }
               __syncwarp();
-  p += n;
             }
+            p = bend;
           }
         }
       }
@@ -654,6 +664,10 @@ int make_bplan(const ChainDev& ch, int64_t m, BPlan* bp, int* R_out, int* nt_out
   if (compute_smem(T, RP, ch.n, idx_bytes, jpad) > budget || prep_smem(T) > 232448 - 1024)
     return set_error(TNB_EINVAL, "bucketed: chain too long for smem");
   bp->T = T;
+  {
+    const char* e = getenv("TNB_L1PF");
+    bp->l1pf = (e && e[0] == '0') ? 0 : 1;
+  }
   bp->nsort = nsort;
   bp->jpad = jpad;
   bp->idx_bytes = idx_bytes;
