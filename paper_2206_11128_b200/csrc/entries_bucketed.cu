@@ -158,6 +158,7 @@ struct BPlan {
   int64_t off_perm, off_starts;
   int8_t slot[kMaxModes];  // mode -> sorted slot or -1
   int l1pf;                // prefetch the next segment's core slice into L1
+  int rounds;              // R <= 24: groups of one warp on different buckets
 };
 
 // Warp-level multisplit: the lanes' keys are transposed into kbits ballots;
@@ -389,6 +390,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
       const IdxT* col = cidx + (size_t)k * T;
       const int rl = md.rl, rr = md.rr;
       bool sorted = false;
+      int k2 = k;  // last mode handled by this iteration (diagonal runs)
       if (k == 0) {
         if (N == 1) {  // [J][1][1]
           for (int s = tid; s < tn; s += NT) out[s0 + s] = __ldg(md.s + col[s]);
@@ -406,9 +408,34 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
           }
         }
       } else if (md.layout == TNB_LAYOUT_DIAG) {
-        for (int e = tid; e < tn * R; e += NT) {
-          const int s = e / R, c = e - (e / R) * R;
-          if (c < rl) state[s * RP + c] *= __ldg(md.s + (int64_t)col[s] * rl + c);
+        // a run of consecutive interior CP modes is one elementwise product:
+        // v[c] *= D_k[j_k][c] * D_k+1[j_k+1][c] * ..., done in ONE pass over
+        // the state (16-byte rows when the rank allows)
+        while (k2 + 1 < N - 1 && ch.m[k2 + 1].layout == TNB_LAYOUT_DIAG) ++k2;
+        if ((rl & 3) == 0) {
+          const int q4 = rl >> 2;
+#pragma unroll 2
+          for (int e = tid; e < tn * q4; e += NT) {
+            const int s = e / q4, c4 = e - (e / q4) * q4;
+            float4 f = *reinterpret_cast<const float4*>(state + s * RP + c4 * 4);
+            for (int kk = k; kk <= k2; ++kk) {
+              const ModeDev& mk = ch.m[kk];
+              const float4 d = __ldg(reinterpret_cast<const float4*>(mk.s + (int64_t)cidx[(size_t)kk * T + s] * rl) + c4);
+              f.x *= d.x;
+              f.y *= d.y;
+              f.z *= d.z;
+              f.w *= d.w;
+            }
+            *reinterpret_cast<float4*>(state + s * RP + c4 * 4) = f;
+          }
+        } else {
+          for (int e = tid; e < tn * rl; e += NT) {
+            const int s = e / rl, c = e - (e / rl) * rl;
+            float f = state[s * RP + c];
+            for (int kk = k; kk <= k2; ++kk)
+              f *= __ldg(ch.m[kk].s + (int64_t)cidx[(size_t)kk * T + s] * rl + c);
+            state[s * RP + c] = f;
+          }
         }
       } else if (k == N - 1) {  // rr == 1: out = state . G[j][:, 0]
         if (rl == R) {
@@ -514,6 +541,85 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
           }
         }
         } else {
+          if (!bp.rounds) {
+          // one bucket per warp at a time: all G groups take samples of it
+          int p = lo;
+          while (p < hi) {
+            const int key = col[perm[p]];
+            const int bend = min((int)st[key + 1], hi);
+            // core slice -> registers (see Geo for the column ownership)
+            constexpr int C1 = (C == 3) ? 1 : 0;
+            uint64_t g2[R];
+            float g1[C1 ? R : 1];
+            const float* gs = md.s + (int64_t)key * rl * rr;
+            const int cp = 2 * q, cs = 16 + q;
+            if (rl == R && rr == R) {  // full rank: unpredicated 8-byte loads
+  #pragma unroll
+              for (int a = 0; a < R; ++a) {
+                g2[a] = ldg_b64(gs + a * R + cp);
+                if constexpr (C1) g1[a] = __ldg(gs + a * R + cs);
+              }
+            } else {
+  #pragma unroll
+              for (int a = 0; a < R; ++a) {
+                const bool ra = a < rl;
+                const float x0 = (ra && cp < rr) ? __ldg(gs + a * rr + cp) : 0.f;
+                const float x1 = (ra && cp + 1 < rr) ? __ldg(gs + a * rr + cp + 1) : 0.f;
+                g2[a] = pack2(x0, x1);
+                if constexpr (C1) g1[a] = (ra && cs < rr) ? __ldg(gs + a * rr + cs) : 0.f;
+              }
+            }
+            while (p < bend) {
+              const int n = min(8, bend - p);
+              // empty slots of a ragged last iteration point at the dummy row T
+              uint32_t row[P];
+  #pragma unroll
+              for (int pi = 0; pi < P; ++pi) {
+                const int w = pi * G + gi;
+                const int sidx = (w < n) ? (int)perm[p + w] : T;
+                row[pi] = s_state + (uint32_t)sidx * (RP * 4);
+              }
+              uint64_t acc2[P];
+              float acc1[P];
+  #pragma unroll
+              for (int pi = 0; pi < P; ++pi) {
+                acc2[pi] = 0ull;
+                acc1[pi] = 0.f;
+              }
+  #pragma unroll
+              for (int a4 = 0; a4 < R / 4; ++a4) {
+                float4 v[P];
+  #pragma unroll
+                for (int pi = 0; pi < P; ++pi) v[pi] = lds128(row[pi] + a4 * 16);
+              #pragma unroll
+              for (int pi = 0; pi < P; ++pi) ffma2(acc2[pi], g2[a4 * 4 + 0], v[pi].x);
+              #pragma unroll
+              for (int pi = 0; pi < P; ++pi) ffma2(acc2[pi], g2[a4 * 4 + 1], v[pi].y);
+              #pragma unroll
+              for (int pi = 0; pi < P; ++pi) ffma2(acc2[pi], g2[a4 * 4 + 2], v[pi].z);
+              #pragma unroll
+              for (int pi = 0; pi < P; ++pi) ffma2(acc2[pi], g2[a4 * 4 + 3], v[pi].w);
+              if constexpr (C1) {
+              #pragma unroll
+                for (int pi = 0; pi < P; ++pi) {
+                  acc1[pi] = fmaf(v[pi].x, g1[a4 * 4 + 0], acc1[pi]);
+                  acc1[pi] = fmaf(v[pi].y, g1[a4 * 4 + 1], acc1[pi]);
+                  acc1[pi] = fmaf(v[pi].z, g1[a4 * 4 + 2], acc1[pi]);
+                  acc1[pi] = fmaf(v[pi].w, g1[a4 * 4 + 3], acc1[pi]);
+                }
+              }
+              }
+              __syncwarp();  // every lane of a group has read its sample's row
+  #pragma unroll
+              for (int pi = 0; pi < P; ++pi) {
+                sts_b64(row[pi] + cp * 4, acc2[pi]);
+                if constexpr (C1) sts32(row[pi] + cs * 4, acc1[pi]);
+              }
+              __syncwarp();
+  p += n;
+            }
+          }
+          } else {
           // Groups of L lanes work on DIFFERENT buckets (small buckets, e.g.
           // J = 128): the warp range is split into G sub-ranges; per round
           // every group loads one core slice (G loads share one latency) and
@@ -592,18 +698,21 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
             }
             p = bend;
           }
+          }
         }
       }
       __syncthreads();
       if (tid == 0) {
-        // cidx row k of this tile is dead: prefetch the next tile's row k
+        // cidx rows k..k2 of this tile are dead: prefetch the next tile's rows
         if (ntile < ntiles) {
           if (k == 0) mb_expect(cbar, row_bytes * N);
-          bulk(cidx + (size_t)k * T, ws + ntile * bp.tile_bytes + (size_t)k * row_bytes, row_bytes, cbar);
+          for (int kk = k; kk <= k2; ++kk)
+            bulk(cidx + (size_t)kk * T, ws + ntile * bp.tile_bytes + (size_t)kk * row_bytes, row_bytes, cbar);
         }
         if (sorted) issue_slot(item + 2);  // this slot buffer is free again
       }
       if (sorted) ++item;
+      k = k2;
     }
   }
 }
@@ -666,7 +775,9 @@ int make_bplan(const ChainDev& ch, int64_t m, BPlan* bp, int* R_out, int* nt_out
   bp->T = T;
   {
     const char* e = getenv("TNB_L1PF");
-    bp->l1pf = (e && e[0] == '0') ? 0 : 1;
+    bp->l1pf = (e && e[0] == '1') ? 1 : 0;
+    const char* r = getenv("TNB_ROUNDS");
+    bp->rounds = (r && r[0] == '1') ? 1 : 0;
   }
   bp->nsort = nsort;
   bp->jpad = jpad;
