@@ -410,9 +410,54 @@ def _index_tensor(t: TnTensor, indices, device) -> torch.Tensor:
     return idx.to(device=device, dtype=torch.int64).contiguous()
 
 
+# host index matrices at least this long are streamed in chunks (H2D of
+# chunk i+1 overlaps the kernels of chunk i)
+_PIPELINE_ROWS = 1 << 21
+
+
+def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: int) -> torch.Tensor:
+    """entries() for a large PINNED int64 host index matrix: chunked
+    copy-stream H2D overlapped with the K1 launches on the compute stream."""
+    dev = p.device
+    m = int(idx_host.shape[0])
+    out = torch.empty(m, dtype=torch.float32, device=dev)
+    comp = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    chunk = _PIPELINE_ROWS
+    nch = (m + chunk - 1) // chunk
+    errs = torch.empty(nch, dtype=torch.int32, device=dev)
+    bufs = [torch.empty((min(chunk, m), t.ndim), dtype=torch.int64, device=dev) for _ in range(2)]
+    done = [torch.cuda.Event() for _ in range(2)]  # compute finished with buffer b
+    ws = None
+    copy.wait_stream(comp)
+    for c in range(nch):
+        lo, hi = c * chunk, min(m, (c + 1) * chunk)
+        b = c & 1
+        buf = bufs[b][: hi - lo]
+        with torch.cuda.stream(copy):
+            if c >= 2:
+                copy.wait_event(done[b])
+            buf.copy_(idx_host[lo:hi], non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(copy)
+        comp.wait_event(ready)
+        buf.record_stream(comp)
+        ws = launch_entries(p, buf, out[lo:hi], errs[c:c + 1], algo, ws)
+        done[b].record(comp)
+    code = int(errs.min().item())
+    if code < t.ndim:
+        raise ContractViolationError(f"index out of bounds on mode {code}")
+    return out
+
+
 def entries(t: TnTensor, indices, *, algo: int = N.ALGO_AUTO) -> torch.Tensor:
     """Values at explicit multi-indices: shape (M,), or (M, B) if batched."""
     p = t._packed()
+    if (isinstance(indices, torch.Tensor) and indices.device.type == "cpu" and indices.is_pinned()
+            and indices.dtype == torch.int64 and indices.dim() == 2 and indices.shape[1] == t.ndim
+            and indices.is_contiguous() and indices.shape[0] >= 2 * _PIPELINE_ROWS
+            and t.batch_size is None):
+        return _entries_pipelined(t, p, indices, algo)
     idx = _index_tensor(t, indices, p.device)
     m = int(idx.shape[0])
     b = t.batch_size

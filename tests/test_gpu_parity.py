@@ -254,3 +254,35 @@ def test_dot_rank16_fast_and_generic(generic, monkeypatch):
     a1 = O.random_tt((16,) * 3, 16, seed=5, scale=0.25)
     t1, o1 = facade([("tt", c, None) for c in a1]), O.make_chain([("tt", c) for c in a1])
     assert abs(tb.norm(t1) - O.norm(o1)) <= 1e-5 * O.norm(o1)
+
+
+def test_pipelined_host_indices_match_device_path():
+    # a large pinned int64 host matrix takes the chunked copy/compute pipeline;
+    # per-sample results do not depend on chunking or tiling (bitwise equal)
+    from paper_2206_11128_b200 import core as C
+
+    cores = O.random_tt((32,) * 6, 16, seed=11, scale=0.25)
+    t = facade([("tt", c, None) for c in cores])
+    m = 2 * C._PIPELINE_ROWS + 12345
+    idx = torch.from_numpy(O.uniform_indices((32,) * 6, m, 3)).pin_memory()
+    got = tb.entries(t, idx)
+    ref = tb.entries(t, idx.cuda())
+    assert torch.equal(got, ref)
+    o = O.make_chain([("tt", c) for c in cores])
+    sel = np.arange(0, m, 997)
+    assert_close(to_np(got)[sel], O.entries(o, idx.numpy()[sel]))
+    bad = idx.clone()
+    bad[m - 5, 4] = 40
+    with pytest.raises(tb.ContractViolationError, match="mode 4"):
+        tb.entries(t, bad.pin_memory())
+
+
+@pytest.mark.parametrize("rounds", ["0", "1"])
+def test_bucketed_group_variants(rounds, monkeypatch):
+    # both R<=24 work distributions (one bucket per warp / per lane group)
+    monkeypatch.setenv("TNB_ROUNDS", rounds)
+    nodes = O.cfg5_nodes(seed=1)
+    t = facade(nodes)
+    o = O.make_chain(nodes)
+    idx = O.uniform_indices((128,) * 8, 70000, 9)
+    assert_close(tb.entries(t, idx, algo=N.ALGO_BUCKETED), O.entries(o, idx))
