@@ -429,6 +429,9 @@ def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: in
     bufs = [torch.empty((min(chunk, m), t.ndim), dtype=torch.int64, device=dev) for _ in range(2)]
     done = [torch.cuda.Event() for _ in range(2)]  # compute finished with buffer b
     ws = None
+    if algo == N.ALGO_AUTO and N.load().tnb_entries_workspace_bytes(
+            ctypes.byref(p.chain), chunk, N.ALGO_BUCKETED) > 0:
+        algo = N.ALGO_BUCKETED  # one kernel for every chunk, even a short last one
     copy.wait_stream(comp)
     for c in range(nch):
         lo, hi = c * chunk, min(m, (c + 1) * chunk)

@@ -59,6 +59,33 @@ __global__ void __launch_bounds__(256) ffma2_kernel(float* out, float s) {
   if (r == 12345.f) out[0] = r;
 }
 
+// legacy warp-level tensor-core MMA (mma.sync m16n8k8 tf32 -> HMMA on sm_100)
+__global__ void __launch_bounds__(256) hmma_tf32_kernel(float* out, int iters) {
+  uint32_t a[4], b[2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) a[i] = __float_as_uint(1.0f + threadIdx.x * 1e-3f + i);
+  b[0] = __float_as_uint(0.5f);
+  b[1] = __float_as_uint(0.25f);
+  float c[8][4];
+#pragma unroll
+  for (int t = 0; t < 8; ++t)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) c[t][i] = 0.f;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t)
+      asm volatile(
+          "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+          "{%0, %1, %2, %3};"
+          : "+f"(c[t][0]), "+f"(c[t][1]), "+f"(c[t][2]), "+f"(c[t][3])
+          : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+  }
+  float r = 0.f;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) r += c[t][0] + c[t][1] + c[t][2] + c[t][3];
+  if (r == 12345.f) out[0] = r;
+}
+
 __global__ void write_kernel(float4* __restrict__ p, int64_t n) {
   const float4 v = make_float4(1.f, 2.f, 3.f, 4.f);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -114,6 +141,10 @@ int main() {
   float ms_ffma_r = best_ms([&] { ffma_kernel<true><<<blocks, threads>>>(d_out, 0.999f); }, 10);
   float ms_ffma2 = best_ms([&] { ffma2_kernel<<<blocks, threads>>>(d_out, 0.999f); }, 10);
   CK(cudaGetLastError());
+  const int hm_iters = 2048;
+  float ms_hmma = best_ms([&] { hmma_tf32_kernel<<<blocks, threads>>>(d_out, hm_iters); }, 10);
+  const double hmma_flops = (double)blocks * (threads / 32) * hm_iters * 8 * (2.0 * 16 * 8 * 8);
+  CK(cudaGetLastError());
   const int64_t bytes = 8LL << 30;  // 8 GiB, far above L2
   float4 *a, *b;
   CK(cudaMalloc(&a, bytes));
@@ -125,12 +156,12 @@ int main() {
   float ms_c = best_ms([&] { copy_kernel<<<bw_blocks, 512>>>(a, b, n); }, 8);
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
-  printf("{\"fp32_ffma_tflops\": %.2f, \"fp32_ffma_3reg_tflops\": %.2f, \"fp32_ffma2_tflops\": %.2f, \"hbm_write_gbs\": %.1f, "
+  printf("{\"fp32_ffma_tflops\": %.2f, \"fp32_ffma_3reg_tflops\": %.2f, \"fp32_ffma2_tflops\": %.2f, \"hmma_tf32_mma_sync_tflops\": %.2f, \"hbm_write_gbs\": %.1f, "
          "\"hbm_read_gbs\": %.1f, \"hbm_copy_gbs\": %.1f, \"sms\": %d, "
          "\"how\": \"best of 10 (ffma: %d blocks x 256 thr x 16 chains x %d iters) / best of 8 over 8 GiB "
          "(write __stcs float4, read __ldcs float4, copy counts read+write)\"}\n",
          2 * fmas / (ms_ffma * 1e-3) / 1e12, 2 * fmas / (ms_ffma_r * 1e-3) / 1e12, 2 * fmas / (ms_ffma2 * 1e-3) / 1e12,
-         bytes / (ms_w * 1e-3) / 1e9, bytes / (ms_r * 1e-3) / 1e9, 2.0 * bytes / (ms_c * 1e-3) / 1e9,
+         hmma_flops / (ms_hmma * 1e-3) / 1e12, bytes / (ms_w * 1e-3) / 1e9, bytes / (ms_r * 1e-3) / 1e9, 2.0 * bytes / (ms_c * 1e-3) / 1e9,
          sms, blocks, kIters);
   return 0;
 }
