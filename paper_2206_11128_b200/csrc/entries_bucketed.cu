@@ -385,6 +385,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
     const int64_t ntile = tile + gridDim.x;
     mb_wait(cbar, c_it & 1);
     ++c_it;
+    int fold = -1;  // first CP mode of a diagonal run folded into the last mode
     for (int k = 0; k < N; ++k) {
       const ModeDev& md = ch.m[k];
       const IdxT* col = cidx + (size_t)k * T;
@@ -412,7 +413,9 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
         // v[c] *= D_k[j_k][c] * D_k+1[j_k+1][c] * ..., done in ONE pass over
         // the state (16-byte rows when the rank allows)
         while (k2 + 1 < N - 1 && ch.m[k2 + 1].layout == TNB_LAYOUT_DIAG) ++k2;
-        if ((rl & 3) == 0) {
+        if (k2 == N - 2 && ch.m[N - 1].rl == R && ch.m[N - 1].rr == 1 && (R & 3) == 0) {
+          fold = k;  // the last mode multiplies these rows in (no state pass)
+        } else if ((rl & 3) == 0) {
           const int q4 = rl >> 2;
 #pragma unroll 2
           for (int e = tid; e < tn * q4; e += NT) {
@@ -438,7 +441,37 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
           }
         }
       } else if (k == N - 1) {  // rr == 1: out = state . G[j][:, 0]
-        if (rl == R) {
+        if (rl == R && fold >= 0) {
+          // out = sum_a v[a] * prod_{folded CP modes} D_kk[j][a] * G[j][a]
+          for (int s = tid; s < tn; s += NT) {
+            float4 gv[R / 4];
+            const float4* g4 = reinterpret_cast<const float4*>(md.s + (int64_t)col[s] * R);
+#pragma unroll
+            for (int a4 = 0; a4 < R / 4; ++a4) gv[a4] = __ldg(g4 + a4);
+            for (int kk = fold; kk < N - 1; ++kk) {
+              const float4* d4 = reinterpret_cast<const float4*>(ch.m[kk].s + (int64_t)cidx[(size_t)kk * T + s] * R);
+#pragma unroll
+              for (int a4 = 0; a4 < R / 4; ++a4) {
+                const float4 d = __ldg(d4 + a4);
+                gv[a4].x *= d.x;
+                gv[a4].y *= d.y;
+                gv[a4].z *= d.z;
+                gv[a4].w *= d.w;
+              }
+            }
+            const uint32_t vrow = s_state + (uint32_t)s * (RP * 4);
+            float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+            for (int a4 = 0; a4 < R / 4; ++a4) {
+              const float4 v = lds128(vrow + a4 * 16);
+              acc0 = fmaf(v.x, gv[a4].x, acc0);
+              acc1 = fmaf(v.y, gv[a4].y, acc1);
+              acc0 = fmaf(v.z, gv[a4].z, acc0);
+              acc1 = fmaf(v.w, gv[a4].w, acc1);
+            }
+            out[s0 + s] = acc0 + acc1;
+          }
+        } else if (rl == R) {
           // two samples per thread per iteration: 2 x R/4 independent 16-byte
           // loads of random core rows in flight (L2 latency bound otherwise)
           for (int s = tid; s < tn; s += 2 * NT) {
@@ -706,8 +739,11 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
         // cidx rows k..k2 of this tile are dead: prefetch the next tile's rows
         if (ntile < ntiles) {
           if (k == 0) mb_expect(cbar, row_bytes * N);
-          for (int kk = k; kk <= k2; ++kk)
-            bulk(cidx + (size_t)kk * T, ws + ntile * bp.tile_bytes + (size_t)kk * row_bytes, row_bytes, cbar);
+          // rows of a folded diagonal run stay live until the last mode
+          const int klo = (k == N - 1 && fold >= 0) ? fold : k;
+          if (!(fold >= 0 && k >= fold && k < N - 1))
+            for (int kk = klo; kk <= k2; ++kk)
+              bulk(cidx + (size_t)kk * T, ws + ntile * bp.tile_bytes + (size_t)kk * row_bytes, row_bytes, cbar);
         }
         if (sorted) issue_slot(item + 2);  // this slot buffer is free again
       }
