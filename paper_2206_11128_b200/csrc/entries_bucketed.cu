@@ -321,7 +321,10 @@ __device__ __forceinline__ void bulk(void* dst, const void* src, uint32_t bytes,
       : "memory");
 }
 
-template <int R, typename IdxT, int NT>
+// FOLD: the chain ends in interior CP modes followed by the last mode; that
+// run is folded into the last-mode dot product (separate instantiation so
+// chains without it keep the leaner register allocation)
+template <int R, typename IdxT, int NT, bool FOLD>
 __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
     entries_compute_kernel(const __grid_constant__ ChainDev ch, const __grid_constant__ BPlan bp,
                            const unsigned char* __restrict__ ws, int64_t m, float* __restrict__ out) {
@@ -413,7 +416,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
         // v[c] *= D_k[j_k][c] * D_k+1[j_k+1][c] * ..., done in ONE pass over
         // the state (16-byte rows when the rank allows)
         while (k2 + 1 < N - 1 && ch.m[k2 + 1].layout == TNB_LAYOUT_DIAG) ++k2;
-        if (k2 == N - 2 && ch.m[N - 1].rl == R && ch.m[N - 1].rr == 1 && (R & 3) == 0) {
+        if (FOLD && k2 == N - 2 && ch.m[N - 1].rl == R && ch.m[N - 1].rr == 1 && (R & 3) == 0) {
           fold = k;  // the last mode multiplies these rows in (no state pass)
         } else if ((rl & 3) == 0) {
           const int q4 = rl >> 2;
@@ -441,7 +444,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
           }
         }
       } else if (k == N - 1) {  // rr == 1: out = state . G[j][:, 0]
-        if (rl == R && fold >= 0) {
+        if (FOLD && rl == R && fold >= 0) {
           // out = sum_a v[a] * prod_{folded CP modes} D_kk[j][a] * G[j][a]
           for (int s = tid; s < tn; s += NT) {
             float4 gv[R / 4];
@@ -740,8 +743,8 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
         if (ntile < ntiles) {
           if (k == 0) mb_expect(cbar, row_bytes * N);
           // rows of a folded diagonal run stay live until the last mode
-          const int klo = (k == N - 1 && fold >= 0) ? fold : k;
-          if (!(fold >= 0 && k >= fold && k < N - 1))
+          const int klo = (FOLD && k == N - 1 && fold >= 0) ? fold : k;
+          if (!(FOLD && fold >= 0 && k >= fold && k < N - 1))
             for (int kk = klo; kk <= k2; ++kk)
               bulk(cidx + (size_t)kk * T, ws + ntile * bp.tile_bytes + (size_t)kk * row_bytes, row_bytes, cbar);
         }
@@ -828,7 +831,7 @@ int make_bplan(const ChainDev& ch, int64_t m, BPlan* bp, int* R_out, int* nt_out
   return TNB_OK;
 }
 
-template <int R, typename IdxT, int NT>
+template <int R, typename IdxT, int NT, bool FOLD>
 int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m, float* out,
               int32_t* err, unsigned char* ws, cudaStream_t st) {
   // prep: one CTA per tile
@@ -848,7 +851,7 @@ int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m
   rc = check_launch("entries_prep");
   if (rc) return rc;
   const size_t csmem = compute_smem(bp.T, R + 4, ch.n, (int)sizeof(IdxT), bp.jpad);
-  auto ck = entries_compute_kernel<R, IdxT, NT>;
+  auto ck = entries_compute_kernel<R, IdxT, NT, FOLD>;
   rc = check_cuda(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem),
                   "compute smem attr");
   if (rc) return rc;
@@ -861,10 +864,14 @@ int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m
 template <int R, typename IdxT>
 int launch_ri(const ChainDev& ch, const BPlan& bp, int nt, const int64_t* idx, int64_t m, float* out,
               int32_t* err, unsigned char* ws, cudaStream_t st) {
-  if (nt == 256) return launch_rt<R, IdxT, 256>(ch, bp, idx, m, out, err, ws, st);
-  if (nt == 640) return launch_rt<R, IdxT, 640>(ch, bp, idx, m, out, err, ws, st);
-  if (nt == 768) return launch_rt<R, IdxT, 768>(ch, bp, idx, m, out, err, ws, st);
-  return launch_rt<R, IdxT, 512>(ch, bp, idx, m, out, err, ws, st);
+  const int N = ch.n;
+  const bool fold = (R & 3) == 0 && N >= 3 && ch.m[N - 2].layout == TNB_LAYOUT_DIAG && ch.m[N - 1].rl == R &&
+                    ch.m[N - 1].rr == 1;
+  if (fold) return launch_rt<R, IdxT, 512, true>(ch, bp, idx, m, out, err, ws, st);
+  if (nt == 256) return launch_rt<R, IdxT, 256, false>(ch, bp, idx, m, out, err, ws, st);
+  if (nt == 640) return launch_rt<R, IdxT, 640, false>(ch, bp, idx, m, out, err, ws, st);
+  if (nt == 768) return launch_rt<R, IdxT, 768, false>(ch, bp, idx, m, out, err, ws, st);
+  return launch_rt<R, IdxT, 512, false>(ch, bp, idx, m, out, err, ws, st);
 }
 
 }  // namespace
