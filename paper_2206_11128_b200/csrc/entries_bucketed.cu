@@ -129,12 +129,24 @@ __device__ __forceinline__ void ks_passes(const uint64_t (&g2)[16], const uint16
 #pragma unroll
     for (int pi = 0; pi < NP; ++pi) ffma2(acc2[pi], g2[a4 * 4 + 3], v[pi].w);
   }
+  if constexpr (NP == 1) {
+    acc2[0] = add2(acc2[0], __shfl_xor_sync(0xffffffffu, acc2[0], 16));
+    __syncwarp();  // every lane has read its rows
+    if (h == 0) sts_b64(rowb[0] + qq * 8, acc2[0]);
+  } else {
+    // sample pair (2i, 2i+1): half h finishes sample 2i+h, so each lane sends
+    // the partial its partner finishes -- one 64-bit shuffle per pair
+    uint64_t res[NP / 2];
 #pragma unroll
-  for (int pi = 0; pi < NP; ++pi) acc2[pi] = add2(acc2[pi], __shfl_xor_sync(0xffffffffu, acc2[pi], 16));
-  __syncwarp();  // every lane has read its rows
+    for (int i = 0; i < NP / 2; ++i) {
+      const uint64_t keep = h ? acc2[2 * i + 1] : acc2[2 * i];
+      const uint64_t send = h ? acc2[2 * i] : acc2[2 * i + 1];
+      res[i] = add2(keep, __shfl_xor_sync(0xffffffffu, send, 16));
+    }
+    __syncwarp();  // every lane has read its rows
 #pragma unroll
-  for (int pi = 0; pi < NP; ++pi)
-    if ((pi & 1) == (NP > 1 ? h : 0)) sts_b64(rowb[pi] + qq * 8, acc2[pi]);
+    for (int i = 0; i < NP / 2; ++i) sts_b64((h ? rowb[2 * i + 1] : rowb[2 * i]) + qq * 8, res[i]);
+  }
   __syncwarp();
 }
 
@@ -444,68 +456,76 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
           }
         }
       } else if (k == N - 1) {  // rr == 1: out = state . G[j][:, 0]
-        if (FOLD && rl == R && fold >= 0) {
-          // out = sum_a v[a] * prod_{folded CP modes} D_kk[j][a] * G[j][a]
-          for (int s = tid; s < tn; s += NT) {
-            float4 gv[R / 4];
-            const float4* g4 = reinterpret_cast<const float4*>(md.s + (int64_t)col[s] * R);
+        if (rl == R) {
+          // groups of GS lanes per sample, lane c owns the 16-byte chunk c of
+          // the random core row (one L1 line per group instead of one per
+          // lane); folded CP rows multiply in before the dot; 2 samples per
+          // group in flight
+          constexpr int CH = R / 4;
+          constexpr int GS = CH <= 2 ? 2 : (CH <= 4 ? 4 : 8);
+          constexpr int SPW = 32 / GS;
+          const int c = lane % GS, g = lane / GS;
+          const int cc = c < CH ? c : 0;  // idle lanes (R = 24) re-read chunk 0
+          const int kf = (FOLD && fold >= 0) ? fold : N - 1;
+          const int nf = N - 1 - kf;  // folded CP modes
+          for (int base = warp * (2 * SPW); base < tn; base += nwarps * 2 * SPW) {
+            // every load of both samples is issued before any use
+            constexpr int MF = FOLD ? 4 : 1;
+            float4 gv[2], v[2], dv[2][MF];
+            bool act[2];
 #pragma unroll
-            for (int a4 = 0; a4 < R / 4; ++a4) gv[a4] = __ldg(g4 + a4);
-            for (int kk = fold; kk < N - 1; ++kk) {
-              const float4* d4 = reinterpret_cast<const float4*>(ch.m[kk].s + (int64_t)cidx[(size_t)kk * T + s] * R);
+            for (int u = 0; u < 2; ++u) {
+              const int s = base + u * SPW + g;
+              act[u] = s < tn && c < CH;
+              const int sc = act[u] ? s : 0;
+              gv[u] = __ldg(reinterpret_cast<const float4*>(md.s + (int64_t)col[sc] * R) + cc);
+              if constexpr (FOLD) {
 #pragma unroll
-              for (int a4 = 0; a4 < R / 4; ++a4) {
-                const float4 d = __ldg(d4 + a4);
-                gv[a4].x *= d.x;
-                gv[a4].y *= d.y;
-                gv[a4].z *= d.z;
-                gv[a4].w *= d.w;
+                for (int i = 0; i < MF; ++i)
+                  dv[u][i] = (i < nf) ? __ldg(reinterpret_cast<const float4*>(
+                                            ch.m[kf + i].s + (int64_t)cidx[(size_t)(kf + i) * T + sc] * R) + cc)
+                                      : make_float4(1.f, 1.f, 1.f, 1.f);  // x * 1 is exact
               }
+              v[u] = lds128(s_state + (uint32_t)sc * (RP * 4) + cc * 16);
             }
-            const uint32_t vrow = s_state + (uint32_t)s * (RP * 4);
-            float acc0 = 0.f, acc1 = 0.f;
+            float part[2];
 #pragma unroll
-            for (int a4 = 0; a4 < R / 4; ++a4) {
-              const float4 v = lds128(vrow + a4 * 16);
-              acc0 = fmaf(v.x, gv[a4].x, acc0);
-              acc1 = fmaf(v.y, gv[a4].y, acc1);
-              acc0 = fmaf(v.z, gv[a4].z, acc0);
-              acc1 = fmaf(v.w, gv[a4].w, acc1);
-            }
-            out[s0 + s] = acc0 + acc1;
-          }
-        } else if (rl == R) {
-          // two samples per thread per iteration: 2 x R/4 independent 16-byte
-          // loads of random core rows in flight (L2 latency bound otherwise)
-          for (int s = tid; s < tn; s += 2 * NT) {
-            const int s2 = s + NT;
-            const bool two = s2 < tn;
-            const float4* g4 = reinterpret_cast<const float4*>(md.s + (int64_t)col[s] * R);
-            const float4* h4 = reinterpret_cast<const float4*>(md.s + (int64_t)col[two ? s2 : s] * R);
-            float4 gv[R / 4], hv[R / 4];
+            for (int u = 0; u < 2; ++u) {
+              const int s = act[u] ? base + u * SPW + g : 0;
+              float4 w = gv[u];
+              if constexpr (FOLD) {
 #pragma unroll
-            for (int a4 = 0; a4 < R / 4; ++a4) {
-              gv[a4] = __ldg(g4 + a4);
-              hv[a4] = __ldg(h4 + a4);
+                for (int i = 0; i < MF; ++i) {
+                  w.x *= dv[u][i].x;
+                  w.y *= dv[u][i].y;
+                  w.z *= dv[u][i].z;
+                  w.w *= dv[u][i].w;
+                }
+                for (int kk = kf + MF; kk < N - 1; ++kk) {
+                  const float4 d =
+                      __ldg(reinterpret_cast<const float4*>(ch.m[kk].s + (int64_t)cidx[(size_t)kk * T + s] * R) + cc);
+                  w.x *= d.x;
+                  w.y *= d.y;
+                  w.z *= d.z;
+                  w.w *= d.w;
+                }
+              }
+              float a = v[u].x * w.x;
+              a = fmaf(v[u].y, w.y, a);
+              a = fmaf(v[u].z, w.z, a);
+              a = fmaf(v[u].w, w.w, a);
+              part[u] = act[u] ? a : 0.f;
             }
-            const uint32_t vrow = s_state + (uint32_t)s * (RP * 4);
-            const uint32_t wrow = s_state + (uint32_t)(two ? s2 : s) * (RP * 4);
-            float acc0 = 0.f, acc1 = 0.f, bcc0 = 0.f, bcc1 = 0.f;
 #pragma unroll
-            for (int a4 = 0; a4 < R / 4; ++a4) {
-              const float4 v = lds128(vrow + a4 * 16);
-              const float4 w = lds128(wrow + a4 * 16);
-              acc0 = fmaf(v.x, gv[a4].x, acc0);
-              acc1 = fmaf(v.y, gv[a4].y, acc1);
-              acc0 = fmaf(v.z, gv[a4].z, acc0);
-              acc1 = fmaf(v.w, gv[a4].w, acc1);
-              bcc0 = fmaf(w.x, hv[a4].x, bcc0);
-              bcc1 = fmaf(w.y, hv[a4].y, bcc1);
-              bcc0 = fmaf(w.z, hv[a4].z, bcc0);
-              bcc1 = fmaf(w.w, hv[a4].w, bcc1);
+            for (int o = GS / 2; o > 0; o >>= 1) {
+              part[0] += __shfl_xor_sync(0xffffffffu, part[0], o);
+              part[1] += __shfl_xor_sync(0xffffffffu, part[1], o);
             }
-            out[s0 + s] = acc0 + acc1;
-            if (two) out[s0 + s2] = bcc0 + bcc1;
+            if (c == 0) {
+              const int sa = base + g, sb = base + SPW + g;
+              if (sa < tn) out[s0 + sa] = part[0];
+              if (sb < tn) out[s0 + sb] = part[1];
+            }
           }
         } else {
           for (int s = tid; s < tn; s += NT) {
