@@ -420,13 +420,15 @@ def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: in
     copy-stream H2D overlapped with the K1 launches on the compute stream."""
     dev = p.device
     m = int(idx_host.shape[0])
-    out = torch.empty(m, dtype=torch.float32, device=dev)
-    comp = torch.cuda.current_stream(dev)
-    copy = torch.cuda.Stream(dev)
     chunk = _PIPELINE_ROWS
     nch = (m + chunk - 1) // chunk
+    # every launch sees exactly `chunk` rows (the short last chunk is padded
+    # with index 0), so all chunks run the same plan as one whole-array call
+    out = torch.empty(nch * chunk, dtype=torch.float32, device=dev)
+    comp = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
     errs = torch.empty(nch, dtype=torch.int32, device=dev)
-    bufs = [torch.empty((min(chunk, m), t.ndim), dtype=torch.int64, device=dev) for _ in range(2)]
+    bufs = [torch.empty((chunk, t.ndim), dtype=torch.int64, device=dev) for _ in range(2)]
     done = [torch.cuda.Event() for _ in range(2)]  # compute finished with buffer b
     ws = None
     if algo == N.ALGO_AUTO and N.load().tnb_entries_workspace_bytes(
@@ -436,21 +438,23 @@ def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: in
     for c in range(nch):
         lo, hi = c * chunk, min(m, (c + 1) * chunk)
         b = c & 1
-        buf = bufs[b][: hi - lo]
+        buf = bufs[b]
         with torch.cuda.stream(copy):
             if c >= 2:
                 copy.wait_event(done[b])
-            buf.copy_(idx_host[lo:hi], non_blocking=True)
+            buf[: hi - lo].copy_(idx_host[lo:hi], non_blocking=True)
+            if hi - lo < chunk:
+                buf[hi - lo:].zero_()
             ready = torch.cuda.Event()
             ready.record(copy)
         comp.wait_event(ready)
         buf.record_stream(comp)
-        ws = launch_entries(p, buf, out[lo:hi], errs[c:c + 1], algo, ws)
+        ws = launch_entries(p, buf, out[lo:lo + chunk], errs[c:c + 1], algo, ws)
         done[b].record(comp)
     code = int(errs.min().item())
     if code < t.ndim:
         raise ContractViolationError(f"index out of bounds on mode {code}")
-    return out
+    return out[:m]
 
 
 def entries(t: TnTensor, indices, *, algo: int = N.ALGO_AUTO) -> torch.Tensor:

@@ -27,6 +27,8 @@
 //     shared memory; the next tile's indices are prefetched into L2.
 // Each sample's arithmetic is a fixed FMA sequence, so results do not depend
 // on the sort order or the tile a sample lands in.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace tnb {
@@ -171,6 +173,14 @@ struct BPlan {
   int8_t slot[kMaxModes];  // mode -> sorted slot or -1
   int l1pf;                // prefetch the next segment's core slice into L1
   int rounds;              // R <= 24: groups of one warp on different buckets
+  // mode merging: the kernels run a VIRTUAL chain whose first / last modes
+  // may be prefix / suffix tables over several original modes; the prep
+  // kernel reads the n0 original index columns, validates each against its
+  // own extent oJ (error = lowest original mode) and combines the columns of
+  // one virtual mode in C order (vmap: original mode -> virtual mode)
+  int n0;
+  int32_t oJ[kMaxModes];
+  int8_t vmap[kMaxModes];
 };
 
 // Warp-level multisplit: the lanes' keys are transposed into kbits ballots;
@@ -204,25 +214,42 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
   unsigned char* rec = ws + tile * bp.tile_bytes;
 
   if (tid < N && bp.slot[tid] >= 0) smode[bp.slot[tid]] = (int8_t)tid;
-  // ---- indices: thread = sample row (N int64 values, 16-byte loads when the
-  //      row stride allows), wrap/validate per mode, compact to [N][T]
+  // ---- indices: thread = sample row (n0 int64 values, 16-byte loads when
+  //      the row stride allows), wrap/validate per original mode, combine
+  //      merged modes, compact to [N][T]
   {
-    const int64_t* src = idx + s0 * N;
-    const bool v2 = (N & 1) == 0 && (reinterpret_cast<uintptr_t>(idx) & 15) == 0;
+    const int N0 = bp.n0;
+    const int64_t* src = idx + s0 * N0;
+    const bool v2 = (N0 & 1) == 0 && (reinterpret_cast<uintptr_t>(idx) & 15) == 0;
     for (int s = tid; s < T; s += NT) {
-      const int64_t* row = src + (int64_t)s * N;
+      const int64_t* row = src + (int64_t)s * N0;
       if (s >= tn) {
         for (int k = 0; k < N; ++k) idxs[(size_t)k * T + s] = (IdxT)0;  // tail rows: index 0
-      } else if (v2) {
-        for (int k = 0; k < N; k += 2) {
-          const longlong2 w = __ldg(reinterpret_cast<const longlong2*>(row + k));
-          idxs[(size_t)k * T + s] = (IdxT)norm_index(w.x, ch.m[k].J, k, err);
-          idxs[(size_t)(k + 1) * T + s] = (IdxT)norm_index(w.y, ch.m[k + 1].J, k + 1, err);
+        continue;
+      }
+      int vk = 0;
+      uint32_t cur = 0;
+      auto put = [&](int o, int64_t raw) {
+        const int32_t J = bp.oJ[o];
+        const uint32_t v = (uint32_t)norm_index(raw, J, o, err);
+        const int tk = bp.vmap[o];
+        if (tk != vk) {
+          idxs[(size_t)vk * T + s] = (IdxT)cur;
+          vk = tk;
+          cur = 0;
+        }
+        cur = cur * (uint32_t)J + v;
+      };
+      if (v2) {
+        for (int o = 0; o < N0; o += 2) {
+          const longlong2 w = __ldg(reinterpret_cast<const longlong2*>(row + o));
+          put(o, w.x);
+          put(o + 1, w.y);
         }
       } else {
-        for (int k = 0; k < N; ++k)
-          idxs[(size_t)k * T + s] = (IdxT)norm_index(__ldg(row + k), ch.m[k].J, k, err);
+        for (int o = 0; o < N0; ++o) put(o, __ldg(row + o));
       }
+      idxs[(size_t)vk * T + s] = (IdxT)cur;
     }
   }
   __syncthreads();
@@ -776,6 +803,193 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
   }
 }
 
+// ---- prefix / suffix tables for mode merging -------------------------------
+// prefix step (rows in C order of the merged indices):
+//   out[(p*J + j)*rr + c] = sum_a in[p*rl + a] * G(j, a, c)      (dense)
+//                         = in[p*rl + c] * D(j, c)               (CP diagonal)
+__global__ void table_prefix_step(ModeDev md, const float* __restrict__ in, int64_t P,
+                                  float* __restrict__ out) {
+  const int J = md.J, rl = md.rl, rr = md.rr;
+  const int64_t total = P * J * rr;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = t / ((int64_t)J * rr);
+    const int64_t r = t - p * J * rr;
+    const int j = (int)(r / rr), c = (int)(r - (int64_t)(r / rr) * rr);
+    const float* x = in + p * rl;
+    float acc;
+    if (md.layout == TNB_LAYOUT_DIAG) {
+      acc = x[c] * __ldg(md.s + (int64_t)j * rl + c);
+    } else {
+      acc = 0.f;
+      const float* g = md.s + (int64_t)j * rl * rr + c;
+      for (int a = 0; a < rl; ++a) acc = fmaf(x[a], __ldg(g + (int64_t)a * rr), acc);
+    }
+    out[t] = acc;
+  }
+}
+
+// suffix step (row = j * n + x, the new mode's index slowest):
+//   out[(j*n + x)*rl + a] = sum_c G(j, a, c) * in[x*rr + c]     (dense)
+//                         = D(j, a) * in[x*rr + a]               (CP diagonal)
+__global__ void table_suffix_step(ModeDev md, const float* __restrict__ in, int64_t n,
+                                  float* __restrict__ out) {
+  const int J = md.J, rl = md.rl, rr = md.rr;
+  const int64_t total = (int64_t)J * n * rl;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = t / rl;
+    const int a = (int)(t - row * rl);
+    const int j = (int)(row / n);
+    const int64_t x = row - (int64_t)j * n;
+    const float* y = in + x * rr;
+    float acc;
+    if (md.layout == TNB_LAYOUT_DIAG) {
+      acc = __ldg(md.s + (int64_t)j * rl + a) * y[a];
+    } else {
+      acc = 0.f;
+      const float* g = md.s + ((int64_t)j * rl + a) * rr;
+      for (int c = 0; c < rr; ++c) acc = fmaf(__ldg(g + c), y[c], acc);
+    }
+    out[t] = acc;
+  }
+}
+
+// Which original modes are merged: prefix [0, a) and suffix [n - b, n).  A
+// side is merged when its index space stays <= 65535 (uint16 compact
+// indices), the table has at most m / 16 rows (building it costs a small
+// fraction of the per-entry work it removes) and it absorbs at least one
+// interior dense mode.  TNB_ENTRIES_MERGE=0 disables merging.
+struct MergePlan {
+  int a = 1, b = 1;
+  int64_t Jp = 0, Js = 0;       // merged index extents
+  int64_t off[kMaxModes];       // table level offsets (bytes) in the workspace
+  int64_t table_bytes = 0;      // 256-aligned
+};
+
+int merge_env() {
+  const char* e = getenv("TNB_ENTRIES_MERGE");
+  return (e && e[0] == '0') ? 0 : 1;
+}
+
+void plan_merge(const ChainDev& ch, int64_t m, MergePlan* mp) {
+  const int N = ch.n;
+  mp->a = mp->b = 1;
+  mp->table_bytes = 0;
+  if (!merge_env() || N < 3) return;
+  const int64_t lim = m / 16 < 65535 ? m / 16 : 65535;
+  int64_t rows = ch.m[0].J;
+  int a = 1, dense = 0;
+  while (a < N - 1 && rows * ch.m[a].J <= lim) {
+    rows *= ch.m[a].J;
+    dense += ch.m[a].layout == TNB_LAYOUT_DENSE;
+    ++a;
+  }
+  if (dense == 0) a = 1;
+  int64_t rs = ch.m[N - 1].J;
+  int b = 1;
+  dense = 0;
+  while (N - 1 - b >= a && rs * ch.m[N - 1 - b].J <= lim) {
+    rs *= ch.m[N - 1 - b].J;
+    dense += ch.m[N - 1 - b].layout == TNB_LAYOUT_DENSE;
+    ++b;
+  }
+  if (dense == 0) b = 1;
+  mp->a = a;
+  mp->b = b;
+  int64_t off = 0;
+  rows = ch.m[0].J;
+  for (int k = 1; k < a; ++k) {  // prefix levels: rows x rr_k
+    rows *= ch.m[k].J;
+    mp->off[k] = off;
+    off += (rows * ch.m[k].rr * 4 + 255) & ~(int64_t)255;
+  }
+  mp->Jp = rows;
+  rs = ch.m[N - 1].J;
+  for (int k = N - 2; k >= N - b; --k) {  // suffix levels: rows x rl_k
+    rs *= ch.m[k].J;
+    mp->off[k] = off;
+    off += (rs * ch.m[k].rl * 4 + 255) & ~(int64_t)255;
+  }
+  mp->Js = rs;
+  mp->table_bytes = off;
+}
+
+// The virtual chain the kernels run; table pointers are filled when `base`
+// is the workspace (nullptr for size queries).
+void virtual_chain(const ChainDev& ch, const MergePlan& mp, unsigned char* base, ChainDev* v) {
+  const int N = ch.n, a = mp.a, b = mp.b;
+  v->batch = 1;
+  v->n = N - (a - 1) - (b - 1);
+  int k = 0;
+  if (a > 1) {
+    ModeDev d = ch.m[a - 1];
+    d.s = base ? reinterpret_cast<const float*>(base + mp.off[a - 1]) : nullptr;
+    d.bstride = 0;
+    d.layout = TNB_LAYOUT_DENSE;
+    d.J = (int32_t)mp.Jp;
+    d.rl = 1;
+    d.rr = ch.m[a - 1].rr;
+    v->m[k++] = d;
+  } else {
+    v->m[k++] = ch.m[0];
+  }
+  for (int o = a; o < N - b; ++o) v->m[k++] = ch.m[o];
+  if (b > 1) {
+    ModeDev d = ch.m[N - b];
+    d.s = base ? reinterpret_cast<const float*>(base + mp.off[N - b]) : nullptr;
+    d.bstride = 0;
+    d.layout = TNB_LAYOUT_DENSE;
+    d.J = (int32_t)mp.Js;
+    d.rl = ch.m[N - b].rl;
+    d.rr = 1;
+    v->m[k++] = d;
+  } else {
+    v->m[k++] = ch.m[N - 1];
+  }
+  int rmax = 1;
+  for (int i = 0; i < v->n; ++i) rmax = max(rmax, max(v->m[i].rl, v->m[i].rr));
+  v->rmax = rmax;
+}
+
+int build_tables(const ChainDev& ch, const MergePlan& mp, unsigned char* base, cudaStream_t st) {
+  const int N = ch.n;
+  const int grid_cap = num_sms() * 8;
+  auto grid = [&](int64_t total) { return (int)std::min<int64_t>(ceil_div(total, 256), grid_cap); };
+  const float* in = ch.m[0].s;  // [J0][1][r1] == [J0][r1]
+  int64_t rows = ch.m[0].J;
+  for (int k = 1; k < mp.a; ++k) {
+    float* o = reinterpret_cast<float*>(base + mp.off[k]);
+    const int64_t total = rows * ch.m[k].J * ch.m[k].rr;
+    if (total > 0) table_prefix_step<<<grid(total), 256, 0, st>>>(ch.m[k], in, rows, o);
+    int rc = check_launch("table_prefix_step");
+    if (rc) return rc;
+    in = o;
+    rows *= ch.m[k].J;
+  }
+  in = ch.m[N - 1].s;  // [J][r][1] == [J][r]
+  int64_t n = ch.m[N - 1].J;
+  for (int k = N - 2; k >= N - mp.b; --k) {
+    float* o = reinterpret_cast<float*>(base + mp.off[k]);
+    const int64_t total = (int64_t)ch.m[k].J * n * ch.m[k].rl;
+    if (total > 0) table_suffix_step<<<grid(total), 256, 0, st>>>(ch.m[k], in, n, o);
+    int rc = check_launch("table_suffix_step");
+    if (rc) return rc;
+    in = o;
+    n *= ch.m[k].J;
+  }
+  return TNB_OK;
+}
+
+void set_vmap(const ChainDev& ch, const MergePlan& mp, int vn, BPlan* bp) {
+  const int N = ch.n;
+  bp->n0 = N;
+  for (int o = 0; o < N; ++o) {
+    bp->oJ[o] = ch.m[o].J;
+    bp->vmap[o] = (int8_t)(o < mp.a ? 0 : (o >= N - mp.b ? vn - 1 : o - mp.a + 1));
+  }
+}
+
 int pick_R(int rmax) {
   if (rmax <= 8) return 8;
   if (rmax <= 16) return 16;
@@ -911,34 +1125,53 @@ bool bucketed_supported(const ChainDev& ch) {
 int64_t bucketed_workspace(const ChainDev& ch, int64_t m) {
   BPlan bp;
   int R, nt;
-  if (m <= 0 || !bucketed_supported(ch) || make_bplan(ch, m, &bp, &R, &nt)) return 0;
-  return bp.ntiles * bp.tile_bytes;
+  if (m <= 0 || !bucketed_supported(ch)) return 0;
+  MergePlan mp;
+  plan_merge(ch, m, &mp);
+  ChainDev v;
+  virtual_chain(ch, mp, nullptr, &v);
+  if (make_bplan(v, m, &bp, &R, &nt)) return 0;
+  return mp.table_bytes + bp.ntiles * bp.tile_bytes;
 }
 
 int launch_entries_bucketed(const ChainDev& ch, const int64_t* idx, int64_t m, float* out,
                             int32_t* err, void* ws, int64_t ws_bytes, cudaStream_t st) {
+  MergePlan mp;
+  plan_merge(ch, m, &mp);
+  ChainDev v;
+  virtual_chain(ch, mp, nullptr, &v);
   BPlan bp;
   int R, nt;
-  int rc = make_bplan(ch, m, &bp, &R, &nt);
+  int rc = make_bplan(v, m, &bp, &R, &nt);
   if (rc) return rc;
-  if (!ws || ws_bytes < bp.ntiles * bp.tile_bytes)
+  const int64_t need = mp.table_bytes + bp.ntiles * bp.tile_bytes;
+  if (!ws || ws_bytes < need)
     return set_error(TNB_EWORKSPACE, "bucketed entries needs %lld workspace bytes, got %lld",
-                     (long long)(bp.ntiles * bp.tile_bytes), (long long)ws_bytes);
+                     (long long)need, (long long)ws_bytes);
+  unsigned char* base = static_cast<unsigned char*>(ws);
+  if (mp.table_bytes) {
+    rc = build_tables(ch, mp, base, st);
+    if (rc) return rc;
+    virtual_chain(ch, mp, base, &v);
+  }
+  set_vmap(ch, mp, v.n, &bp);
+  ws = base + mp.table_bytes;
+  const ChainDev& chv = v;
   unsigned char* w = static_cast<unsigned char*>(ws);
   const bool small = bp.idx_bytes == 1;
   switch (R) {
     case 8:
-      return small ? launch_ri<8, uint8_t>(ch, bp, nt, idx, m, out, err, w, st)
-                   : launch_ri<8, uint16_t>(ch, bp, nt, idx, m, out, err, w, st);
+      return small ? launch_ri<8, uint8_t>(chv, bp, nt, idx, m, out, err, w, st)
+                   : launch_ri<8, uint16_t>(chv, bp, nt, idx, m, out, err, w, st);
     case 16:
-      return small ? launch_ri<16, uint8_t>(ch, bp, nt, idx, m, out, err, w, st)
-                   : launch_ri<16, uint16_t>(ch, bp, nt, idx, m, out, err, w, st);
+      return small ? launch_ri<16, uint8_t>(chv, bp, nt, idx, m, out, err, w, st)
+                   : launch_ri<16, uint16_t>(chv, bp, nt, idx, m, out, err, w, st);
     case 24:
-      return small ? launch_ri<24, uint8_t>(ch, bp, nt, idx, m, out, err, w, st)
-                   : launch_ri<24, uint16_t>(ch, bp, nt, idx, m, out, err, w, st);
+      return small ? launch_ri<24, uint8_t>(chv, bp, nt, idx, m, out, err, w, st)
+                   : launch_ri<24, uint16_t>(chv, bp, nt, idx, m, out, err, w, st);
     default:
-      return small ? launch_ri<32, uint8_t>(ch, bp, nt, idx, m, out, err, w, st)
-                   : launch_ri<32, uint16_t>(ch, bp, nt, idx, m, out, err, w, st);
+      return small ? launch_ri<32, uint8_t>(chv, bp, nt, idx, m, out, err, w, st)
+                   : launch_ri<32, uint16_t>(chv, bp, nt, idx, m, out, err, w, st);
   }
 }
 

@@ -286,3 +286,47 @@ def test_bucketed_group_variants(rounds, monkeypatch):
     o = O.make_chain(nodes)
     idx = O.uniform_indices((128,) * 8, 70000, 9)
     assert_close(tb.entries(t, idx, algo=N.ALGO_BUCKETED), O.entries(o, idx))
+
+
+MERGE_CASES = {
+    # prefix 0-2 and suffix 7-9 tables (cfg2 shape, smaller J)
+    "tt10": lambda rng: [("tt", c, None) for c in O.random_tt((8,) * 10, 16, seed=7, scale=0.25)],
+    # every mode merged into two tables (virtual chain of 2 modes)
+    "two_tables": lambda rng: [("tt", c, None) for c in O.random_tt((8,) * 6, 8, seed=8, scale=0.35)],
+    # CP modes inside the merged ranges, Tucker factors, ragged extents
+    "hybrid": lambda rng: [
+        ("tt", rng.standard_normal((1, 5, 6)).astype(np.float32), None),
+        ("cp", rng.standard_normal((7, 6)).astype(np.float32), rng.standard_normal((9, 7)).astype(np.float32)),
+        ("tt", rng.standard_normal((6, 6, 6)).astype(np.float32) * 0.4, None),
+        ("tt", rng.standard_normal((6, 11, 6)).astype(np.float32) * 0.4, None),
+        ("tt", rng.standard_normal((6, 3, 6)).astype(np.float32) * 0.4, None),
+        ("cp", rng.standard_normal((4, 6)).astype(np.float32), None),
+        ("tt", rng.standard_normal((6, 5, 1)).astype(np.float32), None),
+    ],
+    # cfg5 structure: prefix 0-1, suffix 6-7 (CP), CP 4-5 folded into the last mode
+    "cfg5": lambda rng: O.cfg5_nodes(seed=2),
+}
+
+
+@pytest.mark.parametrize("case", sorted(MERGE_CASES))
+@pytest.mark.parametrize("merge", ["1", "0"])
+def test_bucketed_mode_merging(case, merge, monkeypatch):
+    # prefix/suffix tables over merged modes give the oracle's values; the
+    # index checks still run per ORIGINAL mode (lowest bad mode reported)
+    monkeypatch.setenv("TNB_ENTRIES_MERGE", merge)
+    rng = np.random.default_rng(5)
+    nodes = MERGE_CASES[case](rng)
+    t = facade(nodes)
+    o = O.make_chain(nodes)
+    m = 1 << 20 if case == "cfg5" else 300000
+    idx = O.uniform_indices(t.shape, m, 3)
+    idx[::5] -= np.asarray(t.shape)
+    got = tb.entries(t, idx, algo=N.ALGO_BUCKETED)
+    sel = np.arange(0, m, 7)
+    assert_close(to_np(got)[sel], O.entries(o, idx[sel]), what=case)
+    for k in (0, 1, t.ndim - 1):
+        bad = idx.copy()
+        bad[m // 3, k] = t.shape[k]
+        bad[m // 2, t.ndim - 1] = -t.shape[t.ndim - 1] - 1
+        with pytest.raises(tb.ContractViolationError, match=f"mode {k}"):
+            tb.entries(t, bad, algo=N.ALGO_BUCKETED)
