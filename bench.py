@@ -124,6 +124,19 @@ def load_json(name):
     return None
 
 
+def ncu_traffic(tag, kernel):
+    """dram read+write bytes per launch of `kernel` from the newest committed
+    `ncu --set full` summary profiles/ncu_r<NN>_<tag>.json (None if absent)."""
+    import glob
+
+    for path in sorted(glob.glob(os.path.join(PROFILES, f"ncu_r*_{tag}.json")), reverse=True):
+        with open(path) as f:
+            d = json.load(f)
+        if kernel in d and d[kernel].get("dram_bytes_per_launch") is not None:
+            return d[kernel]["dram_bytes_per_launch"], os.path.relpath(path, ROOT)
+    return None, None
+
+
 def fp32_peak():
     """Measured FFMA peak (tools/peaks.cu, committed in profiles/), else the
     nominal 148 SMs x 128 FMA/clk x 2 x 1.965 GHz."""
@@ -205,8 +218,13 @@ def cfg2_config(n, m):
 # ---------------------------------------------------------------------------
 # our arm
 
-def timed_steps(fn, steps, warmup, stream, dist):
+def timed_steps(fn, steps, warmup, stream, dist, kernel_timing=False):
+    """Device time of exactly `steps` calls (CUDA events on `stream`, max over
+    ranks).  kernel_timing: libtnb brackets its own launches inside the timed
+    region with CUDA events (read back with _native.timing_read)."""
     import torch
+
+    from paper_2206_11128_b200 import _native as N
 
     for _ in range(warmup):
         fn()
@@ -214,6 +232,8 @@ def timed_steps(fn, steps, warmup, stream, dist):
     if dist:
         torch.distributed.barrier()
     torch.cuda.synchronize()
+    if kernel_timing:
+        N.timing_enable(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(steps):
@@ -247,8 +267,11 @@ def bench_entries(args, cfg, dev, dist, ws, rank):
         t = tb.TnTensor([tb.ModeNode(k, c, f) for k, c, f in W.hybrid_nodes(seed)])
         m = 1 << 26
     p = t._packed()
+    from paper_2206_11128_b200 import _native as N
+
     modes = [("diag" if md.layout == 1 else "dense", md.r_left, md.r_right) for md in p.modes]
-    flops_per_entry = W.entry_flops(modes)
+    chain_flops_per_entry = W.entry_flops(modes)
+    plan = N.entries_plan(p.chain, m, args.algo)
     idx_host = torch.from_numpy(W.indices(shape, m, seed + 2 + rank)).pin_memory()
     idx = idx_host.to(dev)
     out = torch.empty(m, dtype=torch.float32, device=dev)
@@ -260,21 +283,43 @@ def bench_entries(args, cfg, dev, dist, ws, rank):
         wsbuf[0] = C.launch_entries(p, idx, out, err, args.algo, wsbuf[0])
 
     with ClockSampler(dev.index) as clk:
-        ms = timed_steps(step, args.steps, args.warmup, stream, dist)
+        ms = timed_steps(step, args.steps, args.warmup, stream, dist, kernel_timing=True)
+    kt = {k: N.timing_read(k) for k in ("entries_prep", "entries_compute", "entries_tables")}
+    N.timing_enable(False)
     assert int(err.item()) >= t.ndim, "bench inputs must be in bounds"
     ms_step = ms / args.steps
     value = ws * m / (ms_step * 1e-3)
-    achieved = flops_per_entry * m / (ms_step * 1e-3) / 1e12
     peak, peak_src = fp32_peak()
-    ncu = load_json(f"ncu_{cfg}_entries.json") or {}
+    traffic, traffic_src = ncu_traffic(f"{cfg}_entries", "entries_compute_kernel")
+    kms, kn = kt["entries_compute"]
+    if kn:  # bucketed: the per-entry compute kernel, timed on its own stream
+        k_ms = kms / kn
+        achieved = plan["kernel_flops"] / (k_ms * 1e-3) / 1e12
+        kernel = "entries_compute_kernel"
+    else:  # chain / layered algorithm: one kernel is the whole step
+        k_ms = ms_step
+        achieved = plan["kernel_flops"] / (ms_step * 1e-3) / 1e12
+        kernel = "entries_chain_kernel"
+    per_entry = plan["kernel_flops"] / m
+    launches = sum(n for _, n in kt.values()) + (
+        args.steps * (plan["prefix_modes"] - 1 + plan["suffix_modes"] - 1) if kn else 0)
     roof = {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-            "frac": achieved / peak, "traffic": ncu.get("dram_bytes_per_launch"),
-            "peak_source": peak_src,
-            "algorithmic": f"{flops_per_entry} flop/entry (2*r_l*r_r per dense mode, R per diag mode) x {m} entries per launch",
+            "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+            "peak_source": peak_src, "kernel": kernel,
+            "kernel_ms": k_ms, "kernel_share_of_step": k_ms / ms_step,
+            "algorithmic": (f"{per_entry:.0f} flop/entry (2*r_l*r_r per dense step, R per diagonal step, "
+                            f"2*r closing dot) over the {plan['n_virtual']}-mode chain the kernel runs "
+                            f"(prefix table over modes 0..{plan['prefix_modes'] - 1}, suffix table over the "
+                            f"last {plan['suffix_modes']} modes) x {m} entries per launch"),
+            "plan": {k: plan[k] for k in ("algo", "n_virtual", "prefix_modes", "suffix_modes",
+                                          "prefix_rows", "suffix_rows", "table_flops")},
+            "other_kernels_ms": {k: (v[0] / v[1] if v[1] else None) for k, v in kt.items()
+                                 if k != "entries_compute"},
+            "chain_equivalent_tflops": chain_flops_per_entry * m / (ms_step * 1e-3) / 1e12,
             "hbm_view": {"bytes_per_launch": (8 * len(shape) + 4) * m,
                          "achieved_gbs": (8 * len(shape) + 4) * m / (ms_step * 1e-3) / 1e9}}
     fields = {"value": value, "ms_per_step": ms_step, "roofline": roof, "clocks": clk.summary(),
-              "gpu_launches": args.steps}
+              "gpu_launches": launches}
     # e2e through the public API from pinned host memory: H2D of the step's
     # indices + K1 + D2H of the step's output, every step
     e2e_steps = max(2, min(args.steps, 3))
@@ -345,11 +390,21 @@ def bench_full(dev, steps, warmup, dist):
         N.check(lib.tnb_full_f32(ctypes.byref(p.chain), 0, shape[0], out.data_ptr(),
                                  wsbuf.data_ptr(), wsb, st), "full")
 
-    ms = timed_steps(step, steps, warmup, torch.cuda.current_stream(dev), dist) / steps
+    ms = timed_steps(step, steps, warmup, torch.cuda.current_stream(dev), dist, kernel_timing=True) / steps
+    g_ms, g_n = N.timing_read("full_gemm")
+    N.timing_enable(False)
     nbytes = out.numel() * 4
     del out
+    peak, src = hbm_peak()
+    k_ms = g_ms / g_n if g_n else ms
+    traffic, tsrc = ncu_traffic("cfg3_full", "full_tc_kernel")
     return {"op": "full", "workload": "cfg3", "ms_per_step": ms, "GB/s": nbytes / (ms * 1e-3) / 1e9,
-            "bytes_written": nbytes}
+            "bytes_written": nbytes,
+            "roofline": {"bound": "hbm", "achieved": nbytes / (k_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": nbytes / (k_ms * 1e-3) / 1e9 / peak, "traffic": traffic,
+                         "traffic_source": tsrc, "peak_source": src, "kernel": "full_gemm (tcgen05 3xTF32)",
+                         "kernel_ms": k_ms, "kernel_share_of_step": k_ms / ms,
+                         "algorithmic": f"{nbytes} output bytes written per launch (4 B x 256^4)"}}
 
 
 def bench_dot(dev, steps, warmup, dist, is_norm=False):
@@ -384,11 +439,19 @@ def bench_dot(dev, steps, warmup, dist, is_norm=False):
         else:
             N.check(lib.tnb_dot_f32(ctypes.byref(pa.chain), ctypes.byref(pb.chain), out.data_ptr(), st), "dot")
 
-    ms = timed_steps(step, steps, warmup, torch.cuda.current_stream(dev), dist) / steps
+    ms = timed_steps(step, steps, warmup, torch.cuda.current_stream(dev), dist, kernel_timing=True) / steps
+    d_ms, d_n = N.timing_read("dot")
+    N.timing_enable(False)
+    k_ms = d_ms / d_n if d_n else ms
     per_pair = sum(ranks[k] * s * ranks[k + 1] for k, s in enumerate(shape)) * 4
     nbytes = 4096 * per_pair * (1 if is_norm else 2)
+    peak, src = hbm_peak()
     return {"op": "norm" if is_norm else "dot", "workload": "cfg4", "ms_per_step": ms,
-            "pairs/s": 4096 / (ms * 1e-3), "GB/s": nbytes / (ms * 1e-3) / 1e9}
+            "pairs/s": 4096 / (ms * 1e-3), "GB/s": nbytes / (ms * 1e-3) / 1e9,
+            "roofline": {"bound": "hbm", "achieved": nbytes / (k_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": nbytes / (k_ms * 1e-3) / 1e9 / peak, "traffic": None, "peak_source": src,
+                         "kernel": "dot_r16_kernel", "kernel_ms": k_ms,
+                         "algorithmic": f"{nbytes} core bytes read per launch (each core read once)"}}
 
 
 def run_ours(args):
@@ -437,11 +500,13 @@ def run_ours(args):
     elif args.op == "full":
         r = bench_full(dev, args.steps, args.warmup, dist)
         line.update({"metric": "full() GB/s", "unit": "GB/s", "value": r["GB/s"] * ws,
-                     "ms_per_step": r["ms_per_step"], "config": {"workload": "cfg3"}})
+                     "ms_per_step": r["ms_per_step"], "roofline": r["roofline"],
+                     "config": {"workload": "cfg3", "l2": "17 GB output, larger than L2"}})
     else:
         r = bench_dot(dev, args.steps, args.warmup, dist, args.op == "norm")
         line.update({"metric": f"{args.op}s/sec", "unit": "pairs/s", "value": r["pairs/s"] * ws,
-                     "ms_per_step": r["ms_per_step"], "config": {"workload": "cfg4"}})
+                     "ms_per_step": r["ms_per_step"], "roofline": r["roofline"],
+                     "config": {"workload": "cfg4", "l2": "4096 x 16 cores = 268 MB per operand, larger than L2"}})
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:

@@ -18,7 +18,8 @@
  *     as void*; NULL = legacy default stream);
  *   - status codes only, no exceptions cross the ABI; tnb_last_error() gives a
  *     thread-local message for the last non-zero status;
- *   - no global mutable state: calls on distinct streams/threads are safe.
+ *   - no global mutable state (except the opt-in kernel timing below): calls
+ *     on distinct streams/threads are safe.
  */
 #ifndef TNB_H_
 #define TNB_H_
@@ -156,6 +157,35 @@ int tnb_full_f32(const tnb_chain* chain, int64_t lead_lo, int64_t lead_hi, float
 int tnb_dot_f32(const tnb_chain* a, const tnb_chain* b, float* out, void* stream);
 /* out[e] = sqrt(max(<t_e, t_e>, 0))  (core.py:387-391) */
 int tnb_norm_f32(const tnb_chain* t, float* out, void* stream);
+
+/* --- plan introspection and kernel timing (bench / profiling) ------------ */
+/*
+ * What tnb_entries_f32(chain, ., m, ., ., algo, ...) will run: the resolved
+ * algorithm, the mode merging of the bucketed path (leading / trailing modes
+ * contracted into prefix / suffix tables once per call, so the per-entry
+ * kernel runs a shorter "virtual" chain) and the algorithmic flops of the
+ * per-entry kernel and of the table build.  No device work.
+ */
+typedef struct {
+  int32_t algo;          /* TNB_ALGO_LAYERED / CHAIN / BUCKETED               */
+  int32_t n_virtual;     /* modes of the chain the per-entry kernel runs       */
+  int32_t prefix_modes;  /* original modes in the prefix table (1 = no table)  */
+  int32_t suffix_modes;  /* original modes in the suffix table (1 = no table)  */
+  int64_t prefix_rows;   /* rows of the prefix table (0 = none)                */
+  int64_t suffix_rows;   /* rows of the suffix table (0 = none)                */
+  double kernel_flops;   /* per call: 2*r_l*r_r per dense step, R per diagonal */
+  double table_flops;    /* per call: building the tables                      */
+} tnb_entries_info;
+int tnb_entries_plan(const tnb_chain* chain, int64_t m, int32_t algo, tnb_entries_info* info);
+
+/*
+ * Opt-in CUDA-event timing of libtnb's own kernels on their launching
+ * streams (the only process-global state; off by default).  Names:
+ * "entries_prep", "entries_compute", "entries_tables", "full_gemm", "dot".
+ * enable(0/1) resets every accumulator; read() waits for the recorded events.
+ */
+int tnb_timing_enable(int32_t on);
+int tnb_timing_read(const char* kernel, double* total_ms, int64_t* launches);
 
 #ifdef __cplusplus
 }

@@ -8,7 +8,7 @@ from __future__ import annotations
 
 import ctypes
 import threading
-from ctypes import POINTER, c_char_p, c_int, c_int32, c_int64, c_void_p
+from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_int64, c_void_p
 from pathlib import Path
 
 from .errors import ContractViolationError, NativeError
@@ -38,6 +38,12 @@ class TnbChain(ctypes.Structure):
                 ("modes", POINTER(TnbMode))]
 
 
+class TnbEntriesInfo(ctypes.Structure):
+    _fields_ = [("algo", c_int32), ("n_virtual", c_int32), ("prefix_modes", c_int32),
+                ("suffix_modes", c_int32), ("prefix_rows", c_int64), ("suffix_rows", c_int64),
+                ("kernel_flops", c_double), ("table_flops", c_double)]
+
+
 # name -> (restype, argtypes); exactly the declarations of include/tnb.h
 SIGNATURES = {
     "tnb_version": (c_char_p, []),
@@ -56,6 +62,9 @@ SIGNATURES = {
                              c_int64, c_void_p]),
     "tnb_dot_f32": (c_int, [POINTER(TnbChain), POINTER(TnbChain), c_void_p, c_void_p]),
     "tnb_norm_f32": (c_int, [POINTER(TnbChain), c_void_p, c_void_p]),
+    "tnb_entries_plan": (c_int, [POINTER(TnbChain), c_int64, c_int32, POINTER(TnbEntriesInfo)]),
+    "tnb_timing_enable": (c_int, [c_int32]),
+    "tnb_timing_read": (c_int, [c_char_p, POINTER(c_double), POINTER(c_int64)]),
 }
 
 _lock = threading.Lock()
@@ -115,3 +124,23 @@ def stream_ptr(device) -> int:
     import torch
 
     return torch.cuda.current_stream(device).cuda_stream
+
+
+def entries_plan(chain: TnbChain, m: int, algo: int = ALGO_AUTO) -> dict:
+    """What tnb_entries_f32 would run for (chain, m, algo): algorithm, mode
+    merging and the per-call algorithmic flops (no device work)."""
+    info = TnbEntriesInfo()
+    check(load().tnb_entries_plan(ctypes.byref(chain), m, algo, ctypes.byref(info)), "entries plan")
+    return {f: getattr(info, f) for f, _ in TnbEntriesInfo._fields_}
+
+
+def timing_enable(on: bool) -> None:
+    check(load().tnb_timing_enable(1 if on else 0), "timing")
+
+
+def timing_read(kernel: str) -> tuple:
+    """(total milliseconds, launches) of libtnb's kernel ``kernel`` since the
+    last timing_enable(True); waits for the recorded events."""
+    ms, n = c_double(), c_int64()
+    check(load().tnb_timing_read(kernel.encode(), ctypes.byref(ms), ctypes.byref(n)), "timing")
+    return ms.value, n.value

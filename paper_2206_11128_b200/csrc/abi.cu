@@ -226,3 +226,7 @@ int tnb_norm_f32(const tnb_chain* t, float* out, void* stream) {
 }
 
 }  // extern "C"
+
+extern "C" int tnb_entries_plan(const tnb_chain* chain, int64_t m, int32_t algo, tnb_entries_info* info) {
+  return tnb::entries_plan(chain, m, algo, info);
+}

@@ -42,6 +42,26 @@ int64_t mode_floats(const tnb_mode& m);
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Opt-in per-kernel timing (tnb_timing_enable): brackets a launch with CUDA
+// events on its stream; a no-op unless enabled.
+bool timing_on();
+void timing_push(const char* name, cudaEvent_t a, cudaEvent_t b);
+struct KTimer {
+  const char* name;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  KTimer(const char* n, cudaStream_t s) : name(n), st(s) {
+    if (timing_on() && cudaEventCreate(&a) == cudaSuccess) cudaEventRecord(a, st);
+  }
+  ~KTimer() {
+    cudaEvent_t b;
+    if (a && cudaEventCreate(&b) == cudaSuccess) {
+      cudaEventRecord(b, st);
+      timing_push(name, a, b);
+    }
+  }
+};
+
 // Number of SMs of the current device (cached per device).
 int num_sms();
 
@@ -71,6 +91,7 @@ int launch_tt_core(const ChainDev& ch, int k, float* out, cudaStream_t st);
 int launch_promote_cp(const tnb_node* node, int position, int64_t batch, float* out,
                       cudaStream_t st);
 int64_t entries_workspace(const tnb_chain* c, int64_t m, int algo);
+int entries_plan(const tnb_chain* c, int64_t m, int algo, tnb_entries_info* info);
 int launch_entries(const tnb_chain* c, const int64_t* idx, int64_t m, float* out, int32_t* err,
                    int algo, void* ws, int64_t ws_bytes, cudaStream_t st);
 int64_t full_workspace(const tnb_chain* c, int64_t lo, int64_t hi);

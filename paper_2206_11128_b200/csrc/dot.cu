@@ -85,6 +85,7 @@ int launch_dot(const tnb_chain* a, const tnb_chain* b, float* out, bool is_norm,
       return set_error(TNB_EINVAL, "shape mismatch on mode %d: %d vs %d", k, a->modes[k].phys,
                        b->modes[k].phys);
   if (a->batch != b->batch) return set_error(TNB_EINVAL, "operands must agree on batching");
+  KTimer kt("dot", st);
   const char* gen = getenv("TNB_DOT_GENERIC");
   if (!(gen && gen[0] == '1') && dot_fast_supported(ca, cb))
     return launch_dot_fast(ca, cb, out, is_norm, st);

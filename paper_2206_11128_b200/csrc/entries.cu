@@ -19,6 +19,8 @@ int launch_entries_bucketed(const ChainDev& ch, const int64_t* idx, int64_t m, f
                             int32_t* err, void* ws, int64_t ws_bytes, cudaStream_t st);
 bool bucketed_supported(const ChainDev& ch);
 int64_t bucketed_workspace(const ChainDev& ch, int64_t m);
+void bucketed_info(const ChainDev& ch, int64_t m, tnb_entries_info* info);
+double chain_entry_flops(const ChainDev& ch);
 
 namespace {
 
@@ -145,6 +147,38 @@ int64_t entries_workspace(const tnb_chain* c, int64_t m, int algo) {
   if (pick_algo(c, algo, rmax) != TNB_ALGO_LAYERED) return 0;
   const int64_t B = c->batch > 0 ? c->batch : 1;
   return 2 * m * B * (int64_t)rmax * (int64_t)sizeof(float);
+}
+
+// per-entry kernel flops of a chain: 2*r_l*r_r per interior dense step, R
+// per diagonal (CP) step, 2*r_l for the closing dot; the first mode is a copy
+double chain_entry_flops(const ChainDev& ch) {
+  double f = 0.0;
+  for (int k = 1; k < ch.n; ++k) {
+    const ModeDev& md = ch.m[k];
+    if (md.layout == TNB_LAYOUT_DIAG) f += md.rl;
+    else f += 2.0 * md.rl * md.rr;
+  }
+  return f * (double)ch.batch;
+}
+
+int entries_plan(const tnb_chain* c, int64_t m, int algo, tnb_entries_info* info) {
+  static thread_local ChainDev ch;
+  if (!c || !c->modes || !info || m < 0) return set_error(TNB_EINVAL, "null argument");
+  const int use = pick_algo(c, algo, chain_rmax(c));
+  int rc = make_chain_dev(c, &ch, use != TNB_ALGO_LAYERED);
+  if (rc) return rc;
+  info->algo = use;
+  info->n_virtual = ch.n;
+  info->prefix_modes = info->suffix_modes = 1;
+  info->prefix_rows = info->suffix_rows = 0;
+  info->table_flops = 0.0;
+  if (use_bucketed(ch, m, algo) && bucketed_supported(ch)) {
+    info->algo = TNB_ALGO_BUCKETED;
+    bucketed_info(ch, m, info);
+    return TNB_OK;
+  }
+  info->kernel_flops = chain_entry_flops(ch) * (double)m;
+  return TNB_OK;
 }
 
 int launch_entries(const tnb_chain* c, const int64_t* idx, int64_t m, float* out, int32_t* err,

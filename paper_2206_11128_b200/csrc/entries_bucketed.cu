@@ -376,9 +376,10 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
   uint16_t* permb = reinterpret_cast<uint16_t*>(cidx + (size_t)N * T);             // [2][T]
   uint16_t* startb = permb + 2 * T;                                                // [2][jpad]
   uint64_t* bars = reinterpret_cast<uint64_t*>(
-      (reinterpret_cast<uintptr_t>(startb + 2 * bp.jpad) + 15) & ~(uintptr_t)15);  // cbar, pbar[2]
+      (reinterpret_cast<uintptr_t>(startb + 2 * bp.jpad) + 15) & ~(uintptr_t)15);  // cbar, pbar[2], fbar
   uint64_t* cbar = bars;
   uint64_t* pbar = bars + 1;
+  uint64_t* fbar = bars + 3;  // first-mode row gather
 
   const uint32_t s_state = s32(state);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -408,6 +409,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
     mb_init(cbar, 1);
     mb_init(&pbar[0], 1);
     mb_init(&pbar[1], 1);
+    mb_init(fbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (blockIdx.x < ntiles) {
       const unsigned char* rec = ws + (int64_t)blockIdx.x * bp.tile_bytes;
@@ -419,7 +421,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
   }
   __syncthreads();
 
-  uint32_t c_it = 0;
+  uint32_t c_it = 0, f_it = 0;
   int64_t item = 0;  // slot items consumed
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t s0 = tile * T;
@@ -437,13 +439,17 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
       if (k == 0) {
         if (N == 1) {  // [J][1][1]
           for (int s = tid; s < tn; s += NT) out[s0 + s] = __ldg(md.s + col[s]);
-        } else if (rr == R) {  // state row = G_0[j][0][:] (16-byte copies)
-#pragma unroll 4
-          for (int e = tid; e < tn * (R / 4); e += NT) {
-            const int s = e / (R / 4), c4 = e - (e / (R / 4)) * (R / 4);
-            const float4 g = __ldg(reinterpret_cast<const float4*>(md.s + (int64_t)col[s] * R) + c4);
-            *reinterpret_cast<float4*>(state + s * RP + c4 * 4) = g;
-          }
+        } else if (rr == R) {
+          // state row = G_0[j][0][:]: one bulk copy per sample, all of the
+          // tile's rows in flight at once on the TMA engine (a prefix table
+          // lives in L2: a register gather would be latency-bound)
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before async writes
+          if (tid == 0) mb_expect(fbar, (uint32_t)tn * R * 4);
+          __syncthreads();
+          for (int s = tid; s < tn; s += NT)
+            bulk(state + s * RP, md.s + (int64_t)col[s] * R, R * 4, fbar);
+          mb_wait(fbar, f_it & 1);
+          ++f_it;
         } else {  // zero padded to R
           for (int e = tid; e < tn * R; e += NT) {
             const int s = e / R, c = e - (e / R) * R;
@@ -495,13 +501,14 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
           const int cc = c < CH ? c : 0;  // idle lanes (R = 24) re-read chunk 0
           const int kf = (FOLD && fold >= 0) ? fold : N - 1;
           const int nf = N - 1 - kf;  // folded CP modes
-          for (int base = warp * (2 * SPW); base < tn; base += nwarps * 2 * SPW) {
-            // every load of both samples is issued before any use
+          constexpr int U = FOLD ? 2 : 4;  // samples per lane group in flight
+          for (int base = warp * (U * SPW); base < tn; base += nwarps * U * SPW) {
+            // every load of the U samples is issued before any use
             constexpr int MF = FOLD ? 4 : 1;
-            float4 gv[2], v[2], dv[2][MF];
-            bool act[2];
+            float4 gv[U], v[U], dv[U][MF];
+            bool act[U];
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
+            for (int u = 0; u < U; ++u) {
               const int s = base + u * SPW + g;
               act[u] = s < tn && c < CH;
               const int sc = act[u] ? s : 0;
@@ -515,9 +522,9 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
               }
               v[u] = lds128(s_state + (uint32_t)sc * (RP * 4) + cc * 16);
             }
-            float part[2];
+            float part[U];
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
+            for (int u = 0; u < U; ++u) {
               const int s = act[u] ? base + u * SPW + g : 0;
               float4 w = gv[u];
               if constexpr (FOLD) {
@@ -545,13 +552,15 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
             }
 #pragma unroll
             for (int o = GS / 2; o > 0; o >>= 1) {
-              part[0] += __shfl_xor_sync(0xffffffffu, part[0], o);
-              part[1] += __shfl_xor_sync(0xffffffffu, part[1], o);
+#pragma unroll
+              for (int u = 0; u < U; ++u) part[u] += __shfl_xor_sync(0xffffffffu, part[u], o);
             }
             if (c == 0) {
-              const int sa = base + g, sb = base + SPW + g;
-              if (sa < tn) out[s0 + sa] = part[0];
-              if (sb < tn) out[s0 + sb] = part[1];
+#pragma unroll
+              for (int u = 0; u < U; ++u) {
+                const int su = base + u * SPW + g;
+                if (su < tn) out[s0 + su] = part[u];
+              }
             }
           }
         } else {
@@ -832,27 +841,35 @@ __global__ void table_prefix_step(ModeDev md, const float* __restrict__ in, int6
 // suffix step (row = j * n + x, the new mode's index slowest):
 //   out[(j*n + x)*rl + a] = sum_c G(j, a, c) * in[x*rr + c]     (dense)
 //                         = D(j, a) * in[x*rr + a]               (CP diagonal)
-__global__ void table_suffix_step(ModeDev md, const float* __restrict__ in, int64_t n,
-                                  float* __restrict__ out) {
+__global__ void __launch_bounds__(256) table_suffix_step(ModeDev md, const float* __restrict__ in,
+                                                          int64_t n, float* __restrict__ out) {
+  // block = (chunk of x, one j): the slice G(j) is staged transposed in
+  // shared memory so lane a reads GT[c][a] (conflict-free) while in[x] rows
+  // are broadcast; output rows are written coalesced
+  __shared__ float gt[32 * 33];
   const int J = md.J, rl = md.rl, rr = md.rr;
-  const int64_t total = (int64_t)J * n * rl;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = t / rl;
-    const int a = (int)(t - row * rl);
-    const int j = (int)(row / n);
-    const int64_t x = row - (int64_t)j * n;
+  const int j = blockIdx.y;
+  if (md.layout != TNB_LAYOUT_DIAG)
+    for (int e = threadIdx.x; e < rl * rr; e += blockDim.x) {
+      const int a = e / rr, c = e - (e / rr) * rr;
+      gt[c * 33 + a] = __ldg(md.s + (int64_t)j * rl * rr + e);
+    }
+  __syncthreads();
+  const int per = blockDim.x / rl;  // x rows per pass
+  const int xl = threadIdx.x / rl, a = threadIdx.x - xl * rl;
+  if (xl >= per) return;
+  for (int64_t x = blockIdx.x * (int64_t)per + xl; x < n; x += (int64_t)gridDim.x * per) {
     const float* y = in + x * rr;
     float acc;
     if (md.layout == TNB_LAYOUT_DIAG) {
       acc = __ldg(md.s + (int64_t)j * rl + a) * y[a];
     } else {
       acc = 0.f;
-      const float* g = md.s + ((int64_t)j * rl + a) * rr;
-      for (int c = 0; c < rr; ++c) acc = fmaf(__ldg(g + c), y[c], acc);
+      for (int c = 0; c < rr; ++c) acc = fmaf(gt[c * 33 + a], y[c], acc);
     }
-    out[t] = acc;
+    out[((int64_t)j * n + x) * rl + a] = acc;
   }
+  (void)J;
 }
 
 // Which original modes are merged: prefix [0, a) and suffix [n - b, n).  A
@@ -953,6 +970,7 @@ void virtual_chain(const ChainDev& ch, const MergePlan& mp, unsigned char* base,
 }
 
 int build_tables(const ChainDev& ch, const MergePlan& mp, unsigned char* base, cudaStream_t st) {
+  KTimer kt("entries_tables", st);
   const int N = ch.n;
   const int grid_cap = num_sms() * 8;
   auto grid = [&](int64_t total) { return (int)std::min<int64_t>(ceil_div(total, 256), grid_cap); };
@@ -972,7 +990,11 @@ int build_tables(const ChainDev& ch, const MergePlan& mp, unsigned char* base, c
   for (int k = N - 2; k >= N - mp.b; --k) {
     float* o = reinterpret_cast<float*>(base + mp.off[k]);
     const int64_t total = (int64_t)ch.m[k].J * n * ch.m[k].rl;
-    if (total > 0) table_suffix_step<<<grid(total), 256, 0, st>>>(ch.m[k], in, n, o);
+    if (total > 0) {
+      const int per = 256 / ch.m[k].rl;
+      const int gx = (int)std::min<int64_t>(ceil_div(n, per), std::max<int64_t>(1, grid_cap / ch.m[k].J));
+      table_suffix_step<<<dim3(gx, ch.m[k].J), 256, 0, st>>>(ch.m[k], in, n, o);
+    }
     int rc = check_launch("table_suffix_step");
     if (rc) return rc;
     in = o;
@@ -1015,7 +1037,7 @@ size_t prep_smem_bytes(int N, int T, int idx_bytes, int nsort, int jpad) {
 
 size_t compute_smem(int T, int RP, int N, int idx_bytes, int jpad) {
   size_t b = (size_t)(T + 1) * RP * 4 + (size_t)N * T * idx_bytes + (size_t)2 * T * 2 + (size_t)2 * jpad * 2;
-  return ((b + 15) & ~(size_t)15) + 3 * 8;
+  return ((b + 15) & ~(size_t)15) + 4 * 8;
 }
 
 // Shared by the workspace query and the launcher so both agree on T.
@@ -1081,7 +1103,10 @@ int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m
   int rc = check_cuda(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem),
                       "prep smem attr");
   if (rc) return rc;
-  pk<<<(unsigned)bp.ntiles, 512, psmem, st>>>(ch, bp, idx, m, err, ws);
+  {
+    KTimer kt("entries_prep", st);
+    pk<<<(unsigned)bp.ntiles, 512, psmem, st>>>(ch, bp, idx, m, err, ws);
+  }
   rc = check_launch("entries_prep");
   if (rc) return rc;
   const size_t csmem = compute_smem(bp.T, R + 4, ch.n, (int)sizeof(IdxT), bp.jpad);
@@ -1091,7 +1116,10 @@ int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m
   if (rc) return rc;
   const int64_t slots = (int64_t)num_sms() * (NT <= 256 ? 2 : 1);
   const int grid = (int)(bp.ntiles < slots ? bp.ntiles : slots);
-  ck<<<grid, NT, csmem, st>>>(ch, bp, ws, m, out);
+  {
+    KTimer kt("entries_compute", st);
+    ck<<<grid, NT, csmem, st>>>(ch, bp, ws, m, out);
+  }
   return check_launch("entries_compute");
 }
 
@@ -1132,6 +1160,35 @@ int64_t bucketed_workspace(const ChainDev& ch, int64_t m) {
   virtual_chain(ch, mp, nullptr, &v);
   if (make_bplan(v, m, &bp, &R, &nt)) return 0;
   return mp.table_bytes + bp.ntiles * bp.tile_bytes;
+}
+
+double chain_entry_flops(const ChainDev& ch);
+
+void bucketed_info(const ChainDev& ch, int64_t m, tnb_entries_info* info) {
+  MergePlan mp;
+  plan_merge(ch, m, &mp);
+  ChainDev v;
+  virtual_chain(ch, mp, nullptr, &v);
+  info->n_virtual = v.n;
+  info->prefix_modes = mp.a;
+  info->suffix_modes = mp.b;
+  info->prefix_rows = mp.a > 1 ? mp.Jp : 0;
+  info->suffix_rows = mp.b > 1 ? mp.Js : 0;
+  info->kernel_flops = chain_entry_flops(v) * (double)m;
+  double tf = 0.0;
+  int64_t rows = ch.m[0].J;
+  for (int k = 1; k < mp.a; ++k) {
+    const ModeDev& md = ch.m[k];
+    rows *= md.J;
+    tf += (double)rows * md.rr * (md.layout == TNB_LAYOUT_DIAG ? 1.0 : 2.0 * md.rl);
+  }
+  rows = ch.m[ch.n - 1].J;
+  for (int k = ch.n - 2; k >= ch.n - mp.b; --k) {
+    const ModeDev& md = ch.m[k];
+    rows *= md.J;
+    tf += (double)rows * md.rl * (md.layout == TNB_LAYOUT_DIAG ? 1.0 : 2.0 * md.rr);
+  }
+  info->table_flops = tf;
 }
 
 int launch_entries_bucketed(const ChainDev& ch, const int64_t* idx, int64_t m, float* out,

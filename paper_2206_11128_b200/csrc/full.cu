@@ -373,6 +373,7 @@ int launch_full(const tnb_chain* c, int64_t lo, int64_t hi, float* out, void* ws
     cols *= md.J;
   }
   // ---- out = L @ R ----
+  KTimer kt("full_gemm", st);
   const int K = c->modes[p].r_left;
   if (K == 0) return check_cuda(cudaMemsetAsync(out, 0, P.out_per * B * sizeof(float), st), "memset");
   if (P.tc_bytes > 0) {

@@ -150,3 +150,56 @@ def test_no_cpu_fallback():
         tb.full(t)
     with pytest.raises(tb.NativeError):
         t[np.zeros((1, 1), dtype=np.int64)]
+
+
+def _chain(specs):
+    """tnb_chain over (layout, J, r_l, r_r) specs with dummy slice pointers
+    (plan queries never touch device memory)."""
+    from paper_2206_11128_b200 import _native as N
+
+    modes = (N.TnbMode * len(specs))()
+    for k, (lay, J, rl, rr) in enumerate(specs):
+        modes[k].layout, modes[k].phys, modes[k].r_left, modes[k].r_right = lay, J, rl, rr
+        modes[k].slices = 0x1000
+    ch = N.TnbChain()
+    ch.n_modes, ch.batch, ch.modes = len(specs), 0, modes
+    ch._keep = modes
+    return ch
+
+
+def test_entries_plan_merges_cfg2_and_cfg5(lib, monkeypatch):
+    from paper_2206_11128_b200 import _native as N
+
+    monkeypatch.delenv("TNB_ENTRIES_MERGE", raising=False)
+    # cfg2: 10 x TT, J=32, r=32, m=2^24 -> prefix 0-2 and suffix 7-9 tables
+    r = 32
+    specs = [(0, 32, 1, r)] + [(0, 32, r, r)] * 8 + [(0, 32, r, 1)]
+    info = N.entries_plan(_chain(specs), 1 << 24)
+    assert info["algo"] == N.ALGO_BUCKETED
+    assert (info["prefix_modes"], info["suffix_modes"], info["n_virtual"]) == (3, 3, 6)
+    assert info["prefix_rows"] == info["suffix_rows"] == 32 ** 3
+    # virtual chain: 4 dense r x r steps + closing dot
+    assert info["kernel_flops"] == (4 * 2 * r * r + 2 * r) * float(1 << 24)
+    assert info["table_flops"] == 2 * (32 ** 2 * r * 2 * r + 32 ** 3 * r * 2 * r)
+    # cfg5: TT 0-3 (r=24), CP 4-7 (diag interior, dense right end), J=128
+    specs5 = [(0, 128, 1, 24)] + [(0, 128, 24, 24)] * 3 + [(1, 128, 24, 24)] * 3 + [(0, 128, 24, 1)]
+    info5 = N.entries_plan(_chain(specs5), 1 << 26)
+    # prefix 0-1 (16384 rows); the CP-only suffix saves no dense step: kept
+    assert (info5["prefix_modes"], info5["suffix_modes"], info5["n_virtual"]) == (2, 1, 7)
+    # smaller m: tables limited to m / 16 rows (2^16 -> 32*32 rows per side);
+    # the chain kernel below 2^16 samples
+    small = N.entries_plan(_chain(specs), 1 << 16)
+    assert small["algo"] == N.ALGO_BUCKETED and small["prefix_modes"] == small["suffix_modes"] == 2
+    assert small["prefix_rows"] == 1024 and small["n_virtual"] == 8
+    assert N.entries_plan(_chain(specs), 1000)["algo"] == N.ALGO_CHAIN
+    monkeypatch.setenv("TNB_ENTRIES_MERGE", "0")
+    off = N.entries_plan(_chain(specs), 1 << 24)
+    assert off["n_virtual"] == 10 and off["kernel_flops"] == (8 * 2 * r * r + 2 * r) * float(1 << 24)
+
+
+def test_timing_is_opt_in(lib):
+    from paper_2206_11128_b200 import _native as N
+
+    N.timing_enable(True)
+    assert N.timing_read("entries_compute") == (0.0, 0)
+    N.timing_enable(False)
