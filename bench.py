@@ -284,7 +284,7 @@ def bench_entries(args, cfg, dev, dist, ws, rank):
 
     with ClockSampler(dev.index) as clk:
         ms = timed_steps(step, args.steps, args.warmup, stream, dist, kernel_timing=True)
-    kt = {k: N.timing_read(k) for k in ("entries_prep", "entries_compute", "entries_tables")}
+    kt = {k: N.timing_read(k) for k in ("entries_prep", "entries_sort", "entries_compute", "entries_tables")}
     N.timing_enable(False)
     assert int(err.item()) >= t.ndim, "bench inputs must be in bounds"
     ms_step = ms / args.steps
@@ -301,7 +301,7 @@ def bench_entries(args, cfg, dev, dist, ws, rank):
         achieved = plan["kernel_flops"] / (ms_step * 1e-3) / 1e12
         kernel = "entries_chain_kernel"
     per_entry = plan["kernel_flops"] / m
-    launches = sum(n for _, n in kt.values()) + (
+    launches = sum(n for k_, (_, n) in kt.items() if k_ != "entries_tables") + (
         args.steps * (plan["prefix_modes"] - 1 + plan["suffix_modes"] - 1) if kn else 0)
     roof = {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,

@@ -181,7 +181,8 @@ int tnb_entries_plan(const tnb_chain* chain, int64_t m, int32_t algo, tnb_entrie
 /*
  * Opt-in CUDA-event timing of libtnb's own kernels on their launching
  * streams (the only process-global state; off by default).  Names:
- * "entries_prep", "entries_compute", "entries_tables", "full_gemm", "dot".
+ * "entries_prep", "entries_sort", "entries_compute", "entries_tables",
+ * "full_gemm", "dot".
  * enable(0/1) resets every accumulator; read() waits for the recorded events.
  */
 int tnb_timing_enable(int32_t on);

@@ -181,39 +181,28 @@ struct BPlan {
   int n0;
   int32_t oJ[kMaxModes];
   int8_t vmap[kMaxModes];
+  int8_t smode[kMaxModes];  // sorted slot -> (virtual) mode
 };
 
-// Warp-level multisplit: the lanes' keys are transposed into kbits ballots;
-// lane j owns buckets j, j+32, ... and gets each bucket's member mask from the
-// ballots alone -- no atomics, no MATCH loops.
-template <int KB>
-__device__ __forceinline__ unsigned key_mask(const unsigned (&b)[KB], int key, unsigned amask) {
-  unsigned m = amask;
-#pragma unroll
-  for (int i = 0; i < KB; ++i) m &= b[i] ^ (((key >> i) & 1) ? 0u : 0xffffffffu);
-  return m;
-}
-
-template <typename IdxT, int MAXBPL, int KB>
+// prep: one CTA per tile -- reads the tile's n0 int64 index columns
+// (coalesced), validates and combines them, and writes the compact [N][T]
+// index block of the tile record.
+template <typename IdxT>
 __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant__ ChainDev ch,
                                                            const __grid_constant__ BPlan bp,
                                                            const int64_t* __restrict__ idx, int64_t m,
                                                            int32_t* __restrict__ err,
                                                            unsigned char* __restrict__ ws) {
-  constexpr int NT = 512, NW = NT / 32;  // MAXBPL: buckets per lane (J <= 32 * MAXBPL)
+  constexpr int NT = 512;
   extern __shared__ __align__(16) unsigned char smem[];
-  const int N = ch.n, T = bp.T, NS = bp.nsort, JP = bp.jpad;
-  IdxT* idxs = reinterpret_cast<IdxT*>(smem);                                          // [N][T]
-  uint16_t* perm = reinterpret_cast<uint16_t*>(smem + (size_t)N * T * sizeof(IdxT));  // [NS][T]
-  int8_t* smode = reinterpret_cast<int8_t*>(perm + (size_t)NS * T);                    // slot -> mode
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const unsigned lt_mask = (1u << lane) - 1u;
+  const int N = ch.n, T = bp.T;
+  IdxT* idxs = reinterpret_cast<IdxT*>(smem);  // [N][T]
+  const int tid = threadIdx.x;
   const int64_t tile = blockIdx.x;
   const int64_t s0 = tile * T;
   const int tn = (int)((m - s0) < T ? (m - s0) : T);
   unsigned char* rec = ws + tile * bp.tile_bytes;
 
-  if (tid < N && bp.slot[tid] >= 0) smode[bp.slot[tid]] = (int8_t)tid;
   // ---- indices: thread = sample row (n0 int64 values, 16-byte loads when
   //      the row stride allows), wrap/validate per original mode, combine
   //      merged modes, compact to [N][T]
@@ -258,83 +247,65 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
     for (int i = tid; i < n16; i += NT)
       reinterpret_cast<uint4*>(rec)[i] = reinterpret_cast<const uint4*>(idxs)[i];
   }
-  // ---- one warp per sorted slot: count, warp scan, scatter (no block
-  //      barriers, no atomics; lane j owns buckets j, j+32, ...)
-  const int chunks = (tn + 31) >> 5;
-  uint16_t* gst_all = reinterpret_cast<uint16_t*>(rec + bp.off_starts);
-  for (int sl = warp; sl < NS; sl += NW) {
-    const int k = smode[sl];
-    const int J = ch.m[k].J;
-    const int bpl = (J + 31) >> 5;
-    const IdxT* col = idxs + (size_t)k * T;
-    uint16_t* pm = perm + (size_t)sl * T;
-    int cnt[MAXBPL];
+}
+
+// sort: ONE WARP per (tile, sorted mode), independent of every other warp (no
+// CTA barriers): counting sort of the tile's compact indices of that mode with
+// a per-warp shared-memory histogram -- count (shared atomics), warp scan,
+// scatter (shared atomics hand out the slots) -- writing the permutation and
+// the bucket starts of the record.  The order inside a bucket is not fixed,
+// and need not be: a sample's arithmetic does not depend on its position.
+template <typename IdxT>
+__global__ void __launch_bounds__(256) entries_sort_kernel(const __grid_constant__ ChainDev ch,
+                                                           const __grid_constant__ BPlan bp, int64_t m,
+                                                           unsigned char* __restrict__ ws) {
+  extern __shared__ __align__(16) int hist_all[];  // per warp: [jpad] counts, [T] permutation
+  const int NS = bp.nsort, T = bp.T, JP = bp.jpad;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t gw = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp;
+  const int64_t tile = gw / NS;
+  if (tile >= bp.ntiles) return;
+  const int sl = (int)(gw - tile * NS);
+  const int64_t s0 = tile * T;
+  const int tn = (int)((m - s0) < T ? (m - s0) : T);
+  unsigned char* rec = ws + tile * bp.tile_bytes;
+  const int k = bp.smode[sl];
+  const int J = ch.m[k].J;
+  const IdxT* col = reinterpret_cast<const IdxT*>(rec) + (size_t)k * T;
+  uint16_t* pm = reinterpret_cast<uint16_t*>(rec + bp.off_perm) + (size_t)sl * T;
+  uint16_t* gst = reinterpret_cast<uint16_t*>(rec + bp.off_starts) + (size_t)sl * JP;
+  int* h = hist_all + (size_t)warp * (JP + T / 2);
+  uint16_t* pb = reinterpret_cast<uint16_t*>(h + JP);  // JP and T/2 are multiples of 4: 16-B aligned
+  for (int j = lane; j < JP; j += 32) h[j] = 0;
+  __syncwarp();
+#pragma unroll 4
+  for (int s = lane; s < tn; s += 32) atomicAdd(&h[col[s]], 1);
+  __syncwarp();
+  // exclusive scan: lane owns the contiguous bucket range [lane*per, ...)
+  const int per = (J + 31) >> 5;
+  const int j0 = lane * per, j1 = min(j0 + per, J);
+  int sum = 0;
+  for (int j = j0; j < j1; ++j) sum += h[j];
+  int incl = sum;
 #pragma unroll
-    for (int u = 0; u < MAXBPL; ++u) cnt[u] = 0;
-    for (int c = 0; c < chunks; ++c) {
-      const int s = c * 32 + lane;
-      const unsigned amask = __ballot_sync(0xffffffffu, s < tn);
-      const int key = s < tn ? (int)col[s] : 0;
-      unsigned b[KB];  // KB >= bits of every slot's J: higher key bits are 0
-#pragma unroll
-      for (int i = 0; i < KB; ++i) b[i] = __ballot_sync(0xffffffffu, (key >> i) & 1);
-#pragma unroll
-      for (int u = 0; u < MAXBPL; ++u)
-        if (u < bpl) cnt[u] += __popc(key_mask<KB>(b, lane + 32 * u, amask));
-    }
-    // exclusive scan over buckets j = lane + 32u (u-major, then lane)
-    int run[MAXBPL];
-    int carry = 0;
-#pragma unroll
-    for (int u = 0; u < MAXBPL; ++u) {
-      if (u < bpl) {
-        int incl = cnt[u];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += y;
-        }
-        run[u] = carry + incl - cnt[u];
-        carry += __shfl_sync(0xffffffffu, incl, 31);
-      } else {
-        run[u] = 0;
-      }
-    }
-    uint16_t* gst = gst_all + (size_t)sl * JP;
-#pragma unroll
-    for (int u = 0; u < MAXBPL; ++u) {
-      const int j = lane + 32 * u;
-      if (u < bpl && j < J) gst[j] = (uint16_t)run[u];
-    }
-    for (int j = J + lane; j < JP; j += 32) gst[j] = (uint16_t)tn;
-    for (int c = 0; c < chunks; ++c) {
-      const int s = c * 32 + lane;
-      const unsigned amask = __ballot_sync(0xffffffffu, s < tn);
-      const int key = s < tn ? (int)col[s] : 0;
-      unsigned b[KB];
-#pragma unroll
-      for (int i = 0; i < KB; ++i) b[i] = __ballot_sync(0xffffffffu, (key >> i) & 1);
-      const unsigned peers = key_mask<KB>(b, key, amask);
-      int base = 0;
-#pragma unroll
-      for (int u = 0; u < MAXBPL; ++u) {
-        if (u < bpl) {
-          const int v = __shfl_sync(0xffffffffu, run[u], key & 31);
-          if ((key >> 5) == u) base = v;
-        }
-      }
-      if (s < tn) pm[base + __popc(peers & lt_mask)] = (uint16_t)s;
-#pragma unroll
-      for (int u = 0; u < MAXBPL; ++u)
-        if (u < bpl) run[u] += __popc(key_mask<KB>(b, lane + 32 * u, amask));
-    }
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
   }
-  __syncthreads();
-  {
-    uint4* gp = reinterpret_cast<uint4*>(rec + bp.off_perm);
-    const int n16 = NS * T * 2 / 16;
-    for (int i = tid; i < n16; i += NT) gp[i] = reinterpret_cast<const uint4*>(perm)[i];
+  int run = incl - sum;
+  for (int j = j0; j < j1; ++j) {
+    const int c = h[j];
+    h[j] = run;
+    gst[j] = (uint16_t)run;
+    run += c;
   }
+  for (int j = J + lane; j < JP; j += 32) gst[j] = (uint16_t)tn;
+  __syncwarp();
+#pragma unroll 4
+  for (int s = lane; s < tn; s += 32) pb[atomicAdd(&h[col[s]], 1)] = (uint16_t)s;
+  __syncwarp();
+  // coalesced 16-byte copy-out of the permutation
+  for (int i = lane; i < T / 8; i += 32) reinterpret_cast<uint4*>(pm)[i] = reinterpret_cast<const uint4*>(pb)[i];
 }
 
 __device__ __forceinline__ uint32_t s32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -1030,10 +1001,7 @@ int bucket_threads() {
   return v;
 }
 
-size_t prep_smem_bytes(int N, int T, int idx_bytes, int nsort, int jpad) {
-  (void)jpad;
-  return (size_t)N * T * idx_bytes + (size_t)nsort * T * 2 + 256;
-}
+size_t prep_smem_bytes(int N, int T, int idx_bytes) { return (size_t)N * T * idx_bytes + 256; }
 
 size_t compute_smem(int T, int RP, int N, int idx_bytes, int jpad) {
   size_t b = (size_t)(T + 1) * RP * 4 + (size_t)N * T * idx_bytes + (size_t)2 * T * 2 + (size_t)2 * jpad * 2;
@@ -1051,6 +1019,7 @@ int make_bplan(const ChainDev& ch, int64_t m, BPlan* bp, int* R_out, int* nt_out
     const bool srt = k > 0 && k < ch.n - 1 && ch.m[k].layout == TNB_LAYOUT_DENSE;
     bp->slot[k] = srt ? (int8_t)nsort : (int8_t)-1;
     if (srt) {
+      bp->smode[nsort] = (int8_t)k;
       ++nsort;
       jmax = ch.m[k].J > jmax ? ch.m[k].J : jmax;
     }
@@ -1061,7 +1030,7 @@ int make_bplan(const ChainDev& ch, int64_t m, BPlan* bp, int* R_out, int* nt_out
   const int jpad = ((jmax + 1) + 7) & ~7;
   const size_t budget = (size_t)(233472 / (NT <= 256 ? 2 : 1)) - 1024;
   // the prep kernel holds every slot's permutation and per-warp counts at once
-  auto prep_smem = [&](int t) { return prep_smem_bytes(ch.n, t, idx_bytes, nsort, jpad); };
+  auto prep_smem = [&](int t) { return prep_smem_bytes(ch.n, t, idx_bytes); };
   int T = 65504;
   while (T > 32 && (compute_smem(T, RP, ch.n, idx_bytes, jpad) > budget || prep_smem(T) > 232448 - 1024))
     T -= 32;
@@ -1090,25 +1059,34 @@ int make_bplan(const ChainDev& ch, int64_t m, BPlan* bp, int* R_out, int* nt_out
 template <int R, typename IdxT, int NT, bool FOLD>
 int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m, float* out,
               int32_t* err, unsigned char* ws, cudaStream_t st) {
-  // prep: one CTA per tile
-  const size_t psmem = prep_smem_bytes(ch.n, bp.T, (int)sizeof(IdxT), bp.nsort, bp.jpad);
-  int jmax = 1;
-  for (int k = 0; k < ch.n; ++k)
-    if (bp.slot[k] >= 0 && ch.m[k].J > jmax) jmax = ch.m[k].J;
-  const int kb = 32 - __builtin_clz((unsigned)(jmax > 1 ? jmax - 1 : 1));
-  auto pk = kb <= 5   ? entries_prep_kernel<IdxT, 1, 5>
-            : kb == 6 ? entries_prep_kernel<IdxT, 2, 6>
-            : kb == 7 ? entries_prep_kernel<IdxT, 4, 7>
-                      : entries_prep_kernel<IdxT, kMaxJ / 32, 10>;
-  int rc = check_cuda(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem),
+  // prep: one CTA per tile; sort: one warp per (tile, sorted mode)
+  const size_t psmem = prep_smem_bytes(ch.n, bp.T, (int)sizeof(IdxT));
+  int rc = check_cuda(cudaFuncSetAttribute(entries_prep_kernel<IdxT>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem),
                       "prep smem attr");
   if (rc) return rc;
   {
     KTimer kt("entries_prep", st);
-    pk<<<(unsigned)bp.ntiles, 512, psmem, st>>>(ch, bp, idx, m, err, ws);
+    entries_prep_kernel<IdxT><<<(unsigned)bp.ntiles, 512, psmem, st>>>(ch, bp, idx, m, err, ws);
   }
   rc = check_launch("entries_prep");
   if (rc) return rc;
+  if (bp.nsort > 0) {
+    const int64_t warps = bp.ntiles * bp.nsort;
+    const size_t per_warp = (size_t)bp.jpad * 4 + (size_t)bp.T * 2;
+    int wpb = 8;
+    while (wpb > 1 && wpb * per_warp > 96 * 1024) wpb >>= 1;
+    rc = check_cuda(cudaFuncSetAttribute(entries_sort_kernel<IdxT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(wpb * per_warp)),
+                    "sort smem attr");
+    if (rc) return rc;
+    {
+      KTimer kt("entries_sort", st);
+      entries_sort_kernel<IdxT><<<(unsigned)ceil_div(warps, wpb), 32 * wpb, wpb * per_warp, st>>>(ch, bp, m, ws);
+    }
+    rc = check_launch("entries_sort");
+    if (rc) return rc;
+  }
   const size_t csmem = compute_smem(bp.T, R + 4, ch.n, (int)sizeof(IdxT), bp.jpad);
   auto ck = entries_compute_kernel<R, IdxT, NT, FOLD>;
   rc = check_cuda(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem),
