@@ -302,7 +302,7 @@ def bench_entries(args, cfg, dev, dist, ws, rank):
         kernel = "entries_chain_kernel"
     per_entry = plan["kernel_flops"] / m
     launches = sum(n for k_, (_, n) in kt.items() if k_ != "entries_tables") + (
-        args.steps * (plan["prefix_modes"] - 1 + plan["suffix_modes"] - 1) if kn else 0)
+        args.steps * plan["table_launches"] if kn else 0)
     roof = {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
             "peak_source": peak_src, "kernel": kernel,
@@ -312,7 +312,7 @@ def bench_entries(args, cfg, dev, dist, ws, rank):
                             f"(prefix table over modes 0..{plan['prefix_modes'] - 1}, suffix table over the "
                             f"last {plan['suffix_modes']} modes) x {m} entries per launch"),
             "plan": {k: plan[k] for k in ("algo", "n_virtual", "prefix_modes", "suffix_modes",
-                                          "prefix_rows", "suffix_rows", "table_flops")},
+                                          "prefix_rows", "suffix_rows", "diag_tables", "table_flops")},
             "other_kernels_ms": {k: (v[0] / v[1] if v[1] else None) for k, v in kt.items()
                                  if k != "entries_compute"},
             "chain_equivalent_tflops": chain_flops_per_entry * m / (ms_step * 1e-3) / 1e12,

@@ -162,9 +162,10 @@ int tnb_norm_f32(const tnb_chain* t, float* out, void* stream);
 /*
  * What tnb_entries_f32(chain, ., m, ., ., algo, ...) will run: the resolved
  * algorithm, the mode merging of the bucketed path (leading / trailing modes
- * contracted into prefix / suffix tables once per call, so the per-entry
- * kernel runs a shorter "virtual" chain) and the algorithmic flops of the
- * per-entry kernel and of the table build.  No device work.
+ * contracted into prefix / suffix tables and runs of interior CP modes into
+ * diagonal product tables, once per call, so the per-entry kernel runs a
+ * shorter "virtual" chain) and the algorithmic flops of the per-entry kernel
+ * and of the table build.  No device work.
  */
 typedef struct {
   int32_t algo;          /* TNB_ALGO_LAYERED / CHAIN / BUCKETED               */
@@ -175,6 +176,8 @@ typedef struct {
   int64_t suffix_rows;   /* rows of the suffix table (0 = none)                */
   double kernel_flops;   /* per call: 2*r_l*r_r per dense step, R per diagonal */
   double table_flops;    /* per call: building the tables                      */
+  int32_t diag_tables;   /* runs of interior CP modes merged into product tables */
+  int32_t table_launches;/* kernel launches that build the tables per call     */
 } tnb_entries_info;
 int tnb_entries_plan(const tnb_chain* chain, int64_t m, int32_t algo, tnb_entries_info* info);
 

@@ -843,16 +843,28 @@ __global__ void __launch_bounds__(256) table_suffix_step(ModeDev md, const float
   (void)J;
 }
 
-// Which original modes are merged: prefix [0, a) and suffix [n - b, n).  A
-// side is merged when its index space stays <= 65535 (uint16 compact
-// indices), the table has at most m / 16 rows (building it costs a small
-// fraction of the per-entry work it removes) and it absorbs at least one
-// interior dense mode.  TNB_ENTRIES_MERGE=0 disables merging.
+// Mode merging: the original modes are partitioned into groups, each one
+// VIRTUAL mode of the chain the kernels run:
+//   prefix [0, a)      -> dense table P[(j_0..j_{a-1})][r_a]    (first mode)
+//   suffix [n - b, n)  -> dense table S[(j_{n-b}..j_{n-1})][r]  (last mode)
+//   runs of interior CP modes -> diagonal product table D[(j..)][R]
+//   every other mode stays as it is.
+// Table row indices are the C-order combinations of the original indices
+// (the prep kernel combines them).  A group may hold at most min(m / 16,
+// 65535) rows: uint16 compact indices, and building a table costs a small
+// fraction of the per-entry work it removes (a gathered row replaces one
+// dense r x r step or one diagonal gather per merged mode).
+// TNB_ENTRIES_MERGE=0 disables merging.
+enum GroupKind { kOrig = 0, kPrefix = 1, kSuffix = 2, kDiag = 3 };
 struct MergePlan {
-  int a = 1, b = 1;
-  int64_t Jp = 0, Js = 0;       // merged index extents
-  int64_t off[kMaxModes];       // table level offsets (bytes) in the workspace
-  int64_t table_bytes = 0;      // 256-aligned
+  int ng = 0;                    // virtual modes
+  int lo[kMaxModes], hi[kMaxModes];
+  int kind[kMaxModes];
+  int64_t rows[kMaxModes];
+  int64_t lvl[kMaxModes];        // byte offset of the level ending at original mode o
+  int64_t table_bytes = 0;       // 256-aligned
+  int a() const { return kind[0] == kPrefix ? hi[0] - lo[0] : 1; }
+  int b() const { return kind[ng - 1] == kSuffix ? hi[ng - 1] - lo[ng - 1] : 1; }
 };
 
 int merge_env() {
@@ -862,125 +874,152 @@ int merge_env() {
 
 void plan_merge(const ChainDev& ch, int64_t m, MergePlan* mp) {
   const int N = ch.n;
-  mp->a = mp->b = 1;
+  const int64_t lim = (merge_env() && N >= 3) ? (m / 16 < 65535 ? m / 16 : 65535) : 0;
+  int a = 1, b = 1;
+  int64_t rows = ch.m[0].J, rs = ch.m[N - 1].J;
+  if (lim > 0) {
+    while (a < N - 1 && rows * ch.m[a].J <= lim) rows *= ch.m[a++].J;
+    while (N - 1 - b >= a && rs * ch.m[N - 1 - b].J <= lim) rs *= ch.m[N - 1 - b++].J;
+  }
   mp->table_bytes = 0;
-  if (!merge_env() || N < 3) return;
-  const int64_t lim = m / 16 < 65535 ? m / 16 : 65535;
-  int64_t rows = ch.m[0].J;
-  int a = 1, dense = 0;
-  while (a < N - 1 && rows * ch.m[a].J <= lim) {
-    rows *= ch.m[a].J;
-    dense += ch.m[a].layout == TNB_LAYOUT_DENSE;
-    ++a;
+  if (N == 1) {
+    mp->ng = 1;
+    mp->lo[0] = 0;
+    mp->hi[0] = 1;
+    mp->kind[0] = kOrig;
+    mp->rows[0] = ch.m[0].J;
+    return;
   }
-  if (dense == 0) a = 1;
-  int64_t rs = ch.m[N - 1].J;
-  int b = 1;
-  dense = 0;
-  while (N - 1 - b >= a && rs * ch.m[N - 1 - b].J <= lim) {
-    rs *= ch.m[N - 1 - b].J;
-    dense += ch.m[N - 1 - b].layout == TNB_LAYOUT_DENSE;
-    ++b;
+  int g = 0;
+  auto add = [&](int lo, int hi, int kind, int64_t r) {
+    mp->lo[g] = lo;
+    mp->hi[g] = hi;
+    mp->kind[g] = kind;
+    mp->rows[g] = r;
+    ++g;
+  };
+  if (a > 1) add(0, a, kPrefix, rows);
+  else add(0, 1, kOrig, ch.m[0].J);
+  for (int o = a; o < N - b;) {
+    int e = o + 1;
+    int64_t r = ch.m[o].J;
+    if (lim > 0 && ch.m[o].layout == TNB_LAYOUT_DIAG)
+      while (e < N - b && ch.m[e].layout == TNB_LAYOUT_DIAG && r * ch.m[e].J <= lim) r *= ch.m[e++].J;
+    add(o, e, e - o > 1 ? kDiag : kOrig, r);
+    o = e;
   }
-  if (dense == 0) b = 1;
-  mp->a = a;
-  mp->b = b;
+  if (b > 1) add(N - b, N, kSuffix, rs);
+  else add(N - 1, N, kOrig, ch.m[N - 1].J);
+  mp->ng = g;
+  // table levels: prefix / diag levels end at original mode o (o > lo),
+  // suffix levels start at o (o < hi - 1); the group's first level is a view
   int64_t off = 0;
-  rows = ch.m[0].J;
-  for (int k = 1; k < a; ++k) {  // prefix levels: rows x rr_k
-    rows *= ch.m[k].J;
-    mp->off[k] = off;
-    off += (rows * ch.m[k].rr * 4 + 255) & ~(int64_t)255;
+  for (int v = 0; v < g; ++v) {
+    const int lo = mp->lo[v], hi = mp->hi[v];
+    if (mp->kind[v] == kPrefix || mp->kind[v] == kDiag) {
+      int64_t r = ch.m[lo].J;
+      for (int o = lo + 1; o < hi; ++o) {
+        r *= ch.m[o].J;
+        mp->lvl[o] = off;
+        off += (r * ch.m[o].rr * 4 + 255) & ~(int64_t)255;
+      }
+    } else if (mp->kind[v] == kSuffix) {
+      int64_t r = ch.m[hi - 1].J;
+      for (int o = hi - 2; o >= lo; --o) {
+        r *= ch.m[o].J;
+        mp->lvl[o] = off;
+        off += (r * ch.m[o].rl * 4 + 255) & ~(int64_t)255;
+      }
+    }
   }
-  mp->Jp = rows;
-  rs = ch.m[N - 1].J;
-  for (int k = N - 2; k >= N - b; --k) {  // suffix levels: rows x rl_k
-    rs *= ch.m[k].J;
-    mp->off[k] = off;
-    off += (rs * ch.m[k].rl * 4 + 255) & ~(int64_t)255;
-  }
-  mp->Js = rs;
   mp->table_bytes = off;
 }
 
 // The virtual chain the kernels run; table pointers are filled when `base`
 // is the workspace (nullptr for size queries).
 void virtual_chain(const ChainDev& ch, const MergePlan& mp, unsigned char* base, ChainDev* v) {
-  const int N = ch.n, a = mp.a, b = mp.b;
   v->batch = 1;
-  v->n = N - (a - 1) - (b - 1);
-  int k = 0;
-  if (a > 1) {
-    ModeDev d = ch.m[a - 1];
-    d.s = base ? reinterpret_cast<const float*>(base + mp.off[a - 1]) : nullptr;
-    d.bstride = 0;
-    d.layout = TNB_LAYOUT_DENSE;
-    d.J = (int32_t)mp.Jp;
-    d.rl = 1;
-    d.rr = ch.m[a - 1].rr;
-    v->m[k++] = d;
-  } else {
-    v->m[k++] = ch.m[0];
-  }
-  for (int o = a; o < N - b; ++o) v->m[k++] = ch.m[o];
-  if (b > 1) {
-    ModeDev d = ch.m[N - b];
-    d.s = base ? reinterpret_cast<const float*>(base + mp.off[N - b]) : nullptr;
-    d.bstride = 0;
-    d.layout = TNB_LAYOUT_DENSE;
-    d.J = (int32_t)mp.Js;
-    d.rl = ch.m[N - b].rl;
-    d.rr = 1;
-    v->m[k++] = d;
-  } else {
-    v->m[k++] = ch.m[N - 1];
-  }
+  v->n = mp.ng;
   int rmax = 1;
-  for (int i = 0; i < v->n; ++i) rmax = max(rmax, max(v->m[i].rl, v->m[i].rr));
+  for (int g = 0; g < mp.ng; ++g) {
+    const int lo = mp.lo[g], hi = mp.hi[g];
+    ModeDev d = ch.m[lo];
+    if (mp.kind[g] != kOrig) {
+      const int64_t off = mp.kind[g] == kSuffix ? mp.lvl[lo] : mp.lvl[hi - 1];
+      d.s = base ? reinterpret_cast<const float*>(base + off) : nullptr;
+      d.bstride = 0;
+      d.J = (int32_t)mp.rows[g];
+      if (mp.kind[g] == kPrefix) {
+        d.layout = TNB_LAYOUT_DENSE;
+        d.rl = 1;
+        d.rr = ch.m[hi - 1].rr;
+      } else if (mp.kind[g] == kSuffix) {
+        d.layout = TNB_LAYOUT_DENSE;
+        d.rl = ch.m[lo].rl;
+        d.rr = 1;
+      }  // kDiag keeps layout DIAG and rl == rr == R
+    }
+    v->m[g] = d;
+    rmax = max(rmax, max(d.rl, d.rr));
+  }
   v->rmax = rmax;
 }
 
 int build_tables(const ChainDev& ch, const MergePlan& mp, unsigned char* base, cudaStream_t st) {
+  if (!mp.table_bytes) return TNB_OK;
   KTimer kt("entries_tables", st);
-  const int N = ch.n;
   const int grid_cap = num_sms() * 8;
   auto grid = [&](int64_t total) { return (int)std::min<int64_t>(ceil_div(total, 256), grid_cap); };
-  const float* in = ch.m[0].s;  // [J0][1][r1] == [J0][r1]
-  int64_t rows = ch.m[0].J;
-  for (int k = 1; k < mp.a; ++k) {
-    float* o = reinterpret_cast<float*>(base + mp.off[k]);
-    const int64_t total = rows * ch.m[k].J * ch.m[k].rr;
-    if (total > 0) table_prefix_step<<<grid(total), 256, 0, st>>>(ch.m[k], in, rows, o);
-    int rc = check_launch("table_prefix_step");
-    if (rc) return rc;
-    in = o;
-    rows *= ch.m[k].J;
-  }
-  in = ch.m[N - 1].s;  // [J][r][1] == [J][r]
-  int64_t n = ch.m[N - 1].J;
-  for (int k = N - 2; k >= N - mp.b; --k) {
-    float* o = reinterpret_cast<float*>(base + mp.off[k]);
-    const int64_t total = (int64_t)ch.m[k].J * n * ch.m[k].rl;
-    if (total > 0) {
-      const int per = 256 / ch.m[k].rl;
-      const int gx = (int)std::min<int64_t>(ceil_div(n, per), std::max<int64_t>(1, grid_cap / ch.m[k].J));
-      table_suffix_step<<<dim3(gx, ch.m[k].J), 256, 0, st>>>(ch.m[k], in, n, o);
+  for (int g = 0; g < mp.ng; ++g) {
+    const int lo = mp.lo[g], hi = mp.hi[g];
+    if (mp.kind[g] == kPrefix || mp.kind[g] == kDiag) {
+      // [J_lo][r] view of the first mode (prefix: rl == 1; diag: the table)
+      const float* in = ch.m[lo].s;
+      int64_t rows = ch.m[lo].J;
+      for (int o = lo + 1; o < hi; ++o) {
+        float* out = reinterpret_cast<float*>(base + mp.lvl[o]);
+        const int64_t total = rows * ch.m[o].J * ch.m[o].rr;
+        if (total > 0) table_prefix_step<<<grid(total), 256, 0, st>>>(ch.m[o], in, rows, out);
+        int rc = check_launch("table_prefix_step");
+        if (rc) return rc;
+        in = out;
+        rows *= ch.m[o].J;
+      }
+    } else if (mp.kind[g] == kSuffix) {
+      const float* in = ch.m[hi - 1].s;  // [J][r][1] == [J][r]
+      int64_t n = ch.m[hi - 1].J;
+      for (int o = hi - 2; o >= lo; --o) {
+        float* out = reinterpret_cast<float*>(base + mp.lvl[o]);
+        const ModeDev& md = ch.m[o];
+        if ((int64_t)md.J * n * md.rl > 0) {
+          const int per = 256 / md.rl;
+          const int gx = (int)std::min<int64_t>(ceil_div(n, per), std::max<int64_t>(1, grid_cap / md.J));
+          table_suffix_step<<<dim3(gx, md.J), 256, 0, st>>>(md, in, n, out);
+        }
+        int rc = check_launch("table_suffix_step");
+        if (rc) return rc;
+        in = out;
+        n *= md.J;
+      }
     }
-    int rc = check_launch("table_suffix_step");
-    if (rc) return rc;
-    in = o;
-    n *= ch.m[k].J;
   }
   return TNB_OK;
 }
 
-void set_vmap(const ChainDev& ch, const MergePlan& mp, int vn, BPlan* bp) {
-  const int N = ch.n;
-  bp->n0 = N;
-  for (int o = 0; o < N; ++o) {
-    bp->oJ[o] = ch.m[o].J;
-    bp->vmap[o] = (int8_t)(o < mp.a ? 0 : (o >= N - mp.b ? vn - 1 : o - mp.a + 1));
-  }
+int table_launches(const MergePlan& mp) {
+  int n = 0;
+  for (int g = 0; g < mp.ng; ++g)
+    if (mp.kind[g] != kOrig) n += mp.hi[g] - mp.lo[g] - 1;
+  return n;
+}
+
+void set_vmap(const ChainDev& ch, const MergePlan& mp, BPlan* bp) {
+  bp->n0 = ch.n;
+  for (int g = 0; g < mp.ng; ++g)
+    for (int o = mp.lo[g]; o < mp.hi[g]; ++o) {
+      bp->oJ[o] = ch.m[o].J;
+      bp->vmap[o] = (int8_t)g;
+    }
 }
 
 int pick_R(int rmax) {
@@ -1148,23 +1187,32 @@ void bucketed_info(const ChainDev& ch, int64_t m, tnb_entries_info* info) {
   ChainDev v;
   virtual_chain(ch, mp, nullptr, &v);
   info->n_virtual = v.n;
-  info->prefix_modes = mp.a;
-  info->suffix_modes = mp.b;
-  info->prefix_rows = mp.a > 1 ? mp.Jp : 0;
-  info->suffix_rows = mp.b > 1 ? mp.Js : 0;
+  info->prefix_modes = mp.a();
+  info->suffix_modes = mp.b();
+  info->prefix_rows = mp.a() > 1 ? mp.rows[0] : 0;
+  info->suffix_rows = mp.b() > 1 ? mp.rows[mp.ng - 1] : 0;
+  info->diag_tables = 0;
+  info->table_launches = table_launches(mp);
   info->kernel_flops = chain_entry_flops(v) * (double)m;
   double tf = 0.0;
-  int64_t rows = ch.m[0].J;
-  for (int k = 1; k < mp.a; ++k) {
-    const ModeDev& md = ch.m[k];
-    rows *= md.J;
-    tf += (double)rows * md.rr * (md.layout == TNB_LAYOUT_DIAG ? 1.0 : 2.0 * md.rl);
-  }
-  rows = ch.m[ch.n - 1].J;
-  for (int k = ch.n - 2; k >= ch.n - mp.b; --k) {
-    const ModeDev& md = ch.m[k];
-    rows *= md.J;
-    tf += (double)rows * md.rl * (md.layout == TNB_LAYOUT_DIAG ? 1.0 : 2.0 * md.rr);
+  for (int g = 0; g < mp.ng; ++g) {
+    const int lo = mp.lo[g], hi = mp.hi[g];
+    if (mp.kind[g] == kDiag) ++info->diag_tables;
+    if (mp.kind[g] == kPrefix || mp.kind[g] == kDiag) {
+      int64_t rows = ch.m[lo].J;
+      for (int o = lo + 1; o < hi; ++o) {
+        const ModeDev& md = ch.m[o];
+        rows *= md.J;
+        tf += (double)rows * md.rr * (md.layout == TNB_LAYOUT_DIAG ? 1.0 : 2.0 * md.rl);
+      }
+    } else if (mp.kind[g] == kSuffix) {
+      int64_t rows = ch.m[hi - 1].J;
+      for (int o = hi - 2; o >= lo; --o) {
+        const ModeDev& md = ch.m[o];
+        rows *= md.J;
+        tf += (double)rows * md.rl * (md.layout == TNB_LAYOUT_DIAG ? 1.0 : 2.0 * md.rr);
+      }
+    }
   }
   info->table_flops = tf;
 }
@@ -1189,7 +1237,7 @@ int launch_entries_bucketed(const ChainDev& ch, const int64_t* idx, int64_t m, f
     if (rc) return rc;
     virtual_chain(ch, mp, base, &v);
   }
-  set_vmap(ch, mp, v.n, &bp);
+  set_vmap(ch, mp, &bp);
   ws = base + mp.table_bytes;
   const ChainDev& chv = v;
   unsigned char* w = static_cast<unsigned char*>(ws);

@@ -184,8 +184,11 @@ def test_entries_plan_merges_cfg2_and_cfg5(lib, monkeypatch):
     # cfg5: TT 0-3 (r=24), CP 4-7 (diag interior, dense right end), J=128
     specs5 = [(0, 128, 1, 24)] + [(0, 128, 24, 24)] * 3 + [(1, 128, 24, 24)] * 3 + [(0, 128, 24, 1)]
     info5 = N.entries_plan(_chain(specs5), 1 << 26)
-    # prefix 0-1 (16384 rows); the CP-only suffix saves no dense step: kept
-    assert (info5["prefix_modes"], info5["suffix_modes"], info5["n_virtual"]) == (2, 1, 7)
+    # prefix 0-1 and CP suffix 6-7 tables (16384 rows each), CP 4-5 as one
+    # diagonal product table: virtual chain P01, G2, G3, D45, S67
+    assert (info5["prefix_modes"], info5["suffix_modes"], info5["n_virtual"]) == (2, 2, 5)
+    assert info5["diag_tables"] == 1 and info5["table_launches"] == 3
+    assert info5["kernel_flops"] == (2 * 2 * 24 * 24 + 24 + 2 * 24) * float(1 << 26)
     # smaller m: tables limited to m / 16 rows (2^16 -> 32*32 rows per side);
     # the chain kernel below 2^16 samples
     small = N.entries_plan(_chain(specs), 1 << 16)

@@ -303,8 +303,20 @@ MERGE_CASES = {
         ("cp", rng.standard_normal((4, 6)).astype(np.float32), None),
         ("tt", rng.standard_normal((6, 5, 1)).astype(np.float32), None),
     ],
-    # cfg5 structure: prefix 0-1, suffix 6-7 (CP), CP 4-5 folded into the last mode
+    # cfg5 structure: prefix 0-1, CP suffix 6-7, CP 4-5 as a diagonal product
+    # table folded into the last mode
     "cfg5": lambda rng: O.cfg5_nodes(seed=2),
+    # no prefix/suffix (large extents); the interior CP run 2-4 becomes one
+    # diagonal product table between two sorted modes
+    "cp_run": lambda rng: [
+        ("tt", rng.standard_normal((1, 200, 5)).astype(np.float32), None),
+        ("tt", rng.standard_normal((5, 150, 5)).astype(np.float32) * 0.45, None),
+        ("cp", rng.standard_normal((10, 5)).astype(np.float32), None),
+        ("cp", rng.standard_normal((12, 5)).astype(np.float32), None),
+        ("cp", rng.standard_normal((9, 5)).astype(np.float32), None),
+        ("tt", rng.standard_normal((5, 160, 5)).astype(np.float32) * 0.45, None),
+        ("tt", rng.standard_normal((5, 170, 1)).astype(np.float32), None),
+    ],
 }
 
 
