@@ -472,10 +472,20 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
           const int cc = c < CH ? c : 0;  // idle lanes (R = 24) re-read chunk 0
           const int kf = (FOLD && fold >= 0) ? fold : N - 1;
           const int nf = N - 1 - kf;  // folded CP modes
-          constexpr int U = FOLD ? 2 : 4;  // samples per lane group in flight
+          // loop-invariant sources of the first MF folded modes (slot i >= nf
+          // re-reads mode kf and is multiplied in as 1)
+          constexpr int MF = 1;  // after diagonal merging a folded run is usually one mode
+          const float* dps[MF];
+          const IdxT* dcs[MF];
+#pragma unroll
+          for (int i = 0; i < MF; ++i) {
+            const int kk = kf + (i < nf ? i : 0);
+            dps[i] = FOLD ? ch.m[kk].s : md.s;
+            dcs[i] = cidx + (size_t)kk * T;
+          }
+          constexpr int U = 4;  // samples per lane group in flight (L2 latency)
           for (int base = warp * (U * SPW); base < tn; base += nwarps * U * SPW) {
             // every load of the U samples is issued before any use
-            constexpr int MF = FOLD ? 4 : 1;
             float4 gv[U], v[U], dv[U][MF];
             bool act[U];
 #pragma unroll
@@ -487,9 +497,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
               if constexpr (FOLD) {
 #pragma unroll
                 for (int i = 0; i < MF; ++i)
-                  dv[u][i] = (i < nf) ? __ldg(reinterpret_cast<const float4*>(
-                                            ch.m[kf + i].s + (int64_t)cidx[(size_t)(kf + i) * T + sc] * R) + cc)
-                                      : make_float4(1.f, 1.f, 1.f, 1.f);  // x * 1 is exact
+                  dv[u][i] = __ldg(reinterpret_cast<const float4*>(dps[i] + (int64_t)dcs[i][sc] * R) + cc);
               }
               v[u] = lds128(s_state + (uint32_t)sc * (RP * 4) + cc * 16);
             }
@@ -500,12 +508,13 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
               float4 w = gv[u];
               if constexpr (FOLD) {
 #pragma unroll
-                for (int i = 0; i < MF; ++i) {
-                  w.x *= dv[u][i].x;
-                  w.y *= dv[u][i].y;
-                  w.z *= dv[u][i].z;
-                  w.w *= dv[u][i].w;
-                }
+                for (int i = 0; i < MF; ++i)
+                  if (i < nf) {
+                    w.x *= dv[u][i].x;
+                    w.y *= dv[u][i].y;
+                    w.z *= dv[u][i].z;
+                    w.w *= dv[u][i].w;
+                  }
                 for (int kk = kf + MF; kk < N - 1; ++kk) {
                   const float4 d =
                       __ldg(reinterpret_cast<const float4*>(ch.m[kk].s + (int64_t)cidx[(size_t)kk * T + s] * R) + cc);
