@@ -29,6 +29,12 @@
 // on the sort order or the tile a sample lands in.
 #include <algorithm>
 
+// state row padding in floats (sorted modes read rows in permuted order, so a
+// pad buys little; 0 maximises the tile size)
+#ifndef TNB_RPAD
+#define TNB_RPAD 0
+#endif
+
 #include "common.cuh"
 
 namespace tnb {
@@ -89,7 +95,7 @@ struct Geo {
   static constexpr int L = R / C;              // lanes per sample group
   static constexpr int G = 32 / L;             // sample groups per warp
   static constexpr int P = 8 / G;              // passes per iteration (8 samples)
-  static constexpr int RP = R + 4;             // padded state row (bank spread)
+  static constexpr int RP = R + TNB_RPAD;       // state row stride (floats)
   static_assert(L * C == R && 32 % L == 0 && G * P == 8, "geometry");
 };
 
@@ -1073,7 +1079,7 @@ int make_bplan(const ChainDev& ch, int64_t m, BPlan* bp, int* R_out, int* nt_out
     }
   }
   const int NT = bucket_threads();
-  const int RP = R + 4;
+  const int RP = R + TNB_RPAD;
   const int idx_bytes = small ? 1 : 2;
   const int jpad = ((jmax + 1) + 7) & ~7;
   const size_t budget = (size_t)(233472 / (NT <= 256 ? 2 : 1)) - 1024;
@@ -1135,7 +1141,7 @@ int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m
     rc = check_launch("entries_sort");
     if (rc) return rc;
   }
-  const size_t csmem = compute_smem(bp.T, R + 4, ch.n, (int)sizeof(IdxT), bp.jpad);
+  const size_t csmem = compute_smem(bp.T, R + TNB_RPAD, ch.n, (int)sizeof(IdxT), bp.jpad);
   auto ck = entries_compute_kernel<R, IdxT, NT, FOLD>;
   rc = check_cuda(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem),
                   "compute smem attr");
