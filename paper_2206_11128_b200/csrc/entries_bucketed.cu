@@ -77,6 +77,11 @@ __device__ __forceinline__ uint64_t ldg_b64(const float* p) {
   asm volatile("ld.global.nc.b64 %0, [%1];" : "=l"(v) : "l"(p));
   return v;
 }
+__device__ __forceinline__ ulonglong2 ldg_u2(const float* p) {
+  ulonglong2 v;
+  asm volatile("ld.global.nc.v2.b64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p));
+  return v;
+}
 __device__ __forceinline__ uint64_t pack2(float lo, float hi) {
   uint64_t v;
   asm("mov.b64 %0, {%1, %2};" : "=l"(v) : "f"(lo), "f"(hi));
@@ -188,6 +193,7 @@ struct BPlan {
   int32_t oJ[kMaxModes];
   int8_t vmap[kMaxModes];
   int8_t smode[kMaxModes];  // sorted slot -> (virtual) mode
+  int8_t lmaj[kMaxModes];   // sorted mode whose slices are in lane-major order
 };
 
 // prep: one CTA per tile -- reads the tile's n0 int64 index columns
@@ -587,7 +593,14 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
               const float* ngs = md.s + (int64_t)nkey * rl * rr;
               if (lane * 32 < rl * rr) asm volatile("prefetch.global.L1 [%0];" ::"l"(ngs + lane * 32));
             }
-            if (rl == R && rr == R) {
+            if (bp.lmaj[k]) {  // lane-major slice: 8 x 16-byte loads, chunk c = (g2[2c], g2[2c+1])
+#pragma unroll
+              for (int c = 0; c < 8; ++c) {
+                const ulonglong2 v = ldg_u2(gs + (c * 32 + lane) * 4);
+                g2[2 * c] = v.x;
+                g2[2 * c + 1] = v.y;
+              }
+            } else if (rl == R && rr == R) {
 #pragma unroll
               for (int i = 0; i < 16; ++i) g2[i] = ldg_b64(gs + (16 * h + i) * R + 2 * qq);
             } else {
@@ -631,7 +644,24 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
             float g1[C1 ? R : 1];
             const float* gs = md.s + (int64_t)key * rl * rr;
             const int cp = 2 * q, cs = 16 + q;
-            if (rl == R && rr == R) {  // full rank: unpredicated 8-byte loads
+            if (bp.lmaj[k]) {  // lane-major slice: 16-byte loads (g2 pairs, then g1)
+#pragma unroll
+              for (int c = 0; c < R / 2; ++c) {
+                const ulonglong2 v = ldg_u2(gs + (c * L + q) * 4);
+                g2[2 * c] = v.x;
+                g2[2 * c + 1] = v.y;
+              }
+              if constexpr (C1) {
+#pragma unroll
+                for (int c = 0; c < R / 4; ++c) {
+                  const float4 v = __ldg(reinterpret_cast<const float4*>(gs + ((R / 2 + c) * L + q) * 4));
+                  g1[4 * c] = v.x;
+                  g1[4 * c + 1] = v.y;
+                  g1[4 * c + 2] = v.z;
+                  g1[4 * c + 3] = v.w;
+                }
+              }
+            } else if (rl == R && rr == R) {  // full rank: unpredicated 8-byte loads
   #pragma unroll
               for (int a = 0; a < R; ++a) {
                 g2[a] = ldg_b64(gs + a * R + cp);
@@ -714,7 +744,24 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
             uint64_t g2[R];
             float g1[C1 ? R : 1];
             const float* gs = md.s + (int64_t)key * rl * rr;
-            if (rl == R && rr == R) {
+            if (bp.lmaj[k]) {
+#pragma unroll
+              for (int c = 0; c < R / 2; ++c) {
+                const ulonglong2 v = ldg_u2(gs + (c * L + q) * 4);
+                g2[2 * c] = v.x;
+                g2[2 * c + 1] = v.y;
+              }
+              if constexpr (C1) {
+#pragma unroll
+                for (int c = 0; c < R / 4; ++c) {
+                  const float4 v = __ldg(reinterpret_cast<const float4*>(gs + ((R / 2 + c) * L + q) * 4));
+                  g1[4 * c] = v.x;
+                  g1[4 * c + 1] = v.y;
+                  g1[4 * c + 2] = v.z;
+                  g1[4 * c + 3] = v.w;
+                }
+              }
+            } else if (rl == R && rr == R) {
 #pragma unroll
               for (int a = 0; a < R; ++a) {
                 g2[a] = ldg_b64(gs + a * R + cp);
@@ -858,6 +905,46 @@ __global__ void __launch_bounds__(256) table_suffix_step(ModeDev md, const float
   (void)J;
 }
 
+// Lane-major copy of a full-rank (R x R) sorted mode: the values one lane of
+// the compute kernel holds are contiguous 16-byte chunks, chunk-major across
+// lanes ([chunk][lane][4]) so a warp's load of chunk c is coalesced.
+//   R == 32 (K-split, lane = 16h + qq): chunk c = G[16h+2c][2qq..], G[16h+2c+1][2qq..]
+//   R <= 24 (Geo, lane q of L): float f < 2R -> G[f/2][2q + f%2],
+//                                f >= 2R   -> G[f-2R][16+q]   (R == 24 only)
+__global__ void lane_major_kernel(const float* __restrict__ src, float* __restrict__ dst, int J, int R) {
+  const int L = R == 32 ? 32 : (R == 24 ? 8 : R / 2);
+  const int per = R * R;
+  const int64_t total = (int64_t)J * per;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = t / per;
+    const int r = (int)(t - j * per);
+    const int c = r / (L * 4), q = (r / 4) % L, e = r & 3;
+    int a, col;
+    if (R == 32) {
+      a = 16 * (q >> 4) + 2 * c + (e >> 1);
+      col = 2 * (q & 15) + (e & 1);
+    } else {
+      const int f = 4 * c + e;
+      if (f < 2 * R) {
+        a = f >> 1;
+        col = 2 * q + (f & 1);
+      } else {
+        a = f - 2 * R;
+        col = 16 + q;
+      }
+    }
+    dst[t] = __ldg(src + j * per + a * R + col);
+  }
+}
+
+int pick_R(int rmax);
+
+int lane_major_env() {
+  const char* e = getenv("TNB_LANE_MAJOR");
+  return (e && e[0] == '0') ? 0 : 1;
+}
+
 // Mode merging: the original modes are partitioned into groups, each one
 // VIRTUAL mode of the chain the kernels run:
 //   prefix [0, a)      -> dense table P[(j_0..j_{a-1})][r_a]    (first mode)
@@ -877,6 +964,9 @@ struct MergePlan {
   int kind[kMaxModes];
   int64_t rows[kMaxModes];
   int64_t lvl[kMaxModes];        // byte offset of the level ending at original mode o
+  int8_t lm[kMaxModes];          // virtual mode g gets a lane-major copy ...
+  int64_t lm_off[kMaxModes];     // ... at this byte offset
+  int R = 0;                     // register geometry of the virtual chain
   int64_t table_bytes = 0;       // 256-aligned
   int a() const { return kind[0] == kPrefix ? hi[0] - lo[0] : 1; }
   int b() const { return kind[ng - 1] == kSuffix ? hi[ng - 1] - lo[ng - 1] : 1; }
@@ -903,6 +993,7 @@ void plan_merge(const ChainDev& ch, int64_t m, MergePlan* mp) {
     mp->hi[0] = 1;
     mp->kind[0] = kOrig;
     mp->rows[0] = ch.m[0].J;
+    mp->lm[0] = 0;
     return;
   }
   int g = 0;
@@ -947,6 +1038,24 @@ void plan_merge(const ChainDev& ch, int64_t m, MergePlan* mp) {
       }
     }
   }
+  // lane-major copies of the full-rank sorted modes of the virtual chain
+  int vr = 1;
+  for (int v = 0; v < g; ++v) {
+    const int lo = mp->lo[v], hi = mp->hi[v];
+    const int rl = mp->kind[v] == kPrefix ? 1 : ch.m[lo].rl;
+    const int rr = mp->kind[v] == kSuffix ? 1 : ch.m[hi - 1].rr;
+    vr = max(vr, max(rl, rr));
+  }
+  mp->R = pick_R(vr);
+  for (int v = 0; v < g; ++v) {
+    const ModeDev& md = ch.m[mp->lo[v]];
+    mp->lm[v] = (int8_t)(lane_major_env() && mp->R && v > 0 && v < g - 1 && mp->kind[v] == kOrig &&
+                         md.layout == TNB_LAYOUT_DENSE && md.rl == mp->R && md.rr == mp->R);
+    if (mp->lm[v]) {
+      mp->lm_off[v] = off;
+      off += ((int64_t)md.J * md.rl * md.rr * 4 + 255) & ~(int64_t)255;
+    }
+  }
   mp->table_bytes = off;
 }
 
@@ -974,6 +1083,7 @@ void virtual_chain(const ChainDev& ch, const MergePlan& mp, unsigned char* base,
         d.rr = 1;
       }  // kDiag keeps layout DIAG and rl == rr == R
     }
+    if (mp.lm[g]) d.s = base ? reinterpret_cast<const float*>(base + mp.lm_off[g]) : nullptr;
     v->m[g] = d;
     rmax = max(rmax, max(d.rl, d.rr));
   }
@@ -1000,6 +1110,12 @@ int build_tables(const ChainDev& ch, const MergePlan& mp, unsigned char* base, c
         in = out;
         rows *= ch.m[o].J;
       }
+    } else if (mp.lm[g]) {
+      const ModeDev& md = ch.m[lo];
+      lane_major_kernel<<<grid((int64_t)md.J * md.rl * md.rr), 256, 0, st>>>(
+          md.s, reinterpret_cast<float*>(base + mp.lm_off[g]), md.J, md.rl);
+      int rc = check_launch("lane_major");
+      if (rc) return rc;
     } else if (mp.kind[g] == kSuffix) {
       const float* in = ch.m[hi - 1].s;  // [J][r][1] == [J][r]
       int64_t n = ch.m[hi - 1].J;
@@ -1024,12 +1140,13 @@ int build_tables(const ChainDev& ch, const MergePlan& mp, unsigned char* base, c
 int table_launches(const MergePlan& mp) {
   int n = 0;
   for (int g = 0; g < mp.ng; ++g)
-    if (mp.kind[g] != kOrig) n += mp.hi[g] - mp.lo[g] - 1;
+    n += mp.kind[g] != kOrig ? mp.hi[g] - mp.lo[g] - 1 : mp.lm[g];
   return n;
 }
 
 void set_vmap(const ChainDev& ch, const MergePlan& mp, BPlan* bp) {
   bp->n0 = ch.n;
+  for (int g = 0; g < mp.ng; ++g) bp->lmaj[g] = mp.lm[g];
   for (int g = 0; g < mp.ng; ++g)
     for (int o = mp.lo[g]; o < mp.hi[g]; ++o) {
       bp->oJ[o] = ch.m[o].J;

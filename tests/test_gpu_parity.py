@@ -229,9 +229,12 @@ def test_bucketed_tiles_and_tails(m, algo):
         tb.entries(t, bad, algo=algo)
 
 
+@pytest.mark.parametrize("lane_major", ["1", "0"])
 @pytest.mark.parametrize("r,J", [(8, 300), (16, 40), (24, 128), (32, 32), (32, 1024)])
-def test_bucketed_rank_classes(r, J):
-    # every register geometry (R = 8/16/24/32) and the uint16 index path
+def test_bucketed_rank_classes(r, J, lane_major, monkeypatch):
+    # every register geometry (R = 8/16/24/32), the uint16 index path, and
+    # core slices read from lane-major copies or from the repacked cores
+    monkeypatch.setenv("TNB_LANE_MAJOR", lane_major)
     cores = O.random_tt((J, J, 5, J), r, seed=r + J, scale=r ** -0.5)
     t = facade([("tt", c, None) for c in cores])
     o = O.make_chain([("tt", c) for c in cores])
