@@ -64,6 +64,19 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// L tiles are re-read once per column block: keep them in L2 (evict_last)
+// while the output streams past them (st.global.cs = evict-first)
+__device__ __forceinline__ void bulk_g2s_keep(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+      "%4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void st_stream(float* p, uint32_t v) {
+  asm volatile("st.global.cs.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_commit(uint64_t* b) {
@@ -269,13 +282,15 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
   } else if (warp == 1) {
     // ================= producer: L tiles -> smem ring =================
     if (lane == 0) {
+      uint64_t keep;
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
       uint32_t it = 0;
       for (int64_t t = t0; t < t1; ++t) {
         const int64_t mt = t % n_mt;
         const int s = it % kStages;
         mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
         mbar_expect_tx(&full[s], kTileBytes);
-        bulk_g2s(sL + s * kTileBytes, args.Ls + mt * kTileBytes, kTileBytes, &full[s]);
+        bulk_g2s_keep(sL + s * kTileBytes, args.Ls + mt * kTileBytes, kTileBytes, &full[s], keep);
         ++it;
       }
     }
@@ -308,13 +323,13 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
             // one st.global per row: the warp's 32 lanes write 128 contiguous bytes
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-              *p = __uint_as_float(cur[j]);
+              st_stream(p, cur[j]);
               p += ldc;
             }
           } else {
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-              if (cok && ch * 32 + j < rows_left) *p = __uint_as_float(cur[j]);
+              if (cok && ch * 32 + j < rows_left) st_stream(p, cur[j]);
               p += ldc;
             }
           }
