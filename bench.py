@@ -324,10 +324,12 @@ def bench_entries(args, cfg, dev, dist, ws, rank):
     # indices + K1 + D2H of the step's output, every step
     e2e_steps = max(2, min(args.steps, 3))
 
+    out_pin = torch.empty(m, dtype=torch.float32).pin_memory()  # reused, like a serving loop would
+
     def e2e_step():
-        res = tb.entries(t, idx_host)  # façade: H2D, launch, error-word check
-        host = res.cpu()
-        return host
+        # façade: chunked H2D of the pinned indices, launches, error-word
+        # check and the D2H of every chunk's values into pinned host memory
+        return tb.entries(t, idx_host, out=out_pin)
 
     e2e_step()
     torch.cuda.synchronize()
@@ -344,7 +346,7 @@ def bench_entries(args, cfg, dev, dist, ws, rank):
         el = float(tt_.item())
     fields["e2e"] = {"value": ws * m * e2e_steps / el, "unit": "entries/s",
                      "h2d_bytes_per_step": idx_host.numel() * 8, "d2h_bytes_per_step": m * 4,
-                     "steps": e2e_steps, "path": "paper_2206_11128_b200.entries(t, pinned host int64) + .cpu()"}
+                     "steps": e2e_steps, "path": "paper_2206_11128_b200.entries(t, pinned host int64, out=pinned host float32)"}
     fields["_t"], fields["_out"], fields["_idx_host"] = t, out, idx_host
     return fields
 
@@ -397,7 +399,7 @@ def bench_full(dev, steps, warmup, dist):
     del out
     peak, src = hbm_peak()
     k_ms = g_ms / g_n if g_n else ms
-    traffic, tsrc = ncu_traffic("cfg3_full", "full_tc_kernel")
+    traffic, tsrc = ncu_traffic("cfg3_full", "full_tc_gemm_kernel")
     return {"op": "full", "workload": "cfg3", "ms_per_step": ms, "GB/s": nbytes / (ms * 1e-3) / 1e9,
             "bytes_written": nbytes,
             "roofline": {"bound": "hbm", "achieved": nbytes / (k_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
@@ -446,11 +448,12 @@ def bench_dot(dev, steps, warmup, dist, is_norm=False):
     per_pair = sum(ranks[k] * s * ranks[k + 1] for k, s in enumerate(shape)) * 4
     nbytes = 4096 * per_pair * (1 if is_norm else 2)
     peak, src = hbm_peak()
+    traffic, tsrc = ncu_traffic("cfg4_dot", "dot_r16_kernel") if not is_norm else (None, None)
     return {"op": "norm" if is_norm else "dot", "workload": "cfg4", "ms_per_step": ms,
             "pairs/s": 4096 / (ms * 1e-3), "GB/s": nbytes / (ms * 1e-3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": nbytes / (k_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
-                         "frac": nbytes / (k_ms * 1e-3) / 1e9 / peak, "traffic": None, "peak_source": src,
-                         "kernel": "dot_r16_kernel", "kernel_ms": k_ms,
+                         "frac": nbytes / (k_ms * 1e-3) / 1e9 / peak, "traffic": traffic, "traffic_source": tsrc,
+                         "peak_source": src, "kernel": "dot_r16_kernel", "kernel_ms": k_ms,
                          "algorithmic": f"{nbytes} core bytes read per launch (each core read once)"}}
 
 

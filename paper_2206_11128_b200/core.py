@@ -415,9 +415,12 @@ def _index_tensor(t: TnTensor, indices, device) -> torch.Tensor:
 _PIPELINE_ROWS = 1 << 21
 
 
-def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: int) -> torch.Tensor:
+def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: int,
+                       out_host: Optional[torch.Tensor] = None) -> torch.Tensor:
     """entries() for a large PINNED int64 host index matrix: chunked
-    copy-stream H2D overlapped with the K1 launches on the compute stream."""
+    copy-stream H2D overlapped with the K1 launches on the compute stream;
+    with a pinned host ``out_host`` each chunk's values are copied back on a
+    second copy stream (PCIe is full duplex) behind the next chunk's work."""
     dev = p.device
     m = int(idx_host.shape[0])
     chunk = _PIPELINE_ROWS
@@ -430,6 +433,7 @@ def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: in
     errs = torch.empty(nch, dtype=torch.int32, device=dev)
     bufs = [torch.empty((chunk, t.ndim), dtype=torch.int64, device=dev) for _ in range(2)]
     done = [torch.cuda.Event() for _ in range(2)]  # compute finished with buffer b
+    back = torch.cuda.Stream(dev) if out_host is not None else None
     ws = None
     if algo == N.ALGO_AUTO and N.load().tnb_entries_workspace_bytes(
             ctypes.byref(p.chain), chunk, N.ALGO_BUCKETED) > 0:
@@ -451,32 +455,71 @@ def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: in
         buf.record_stream(comp)
         ws = launch_entries(p, buf, out[lo:lo + chunk], errs[c:c + 1], algo, ws)
         done[b].record(comp)
+        if back is not None:
+            back.wait_event(done[b])
+            with torch.cuda.stream(back):
+                out_host[lo:hi].copy_(out[lo:hi], non_blocking=True)
     code = int(errs.min().item())
+    if back is not None:
+        back.synchronize()
     if code < t.ndim:
         raise ContractViolationError(f"index out of bounds on mode {code}")
-    return out[:m]
+    return out_host if out_host is not None else out[:m]
 
 
-def entries(t: TnTensor, indices, *, algo: int = N.ALGO_AUTO) -> torch.Tensor:
-    """Values at explicit multi-indices: shape (M,), or (M, B) if batched."""
+def _check_out(t: TnTensor, p: _Packed, out: torch.Tensor, m: int) -> None:
+    b = t.batch_size
+    shape = (m, b) if b else (m,)
+    if (not isinstance(out, torch.Tensor) or out.dtype != torch.float32 or tuple(out.shape) != shape
+            or not out.is_contiguous()):
+        raise ContractViolationError(f"out must be a contiguous float32 tensor of shape {shape}")
+    if out.device.type == "cpu":
+        if not out.is_pinned():
+            raise ContractViolationError("a host out tensor must be in pinned memory")
+    elif out.device != p.device:
+        raise ContractViolationError(f"out is on {out.device}, the tensor on {p.device}")
+
+
+def entries(t: TnTensor, indices, *, algo: int = N.ALGO_AUTO,
+            out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Values at explicit multi-indices: shape (M,), or (M, B) if batched.
+
+    ``out`` (optional): a contiguous float32 tensor of that shape, either on
+    the tensor's device or in PINNED host memory; the values are written
+    there and ``out`` is returned (a host ``out`` is complete on return).
+    """
     p = t._packed()
+    host_out = out is not None and out.device.type == "cpu"
     if (isinstance(indices, torch.Tensor) and indices.device.type == "cpu" and indices.is_pinned()
             and indices.dtype == torch.int64 and indices.dim() == 2 and indices.shape[1] == t.ndim
             and indices.is_contiguous() and indices.shape[0] >= 2 * _PIPELINE_ROWS
             and t.batch_size is None):
-        return _entries_pipelined(t, p, indices, algo)
+        if out is not None:
+            _check_out(t, p, out, int(indices.shape[0]))
+        res = _entries_pipelined(t, p, indices, algo, out if host_out else None)
+        if out is not None and not host_out:
+            out.copy_(res)
+            return out
+        return res
     idx = _index_tensor(t, indices, p.device)
     m = int(idx.shape[0])
     b = t.batch_size
-    out = torch.empty((m, b) if b else (m,), dtype=torch.float32, device=p.device)
+    if out is not None:
+        _check_out(t, p, out, m)
+    dev_out = out if (out is not None and not host_out) else \
+        torch.empty((m, b) if b else (m,), dtype=torch.float32, device=p.device)
     if m == 0:
-        return out
+        return out if out is not None else dev_out
     err = torch.empty(1, dtype=torch.int32, device=p.device)
-    launch_entries(p, idx, out, err, algo)
+    launch_entries(p, idx, dev_out, err, algo)
+    if host_out:
+        out.copy_(dev_out, non_blocking=True)
     code = int(err.item())
+    if host_out:
+        torch.cuda.current_stream(p.device).synchronize()
     if code < t.ndim:
         raise ContractViolationError(f"index out of bounds on mode {code}")
-    return out
+    return out if out is not None else dev_out
 
 
 def launch_entries(p: _Packed, idx: torch.Tensor, out: torch.Tensor, err: torch.Tensor,

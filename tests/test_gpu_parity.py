@@ -345,3 +345,32 @@ def test_bucketed_mode_merging(case, merge, monkeypatch):
         bad[m // 2, t.ndim - 1] = -t.shape[t.ndim - 1] - 1
         with pytest.raises(tb.ContractViolationError, match=f"mode {k}"):
             tb.entries(t, bad, algo=N.ALGO_BUCKETED)
+
+
+def test_entries_out_argument():
+    # out= on the device or in pinned host memory (pipelined and direct paths)
+    from paper_2206_11128_b200 import core as C
+
+    cores = O.random_tt((16,) * 5, 8, seed=21, scale=0.4)
+    t = facade([("tt", c, None) for c in cores])
+    m = 2 * C._PIPELINE_ROWS + 777
+    idx = torch.from_numpy(O.uniform_indices((16,) * 5, m, 4)).pin_memory()
+    ref = tb.entries(t, idx.cuda())
+    host = torch.empty(m, dtype=torch.float32).pin_memory()
+    assert tb.entries(t, idx, out=host) is host
+    assert torch.equal(host, ref.cpu())
+    dev = torch.empty(m, dtype=torch.float32, device="cuda")
+    assert tb.entries(t, idx, out=dev) is dev and torch.equal(dev, ref)
+    small = idx[:1000].clone()
+    h2 = torch.empty(1000, dtype=torch.float32).pin_memory()
+    assert torch.equal(tb.entries(t, small, out=h2), tb.entries(t, small.cuda()).cpu())
+    with pytest.raises(tb.ContractViolationError, match="pinned"):
+        tb.entries(t, small, out=torch.empty(1000, dtype=torch.float32))
+    with pytest.raises(tb.ContractViolationError, match="shape"):
+        tb.entries(t, small, out=torch.empty(999, dtype=torch.float32).pin_memory())
+    with pytest.raises(tb.ContractViolationError, match="float32"):
+        tb.entries(t, small, out=torch.empty(1000, dtype=torch.float64).pin_memory())
+    bad = idx.clone()
+    bad[m - 3, 2] = 16
+    with pytest.raises(tb.ContractViolationError, match="mode 2"):
+        tb.entries(t, bad.pin_memory(), out=host)
