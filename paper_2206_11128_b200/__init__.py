@@ -8,7 +8,7 @@ the hot path; compute runs in libtnb.so (hand-written sm_100a CUDA behind the
 C ABI of include/tnb.h).  There is no CPU fallback.
 """
 
-from . import arithmetic, indexing
+from . import arithmetic, callers, indexing, serialization
 from .arithmetic import dot
 from .core import (
     CP,
@@ -25,8 +25,18 @@ from .core import (
     norm,
     promote_cp_node,
 )
-from .errors import ContractViolationError, NativeError, StructuralError, TntzError
+from .errors import (
+    ChecksumError,
+    ContractViolationError,
+    DataError,
+    MagicError,
+    NativeError,
+    SizeError,
+    StructuralError,
+    TntzError,
+)
 from .indexing import getitem
+from .serialization import load, read_dense, read_header, save, write_dense
 
 Tensor = TnTensor  # tntorch spelling
 
@@ -35,5 +45,6 @@ __version__ = "0.1.0"
 __all__ = [
     "CP", "TT", "INTERIOR", "LEFT_BOUNDARY", "RIGHT_BOUNDARY", "ModeNode", "TnTensor", "Tensor",
     "chain_dot", "dot", "entries", "full", "getitem", "node_tt_core", "norm", "promote_cp_node",
-    "ContractViolationError", "StructuralError", "TntzError", "NativeError",
+    "ContractViolationError", "StructuralError", "TntzError", "NativeError", "DataError", "MagicError",
+    "ChecksumError", "SizeError", "load", "save", "read_header", "read_dense", "write_dense",
 ]
