@@ -73,6 +73,80 @@ __device__ __forceinline__ void sts128x2(uint32_t a, uint64_t p0, uint64_t p1) {
   asm volatile("st.shared.v2.b64 [%0], {%1, %2};" ::"r"(a), "l"(p0), "l"(p1) : "memory");
 }
 
+// Split-TF32 on mma.sync m16n8k8: x = hi + lo (both tf32; lo's rounding
+// residual is <= 2^-23 |x|), D += [Alo*Blo +] Alo*Bhi + Ahi*Blo + Ahi*Bhi in
+// fp32.  The lo*lo term (TNB_DOT_4TERM) halves the per-product error, which
+// cfg4's heavily cancelling dots need to stay inside 1e-5.
+#ifndef TNB_DOT_4TERM
+#define TNB_DOT_4TERM 0
+#endif
+__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
+  const float r = x - __uint_as_float(hi);
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo) : "f"(r));
+}
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void mma3(float (&d)[4], const uint32_t (&ah)[4], const uint32_t (&al)[4], float b0,
+                                     float b1) {
+  uint32_t h0, l0, h1, l1;
+  split_tf32(b0, h0, l0);
+  split_tf32(b1, h1, l1);
+#if TNB_DOT_4TERM
+  mma_tf32(d, al, l0, l1);
+#endif
+  mma_tf32(d, al, h0, h1);
+  mma_tf32(d, ah, l0, l1);
+  mma_tf32(d, ah, h0, h1);
+}
+
+// One interior slice on tensor cores.  Fragments (m16n8k8 tf32, g = lane/4,
+// t = lane%4) with the K slots permuted: slot t <-> index 2t, slot t+4 <->
+// 2t+1 of each 8-chunk kc.  Then the accumulator fragment of one product is
+// exactly the B fragment of the next, so M and Y never leave registers:
+//   Mc[nt] = {M[g][8nt+2t], M[g][8nt+2t+1], M[g+8][8nt+2t], M[g+8][8nt+2t+1]}
+//   step 1: Y^T = B_j^T M^T   (A = B_j^T from smem, B(kc, nt) = Mc[kc] halves)
+//   step 2: Mw += A_j^T Y     (A = A_j^T from smem, B(kc, nt) = Y^T halves)
+__device__ __forceinline__ void slice_afrag(const float* S, int kc, int g, int t, uint32_t (&ah)[4],
+                                            uint32_t (&al)[4]) {
+  const float* r0 = S + (8 * kc + 2 * t) * 16;
+  split_tf32(r0[g], ah[0], al[0]);
+  split_tf32(r0[g + 8], ah[1], al[1]);
+  split_tf32(r0[16 + g], ah[2], al[2]);
+  split_tf32(r0[16 + g + 8], ah[3], al[3]);
+}
+__device__ __forceinline__ void slice_mma(const float* Aj, const float* Bj, const float (&Mc)[2][4],
+                                          float (&Mw)[2][4], int g, int t) {
+  float Y[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+  for (int kc = 0; kc < 2; ++kc) {
+    uint32_t ah[4], al[4];
+    slice_afrag(Bj, kc, g, t, ah, al);
+    mma3(Y[0], ah, al, Mc[kc][0], Mc[kc][1]);
+    mma3(Y[1], ah, al, Mc[kc][2], Mc[kc][3]);
+  }
+  // this slice's A_j^T Y starts from zero and joins the running partial
+  // with round-to-nearest FADDs: the MMA accumulator only ever sums the 6
+  // products of one slice
+  float Z[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+  for (int kc = 0; kc < 2; ++kc) {
+    uint32_t ah[4], al[4];
+    slice_afrag(Aj, kc, g, t, ah, al);
+    mma3(Z[0], ah, al, Y[kc][0], Y[kc][1]);
+    mma3(Z[1], ah, al, Y[kc][2], Y[kc][3]);
+  }
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) Mw[nt][i] += Z[nt][i];
+}
+
 struct DotArgs {
   ChainDev a, b;  // a.m[k].s + e * bstride = slices of pair e
   float* out;
@@ -85,6 +159,7 @@ struct Walk {
   int k, c;
 };
 
+template <bool MMA>
 __global__ void __launch_bounds__(kThreads, 2) dot_r16_kernel(const __grid_constant__ DotArgs args) {
   extern __shared__ __align__(128) unsigned char smem[];
   float* stA = reinterpret_cast<float*>(smem);                      // [kStages][CH*R*R]
@@ -98,6 +173,7 @@ __global__ void __launch_bounds__(kThreads, 2) dot_r16_kernel(const __grid_const
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ap = lane >> 2, dq = lane & 3;  // rows/cols 2ap,2ap+1 ; 4dq..4dq+3
+  const int fg = lane >> 2, ft = lane & 3;  // mma fragment coordinates (MMA path)
   const int N = args.a.n, J = args.a.m[0].J;
   const int nch = (J + CH - 1) / CH;
   const int64_t B = args.a.batch;
@@ -142,11 +218,13 @@ __global__ void __launch_bounds__(kThreads, 2) dot_r16_kernel(const __grid_const
 
   uint32_t c_it = 0;
   for (int64_t e = blockIdx.x; e < B; e += gridDim.x) {
-    float mrow[2][R];  // M rows 2ap, 2ap+1 (registers)
+    float mrow[2][R];  // M rows 2ap, 2ap+1 (registers, SIMT path)
+    float Mc[2][4];    // M as mma fragments (MMA path)
     for (int k = 0; k < N; ++k) {
       const bool first = (k == 0), last = (k == N - 1);
       uint64_t mn[2][2] = {{0ull, 0ull}, {0ull, 0ull}};
       uint64_t mn2[2][2] = {{0ull, 0ull}, {0ull, 0ull}};  // second slice of the pair
+      float Mw[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};  // MMA partial M
       float lastacc = 0.f;
       float4 mq0 = make_float4(0.f, 0.f, 0.f, 0.f), mq1 = mq0;  // M[2ap(+1)][4dq..]
       if (last && !first) {
@@ -186,6 +264,8 @@ __global__ void __launch_bounds__(kThreads, 2) dot_r16_kernel(const __grid_const
             y1 = fmaf(mq1.w, bv.w, y1);
             lastacc = fmaf(a0, y0, lastacc);
             lastacc = fmaf(a1, y1, lastacc);
+          } else if (MMA) {
+            slice_mma(A + jj * R * R, Bm + jj * R * R, Mc, Mw, fg, ft);
           } else if (jj < kWarps) {
             // two slices per warp (jj, jj + kWarps): 8 independent FFMA2 chains
             const int j2 = jj + kWarps;
@@ -256,6 +336,13 @@ __global__ void __launch_bounds__(kThreads, 2) dot_r16_kernel(const __grid_const
         __syncthreads();
       } else {
         float* rw = red + warp * R * R;
+        if (MMA && !first) {
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            *reinterpret_cast<float2*>(rw + fg * R + 8 * nt + 2 * ft) = make_float2(Mw[nt][0], Mw[nt][1]);
+            *reinterpret_cast<float2*>(rw + (fg + 8) * R + 8 * nt + 2 * ft) = make_float2(Mw[nt][2], Mw[nt][3]);
+          }
+        } else
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           float x0, x1, x2, x3, z0, z1, z2, z3;
@@ -277,10 +364,22 @@ __global__ void __launch_bounds__(kThreads, 2) dot_r16_kernel(const __grid_const
           msm[tid] = v;
         }
         __syncthreads();
+        if (MMA) {
 #pragma unroll
-        for (int i = 0; i < 2; ++i)
+          for (int nt = 0; nt < 2; ++nt) {
+            const float2 u = *reinterpret_cast<const float2*>(msm + fg * R + 8 * nt + 2 * ft);
+            const float2 v = *reinterpret_cast<const float2*>(msm + (fg + 8) * R + 8 * nt + 2 * ft);
+            Mc[nt][0] = u.x;
+            Mc[nt][1] = u.y;
+            Mc[nt][2] = v.x;
+            Mc[nt][3] = v.y;
+          }
+        } else {
 #pragma unroll
-          for (int b = 0; b < R; ++b) mrow[i][b] = msm[(2 * ap + i) * R + b];
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int b = 0; b < R; ++b) mrow[i][b] = msm[(2 * ap + i) * R + b];
+        }
         __syncthreads();
       }
     }
@@ -320,13 +419,14 @@ int launch_dot_fast(const ChainDev& a, const ChainDev& b, float* out, bool is_no
   args.out = out;
   args.norm = is_norm ? 1 : 0;
   const size_t smem = dot_smem(is_norm);
-  int rc = check_cuda(cudaFuncSetAttribute(dot_r16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem),
+  const char* e = getenv("TNB_DOT_SIMT");
+  auto kern = (e && e[0] == '1') ? dot_r16_kernel<false> : dot_r16_kernel<true>;
+  int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                       "dot smem attr");
   if (rc) return rc;
   const int64_t slots = (int64_t)num_sms() * 2;
   const int grid = (int)(a.batch < slots ? a.batch : slots);
-  dot_r16_kernel<<<grid, kThreads, smem, st>>>(args);
+  kern<<<grid, kThreads, smem, st>>>(args);
   return check_launch("dot_r16");
 }
 
