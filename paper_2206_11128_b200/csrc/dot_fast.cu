@@ -92,6 +92,12 @@ __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], 
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
+__device__ __forceinline__ void mma3s(float (&d)[4], const uint32_t (&ah)[4], const uint32_t (&al)[4], uint32_t h0,
+                                      uint32_t h1, uint32_t l0, uint32_t l1) {
+  mma_tf32(d, al, h0, h1);
+  mma_tf32(d, ah, l0, l1);
+  mma_tf32(d, ah, h0, h1);
+}
 __device__ __forceinline__ void mma3(float (&d)[4], const uint32_t (&ah)[4], const uint32_t (&al)[4], float b0,
                                      float b1) {
   uint32_t h0, l0, h1, l1;
@@ -120,15 +126,15 @@ __device__ __forceinline__ void slice_afrag(const float* S, int kc, int g, int t
   split_tf32(r0[16 + g], ah[2], al[2]);
   split_tf32(r0[16 + g + 8], ah[3], al[3]);
 }
-__device__ __forceinline__ void slice_mma(const float* Aj, const float* Bj, const float (&Mc)[2][4],
-                                          float (&Mw)[2][4], int g, int t) {
+__device__ __forceinline__ void slice_mma(const float* Aj, const float* Bj, const uint32_t (&Mh)[2][4],
+                                          const uint32_t (&Ml)[2][4], float (&Mw)[2][4], int g, int t) {
   float Y[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
   for (int kc = 0; kc < 2; ++kc) {
     uint32_t ah[4], al[4];
     slice_afrag(Bj, kc, g, t, ah, al);
-    mma3(Y[0], ah, al, Mc[kc][0], Mc[kc][1]);
-    mma3(Y[1], ah, al, Mc[kc][2], Mc[kc][3]);
+    mma3s(Y[0], ah, al, Mh[kc][0], Mh[kc][1], Ml[kc][0], Ml[kc][1]);
+    mma3s(Y[1], ah, al, Mh[kc][2], Mh[kc][3], Ml[kc][2], Ml[kc][3]);
   }
   // this slice's A_j^T Y starts from zero and joins the running partial
   // with round-to-nearest FADDs: the MMA accumulator only ever sums the 6
@@ -219,7 +225,7 @@ __global__ void __launch_bounds__(kThreads, 2) dot_r16_kernel(const __grid_const
   uint32_t c_it = 0;
   for (int64_t e = blockIdx.x; e < B; e += gridDim.x) {
     float mrow[2][R];  // M rows 2ap, 2ap+1 (registers, SIMT path)
-    float Mc[2][4];    // M as mma fragments (MMA path)
+    uint32_t Mh[2][4], Ml[2][4];  // M as split-TF32 mma fragments (MMA path)
     for (int k = 0; k < N; ++k) {
       const bool first = (k == 0), last = (k == N - 1);
       uint64_t mn[2][2] = {{0ull, 0ull}, {0ull, 0ull}};
@@ -265,7 +271,7 @@ __global__ void __launch_bounds__(kThreads, 2) dot_r16_kernel(const __grid_const
             lastacc = fmaf(a0, y0, lastacc);
             lastacc = fmaf(a1, y1, lastacc);
           } else if (MMA) {
-            slice_mma(A + jj * R * R, Bm + jj * R * R, Mc, Mw, fg, ft);
+            slice_mma(A + jj * R * R, Bm + jj * R * R, Mh, Ml, Mw, fg, ft);
           } else if (jj < kWarps) {
             // two slices per warp (jj, jj + kWarps): 8 independent FFMA2 chains
             const int j2 = jj + kWarps;
@@ -369,10 +375,10 @@ __global__ void __launch_bounds__(kThreads, 2) dot_r16_kernel(const __grid_const
           for (int nt = 0; nt < 2; ++nt) {
             const float2 u = *reinterpret_cast<const float2*>(msm + fg * R + 8 * nt + 2 * ft);
             const float2 v = *reinterpret_cast<const float2*>(msm + (fg + 8) * R + 8 * nt + 2 * ft);
-            Mc[nt][0] = u.x;
-            Mc[nt][1] = u.y;
-            Mc[nt][2] = v.x;
-            Mc[nt][3] = v.y;
+            split_tf32(u.x, Mh[nt][0], Ml[nt][0]);
+            split_tf32(u.y, Mh[nt][1], Ml[nt][1]);
+            split_tf32(v.x, Mh[nt][2], Ml[nt][2]);
+            split_tf32(v.y, Mh[nt][3], Ml[nt][3]);
           }
         } else {
 #pragma unroll
@@ -380,7 +386,8 @@ __global__ void __launch_bounds__(kThreads, 2) dot_r16_kernel(const __grid_const
 #pragma unroll
             for (int b = 0; b < R; ++b) mrow[i][b] = msm[(2 * ap + i) * R + b];
         }
-        __syncthreads();
+        // no barrier here: the next writes of red / msm come after the next
+        // mode's first barrier, which every warp reaches only after these reads
       }
     }
   }
