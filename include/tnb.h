@@ -158,6 +158,31 @@ int tnb_dot_f32(const tnb_chain* a, const tnb_chain* b, float* out, void* stream
 /* out[e] = sqrt(max(<t_e, t_e>, 0))  (core.py:387-391) */
 int tnb_norm_f32(const tnb_chain* t, float* out, void* stream);
 
+/* --- float64 instantiation -------------------------- */
+/*
+ * The reference computes in float64 (core.py:37-38, 54).  These entry points
+ * run the same contracts in double on the generic kernels (register chain /
+ * layered entries, step kernels + SIMT GEMM for full, per-pair transfer
+ * matrices for dot/norm; no tensor cores, no bucketing), so results can be
+ * checked against the reference at its own tolerances.  Every pointer in the
+ * node / mode structs and every data argument then points to DOUBLE data
+ * (element counts from tnb_mode_floats are the same).
+ */
+int tnb_repack_f64(const tnb_node* nodes, int32_t n_modes, int64_t batch,
+                   const tnb_mode* modes, void* stream);
+int tnb_tt_core_f64(const tnb_chain* chain, int32_t k, double* out, void* stream);
+int tnb_promote_cp_f64(const tnb_node* node, int32_t position, int64_t batch,
+                       double* out, void* stream);
+int64_t tnb_entries_workspace_bytes_f64(const tnb_chain* chain, int64_t m, int32_t algo);
+int tnb_entries_f64(const tnb_chain* chain, const int64_t* idx, int64_t m,
+                    double* out, int32_t* err_mode, int32_t algo,
+                    void* workspace, int64_t workspace_bytes, void* stream);
+int64_t tnb_full_workspace_bytes_f64(const tnb_chain* chain, int64_t lead_lo, int64_t lead_hi);
+int tnb_full_f64(const tnb_chain* chain, int64_t lead_lo, int64_t lead_hi, double* out,
+                 void* workspace, int64_t workspace_bytes, void* stream);
+int tnb_dot_f64(const tnb_chain* a, const tnb_chain* b, double* out, void* stream);
+int tnb_norm_f64(const tnb_chain* t, double* out, void* stream);
+
 /* --- plan introspection and kernel timing (bench / profiling) ------------ */
 /*
  * What tnb_entries_f32(chain, ., m, ., ., algo, ...) will run: the resolved

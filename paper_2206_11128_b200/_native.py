@@ -63,6 +63,17 @@ SIGNATURES = {
                              c_int64, c_void_p]),
     "tnb_dot_f32": (c_int, [POINTER(TnbChain), POINTER(TnbChain), c_void_p, c_void_p]),
     "tnb_norm_f32": (c_int, [POINTER(TnbChain), c_void_p, c_void_p]),
+    "tnb_repack_f64": (c_int, [POINTER(TnbNode), c_int32, c_int64, POINTER(TnbMode), c_void_p]),
+    "tnb_tt_core_f64": (c_int, [POINTER(TnbChain), c_int32, c_void_p, c_void_p]),
+    "tnb_promote_cp_f64": (c_int, [POINTER(TnbNode), c_int32, c_int64, c_void_p, c_void_p]),
+    "tnb_entries_workspace_bytes_f64": (c_int64, [POINTER(TnbChain), c_int64, c_int32]),
+    "tnb_entries_f64": (c_int, [POINTER(TnbChain), c_void_p, c_int64, c_void_p, c_void_p,
+                                c_int32, c_void_p, c_int64, c_void_p]),
+    "tnb_full_workspace_bytes_f64": (c_int64, [POINTER(TnbChain), c_int64, c_int64]),
+    "tnb_full_f64": (c_int, [POINTER(TnbChain), c_int64, c_int64, c_void_p, c_void_p,
+                             c_int64, c_void_p]),
+    "tnb_dot_f64": (c_int, [POINTER(TnbChain), POINTER(TnbChain), c_void_p, c_void_p]),
+    "tnb_norm_f64": (c_int, [POINTER(TnbChain), c_void_p, c_void_p]),
     "tnb_entries_plan": (c_int, [POINTER(TnbChain), c_int64, c_int32, POINTER(TnbEntriesInfo)]),
     "tnb_timing_enable": (c_int, [c_int32]),
     "tnb_timing_read": (c_int, [c_char_p, POINTER(c_double), POINTER(c_int64)]),

@@ -51,15 +51,22 @@ def _default_device() -> torch.device:
     return torch.device("cpu")
 
 
-def _as_f32(a) -> torch.Tensor:
-    """fp32, contiguous, on the current CUDA device when one exists."""
+_DTYPES = (torch.float32, torch.float64)
+
+
+def _as_f32(a, dtype=torch.float32) -> torch.Tensor:
+    """``dtype`` (fp32 by default, float64 for the reference-precision
+    instantiation), contiguous, on the current CUDA device when one exists."""
+    if dtype not in _DTYPES:
+        raise ContractViolationError(f"dtype must be torch.float32 or torch.float64, got {dtype}")
     if isinstance(a, torch.Tensor):
         t = a.detach()
         dev = t.device if t.device.type == "cuda" else _default_device()
     else:
-        t = torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float32)))
+        np_dt = np.float64 if dtype == torch.float64 else np.float32
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np_dt)))
         dev = _default_device()
-    return t.to(device=dev, dtype=torch.float32).contiguous()
+    return t.to(device=dev, dtype=dtype).contiguous()
 
 
 class ModeNode:
@@ -69,16 +76,16 @@ class ModeNode:
 
     __slots__ = ("kind", "core", "factor", "batched")
 
-    def __init__(self, kind: str, core, factor=None, batched: bool = False):
+    def __init__(self, kind: str, core, factor=None, batched: bool = False, dtype=torch.float32):
         if kind not in (TT, CP):
             raise ContractViolationError(f"unknown node kind {kind!r}")
-        core = _as_f32(core)
+        core = _as_f32(core, dtype)
         expected = (3 if kind == TT else 2) + (1 if batched else 0)
         if core.dim() != expected:
             raise StructuralError(
                 f"{kind} core must have {expected} axes, got shape {tuple(core.shape)}")
         if factor is not None:
-            factor = _as_f32(factor)
+            factor = _as_f32(factor, dtype)
             if factor.dim() != 2 + (1 if batched else 0):
                 raise StructuralError(
                     f"factor must have {2 + batched} axes, got shape {tuple(factor.shape)}")
@@ -109,8 +116,12 @@ class ModeNode:
             raise ContractViolationError("cp_rank is only defined for CP nodes")
         return int(self.core.shape[-1])
 
+    @property
+    def dtype(self) -> torch.dtype:
+        return self.core.dtype
+
     def copy(self) -> "ModeNode":
-        return ModeNode(self.kind, self.core, self.factor, self.batched)
+        return ModeNode(self.kind, self.core, self.factor, self.batched, dtype=self.core.dtype)
 
     def _native(self) -> N.TnbNode:
         nd = N.TnbNode()
@@ -165,10 +176,13 @@ class TnTensor:
         ranks = _rank_chain(nodes)
         if ranks[0] != 1 or ranks[-1] != 1:
             raise StructuralError(f"boundary ranks must be 1, got {ranks[0]}, {ranks[-1]}")
+        dt = nodes[0].dtype
+        if any(n.dtype != dt for n in nodes):
+            raise ContractViolationError("all nodes must share one dtype (float32 or float64)")
         dev = nodes[0].core.device
         if any(n.core.device != dev for n in nodes):
             nodes = tuple(ModeNode(n.kind, n.core.to(dev),
-                                   None if n.factor is None else n.factor.to(dev), n.batched)
+                                   None if n.factor is None else n.factor.to(dev), n.batched, dtype=dt)
                           for n in nodes)
         self._nodes = nodes
         self._batch_size = batch_size
@@ -182,6 +196,25 @@ class TnTensor:
     @property
     def batch_size(self) -> Optional[int]:
         return self._batch_size
+
+    @property
+    def dtype(self) -> torch.dtype:
+        """torch.float32 (the hot path) or torch.float64 (the reference's
+        precision, generic kernels)."""
+        return self._nodes[0].dtype
+
+    def to(self, dtype) -> "TnTensor":
+        """The same chain with values in ``dtype`` (float32 / float64)."""
+        if dtype == self.dtype:
+            return self
+        return TnTensor([ModeNode(n.kind, n.core, n.factor, n.batched, dtype=dtype) for n in self._nodes],
+                        self._batch_size)
+
+    def double(self) -> "TnTensor":
+        return self.to(torch.float64)
+
+    def float(self) -> "TnTensor":
+        return self.to(torch.float32)
 
     @property
     def ndim(self) -> int:
@@ -221,7 +254,7 @@ class TnTensor:
     def batch_element(self, b: int) -> "TnTensor":
         if self._batch_size is None:
             raise ContractViolationError("tensor is not batched")
-        nodes = [ModeNode(n.kind, n.core[b], None if n.factor is None else n.factor[b])
+        nodes = [ModeNode(n.kind, n.core[b], None if n.factor is None else n.factor[b], dtype=n.dtype)
                  for n in self._nodes]
         return TnTensor(nodes)
 
@@ -250,11 +283,12 @@ class TnTensor:
         bufs = []
         for k in range(n):
             cnt = lib.tnb_mode_floats(ctypes.byref(modes[k]), batch)
-            buf = torch.empty(max(cnt, 1), dtype=torch.float32, device=dev)
+            buf = torch.empty(max(cnt, 1), dtype=self.dtype, device=dev)
             modes[k].slices = buf.data_ptr()
             bufs.append(buf)
+        repack = lib.tnb_repack_f64 if self.dtype == torch.float64 else lib.tnb_repack_f32
         with torch.cuda.device(dev):
-            N.check(lib.tnb_repack_f32(nodes, n, batch, modes, N.stream_ptr(dev)), "repack")
+            N.check(repack(nodes, n, batch, modes, N.stream_ptr(dev)), "repack")
         chain = N.TnbChain(n, 0, batch, ctypes.cast(modes, ctypes.POINTER(N.TnbMode)))
         self._pack = _Packed(chain, modes, bufs, dev, n)
         return self._pack
@@ -298,11 +332,11 @@ def promote_cp_node(node: ModeNode, position: str) -> torch.Tensor:
     r, i = node.cp_rank, node.internal_size
     b = int(node.core.shape[0]) if node.batched else 0
     shape = {INTERIOR: (r, i, r), LEFT_BOUNDARY: (1, i, r), RIGHT_BOUNDARY: (r, i, 1)}[position]
-    out = torch.empty(((b,) if b else ()) + shape, dtype=torch.float32, device=dev)
-    nd = ModeNode(CP, node.core, None, node.batched)._native()
+    out = torch.empty(((b,) if b else ()) + shape, dtype=node.dtype, device=dev)
+    nd = ModeNode(CP, node.core, None, node.batched, dtype=node.dtype)._native()
+    fn = N.load().tnb_promote_cp_f64 if node.dtype == torch.float64 else N.load().tnb_promote_cp_f32
     with torch.cuda.device(dev):
-        N.check(N.load().tnb_promote_cp_f32(ctypes.byref(nd), _POS[position], b,
-                                            out.data_ptr(), N.stream_ptr(dev)), "promote_cp_node")
+        N.check(fn(ctypes.byref(nd), _POS[position], b, out.data_ptr(), N.stream_ptr(dev)), "promote_cp_node")
     return out
 
 
@@ -315,10 +349,10 @@ def node_tt_core(t: TnTensor, k: int) -> torch.Tensor:
     m = p.modes[k]
     b = t.batch_size
     shape = (m.r_left, m.phys, m.r_right)
-    out = torch.empty(((b,) if b else ()) + shape, dtype=torch.float32, device=p.device)
+    out = torch.empty(((b,) if b else ()) + shape, dtype=t.dtype, device=p.device)
+    fn = N.load().tnb_tt_core_f64 if t.dtype == torch.float64 else N.load().tnb_tt_core_f32
     with torch.cuda.device(p.device):
-        N.check(N.load().tnb_tt_core_f32(ctypes.byref(p.chain), k, out.data_ptr(),
-                                         N.stream_ptr(p.device)), "node_tt_core")
+        N.check(fn(ctypes.byref(p.chain), k, out.data_ptr(), N.stream_ptr(p.device)), "node_tt_core")
     return out
 
 
@@ -338,15 +372,16 @@ def full(t: TnTensor, *, lead: Optional[tuple] = None) -> torch.Tensor:
     oshape = (hi - lo,) + tuple(shape[1:])
     if t.batch_size is not None:
         oshape = (t.batch_size,) + oshape
-    out = torch.empty(oshape, dtype=torch.float32, device=p.device)
+    out = torch.empty(oshape, dtype=t.dtype, device=p.device)
     lib = N.load()
-    wsb = lib.tnb_full_workspace_bytes(ctypes.byref(p.chain), lo, hi)
+    f64 = t.dtype == torch.float64
+    wsb = (lib.tnb_full_workspace_bytes_f64 if f64 else lib.tnb_full_workspace_bytes)(ctypes.byref(p.chain), lo, hi)
     if wsb < 0:
         N.check(N.TNB_EINVAL, "full")
     ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=p.device)
     with torch.cuda.device(p.device):
-        N.check(lib.tnb_full_f32(ctypes.byref(p.chain), lo, hi, out.data_ptr(), ws.data_ptr(),
-                                 wsb, N.stream_ptr(p.device)), "full")
+        N.check((lib.tnb_full_f64 if f64 else lib.tnb_full_f32)(
+            ctypes.byref(p.chain), lo, hi, out.data_ptr(), ws.data_ptr(), wsb, N.stream_ptr(p.device)), "full")
     return out
 
 
@@ -358,13 +393,16 @@ def chain_dot(a: TnTensor, b: TnTensor):
         raise ContractViolationError(f"shape mismatch: {a.shape} vs {b.shape}")
     if a.batch_size != b.batch_size:
         raise ContractViolationError("operands must agree on batching")
+    if a.dtype != b.dtype:
+        raise ContractViolationError(f"operands must share a dtype: {a.dtype} vs {b.dtype}")
     pa, pb = a._packed(), b._packed()
     if pa.device != pb.device:
         raise ContractViolationError("operands live on different devices")
-    out = torch.empty(a.batch_size or 1, dtype=torch.float32, device=pa.device)
+    out = torch.empty(a.batch_size or 1, dtype=a.dtype, device=pa.device)
+    fn = N.load().tnb_dot_f64 if a.dtype == torch.float64 else N.load().tnb_dot_f32
     with torch.cuda.device(pa.device):
-        N.check(N.load().tnb_dot_f32(ctypes.byref(pa.chain), ctypes.byref(pb.chain),
-                                     out.data_ptr(), N.stream_ptr(pa.device)), "chain_dot")
+        N.check(fn(ctypes.byref(pa.chain), ctypes.byref(pb.chain), out.data_ptr(), N.stream_ptr(pa.device)),
+                "chain_dot")
     if a.batch_size is None:
         return float(out[0].item())
     return out
@@ -372,10 +410,10 @@ def chain_dot(a: TnTensor, b: TnTensor):
 
 def norm(t: TnTensor):
     p = t._packed()
-    out = torch.empty(t.batch_size or 1, dtype=torch.float32, device=p.device)
+    out = torch.empty(t.batch_size or 1, dtype=t.dtype, device=p.device)
+    fn = N.load().tnb_norm_f64 if t.dtype == torch.float64 else N.load().tnb_norm_f32
     with torch.cuda.device(p.device):
-        N.check(N.load().tnb_norm_f32(ctypes.byref(p.chain), out.data_ptr(),
-                                      N.stream_ptr(p.device)), "norm")
+        N.check(fn(ctypes.byref(p.chain), out.data_ptr(), N.stream_ptr(p.device)), "norm")
     if t.batch_size is None:
         return float(out[0].item())
     return out
@@ -470,9 +508,10 @@ def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: in
 def _check_out(t: TnTensor, p: _Packed, out: torch.Tensor, m: int) -> None:
     b = t.batch_size
     shape = (m, b) if b else (m,)
-    if (not isinstance(out, torch.Tensor) or out.dtype != torch.float32 or tuple(out.shape) != shape
+    if (not isinstance(out, torch.Tensor) or out.dtype != t.dtype or tuple(out.shape) != shape
             or not out.is_contiguous()):
-        raise ContractViolationError(f"out must be a contiguous float32 tensor of shape {shape}")
+        name = "float64" if t.dtype == torch.float64 else "float32"
+        raise ContractViolationError(f"out must be a contiguous {name} tensor of shape {shape}")
     if out.device.type == "cpu":
         if not out.is_pinned():
             raise ContractViolationError("a host out tensor must be in pinned memory")
@@ -493,7 +532,7 @@ def entries(t: TnTensor, indices, *, algo: int = N.ALGO_AUTO,
     if (isinstance(indices, torch.Tensor) and indices.device.type == "cpu" and indices.is_pinned()
             and indices.dtype == torch.int64 and indices.dim() == 2 and indices.shape[1] == t.ndim
             and indices.is_contiguous() and indices.shape[0] >= 2 * _PIPELINE_ROWS
-            and t.batch_size is None):
+            and t.batch_size is None and t.dtype == torch.float32):
         if out is not None:
             _check_out(t, p, out, int(indices.shape[0]))
         res = _entries_pipelined(t, p, indices, algo, out if host_out else None)
@@ -507,7 +546,7 @@ def entries(t: TnTensor, indices, *, algo: int = N.ALGO_AUTO,
     if out is not None:
         _check_out(t, p, out, m)
     dev_out = out if (out is not None and not host_out) else \
-        torch.empty((m, b) if b else (m,), dtype=torch.float32, device=p.device)
+        torch.empty((m, b) if b else (m,), dtype=t.dtype, device=p.device)
     if m == 0:
         return out if out is not None else dev_out
     err = torch.empty(1, dtype=torch.int32, device=p.device)
@@ -528,14 +567,15 @@ def launch_entries(p: _Packed, idx: torch.Tensor, out: torch.Tensor, err: torch.
     caller reads ``err`` (>= n_modes means every index was valid)."""
     lib = N.load()
     m = int(idx.shape[0])
-    wsb = lib.tnb_entries_workspace_bytes(ctypes.byref(p.chain), m, algo)
+    f64 = out.dtype == torch.float64  # the reference-precision instantiation
+    wsb = (lib.tnb_entries_workspace_bytes_f64 if f64 else lib.tnb_entries_workspace_bytes)(
+        ctypes.byref(p.chain), m, algo)
     if wsb < 0:
         N.check(N.TNB_EINVAL, "entries")
     if wsb > 0 and (ws is None or ws.numel() < wsb):
         ws = torch.empty(wsb, dtype=torch.uint8, device=p.device)
     with torch.cuda.device(p.device):
-        N.check(lib.tnb_entries_f32(ctypes.byref(p.chain), idx.data_ptr(), m, out.data_ptr(),
-                                    err.data_ptr(), algo,
-                                    ws.data_ptr() if wsb > 0 else None, wsb,
-                                    N.stream_ptr(p.device)), "entries")
+        N.check((lib.tnb_entries_f64 if f64 else lib.tnb_entries_f32)(
+            ctypes.byref(p.chain), idx.data_ptr(), m, out.data_ptr(), err.data_ptr(), algo,
+            ws.data_ptr() if wsb > 0 else None, wsb, N.stream_ptr(p.device)), "entries")
     return ws

@@ -164,8 +164,8 @@ int64_t tnb_mode_floats(const tnb_mode* mode, int64_t batch) {
   return mode_floats(*mode) * (batch > 0 ? batch : 1);
 }
 
-int tnb_repack_f32(const tnb_node* nodes, int32_t n, int64_t batch, const tnb_mode* modes,
-                   void* stream) {
+static int repack_any(const tnb_node* nodes, int32_t n, int64_t batch, const tnb_mode* modes, void* stream,
+                      int elt) {
   if (!nodes || !modes || n < 1) return set_error(TNB_EINVAL, "null argument");
   if (batch < 0) return set_error(TNB_EINVAL, "batch must be >= 0");
   for (int k = 0; k < n; ++k) {
@@ -173,56 +173,117 @@ int tnb_repack_f32(const tnb_node* nodes, int32_t n, int64_t batch, const tnb_mo
       return set_error(TNB_EINVAL, "mode %d: null slices", k);
     if (!nodes[k].core) return set_error(TNB_EINVAL, "node %d: null core", k);
   }
-  return launch_repack(nodes, n, batch, modes, (cudaStream_t)stream);
+  return launch_repack(nodes, n, batch, modes, (cudaStream_t)stream, elt);
 }
 
-int tnb_tt_core_f32(const tnb_chain* chain, int32_t k, float* out, void* stream) {
+static int tt_core_any(const tnb_chain* chain, int32_t k, void* out, void* stream, int elt) {
   static thread_local ChainDev ch;
   int rc = make_chain_dev(chain, &ch, true);
   if (rc) return rc;
   if (k < 0 || k >= chain->n_modes) return set_error(TNB_EINVAL, "mode %d out of range", k);
   if (!out) return set_error(TNB_EINVAL, "null output");
-  return launch_tt_core(ch, k, out, (cudaStream_t)stream);
+  return launch_tt_core(ch, k, out, (cudaStream_t)stream, elt);
 }
 
-int tnb_promote_cp_f32(const tnb_node* node, int32_t position, int64_t batch, float* out,
-                       void* stream) {
+static int promote_any(const tnb_node* node, int32_t position, int64_t batch, void* out, void* stream, int elt) {
   if (!node || !out) return set_error(TNB_EINVAL, "null argument");
   if (node->kind != TNB_KIND_CP) return set_error(TNB_EINVAL, "promote_cp_node expects a CP node");
   if (position < TNB_POS_INTERIOR || position > TNB_POS_SINGLE)
     return set_error(TNB_EINVAL, "unknown position %d", position);
-  return launch_promote_cp(node, position, batch, out, (cudaStream_t)stream);
+  return launch_promote_cp(node, position, batch, out, (cudaStream_t)stream, elt);
+}
+
+static int entries_any(const tnb_chain* chain, const int64_t* idx, int64_t m, void* out, int32_t* err_mode,
+                       int32_t algo, void* ws, int64_t ws_bytes, void* stream, int elt) {
+  if (m < 0) return set_error(TNB_EINVAL, "negative sample count");
+  if (!err_mode) return set_error(TNB_EINVAL, "null err_mode");
+  if (m > 0 && (!idx || !out)) return set_error(TNB_EINVAL, "null index or output");
+  return launch_entries(chain, idx, m, out, err_mode, algo, ws, ws_bytes, (cudaStream_t)stream, elt);
+}
+
+int tnb_repack_f32(const tnb_node* nodes, int32_t n, int64_t batch, const tnb_mode* modes,
+                   void* stream) {
+  return repack_any(nodes, n, batch, modes, stream, 4);
+}
+
+int tnb_tt_core_f32(const tnb_chain* chain, int32_t k, float* out, void* stream) {
+  return tt_core_any(chain, k, out, stream, 4);
+}
+
+int tnb_promote_cp_f32(const tnb_node* node, int32_t position, int64_t batch, float* out,
+                       void* stream) {
+  return promote_any(node, position, batch, out, stream, 4);
 }
 
 int64_t tnb_entries_workspace_bytes(const tnb_chain* chain, int64_t m, int32_t algo) {
-  return entries_workspace(chain, m, algo);
+  return entries_workspace(chain, m, algo, 4);
 }
 
 int tnb_entries_f32(const tnb_chain* chain, const int64_t* idx, int64_t m, float* out,
                     int32_t* err_mode, int32_t algo, void* ws, int64_t ws_bytes, void* stream) {
-  if (m < 0) return set_error(TNB_EINVAL, "negative sample count");
-  if (!err_mode) return set_error(TNB_EINVAL, "null err_mode");
-  if (m > 0 && (!idx || !out)) return set_error(TNB_EINVAL, "null index or output");
-  return launch_entries(chain, idx, m, out, err_mode, algo, ws, ws_bytes, (cudaStream_t)stream);
+  return entries_any(chain, idx, m, out, err_mode, algo, ws, ws_bytes, stream, 4);
 }
 
 int64_t tnb_full_workspace_bytes(const tnb_chain* chain, int64_t lo, int64_t hi) {
-  return full_workspace(chain, lo, hi);
+  return full_workspace(chain, lo, hi, 4);
 }
 
 int tnb_full_f32(const tnb_chain* chain, int64_t lo, int64_t hi, float* out, void* ws,
                  int64_t ws_bytes, void* stream) {
-  return launch_full(chain, lo, hi, out, ws, ws_bytes, (cudaStream_t)stream);
+  return launch_full(chain, lo, hi, out, ws, ws_bytes, (cudaStream_t)stream, 4);
 }
 
 int tnb_dot_f32(const tnb_chain* a, const tnb_chain* b, float* out, void* stream) {
   if (!out) return set_error(TNB_EINVAL, "null output");
-  return launch_dot(a, b, out, false, (cudaStream_t)stream);
+  return launch_dot(a, b, out, false, (cudaStream_t)stream, 4);
 }
 
 int tnb_norm_f32(const tnb_chain* t, float* out, void* stream) {
   if (!out) return set_error(TNB_EINVAL, "null output");
-  return launch_dot(t, t, out, true, (cudaStream_t)stream);
+  return launch_dot(t, t, out, true, (cudaStream_t)stream, 4);
+}
+
+// ---- float64 instantiation (the generic kernels in double) ----------------
+int tnb_repack_f64(const tnb_node* nodes, int32_t n, int64_t batch, const tnb_mode* modes,
+                   void* stream) {
+  return repack_any(nodes, n, batch, modes, stream, 8);
+}
+
+int tnb_tt_core_f64(const tnb_chain* chain, int32_t k, double* out, void* stream) {
+  return tt_core_any(chain, k, out, stream, 8);
+}
+
+int tnb_promote_cp_f64(const tnb_node* node, int32_t position, int64_t batch, double* out,
+                       void* stream) {
+  return promote_any(node, position, batch, out, stream, 8);
+}
+
+int64_t tnb_entries_workspace_bytes_f64(const tnb_chain* chain, int64_t m, int32_t algo) {
+  return entries_workspace(chain, m, algo, 8);
+}
+
+int tnb_entries_f64(const tnb_chain* chain, const int64_t* idx, int64_t m, double* out,
+                    int32_t* err_mode, int32_t algo, void* ws, int64_t ws_bytes, void* stream) {
+  return entries_any(chain, idx, m, out, err_mode, algo, ws, ws_bytes, stream, 8);
+}
+
+int64_t tnb_full_workspace_bytes_f64(const tnb_chain* chain, int64_t lo, int64_t hi) {
+  return full_workspace(chain, lo, hi, 8);
+}
+
+int tnb_full_f64(const tnb_chain* chain, int64_t lo, int64_t hi, double* out, void* ws,
+                 int64_t ws_bytes, void* stream) {
+  return launch_full(chain, lo, hi, out, ws, ws_bytes, (cudaStream_t)stream, 8);
+}
+
+int tnb_dot_f64(const tnb_chain* a, const tnb_chain* b, double* out, void* stream) {
+  if (!out) return set_error(TNB_EINVAL, "null output");
+  return launch_dot(a, b, out, false, (cudaStream_t)stream, 8);
+}
+
+int tnb_norm_f64(const tnb_chain* t, double* out, void* stream) {
+  if (!out) return set_error(TNB_EINVAL, "null output");
+  return launch_dot(t, t, out, true, (cudaStream_t)stream, 8);
 }
 
 }  // extern "C"

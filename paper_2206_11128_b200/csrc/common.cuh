@@ -85,17 +85,19 @@ __device__ __forceinline__ int32_t norm_index(int64_t raw, int32_t J, int32_t k,
 
 // launchers implemented across translation units
 namespace tnb {
+// elt: element size in bytes, 4 (fp32, the hot path) or 8 (float64, the
+// reference's dtype; generic kernels only)
 int launch_repack(const tnb_node* nodes, int32_t n, int64_t batch, const tnb_mode* modes,
-                  cudaStream_t st);
-int launch_tt_core(const ChainDev& ch, int k, float* out, cudaStream_t st);
-int launch_promote_cp(const tnb_node* node, int position, int64_t batch, float* out,
-                      cudaStream_t st);
-int64_t entries_workspace(const tnb_chain* c, int64_t m, int algo);
+                  cudaStream_t st, int elt);
+int launch_tt_core(const ChainDev& ch, int k, void* out, cudaStream_t st, int elt);
+int launch_promote_cp(const tnb_node* node, int position, int64_t batch, void* out,
+                      cudaStream_t st, int elt);
+int64_t entries_workspace(const tnb_chain* c, int64_t m, int algo, int elt);
 int entries_plan(const tnb_chain* c, int64_t m, int algo, tnb_entries_info* info);
-int launch_entries(const tnb_chain* c, const int64_t* idx, int64_t m, float* out, int32_t* err,
-                   int algo, void* ws, int64_t ws_bytes, cudaStream_t st);
-int64_t full_workspace(const tnb_chain* c, int64_t lo, int64_t hi);
-int launch_full(const tnb_chain* c, int64_t lo, int64_t hi, float* out, void* ws,
-                int64_t ws_bytes, cudaStream_t st);
-int launch_dot(const tnb_chain* a, const tnb_chain* b, float* out, bool is_norm, cudaStream_t st);
+int launch_entries(const tnb_chain* c, const int64_t* idx, int64_t m, void* out, int32_t* err,
+                   int algo, void* ws, int64_t ws_bytes, cudaStream_t st, int elt);
+int64_t full_workspace(const tnb_chain* c, int64_t lo, int64_t hi, int elt);
+int launch_full(const tnb_chain* c, int64_t lo, int64_t hi, void* out, void* ws,
+                int64_t ws_bytes, cudaStream_t st, int elt);
+int launch_dot(const tnb_chain* a, const tnb_chain* b, void* out, bool is_norm, cudaStream_t st, int elt);
 }  // namespace tnb

@@ -24,10 +24,14 @@ double chain_entry_flops(const ChainDev& ch);
 
 namespace {
 
-template <int RMAX>
+__device__ __forceinline__ float fmat(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ double fmat(double a, double b, double c) { return fma(a, b, c); }
+
+// T = float (the hot path) or double (the reference's dtype)
+template <typename T, int RMAX>
 __global__ void __launch_bounds__(256) entries_chain_kernel(const __grid_constant__ ChainDev ch,
                                                             const int64_t* __restrict__ idx,
-                                                            int64_t m, float* __restrict__ out,
+                                                            int64_t m, T* __restrict__ out,
                                                             int32_t* err) {
   const int64_t B = ch.batch;
   const int N = ch.n;
@@ -37,14 +41,14 @@ __global__ void __launch_bounds__(256) entries_chain_kernel(const __grid_constan
     const int64_t s = t / B;
     const int64_t e = t - s * B;
     const int64_t* row = idx + s * N;
-    float v[RMAX];
+    T v[RMAX];
 #pragma unroll
-    for (int a = 0; a < RMAX; ++a) v[a] = (a == 0) ? 1.f : 0.f;
+    for (int a = 0; a < RMAX; ++a) v[a] = (a == 0) ? T(1) : T(0);
     for (int k = 0; k < N; ++k) {
       const ModeDev& md = ch.m[k];
       const int j = norm_index(row[k], md.J, k, err);
       if (md.J == 0) continue;
-      const float* g = md.s + e * md.bstride;
+      const T* g = reinterpret_cast<const T*>(md.s) + e * md.bstride;
       if (md.layout == TNB_LAYOUT_DIAG) {
         g += (int64_t)j * md.rl;
 #pragma unroll
@@ -53,17 +57,17 @@ __global__ void __launch_bounds__(256) entries_chain_kernel(const __grid_constan
       } else {
         const int rl = md.rl, rr = md.rr;
         g += (int64_t)j * rl * rr;
-        float w[RMAX];
+        T w[RMAX];
 #pragma unroll
-        for (int c = 0; c < RMAX; ++c) w[c] = 0.f;
+        for (int c = 0; c < RMAX; ++c) w[c] = T(0);
 #pragma unroll
         for (int a = 0; a < RMAX; ++a) {
           if (a < rl) {
-            const float va = v[a];
-            const float* ga = g + a * rr;
+            const T va = v[a];
+            const T* ga = g + a * rr;
 #pragma unroll
             for (int c = 0; c < RMAX; ++c)
-              if (c < rr) w[c] = fmaf(va, __ldg(ga + c), w[c]);
+              if (c < rr) w[c] = fmat(va, __ldg(ga + c), w[c]);
           }
         }
 #pragma unroll
@@ -75,10 +79,11 @@ __global__ void __launch_bounds__(256) entries_chain_kernel(const __grid_constan
 }
 
 // One mode of the layered algorithm: thread per (sample, batch element, c).
+template <typename T>
 __global__ void entries_layer_kernel(ModeDev md, int k, int N, int64_t B,
                                      const int64_t* __restrict__ idx, int64_t m,
-                                     const float* __restrict__ vin, float* __restrict__ vout,
-                                     int stride, float* __restrict__ out, int last,
+                                     const T* __restrict__ vin, T* __restrict__ vout,
+                                     int stride, T* __restrict__ out, int last,
                                      int32_t* err) {
   const int rl = md.rl, rr = md.rr;
   const int64_t total = m * B * rr;
@@ -89,15 +94,15 @@ __global__ void entries_layer_kernel(ModeDev md, int k, int N, int64_t B,
     const int64_t s = se / B;
     const int64_t e = se - s * B;
     const int j = norm_index(idx[s * N + k], md.J, k, err);
-    float acc = 0.f;
+    T acc = 0;
     if (md.J > 0) {
-      const float* g = md.s + e * md.bstride;
-      const float* vi = vin ? vin + se * stride : nullptr;
+      const T* g = reinterpret_cast<const T*>(md.s) + e * md.bstride;
+      const T* vi = vin ? vin + se * stride : nullptr;
       if (md.layout == TNB_LAYOUT_DIAG) {
-        acc = (vi ? vi[c] : 1.f) * __ldg(g + (int64_t)j * rl + c);
+        acc = (vi ? vi[c] : T(1)) * __ldg(g + (int64_t)j * rl + c);
       } else {
-        const float* gj = g + (int64_t)j * rl * rr + c;
-        for (int a = 0; a < rl; ++a) acc = fmaf(vi ? vi[a] : 1.f, __ldg(gj + (int64_t)a * rr), acc);
+        const T* gj = g + (int64_t)j * rl * rr + c;
+        for (int a = 0; a < rl; ++a) acc = fmat(vi ? vi[a] : T(1), __ldg(gj + (int64_t)a * rr), acc);
       }
     }
     if (last)
@@ -136,9 +141,14 @@ bool use_bucketed(const ChainDev& ch, int64_t m, int algo) {
   return algo == TNB_ALGO_AUTO && m >= (1 << 16) && bucketed_supported(ch);
 }
 
-int64_t entries_workspace(const tnb_chain* c, int64_t m, int algo) {
+int64_t entries_workspace(const tnb_chain* c, int64_t m, int algo, int elt) {
   if (!c || !c->modes || c->n_modes < 1 || m < 0) return -1;
   const int rmax = chain_rmax(c);
+  if (elt == 8) {
+    if (pick_algo(c, algo, rmax) != TNB_ALGO_LAYERED) return 0;
+    const int64_t B = c->batch > 0 ? c->batch : 1;
+    return 2 * m * B * (int64_t)rmax * 8;
+  }
   if (c->n_modes <= kMaxModes && (algo == TNB_ALGO_AUTO || algo == TNB_ALGO_BUCKETED)) {
     static thread_local ChainDev ch;
     if (make_chain_dev(c, &ch, true) == TNB_OK && use_bucketed(ch, m, algo))
@@ -182,45 +192,31 @@ int entries_plan(const tnb_chain* c, int64_t m, int algo, tnb_entries_info* info
   return TNB_OK;
 }
 
-int launch_entries(const tnb_chain* c, const int64_t* idx, int64_t m, float* out, int32_t* err,
-                   int algo, void* ws, int64_t ws_bytes, cudaStream_t st) {
-  static thread_local ChainDev ch;
-  if (!c || !c->modes) return set_error(TNB_EINVAL, "null chain");
-  const int rmax0 = chain_rmax(c);
-  const int use = pick_algo(c, algo, rmax0);
-  int rc = make_chain_dev(c, &ch, use != TNB_ALGO_LAYERED);
-  if (rc) return rc;
-  // "no error" sentinel 0x7f7f7f7f >= n_modes
-  rc = check_cuda(cudaMemsetAsync(err, 0x7f, sizeof(int32_t), st), "memset err");
-  if (rc || m == 0) return rc;
+template <typename T>
+int entries_generic(const tnb_chain* c, const ChainDev& ch, int use, const int64_t* idx, int64_t m, T* out,
+                    int32_t* err, void* ws, int64_t ws_bytes, cudaStream_t st) {
   const int64_t B = ch.batch;
-  if (algo == TNB_ALGO_AUTO && use_bucketed(ch, m, algo))
-    return launch_entries_bucketed(ch, idx, m, out, err, ws, ws_bytes, st);
+  int rc;
   if (use == TNB_ALGO_CHAIN) {
     const int64_t total = m * B;
     const int g = grid_for(total, 256);
     if (ch.rmax <= 8)
-      entries_chain_kernel<8><<<g, 256, 0, st>>>(ch, idx, m, out, err);
+      entries_chain_kernel<T, 8><<<g, 256, 0, st>>>(ch, idx, m, out, err);
     else if (ch.rmax <= 16)
-      entries_chain_kernel<16><<<g, 256, 0, st>>>(ch, idx, m, out, err);
+      entries_chain_kernel<T, 16><<<g, 256, 0, st>>>(ch, idx, m, out, err);
     else if (ch.rmax <= 32)
-      entries_chain_kernel<32><<<g, 256, 0, st>>>(ch, idx, m, out, err);
+      entries_chain_kernel<T, 32><<<g, 256, 0, st>>>(ch, idx, m, out, err);
     else
       return set_error(TNB_EINVAL, "chain algorithm supports ranks <= 32, got %d", ch.rmax);
     return check_launch("entries_chain");
   }
-  if (use == TNB_ALGO_BUCKETED) {
-    if (!bucketed_supported(ch))
-      return set_error(TNB_EINVAL, "bucketed algorithm does not support this chain");
-    return launch_entries_bucketed(ch, idx, m, out, err, ws, ws_bytes, st);
-  }
-  if (use != TNB_ALGO_LAYERED) return set_error(TNB_EINVAL, "unknown entries algorithm %d", algo);
-  const int64_t need = 2 * m * B * (int64_t)ch.rmax * (int64_t)sizeof(float);
+  if (use != TNB_ALGO_LAYERED) return set_error(TNB_EINVAL, "unknown entries algorithm %d", use);
+  const int64_t need = 2 * m * B * (int64_t)ch.rmax * (int64_t)sizeof(T);
   if (!ws || ws_bytes < need)
     return set_error(TNB_EWORKSPACE, "entries needs %lld workspace bytes, got %lld",
                      (long long)need, (long long)ws_bytes);
-  float* buf[2] = {(float*)ws, (float*)ws + m * B * ch.rmax};
-  const float* vin = nullptr;
+  T* buf[2] = {(T*)ws, (T*)ws + m * B * ch.rmax};
+  const T* vin = nullptr;
   for (int k = 0; k < c->n_modes; ++k) {
     const tnb_mode& mm = c->modes[k];
     ModeDev md;
@@ -231,17 +227,42 @@ int launch_entries(const tnb_chain* c, const int64_t* idx, int64_t m, float* out
     md.rl = mm.r_left;
     md.rr = mm.r_right;
     const int last = (k == c->n_modes - 1);
-    float* vout = buf[k & 1];
+    T* vout = buf[k & 1];
     const int64_t total = m * B * md.rr;
     if (total > 0)
-      entries_layer_kernel<<<grid_for(total, 256), 256, 0, st>>>(md, k, c->n_modes, B, idx, m,
-                                                                 vin, vout, ch.rmax, out, last,
-                                                                 err);
+      entries_layer_kernel<T><<<grid_for(total, 256), 256, 0, st>>>(md, k, c->n_modes, B, idx, m, vin, vout,
+                                                                    ch.rmax, out, last, err);
     rc = check_launch("entries_layer");
     if (rc) return rc;
     vin = vout;
   }
   return TNB_OK;
+}
+
+int launch_entries(const tnb_chain* c, const int64_t* idx, int64_t m, void* out_v, int32_t* err,
+                   int algo, void* ws, int64_t ws_bytes, cudaStream_t st, int elt) {
+  static thread_local ChainDev ch;
+  if (!c || !c->modes) return set_error(TNB_EINVAL, "null chain");
+  const int rmax0 = chain_rmax(c);
+  const int use = pick_algo(c, algo, rmax0);
+  int rc = make_chain_dev(c, &ch, use != TNB_ALGO_LAYERED);
+  if (rc) return rc;
+  // "no error" sentinel 0x7f7f7f7f >= n_modes
+  rc = check_cuda(cudaMemsetAsync(err, 0x7f, sizeof(int32_t), st), "memset err");
+  if (rc || m == 0) return rc;
+  if (elt == 8) {  // float64: the generic algorithms only
+    if (use == TNB_ALGO_BUCKETED) return set_error(TNB_EINVAL, "the bucketed algorithm is fp32 only");
+    return entries_generic<double>(c, ch, use, idx, m, static_cast<double*>(out_v), err, ws, ws_bytes, st);
+  }
+  float* out = static_cast<float*>(out_v);
+  if (algo == TNB_ALGO_AUTO && use_bucketed(ch, m, algo))
+    return launch_entries_bucketed(ch, idx, m, out, err, ws, ws_bytes, st);
+  if (use == TNB_ALGO_BUCKETED) {
+    if (!bucketed_supported(ch))
+      return set_error(TNB_EINVAL, "bucketed algorithm does not support this chain");
+    return launch_entries_bucketed(ch, idx, m, out, err, ws, ws_bytes, st);
+  }
+  return entries_generic<float>(c, ch, use, idx, m, out, err, ws, ws_bytes, st);
 }
 
 }  // namespace tnb

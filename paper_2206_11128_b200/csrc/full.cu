@@ -11,6 +11,7 @@
 // A slab [lo, hi) of the leading mode restricts L's rows, which is the
 // reference's own full(t[lo:hi]) (indexing.py:132-137); it is also how the
 // multi-GPU runner shards full() across devices.
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -42,7 +43,10 @@ struct FullPlan {
   int64_t tc_bytes = 0; // tensor-core GEMM workspace (split L tiles)
 };
 
-int make_plan(const tnb_chain* c, int64_t lo, int64_t hi, FullPlan* P) {
+__device__ __forceinline__ float fmat(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ double fmat(double a, double b, double c) { return fma(a, b, c); }
+
+int make_plan(const tnb_chain* c, int64_t lo, int64_t hi, FullPlan* P, int elt) {
   if (!c || !c->modes || c->n_modes < 1) return set_error(TNB_EINVAL, "null chain");
   const int n = c->n_modes;
   const tnb_mode* m = c->modes;
@@ -108,14 +112,15 @@ int make_plan(const tnb_chain* c, int64_t lo, int64_t hi, FullPlan* P) {
   P->l_buf = lmax;
   P->r_buf = rmax;
   P->tc_bytes = 0;
-  if (p < n && tc_gemm_supported(P->rowsL, cols, m[p].r_left, m[p].r_left, cols, cols))
+  if (elt == 4 && p < n && tc_gemm_supported(P->rowsL, cols, m[p].r_left, m[p].r_left, cols, cols))
     P->tc_bytes = tc_gemm_workspace(P->rowsL);
   return TNB_OK;
 }
 
 // left step: out[e][(p*J + j)*rr + c] = sum_a in[e][p*rl + a] * G_e(j, a, c)
-__global__ void full_left_step(ModeDev md, int64_t B, const float* __restrict__ in, int64_t in_bs,
-                               int64_t P, float* __restrict__ out, int64_t out_bs) {
+template <typename T>
+__global__ void full_left_step(ModeDev md, int64_t B, const T* __restrict__ in, int64_t in_bs,
+                               int64_t P, T* __restrict__ out, int64_t out_bs) {
   const int J = md.J, rl = md.rl, rr = md.rr;
   const int64_t per = P * J * rr;
   const int64_t total = per * B;
@@ -127,22 +132,23 @@ __global__ void full_left_step(ModeDev md, int64_t B, const float* __restrict__ 
     r -= p * J * rr;
     const int j = (int)(r / rr);
     const int c = (int)(r - (int64_t)j * rr);
-    const float* g = md.s + e * md.bstride;
-    const float* x = in + e * in_bs + p * rl;
-    float acc;
+    const T* g = reinterpret_cast<const T*>(md.s) + e * md.bstride;
+    const T* x = in + e * in_bs + p * rl;
+    T acc;
     if (md.layout == TNB_LAYOUT_DIAG) {
       acc = x[c] * __ldg(g + (int64_t)j * rl + c);
     } else {
-      acc = 0.f;
-      const float* gj = g + (int64_t)j * rl * rr + c;
-      for (int a = 0; a < rl; ++a) acc = fmaf(x[a], __ldg(gj + (int64_t)a * rr), acc);
+      acc = 0;
+      const T* gj = g + (int64_t)j * rl * rr + c;
+      for (int a = 0; a < rl; ++a) acc = fmat(x[a], __ldg(gj + (int64_t)a * rr), acc);
     }
     out[e * out_bs + r + p * J * rr] = acc;
   }
 }
 
 // R of the last mode: out[e][a*J + j] = G_e(j, a, 0)
-__global__ void full_right_first(ModeDev md, int64_t B, float* __restrict__ out, int64_t out_bs) {
+template <typename T>
+__global__ void full_right_first(ModeDev md, int64_t B, T* __restrict__ out, int64_t out_bs) {
   const int J = md.J, rl = md.rl;
   const int64_t per = (int64_t)rl * J;
   const int64_t total = per * B;
@@ -152,13 +158,14 @@ __global__ void full_right_first(ModeDev md, int64_t B, float* __restrict__ out,
     const int64_t r = t - e * per;
     const int a = (int)(r / J);
     const int j = (int)(r - (int64_t)a * J);
-    out[e * out_bs + r] = __ldg(md.s + e * md.bstride + (int64_t)j * rl + a);
+    out[e * out_bs + r] = __ldg(reinterpret_cast<const T*>(md.s) + e * md.bstride + (int64_t)j * rl + a);
   }
 }
 
 // right step: out[e][a][j*n + x] = sum_c G_e(j, a, c) * in[e][c][x]
-__global__ void full_right_step(ModeDev md, int64_t B, const float* __restrict__ in,
-                                int64_t in_bs, int64_t n, float* __restrict__ out,
+template <typename T>
+__global__ void full_right_step(ModeDev md, int64_t B, const T* __restrict__ in,
+                                int64_t in_bs, int64_t n, T* __restrict__ out,
                                 int64_t out_bs) {
   const int J = md.J, rl = md.rl, rr = md.rr;
   const int64_t per = (int64_t)rl * J * n;
@@ -171,15 +178,15 @@ __global__ void full_right_step(ModeDev md, int64_t B, const float* __restrict__
     const int64_t rem = r - (int64_t)a * J * n;
     const int j = (int)(rem / n);
     const int64_t x = rem - (int64_t)j * n;
-    const float* g = md.s + e * md.bstride;
-    const float* y = in + e * in_bs + x;
-    float acc;
+    const T* g = reinterpret_cast<const T*>(md.s) + e * md.bstride;
+    const T* y = in + e * in_bs + x;
+    T acc;
     if (md.layout == TNB_LAYOUT_DIAG) {
       acc = __ldg(g + (int64_t)j * rl + a) * y[(int64_t)a * n];
     } else {
-      acc = 0.f;
-      const float* ga = g + ((int64_t)j * rl + a) * rr;
-      for (int c = 0; c < rr; ++c) acc = fmaf(__ldg(ga + c), y[(int64_t)c * n], acc);
+      acc = 0;
+      const T* ga = g + ((int64_t)j * rl + a) * rr;
+      for (int c = 0; c < rr; ++c) acc = fmat(__ldg(ga + c), y[(int64_t)c * n], acc);
     }
     out[e * out_bs + r] = acc;
   }
@@ -189,48 +196,51 @@ __global__ void full_right_step(ModeDev md, int64_t B, const float* __restrict__
 // 128x128 tile, BK=8, 256 threads, 8x8 outputs per thread (two 4x4 quads per
 // axis so shared-memory reads and global stores are float4 and coalesced).
 constexpr int GBM = 128, GBN = 128, GBK = 8;
-__global__ void __launch_bounds__(256) sgemm_kernel(const float* __restrict__ A, int64_t lda,
-                                                    int64_t sA, const float* __restrict__ Bm,
-                                                    int64_t ldb, int64_t sB,
-                                                    float* __restrict__ C, int64_t ldc, int64_t sC,
-                                                    int64_t M, int64_t N, int K) {
-  __shared__ __align__(16) float As[GBK][GBM];
-  __shared__ __align__(16) float Bs[GBK][GBN];
+template <typename T>
+__global__ void __launch_bounds__(256) gemm_kernel(const T* __restrict__ A, int64_t lda,
+                                                   int64_t sA, const T* __restrict__ Bm,
+                                                   int64_t ldb, int64_t sB,
+                                                   T* __restrict__ C, int64_t ldc, int64_t sC,
+                                                   int64_t M, int64_t N, int K) {
+  __shared__ __align__(16) T As[GBK][GBM];
+  __shared__ __align__(16) T Bs[GBK][GBN];
   const int64_t e = blockIdx.z;
   A += e * sA;
   Bm += e * sB;
   C += e * sC;
   const int64_t m0 = (int64_t)blockIdx.y * GBM, n0 = (int64_t)blockIdx.x * GBN;
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  float acc[8][8];
+  T acc[8][8];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0;
   for (int k0 = 0; k0 < K; k0 += GBK) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int l = tid + i * 256;
       const int r = l / GBK, kk = l % GBK;
       const int64_t gm = m0 + r;
-      As[kk][r] = (gm < M && k0 + kk < K) ? __ldg(A + gm * lda + k0 + kk) : 0.f;
+      As[kk][r] = (gm < M && k0 + kk < K) ? __ldg(A + gm * lda + k0 + kk) : T(0);
       const int kb = l / GBN, cb = l % GBN;
       const int64_t gn = n0 + cb;
-      Bs[kb][cb] = (k0 + kb < K && gn < N) ? __ldg(Bm + (int64_t)(k0 + kb) * ldb + gn) : 0.f;
+      Bs[kb][cb] = (k0 + kb < K && gn < N) ? __ldg(Bm + (int64_t)(k0 + kb) * ldb + gn) : T(0);
     }
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < GBK; ++kk) {
-      const float4 a0 = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
-      const float4 a1 = *reinterpret_cast<const float4*>(&As[kk][64 + ty * 4]);
-      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
-      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[kk][64 + tx * 4]);
-      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+      T av[8], bv[8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        av[q] = As[kk][ty * 4 + q];
+        av[4 + q] = As[kk][64 + ty * 4 + q];
+        bv[q] = Bs[kk][tx * 4 + q];
+        bv[4 + q] = Bs[kk][64 + tx * 4 + q];
+      }
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmat(av[i], bv[j], acc[i][j]);
     }
     __syncthreads();
   }
@@ -242,11 +252,15 @@ __global__ void __launch_bounds__(256) sgemm_kernel(const float* __restrict__ A,
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int64_t gn = n0 + h * 64 + tx * 4;
-      float* dst = C + gm * ldc + gn;
-      if (vec && gn + 3 < N) {
-        __stcs(reinterpret_cast<float4*>(dst),
-               make_float4(acc[i][h * 4], acc[i][h * 4 + 1], acc[i][h * 4 + 2], acc[i][h * 4 + 3]));
-      } else {
+      T* dst = C + gm * ldc + gn;
+      if constexpr (std::is_same<T, float>::value) {
+        if (vec && gn + 3 < N) {
+          __stcs(reinterpret_cast<float4*>(dst),
+                 make_float4(acc[i][h * 4], acc[i][h * 4 + 1], acc[i][h * 4 + 2], acc[i][h * 4 + 3]));
+          continue;
+        }
+      }
+      {
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           if (gn + q < N) dst[q] = acc[i][h * 4 + q];
@@ -263,8 +277,8 @@ inline int grid_for(int64_t total) {
 }
 
 // byte offset of the tensor-core workspace (256-byte aligned)
-int64_t tc_offset(const FullPlan& P, int64_t B) {
-  return ((2 * P.l_buf + 2 * P.r_buf) * B * (int64_t)sizeof(float) + 255) & ~(int64_t)255;
+int64_t tc_offset(const FullPlan& P, int64_t B, int elt) {
+  return ((2 * P.l_buf + 2 * P.r_buf) * B * (int64_t)elt + 255) & ~(int64_t)255;
 }
 
 ModeDev mode_dev(const tnb_chain* c, int k) {
@@ -281,28 +295,30 @@ ModeDev mode_dev(const tnb_chain* c, int k) {
 
 }  // namespace
 
-int launch_sgemm(const float* A, int64_t lda, int64_t sA, const float* B, int64_t ldb, int64_t sB,
-                 float* C, int64_t ldc, int64_t sC, int64_t M, int64_t N, int K, int64_t batch,
-                 cudaStream_t st) {
+template <typename T>
+int launch_gemm(const T* A, int64_t lda, int64_t sA, const T* B, int64_t ldb, int64_t sB,
+                T* C, int64_t ldc, int64_t sC, int64_t M, int64_t N, int K, int64_t batch,
+                cudaStream_t st) {
   if (M == 0 || N == 0 || batch == 0) return TNB_OK;
   if (batch > 65535) return set_error(TNB_EINVAL, "gemm batch too large");
   dim3 grid((unsigned)ceil_div(N, GBN), (unsigned)ceil_div(M, GBM), (unsigned)batch);
   if (grid.y > 65535) return set_error(TNB_EINVAL, "gemm M too large");
-  sgemm_kernel<<<grid, 256, 0, st>>>(A, lda, sA, B, ldb, sB, C, ldc, sC, M, N, K);
-  return check_launch("sgemm");
+  gemm_kernel<T><<<grid, 256, 0, st>>>(A, lda, sA, B, ldb, sB, C, ldc, sC, M, N, K);
+  return check_launch("gemm");
 }
 
-int64_t full_workspace(const tnb_chain* c, int64_t lo, int64_t hi) {
+int64_t full_workspace(const tnb_chain* c, int64_t lo, int64_t hi, int elt) {
   FullPlan P;
-  if (make_plan(c, lo, hi, &P)) return -1;
+  if (make_plan(c, lo, hi, &P, elt)) return -1;
   const int64_t B = c->batch > 0 ? c->batch : 1;
-  return tc_offset(P, B) + P.tc_bytes;
+  return tc_offset(P, B, elt) + P.tc_bytes;
 }
 
-int launch_full(const tnb_chain* c, int64_t lo, int64_t hi, float* out, void* ws,
-                int64_t ws_bytes, cudaStream_t st) {
+template <typename T>
+int full_t(const tnb_chain* c, int64_t lo, int64_t hi, T* out, void* ws, int64_t ws_bytes, cudaStream_t st) {
+  constexpr int elt = (int)sizeof(T);
   FullPlan P;
-  int rc = make_plan(c, lo, hi, &P);
+  int rc = make_plan(c, lo, hi, &P, elt);
   if (rc) return rc;
   ChainDev tmp;
   rc = make_chain_dev(c, &tmp, false);  // validates ranks
@@ -310,24 +326,24 @@ int launch_full(const tnb_chain* c, int64_t lo, int64_t hi, float* out, void* ws
   const int64_t B = c->batch > 0 ? c->batch : 1;
   if (P.out_per == 0) return TNB_OK;
   if (!out) return set_error(TNB_EINVAL, "null output");
-  const int64_t need = tc_offset(P, B) + P.tc_bytes;
+  const int64_t need = tc_offset(P, B, elt) + P.tc_bytes;
   if (need > 0 && (!ws || ws_bytes < need))
     return set_error(TNB_EWORKSPACE, "full needs %lld workspace bytes, got %lld",
                      (long long)need, (long long)ws_bytes);
-  float* lb[2] = {(float*)ws, (float*)ws + P.l_buf * B};
-  float* rb[2] = {(float*)ws + 2 * P.l_buf * B, (float*)ws + 2 * P.l_buf * B + P.r_buf * B};
+  T* lb[2] = {(T*)ws, (T*)ws + P.l_buf * B};
+  T* rb[2] = {(T*)ws + 2 * P.l_buf * B, (T*)ws + 2 * P.l_buf * B + P.r_buf * B};
   const int n = P.n, p = P.p;
 
   // ---- left partial: L0 is a view of mode 0's slices (rows lo..hi) ----
   const ModeDev m0 = mode_dev(c, 0);
-  const float* L = m0.s + lo * (int64_t)m0.rl * m0.rr;  // dense, rl == 1
+  const T* L = reinterpret_cast<const T*>(m0.s) + lo * (int64_t)m0.rl * m0.rr;  // dense, rl == 1
   int64_t L_bs = m0.bstride;
   int64_t rows = P.slab_rows;
   if (n == 1) {
     // out[e][j] = G_e(lo + j, 0, 0)
     for (int64_t e = 0; e < B; ++e) {
       rc = check_cuda(cudaMemcpyAsync(out + e * P.out_per, L + e * L_bs,
-                                      P.out_per * sizeof(float), cudaMemcpyDeviceToDevice, st),
+                                      P.out_per * sizeof(T), cudaMemcpyDeviceToDevice, st),
                       "copy");
       if (rc) return rc;
     }
@@ -336,11 +352,11 @@ int launch_full(const tnb_chain* c, int64_t lo, int64_t hi, float* out, void* ws
   for (int k = 1; k < p; ++k) {
     const ModeDev md = mode_dev(c, k);
     const bool writes_out = (p == n && k == n - 1);
-    float* dst = writes_out ? out : lb[k & 1];
+    T* dst = writes_out ? out : lb[k & 1];
     const int64_t dst_bs = writes_out ? P.out_per : P.l_buf;
     const int64_t total = rows * md.J * md.rr * B;
     if (total > 0)
-      full_left_step<<<grid_for(total), 256, 0, st>>>(md, B, L, L_bs, rows, dst, dst_bs);
+      full_left_step<T><<<grid_for(total), 256, 0, st>>>(md, B, L, L_bs, rows, dst, dst_bs);
     rc = check_launch("full_left_step");
     if (rc) return rc;
     L = dst;
@@ -351,21 +367,21 @@ int launch_full(const tnb_chain* c, int64_t lo, int64_t hi, float* out, void* ws
 
   // ---- right partial ----
   const ModeDev ml = mode_dev(c, n - 1);
-  float* R = rb[0];
+  T* R = rb[0];
   int64_t cols = ml.J;
   {
     const int64_t total = (int64_t)ml.rl * ml.J * B;
-    if (total > 0) full_right_first<<<grid_for(total), 256, 0, st>>>(ml, B, R, P.r_buf);
+    if (total > 0) full_right_first<T><<<grid_for(total), 256, 0, st>>>(ml, B, R, P.r_buf);
     rc = check_launch("full_right_first");
     if (rc) return rc;
   }
   int which = 0;
   for (int k = n - 2; k >= p; --k) {
     const ModeDev md = mode_dev(c, k);
-    float* dst = rb[which ^ 1];
+    T* dst = rb[which ^ 1];
     const int64_t total = (int64_t)md.rl * md.J * cols * B;
     if (total > 0)
-      full_right_step<<<grid_for(total), 256, 0, st>>>(md, B, R, P.r_buf, cols, dst, P.r_buf);
+      full_right_step<T><<<grid_for(total), 256, 0, st>>>(md, B, R, P.r_buf, cols, dst, P.r_buf);
     rc = check_launch("full_right_step");
     if (rc) return rc;
     R = dst;
@@ -375,12 +391,20 @@ int launch_full(const tnb_chain* c, int64_t lo, int64_t hi, float* out, void* ws
   // ---- out = L @ R ----
   KTimer kt("full_gemm", st);
   const int K = c->modes[p].r_left;
-  if (K == 0) return check_cuda(cudaMemsetAsync(out, 0, P.out_per * B * sizeof(float), st), "memset");
-  if (P.tc_bytes > 0) {
-    void* tcw = (unsigned char*)ws + tc_offset(P, B);
-    return launch_tc_gemm(L, K, L_bs, R, cols, P.r_buf, out, cols, P.out_per, rows, cols, K, B, tcw, st);
+  if (K == 0) return check_cuda(cudaMemsetAsync(out, 0, P.out_per * B * sizeof(T), st), "memset");
+  if constexpr (std::is_same<T, float>::value) {
+    if (P.tc_bytes > 0) {
+      void* tcw = (unsigned char*)ws + tc_offset(P, B, elt);
+      return launch_tc_gemm(L, K, L_bs, R, cols, P.r_buf, out, cols, P.out_per, rows, cols, K, B, tcw, st);
+    }
   }
-  return launch_sgemm(L, K, L_bs, R, cols, P.r_buf, out, cols, P.out_per, rows, cols, K, B, st);
+  return launch_gemm<T>(L, K, L_bs, R, cols, P.r_buf, out, cols, P.out_per, rows, cols, K, B, st);
+}
+
+int launch_full(const tnb_chain* c, int64_t lo, int64_t hi, void* out, void* ws, int64_t ws_bytes,
+                cudaStream_t st, int elt) {
+  if (elt == 8) return full_t<double>(c, lo, hi, static_cast<double*>(out), ws, ws_bytes, st);
+  return full_t<float>(c, lo, hi, static_cast<float*>(out), ws, ws_bytes, st);
 }
 
 }  // namespace tnb

@@ -113,17 +113,18 @@ def read_container(path) -> Tuple[dict, List[Tuple[str, np.ndarray, Optional[np.
     return header, out
 
 
-def load(path, device=None) -> TnTensor:
+def load(path, device=None, dtype=torch.float32) -> TnTensor:
     """Container -> TnTensor on ``device`` (default: the current CUDA
-    device): one pinned H2D copy of the checked payload, fp64 -> fp32 cast
-    and per-node views on the device."""
+    device): one pinned H2D copy of the checked payload, then per-node views
+    on the device -- cast to fp32 (the hot path) or, with
+    ``dtype=torch.float64``, the payload floats bit for bit."""
     header, payload = _checked_payload(path)
     layout = _layout(header)
     dev = torch.device(device) if device is not None else _default_device()
     host = torch.frombuffer(bytearray(payload), dtype=torch.float64)
     if dev.type == "cuda":
         host = host.pin_memory()
-    flat = host.to(dev, non_blocking=True).to(torch.float32)
+    flat = host.to(dev, non_blocking=True).to(dtype)
     batch = header.get("batch_size")
     nodes, off = [], 0
     for kind, cs, fs in layout:
@@ -135,7 +136,7 @@ def load(path, device=None) -> TnTensor:
             n = int(np.prod(fs))
             factor = flat[off:off + n].view(fs)
             off += n
-        nodes.append(ModeNode(kind, core, factor, batched=batch is not None))
+        nodes.append(ModeNode(kind, core, factor, batched=batch is not None, dtype=dtype))
     return TnTensor(nodes, batch)
 
 

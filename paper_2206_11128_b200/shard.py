@@ -73,7 +73,7 @@ def batch_slice(t: TnTensor, lo: int, hi: int) -> TnTensor:
     """Batch elements [lo, hi) of a batched chain (views, no copies)."""
     from .core import ModeNode
 
-    nodes = [ModeNode(n.kind, n.core[lo:hi], None if n.factor is None else n.factor[lo:hi], True)
+    nodes = [ModeNode(n.kind, n.core[lo:hi], None if n.factor is None else n.factor[lo:hi], True, dtype=n.dtype)
              for n in t.nodes]
     return TnTensor(nodes, hi - lo)
 
