@@ -5,26 +5,27 @@
 // their index value so every group shares one core slice and the group's
 // update is a real (n_j x r) @ (r x s) product.  A global re-sort per mode
 // would cost 2 x M x r x 4 bytes of HBM traffic per mode, so
-// here the grouping happens per CTA tile, on chip:
+// here the grouping happens per tile, on chip, after the chain is shortened:
 //
-//   * a persistent CTA (one per SM) owns a tile of T samples; their r-vector
-//     states live in shared memory at FIXED slots (sample id), so no state
-//     ever moves between modes -- only a permutation is rebuilt;
-//   * per interior dense mode, a counting sort of the tile's indices
-//     (warp-aggregated match_any + smem atomics) yields perm, bucket starts
-//     and counts;
-//   * each warp takes an equal contiguous range of sorted positions; for each
-//     bucket in its range it loads that core slice ONCE into registers
-//     (lane group of L lanes holds all r rows x C columns), then streams its
-//     samples: a group reads a sample's state row (LDS.128 broadcast within
-//     the group), does r x C FMAs per lane, and writes its C output columns
-//     back into the same slot (__syncwarp between reads and writes);
-//   * the first mode (rank 1 on the left) is a row copy, interior CP modes
-//     are diagonal scalings, the last mode (rank 1 on the right) a dot
-//     product -- none of those need sorting;
-//   * index tuples are read once per tile (coalesced int64), validated
-//     (negative wrap, lowest OOB mode -> *err), compacted to uint8/uint16 in
-//     shared memory; the next tile's indices are prefetched into L2.
+//   * mode merging (plan_merge): leading / trailing modes become prefix /
+//     suffix tables and runs of interior CP modes diagonal product tables,
+//     built per call and L2-resident; the kernels run that VIRTUAL chain;
+//   * entries_prep_kernel (one CTA per tile): reads the tile's int64 index
+//     rows, wraps and validates every ORIGINAL mode (lowest bad mode ->
+//     *err, core.py:409-416), combines merged modes and writes the compact
+//     uint8/uint16 [N][T] index block of the tile record -- HBM-bound;
+//   * entries_sort_kernel (one warp per (tile, sorted mode)): counting sort
+//     with a per-warp shared-memory histogram -> permutation + bucket starts;
+//   * entries_compute_kernel (persistent, one 512-thread CTA per SM): streams
+//     each tile record into shared memory with cp.async.bulk (the next tile's
+//     rows are prefetched as soon as the current tile stops needing them);
+//     the samples' r-vector states live in shared memory at FIXED slots, so
+//     no state ever moves between modes.  First mode: a TMA bulk gather of
+//     table rows.  Sorted modes: each warp takes an equal range of sorted
+//     positions and, per bucket, loads the core slice once into registers
+//     (K-split layout at r=32, lane groups at r<=24) and streams the bucket's
+//     samples.  Diagonal runs: one vectorised pass, or folded into the last
+//     mode's dot.  Last mode: lane groups per sample, several in flight.
 // Each sample's arithmetic is a fixed FMA sequence, so results do not depend
 // on the sort order or the tile a sample lands in.
 #include <algorithm>
@@ -41,6 +42,7 @@ namespace tnb {
 namespace {
 
 constexpr int kMaxJ = 1024;          // bucket count limit for sorted modes
+constexpr int kComputeThreads = 512;  // one 16-warp compute CTA per SM
 
 
 
@@ -182,8 +184,6 @@ struct BPlan {
   int64_t tile_bytes;
   int64_t off_perm, off_starts;
   int8_t slot[kMaxModes];  // mode -> sorted slot or -1
-  int l1pf;                // prefetch the next segment's core slice into L1
-  int rounds;              // R <= 24: groups of one warp on different buckets
   // mode merging: the kernels run a VIRTUAL chain whose first / last modes
   // may be prefix / suffix tables over several original modes; the prep
   // kernel reads the n0 original index columns, validates each against its
@@ -347,7 +347,7 @@ __device__ __forceinline__ void bulk(void* dst, const void* src, uint32_t bytes,
 // run is folded into the last-mode dot product (separate instantiation so
 // chains without it keep the leaner register allocation)
 template <int R, typename IdxT, int NT, bool FOLD>
-__global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
+__global__ void __launch_bounds__(NT, 1)
     entries_compute_kernel(const __grid_constant__ ChainDev ch, const __grid_constant__ BPlan bp,
                            const unsigned char* __restrict__ ws, int64_t m, float* __restrict__ out) {
   using Gm = Geo<R>;
@@ -588,11 +588,6 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
             const int h = lane >> 4, qq = lane & 15;
             uint64_t g2[16];
             const float* gs = md.s + (int64_t)key * rl * rr;
-            if (bp.l1pf && bend < hi) {  // warm L1 with the next segment's slice (one line per lane)
-              const int nkey = col[perm[bend]];
-              const float* ngs = md.s + (int64_t)nkey * rl * rr;
-              if (lane * 32 < rl * rr) asm volatile("prefetch.global.L1 [%0];" ::"l"(ngs + lane * 32));
-            }
             if (bp.lmaj[k]) {  // lane-major slice: 8 x 16-byte loads, chunk c = (g2[2c], g2[2c+1])
 #pragma unroll
               for (int c = 0; c < 8; ++c) {
@@ -632,7 +627,6 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
           }
         }
         } else {
-          if (!bp.rounds) {
           // one bucket per warp at a time: all G groups take samples of it
           int p = lo;
           while (p < hi) {
@@ -726,103 +720,6 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1)
               __syncwarp();
   p += n;
             }
-          }
-          } else {
-          // Groups of L lanes work on DIFFERENT buckets (small buckets, e.g.
-          // J = 128): the warp range is split into G sub-ranges; per round
-          // every group loads one core slice (G loads share one latency) and
-          // streams that segment two samples per pass; groups that finish
-          // early idle until the round ends.
-          constexpr int C1 = (C == 3) ? 1 : 0;
-          const int glo = lo + ((hi - lo) * gi) / G, ghi = lo + ((hi - lo) * (gi + 1)) / G;
-          const int cp = 2 * q, cs = 16 + q;
-          int p = glo;
-          while (__any_sync(0xffffffffu, p < ghi)) {
-            const bool act = p < ghi;
-            const int key = act ? (int)col[perm[p]] : 0;
-            const int bend = act ? min((int)st[key + 1], ghi) : p;
-            uint64_t g2[R];
-            float g1[C1 ? R : 1];
-            const float* gs = md.s + (int64_t)key * rl * rr;
-            if (bp.lmaj[k]) {
-#pragma unroll
-              for (int c = 0; c < R / 2; ++c) {
-                const ulonglong2 v = ldg_u2(gs + (c * L + q) * 4);
-                g2[2 * c] = v.x;
-                g2[2 * c + 1] = v.y;
-              }
-              if constexpr (C1) {
-#pragma unroll
-                for (int c = 0; c < R / 4; ++c) {
-                  const float4 v = __ldg(reinterpret_cast<const float4*>(gs + ((R / 2 + c) * L + q) * 4));
-                  g1[4 * c] = v.x;
-                  g1[4 * c + 1] = v.y;
-                  g1[4 * c + 2] = v.z;
-                  g1[4 * c + 3] = v.w;
-                }
-              }
-            } else if (rl == R && rr == R) {
-#pragma unroll
-              for (int a = 0; a < R; ++a) {
-                g2[a] = ldg_b64(gs + a * R + cp);
-                if constexpr (C1) g1[a] = __ldg(gs + a * R + cs);
-              }
-            } else {
-#pragma unroll
-              for (int a = 0; a < R; ++a) {
-                const bool ra = a < rl;
-                const float x0 = (ra && cp < rr) ? __ldg(gs + a * rr + cp) : 0.f;
-                const float x1 = (ra && cp + 1 < rr) ? __ldg(gs + a * rr + cp + 1) : 0.f;
-                g2[a] = pack2(x0, x1);
-                if constexpr (C1) g1[a] = (ra && cs < rr) ? __ldg(gs + a * rr + cs) : 0.f;
-              }
-            }
-            int n = bend - p;  // this group's segment length; the round runs the warp max
-            int nmax = n;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
-            for (int it = 0; it < nmax; it += 2) {
-              uint32_t row[2];
-#pragma unroll
-              for (int pi = 0; pi < 2; ++pi) {
-                const int w = it + pi;
-                row[pi] = s_state + (uint32_t)((w < n) ? (int)perm[p + w] : T) * (RP * 4);
-              }
-              uint64_t acc2[2] = {0ull, 0ull};
-              float acc1[2] = {0.f, 0.f};
-#pragma unroll
-              for (int a4 = 0; a4 < R / 4; ++a4) {
-                float4 v[2];
-#pragma unroll
-                for (int pi = 0; pi < 2; ++pi) v[pi] = lds128(row[pi] + a4 * 16);
-#pragma unroll
-                for (int pi = 0; pi < 2; ++pi) ffma2(acc2[pi], g2[a4 * 4 + 0], v[pi].x);
-#pragma unroll
-                for (int pi = 0; pi < 2; ++pi) ffma2(acc2[pi], g2[a4 * 4 + 1], v[pi].y);
-#pragma unroll
-                for (int pi = 0; pi < 2; ++pi) ffma2(acc2[pi], g2[a4 * 4 + 2], v[pi].z);
-#pragma unroll
-                for (int pi = 0; pi < 2; ++pi) ffma2(acc2[pi], g2[a4 * 4 + 3], v[pi].w);
-                if constexpr (C1) {
-#pragma unroll
-                  for (int pi = 0; pi < 2; ++pi) {
-                    acc1[pi] = fmaf(v[pi].x, g1[a4 * 4 + 0], acc1[pi]);
-                    acc1[pi] = fmaf(v[pi].y, g1[a4 * 4 + 1], acc1[pi]);
-                    acc1[pi] = fmaf(v[pi].z, g1[a4 * 4 + 2], acc1[pi]);
-                    acc1[pi] = fmaf(v[pi].w, g1[a4 * 4 + 3], acc1[pi]);
-                  }
-                }
-              }
-              __syncwarp();  // every lane of a group has read its sample's row
-#pragma unroll
-              for (int pi = 0; pi < 2; ++pi) {
-                sts_b64(row[pi] + cp * 4, acc2[pi]);
-                if constexpr (C1) sts32(row[pi] + cs * 4, acc1[pi]);
-              }
-              __syncwarp();
-            }
-            p = bend;
-          }
           }
         }
       }
@@ -1162,16 +1059,6 @@ int pick_R(int rmax) {
   return 0;
 }
 
-int bucket_threads() {
-  static int v = 0;
-  if (v == 0) {
-    const char* e = getenv("TNB_BUCKET_THREADS");
-    const int x = e ? atoi(e) : 512;
-    v = (x == 256 || x == 640 || x == 768) ? x : 512;
-  }
-  return v;
-}
-
 size_t prep_smem_bytes(int N, int T, int idx_bytes) { return (size_t)N * T * idx_bytes + 256; }
 
 size_t compute_smem(int T, int RP, int N, int idx_bytes, int jpad) {
@@ -1195,11 +1082,11 @@ int make_bplan(const ChainDev& ch, int64_t m, BPlan* bp, int* R_out, int* nt_out
       jmax = ch.m[k].J > jmax ? ch.m[k].J : jmax;
     }
   }
-  const int NT = bucket_threads();
+  constexpr int NT = kComputeThreads;
   const int RP = R + TNB_RPAD;
   const int idx_bytes = small ? 1 : 2;
   const int jpad = ((jmax + 1) + 7) & ~7;
-  const size_t budget = (size_t)(233472 / (NT <= 256 ? 2 : 1)) - 1024;
+  const size_t budget = (size_t)233472 - 1024;
   // the prep kernel holds every slot's permutation and per-warp counts at once
   auto prep_smem = [&](int t) { return prep_smem_bytes(ch.n, t, idx_bytes); };
   int T = 65504;
@@ -1208,12 +1095,6 @@ int make_bplan(const ChainDev& ch, int64_t m, BPlan* bp, int* R_out, int* nt_out
   if (compute_smem(T, RP, ch.n, idx_bytes, jpad) > budget || prep_smem(T) > 232448 - 1024)
     return set_error(TNB_EINVAL, "bucketed: chain too long for smem");
   bp->T = T;
-  {
-    const char* e = getenv("TNB_L1PF");
-    bp->l1pf = (e && e[0] == '1') ? 1 : 0;
-    const char* r = getenv("TNB_ROUNDS");
-    bp->rounds = (r && r[0] == '1') ? 1 : 0;
-  }
   bp->nsort = nsort;
   bp->jpad = jpad;
   bp->idx_bytes = idx_bytes;
@@ -1263,7 +1144,7 @@ int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m
   rc = check_cuda(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem),
                   "compute smem attr");
   if (rc) return rc;
-  const int64_t slots = (int64_t)num_sms() * (NT <= 256 ? 2 : 1);
+  const int64_t slots = (int64_t)num_sms();
   const int grid = (int)(bp.ntiles < slots ? bp.ntiles : slots);
   {
     KTimer kt("entries_compute", st);
@@ -1278,11 +1159,9 @@ int launch_ri(const ChainDev& ch, const BPlan& bp, int nt, const int64_t* idx, i
   const int N = ch.n;
   const bool fold = (R & 3) == 0 && N >= 3 && ch.m[N - 2].layout == TNB_LAYOUT_DIAG && ch.m[N - 1].rl == R &&
                     ch.m[N - 1].rr == 1;
-  if (fold) return launch_rt<R, IdxT, 512, true>(ch, bp, idx, m, out, err, ws, st);
-  if (nt == 256) return launch_rt<R, IdxT, 256, false>(ch, bp, idx, m, out, err, ws, st);
-  if (nt == 640) return launch_rt<R, IdxT, 640, false>(ch, bp, idx, m, out, err, ws, st);
-  if (nt == 768) return launch_rt<R, IdxT, 768, false>(ch, bp, idx, m, out, err, ws, st);
-  return launch_rt<R, IdxT, 512, false>(ch, bp, idx, m, out, err, ws, st);
+  (void)nt;
+  if (fold) return launch_rt<R, IdxT, kComputeThreads, true>(ch, bp, idx, m, out, err, ws, st);
+  return launch_rt<R, IdxT, kComputeThreads, false>(ch, bp, idx, m, out, err, ws, st);
 }
 
 }  // namespace

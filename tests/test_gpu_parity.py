@@ -280,10 +280,8 @@ def test_pipelined_host_indices_match_device_path():
         tb.entries(t, bad.pin_memory())
 
 
-@pytest.mark.parametrize("rounds", ["0", "1"])
-def test_bucketed_group_variants(rounds, monkeypatch):
-    # both R<=24 work distributions (one bucket per warp / per lane group)
-    monkeypatch.setenv("TNB_ROUNDS", rounds)
+def test_bucketed_cfg5_structure():
+    # the R=24 lane-group geometry on the cfg5 structure (J=128 buckets)
     nodes = O.cfg5_nodes(seed=1)
     t = facade(nodes)
     o = O.make_chain(nodes)

@@ -52,7 +52,7 @@ if __name__ == "__main__":
         algo = int(sys.argv[sys.argv.index("--algo") + 1]) if "--algo" in sys.argv else 0
         print(json.dumps(one(cfg, algo)))
         sys.exit(0)
-    variants = [{}, {"TNB_ROUNDS": "1"}, {"TNB_L1PF": "1"}]
+    variants = [{}, {"TNB_ENTRIES_MERGE": "0"}, {"TNB_LANE_MAJOR": "0"}]
     for v in variants:
         for cfg in ("cfg2", "cfg5"):
             env = dict(os.environ, **v)
