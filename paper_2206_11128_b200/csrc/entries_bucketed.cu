@@ -182,7 +182,11 @@ struct BPlan {
   int idx_bytes;   // sizeof(IdxT)
   int64_t ntiles;
   int64_t tile_bytes;
-  int64_t off_perm, off_starts;
+  int64_t off_wide, off_perm, off_starts;
+  // wide virtual modes: a prefix (mode 0) / suffix (mode N-1) table with more
+  // than 65535 rows; their combined indices are uint32 rows [nw][T] stored
+  // right after the compact [N][T] block (record and shared memory alike)
+  int wide0, wideL, nw;
   int8_t slot[kMaxModes];  // mode -> sorted slot or -1
   // mode merging: the kernels run a VIRTUAL chain whose first / last modes
   // may be prefix / suffix tables over several original modes; the prep
@@ -208,7 +212,8 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
   constexpr int NT = 512;
   extern __shared__ __align__(16) unsigned char smem[];
   const int N = ch.n, T = bp.T;
-  IdxT* idxs = reinterpret_cast<IdxT*>(smem);  // [N][T]
+  IdxT* idxs = reinterpret_cast<IdxT*>(smem);                                   // [N][T]
+  uint32_t* widx = reinterpret_cast<uint32_t*>(smem + (size_t)N * T * sizeof(IdxT));  // [nw][T]
   const int tid = threadIdx.x;
   const int64_t tile = blockIdx.x;
   const int64_t s0 = tile * T;
@@ -226,8 +231,14 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
       const int64_t* row = src + (int64_t)s * N0;
       if (s >= tn) {
         for (int k = 0; k < N; ++k) idxs[(size_t)k * T + s] = (IdxT)0;  // tail rows: index 0
+        for (int w = 0; w < bp.nw; ++w) widx[(size_t)w * T + s] = 0u;
         continue;
       }
+      auto store = [&](int v, uint32_t x) {
+        if (v == 0 && bp.wide0) widx[s] = x;
+        else if (v == N - 1 && bp.wideL) widx[(size_t)bp.wide0 * T + s] = x;
+        else idxs[(size_t)v * T + s] = (IdxT)x;
+      };
       int vk = 0;
       uint32_t cur = 0;
       auto put = [&](int o, int64_t raw) {
@@ -235,7 +246,7 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
         const uint32_t v = (uint32_t)norm_index(raw, J, o, err);
         const int tk = bp.vmap[o];
         if (tk != vk) {
-          idxs[(size_t)vk * T + s] = (IdxT)cur;
+          store(vk, cur);
           vk = tk;
           cur = 0;
         }
@@ -250,12 +261,12 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
       } else {
         for (int o = 0; o < N0; ++o) put(o, __ldg(row + o));
       }
-      idxs[(size_t)vk * T + s] = (IdxT)cur;
+      store(vk, cur);
     }
   }
   __syncthreads();
-  {  // compact block -> record (16-byte stores)
-    const int n16 = (int)(((size_t)N * T * sizeof(IdxT)) / 16);
+  {  // compact block (+ wide rows) -> record (16-byte stores)
+    const int n16 = (int)(((size_t)N * T * sizeof(IdxT) + (size_t)bp.nw * T * 4) / 16);
     for (int i = tid; i < n16; i += NT)
       reinterpret_cast<uint4*>(rec)[i] = reinterpret_cast<const uint4*>(idxs)[i];
   }
@@ -356,7 +367,8 @@ __global__ void __launch_bounds__(NT, 1)
   const int N = ch.n, T = bp.T;
   float* state = reinterpret_cast<float*>(smem);                                   // [T+1][RP]
   IdxT* cidx = reinterpret_cast<IdxT*>(state + (size_t)(T + 1) * RP);              // [N][T]
-  uint16_t* permb = reinterpret_cast<uint16_t*>(cidx + (size_t)N * T);             // [2][T]
+  uint32_t* widx = reinterpret_cast<uint32_t*>(cidx + (size_t)N * T);              // [nw][T]
+  uint16_t* permb = reinterpret_cast<uint16_t*>(widx + (size_t)bp.nw * T);         // [2][T]
   uint16_t* startb = permb + 2 * T;                                                // [2][jpad]
   uint64_t* bars = reinterpret_cast<uint64_t*>(
       (reinterpret_cast<uintptr_t>(startb + 2 * bp.jpad) + 15) & ~(uintptr_t)15);  // cbar, pbar[2], fbar
@@ -371,6 +383,9 @@ __global__ void __launch_bounds__(NT, 1)
   const int q = lane % L;
   const int64_t ntiles = bp.ntiles;
   const uint32_t row_bytes = (uint32_t)T * sizeof(IdxT);
+  const uint32_t wrow_bytes = (uint32_t)T * 4;
+  const uint32_t* widx0 = widx;                           // first mode (wide)
+  const uint32_t* widxL = widx + (size_t)bp.wide0 * T;    // last mode (wide)
   const uint32_t slot_bytes = (uint32_t)T * 2 + (uint32_t)bp.jpad * 2;
   const int ns = bp.nsort;
 
@@ -396,8 +411,9 @@ __global__ void __launch_bounds__(NT, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (blockIdx.x < ntiles) {
       const unsigned char* rec = ws + (int64_t)blockIdx.x * bp.tile_bytes;
-      mb_expect(cbar, row_bytes * N);
+      mb_expect(cbar, row_bytes * N + wrow_bytes * bp.nw);
       for (int k = 0; k < N; ++k) bulk(cidx + (size_t)k * T, rec + (size_t)k * row_bytes, row_bytes, cbar);
+      for (int w = 0; w < bp.nw; ++w) bulk(widx + (size_t)w * T, rec + bp.off_wide + (size_t)w * wrow_bytes, wrow_bytes, cbar);
       issue_slot(0);
       issue_slot(1);
     }
@@ -429,14 +445,17 @@ __global__ void __launch_bounds__(NT, 1)
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before async writes
           if (tid == 0) mb_expect(fbar, (uint32_t)tn * R * 4);
           __syncthreads();
-          for (int s = tid; s < tn; s += NT)
-            bulk(state + s * RP, md.s + (int64_t)col[s] * R, R * 4, fbar);
+          for (int s = tid; s < tn; s += NT) {
+            const int64_t j = bp.wide0 ? (int64_t)widx0[s] : (int64_t)col[s];
+            bulk(state + s * RP, md.s + j * R, R * 4, fbar);
+          }
           mb_wait(fbar, f_it & 1);
           ++f_it;
         } else {  // zero padded to R
           for (int e = tid; e < tn * R; e += NT) {
             const int s = e / R, c = e - (e / R) * R;
-            state[s * RP + c] = (c < rr) ? __ldg(md.s + (int64_t)col[s] * rr + c) : 0.f;
+            const int64_t j = bp.wide0 ? (int64_t)widx0[s] : (int64_t)col[s];
+            state[s * RP + c] = (c < rr) ? __ldg(md.s + j * rr + c) : 0.f;
           }
         }
       } else if (md.layout == TNB_LAYOUT_DIAG) {
@@ -505,7 +524,8 @@ __global__ void __launch_bounds__(NT, 1)
               const int s = base + u * SPW + g;
               act[u] = s < tn && c < CH;
               const int sc = act[u] ? s : 0;
-              gv[u] = __ldg(reinterpret_cast<const float4*>(md.s + (int64_t)col[sc] * R) + cc);
+              const int64_t jl = bp.wideL ? (int64_t)widxL[sc] : (int64_t)col[sc];
+              gv[u] = __ldg(reinterpret_cast<const float4*>(md.s + jl * R) + cc);
               if constexpr (FOLD) {
 #pragma unroll
                 for (int i = 0; i < MF; ++i)
@@ -557,7 +577,7 @@ __global__ void __launch_bounds__(NT, 1)
           }
         } else {
           for (int s = tid; s < tn; s += NT) {
-            const float* g = md.s + (int64_t)col[s] * rl;
+            const float* g = md.s + (bp.wideL ? (int64_t)widxL[s] : (int64_t)col[s]) * rl;
             const float* v = state + s * RP;
             float acc = 0.f;
 #pragma unroll
@@ -727,12 +747,15 @@ __global__ void __launch_bounds__(NT, 1)
       if (tid == 0) {
         // cidx rows k..k2 of this tile are dead: prefetch the next tile's rows
         if (ntile < ntiles) {
-          if (k == 0) mb_expect(cbar, row_bytes * N);
+          if (k == 0) mb_expect(cbar, row_bytes * N + wrow_bytes * bp.nw);
           // rows of a folded diagonal run stay live until the last mode
           const int klo = (FOLD && k == N - 1 && fold >= 0) ? fold : k;
           if (!(FOLD && fold >= 0 && k >= fold && k < N - 1))
             for (int kk = klo; kk <= k2; ++kk)
               bulk(cidx + (size_t)kk * T, ws + ntile * bp.tile_bytes + (size_t)kk * row_bytes, row_bytes, cbar);
+          const unsigned char* nrec = ws + ntile * bp.tile_bytes + bp.off_wide;
+          if (k == 0 && bp.wide0) bulk(widx, nrec, wrow_bytes, cbar);
+          if (k == N - 1 && bp.wideL) bulk(widx + (size_t)bp.wide0 * T, nrec + (size_t)bp.wide0 * wrow_bytes, wrow_bytes, cbar);
         }
         if (sorted) issue_slot(item + 2);  // this slot buffer is free again
       }
@@ -874,14 +897,29 @@ int merge_env() {
   return (e && e[0] == '0') ? 0 : 1;
 }
 
+int wide_env() {
+  const char* e = getenv("TNB_MERGE_WIDE");
+  return (e && e[0] == '0') ? 0 : 1;
+}
+
 void plan_merge(const ChainDev& ch, int64_t m, MergePlan* mp) {
   const int N = ch.n;
+  // uint16-indexed, L2-resident tables: up to min(m/16, 65535) rows.  A
+  // prefix / suffix may grow further ("wide": uint32 indices, HBM-resident,
+  // up to m/8 rows and 1.5 GB) but only by absorbing DENSE modes -- each
+  // one removes a sorted r x r step per entry for one gathered row.
   const int64_t lim = (merge_env() && N >= 3) ? (m / 16 < 65535 ? m / 16 : 65535) : 0;
+  const int64_t limw = (lim > 0 && wide_env()) ? std::min<int64_t>(m / 8, (int64_t)1 << 30) : lim;
+  const double max_table = 1.5e9;
+  auto grow = [&](int64_t nr, const ModeDev& md, int width) {
+    return nr <= lim || (nr <= limw && md.layout == TNB_LAYOUT_DENSE && (double)nr * width * 4 <= max_table);
+  };
   int a = 1, b = 1;
   int64_t rows = ch.m[0].J, rs = ch.m[N - 1].J;
   if (lim > 0) {
-    while (a < N - 1 && rows * ch.m[a].J <= lim) rows *= ch.m[a++].J;
-    while (N - 1 - b >= a && rs * ch.m[N - 1 - b].J <= lim) rs *= ch.m[N - 1 - b++].J;
+    while (a < N - 1 && grow(rows * ch.m[a].J, ch.m[a], ch.m[a].rr)) rows *= ch.m[a++].J;
+    while (N - 1 - b >= a && grow(rs * ch.m[N - 1 - b].J, ch.m[N - 1 - b], ch.m[N - 1 - b].rl))
+      rs *= ch.m[N - 1 - b++].J;
   }
   mp->table_bytes = 0;
   if (N == 1) {
@@ -1059,10 +1097,13 @@ int pick_R(int rmax) {
   return 0;
 }
 
-size_t prep_smem_bytes(int N, int T, int idx_bytes) { return (size_t)N * T * idx_bytes + 256; }
+size_t prep_smem_bytes(int N, int T, int idx_bytes, int nw) {
+  return (size_t)N * T * idx_bytes + (size_t)nw * T * 4 + 256;
+}
 
-size_t compute_smem(int T, int RP, int N, int idx_bytes, int jpad) {
-  size_t b = (size_t)(T + 1) * RP * 4 + (size_t)N * T * idx_bytes + (size_t)2 * T * 2 + (size_t)2 * jpad * 2;
+size_t compute_smem(int T, int RP, int N, int idx_bytes, int jpad, int nw) {
+  size_t b = (size_t)(T + 1) * RP * 4 + (size_t)N * T * idx_bytes + (size_t)nw * T * 4 + (size_t)2 * T * 2 +
+             (size_t)2 * jpad * 2;
   return ((b + 15) & ~(size_t)15) + 4 * 8;
 }
 
@@ -1072,8 +1113,13 @@ int make_bplan(const ChainDev& ch, int64_t m, BPlan* bp, int* R_out, int* nt_out
   if (!R) return set_error(TNB_EINVAL, "bucketed: rank > 32");
   int jmax = 1, nsort = 0;
   bool small = true;
+  const int N = ch.n;
+  bp->wide0 = ch.m[0].J > 65535;
+  bp->wideL = N > 1 && ch.m[N - 1].J > 65535;
+  bp->nw = bp->wide0 + bp->wideL;
   for (int k = 0; k < ch.n; ++k) {
-    if (ch.m[k].J > 256) small = false;
+    const bool wide = (k == 0 && bp->wide0) || (k == N - 1 && bp->wideL);
+    if (!wide && ch.m[k].J > 256) small = false;
     const bool srt = k > 0 && k < ch.n - 1 && ch.m[k].layout == TNB_LAYOUT_DENSE;
     bp->slot[k] = srt ? (int8_t)nsort : (int8_t)-1;
     if (srt) {
@@ -1088,18 +1134,21 @@ int make_bplan(const ChainDev& ch, int64_t m, BPlan* bp, int* R_out, int* nt_out
   const int jpad = ((jmax + 1) + 7) & ~7;
   const size_t budget = (size_t)233472 - 1024;
   // the prep kernel holds every slot's permutation and per-warp counts at once
-  auto prep_smem = [&](int t) { return prep_smem_bytes(ch.n, t, idx_bytes); };
+  auto prep_smem = [&](int t) { return prep_smem_bytes(ch.n, t, idx_bytes, bp->nw); };
+  auto comp_smem = [&](int t) { return compute_smem(t, RP, ch.n, idx_bytes, jpad, bp->nw); };
   int T = 65504;
-  while (T > 32 && (compute_smem(T, RP, ch.n, idx_bytes, jpad) > budget || prep_smem(T) > 232448 - 1024))
-    T -= 32;
-  if (compute_smem(T, RP, ch.n, idx_bytes, jpad) > budget || prep_smem(T) > 232448 - 1024)
+  while (T > 32 && (comp_smem(T) > budget || prep_smem(T) > 232448 - 1024)) T -= 32;
+  if (comp_smem(T) > budget || prep_smem(T) > 232448 - 1024)
     return set_error(TNB_EINVAL, "bucketed: chain too long for smem");
   bp->T = T;
   bp->nsort = nsort;
   bp->jpad = jpad;
   bp->idx_bytes = idx_bytes;
   bp->ntiles = (m + T - 1) / T;
-  const int64_t cidx_b = (((int64_t)ch.n * T * idx_bytes) + 15) & ~(int64_t)15;
+  // [N][T] compact rows, [nw][T] uint32 wide rows (contiguous: N*T*idx_bytes
+  // is a multiple of 32), then the sorted slots
+  bp->off_wide = (int64_t)ch.n * T * idx_bytes;
+  const int64_t cidx_b = bp->off_wide + (int64_t)bp->nw * T * 4;
   bp->off_perm = cidx_b;
   bp->off_starts = cidx_b + (int64_t)nsort * T * 2;
   bp->tile_bytes = (bp->off_starts + (int64_t)nsort * jpad * 2 + 127) & ~(int64_t)127;
@@ -1112,7 +1161,7 @@ template <int R, typename IdxT, int NT, bool FOLD>
 int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m, float* out,
               int32_t* err, unsigned char* ws, cudaStream_t st) {
   // prep: one CTA per tile; sort: one warp per (tile, sorted mode)
-  const size_t psmem = prep_smem_bytes(ch.n, bp.T, (int)sizeof(IdxT));
+  const size_t psmem = prep_smem_bytes(ch.n, bp.T, (int)sizeof(IdxT), bp.nw);
   int rc = check_cuda(cudaFuncSetAttribute(entries_prep_kernel<IdxT>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem),
                       "prep smem attr");
@@ -1139,7 +1188,7 @@ int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m
     rc = check_launch("entries_sort");
     if (rc) return rc;
   }
-  const size_t csmem = compute_smem(bp.T, R + TNB_RPAD, ch.n, (int)sizeof(IdxT), bp.jpad);
+  const size_t csmem = compute_smem(bp.T, R + TNB_RPAD, ch.n, (int)sizeof(IdxT), bp.jpad, bp.nw);
   auto ck = entries_compute_kernel<R, IdxT, NT, FOLD>;
   rc = check_cuda(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem),
                   "compute smem attr");

@@ -171,25 +171,32 @@ def test_entries_plan_merges_cfg2_and_cfg5(lib, monkeypatch):
     from paper_2206_11128_b200 import _native as N
 
     monkeypatch.delenv("TNB_ENTRIES_MERGE", raising=False)
-    # cfg2: 10 x TT, J=32, r=32, m=2^24 -> prefix 0-2 and suffix 7-9 tables
+    # cfg2: 10 x TT, J=32, r=32, m=2^24 -> wide (HBM) prefix 0-3 and suffix
+    # 6-9 tables of 2^20 rows: two sorted modes remain
     r = 32
     specs = [(0, 32, 1, r)] + [(0, 32, r, r)] * 8 + [(0, 32, r, 1)]
     info = N.entries_plan(_chain(specs), 1 << 24)
     assert info["algo"] == N.ALGO_BUCKETED
+    assert (info["prefix_modes"], info["suffix_modes"], info["n_virtual"]) == (4, 4, 4)
+    assert info["prefix_rows"] == info["suffix_rows"] == 32 ** 4
+    # virtual chain: 2 dense r x r steps + closing dot
+    assert info["kernel_flops"] == (2 * 2 * r * r + 2 * r) * float(1 << 24)
+    # without wide tables: 16-bit indexed L2 tables over modes 0-2 and 7-9
+    monkeypatch.setenv("TNB_MERGE_WIDE", "0")
+    info = N.entries_plan(_chain(specs), 1 << 24)
     assert (info["prefix_modes"], info["suffix_modes"], info["n_virtual"]) == (3, 3, 6)
     assert info["prefix_rows"] == info["suffix_rows"] == 32 ** 3
-    # virtual chain: 4 dense r x r steps + closing dot
     assert info["kernel_flops"] == (4 * 2 * r * r + 2 * r) * float(1 << 24)
     assert info["table_flops"] == 2 * (32 ** 2 * r * 2 * r + 32 ** 3 * r * 2 * r)
+    monkeypatch.delenv("TNB_MERGE_WIDE")
     # cfg5: TT 0-3 (r=24), CP 4-7 (diag interior, dense right end), J=128
     specs5 = [(0, 128, 1, 24)] + [(0, 128, 24, 24)] * 3 + [(1, 128, 24, 24)] * 3 + [(0, 128, 24, 1)]
     info5 = N.entries_plan(_chain(specs5), 1 << 26)
-    # prefix 0-1 and CP suffix 6-7 tables (16384 rows each), CP 4-5 as one
-    # diagonal product table: virtual chain P01, G2, G3, D45, S67
-    assert (info5["prefix_modes"], info5["suffix_modes"], info5["n_virtual"]) == (2, 2, 5)
-    # 3 table levels + lane-major copies of the two sorted modes
-    assert info5["diag_tables"] == 1 and info5["table_launches"] == 5
-    assert info5["kernel_flops"] == (2 * 2 * 24 * 24 + 24 + 2 * 24) * float(1 << 26)
+    # wide prefix 0-2 (2^21 rows), CP suffix 6-7 (16384 rows), CP 4-5 as one
+    # diagonal product table: virtual chain P012, G3, D45, S67
+    assert (info5["prefix_modes"], info5["suffix_modes"], info5["n_virtual"]) == (3, 2, 4)
+    assert info5["prefix_rows"] == 128 ** 3 and info5["diag_tables"] == 1
+    assert info5["kernel_flops"] == (2 * 24 * 24 + 24 + 2 * 24) * float(1 << 26)
     # smaller m: tables limited to m / 16 rows (2^16 -> 32*32 rows per side);
     # the chain kernel below 2^16 samples
     small = N.entries_plan(_chain(specs), 1 << 16)

@@ -372,3 +372,35 @@ def test_entries_out_argument():
     bad[m - 3, 2] = 16
     with pytest.raises(tb.ContractViolationError, match="mode 2"):
         tb.entries(t, bad.pin_memory(), out=host)
+
+
+@pytest.mark.parametrize("wide", ["1", "0"])
+def test_bucketed_wide_tables(wide, monkeypatch):
+    # prefix 0-3 and suffix 5-8 grow past 65535 rows (uint32 indices, tables in
+    # HBM) when m allows; both ends wide, a CP mode inside the prefix, ragged m
+    monkeypatch.setenv("TNB_MERGE_WIDE", wide)
+    rng = np.random.default_rng(11)
+    r = 8
+    nodes = [("tt", rng.standard_normal((1, 16, r)).astype(np.float32) * 0.5, None),
+             ("cp", rng.standard_normal((16, r)).astype(np.float32) * 0.7, None)]
+    nodes += [("tt", rng.standard_normal((r, 16, r)).astype(np.float32) * 0.35, None) for _ in range(6)]
+    nodes += [("tt", rng.standard_normal((r, 16, 1)).astype(np.float32) * 0.5, None)]
+    t = facade(nodes)
+    o = O.make_chain(nodes)
+    m = (1 << 20) + 123
+    plan = N.entries_plan(t._packed().chain, m, N.ALGO_AUTO)
+    if wide == "1":
+        assert plan["prefix_rows"] == 16 ** 4 and plan["suffix_rows"] == 16 ** 4 and plan["n_virtual"] == 3
+    else:
+        assert plan["prefix_rows"] < 65536 and plan["suffix_rows"] < 65536
+    idx = O.uniform_indices(t.shape, m, 21)
+    idx[::7] -= np.asarray(t.shape)
+    got = to_np(tb.entries(t, idx))
+    sel = np.concatenate([np.arange(0, 4096), np.arange(m - 4096, m), np.arange(5000, m - 5000, 101)])
+    assert_close(got[sel], O.entries(o, idx[sel]), what=f"wide={wide}")
+    for k in (0, 3, 5, 8):  # OOB on modes inside the wide prefix / suffix
+        bad = idx.copy()
+        bad[m // 2, k] = t.shape[k]
+        bad[m - 1, 8] = -17
+        with pytest.raises(tb.ContractViolationError, match=f"mode {k}"):
+            tb.entries(t, bad)
