@@ -825,6 +825,74 @@ __global__ void __launch_bounds__(256) table_suffix_step(ModeDev md, const float
   (void)J;
 }
 
+// Dense table steps as a tiled SIMT GEMM (the naive steps above re-read the
+// input row per output element and ran the FMA pipe at < 10%).  Per z = j:
+//   prefix: C_j[i][n] = sum_k A[i][k] G(j, k, n)  -> out[(i*J + j)*Nn + n]
+//   suffix: C_j[i][n] = sum_k A[i][k] G(j, n, k)  -> out[(j*rows + i)*Nn + n]
+// K, Nn <= 32 and Nn % 4 == 0.  CTA tile: 256 rows of A (transposed into
+// shared memory once) x kTZ slices; thread = 8 rows x 4 columns, so a warp's
+// 8 column quads of one row are one 128-byte store.
+constexpr int kTRows = 256, kTZ = 4;
+template <bool SUFFIX>
+__global__ void __launch_bounds__(256) table_gemm(ModeDev md, const float* __restrict__ A, int64_t rows,
+                                                  float* __restrict__ out) {
+  __shared__ __align__(16) float As[32][kTRows + 4];
+  __shared__ __align__(16) float Bs[32][32];
+  const int J = md.J;
+  const int K = SUFFIX ? md.rr : md.rl, Nn = SUFFIX ? md.rl : md.rr;
+  const int tid = threadIdx.x, tx = tid & 7, ty = tid >> 3;
+  const int64_t i0 = (int64_t)blockIdx.x * kTRows;
+  const int nr = (int)(rows - i0 < kTRows ? rows - i0 : kTRows);
+  for (int e = tid; e < kTRows * K; e += 256) {
+    const int r = e / K, k = e - r * K;
+    As[k][r] = r < nr ? __ldg(A + i0 * K + e) : 0.f;
+  }
+  const bool colok = 4 * tx < Nn;
+  for (int j = blockIdx.y * kTZ; j < min(J, (int)(blockIdx.y + 1) * kTZ); ++j) {
+    __syncthreads();  // As ready / previous Bs consumed
+    const float* g = md.s + (int64_t)j * md.rl * md.rr;
+    for (int e = tid; e < md.rl * md.rr; e += 256) {
+      const int a = e / md.rr, c = e - a * md.rr;
+      if (SUFFIX) Bs[c][a] = __ldg(g + e);
+      else Bs[a][c] = __ldg(g + e);
+    }
+    __syncthreads();
+    float acc[8][4];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[r][c] = 0.f;
+    if (colok) {
+      for (int k = 0; k < K; ++k) {
+        const float4 a0 = *reinterpret_cast<const float4*>(&As[k][ty * 8]);
+        const float4 a1 = *reinterpret_cast<const float4*>(&As[k][ty * 8 + 4]);
+        const float4 b = *reinterpret_cast<const float4*>(&Bs[k][4 * tx]);
+        const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          acc[r][0] = fmaf(av[r], b.x, acc[r][0]);
+          acc[r][1] = fmaf(av[r], b.y, acc[r][1]);
+          acc[r][2] = fmaf(av[r], b.z, acc[r][2]);
+          acc[r][3] = fmaf(av[r], b.w, acc[r][3]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int ri = ty * 8 + r;
+        if (ri >= nr) break;
+        const int64_t i = i0 + ri;
+        float* dst = SUFFIX ? out + ((int64_t)j * rows + i) * Nn : out + (i * J + j) * Nn;
+        *reinterpret_cast<float4*>(dst + 4 * tx) = make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]);
+      }
+    }
+  }
+}
+
+bool table_gemm_ok(const ModeDev& md, bool suffix) {
+  const int K = suffix ? md.rr : md.rl, Nn = suffix ? md.rl : md.rr;
+  return md.layout == TNB_LAYOUT_DENSE && K >= 1 && K <= 32 && Nn >= 4 && Nn <= 32 && (Nn & 3) == 0;
+}
+
 // Lane-major copy of a full-rank (R x R) sorted mode: the values one lane of
 // the compute kernel holds are contiguous 16-byte chunks, chunk-major across
 // lanes ([chunk][lane][4]) so a warp's load of chunk c is coalesced.
@@ -1039,7 +1107,11 @@ int build_tables(const ChainDev& ch, const MergePlan& mp, unsigned char* base, c
       for (int o = lo + 1; o < hi; ++o) {
         float* out = reinterpret_cast<float*>(base + mp.lvl[o]);
         const int64_t total = rows * ch.m[o].J * ch.m[o].rr;
-        if (total > 0) table_prefix_step<<<grid(total), 256, 0, st>>>(ch.m[o], in, rows, out);
+        if (total > 0 && table_gemm_ok(ch.m[o], false))
+          table_gemm<false><<<dim3((unsigned)ceil_div(rows, kTRows), (unsigned)ceil_div(ch.m[o].J, kTZ)), 256, 0,
+                              st>>>(ch.m[o], in, rows, out);
+        else if (total > 0)
+          table_prefix_step<<<grid(total), 256, 0, st>>>(ch.m[o], in, rows, out);
         int rc = check_launch("table_prefix_step");
         if (rc) return rc;
         in = out;
@@ -1057,7 +1129,10 @@ int build_tables(const ChainDev& ch, const MergePlan& mp, unsigned char* base, c
       for (int o = hi - 2; o >= lo; --o) {
         float* out = reinterpret_cast<float*>(base + mp.lvl[o]);
         const ModeDev& md = ch.m[o];
-        if ((int64_t)md.J * n * md.rl > 0) {
+        if ((int64_t)md.J * n * md.rl > 0 && table_gemm_ok(md, true)) {
+          table_gemm<true><<<dim3((unsigned)ceil_div(n, kTRows), (unsigned)ceil_div(md.J, kTZ)), 256, 0, st>>>(
+              md, in, n, out);
+        } else if ((int64_t)md.J * n * md.rl > 0) {
           const int per = 256 / md.rl;
           const int gx = (int)std::min<int64_t>(ceil_div(n, per), std::max<int64_t>(1, grid_cap / md.J));
           table_suffix_step<<<dim3(gx, md.J), 256, 0, st>>>(md, in, n, out);
