@@ -203,6 +203,9 @@ typedef struct {
   double table_flops;    /* per call: building the tables                      */
   int32_t diag_tables;   /* runs of interior CP modes merged into product tables */
   int32_t table_launches;/* kernel launches that build the tables per call     */
+  int32_t compute_kernel;/* bucketed: 0 = state kernel, 1 = stream kernel (one
+                            sorted mode; no per-sample state in shared memory) */
+  int32_t tile;          /* bucketed: samples per tile                          */
 } tnb_entries_info;
 int tnb_entries_plan(const tnb_chain* chain, int64_t m, int32_t algo, tnb_entries_info* info);
 

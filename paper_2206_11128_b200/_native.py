@@ -7,13 +7,16 @@ device is present, every compute entry point raises :class:`NativeError`.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_int64, c_void_p
 from pathlib import Path
 
 from .errors import ContractViolationError, NativeError
 
-LIB_PATH = Path(__file__).resolve().parent / "libtnb.so"
+# TNB_LIB: an alternative build of the same library (tools/build_variant.py
+# compiles kernel variants for A/B timing); the default is the in-tree build
+LIB_PATH = Path(os.environ.get("TNB_LIB") or Path(__file__).resolve().parent / "libtnb.so")
 
 TNB_OK, TNB_EINVAL, TNB_EINDEX, TNB_ECUDA, TNB_EWORKSPACE = 0, 1, 2, 3, 4
 KIND_TT, KIND_CP = 0, 1
@@ -42,7 +45,7 @@ class TnbEntriesInfo(ctypes.Structure):
     _fields_ = [("algo", c_int32), ("n_virtual", c_int32), ("prefix_modes", c_int32),
                 ("suffix_modes", c_int32), ("prefix_rows", c_int64), ("suffix_rows", c_int64),
                 ("kernel_flops", c_double), ("table_flops", c_double), ("diag_tables", c_int32),
-                ("table_launches", c_int32)]
+                ("table_launches", c_int32), ("compute_kernel", c_int32), ("tile", c_int32)]
 
 
 # name -> (restype, argtypes); exactly the declarations of include/tnb.h

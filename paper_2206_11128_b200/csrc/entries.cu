@@ -183,6 +183,7 @@ int entries_plan(const tnb_chain* c, int64_t m, int algo, tnb_entries_info* info
   info->prefix_rows = info->suffix_rows = 0;
   info->table_flops = 0.0;
   info->diag_tables = info->table_launches = 0;
+  info->compute_kernel = info->tile = 0;
   if (use_bucketed(ch, m, algo) && bucketed_supported(ch)) {
     info->algo = TNB_ALGO_BUCKETED;
     bucketed_info(ch, m, info);

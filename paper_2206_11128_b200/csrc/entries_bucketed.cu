@@ -38,6 +38,29 @@
 
 #include "common.cuh"
 
+#ifndef TNB_STREAM_THREADS
+#define TNB_STREAM_THREADS 384
+#endif
+#ifndef TNB_STREAM_RS
+#define TNB_STREAM_RS 0
+#endif
+#ifndef TNB_STREAM_T
+#define TNB_STREAM_T 6144
+#endif
+#ifndef TNB_STREAM_MMA
+#define TNB_STREAM_MMA 1
+#endif
+// first-mode row gathers: 0 = one cp.async.bulk (TMA) per row, 1 = 16-byte
+// cp.async (LDGSTS) pieces, one commit group per ring chunk
+#ifndef TNB_STREAM_LDGSTS
+#define TNB_STREAM_LDGSTS 1
+#endif
+// L2 prefetch of the first-mode rows TNB_STREAM_PF chunks beyond the ring
+// (same tile only): doubles the gathers in flight without shared memory
+#ifndef TNB_STREAM_PF
+#define TNB_STREAM_PF 0
+#endif
+
 namespace tnb {
 namespace {
 
@@ -187,6 +210,10 @@ struct BPlan {
   // than 65535 rows; their combined indices are uint32 rows [nw][T] stored
   // right after the compact [N][T] block (record and shared memory alike)
   int wide0, wideL, nw;
+  // compact rows stored: virtual modes crow0 .. crow0 + ncrow - 1 (all N for
+  // the state kernel; stream plans skip the first mode (always wide) and a
+  // wide last mode)
+  int crow0, ncrow;
   int8_t slot[kMaxModes];  // mode -> sorted slot or -1
   // mode merging: the kernels run a VIRTUAL chain whose first / last modes
   // may be prefix / suffix tables over several original modes; the prep
@@ -212,8 +239,8 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
   constexpr int NT = 512;
   extern __shared__ __align__(16) unsigned char smem[];
   const int N = ch.n, T = bp.T;
-  IdxT* idxs = reinterpret_cast<IdxT*>(smem);                                   // [N][T]
-  uint32_t* widx = reinterpret_cast<uint32_t*>(smem + (size_t)N * T * sizeof(IdxT));  // [nw][T]
+  IdxT* idxs = reinterpret_cast<IdxT*>(smem);                                         // [ncrow][T]
+  uint32_t* widx = reinterpret_cast<uint32_t*>(smem + (size_t)bp.ncrow * T * sizeof(IdxT));  // [nw][T]
   const int tid = threadIdx.x;
   const int64_t tile = blockIdx.x;
   const int64_t s0 = tile * T;
@@ -230,14 +257,14 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
     for (int s = tid; s < T; s += NT) {
       const int64_t* row = src + (int64_t)s * N0;
       if (s >= tn) {
-        for (int k = 0; k < N; ++k) idxs[(size_t)k * T + s] = (IdxT)0;  // tail rows: index 0
+        for (int k = 0; k < bp.ncrow; ++k) idxs[(size_t)k * T + s] = (IdxT)0;  // tail rows: index 0
         for (int w = 0; w < bp.nw; ++w) widx[(size_t)w * T + s] = 0u;
         continue;
       }
       auto store = [&](int v, uint32_t x) {
         if (v == 0 && bp.wide0) widx[s] = x;
         else if (v == N - 1 && bp.wideL) widx[(size_t)bp.wide0 * T + s] = x;
-        else idxs[(size_t)v * T + s] = (IdxT)x;
+        else idxs[(size_t)(v - bp.crow0) * T + s] = (IdxT)x;
       };
       int vk = 0;
       uint32_t cur = 0;
@@ -266,7 +293,7 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
   }
   __syncthreads();
   {  // compact block (+ wide rows) -> record (16-byte stores)
-    const int n16 = (int)(((size_t)N * T * sizeof(IdxT) + (size_t)bp.nw * T * 4) / 16);
+    const int n16 = (int)(((size_t)bp.ncrow * T * sizeof(IdxT) + (size_t)bp.nw * T * 4) / 16);
     for (int i = tid; i < n16; i += NT)
       reinterpret_cast<uint4*>(rec)[i] = reinterpret_cast<const uint4*>(idxs)[i];
   }
@@ -294,7 +321,7 @@ __global__ void __launch_bounds__(256) entries_sort_kernel(const __grid_constant
   unsigned char* rec = ws + tile * bp.tile_bytes;
   const int k = bp.smode[sl];
   const int J = ch.m[k].J;
-  const IdxT* col = reinterpret_cast<const IdxT*>(rec) + (size_t)k * T;
+  const IdxT* col = reinterpret_cast<const IdxT*>(rec) + (size_t)(k - bp.crow0) * T;
   uint16_t* pm = reinterpret_cast<uint16_t*>(rec + bp.off_perm) + (size_t)sl * T;
   uint16_t* gst = reinterpret_cast<uint16_t*>(rec + bp.off_starts) + (size_t)sl * JP;
   int* h = hist_all + (size_t)warp * (JP + T / 2);
@@ -765,6 +792,504 @@ __global__ void __launch_bounds__(NT, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// STREAM compute kernel: virtual chains with exactly ONE sorted mode, right
+// after the first one:   first (row gather) . G (R x R, sorted) . D* . last
+// (cfg5 after merging: P012 . G3 . D45 . S67).  There is no per-sample state
+// array, so a tile is not bounded by shared memory (T = 4096: a bucket holds
+// T / J samples, 32 at J = 128, against 16 in the state kernel).
+//   * the CTA streams tile records (compact indices, permutation, bucket
+//     starts) into a double buffer with one cp.async.bulk each;
+//   * each warp owns a contiguous range of sorted positions and is its own
+//     producer: its lanes gather the first-mode rows of the next samples, in
+//     sorted order, into a per-warp ring of kSD chunks x kSC rows with
+//     cp.async.bulk (the prefix table may be HBM-resident: the ring keeps
+//     kSD*kSC rows in flight), running ahead into the next tile's range;
+//   * per bucket the slice goes to registers once (Geo<R> column ownership)
+//     and a lane group evaluates a whole sample: w = v G on its columns,
+//     times the diagonal rows and the last row on those columns (direct L2
+//     loads), reduced over the group -> out[s].
+constexpr int kSC = 16;  // rows per ring chunk
+constexpr int kSD = 4;   // chunks per warp ring (ring row = sequence number & 63)
+
+__device__ __forceinline__ bool mb_test(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(s32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// split-TF32 on mma.sync m16n8k8: x = hi + lo, both rounded to tf32; the
+// three products lo*hi + hi*lo + hi*hi keep fp32-level accuracy
+__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
+  const float r = x - __uint_as_float(hi);
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo) : "f"(r));
+}
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ float lds32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+
+// ND: diagonal modes between the sorted and the last mode (0 or 1).  Stream
+// plans store the first and last modes' indices as uint32 rows (wide0 and
+// wideL are always set), the sorted and diagonal ones as IdxT.
+// MMA: the per-bucket (n x R) @ (R x R) products run on the tensor cores
+// (mma.sync m16n8k8, split TF32, 16 samples per warp step) with the slice's
+// B fragments pre-split into hi / lo by the table build (mma_slice_kernel);
+// otherwise FFMA2 lane groups (Geo<R>).
+template <int R, typename IdxT, int NT, int ND, bool MMA>
+__global__ void __launch_bounds__(NT, 1)
+    entries_stream_kernel(const __grid_constant__ ChainDev ch, const __grid_constant__ BPlan bp,
+                          const unsigned char* __restrict__ ws, int64_t m, float* __restrict__ out) {
+  using Gm = Geo<R>;
+  constexpr int C = Gm::C, L = Gm::L, G = Gm::G, P = Gm::P;
+  constexpr int NW = NT / 32;
+  constexpr int RING = kSC * kSD;
+  constexpr int C1 = (C == 3) ? 1 : 0;
+  constexpr int RS = MMA ? R + 4 : R;  // ring row stride (floats): conflict-free A-fragment loads
+  constexpr int KT = R / 8;            // MMA k- and n-tiles
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int N = ch.n, T = bp.T;
+  const int64_t TB = bp.tile_bytes;
+  unsigned char* recs = smem;                                                // [2][tile_bytes]
+  float* ring = reinterpret_cast<float*>(smem + 2 * TB);                     // [NW][RING][RS]
+  uint64_t* rbar = reinterpret_cast<uint64_t*>(ring + (size_t)NW * RING * RS);  // [2]
+  uint64_t* gbar = rbar + 2;                                                 // [NW][kSD]
+  int* rdone = reinterpret_cast<int*>(gbar + NW * kSD);                      // [2]
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gi = lane / L, q = lane % L;
+  const int cp = 2 * q, cs = 16 + q;
+  const int64_t ntiles = bp.ntiles;
+  const float* ftab = ch.m[0].s;
+  const float* gtab = ch.m[1].s;
+  const float* dtab = ch.m[ND ? 2 : 0].s;
+  const float* ltab = ch.m[N - 1].s;
+  const bool lmaj = bp.lmaj[1] != 0;
+  uint64_t* wbar = gbar + warp * kSD;
+  float* wring = ring + (size_t)warp * RING * RS;
+  const uint32_t s_ring = s32(wring);
+
+  auto tile_of = [&](int64_t ti) { return (int64_t)blockIdx.x + ti * gridDim.x; };
+  // the warp's sorted-position range of tile iteration ti (empty past the end)
+  auto range_of = [&](int64_t ti, int& lo, int& hi) {
+    const int64_t tile = tile_of(ti);
+    if (tile >= ntiles) {
+      lo = hi = 0;
+      return false;
+    }
+    const int64_t s0 = tile * T;
+    const int tn = (int)((m - s0) < T ? (m - s0) : T);
+    lo = (int)(((int64_t)warp * tn) / NW);
+    hi = (int)(((int64_t)(warp + 1) * tn) / NW);
+    return true;
+  };
+  auto load_rec = [&](int64_t ti) {  // tid 0
+    const int64_t tile = tile_of(ti);
+    if (tile >= ntiles) return;
+    uint64_t* b = &rbar[ti & 1];
+    mb_expect(b, (uint32_t)TB);
+    bulk(recs + (ti & 1) * TB, ws + tile * TB, (uint32_t)TB, b);
+  };
+  if (tid == 0) {
+    mb_init(&rbar[0], 1);
+    mb_init(&rbar[1], 1);
+    for (int i = 0; i < NW * kSD; ++i) mb_init(&gbar[i], 1);
+    rdone[0] = rdone[1] = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    load_rec(0);
+    load_rec(1);
+  }
+  __syncthreads();
+
+  // Ring bookkeeping in per-warp SEQUENCE numbers: a tile's range occupies
+  // [seq0, seq0 + hi - lo), seq0 a multiple of kSC, so a chunk (kSC
+  // consecutive sequence numbers) never spans two tiles; ring row = seq & 63.
+  int64_t pti = 0;  // producer: tile iteration being issued, its range, next chunk
+  int plo, phi;
+  bool pvalid = range_of(0, plo, phi);
+  int pcc = 0;
+  uint32_t c_issued = 0, c_waited = 0;
+  int64_t cti = 0;  // consumer tile iteration
+  auto try_issue = [&](bool block) -> bool {
+    while (true) {
+      if (!pvalid) return false;
+      if (pcc * kSC < phi - plo) break;
+      if (pti > cti) return false;  // never more than one tile ahead
+      ++pti;
+      pvalid = range_of(pti, plo, phi);
+      pcc = 0;
+    }
+    const int b = (int)(pti & 1);
+    if (pti > cti && !mb_test(&rbar[b], (uint32_t)((pti >> 1) & 1))) {  // next tile's record
+      if (!block) return false;
+      mb_wait(&rbar[b], (uint32_t)((pti >> 1) & 1));
+    }
+    const unsigned char* rec = recs + b * TB;
+    const int n = min(kSC, phi - plo - pcc * kSC);
+    const int slot = (int)(c_issued & (kSD - 1));
+    __syncwarp();
+#if TNB_STREAM_LDGSTS
+    {
+      const uint16_t* pp = reinterpret_cast<const uint16_t*>(rec + bp.off_perm) + plo + pcc * kSC;
+      const uint32_t* wi = reinterpret_cast<const uint32_t*>(rec + bp.off_wide);
+      const uint32_t dst0 = s_ring + (uint32_t)(slot * kSC * RS * 4);
+      for (int i = lane; i < n * (R / 4); i += 32) {
+        const int row = i / (R / 4), piece = i - row * (R / 4);
+        uint32_t j = wi[pp[row]];
+#ifdef TNB_STREAM_DEBUG_L2P
+        j &= TNB_STREAM_DEBUG_L2P;  // timing experiment only: an L2-resident slice of the table
+#endif
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst0 + (uint32_t)(row * RS * 4 + piece * 16)),
+                     "l"(ftab + (int64_t)j * R + piece * 4)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+#else
+    if (lane == 0) mb_expect(&wbar[slot], (uint32_t)(n * R * 4));
+    __syncwarp();
+    if (lane < n) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const int s = reinterpret_cast<const uint16_t*>(rec + bp.off_perm)[plo + pcc * kSC + lane];
+      const uint32_t j = reinterpret_cast<const uint32_t*>(rec + bp.off_wide)[s];
+      bulk(wring + (slot * kSC + lane) * RS, ftab + (int64_t)j * R, R * 4, &wbar[slot]);
+    }
+#endif
+#if TNB_STREAM_PF
+    {
+      const int pf = plo + (pcc + TNB_STREAM_PF) * kSC + (lane & (kSC - 1));
+      if (pf < phi) {
+        const int s = reinterpret_cast<const uint16_t*>(rec + bp.off_perm)[pf];
+        const uint32_t j = reinterpret_cast<const uint32_t*>(rec + bp.off_wide)[s];
+        const float* a = ftab + (int64_t)j * R + (lane >= kSC ? R - 1 : 0);  // first and last line of the row
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+      }
+    }
+#endif
+    ++pcc;
+    ++c_issued;
+    return true;
+  };
+
+  uint32_t seq0 = 0, last_try = ~0u;
+  for (;; ++cti) {
+    const int64_t tile = tile_of(cti);
+    if (tile >= ntiles) break;
+    const int b = (int)(cti & 1);
+    mb_wait(&rbar[b], (uint32_t)((cti >> 1) & 1));
+    const unsigned char* rec = recs + b * TB;
+    // compact rows start at mode 1 (crow0 == 1): sorted mode 1, diagonal
+    // mode 2, then the last mode unless it is wide (uint32 row after the
+    // first mode's)
+    const IdxT* ckey = reinterpret_cast<const IdxT*>(rec);
+    const IdxT* cdiag = reinterpret_cast<const IdxT*>(rec) + (size_t)T;
+    const IdxT* clastc = reinterpret_cast<const IdxT*>(rec) + (size_t)(N - 2) * T;
+    const uint32_t* clastw = reinterpret_cast<const uint32_t*>(rec + bp.off_wide) + (size_t)T;
+    const bool wl = bp.wideL != 0;
+    const uint16_t* perm = reinterpret_cast<const uint16_t*>(rec + bp.off_perm);
+    const uint16_t* st = reinterpret_cast<const uint16_t*>(rec + bp.off_starts);
+    float* otile = out + tile * T;
+    int lo, hi;
+    range_of(cti, lo, hi);
+    const uint32_t sbase = seq0 - (uint32_t)lo;  // seq of position p = sbase + p
+    // closing rows (last mode, diagonal mode) of positions q0 + w: raw loads
+    // whose latency the next iteration's FMA loop covers
+    float2 nlp[P], ndp[P];
+    float nls[P], nds[P];
+    auto load_close = [&](int q0) {
+#pragma unroll
+      for (int pi = 0; pi < P; ++pi) {
+        const int pos = min(q0 + pi * G + gi, hi - 1);
+        const int s = perm[pos];
+        const float* lr = ltab + (int64_t)(wl ? clastw[s] : (uint32_t)clastc[s]) * R;
+        nlp[pi] = __ldg(reinterpret_cast<const float2*>(lr + cp));
+        nls[pi] = C1 ? __ldg(lr + cs) : 0.f;
+        if constexpr (ND) {
+          const float* dr = dtab + (int64_t)cdiag[s] * R;
+          ndp[pi] = __ldg(reinterpret_cast<const float2*>(dr + cp));
+          nds[pi] = C1 ? __ldg(dr + cs) : 0.f;
+        }
+      }
+    };
+    // MMA: the same for rows g, g + 8 of a 16-sample step, columns 8nt + 2t
+    const int mg = lane >> 2, mt = lane & 3;
+    float2 mlp[2][KT], mdp[2][KT];
+    auto load_close_mma = [&](int q0) {
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int s = perm[min(q0 + mg + 8 * r, hi - 1)];
+        const float* lr = ltab + (int64_t)(wl ? clastw[s] : (uint32_t)clastc[s]) * R + 2 * mt;
+        const float* dr = dtab + (int64_t)cdiag[s] * R + 2 * mt;
+#pragma unroll
+        for (int nt = 0; nt < KT; ++nt) {
+          mlp[r][nt] = __ldg(reinterpret_cast<const float2*>(lr + 8 * nt));
+          if constexpr (ND) mdp[r][nt] = __ldg(reinterpret_cast<const float2*>(dr + 8 * nt));
+        }
+      }
+    };
+    if (lo < hi) {
+      if constexpr (MMA) load_close_mma(lo);
+      else load_close(lo);
+    }
+    while (c_issued < (seq0 / kSC) + kSD && try_issue(false)) {
+    }
+    int p = lo;
+    while (p < hi) {
+      const int key = ckey[perm[p]];
+      const int bend = min((int)st[key + 1], hi);
+      uint64_t g2[MMA ? 1 : R];
+      float g1[(C1 && !MMA) ? R : 1];
+      uint32_t bh[MMA ? KT : 1][MMA ? KT : 1][2], bl[MMA ? KT : 1][MMA ? KT : 1][2];
+      const float* gs = gtab + (int64_t)key * R * R * (MMA ? 2 : 1);
+      if constexpr (MMA) {
+        // [chunk][lane][4]: hi fragments (kt, nt, 2) then lo fragments
+        uint32_t f[4 * KT * KT];
+#pragma unroll
+        for (int c = 0; c < KT * KT; ++c) {
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(gs) + c * 32 + lane);
+          f[4 * c] = v.x;
+          f[4 * c + 1] = v.y;
+          f[4 * c + 2] = v.z;
+          f[4 * c + 3] = v.w;
+        }
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt)
+#pragma unroll
+          for (int nt = 0; nt < KT; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              bh[kt][nt][e] = f[(kt * KT + nt) * 2 + e];
+              bl[kt][nt][e] = f[2 * KT * KT + (kt * KT + nt) * 2 + e];
+            }
+      } else if (lmaj) {
+#pragma unroll
+        for (int c = 0; c < R / 2; ++c) {
+          const ulonglong2 v = ldg_u2(gs + (c * L + q) * 4);
+          g2[2 * c] = v.x;
+          g2[2 * c + 1] = v.y;
+        }
+        if constexpr (C1) {
+#pragma unroll
+          for (int c = 0; c < R / 4; ++c) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(gs + ((R / 2 + c) * L + q) * 4));
+            g1[4 * c] = v.x;
+            g1[4 * c + 1] = v.y;
+            g1[4 * c + 2] = v.z;
+            g1[4 * c + 3] = v.w;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int a = 0; a < R; ++a) {
+          g2[a] = ldg_b64(gs + a * R + cp);
+          if constexpr (C1) g1[a] = __ldg(gs + a * R + cs);
+        }
+      }
+      while (p < bend) {
+        const int n = min(MMA ? 16 : P * G, bend - p);
+        // ring chunks up to the one holding position p + n - 1
+        const uint32_t cneed = (sbase + (uint32_t)(p + n - 1)) / kSC;
+        while (c_waited <= cneed) {
+          while (c_issued <= c_waited) try_issue(true);
+#if TNB_STREAM_LDGSTS
+          // chunk c_waited complete: at most c_issued - 1 - c_waited newer groups pending
+          switch (min(c_issued - 1 - c_waited, (uint32_t)kSD - 1)) {
+            case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
+            case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+            case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+            default: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+          }
+          __syncwarp();
+#else
+          mb_wait(&wbar[c_waited & (kSD - 1)], (c_waited / kSD) & 1);
+#endif
+          ++c_waited;
+        }
+        if constexpr (MMA) {
+          // rows g, g + 8 of the step = sorted positions p + g, p + g + 8
+          // (clamped into the bucket: padding rows recompute a real sample)
+          int sr[2];
+          uint32_t vr[2];
+          float2 dcl[2][KT];
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            const int pos = p + min(mg + 8 * r, n - 1);
+            sr[r] = perm[pos];
+            vr[r] = s_ring + ((sbase + (uint32_t)pos) % RING) * (RS * 4) + mt * 4;
+#pragma unroll
+            for (int nt = 0; nt < KT; ++nt) {
+              dcl[r][nt] = mlp[r][nt];
+              if constexpr (ND) {
+                dcl[r][nt].x *= mdp[r][nt].x;
+                dcl[r][nt].y *= mdp[r][nt].y;
+              }
+            }
+          }
+          if (p + n < hi) load_close_mma(p + n);
+          float acc[KT][4];
+#pragma unroll
+          for (int nt = 0; nt < KT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
+#pragma unroll
+          for (int kt = 0; kt < KT; ++kt) {
+            uint32_t ah[4], al[4];
+            split_tf32(lds32(vr[0] + kt * 32), ah[0], al[0]);
+            split_tf32(lds32(vr[1] + kt * 32), ah[1], al[1]);
+            split_tf32(lds32(vr[0] + kt * 32 + 16), ah[2], al[2]);
+            split_tf32(lds32(vr[1] + kt * 32 + 16), ah[3], al[3]);
+#pragma unroll
+            for (int nt = 0; nt < KT; ++nt) {
+              mma_tf32(acc[nt], al, bh[kt][nt][0], bh[kt][nt][1]);
+              mma_tf32(acc[nt], ah, bl[kt][nt][0], bl[kt][nt][1]);
+              mma_tf32(acc[nt], ah, bh[kt][nt][0], bh[kt][nt][1]);
+            }
+          }
+          float part0 = 0.f, part1 = 0.f;
+#pragma unroll
+          for (int nt = 0; nt < KT; ++nt) {
+            part0 = fmaf(acc[nt][0], dcl[0][nt].x, part0);
+            part0 = fmaf(acc[nt][1], dcl[0][nt].y, part0);
+            part1 = fmaf(acc[nt][2], dcl[1][nt].x, part1);
+            part1 = fmaf(acc[nt][3], dcl[1][nt].y, part1);
+          }
+          // reduce-scatter over the 4 lanes of a row: odd lanes finish row g + 8
+          const bool odd = mt & 1;
+          float keep = odd ? part1 : part0;
+          keep += __shfl_xor_sync(0xffffffffu, odd ? part0 : part1, 1);
+          keep += __shfl_xor_sync(0xffffffffu, keep, 2);
+          if (mt < 2 && mg + 8 * mt < n) otile[mt ? sr[1] : sr[0]] = keep;
+        } else {
+        int sp[P];
+        uint32_t vrow[P];
+        float2 dp[P];
+        float ds[P];
+        // this iteration's closing rows (loaded one iteration ahead), then
+        // the prefetch for positions p + n .. (the next iteration, whatever
+        // its bucket)
+#pragma unroll
+        for (int pi = 0; pi < P; ++pi) {
+          dp[pi] = nlp[pi];
+          ds[pi] = nls[pi];
+          if constexpr (ND) {
+            dp[pi].x *= ndp[pi].x;
+            dp[pi].y *= ndp[pi].y;
+            if constexpr (C1) ds[pi] *= nds[pi];
+          }
+        }
+        if (p + n < hi) load_close(p + n);
+#pragma unroll
+        for (int pi = 0; pi < P; ++pi) {
+          const int w = pi * G + gi;
+          const int pos = p + (w < n ? w : n - 1);
+          sp[pi] = perm[pos];
+          vrow[pi] = s_ring + ((sbase + (uint32_t)pos) % RING) * (R * 4);
+        }
+        // two accumulator sets per sample (even / odd rows): 2P independent
+        // FFMA2 chains instead of P
+        uint64_t acc2[P][2];
+        float acc1[P][2];
+#pragma unroll
+        for (int pi = 0; pi < P; ++pi) {
+          acc2[pi][0] = acc2[pi][1] = 0ull;
+          acc1[pi][0] = acc1[pi][1] = 0.f;
+        }
+#pragma unroll
+        for (int a4 = 0; a4 < R / 4; ++a4) {
+          float4 v[P];
+#pragma unroll
+          for (int pi = 0; pi < P; ++pi) v[pi] = lds128(vrow[pi] + a4 * 16);
+#pragma unroll
+          for (int pi = 0; pi < P; ++pi) ffma2(acc2[pi][0], g2[a4 * 4 + 0], v[pi].x);
+#pragma unroll
+          for (int pi = 0; pi < P; ++pi) ffma2(acc2[pi][1], g2[a4 * 4 + 1], v[pi].y);
+#pragma unroll
+          for (int pi = 0; pi < P; ++pi) ffma2(acc2[pi][0], g2[a4 * 4 + 2], v[pi].z);
+#pragma unroll
+          for (int pi = 0; pi < P; ++pi) ffma2(acc2[pi][1], g2[a4 * 4 + 3], v[pi].w);
+          if constexpr (C1) {
+#pragma unroll
+            for (int pi = 0; pi < P; ++pi) {
+              acc1[pi][0] = fmaf(v[pi].x, g1[a4 * 4 + 0], acc1[pi][0]);
+              acc1[pi][1] = fmaf(v[pi].y, g1[a4 * 4 + 1], acc1[pi][1]);
+              acc1[pi][0] = fmaf(v[pi].z, g1[a4 * 4 + 2], acc1[pi][0]);
+              acc1[pi][1] = fmaf(v[pi].w, g1[a4 * 4 + 3], acc1[pi][1]);
+            }
+          }
+        }
+        float part[P];
+#pragma unroll
+        for (int pi = 0; pi < P; ++pi) {
+          const uint64_t w2 = add2(acc2[pi][0], acc2[pi][1]);
+          const float2 w = *reinterpret_cast<const float2*>(&w2);
+          float a = w.x * dp[pi].x;
+          a = fmaf(w.y, dp[pi].y, a);
+          if constexpr (C1) a = fmaf(acc1[pi][0] + acc1[pi][1], ds[pi], a);
+          part[pi] = a;
+        }
+        if constexpr (P == 2 && TNB_STREAM_RS) {
+          // reduce-scatter over the group: the first exchange swaps halves
+          // (lanes q < L/2 finish sample 0, the others sample 1), so two
+          // samples cost log2(L) shuffles instead of 2 log2(L)
+          const bool up = (q & (L / 2)) != 0;
+          float keep = up ? part[1] : part[0];
+          keep += __shfl_xor_sync(0xffffffffu, up ? part[0] : part[1], L / 2);
+#pragma unroll
+          for (int o = L / 4; o > 0; o >>= 1) keep += __shfl_xor_sync(0xffffffffu, keep, o);
+          if ((q & (L / 2 - 1)) == 0 && (up ? G : 0) + gi < n) otile[sp[up ? 1 : 0]] = keep;
+        } else {
+#pragma unroll
+          for (int o = L / 2; o > 0; o >>= 1) {
+#pragma unroll
+            for (int pi = 0; pi < P; ++pi) part[pi] += __shfl_xor_sync(0xffffffffu, part[pi], o);
+          }
+          if (q == 0) {
+#pragma unroll
+            for (int pi = 0; pi < P; ++pi)
+              if (pi * G + gi < n) otile[sp[pi]] = part[pi];
+          }
+        }
+        }
+        p += n;
+        // chunks wholly consumed -> refill the ring (this tile, then the
+        // next); a failed look-ahead is retried only after the next chunk
+        const uint32_t consumed = (sbase + (uint32_t)p) / kSC;
+        if (consumed != last_try && c_issued < consumed + kSD) {
+          last_try = consumed;
+          while (c_issued < consumed + kSD && try_issue(false)) {
+          }
+        }
+      }
+    }
+    seq0 += (uint32_t)((hi - lo + kSC - 1) / kSC * kSC);
+    while (c_issued < seq0 / kSC + kSD && try_issue(false)) {
+    }
+    // the LAST warp done with record buffer b reloads it (no CTA barrier:
+    // warps drift apart by up to a tile)
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      const int old = atomicAdd(&rdone[b], 1);
+      if (old == (int)((cti >> 1) + 1) * NW - 1) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        load_rec(cti + 2);
+      }
+    }
+  }
+}
+
 // ---- prefix / suffix tables for mode merging -------------------------------
 // prefix step (rows in C order of the merged indices):
 //   out[(p*J + j)*rr + c] = sum_a in[p*rl + a] * G(j, a, c)      (dense)
@@ -926,6 +1451,29 @@ __global__ void lane_major_kernel(const float* __restrict__ src, float* __restri
   }
 }
 
+// Tensor-core copy of the stream plan's sorted mode (R x R slices, R % 8 ==
+// 0): per slice [chunk][lane][4] with the lane's m16n8k8 B fragments,
+// b(kt, nt, e) = G[8kt + t + 4e][8nt + g] (g = lane / 4, t = lane % 4), first
+// rounded to tf32 (hi) for every (kt, nt, e), then the tf32 remainders (lo).
+__global__ void mma_slice_kernel(const float* __restrict__ src, float* __restrict__ dst, int J, int R) {
+  const int KT = R / 8, nb = 2 * KT * KT;  // hi values per lane
+  const int per = 32 * 2 * nb;             // floats per slice
+  const int64_t total = (int64_t)J * per;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = i / per;
+    const int r = (int)(i - j * per);
+    const int c = r / 128, lane = (r / 4) % 32, f = 4 * c + (r & 3);
+    const int lo = f >= nb, idx = f % nb;
+    const int kt = idx / (2 * KT), nt = (idx / 2) % KT, e = idx & 1;
+    const int g = lane >> 2, t = lane & 3;
+    const float x = __ldg(src + j * R * R + (int64_t)(8 * kt + t + 4 * e) * R + 8 * nt + g);
+    uint32_t h, l;
+    split_tf32(x, h, l);
+    dst[i] = __uint_as_float(lo ? l : h);
+  }
+}
+
 int pick_R(int rmax);
 
 int lane_major_env() {
@@ -956,6 +1504,7 @@ struct MergePlan {
   int64_t lm_off[kMaxModes];     // ... at this byte offset
   int R = 0;                     // register geometry of the virtual chain
   int64_t table_bytes = 0;       // 256-aligned
+  bool mma1 = false;             // virtual mode 1's copy is the tensor-core layout (stream plans)
   int a() const { return kind[0] == kPrefix ? hi[0] - lo[0] : 1; }
   int b() const { return kind[ng - 1] == kSuffix ? hi[ng - 1] - lo[ng - 1] : 1; }
 };
@@ -1117,6 +1666,10 @@ int build_tables(const ChainDev& ch, const MergePlan& mp, unsigned char* base, c
         in = out;
         rows *= ch.m[o].J;
       }
+    } else if (mp.lm[g] && g == 1 && mp.mma1) {
+      const ModeDev& md = ch.m[lo];
+      mma_slice_kernel<<<grid((int64_t)md.J * md.rl * md.rr * 2), 256, 0, st>>>(
+          md.s, reinterpret_cast<float*>(base + mp.lm_off[g]), md.J, md.rl);
     } else if (mp.lm[g]) {
       const ModeDev& md = ch.m[lo];
       lane_major_kernel<<<grid((int64_t)md.J * md.rl * md.rr), 256, 0, st>>>(
@@ -1183,15 +1736,18 @@ size_t compute_smem(int T, int RP, int N, int idx_bytes, int jpad, int nw) {
 }
 
 // Shared by the workspace query and the launcher so both agree on T.
-int make_bplan(const ChainDev& ch, int64_t m, BPlan* bp, int* R_out, int* nt_out) {
+int make_bplan(const ChainDev& ch, int64_t m, BPlan* bp, int* R_out, int* nt_out, int t_force = 0,
+               bool stream = false) {
   const int R = pick_R(ch.rmax);
   if (!R) return set_error(TNB_EINVAL, "bucketed: rank > 32");
   int jmax = 1, nsort = 0;
   bool small = true;
   const int N = ch.n;
-  bp->wide0 = ch.m[0].J > 65535;
+  bp->wide0 = stream || ch.m[0].J > 65535;
   bp->wideL = N > 1 && ch.m[N - 1].J > 65535;
   bp->nw = bp->wide0 + bp->wideL;
+  bp->crow0 = stream ? 1 : 0;
+  bp->ncrow = stream ? N - 1 - bp->wideL : N;
   for (int k = 0; k < ch.n; ++k) {
     const bool wide = (k == 0 && bp->wide0) || (k == N - 1 && bp->wideL);
     if (!wide && ch.m[k].J > 256) small = false;
@@ -1209,12 +1765,17 @@ int make_bplan(const ChainDev& ch, int64_t m, BPlan* bp, int* R_out, int* nt_out
   const int jpad = ((jmax + 1) + 7) & ~7;
   const size_t budget = (size_t)233472 - 1024;
   // the prep kernel holds every slot's permutation and per-warp counts at once
-  auto prep_smem = [&](int t) { return prep_smem_bytes(ch.n, t, idx_bytes, bp->nw); };
+  auto prep_smem = [&](int t) { return prep_smem_bytes(bp->ncrow, t, idx_bytes, bp->nw); };
   auto comp_smem = [&](int t) { return compute_smem(t, RP, ch.n, idx_bytes, jpad, bp->nw); };
   int T = 65504;
-  while (T > 32 && (comp_smem(T) > budget || prep_smem(T) > 232448 - 1024)) T -= 32;
-  if (comp_smem(T) > budget || prep_smem(T) > 232448 - 1024)
-    return set_error(TNB_EINVAL, "bucketed: chain too long for smem");
+  if (t_force > 0) {
+    T = t_force;
+    if (prep_smem(T) > 232448 - 1024) return set_error(TNB_EINVAL, "bucketed: chain too long for smem");
+  } else {
+    while (T > 32 && (comp_smem(T) > budget || prep_smem(T) > 232448 - 1024)) T -= 32;
+    if (comp_smem(T) > budget || prep_smem(T) > 232448 - 1024)
+      return set_error(TNB_EINVAL, "bucketed: chain too long for smem");
+  }
   bp->T = T;
   bp->nsort = nsort;
   bp->jpad = jpad;
@@ -1222,7 +1783,7 @@ int make_bplan(const ChainDev& ch, int64_t m, BPlan* bp, int* R_out, int* nt_out
   bp->ntiles = (m + T - 1) / T;
   // [N][T] compact rows, [nw][T] uint32 wide rows (contiguous: N*T*idx_bytes
   // is a multiple of 32), then the sorted slots
-  bp->off_wide = (int64_t)ch.n * T * idx_bytes;
+  bp->off_wide = (int64_t)bp->ncrow * T * idx_bytes;
   const int64_t cidx_b = bp->off_wide + (int64_t)bp->nw * T * 4;
   bp->off_perm = cidx_b;
   bp->off_starts = cidx_b + (int64_t)nsort * T * 2;
@@ -1232,11 +1793,94 @@ int make_bplan(const ChainDev& ch, int64_t m, BPlan* bp, int* R_out, int* nt_out
   return TNB_OK;
 }
 
+int stream_env() {
+  const char* e = getenv("TNB_ENTRIES_STREAM");
+  return (e && e[0] == '0') ? 0 : 1;
+}
+
+// first (rl 1, rr R) . G (R x R dense) . D (diagonal, R)* . last (rl R, rr 1)
+bool stream_shape_ok(const ChainDev& v, int R) {
+  if (!stream_env() || (R != 8 && R != 16 && R != 24) || v.n < 3 || v.n > 4) return false;
+  const int N = v.n;
+  const ModeDev &f = v.m[0], &g = v.m[1], &l = v.m[N - 1];
+  if (f.layout != TNB_LAYOUT_DENSE || f.rl != 1 || f.rr != R) return false;
+  if (g.layout != TNB_LAYOUT_DENSE || g.rl != R || g.rr != R || g.J > kMaxJ) return false;
+  if (l.layout != TNB_LAYOUT_DENSE || l.rl != R || l.rr != 1) return false;
+  for (int k = 2; k < N - 1; ++k)
+    if (v.m[k].layout != TNB_LAYOUT_DIAG || v.m[k].rl != R) return false;
+  return true;
+}
+
+constexpr int kStreamThreads = TNB_STREAM_THREADS;
+constexpr bool kStreamMma = TNB_STREAM_MMA != 0;
+size_t stream_smem(const BPlan& bp, int R) {
+  const int rs = kStreamMma ? R + 4 : R;
+  return 2 * (size_t)bp.tile_bytes + (size_t)(kStreamThreads / 32) * kSD * kSC * rs * 4 + 128 +
+         (size_t)(2 + (kStreamThreads / 32) * kSD) * 8 + 16;
+}
+
+// Everything a call needs to know, shared by the workspace query, the plan
+// report and the launcher so all three agree.
+struct EPlan {
+  MergePlan mp;
+  ChainDev v;
+  BPlan bp;
+  int R = 0, nt = 0;
+  bool stream = false;
+};
+int plan_entries(const ChainDev& ch, int64_t m, EPlan* P) {
+  plan_merge(ch, m, &P->mp);
+  virtual_chain(ch, P->mp, nullptr, &P->v);
+  int rc = make_bplan(P->v, m, &P->bp, &P->R, &P->nt);
+  if (rc) return rc;
+  P->stream = false;
+  if (P->bp.nsort == 1 && stream_shape_ok(P->v, P->R) && (!kStreamMma || P->mp.lm[1])) {
+    // tiles of up to 4096 samples, at least two per SM when m allows
+    int T = TNB_STREAM_T;
+    while (T > 256 && (m + T - 1) / T < 2 * 148) T = std::max(256, (T >> 1) & ~31);
+    BPlan bs;
+    int R2, nt2;
+    while (T >= 256) {  // the largest tile whose double-buffered record fits next to the rings
+      if (make_bplan(P->v, m, &bs, &R2, &nt2, T, true) == TNB_OK &&
+          stream_smem(bs, R2) <= (size_t)232448 - 1024) {
+        P->bp = bs;
+        P->stream = true;
+        if (kStreamMma) {  // the sorted mode's copy doubles (hi / lo fragments); it is the last table
+          const ModeDev& g1 = ch.m[P->mp.lo[1]];
+          P->mp.mma1 = true;
+          P->mp.table_bytes = P->mp.lm_off[1] + (((int64_t)g1.J * g1.rl * g1.rr * 2 * 4 + 255) & ~(int64_t)255);
+        }
+        break;
+      }
+      T = T > 1024 ? T - 512 : T >> 1;
+    }
+  }
+  return TNB_OK;
+}
+
+template <int R, typename IdxT>
+int launch_stream(const ChainDev& ch, const BPlan& bp, const unsigned char* ws, int64_t m, float* out,
+                  cudaStream_t st) {
+  const size_t smem = stream_smem(bp, R);
+  auto k = ch.n == 4 ? entries_stream_kernel<R, IdxT, kStreamThreads, 1, kStreamMma>
+                     : entries_stream_kernel<R, IdxT, kStreamThreads, 0, kStreamMma>;
+  int rc = check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                      "stream smem attr");
+  if (rc) return rc;
+  const int64_t slots = (int64_t)num_sms();
+  const int grid = (int)(bp.ntiles < slots ? bp.ntiles : slots);
+  {
+    KTimer kt("entries_compute", st);
+    k<<<grid, kStreamThreads, smem, st>>>(ch, bp, ws, m, out);
+  }
+  return check_launch("entries_stream");
+}
+
 template <int R, typename IdxT, int NT, bool FOLD>
 int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m, float* out,
-              int32_t* err, unsigned char* ws, cudaStream_t st) {
+              int32_t* err, unsigned char* ws, bool stream, cudaStream_t st) {
   // prep: one CTA per tile; sort: one warp per (tile, sorted mode)
-  const size_t psmem = prep_smem_bytes(ch.n, bp.T, (int)sizeof(IdxT), bp.nw);
+  const size_t psmem = prep_smem_bytes(bp.ncrow, bp.T, (int)sizeof(IdxT), bp.nw);
   int rc = check_cuda(cudaFuncSetAttribute(entries_prep_kernel<IdxT>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem),
                       "prep smem attr");
@@ -1263,6 +1907,10 @@ int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m
     rc = check_launch("entries_sort");
     if (rc) return rc;
   }
+  if (stream) {
+    if constexpr (R <= 24) return launch_stream<R, IdxT>(ch, bp, ws, m, out, st);
+    return set_error(TNB_EINVAL, "stream kernel: rank > 24");
+  }
   const size_t csmem = compute_smem(bp.T, R + TNB_RPAD, ch.n, (int)sizeof(IdxT), bp.jpad, bp.nw);
   auto ck = entries_compute_kernel<R, IdxT, NT, FOLD>;
   rc = check_cuda(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem),
@@ -1279,13 +1927,13 @@ int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m
 
 template <int R, typename IdxT>
 int launch_ri(const ChainDev& ch, const BPlan& bp, int nt, const int64_t* idx, int64_t m, float* out,
-              int32_t* err, unsigned char* ws, cudaStream_t st) {
+              int32_t* err, unsigned char* ws, bool stream, cudaStream_t st) {
   const int N = ch.n;
-  const bool fold = (R & 3) == 0 && N >= 3 && ch.m[N - 2].layout == TNB_LAYOUT_DIAG && ch.m[N - 1].rl == R &&
-                    ch.m[N - 1].rr == 1;
+  const bool fold = !stream && (R & 3) == 0 && N >= 3 && ch.m[N - 2].layout == TNB_LAYOUT_DIAG &&
+                    ch.m[N - 1].rl == R && ch.m[N - 1].rr == 1;
   (void)nt;
-  if (fold) return launch_rt<R, IdxT, kComputeThreads, true>(ch, bp, idx, m, out, err, ws, st);
-  return launch_rt<R, IdxT, kComputeThreads, false>(ch, bp, idx, m, out, err, ws, st);
+  if (fold) return launch_rt<R, IdxT, kComputeThreads, true>(ch, bp, idx, m, out, err, ws, stream, st);
+  return launch_rt<R, IdxT, kComputeThreads, false>(ch, bp, idx, m, out, err, ws, stream, st);
 }
 
 }  // namespace
@@ -1303,24 +1951,21 @@ bool bucketed_supported(const ChainDev& ch) {
 }
 
 int64_t bucketed_workspace(const ChainDev& ch, int64_t m) {
-  BPlan bp;
-  int R, nt;
   if (m <= 0 || !bucketed_supported(ch)) return 0;
-  MergePlan mp;
-  plan_merge(ch, m, &mp);
-  ChainDev v;
-  virtual_chain(ch, mp, nullptr, &v);
-  if (make_bplan(v, m, &bp, &R, &nt)) return 0;
-  return mp.table_bytes + bp.ntiles * bp.tile_bytes;
+  EPlan P;
+  if (plan_entries(ch, m, &P)) return 0;
+  return P.mp.table_bytes + P.bp.ntiles * P.bp.tile_bytes;
 }
 
 double chain_entry_flops(const ChainDev& ch);
 
 void bucketed_info(const ChainDev& ch, int64_t m, tnb_entries_info* info) {
-  MergePlan mp;
-  plan_merge(ch, m, &mp);
-  ChainDev v;
-  virtual_chain(ch, mp, nullptr, &v);
+  EPlan P;
+  plan_entries(ch, m, &P);
+  const MergePlan& mp = P.mp;
+  const ChainDev& v = P.v;
+  info->compute_kernel = P.stream ? 1 : 0;
+  info->tile = P.bp.T;
   info->n_virtual = v.n;
   info->prefix_modes = mp.a();
   info->suffix_modes = mp.b();
@@ -1354,14 +1999,14 @@ void bucketed_info(const ChainDev& ch, int64_t m, tnb_entries_info* info) {
 
 int launch_entries_bucketed(const ChainDev& ch, const int64_t* idx, int64_t m, float* out,
                             int32_t* err, void* ws, int64_t ws_bytes, cudaStream_t st) {
-  MergePlan mp;
-  plan_merge(ch, m, &mp);
-  ChainDev v;
-  virtual_chain(ch, mp, nullptr, &v);
-  BPlan bp;
-  int R, nt;
-  int rc = make_bplan(v, m, &bp, &R, &nt);
+  EPlan P;
+  int rc = plan_entries(ch, m, &P);
   if (rc) return rc;
+  const MergePlan& mp = P.mp;
+  ChainDev& v = P.v;
+  BPlan& bp = P.bp;
+  const int R = P.R, nt = P.nt;
+  const bool stream = P.stream;
   const int64_t need = mp.table_bytes + bp.ntiles * bp.tile_bytes;
   if (!ws || ws_bytes < need)
     return set_error(TNB_EWORKSPACE, "bucketed entries needs %lld workspace bytes, got %lld",
@@ -1379,17 +2024,17 @@ int launch_entries_bucketed(const ChainDev& ch, const int64_t* idx, int64_t m, f
   const bool small = bp.idx_bytes == 1;
   switch (R) {
     case 8:
-      return small ? launch_ri<8, uint8_t>(chv, bp, nt, idx, m, out, err, w, st)
-                   : launch_ri<8, uint16_t>(chv, bp, nt, idx, m, out, err, w, st);
+      return small ? launch_ri<8, uint8_t>(chv, bp, nt, idx, m, out, err, w, stream, st)
+                   : launch_ri<8, uint16_t>(chv, bp, nt, idx, m, out, err, w, stream, st);
     case 16:
-      return small ? launch_ri<16, uint8_t>(chv, bp, nt, idx, m, out, err, w, st)
-                   : launch_ri<16, uint16_t>(chv, bp, nt, idx, m, out, err, w, st);
+      return small ? launch_ri<16, uint8_t>(chv, bp, nt, idx, m, out, err, w, stream, st)
+                   : launch_ri<16, uint16_t>(chv, bp, nt, idx, m, out, err, w, stream, st);
     case 24:
-      return small ? launch_ri<24, uint8_t>(chv, bp, nt, idx, m, out, err, w, st)
-                   : launch_ri<24, uint16_t>(chv, bp, nt, idx, m, out, err, w, st);
+      return small ? launch_ri<24, uint8_t>(chv, bp, nt, idx, m, out, err, w, stream, st)
+                   : launch_ri<24, uint16_t>(chv, bp, nt, idx, m, out, err, w, stream, st);
     default:
-      return small ? launch_ri<32, uint8_t>(chv, bp, nt, idx, m, out, err, w, st)
-                   : launch_ri<32, uint16_t>(chv, bp, nt, idx, m, out, err, w, st);
+      return small ? launch_ri<32, uint8_t>(chv, bp, nt, idx, m, out, err, w, stream, st)
+                   : launch_ri<32, uint16_t>(chv, bp, nt, idx, m, out, err, w, stream, st);
   }
 }
 

@@ -197,6 +197,22 @@ def test_entries_plan_merges_cfg2_and_cfg5(lib, monkeypatch):
     assert (info5["prefix_modes"], info5["suffix_modes"], info5["n_virtual"]) == (3, 2, 4)
     assert info5["prefix_rows"] == 128 ** 3 and info5["diag_tables"] == 1
     assert info5["kernel_flops"] == (2 * 24 * 24 + 24 + 2 * 24) * float(1 << 26)
+    # one sorted mode left: the stream kernel (4096-sample tiles); cfg2 keeps
+    # the state kernel (two sorted modes)
+    assert (info5["compute_kernel"], info5["tile"]) == (1, 5632)
+    assert N.entries_plan(_chain(specs), 1 << 24)["compute_kernel"] == 0
+    monkeypatch.setenv("TNB_ENTRIES_STREAM", "0")
+    assert N.entries_plan(_chain(specs5), 1 << 26)["compute_kernel"] == 0
+    monkeypatch.delenv("TNB_ENTRIES_STREAM")
+    # the GPU stream tests' chain (tests/test_gpu_parity.py::_stream_nodes)
+    for rr in (8, 16, 24):
+        st = [(0, 8, 1, rr), (0, 8, rr, rr), (0, 64, rr, rr), (0, 300, rr, rr), (1, 9, rr, rr), (1, 11, rr, rr),
+              (0, 5000, rr, 1)]
+        for mm in (300000, 70001):
+            i = N.entries_plan(_chain(st), mm)
+            assert (i["compute_kernel"], i["n_virtual"], i["prefix_rows"]) == (1, 4, 4096), (rr, mm, i)
+        i = N.entries_plan(_chain(st[:4] + st[6:]), 200000)
+        assert (i["compute_kernel"], i["n_virtual"]) == (1, 3), i
     # smaller m: tables limited to m / 16 rows (2^16 -> 32*32 rows per side);
     # the chain kernel below 2^16 samples
     small = N.entries_plan(_chain(specs), 1 << 16)

@@ -404,3 +404,61 @@ def test_bucketed_wide_tables(wide, monkeypatch):
         bad[m - 1, 8] = -17
         with pytest.raises(tb.ContractViolationError, match=f"mode {k}"):
             tb.entries(t, bad)
+
+
+def _stream_nodes(rng, r, jl=5000):
+    # prefix 0-2 (4096 rows), ONE sorted mode (J=300), the CP run 4-5 as a
+    # diagonal table, a last mode too large to merge: P012 . G3 . D45 . L6
+    s = r ** -0.5
+    return [
+        ("tt", rng.standard_normal((1, 8, r)).astype(np.float32), None),
+        ("tt", (rng.standard_normal((r, 8, r)) * s).astype(np.float32), None),
+        ("tt", (rng.standard_normal((r, 64, r)) * s).astype(np.float32), None),
+        ("tt", (rng.standard_normal((r, 300, r)) * s).astype(np.float32), None),
+        ("cp", rng.standard_normal((9, r)).astype(np.float32), None),
+        ("cp", rng.standard_normal((7, r)).astype(np.float32), rng.standard_normal((11, 7)).astype(np.float32)),
+        ("tt", (rng.standard_normal((r, jl, 1)) * s).astype(np.float32), None),
+    ]
+
+
+@pytest.mark.parametrize("r", [8, 16, 24])
+@pytest.mark.parametrize("m", [300000, 70001])
+def test_bucketed_stream_kernel(r, m, monkeypatch):
+    # virtual chains with one sorted mode run the stream kernel (no state
+    # array): per-warp TMA row rings running ahead across tiles, ragged tiles
+    rng = np.random.default_rng(r)
+    nodes = _stream_nodes(rng, r)
+    t = facade(nodes)
+    o = O.make_chain(nodes)
+    plan = N.entries_plan(t._packed().chain, m, N.ALGO_AUTO)
+    assert plan["compute_kernel"] == 1 and plan["n_virtual"] == 4, plan
+    idx = O.uniform_indices(t.shape, m, 4)
+    idx[::3] -= np.asarray(t.shape)
+    got = to_np(tb.entries(t, idx))
+    sel = np.concatenate([np.arange(0, 5000), np.arange(m - 3000, m), np.arange(5000, m - 3000, 13)])
+    assert_close(got[sel], O.entries(o, idx[sel]), what=f"stream r={r}")
+    monkeypatch.setenv("TNB_ENTRIES_STREAM", "0")
+    assert N.entries_plan(t._packed().chain, m, N.ALGO_AUTO)["compute_kernel"] == 0
+    ref = to_np(tb.entries(t, idx))
+    assert_close(got, ref.astype(np.float64), what="stream vs state kernel")
+    monkeypatch.delenv("TNB_ENTRIES_STREAM")
+    for k in (0, 3, 5, 6):  # OOB inside the prefix, the sorted mode, the CP table, the last mode
+        bad = idx.copy()
+        bad[m // 2, k] = t.shape[k]
+        bad[m - 1, 6] = -t.shape[6] - 1
+        with pytest.raises(tb.ContractViolationError, match=f"mode {k}"):
+            tb.entries(t, bad)
+
+
+def test_bucketed_stream_no_diag():
+    # P012 . G3 . L4: no diagonal modes between the sorted and the last mode
+    rng = np.random.default_rng(3)
+    nodes = _stream_nodes(rng, 24)
+    nodes = nodes[:4] + [nodes[6]]
+    t = facade(nodes)
+    o = O.make_chain(nodes)
+    m = 200000
+    assert N.entries_plan(t._packed().chain, m, N.ALGO_AUTO)["compute_kernel"] == 1
+    idx = O.uniform_indices(t.shape, m, 5)
+    sel = np.arange(0, m, 11)
+    assert_close(to_np(tb.entries(t, idx))[sel], O.entries(o, idx[sel]), what="stream no diag")
