@@ -57,6 +57,11 @@
 #endif
 // L2 prefetch of the first-mode rows TNB_STREAM_PF chunks beyond the ring
 // (same tile only): doubles the gathers in flight without shared memory
+// tile records in flight (a warp may run one tile ahead of the slowest one
+// before the producer's look-ahead stalls)
+#ifndef TNB_STREAM_NREC
+#define TNB_STREAM_NREC 2
+#endif
 #ifndef TNB_STREAM_PF
 #define TNB_STREAM_PF 0
 #endif
@@ -864,11 +869,12 @@ __global__ void __launch_bounds__(NT, 1)
   extern __shared__ __align__(128) unsigned char smem[];
   const int N = ch.n, T = bp.T;
   const int64_t TB = bp.tile_bytes;
-  unsigned char* recs = smem;                                                // [2][tile_bytes]
-  float* ring = reinterpret_cast<float*>(smem + 2 * TB);                     // [NW][RING][RS]
+  constexpr int NR = TNB_STREAM_NREC;
+  unsigned char* recs = smem;                                                // [NR][tile_bytes]
+  float* ring = reinterpret_cast<float*>(smem + NR * TB);                    // [NW][RING][RS]
   uint64_t* rbar = reinterpret_cast<uint64_t*>(ring + (size_t)NW * RING * RS);  // [2]
-  uint64_t* gbar = rbar + 2;                                                 // [NW][kSD]
-  int* rdone = reinterpret_cast<int*>(gbar + NW * kSD);                      // [2]
+  uint64_t* gbar = rbar + NR;                                                // [NW][kSD]
+  int* rdone = reinterpret_cast<int*>(gbar + NW * kSD);                      // [NR]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gi = lane / L, q = lane % L;
@@ -900,18 +906,16 @@ __global__ void __launch_bounds__(NT, 1)
   auto load_rec = [&](int64_t ti) {  // tid 0
     const int64_t tile = tile_of(ti);
     if (tile >= ntiles) return;
-    uint64_t* b = &rbar[ti & 1];
+    uint64_t* b = &rbar[ti % NR];
     mb_expect(b, (uint32_t)TB);
-    bulk(recs + (ti & 1) * TB, ws + tile * TB, (uint32_t)TB, b);
+    bulk(recs + (ti % NR) * TB, ws + tile * TB, (uint32_t)TB, b);
   };
   if (tid == 0) {
-    mb_init(&rbar[0], 1);
-    mb_init(&rbar[1], 1);
+    for (int i = 0; i < NR; ++i) mb_init(&rbar[i], 1);
     for (int i = 0; i < NW * kSD; ++i) mb_init(&gbar[i], 1);
-    rdone[0] = rdone[1] = 0;
+    for (int i = 0; i < NR; ++i) rdone[i] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    load_rec(0);
-    load_rec(1);
+    for (int i = 0; i < NR; ++i) load_rec(i);
   }
   __syncthreads();
 
@@ -933,10 +937,10 @@ __global__ void __launch_bounds__(NT, 1)
       pvalid = range_of(pti, plo, phi);
       pcc = 0;
     }
-    const int b = (int)(pti & 1);
-    if (pti > cti && !mb_test(&rbar[b], (uint32_t)((pti >> 1) & 1))) {  // next tile's record
+    const int b = (int)(pti % NR);
+    if (pti > cti && !mb_test(&rbar[b], (uint32_t)((pti / NR) & 1))) {  // next tile's record
       if (!block) return false;
-      mb_wait(&rbar[b], (uint32_t)((pti >> 1) & 1));
+      mb_wait(&rbar[b], (uint32_t)((pti / NR) & 1));
     }
     const unsigned char* rec = recs + b * TB;
     const int n = min(kSC, phi - plo - pcc * kSC);
@@ -944,18 +948,22 @@ __global__ void __launch_bounds__(NT, 1)
     __syncwarp();
 #if TNB_STREAM_LDGSTS
     {
-      const uint16_t* pp = reinterpret_cast<const uint16_t*>(rec + bp.off_perm) + plo + pcc * kSC;
-      const uint32_t* wi = reinterpret_cast<const uint32_t*>(rec + bp.off_wide);
+      // lane r < n looks up row r's table index once; the 16-byte pieces go
+      // piece-major over the lanes (consecutive lanes, consecutive bytes of
+      // a row) with the index broadcast by a shuffle
+      const uint32_t jr = lane < n ? reinterpret_cast<const uint32_t*>(rec + bp.off_wide)[
+                                         reinterpret_cast<const uint16_t*>(rec + bp.off_perm)[plo + pcc * kSC + lane]]
+                                   : 0u;
       const uint32_t dst0 = s_ring + (uint32_t)(slot * kSC * RS * 4);
-      for (int i = lane; i < n * (R / 4); i += 32) {
+#pragma unroll
+      for (int it = 0; it < (kSC * R / 4 + 31) / 32; ++it) {
+        const int i = lane + 32 * it;
         const int row = i / (R / 4), piece = i - row * (R / 4);
-        uint32_t j = wi[pp[row]];
-#ifdef TNB_STREAM_DEBUG_L2P
-        j &= TNB_STREAM_DEBUG_L2P;  // timing experiment only: an L2-resident slice of the table
-#endif
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst0 + (uint32_t)(row * RS * 4 + piece * 16)),
-                     "l"(ftab + (int64_t)j * R + piece * 4)
-                     : "memory");
+        const uint32_t j = __shfl_sync(0xffffffffu, jr, row & 31);
+        if (row < n)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst0 + (uint32_t)(row * RS * 4 + piece * 16)),
+                       "l"(ftab + (int64_t)j * R + piece * 4)
+                       : "memory");
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
@@ -989,8 +997,8 @@ __global__ void __launch_bounds__(NT, 1)
   for (;; ++cti) {
     const int64_t tile = tile_of(cti);
     if (tile >= ntiles) break;
-    const int b = (int)(cti & 1);
-    mb_wait(&rbar[b], (uint32_t)((cti >> 1) & 1));
+    const int b = (int)(cti % NR);
+    mb_wait(&rbar[b], (uint32_t)((cti / NR) & 1));
     const unsigned char* rec = recs + b * TB;
     // compact rows start at mode 1 (crow0 == 1): sorted mode 1, diagonal
     // mode 2, then the last mode unless it is wide (uint32 row after the
@@ -1282,9 +1290,9 @@ __global__ void __launch_bounds__(NT, 1)
     if (lane == 0) {
       __threadfence_block();
       const int old = atomicAdd(&rdone[b], 1);
-      if (old == (int)((cti >> 1) + 1) * NW - 1) {
+      if (old == (int)((cti / NR) + 1) * NW - 1) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        load_rec(cti + 2);
+        load_rec(cti + NR);
       }
     }
   }
@@ -1815,8 +1823,8 @@ constexpr int kStreamThreads = TNB_STREAM_THREADS;
 constexpr bool kStreamMma = TNB_STREAM_MMA != 0;
 size_t stream_smem(const BPlan& bp, int R) {
   const int rs = kStreamMma ? R + 4 : R;
-  return 2 * (size_t)bp.tile_bytes + (size_t)(kStreamThreads / 32) * kSD * kSC * rs * 4 + 128 +
-         (size_t)(2 + (kStreamThreads / 32) * kSD) * 8 + 16;
+  return TNB_STREAM_NREC * (size_t)bp.tile_bytes + (size_t)(kStreamThreads / 32) * kSD * kSC * rs * 4 + 128 +
+         (size_t)(TNB_STREAM_NREC + (kStreamThreads / 32) * kSD) * 8 + 4 * TNB_STREAM_NREC + 16;
 }
 
 // Everything a call needs to know, shared by the workspace query, the plan
