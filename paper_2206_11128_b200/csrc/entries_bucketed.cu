@@ -38,6 +38,13 @@
 
 #include "common.cuh"
 
+// state kernel: L2 prefetch of wide first / last mode rows
+#ifndef TNB_LAST_U
+#define TNB_LAST_U 4
+#endif
+#ifndef TNB_STATE_PF
+#define TNB_STATE_PF 0
+#endif
 #ifndef TNB_STREAM_THREADS
 #define TNB_STREAM_THREADS 384
 #endif
@@ -364,6 +371,9 @@ __global__ void __launch_bounds__(256) entries_sort_kernel(const __grid_constant
 }
 
 __device__ __forceinline__ uint32_t s32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
+}
 __device__ __forceinline__ void mb_init(uint64_t* b, uint32_t c) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s32(b)), "r"(c));
 }
@@ -460,6 +470,22 @@ __global__ void __launch_bounds__(NT, 1)
     const int64_t ntile = tile + gridDim.x;
     mb_wait(cbar, c_it & 1);
     ++c_it;
+#if TNB_STATE_PF
+    // wide (HBM-resident) prefix / suffix tables: L2 prefetch of this tile's
+    // last-mode rows (used after the sorted modes) and of the NEXT tile's
+    // first-mode rows (indices read from its record in global memory), so
+    // neither gather waits on HBM latency
+    if (bp.wideL) {
+      const ModeDev& ml = ch.m[N - 1];
+      for (int s = tid; s < tn; s += NT) prefetch_l2(ml.s + (int64_t)widxL[s] * ml.rl);
+    }
+    if (bp.wide0 && ntile < ntiles) {
+      const int64_t ns0 = ntile * T;
+      const int ntn = (int)((m - ns0) < T ? (m - ns0) : T);
+      const uint32_t* nw = reinterpret_cast<const uint32_t*>(ws + ntile * bp.tile_bytes + bp.off_wide);
+      for (int s = tid; s < ntn; s += NT) prefetch_l2(ch.m[0].s + (int64_t)__ldg(nw + s) * ch.m[0].rr);
+    }
+#endif
     int fold = -1;  // first CP mode of a diagonal run folded into the last mode
     for (int k = 0; k < N; ++k) {
       const ModeDev& md = ch.m[k];
@@ -546,7 +572,7 @@ __global__ void __launch_bounds__(NT, 1)
             dps[i] = FOLD ? ch.m[kk].s : md.s;
             dcs[i] = cidx + (size_t)kk * T;
           }
-          constexpr int U = 4;  // samples per lane group in flight (L2 latency)
+          constexpr int U = TNB_LAST_U;  // samples per lane group in flight (L2 / HBM latency)
           for (int base = warp * (U * SPW); base < tn; base += nwarps * U * SPW) {
             // every load of the U samples is issued before any use
             float4 gv[U], v[U], dv[U][MF];
