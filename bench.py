@@ -290,11 +290,13 @@ def bench_entries(args, cfg, dev, dist, ws, rank):
     ms_step = ms / args.steps
     value = ws * m / (ms_step * 1e-3)
     peak, peak_src = fp32_peak()
-    traffic, traffic_src = ncu_traffic(f"{cfg}_entries", "entries_compute_kernel")
+    stream_k = plan["compute_kernel"] == 1
+    kname = "entries_stream_kernel" if stream_k else "entries_compute_kernel"
+    traffic, traffic_src = ncu_traffic(f"{cfg}_entries", kname)
     kms, kn = kt["entries_compute"]
     if kn:  # bucketed: the per-entry compute kernel, timed on its own stream
         k_ms = kms / kn
-        kernel = "entries_compute_kernel"
+        kernel = kname
     else:  # chain / layered algorithm: one kernel is the whole step
         k_ms = ms_step
         kernel = "entries_chain_kernel"
@@ -313,15 +315,20 @@ def bench_entries(args, cfg, dev, dist, ws, rank):
             "kernel_ms": k_ms, "kernel_share_of_step": k_ms / ms_step,
             "algorithmic": (f"{chain_flops_per_entry} flop/entry (SURVEY 8(d): 2*r_l*r_r per dense mode, R per "
                             f"CP interior mode) x {m} entries per launch / compute-kernel launch time"),
+            "frac_note": ("frac > 1 is possible: the kernel runs a shorter virtual chain than the reference's "
+                          "(mode merging); 'executed' is its real arithmetic rate"),
             "executed": {"tflops": executed, "frac_of_fp32_peak": executed / peak,
                          "flop_per_entry": per_entry,
-                         "what": (f"FMA work the kernel actually issues: the {plan['n_virtual']}-mode chain left "
+                         "pipe": ("tensor (mma.sync m16n8k8 split-TF32, 3 MMAs per product) for the sorted mode, "
+                                  "FFMA for the closing dot" if stream_k else "fp32 (FFMA2)"),
+                         "what": (f"useful arithmetic of the {plan['n_virtual']}-mode virtual chain the kernel runs "
                                   f"after merging modes 0..{plan['prefix_modes'] - 1} and the last "
-                                  f"{plan['suffix_modes']} modes into L2-resident tables (built every call, "
+                                  f"{plan['suffix_modes']} modes into prefix / suffix tables (built every call, "
                                   f"{plan['table_flops']:.3g} flop) and {plan['diag_tables']} CP run(s) into "
-                                  "product tables")},
+                                  "diagonal product tables")},
             "plan": {k: plan[k] for k in ("algo", "n_virtual", "prefix_modes", "suffix_modes",
-                                          "prefix_rows", "suffix_rows", "diag_tables", "table_flops")},
+                                          "prefix_rows", "suffix_rows", "diag_tables", "table_flops",
+                                          "compute_kernel", "tile")},
             "other_kernels_ms": {k: (v[0] / v[1] if v[1] else None) for k, v in kt.items()
                                  if k != "entries_compute"},
             "step_tflops": algo_flops / (ms_step * 1e-3) / 1e12,
@@ -358,6 +365,21 @@ def bench_entries(args, cfg, dev, dist, ws, rank):
                      "steps": e2e_steps, "path": "paper_2206_11128_b200.entries(t, pinned host int64, out=pinned host float32)"}
     fields["_t"], fields["_out"], fields["_idx_host"] = t, out, idx_host
     return fields
+
+
+def entries_secondary(args, dev, dist, ws, rank):
+    """cfg5 (BASELINE configs[4], the hybrid CP-TT-Tucker chain, 2^26 tuples)
+    as a secondary line of the default run: device-resident throughput, the
+    compute kernel's roofline and the end-to-end rate."""
+    import copy
+
+    a = copy.copy(args)
+    a.steps, a.warmup = 3, 3
+    f = bench_entries(a, "cfg5", dev, dist, ws, rank)
+    for k in ("_t", "_out", "_idx_host"):
+        f.pop(k)
+    return {"op": "entries", "workload": "cfg5: " + W.CONFIGS["cfg5"][0], "ms_per_step": f["ms_per_step"],
+            "entries/s": f["value"], "roofline": f["roofline"], "e2e": f["e2e"], "gpu_launches": f["gpu_launches"]}
 
 
 def cpu_baseline_entries(t_nodes_fn, idx_host, out_dev, m_sample):
@@ -501,10 +523,13 @@ def run_ours(args):
         torch.cuda.empty_cache()
         if not args.no_secondary and ws == 1:
             sec = []
-            for fn in (lambda: bench_full(dev, 3, 2, dist), lambda: bench_dot(dev, 5, 2, dist),
+            for fn in ((lambda: entries_secondary(args, dev, dist, ws, rank)) if cfg == "cfg2" else (lambda: None),
+                       lambda: bench_full(dev, 3, 2, dist), lambda: bench_dot(dev, 5, 2, dist),
                        lambda: bench_dot(dev, 5, 2, dist, True)):
                 try:
-                    sec.append(fn())
+                    r = fn()
+                    if r is not None:
+                        sec.append(r)
                 except Exception as e:  # noqa: BLE001
                     sec.append({"error": repr(e)})
                 torch.cuda.empty_cache()
