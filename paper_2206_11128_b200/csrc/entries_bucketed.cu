@@ -39,6 +39,11 @@
 #include "common.cuh"
 
 // state kernel: L2 prefetch of wide first / last mode rows
+// state kernel: full-rank r = 32 sorted modes on mma.sync split-TF32 (state
+// rows padded to 36 floats for conflict-light A-fragment loads)
+#ifndef TNB_STATE_MMA
+#define TNB_STATE_MMA 1
+#endif
 #ifndef TNB_LAST_U
 #define TNB_LAST_U 4
 #endif
@@ -128,6 +133,26 @@ __device__ __forceinline__ void sts32(uint32_t a, float x) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(x) : "memory");
 }
 
+// split-TF32 on mma.sync m16n8k8: x = hi + lo, both rounded to tf32; the
+// three products lo*hi + hi*lo + hi*hi keep fp32-level accuracy
+__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
+  const float r = x - __uint_as_float(hi);
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo) : "f"(r));
+}
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ float lds32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+
 // Column ownership inside a sample group of L lanes (lane q): C == 2 -> the
 // pair (2q, 2q+1); C == 3 (R = 24, L = 8) -> the pair (2q, 2q+1) plus the
 // single column 16 + q.  Pairs are updated with packed FFMA2 (fma.rn.f32x2).
@@ -137,7 +162,7 @@ struct Geo {
   static constexpr int L = R / C;              // lanes per sample group
   static constexpr int G = 32 / L;             // sample groups per warp
   static constexpr int P = 8 / G;              // passes per iteration (8 samples)
-  static constexpr int RP = R + TNB_RPAD;       // state row stride (floats)
+  static constexpr int RP = R + ((R == 32 && TNB_STATE_MMA) ? 4 : TNB_RPAD);  // state row stride (floats)
   static_assert(L * C == R && 32 % L == 0 && G * P == 8, "geometry");
 };
 
@@ -237,6 +262,7 @@ struct BPlan {
   int8_t vmap[kMaxModes];
   int8_t smode[kMaxModes];  // sorted slot -> (virtual) mode
   int8_t lmaj[kMaxModes];   // sorted mode whose slices are in lane-major order
+  int8_t mmal[kMaxModes];   // ... in the tensor-core fragment order (mma_slice_kernel)
 };
 
 // prep: one CTA per tile -- reads the tile's n0 int64 index columns
@@ -655,6 +681,74 @@ __global__ void __launch_bounds__(NT, 1)
         const int hi = (int)(((int64_t)(warp + 1) * tn) / nwarps);
         if constexpr (R == 32) {
         int p = lo;
+#if TNB_STATE_MMA
+        if (bp.mmal[k]) {
+          // tensor cores: 16 samples of one bucket per step, rows g and g + 8
+          // (sorted positions p + g, p + g + 8) of the m16n8k8 tiles; the
+          // state rows are read as A fragments and overwritten in place by
+          // the C fragments (v <- v G) after the whole step has read them
+          const int mg = lane >> 2, mt = lane & 3;
+          while (p < hi) {
+            const int key = col[perm[p]];
+            const int bend = min((int)st[key + 1], hi);
+            uint32_t bh[4][4][2], bl[4][4][2];
+            {
+              const uint4* gs = reinterpret_cast<const uint4*>(md.s + (int64_t)key * R * R * 2);
+              uint32_t f[64];
+#pragma unroll
+              for (int c = 0; c < 16; ++c) {
+                const uint4 v = __ldg(gs + c * 32 + lane);
+                f[4 * c] = v.x;
+                f[4 * c + 1] = v.y;
+                f[4 * c + 2] = v.z;
+                f[4 * c + 3] = v.w;
+              }
+#pragma unroll
+              for (int kt = 0; kt < 4; ++kt)
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+                  for (int e = 0; e < 2; ++e) {
+                    bh[kt][nt][e] = f[(kt * 4 + nt) * 2 + e];
+                    bl[kt][nt][e] = f[32 + (kt * 4 + nt) * 2 + e];
+                  }
+            }
+            while (p < bend) {
+              const int n = min(16, bend - p);
+              const uint32_t r0 = s_state + (uint32_t)perm[p + min(mg, n - 1)] * (RP * 4);
+              const uint32_t r1 = s_state + (uint32_t)perm[p + min(mg + 8, n - 1)] * (RP * 4);
+              float acc[4][4];
+#pragma unroll
+              for (int nt = 0; nt < 4; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
+#pragma unroll
+              for (int kt = 0; kt < 4; ++kt) {
+                uint32_t ah[4], al[4];
+                split_tf32(lds32(r0 + kt * 32 + mt * 4), ah[0], al[0]);
+                split_tf32(lds32(r1 + kt * 32 + mt * 4), ah[1], al[1]);
+                split_tf32(lds32(r0 + kt * 32 + mt * 4 + 16), ah[2], al[2]);
+                split_tf32(lds32(r1 + kt * 32 + mt * 4 + 16), ah[3], al[3]);
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) {
+                  mma_tf32(acc[nt], al, bh[kt][nt][0], bh[kt][nt][1]);
+                  mma_tf32(acc[nt], ah, bl[kt][nt][0], bl[kt][nt][1]);
+                  mma_tf32(acc[nt], ah, bh[kt][nt][0], bh[kt][nt][1]);
+                }
+              }
+              __syncwarp();  // every row of the step has been read
+              if (mg < n) {
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) sts_b64(r0 + nt * 32 + mt * 8, pack2(acc[nt][0], acc[nt][1]));
+              }
+              if (mg + 8 < n) {
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) sts_b64(r1 + nt * 32 + mt * 8, pack2(acc[nt][2], acc[nt][3]));
+              }
+              __syncwarp();
+              p += n;
+            }
+          }
+        }
+#endif
         while (p < hi) {
           const int key = col[perm[p]];
           const int bend = min((int)st[key + 1], hi);
@@ -852,26 +946,6 @@ __device__ __forceinline__ bool mb_test(uint64_t* b, uint32_t parity) {
       : "r"(s32(b)), "r"(parity)
       : "memory");
   return ok != 0;
-}
-
-// split-TF32 on mma.sync m16n8k8: x = hi + lo, both rounded to tf32; the
-// three products lo*hi + hi*lo + hi*hi keep fp32-level accuracy
-__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
-  const float r = x - __uint_as_float(hi);
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo) : "f"(r));
-}
-__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
-      "{%0, %1, %2, %3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-__device__ __forceinline__ float lds32(uint32_t a) {
-  float v;
-  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
-  return v;
 }
 
 // ND: diagonal modes between the sorted and the last mode (0 or 1).  Stream
@@ -1538,7 +1612,7 @@ struct MergePlan {
   int64_t lm_off[kMaxModes];     // ... at this byte offset
   int R = 0;                     // register geometry of the virtual chain
   int64_t table_bytes = 0;       // 256-aligned
-  bool mma1 = false;             // virtual mode 1's copy is the tensor-core layout (stream plans)
+  int8_t mma[kMaxModes];         // the copy is the tensor-core fragment layout (hi / lo, 2x size)
   int a() const { return kind[0] == kPrefix ? hi[0] - lo[0] : 1; }
   int b() const { return kind[ng - 1] == kSuffix ? hi[ng - 1] - lo[ng - 1] : 1; }
 };
@@ -1580,6 +1654,7 @@ void plan_merge(const ChainDev& ch, int64_t m, MergePlan* mp) {
     mp->kind[0] = kOrig;
     mp->rows[0] = ch.m[0].J;
     mp->lm[0] = 0;
+    mp->mma[0] = 0;
     return;
   }
   int g = 0;
@@ -1637,9 +1712,10 @@ void plan_merge(const ChainDev& ch, int64_t m, MergePlan* mp) {
     const ModeDev& md = ch.m[mp->lo[v]];
     mp->lm[v] = (int8_t)(lane_major_env() && mp->R && v > 0 && v < g - 1 && mp->kind[v] == kOrig &&
                          md.layout == TNB_LAYOUT_DENSE && md.rl == mp->R && md.rr == mp->R);
+    mp->mma[v] = (int8_t)(mp->lm[v] && mp->R == 32 && TNB_STATE_MMA);
     if (mp->lm[v]) {
       mp->lm_off[v] = off;
-      off += ((int64_t)md.J * md.rl * md.rr * 4 + 255) & ~(int64_t)255;
+      off += ((int64_t)md.J * md.rl * md.rr * 4 * (mp->mma[v] ? 2 : 1) + 255) & ~(int64_t)255;
     }
   }
   mp->table_bytes = off;
@@ -1700,7 +1776,7 @@ int build_tables(const ChainDev& ch, const MergePlan& mp, unsigned char* base, c
         in = out;
         rows *= ch.m[o].J;
       }
-    } else if (mp.lm[g] && g == 1 && mp.mma1) {
+    } else if (mp.lm[g] && mp.mma[g]) {
       const ModeDev& md = ch.m[lo];
       mma_slice_kernel<<<grid((int64_t)md.J * md.rl * md.rr * 2), 256, 0, st>>>(
           md.s, reinterpret_cast<float*>(base + mp.lm_off[g]), md.J, md.rl);
@@ -1743,7 +1819,10 @@ int table_launches(const MergePlan& mp) {
 
 void set_vmap(const ChainDev& ch, const MergePlan& mp, BPlan* bp) {
   bp->n0 = ch.n;
-  for (int g = 0; g < mp.ng; ++g) bp->lmaj[g] = mp.lm[g];
+  for (int g = 0; g < mp.ng; ++g) {
+    bp->lmaj[g] = mp.lm[g];
+    bp->mmal[g] = mp.mma[g];
+  }
   for (int g = 0; g < mp.ng; ++g)
     for (int o = mp.lo[g]; o < mp.hi[g]; ++o) {
       bp->oJ[o] = ch.m[o].J;
@@ -1794,7 +1873,7 @@ int make_bplan(const ChainDev& ch, int64_t m, BPlan* bp, int* R_out, int* nt_out
     }
   }
   constexpr int NT = kComputeThreads;
-  const int RP = R + TNB_RPAD;
+  const int RP = R == 32 ? Geo<32>::RP : R + TNB_RPAD;
   const int idx_bytes = small ? 1 : 2;
   const int jpad = ((jmax + 1) + 7) & ~7;
   const size_t budget = (size_t)233472 - 1024;
@@ -1881,7 +1960,7 @@ int plan_entries(const ChainDev& ch, int64_t m, EPlan* P) {
         P->stream = true;
         if (kStreamMma) {  // the sorted mode's copy doubles (hi / lo fragments); it is the last table
           const ModeDev& g1 = ch.m[P->mp.lo[1]];
-          P->mp.mma1 = true;
+          P->mp.mma[1] = 1;
           P->mp.table_bytes = P->mp.lm_off[1] + (((int64_t)g1.J * g1.rl * g1.rr * 2 * 4 + 255) & ~(int64_t)255);
         }
         break;
@@ -1945,7 +2024,7 @@ int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m
     if constexpr (R <= 24) return launch_stream<R, IdxT>(ch, bp, ws, m, out, st);
     return set_error(TNB_EINVAL, "stream kernel: rank > 24");
   }
-  const size_t csmem = compute_smem(bp.T, R + TNB_RPAD, ch.n, (int)sizeof(IdxT), bp.jpad, bp.nw);
+  const size_t csmem = compute_smem(bp.T, Geo<R>::RP, ch.n, (int)sizeof(IdxT), bp.jpad, bp.nw);
   auto ck = entries_compute_kernel<R, IdxT, NT, FOLD>;
   rc = check_cuda(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem),
                   "compute smem attr");
