@@ -47,8 +47,11 @@
 #ifndef TNB_LAST_U
 #define TNB_LAST_U 4
 #endif
+#ifndef TNB_STATE_PF_EARLY
+#define TNB_STATE_PF_EARLY 0
+#endif
 #ifndef TNB_STATE_PF
-#define TNB_STATE_PF 0
+#define TNB_STATE_PF 3
 #endif
 #ifndef TNB_STREAM_THREADS
 #define TNB_STREAM_THREADS 384
@@ -398,7 +401,7 @@ __global__ void __launch_bounds__(256) entries_sort_kernel(const __grid_constant
 
 __device__ __forceinline__ uint32_t s32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 __device__ __forceinline__ void mb_init(uint64_t* b, uint32_t c) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s32(b)), "r"(c));
@@ -496,22 +499,6 @@ __global__ void __launch_bounds__(NT, 1)
     const int64_t ntile = tile + gridDim.x;
     mb_wait(cbar, c_it & 1);
     ++c_it;
-#if TNB_STATE_PF
-    // wide (HBM-resident) prefix / suffix tables: L2 prefetch of this tile's
-    // last-mode rows (used after the sorted modes) and of the NEXT tile's
-    // first-mode rows (indices read from its record in global memory), so
-    // neither gather waits on HBM latency
-    if (bp.wideL) {
-      const ModeDev& ml = ch.m[N - 1];
-      for (int s = tid; s < tn; s += NT) prefetch_l2(ml.s + (int64_t)widxL[s] * ml.rl);
-    }
-    if (bp.wide0 && ntile < ntiles) {
-      const int64_t ns0 = ntile * T;
-      const int ntn = (int)((m - ns0) < T ? (m - ns0) : T);
-      const uint32_t* nw = reinterpret_cast<const uint32_t*>(ws + ntile * bp.tile_bytes + bp.off_wide);
-      for (int s = tid; s < ntn; s += NT) prefetch_l2(ch.m[0].s + (int64_t)__ldg(nw + s) * ch.m[0].rr);
-    }
-#endif
     int fold = -1;  // first CP mode of a diagonal run folded into the last mode
     for (int k = 0; k < N; ++k) {
       const ModeDev& md = ch.m[k];
@@ -673,6 +660,24 @@ __global__ void __launch_bounds__(NT, 1)
       } else {
         // ---- sorted mode: permutation + bucket starts from the prep kernel
         sorted = true;
+#if TNB_STATE_PF
+        // wide (HBM-resident) tables: L2 prefetch, while the last sorted mode
+        // runs, of this tile's last-mode rows (bit 1) and of the NEXT tile's
+        // first-mode rows (bit 2, indices from its record in global memory),
+        // so neither gather waits on HBM latency
+        if (k == (TNB_STATE_PF_EARLY ? (int)bp.smode[0] : N - 2)) {
+          if ((TNB_STATE_PF & 1) && bp.wideL) {
+            const ModeDev& ml = ch.m[N - 1];
+            for (int s = tid; s < tn; s += NT) prefetch_l2(ml.s + (int64_t)widxL[s] * ml.rl);
+          }
+          if ((TNB_STATE_PF & 2) && bp.wide0 && ntile < ntiles) {
+            const int64_t ns0 = ntile * T;
+            const int ntn = (int)((m - ns0) < T ? (m - ns0) : T);
+            const uint32_t* nw = reinterpret_cast<const uint32_t*>(ws + ntile * bp.tile_bytes + bp.off_wide);
+            for (int s = tid; s < ntn; s += NT) prefetch_l2(ch.m[0].s + (int64_t)__ldg(nw + s) * ch.m[0].rr);
+          }
+        }
+#endif
         const int b = (int)(item & 1);
         mb_wait(&pbar[b], (uint32_t)((item >> 1) & 1));
         const uint16_t* perm = permb + b * T;
