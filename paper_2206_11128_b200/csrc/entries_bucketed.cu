@@ -41,6 +41,14 @@
 // state kernel: L2 prefetch of wide first / last mode rows
 // state kernel: full-rank r = 32 sorted modes on mma.sync split-TF32 (state
 // rows padded to 36 floats for conflict-light A-fragment loads)
+// the per-tile counting sorts run inside the prep kernel (block-wide, on the
+// compact indices it already holds in shared memory) instead of a separate
+// one-warp-per-(tile, mode) sort kernel when every sorted mode has at least
+// this many buckets (block-wide shared atomics contend on few buckets:
+// measured faster at J = 128 (cfg5), slower at J = 32 (cfg2)); 0 = never
+#ifndef TNB_SORT_IN_PREP
+#define TNB_SORT_IN_PREP 64
+#endif
 #ifndef TNB_STATE_MMA
 #define TNB_STATE_MMA 1
 #endif
@@ -254,6 +262,7 @@ struct BPlan {
   // the state kernel; stream plans skip the first mode (always wide) and a
   // wide last mode)
   int crow0, ncrow;
+  int psort;  // the prep kernel sorts (TNB_SORT_IN_PREP)
   int8_t slot[kMaxModes];  // mode -> sorted slot or -1
   // mode merging: the kernels run a VIRTUAL chain whose first / last modes
   // may be prefix / suffix tables over several original modes; the prep
@@ -271,8 +280,8 @@ struct BPlan {
 // prep: one CTA per tile -- reads the tile's n0 int64 index columns
 // (coalesced), validates and combines them, and writes the compact [N][T]
 // index block of the tile record.
-template <typename IdxT>
-__global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant__ ChainDev ch,
+template <typename IdxT, bool PSORT>
+__global__ void __launch_bounds__(512, PSORT ? 2 : 3) entries_prep_kernel(const __grid_constant__ ChainDev ch,
                                                            const __grid_constant__ BPlan bp,
                                                            const int64_t* __restrict__ idx, int64_t m,
                                                            int32_t* __restrict__ err,
@@ -333,10 +342,55 @@ __global__ void __launch_bounds__(512) entries_prep_kernel(const __grid_constant
     }
   }
   __syncthreads();
+  const size_t cbytes = (size_t)bp.ncrow * T * sizeof(IdxT) + (size_t)bp.nw * T * 4;
   {  // compact block (+ wide rows) -> record (16-byte stores)
-    const int n16 = (int)(((size_t)bp.ncrow * T * sizeof(IdxT) + (size_t)bp.nw * T * 4) / 16);
+    const int n16 = (int)(cbytes / 16);
     for (int i = tid; i < n16; i += NT)
       reinterpret_cast<uint4*>(rec)[i] = reinterpret_cast<const uint4*>(idxs)[i];
+  }
+  // counting sort of each sorted slot: histogram (shared atomics), warp-0
+  // scan into the bucket starts, scatter into a staged permutation, 16-byte
+  // copy-out.  The order inside a bucket is not fixed, and need not be: a
+  // sample's arithmetic does not depend on its position.
+  const int JP = bp.jpad;
+  int* hist = reinterpret_cast<int*>(smem + ((cbytes + 15) & ~(size_t)15));  // [jpad]
+  uint16_t* pb = reinterpret_cast<uint16_t*>(hist + JP);                      // [T]
+  const int lane = tid & 31;
+  for (int sl = 0; sl < (PSORT ? bp.nsort : 0); ++sl) {
+    const int k = bp.smode[sl];
+    const int J = ch.m[k].J;
+    const IdxT* col = idxs + (size_t)(k - bp.crow0) * T;
+    for (int j = tid; j < JP; j += NT) hist[j] = 0;
+    __syncthreads();
+    for (int s = tid; s < tn; s += NT) atomicAdd(&hist[col[s]], 1);
+    __syncthreads();
+    if (tid < 32) {
+      uint16_t* gst = reinterpret_cast<uint16_t*>(rec + bp.off_starts) + (size_t)sl * JP;
+      const int per = (J + 31) >> 5;
+      const int j0 = lane * per, j1 = min(j0 + per, J);
+      int sum = 0;
+      for (int j = j0; j < j1; ++j) sum += hist[j];
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int run = incl - sum;
+      for (int j = j0; j < j1; ++j) {
+        const int c = hist[j];
+        hist[j] = run;
+        gst[j] = (uint16_t)run;
+        run += c;
+      }
+      for (int j = J + lane; j < JP; j += 32) gst[j] = (uint16_t)tn;
+    }
+    __syncthreads();
+    for (int s = tid; s < tn; s += NT) pb[atomicAdd(&hist[col[s]], 1)] = (uint16_t)s;
+    __syncthreads();
+    uint16_t* pm = reinterpret_cast<uint16_t*>(rec + bp.off_perm) + (size_t)sl * T;
+    for (int i = tid; i < T / 8; i += NT) reinterpret_cast<uint4*>(pm)[i] = reinterpret_cast<const uint4*>(pb)[i];
+    __syncthreads();
   }
 }
 
@@ -1843,8 +1897,9 @@ int pick_R(int rmax) {
   return 0;
 }
 
-size_t prep_smem_bytes(int N, int T, int idx_bytes, int nw) {
-  return (size_t)N * T * idx_bytes + (size_t)nw * T * 4 + 256;
+size_t prep_smem_bytes(int N, int T, int idx_bytes, int nw, int psort, int jpad) {
+  const size_t c = ((size_t)N * T * idx_bytes + (size_t)nw * T * 4 + 15) & ~(size_t)15;
+  return c + (psort ? (size_t)jpad * 4 + (size_t)T * 2 : 0) + 256;
 }
 
 size_t compute_smem(int T, int RP, int N, int idx_bytes, int jpad, int nw) {
@@ -1883,7 +1938,10 @@ int make_bplan(const ChainDev& ch, int64_t m, BPlan* bp, int* R_out, int* nt_out
   const int jpad = ((jmax + 1) + 7) & ~7;
   const size_t budget = (size_t)233472 - 1024;
   // the prep kernel holds every slot's permutation and per-warp counts at once
-  auto prep_smem = [&](int t) { return prep_smem_bytes(bp->ncrow, t, idx_bytes, bp->nw); };
+  int jmin = 1 << 30;
+  for (int i = 0; i < nsort; ++i) jmin = std::min(jmin, (int)ch.m[bp->smode[i]].J);
+  bp->psort = nsort > 0 && TNB_SORT_IN_PREP > 0 && jmin >= TNB_SORT_IN_PREP;
+  auto prep_smem = [&](int t) { return prep_smem_bytes(bp->ncrow, t, idx_bytes, bp->nw, bp->psort, jpad); };
   auto comp_smem = [&](int t) { return compute_smem(t, RP, ch.n, idx_bytes, jpad, bp->nw); };
   int T = 65504;
   if (t_force > 0) {
@@ -1998,18 +2056,18 @@ template <int R, typename IdxT, int NT, bool FOLD>
 int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m, float* out,
               int32_t* err, unsigned char* ws, bool stream, cudaStream_t st) {
   // prep: one CTA per tile; sort: one warp per (tile, sorted mode)
-  const size_t psmem = prep_smem_bytes(bp.ncrow, bp.T, (int)sizeof(IdxT), bp.nw);
-  int rc = check_cuda(cudaFuncSetAttribute(entries_prep_kernel<IdxT>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem),
+  const size_t psmem = prep_smem_bytes(bp.ncrow, bp.T, (int)sizeof(IdxT), bp.nw, bp.psort, bp.jpad);
+  auto pk = bp.psort ? entries_prep_kernel<IdxT, true> : entries_prep_kernel<IdxT, false>;
+  int rc = check_cuda(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem),
                       "prep smem attr");
   if (rc) return rc;
   {
     KTimer kt("entries_prep", st);
-    entries_prep_kernel<IdxT><<<(unsigned)bp.ntiles, 512, psmem, st>>>(ch, bp, idx, m, err, ws);
+    pk<<<(unsigned)bp.ntiles, 512, psmem, st>>>(ch, bp, idx, m, err, ws);
   }
   rc = check_launch("entries_prep");
   if (rc) return rc;
-  if (bp.nsort > 0) {
+  if (bp.nsort > 0 && !bp.psort) {
     const int64_t warps = bp.ntiles * bp.nsort;
     const size_t per_warp = (size_t)bp.jpad * 4 + (size_t)bp.T * 2;
     int wpb = 8;
