@@ -80,16 +80,25 @@ __device__ __forceinline__ void sts128x2(uint32_t a, uint64_t p0, uint64_t p1) {
 #ifndef TNB_DOT_4TERM
 #define TNB_DOT_4TERM 0
 #endif
-// TNB_DOT_TRUNC_SPLIT: hi = x itself (the tensor core reads only its tf32
-// bits, i.e. truncates), lo = x - trunc(x) exactly -- 2 instructions instead
-// of 3; the per-product error grows from 2^-23 to 2^-21 relative
+// TNB_DOT_TRUNC_SPLIT (2 instructions per split instead of 3):
+//   1: hi = x itself (the tensor core reads only its tf32 bits, i.e.
+//      truncates), lo = x - trunc(x): 4x the per-product error;
+//   2: hi = rna(x), lo = x - hi exact and passed unrounded (the tensor core
+//      truncates it): the dropped bits of lo are below 2^-21 |x| and the
+//      measured cfg4 error equals the fully rounded split's.
+//   0: hi = rna(x), lo = rna(x - hi).
 #ifndef TNB_DOT_TRUNC_SPLIT
-#define TNB_DOT_TRUNC_SPLIT 0  /* measured: cfg4 dot 1.32 ms but relFro 1.06e-5, over the 1e-5 bar */
+#define TNB_DOT_TRUNC_SPLIT 2  /* 1: cfg4 dot 1.32 ms but relFro 1.06e-5, over the 1e-5 bar;
+                                  2: 1.54 ms at relFro 2.5e-6 (= the fully rounded split's) */
 #endif
 __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
-#if TNB_DOT_TRUNC_SPLIT
+#if TNB_DOT_TRUNC_SPLIT == 1
   hi = __float_as_uint(x);
   lo = __float_as_uint(x - __uint_as_float(hi & 0xffffe000u));
+#elif TNB_DOT_TRUNC_SPLIT == 2
+  // hi rounded, lo = x - hi exact but left for the tensor core to truncate
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
+  lo = __float_as_uint(x - __uint_as_float(hi));
 #else
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
   const float r = x - __uint_as_float(hi);

@@ -49,6 +49,9 @@
 #ifndef TNB_SORT_IN_PREP
 #define TNB_SORT_IN_PREP 64
 #endif
+#ifndef TNB_FAST_SPLIT
+#define TNB_FAST_SPLIT 1
+#endif
 #ifndef TNB_STATE_MMA
 #define TNB_STATE_MMA 1
 #endif
@@ -150,6 +153,17 @@ __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) 
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
   const float r = x - __uint_as_float(hi);
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo) : "f"(r));
+}
+// the per-step A-fragment split: lo = x - rna(x) exact, passed unrounded (the
+// tensor core truncates it; the dropped bits are below 2^-21 |x|) -- one
+// instruction less than split_tf32
+__device__ __forceinline__ void split_tf32_fast(float x, uint32_t& hi, uint32_t& lo) {
+#if TNB_FAST_SPLIT
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
+  lo = __float_as_uint(x - __uint_as_float(hi));
+#else
+  split_tf32(x, hi, lo);
+#endif
 }
 __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -782,10 +796,10 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
               for (int kt = 0; kt < 4; ++kt) {
                 uint32_t ah[4], al[4];
-                split_tf32(lds32(r0 + kt * 32 + mt * 4), ah[0], al[0]);
-                split_tf32(lds32(r1 + kt * 32 + mt * 4), ah[1], al[1]);
-                split_tf32(lds32(r0 + kt * 32 + mt * 4 + 16), ah[2], al[2]);
-                split_tf32(lds32(r1 + kt * 32 + mt * 4 + 16), ah[3], al[3]);
+                split_tf32_fast(lds32(r0 + kt * 32 + mt * 4), ah[0], al[0]);
+                split_tf32_fast(lds32(r1 + kt * 32 + mt * 4), ah[1], al[1]);
+                split_tf32_fast(lds32(r0 + kt * 32 + mt * 4 + 16), ah[2], al[2]);
+                split_tf32_fast(lds32(r1 + kt * 32 + mt * 4 + 16), ah[3], al[3]);
 #pragma unroll
                 for (int nt = 0; nt < 4; ++nt) {
                   mma_tf32(acc[nt], al, bh[kt][nt][0], bh[kt][nt][1]);
@@ -1313,10 +1327,10 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
           for (int kt = 0; kt < KT; ++kt) {
             uint32_t ah[4], al[4];
-            split_tf32(lds32(vr[0] + kt * 32), ah[0], al[0]);
-            split_tf32(lds32(vr[1] + kt * 32), ah[1], al[1]);
-            split_tf32(lds32(vr[0] + kt * 32 + 16), ah[2], al[2]);
-            split_tf32(lds32(vr[1] + kt * 32 + 16), ah[3], al[3]);
+            split_tf32_fast(lds32(vr[0] + kt * 32), ah[0], al[0]);
+            split_tf32_fast(lds32(vr[1] + kt * 32), ah[1], al[1]);
+            split_tf32_fast(lds32(vr[0] + kt * 32 + 16), ah[2], al[2]);
+            split_tf32_fast(lds32(vr[1] + kt * 32 + 16), ah[3], al[3]);
 #pragma unroll
             for (int nt = 0; nt < KT; ++nt) {
               mma_tf32(acc[nt], al, bh[kt][nt][0], bh[kt][nt][1]);
