@@ -96,7 +96,11 @@ namespace tnb {
 namespace {
 
 constexpr int kMaxJ = 1024;          // bucket count limit for sorted modes
-constexpr int kComputeThreads = 512;  // one 16-warp compute CTA per SM
+#ifndef TNB_STATE_CTAS
+#define TNB_STATE_CTAS 1
+#endif
+constexpr int kStateCtas = TNB_STATE_CTAS;                // state-kernel CTAs per SM
+constexpr int kComputeThreads = 512 / TNB_STATE_CTAS;     // 16 warps per SM
 
 
 
@@ -497,7 +501,7 @@ __device__ __forceinline__ void bulk(void* dst, const void* src, uint32_t bytes,
 // run is folded into the last-mode dot product (separate instantiation so
 // chains without it keep the leaner register allocation)
 template <int R, typename IdxT, int NT, bool FOLD>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(NT, kStateCtas)
     entries_compute_kernel(const __grid_constant__ ChainDev ch, const __grid_constant__ BPlan bp,
                            const unsigned char* __restrict__ ws, int64_t m, float* __restrict__ out) {
   using Gm = Geo<R>;
@@ -1538,7 +1542,10 @@ __global__ void __launch_bounds__(256) table_suffix_step(ModeDev md, const float
 // K, Nn <= 32 and Nn % 4 == 0.  CTA tile: 256 rows of A (transposed into
 // shared memory once) x kTZ slices; thread = 8 rows x 4 columns, so a warp's
 // 8 column quads of one row are one 128-byte store.
-constexpr int kTRows = 256, kTZ = 4;
+#ifndef TNB_TABLE_TZ
+#define TNB_TABLE_TZ 4
+#endif
+constexpr int kTRows = 256, kTZ = TNB_TABLE_TZ;
 template <bool SUFFIX>
 __global__ void __launch_bounds__(256) table_gemm(ModeDev md, const float* __restrict__ A, int64_t rows,
                                                   float* __restrict__ out) {
@@ -1569,6 +1576,7 @@ __global__ void __launch_bounds__(256) table_gemm(ModeDev md, const float* __res
 #pragma unroll
       for (int c = 0; c < 4; ++c) acc[r][c] = 0.f;
     if (colok) {
+#pragma unroll 8
       for (int k = 0; k < K; ++k) {
         const float4 a0 = *reinterpret_cast<const float4*>(&As[k][ty * 8]);
         const float4 a1 = *reinterpret_cast<const float4*>(&As[k][ty * 8 + 4]);
@@ -1950,7 +1958,7 @@ int make_bplan(const ChainDev& ch, int64_t m, BPlan* bp, int* R_out, int* nt_out
   const int RP = R == 32 ? Geo<32>::RP : R + TNB_RPAD;
   const int idx_bytes = small ? 1 : 2;
   const int jpad = ((jmax + 1) + 7) & ~7;
-  const size_t budget = (size_t)233472 - 1024;
+  const size_t budget = ((size_t)233472 - 1024 * kStateCtas) / kStateCtas;
   // the prep kernel holds every slot's permutation and per-warp counts at once
   int jmin = 1 << 30;
   for (int i = 0; i < nsort; ++i) jmin = std::min(jmin, (int)ch.m[bp->smode[i]].J);
@@ -2106,7 +2114,7 @@ int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m
   rc = check_cuda(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem),
                   "compute smem attr");
   if (rc) return rc;
-  const int64_t slots = (int64_t)num_sms();
+  const int64_t slots = (int64_t)num_sms() * kStateCtas;
   const int grid = (int)(bp.ntiles < slots ? bp.ntiles : slots);
   {
     KTimer kt("entries_compute", st);
