@@ -336,6 +336,20 @@ def bench_entries(args, cfg, dev, dist, ws, rank):
                          "achieved_gbs": (8 * len(shape) + 4) * m / (ms_step * 1e-3) / 1e9}}
     fields = {"value": value, "ms_per_step": ms_step, "roofline": roof, "clocks": clk.summary(),
               "gpu_launches": launches}
+    if dist:
+        # the same steps followed by the NCCL all-gather of every
+        # rank's output block to every rank (the only collective entries has)
+        gath = torch.empty(ws * m, dtype=torch.float32, device=dev)
+
+        def step_gather():
+            step()
+            torch.distributed.all_gather_into_tensor(gath, out)
+
+        ms_g = timed_steps(step_gather, args.steps, 1, stream, dist) / args.steps
+        fields["with_gather"] = {"ms_per_step": ms_g, "value": ws * m / (ms_g * 1e-3), "unit": "entries/s",
+                                 "gathered_bytes_per_rank": ws * m * 4,
+                                 "collective": "NCCL all_gather_into_tensor of the fp32 outputs"}
+        del gath
     # e2e through the public API from pinned host memory: H2D of the step's
     # indices + K1 + D2H of the step's output, every step
     e2e_steps = max(2, min(args.steps, 3))
