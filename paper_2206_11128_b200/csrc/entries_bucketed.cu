@@ -55,6 +55,14 @@
 #ifndef TNB_STATE_MMA
 #define TNB_STATE_MMA 1
 #endif
+// state kernel: the closing dot fused into the last sorted (MMA) mode
+#ifndef TNB_FUSE_LAST
+#define TNB_FUSE_LAST 1
+#endif
+// ... with the last-mode rows loaded before the step's MMAs (1) or after (0)
+#ifndef TNB_FUSE_EARLY
+#define TNB_FUSE_EARLY 0
+#endif
 #ifndef TNB_LAST_U
 #define TNB_LAST_U 4
 #endif
@@ -763,8 +771,17 @@ __global__ void __launch_bounds__(NT, kStateCtas)
           // tensor cores: 16 samples of one bucket per step, rows g and g + 8
           // (sorted positions p + g, p + g + 8) of the m16n8k8 tiles; the
           // state rows are read as A fragments and overwritten in place by
-          // the C fragments (v <- v G) after the whole step has read them
+          // the C fragments (v <- v G) after the whole step has read them.
+          // fclose: this is the last sorted mode and the chain ends in a
+          // dense R x 1 mode -- the closing dot runs on the C fragments (the
+          // last-mode rows of the step's samples are loaded before its MMAs)
+          // and the state is never written back: no separate last-mode pass.
           const int mg = lane >> 2, mt = lane & 3;
+          const ModeDev& mlast = ch.m[N - 1];
+          const bool fclose = TNB_FUSE_LAST && k == N - 2 && mlast.layout == TNB_LAYOUT_DENSE && mlast.rl == R &&
+                              mlast.rr == 1;
+          const IdxT* colL = cidx + (size_t)(N - 1) * T;
+          if (fclose) k2 = N - 1;
           while (p < hi) {
             const int key = col[perm[p]];
             const int bend = min((int)st[key + 1], hi);
@@ -792,8 +809,19 @@ __global__ void __launch_bounds__(NT, kStateCtas)
             }
             while (p < bend) {
               const int n = min(16, bend - p);
-              const uint32_t r0 = s_state + (uint32_t)perm[p + min(mg, n - 1)] * (RP * 4);
-              const uint32_t r1 = s_state + (uint32_t)perm[p + min(mg + 8, n - 1)] * (RP * 4);
+              const int sa = perm[p + min(mg, n - 1)], sb = perm[p + min(mg + 8, n - 1)];
+              const uint32_t r0 = s_state + (uint32_t)sa * (RP * 4);
+              const uint32_t r1 = s_state + (uint32_t)sb * (RP * 4);
+              float2 da[4], db[4];
+              if (fclose && TNB_FUSE_EARLY) {
+                const float* la = mlast.s + (int64_t)(bp.wideL ? widxL[sa] : (uint32_t)colL[sa]) * R + 2 * mt;
+                const float* lb = mlast.s + (int64_t)(bp.wideL ? widxL[sb] : (uint32_t)colL[sb]) * R + 2 * mt;
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) {
+                  da[nt] = __ldg(reinterpret_cast<const float2*>(la + 8 * nt));
+                  db[nt] = __ldg(reinterpret_cast<const float2*>(lb + 8 * nt));
+                }
+              }
               float acc[4][4];
 #pragma unroll
               for (int nt = 0; nt < 4; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
@@ -811,16 +839,42 @@ __global__ void __launch_bounds__(NT, kStateCtas)
                   mma_tf32(acc[nt], ah, bh[kt][nt][0], bh[kt][nt][1]);
                 }
               }
-              __syncwarp();  // every row of the step has been read
-              if (mg < n) {
+              if (fclose) {
+                if (!TNB_FUSE_EARLY) {
+                  const float* la = mlast.s + (int64_t)(bp.wideL ? widxL[sa] : (uint32_t)colL[sa]) * R + 2 * mt;
+                  const float* lb = mlast.s + (int64_t)(bp.wideL ? widxL[sb] : (uint32_t)colL[sb]) * R + 2 * mt;
 #pragma unroll
-                for (int nt = 0; nt < 4; ++nt) sts_b64(r0 + nt * 32 + mt * 8, pack2(acc[nt][0], acc[nt][1]));
-              }
-              if (mg + 8 < n) {
+                  for (int nt = 0; nt < 4; ++nt) {
+                    da[nt] = __ldg(reinterpret_cast<const float2*>(la + 8 * nt));
+                    db[nt] = __ldg(reinterpret_cast<const float2*>(lb + 8 * nt));
+                  }
+                }
+                float part0 = 0.f, part1 = 0.f;
 #pragma unroll
-                for (int nt = 0; nt < 4; ++nt) sts_b64(r1 + nt * 32 + mt * 8, pack2(acc[nt][2], acc[nt][3]));
+                for (int nt = 0; nt < 4; ++nt) {
+                  part0 = fmaf(acc[nt][0], da[nt].x, part0);
+                  part0 = fmaf(acc[nt][1], da[nt].y, part0);
+                  part1 = fmaf(acc[nt][2], db[nt].x, part1);
+                  part1 = fmaf(acc[nt][3], db[nt].y, part1);
+                }
+                // reduce-scatter over the 4 lanes of a row: odd lanes finish row g + 8
+                const bool odd = mt & 1;
+                float keep = odd ? part1 : part0;
+                keep += __shfl_xor_sync(0xffffffffu, odd ? part0 : part1, 1);
+                keep += __shfl_xor_sync(0xffffffffu, keep, 2);
+                if (mt < 2 && mg + 8 * mt < n) out[s0 + (mt ? sb : sa)] = keep;
+              } else {
+                __syncwarp();  // every row of the step has been read
+                if (mg < n) {
+#pragma unroll
+                  for (int nt = 0; nt < 4; ++nt) sts_b64(r0 + nt * 32 + mt * 8, pack2(acc[nt][0], acc[nt][1]));
+                }
+                if (mg + 8 < n) {
+#pragma unroll
+                  for (int nt = 0; nt < 4; ++nt) sts_b64(r1 + nt * 32 + mt * 8, pack2(acc[nt][2], acc[nt][3]));
+                }
+                __syncwarp();
               }
-              __syncwarp();
               p += n;
             }
           }
@@ -984,7 +1038,7 @@ __global__ void __launch_bounds__(NT, kStateCtas)
               bulk(cidx + (size_t)kk * T, ws + ntile * bp.tile_bytes + (size_t)kk * row_bytes, row_bytes, cbar);
           const unsigned char* nrec = ws + ntile * bp.tile_bytes + bp.off_wide;
           if (k == 0 && bp.wide0) bulk(widx, nrec, wrow_bytes, cbar);
-          if (k == N - 1 && bp.wideL) bulk(widx + (size_t)bp.wide0 * T, nrec + (size_t)bp.wide0 * wrow_bytes, wrow_bytes, cbar);
+          if (k2 == N - 1 && bp.wideL) bulk(widx + (size_t)bp.wide0 * T, nrec + (size_t)bp.wide0 * wrow_bytes, wrow_bytes, cbar);
         }
         if (sorted) issue_slot(item + 2);  // this slot buffer is free again
       }
