@@ -59,6 +59,11 @@
 #ifndef TNB_FUSE_LAST
 #define TNB_FUSE_LAST 1
 #endif
+// state kernel: the first mode's table rows read by the first sorted (MMA)
+// mode directly (no gather pass)
+#ifndef TNB_FUSE_FIRST
+#define TNB_FUSE_FIRST 1
+#endif
 // ... with the last-mode rows loaded before the step's MMAs (1) or after (0)
 #ifndef TNB_FUSE_EARLY
 #define TNB_FUSE_EARLY 0
@@ -539,6 +544,11 @@ __global__ void __launch_bounds__(NT, kStateCtas)
   const uint32_t* widxL = widx + (size_t)bp.wide0 * T;    // last mode (wide)
   const uint32_t slot_bytes = (uint32_t)T * 2 + (uint32_t)bp.jpad * 2;
   const int ns = bp.nsort;
+  // ffirst: the first mode is a row table feeding a tensor-core sorted mode 1,
+  // whose A fragments are then loaded straight from the table rows (no
+  // first-mode gather into the state, no barrier after it)
+  const bool ffirst = TNB_FUSE_FIRST && R == 32 && N >= 3 && bp.mmal[1] && ch.m[0].layout == TNB_LAYOUT_DENSE &&
+                      ch.m[0].rl == 1 && ch.m[0].rr == R;
 
   // producer (tid 0): slot items in consumption order (tile-major, slot-minor)
   auto issue_slot = [&](int64_t item) {
@@ -581,6 +591,7 @@ __global__ void __launch_bounds__(NT, kStateCtas)
     ++c_it;
     int fold = -1;  // first CP mode of a diagonal run folded into the last mode
     for (int k = 0; k < N; ++k) {
+      if (k == 0 && ffirst) continue;  // the first sorted mode reads the first-mode rows itself
       const ModeDev& md = ch.m[k];
       const IdxT* col = cidx + (size_t)k * T;
       const int rl = md.rl, rr = md.rr;
@@ -825,13 +836,31 @@ __global__ void __launch_bounds__(NT, kStateCtas)
               float acc[4][4];
 #pragma unroll
               for (int nt = 0; nt < 4; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
+              float av[4][4];  // A values: rows g, g + 8 x columns 8kt + t, 8kt + t + 4
+              if (ffirst && k == 1) {
+                const float* pa = ch.m[0].s + (int64_t)(bp.wide0 ? widx0[sa] : (uint32_t)cidx[sa]) * R + mt;
+                const float* pb = ch.m[0].s + (int64_t)(bp.wide0 ? widx0[sb] : (uint32_t)cidx[sb]) * R + mt;
+#pragma unroll
+                for (int kt = 0; kt < 4; ++kt) {
+                  av[kt][0] = __ldg(pa + 8 * kt);
+                  av[kt][1] = __ldg(pb + 8 * kt);
+                  av[kt][2] = __ldg(pa + 8 * kt + 4);
+                  av[kt][3] = __ldg(pb + 8 * kt + 4);
+                }
+              } else {
+#pragma unroll
+                for (int kt = 0; kt < 4; ++kt) {
+                  av[kt][0] = lds32(r0 + kt * 32 + mt * 4);
+                  av[kt][1] = lds32(r1 + kt * 32 + mt * 4);
+                  av[kt][2] = lds32(r0 + kt * 32 + mt * 4 + 16);
+                  av[kt][3] = lds32(r1 + kt * 32 + mt * 4 + 16);
+                }
+              }
 #pragma unroll
               for (int kt = 0; kt < 4; ++kt) {
                 uint32_t ah[4], al[4];
-                split_tf32_fast(lds32(r0 + kt * 32 + mt * 4), ah[0], al[0]);
-                split_tf32_fast(lds32(r1 + kt * 32 + mt * 4), ah[1], al[1]);
-                split_tf32_fast(lds32(r0 + kt * 32 + mt * 4 + 16), ah[2], al[2]);
-                split_tf32_fast(lds32(r1 + kt * 32 + mt * 4 + 16), ah[3], al[3]);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) split_tf32_fast(av[kt][i], ah[i], al[i]);
 #pragma unroll
                 for (int nt = 0; nt < 4; ++nt) {
                   mma_tf32(acc[nt], al, bh[kt][nt][0], bh[kt][nt][1]);
@@ -1030,14 +1059,15 @@ __global__ void __launch_bounds__(NT, kStateCtas)
       if (tid == 0) {
         // cidx rows k..k2 of this tile are dead: prefetch the next tile's rows
         if (ntile < ntiles) {
-          if (k == 0) mb_expect(cbar, row_bytes * N + wrow_bytes * bp.nw);
+          const int kpost0 = ffirst ? 1 : 0;  // the first post-mode section of the tile
+          if (k == kpost0) mb_expect(cbar, row_bytes * N + wrow_bytes * bp.nw);
           // rows of a folded diagonal run stay live until the last mode
-          const int klo = (FOLD && k == N - 1 && fold >= 0) ? fold : k;
+          const int klo = (FOLD && k == N - 1 && fold >= 0) ? fold : (k == kpost0 ? 0 : k);
           if (!(FOLD && fold >= 0 && k >= fold && k < N - 1))
             for (int kk = klo; kk <= k2; ++kk)
               bulk(cidx + (size_t)kk * T, ws + ntile * bp.tile_bytes + (size_t)kk * row_bytes, row_bytes, cbar);
           const unsigned char* nrec = ws + ntile * bp.tile_bytes + bp.off_wide;
-          if (k == 0 && bp.wide0) bulk(widx, nrec, wrow_bytes, cbar);
+          if (k == kpost0 && bp.wide0) bulk(widx, nrec, wrow_bytes, cbar);
           if (k2 == N - 1 && bp.wideL) bulk(widx + (size_t)bp.wide0 * T, nrec + (size_t)bp.wide0 * wrow_bytes, wrow_bytes, cbar);
         }
         if (sorted) issue_slot(item + 2);  // this slot buffer is free again
