@@ -1626,6 +1626,10 @@ __global__ void __launch_bounds__(256) table_suffix_step(ModeDev md, const float
 // K, Nn <= 32 and Nn % 4 == 0.  CTA tile: 256 rows of A (transposed into
 // shared memory once) x kTZ slices; thread = 8 rows x 4 columns, so a warp's
 // 8 column quads of one row are one 128-byte store.
+// dense table levels on tensor cores (split TF32) when K == Nn in {8..32}
+#ifndef TNB_TABLE_TC
+#define TNB_TABLE_TC 1
+#endif
 #ifndef TNB_TABLE_TZ
 #define TNB_TABLE_TZ 4
 #endif
@@ -1684,6 +1688,91 @@ __global__ void __launch_bounds__(256) table_gemm(ModeDev md, const float* __res
       }
     }
   }
+}
+
+// The same table steps on tensor cores (mma.sync m16n8k8, split TF32: hi =
+// rna(x), lo = x - hi) for K, Nn in {8, 16, 24, 32}: CTA = 128 rows of A
+// (staged in shared memory, row stride K + 4: conflict-free fragment loads)
+// x 8 slices, warp w owns slice z0 + w (its B fragments stay in registers)
+// and walks the 8 row tiles of 16.  Large levels (cfg2: 2^20-row tables)
+// are write-bound instead of FFMA-bound.
+constexpr int kTcRows = 128, kTcZ = 8;
+template <int KT, int NTL, bool SUFFIX>
+__global__ void __launch_bounds__(256) table_gemm_tc(ModeDev md, const float* __restrict__ A, int64_t rows,
+                                                     float* __restrict__ out) {
+  constexpr int K = 8 * KT, Nn = 8 * NTL, AS = K + 4;
+  __shared__ __align__(16) float As[kTcRows * AS];
+  const int J = md.J;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t i0 = (int64_t)blockIdx.x * kTcRows;
+  const int nr = (int)(rows - i0 < kTcRows ? rows - i0 : kTcRows);
+  for (int e = tid; e < kTcRows * K; e += 256) {
+    const int r = e / K, k = e - r * K;
+    As[r * AS + k] = r < nr ? __ldg(A + i0 * K + e) : 0.f;
+  }
+  __syncthreads();
+  const int j = blockIdx.y * kTcZ + warp;
+  if (j >= J) return;
+  // B(k, n) = G(j, k, n) (prefix) or G(j, n, k) (suffix); fragment (kt, nt):
+  // b0 = B(8kt + t, 8nt + g), b1 = B(8kt + t + 4, 8nt + g)
+  const float* gj = md.s + (int64_t)j * md.rl * md.rr;
+  uint32_t bh[KT][NTL][2], bl[KT][NTL][2];
+#pragma unroll
+  for (int kt = 0; kt < KT; ++kt)
+#pragma unroll
+    for (int nt = 0; nt < NTL; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int k = 8 * kt + t + 4 * e, n = 8 * nt + g;
+        split_tf32(__ldg(gj + (SUFFIX ? n * K + k : k * Nn + n)), bh[kt][nt][e], bl[kt][nt][e]);
+      }
+  for (int mt = 0; mt < kTcRows / 16; ++mt) {
+    if (mt * 16 >= nr) break;
+    float acc[NTL][4];
+#pragma unroll
+    for (int nt = 0; nt < NTL; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
+    const float* a0 = As + (mt * 16 + g) * AS + t;
+    const float* a1 = a0 + 8 * AS;
+#pragma unroll
+    for (int kt = 0; kt < KT; ++kt) {
+      uint32_t ah[4], al[4];
+      split_tf32_fast(a0[8 * kt], ah[0], al[0]);
+      split_tf32_fast(a1[8 * kt], ah[1], al[1]);
+      split_tf32_fast(a0[8 * kt + 4], ah[2], al[2]);
+      split_tf32_fast(a1[8 * kt + 4], ah[3], al[3]);
+#pragma unroll
+      for (int nt = 0; nt < NTL; ++nt) {
+        mma_tf32(acc[nt], al, bh[kt][nt][0], bh[kt][nt][1]);
+        mma_tf32(acc[nt], ah, bl[kt][nt][0], bl[kt][nt][1]);
+        mma_tf32(acc[nt], ah, bh[kt][nt][0], bh[kt][nt][1]);
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = mt * 16 + g + 8 * h;
+      if (r >= nr) continue;
+      const int64_t i = i0 + r;
+      float* dst = SUFFIX ? out + ((int64_t)j * rows + i) * Nn : out + (i * J + j) * Nn;
+#pragma unroll
+      for (int nt = 0; nt < NTL; ++nt)
+        *reinterpret_cast<float2*>(dst + 8 * nt + 2 * t) = make_float2(acc[nt][2 * h], acc[nt][2 * h + 1]);
+    }
+  }
+}
+
+template <bool SUFFIX>
+bool launch_table_tc(const ModeDev& md, const float* in, int64_t rows, float* out, cudaStream_t st) {
+  const int K = SUFFIX ? md.rr : md.rl, Nn = SUFFIX ? md.rl : md.rr;
+  if (!TNB_TABLE_TC || md.layout != TNB_LAYOUT_DENSE || K != Nn || (K & 7) || K < 8 || K > 32) return false;
+  const dim3 grid((unsigned)ceil_div(rows, kTcRows), (unsigned)ceil_div(md.J, kTcZ));
+  switch (K) {
+    case 8: table_gemm_tc<1, 1, SUFFIX><<<grid, 256, 0, st>>>(md, in, rows, out); break;
+    case 16: table_gemm_tc<2, 2, SUFFIX><<<grid, 256, 0, st>>>(md, in, rows, out); break;
+    case 24: table_gemm_tc<3, 3, SUFFIX><<<grid, 256, 0, st>>>(md, in, rows, out); break;
+    default: table_gemm_tc<4, 4, SUFFIX><<<grid, 256, 0, st>>>(md, in, rows, out); break;
+  }
+  return true;
 }
 
 bool table_gemm_ok(const ModeDev& md, bool suffix) {
@@ -1931,7 +2020,8 @@ int build_tables(const ChainDev& ch, const MergePlan& mp, unsigned char* base, c
       for (int o = lo + 1; o < hi; ++o) {
         float* out = reinterpret_cast<float*>(base + mp.lvl[o]);
         const int64_t total = rows * ch.m[o].J * ch.m[o].rr;
-        if (total > 0 && table_gemm_ok(ch.m[o], false))
+        if (total > 0 && launch_table_tc<false>(ch.m[o], in, rows, out, st)) {
+        } else if (total > 0 && table_gemm_ok(ch.m[o], false))
           table_gemm<false><<<dim3((unsigned)ceil_div(rows, kTRows), (unsigned)ceil_div(ch.m[o].J, kTZ)), 256, 0,
                               st>>>(ch.m[o], in, rows, out);
         else if (total > 0)
@@ -1957,7 +2047,8 @@ int build_tables(const ChainDev& ch, const MergePlan& mp, unsigned char* base, c
       for (int o = hi - 2; o >= lo; --o) {
         float* out = reinterpret_cast<float*>(base + mp.lvl[o]);
         const ModeDev& md = ch.m[o];
-        if ((int64_t)md.J * n * md.rl > 0 && table_gemm_ok(md, true)) {
+        if ((int64_t)md.J * n * md.rl > 0 && launch_table_tc<true>(md, in, n, out, st)) {
+        } else if ((int64_t)md.J * n * md.rl > 0 && table_gemm_ok(md, true)) {
           table_gemm<true><<<dim3((unsigned)ceil_div(n, kTRows), (unsigned)ceil_div(md.J, kTZ)), 256, 0, st>>>(
               md, in, n, out);
         } else if ((int64_t)md.J * n * md.rl > 0) {
