@@ -4,15 +4,16 @@
 // Reference: chain_dot (core.py:362-384) propagates an r_a x r_b transfer
 // matrix M mode by mode, M' = sum_j A_j^T M B_j, as numpy's einsum path
 // "xaic,xab->bcix" then "bcix,xbid->xcd".  Here:
-//   * one CTA per pair at a time (persistent, 2 CTAs per SM, 8 warps);
+//   * one CTA per pair at a time (persistent, 4 CTAs per SM, 4 warps: measured
+//     against 8 and 2 warps per pair, 1.45 vs 1.55 / 1.63 ms at cfg4);
 //   * core slices stream HBM -> shared memory with cp.async.bulk (TMA bulk
-//     copies) in chunks of 16 slices (16 KB per operand), double buffered
+//     copies) in chunks of 8 slices (8 KB per operand), double buffered
 //     behind an mbarrier full/empty pipeline -- each byte is read once;
-//   * warp w takes slices j = w, w+8 of every chunk:
+//   * warp w takes slices j = w, w+4 of every chunk:
 //       Y_j = M B_j   (lane = 2 rows x 4 columns; M rows in registers)
 //       Mw += A_j^T Y_j  (Y_j bounced through a 1 KB per-warp smem tile)
 //     with packed FFMA2 (fma.rn.f32x2) throughout;
-//   * at the end of each core the 8 per-warp partial M's are summed through
+//   * at the end of each core the per-warp partial M's are summed through
 //     shared memory and the new M is broadcast back into registers.
 // The boundary cores (rank 1 outward) use the same pipeline with rank-1
 // special cases.  norm() streams only one operand (A == B).
@@ -21,11 +22,23 @@
 namespace tnb {
 namespace {
 
-constexpr int kWarps = 8;
+// warps per pair (CTA) and slices per pipeline chunk; 16 warps per SM
+#ifndef TNB_DOT_WARPS
+#define TNB_DOT_WARPS 4
+#endif
+#ifndef TNB_DOT_CH
+#define TNB_DOT_CH 8
+#endif
+constexpr int kWarps = TNB_DOT_WARPS;
 constexpr int kThreads = kWarps * 32;
+constexpr int kCtasPerSm = 16 / kWarps;
 constexpr int R = 16;
-constexpr int CH = 16;                 // slices per chunk
-constexpr int kStages = 2;
+constexpr int CH = TNB_DOT_CH;         // slices per chunk
+static_assert(CH == 2 * kWarps, "the FFMA path takes two slices per warp and chunk");
+#ifndef TNB_DOT_STAGES
+#define TNB_DOT_STAGES 2
+#endif
+constexpr int kStages = TNB_DOT_STAGES;
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t c) {
@@ -186,7 +199,7 @@ struct Walk {
 };
 
 template <bool MMA>
-__global__ void __launch_bounds__(kThreads, 2) dot_r16_kernel(const __grid_constant__ DotArgs args) {
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) dot_r16_kernel(const __grid_constant__ DotArgs args) {
   extern __shared__ __align__(128) unsigned char smem[];
   float* stA = reinterpret_cast<float*>(smem);                      // [kStages][CH*R*R]
   float* stB = stA + kStages * CH * R * R;                          // [kStages][CH*R*R]
@@ -383,11 +396,11 @@ __global__ void __launch_bounds__(kThreads, 2) dot_r16_kernel(const __grid_const
           *reinterpret_cast<float4*>(rw + (2 * ap + i) * R + dq * 4) = make_float4(x0, x1, x2, x3);
         }
         __syncthreads();
-        {
+        for (int e = tid; e < R * R; e += kThreads) {
           float v = 0.f;
 #pragma unroll
-          for (int w = 0; w < kWarps; ++w) v += red[w * R * R + tid];
-          msm[tid] = v;
+          for (int w = 0; w < kWarps; ++w) v += red[w * R * R + e];
+          msm[e] = v;
         }
         __syncthreads();
         if (MMA) {
@@ -451,7 +464,7 @@ int launch_dot_fast(const ChainDev& a, const ChainDev& b, float* out, bool is_no
   int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                       "dot smem attr");
   if (rc) return rc;
-  const int64_t slots = (int64_t)num_sms() * 2;
+  const int64_t slots = (int64_t)num_sms() * kCtasPerSm;
   const int grid = (int)(a.batch < slots ? a.batch : slots);
   kern<<<grid, kThreads, smem, st>>>(args);
   return check_launch("dot_r16");
