@@ -36,6 +36,13 @@ constexpr int NB = 2;          // resident n-blocks per column block
 constexpr int KMAX = 64;       // max contraction length
 constexpr int kTileBytes = 2 * 2 * BMT * 128;  // {hi,lo} x 2 K-blocks x 128 rows x 128 B = 64 KB
 constexpr int kStages = 3;
+// epilogue: 1 = each warp transposes a 32 x 32 block through shared memory
+// and writes 16-byte vectors (4 rows x 128 B per store instruction);
+// 0 = one 128-byte row segment per st.global (thread = output column)
+#ifndef TNB_FULL_V4
+#define TNB_FULL_V4 0  /* measured: 3.80 vs 3.73 ms at cfg3 */
+#endif
+constexpr int kEpiBytes = TNB_FULL_V4 ? 4 * 32 * 32 * 4 : 0;
 constexpr uint32_t kTmemCols = 512;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -74,8 +81,17 @@ __device__ __forceinline__ void bulk_g2s_keep(void* dst, const void* src, uint32
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+#ifndef TNB_FULL_ST
+#define TNB_FULL_ST 0  // 0: st.global.cs, 1: plain st.global, 2: st.global.L1::no_allocate
+#endif
 __device__ __forceinline__ void st_stream(float* p, uint32_t v) {
+#if TNB_FULL_ST == 1
+  asm volatile("st.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+#elif TNB_FULL_ST == 2
+  asm volatile("st.global.L1::no_allocate.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+#else
   asm volatile("st.global.cs.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+#endif
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -189,7 +205,8 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   unsigned char* sL = smem;  // [kStages][kTileBytes]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kTileBytes);
+  float* sEpi = reinterpret_cast<float*>(smem + kStages * kTileBytes);  // [4 warps][32][32]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kTileBytes + kEpiBytes);
   uint64_t* full = bars + 0;        // [kStages] tx
   uint64_t* empty = bars + 3;       // [kStages] tcgen05.commit
   uint64_t* acc_full = bars + 6;    // [2] tcgen05.commit
@@ -310,6 +327,7 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
         const int64_t rows_left = M - mt * BMT;
         const bool full_rows = rows_left >= BMT;
         const int64_t ldc = args.ldc;
+        const bool v4ok = (ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(args.C) & 15) == 0;
         float* p = args.C + (mt * BMT) * ldc + col;  // row mt*128, advanced by ldc per row
         uint32_t va[32], vb[32];
         TMEM_LD32(tm_acc0 + cbuf * BMT + lane_base, va);
@@ -319,7 +337,22 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
           uint32_t* cur = (ch & 1) ? vb : va;
           uint32_t* nxt = (ch & 1) ? va : vb;
           if (ch + 1 < BMT / 32) TMEM_LD32(tm_acc0 + cbuf * BMT + lane_base + (ch + 1) * 32, nxt);
-          if (cok && full_rows) {
+          if (TNB_FULL_V4 && v4ok && full_rows && cb * NB * BNB + nb * BNB + q * 32 + 32 <= N) {
+            // transpose the 32 rows x 32 columns through shared memory, then
+            // 16-byte stores: lanes 8r..8r+7 write row r's 128 bytes
+            float* tw = sEpi + q * 32 * 32;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) tw[j * 32 + lane] = __uint_as_float(cur[j]);
+            __syncwarp();
+            float* rowp = args.C + (mt * BMT + ch * 32 + (lane >> 3)) * ldc + (col - lane) + 4 * (lane & 7);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float4 v = *reinterpret_cast<const float4*>(tw + (4 * i + (lane >> 3)) * 32 + 4 * (lane & 7));
+              __stcs(reinterpret_cast<float4*>(rowp + (int64_t)(4 * i) * ldc), v);
+            }
+            __syncwarp();
+            p += 32 * ldc;
+          } else if (cok && full_rows) {
             // one st.global per row: the warp's 32 lanes write 128 contiguous bytes
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
@@ -380,7 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
   }
 }
 
-constexpr size_t kSmemBytes = 1024 + (size_t)kStages * kTileBytes + 128;
+constexpr size_t kSmemBytes = 1024 + (size_t)kStages * kTileBytes + kEpiBytes + 128;
 
 bool tc_disabled() {
   static int v = -1;
