@@ -462,3 +462,31 @@ def test_bucketed_stream_no_diag():
     idx = O.uniform_indices(t.shape, m, 5)
     sel = np.arange(0, m, 11)
     assert_close(to_np(tb.entries(t, idx))[sel], O.entries(o, idx[sel]), what="stream no diag")
+
+
+@pytest.mark.parametrize("lane_major", ["1", "0"])
+def test_bucketed_r32_tensor_core_paths(lane_major, monkeypatch):
+    # an r = 32 sorted mode on tensor cores that reads the rows of a
+    # (non-wide) prefix table itself and is followed by a CP mode, so the
+    # closing dot is NOT fused (the CP row folds into the last mode);
+    # lane_major=0 runs the FFMA2 K-split path on the same chain
+    monkeypatch.setenv("TNB_LANE_MAJOR", lane_major)
+    rng = np.random.default_rng(32)
+    s = 32 ** -0.5
+    nodes = [("tt", rng.standard_normal((1, 40, 32)).astype(np.float32), None),
+             ("tt", (rng.standard_normal((32, 40, 32)) * s).astype(np.float32), None),
+             ("tt", (rng.standard_normal((32, 40, 32)) * s).astype(np.float32), None),
+             ("cp", rng.standard_normal((40, 32)).astype(np.float32), None),
+             ("tt", (rng.standard_normal((32, 40, 1)) * s).astype(np.float32), None)]
+    t = facade(nodes)
+    o = O.make_chain(nodes)
+    m = 20001
+    plan = N.entries_plan(t._packed().chain, m, N.ALGO_BUCKETED)
+    assert (plan["n_virtual"], plan["prefix_rows"], plan["compute_kernel"]) == (4, 1600, 0), plan
+    idx = O.uniform_indices(t.shape, m, 7)
+    idx[::9] -= np.asarray(t.shape)
+    assert_close(tb.entries(t, idx, algo=N.ALGO_BUCKETED), O.entries(o, idx), what=f"r32 lane_major={lane_major}")
+    bad = idx.copy()
+    bad[m // 2, 2] = 40
+    with pytest.raises(tb.ContractViolationError, match="mode 2"):
+        tb.entries(t, bad, algo=N.ALGO_BUCKETED)
