@@ -137,6 +137,11 @@ def ncu_traffic(tag, kernel):
     return None, None
 
 
+def _tc_tf32_peak():
+    pk = load_json("peaks_r01.json") or {}
+    return pk.get("hmma_tf32_mma_sync_tflops") or 277.6
+
+
 def fp32_peak():
     """Measured FFMA peak (tools/peaks.cu, committed in profiles/), else the
     nominal 148 SMs x 128 FMA/clk x 2 x 1.965 GHz."""
@@ -152,6 +157,9 @@ def hbm_peak():
         with open(p) as f:
             return json.load(f)["hbm_gbs"], "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
     return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+TC_TF32_PEAK = None  # set in main() (profiles/peaks_r01.json)
 
 
 def dist_env():
@@ -326,6 +334,12 @@ def bench_entries(args, cfg, dev, dist, ws, rank):
                                   f"{plan['suffix_modes']} modes into prefix / suffix tables (built every call, "
                                   f"{plan['table_flops']:.3g} flop) and {plan['diag_tables']} CP run(s) into "
                                   "diagonal product tables")},
+            "tensor_view": {
+                "executed_tflops": plan["tensor_flops"] / (k_ms * 1e-3) / 1e12,
+                "peak": TC_TF32_PEAK,
+                "frac": plan["tensor_flops"] / (k_ms * 1e-3) / 1e12 / TC_TF32_PEAK,
+                "what": ("split-TF32 mma.sync work of the sorted modes (3 MMAs per product) over the same kernel "
+                         "time, against the measured mma.sync m16n8k8 tf32 peak (profiles/peaks_r01.json)")},
             "plan": {k: plan[k] for k in ("algo", "n_virtual", "prefix_modes", "suffix_modes",
                                           "prefix_rows", "suffix_rows", "diag_tables", "table_flops",
                                           "compute_kernel", "tile")},
@@ -494,12 +508,25 @@ def bench_dot(dev, steps, warmup, dist, is_norm=False):
     nbytes = 4096 * per_pair * (1 if is_norm else 2)
     peak, src = hbm_peak()
     traffic, tsrc = ncu_traffic("cfg4_dot", "dot_r16_kernel") if not is_norm else (None, None)
+    # 2 * sum_k I_k (r_l r_l r_r + r_r r_l r_r) flop per pair
+    # (Y = M B_j, then A_j^T Y), the same for norm
+    flop = 4096 * 2 * sum(s * (ranks[k] * ranks[k] * ranks[k + 1] + ranks[k + 1] * ranks[k] * ranks[k + 1])
+                          for k, s in enumerate(shape))
+    hbm = {"bound": "hbm", "achieved": nbytes / (k_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+           "frac": nbytes / (k_ms * 1e-3) / 1e9 / peak, "traffic": traffic, "traffic_source": tsrc,
+           "peak_source": src, "kernel": "dot_r16_kernel", "kernel_ms": k_ms,
+           "algorithmic": f"{nbytes} core bytes read per launch (each core read once)"}
+    fpk, fsrc = fp32_peak()
+    fp = {"bound": "fp32", "achieved": flop / (k_ms * 1e-3) / 1e12, "peak": fpk, "unit": "TFLOP/s",
+          "frac": flop / (k_ms * 1e-3) / 1e12 / fpk, "traffic": traffic, "traffic_source": tsrc,
+          "peak_source": fsrc, "kernel": "dot_r16_kernel", "kernel_ms": k_ms,
+          "algorithmic": f"{flop} flop per launch (SURVEY 8(d)); executed on tensor cores as split-TF32 "
+                         "mma.sync (3 MMAs per product)"}
+    # binding roofs per SURVEY 8(d): dot -> HBM read bandwidth, norm -> FP32
+    roof, other = (fp, hbm) if is_norm else (hbm, fp)
+    roof = dict(roof, other_roof=other)
     return {"op": "norm" if is_norm else "dot", "workload": "cfg4", "ms_per_step": ms,
-            "pairs/s": 4096 / (ms * 1e-3), "GB/s": nbytes / (ms * 1e-3) / 1e9,
-            "roofline": {"bound": "hbm", "achieved": nbytes / (k_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
-                         "frac": nbytes / (k_ms * 1e-3) / 1e9 / peak, "traffic": traffic, "traffic_source": tsrc,
-                         "peak_source": src, "kernel": "dot_r16_kernel", "kernel_ms": k_ms,
-                         "algorithmic": f"{nbytes} core bytes read per launch (each core read once)"}}
+            "pairs/s": 4096 / (ms * 1e-3), "GB/s": nbytes / (ms * 1e-3) / 1e9, "roofline": roof}
 
 
 def run_ours(args):
@@ -565,6 +592,8 @@ def run_ours(args):
 
 
 def main():
+    global TC_TF32_PEAK
+    TC_TF32_PEAK = _tc_tf32_peak()
     faulthandler.enable()
     args = parse()
     if args.impl == "reference":

@@ -206,6 +206,8 @@ typedef struct {
   int32_t compute_kernel;/* bucketed: 0 = state kernel, 1 = stream kernel (one
                             sorted mode; no per-sample state in shared memory) */
   int32_t tile;          /* bucketed: samples per tile                          */
+  double tensor_flops;   /* per call: tensor-core (split-TF32 mma.sync) flops
+                            the compute kernel issues, 3 MMAs per product      */
 } tnb_entries_info;
 int tnb_entries_plan(const tnb_chain* chain, int64_t m, int32_t algo, tnb_entries_info* info);
 

@@ -45,7 +45,8 @@ class TnbEntriesInfo(ctypes.Structure):
     _fields_ = [("algo", c_int32), ("n_virtual", c_int32), ("prefix_modes", c_int32),
                 ("suffix_modes", c_int32), ("prefix_rows", c_int64), ("suffix_rows", c_int64),
                 ("kernel_flops", c_double), ("table_flops", c_double), ("diag_tables", c_int32),
-                ("table_launches", c_int32), ("compute_kernel", c_int32), ("tile", c_int32)]
+                ("table_launches", c_int32), ("compute_kernel", c_int32), ("tile", c_int32),
+                ("tensor_flops", c_double)]
 
 
 # name -> (restype, argtypes); exactly the declarations of include/tnb.h

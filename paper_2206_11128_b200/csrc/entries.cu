@@ -184,6 +184,7 @@ int entries_plan(const tnb_chain* c, int64_t m, int algo, tnb_entries_info* info
   info->table_flops = 0.0;
   info->diag_tables = info->table_launches = 0;
   info->compute_kernel = info->tile = 0;
+  info->tensor_flops = 0.0;
   if (use_bucketed(ch, m, algo) && bucketed_supported(ch)) {
     info->algo = TNB_ALGO_BUCKETED;
     bucketed_info(ch, m, info);

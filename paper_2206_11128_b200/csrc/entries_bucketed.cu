@@ -2339,6 +2339,9 @@ void bucketed_info(const ChainDev& ch, int64_t m, tnb_entries_info* info) {
   const ChainDev& v = P.v;
   info->compute_kernel = P.stream ? 1 : 0;
   info->tile = P.bp.T;
+  info->tensor_flops = 0.0;
+  for (int g = 0; g < v.n; ++g)
+    if (mp.lm[g] && mp.mma[g]) info->tensor_flops += 3.0 * 2.0 * v.m[g].rl * v.m[g].rr * (double)m;
   info->n_virtual = v.n;
   info->prefix_modes = mp.a();
   info->suffix_modes = mp.b();
