@@ -71,6 +71,9 @@
 #ifndef TNB_LAST_U
 #define TNB_LAST_U 4
 #endif
+#ifndef TNB_STATE_NEARPF
+#define TNB_STATE_NEARPF 0
+#endif
 #ifndef TNB_STATE_PF_EARLY
 #define TNB_STATE_PF_EARLY 0
 #endif
@@ -102,7 +105,7 @@
 #define TNB_STREAM_NREC 2
 #endif
 #ifndef TNB_STREAM_PF
-#define TNB_STREAM_PF 0
+#define TNB_STREAM_PF 2
 #endif
 
 namespace tnb {
@@ -821,6 +824,21 @@ __global__ void __launch_bounds__(NT, kStateCtas)
             while (p < bend) {
               const int n = min(16, bend - p);
               const int sa = perm[p + min(mg, n - 1)], sb = perm[p + min(mg + 8, n - 1)];
+#if TNB_STATE_NEARPF
+              // L2 prefetch of the table rows this warp reads TNB_STATE_NEARPF
+              // positions ahead (first-mode rows in mode 1, closing rows in
+              // the fused last sorted mode)
+              if (lane < 16 && ((ffirst && k == 1) || fclose)) {
+                const int pf = p + TNB_STATE_NEARPF + lane;
+                if (pf < hi) {
+                  const int sp = perm[pf];
+                  const float* a = (ffirst && k == 1)
+                                       ? ch.m[0].s + (int64_t)(bp.wide0 ? widx0[sp] : (uint32_t)cidx[sp]) * R
+                                       : mlast.s + (int64_t)(bp.wideL ? widxL[sp] : (uint32_t)colL[sp]) * R;
+                  prefetch_l2(a);
+                }
+              }
+#endif
               const uint32_t r0 = s_state + (uint32_t)sa * (RP * 4);
               const uint32_t r1 = s_state + (uint32_t)sb * (RP * 4);
               float2 da[4], db[4];
