@@ -112,6 +112,10 @@ namespace tnb {
 namespace {
 
 constexpr int kMaxJ = 1024;          // bucket count limit for sorted modes
+#ifndef TNB_PREP_THREADS
+#define TNB_PREP_THREADS 512
+#endif
+constexpr int kPrepThreads = TNB_PREP_THREADS;
 #ifndef TNB_STATE_CTAS
 #define TNB_STATE_CTAS 1
 #endif
@@ -315,12 +319,12 @@ struct BPlan {
 // (coalesced), validates and combines them, and writes the compact [N][T]
 // index block of the tile record.
 template <typename IdxT, bool PSORT>
-__global__ void __launch_bounds__(512, PSORT ? 2 : 3) entries_prep_kernel(const __grid_constant__ ChainDev ch,
+__global__ void __launch_bounds__(kPrepThreads, PSORT ? 1024 / kPrepThreads : 1536 / kPrepThreads) entries_prep_kernel(const __grid_constant__ ChainDev ch,
                                                            const __grid_constant__ BPlan bp,
                                                            const int64_t* __restrict__ idx, int64_t m,
                                                            int32_t* __restrict__ err,
                                                            unsigned char* __restrict__ ws) {
-  constexpr int NT = 512;
+  constexpr int NT = kPrepThreads;
   extern __shared__ __align__(16) unsigned char smem[];
   const int N = ch.n, T = bp.T;
   IdxT* idxs = reinterpret_cast<IdxT*>(smem);                                         // [ncrow][T]
@@ -2278,7 +2282,7 @@ int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m
   if (rc) return rc;
   {
     KTimer kt("entries_prep", st);
-    pk<<<(unsigned)bp.ntiles, 512, psmem, st>>>(ch, bp, idx, m, err, ws);
+    pk<<<(unsigned)bp.ntiles, kPrepThreads, psmem, st>>>(ch, bp, idx, m, err, ws);
   }
   rc = check_launch("entries_prep");
   if (rc) return rc;
