@@ -19,7 +19,11 @@
  *   - status codes only, no exceptions cross the ABI; tnb_last_error() gives a
  *     thread-local message for the last non-zero status;
  *   - no global mutable state (except the opt-in kernel timing below): calls
- *     on distinct streams/threads are safe.
+ *     on distinct streams/threads are safe.  The bucketed entries path forks
+ *     one thread-local side stream per device (created on first use) to build
+ *     its tables concurrently with the index pass, and joins it back into the
+ *     caller's stream before the per-entry kernel (TNB_TABLE_STREAM=0: no
+ *     fork).
  */
 #ifndef TNB_H_
 #define TNB_H_

@@ -2273,7 +2273,7 @@ int launch_stream(const ChainDev& ch, const BPlan& bp, const unsigned char* ws, 
 
 template <int R, typename IdxT, int NT, bool FOLD>
 int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m, float* out,
-              int32_t* err, unsigned char* ws, bool stream, cudaStream_t st) {
+              int32_t* err, unsigned char* ws, bool stream, cudaStream_t st, cudaEvent_t tables_done) {
   // prep: one CTA per tile; sort: one warp per (tile, sorted mode)
   const size_t psmem = prep_smem_bytes(bp.ncrow, bp.T, (int)sizeof(IdxT), bp.nw, bp.psort, bp.jpad);
   auto pk = bp.psort ? entries_prep_kernel<IdxT, true> : entries_prep_kernel<IdxT, false>;
@@ -2302,6 +2302,10 @@ int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m
     rc = check_launch("entries_sort");
     if (rc) return rc;
   }
+  if (tables_done) {  // the tables were built on the side stream, concurrently with prep / sort
+    rc = check_cuda(cudaStreamWaitEvent(st, tables_done, 0), "join tables");
+    if (rc) return rc;
+  }
   if (stream) {
     if constexpr (R <= 24) return launch_stream<R, IdxT>(ch, bp, ws, m, out, st);
     return set_error(TNB_EINVAL, "stream kernel: rank > 24");
@@ -2322,13 +2326,13 @@ int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m
 
 template <int R, typename IdxT>
 int launch_ri(const ChainDev& ch, const BPlan& bp, int nt, const int64_t* idx, int64_t m, float* out,
-              int32_t* err, unsigned char* ws, bool stream, cudaStream_t st) {
+              int32_t* err, unsigned char* ws, bool stream, cudaStream_t st, cudaEvent_t tables_done) {
   const int N = ch.n;
   const bool fold = !stream && (R & 3) == 0 && N >= 3 && ch.m[N - 2].layout == TNB_LAYOUT_DIAG &&
                     ch.m[N - 1].rl == R && ch.m[N - 1].rr == 1;
   (void)nt;
-  if (fold) return launch_rt<R, IdxT, kComputeThreads, true>(ch, bp, idx, m, out, err, ws, stream, st);
-  return launch_rt<R, IdxT, kComputeThreads, false>(ch, bp, idx, m, out, err, ws, stream, st);
+  if (fold) return launch_rt<R, IdxT, kComputeThreads, true>(ch, bp, idx, m, out, err, ws, stream, st, tables_done);
+  return launch_rt<R, IdxT, kComputeThreads, false>(ch, bp, idx, m, out, err, ws, stream, st, tables_done);
 }
 
 }  // namespace
@@ -2395,6 +2399,34 @@ void bucketed_info(const ChainDev& ch, int64_t m, tnb_entries_info* info) {
   info->table_flops = tf;
 }
 
+// One non-blocking side stream + fork / join events per (host thread,
+// device), created on first use: the only state libtnb keeps besides the
+// device-property cache (reentrant: each thread owns its own).
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+SideStream* side_stream() {
+  static thread_local SideStream ss[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  SideStream& x = ss[dev];
+  if (!x.s) {
+    if (cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      x = SideStream{};
+      return nullptr;
+    }
+  }
+  return &x;
+}
+int table_stream_env() {
+  const char* e = getenv("TNB_TABLE_STREAM");
+  return (e && e[0] == '0') ? 0 : 1;
+}
+
 int launch_entries_bucketed(const ChainDev& ch, const int64_t* idx, int64_t m, float* out,
                             int32_t* err, void* ws, int64_t ws_bytes, cudaStream_t st) {
   EPlan P;
@@ -2410,9 +2442,24 @@ int launch_entries_bucketed(const ChainDev& ch, const int64_t* idx, int64_t m, f
     return set_error(TNB_EWORKSPACE, "bucketed entries needs %lld workspace bytes, got %lld",
                      (long long)need, (long long)ws_bytes);
   unsigned char* base = static_cast<unsigned char*>(ws);
+  cudaEvent_t tables = nullptr;
   if (mp.table_bytes) {
-    rc = build_tables(ch, mp, base, st);
-    if (rc) return rc;
+    // the tables depend only on the cores, prep / sort only on the indices:
+    // build the tables on a side stream forked from st (after everything
+    // already queued on st, e.g. the previous call still reading them) and
+    // join it before the compute kernel
+    SideStream* ss = table_stream_env() ? side_stream() : nullptr;
+    if (ss) {
+      rc = check_cuda(cudaEventRecord(ss->fork, st), "fork");
+      if (!rc) rc = check_cuda(cudaStreamWaitEvent(ss->s, ss->fork, 0), "fork wait");
+      if (!rc) rc = build_tables(ch, mp, base, ss->s);
+      if (!rc) rc = check_cuda(cudaEventRecord(ss->join, ss->s), "join");
+      if (rc) return rc;
+      tables = ss->join;
+    } else {
+      rc = build_tables(ch, mp, base, st);
+      if (rc) return rc;
+    }
     virtual_chain(ch, mp, base, &v);
   }
   set_vmap(ch, mp, &bp);
@@ -2422,17 +2469,17 @@ int launch_entries_bucketed(const ChainDev& ch, const int64_t* idx, int64_t m, f
   const bool small = bp.idx_bytes == 1;
   switch (R) {
     case 8:
-      return small ? launch_ri<8, uint8_t>(chv, bp, nt, idx, m, out, err, w, stream, st)
-                   : launch_ri<8, uint16_t>(chv, bp, nt, idx, m, out, err, w, stream, st);
+      return small ? launch_ri<8, uint8_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables)
+                   : launch_ri<8, uint16_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables);
     case 16:
-      return small ? launch_ri<16, uint8_t>(chv, bp, nt, idx, m, out, err, w, stream, st)
-                   : launch_ri<16, uint16_t>(chv, bp, nt, idx, m, out, err, w, stream, st);
+      return small ? launch_ri<16, uint8_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables)
+                   : launch_ri<16, uint16_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables);
     case 24:
-      return small ? launch_ri<24, uint8_t>(chv, bp, nt, idx, m, out, err, w, stream, st)
-                   : launch_ri<24, uint16_t>(chv, bp, nt, idx, m, out, err, w, stream, st);
+      return small ? launch_ri<24, uint8_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables)
+                   : launch_ri<24, uint16_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables);
     default:
-      return small ? launch_ri<32, uint8_t>(chv, bp, nt, idx, m, out, err, w, stream, st)
-                   : launch_ri<32, uint16_t>(chv, bp, nt, idx, m, out, err, w, stream, st);
+      return small ? launch_ri<32, uint8_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables)
+                   : launch_ri<32, uint16_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables);
   }
 }
 
