@@ -52,6 +52,10 @@
 #ifndef TNB_FAST_SPLIT
 #define TNB_FAST_SPLIT 1
 #endif
+// state kernel: warp ranges balanced in tensor-core steps (write_splits)
+#ifndef TNB_BALANCED
+#define TNB_BALANCED 1
+#endif
 #ifndef TNB_STATE_MMA
 #define TNB_STATE_MMA 1
 #endif
@@ -300,7 +304,8 @@ struct BPlan {
   // the state kernel; stream plans skip the first mode (always wide) and a
   // wide last mode)
   int crow0, ncrow;
-  int psort;  // the prep kernel sorts (TNB_SORT_IN_PREP)
+  int psort;   // the prep kernel sorts (TNB_SORT_IN_PREP)
+  int splits;  // balanced warp ranges are written after the bucket starts (state kernel)
   int8_t slot[kMaxModes];  // mode -> sorted slot or -1
   // mode merging: the kernels run a VIRTUAL chain whose first / last modes
   // may be prefix / suffix tables over several original modes; the prep
@@ -315,10 +320,56 @@ struct BPlan {
   int8_t mmal[kMaxModes];   // ... in the tensor-core fragment order (mma_slice_kernel)
 };
 
+// Balanced warp ranges for the state kernel's sorted modes, written by ONE
+// warp after the bucket starts gst[0..J] (gst[J] = tn): the tile's work is
+// counted in 16-sample steps per bucket (the tensor-core step), and warp w of
+// kSplitWarps starts at step floor(w S / kSplitWarps) -- a position inside
+// its bucket, on a 16-sample boundary -- instead of at w tn / kSplitWarps
+// (equal positions give a warp that straddles more buckets more steps, and
+// the mode barrier waits for it).  gst[J + 1 + w] = start of warp w,
+// gst[J + 1 + kSplitWarps] = tn.
+constexpr int kSplitWarps = 16;
+// `sm` holds the same starts in shared memory (entries 0..J-1).
+__device__ void write_splits(uint16_t* gst, const int* sm, int J, int tn, int lane) {
+  __syncwarp();
+  const int per = (J + 31) >> 5;
+  const int j0 = lane * per, j1 = min(j0 + per, J);
+  auto start = [&](int j) { return j < J ? sm[j] : tn; };
+  int my = 0;
+  for (int j = j0; j < j1; ++j) my += (start(j + 1) - start(j) + 15) >> 4;
+  int incl = my;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int S = __shfl_sync(0xffffffffu, incl, 31);
+  const int excl = incl - my;
+  __syncwarp();
+  for (int w = 0; w < kSplitWarps; ++w) {
+    const int t = (int)(((int64_t)w * S) / kSplitWarps);
+    if (S == 0) {
+      if (lane == 0) gst[J + 1 + w] = 0;
+    } else if (t >= excl && t < incl) {
+      int acc = excl;
+      for (int j = j0; j < j1; ++j) {
+        const int sj = (start(j + 1) - start(j) + 15) >> 4;
+        if (t < acc + sj) {
+          gst[J + 1 + w] = (uint16_t)(start(j) + 16 * (t - acc));
+          break;
+        }
+        acc += sj;
+      }
+    }
+  }
+  if (lane == 0) gst[J + 1 + kSplitWarps] = (uint16_t)tn;
+  __syncwarp();
+}
+
 // prep: one CTA per tile -- reads the tile's n0 int64 index columns
 // (coalesced), validates and combines them, and writes the compact [N][T]
 // index block of the tile record.
-template <typename IdxT, bool PSORT>
+template <typename IdxT, bool PSORT, bool SPLITS>
 __global__ void __launch_bounds__(kPrepThreads, PSORT ? 1024 / kPrepThreads : 1536 / kPrepThreads) entries_prep_kernel(const __grid_constant__ ChainDev ch,
                                                            const __grid_constant__ BPlan bp,
                                                            const int64_t* __restrict__ idx, int64_t m,
@@ -422,6 +473,7 @@ __global__ void __launch_bounds__(kPrepThreads, PSORT ? 1024 / kPrepThreads : 15
         run += c;
       }
       for (int j = J + lane; j < JP; j += 32) gst[j] = (uint16_t)tn;
+      if constexpr (SPLITS) write_splits(gst, hist, J, tn, lane);
     }
     __syncthreads();
     for (int s = tid; s < tn; s += NT) pb[atomicAdd(&hist[col[s]], 1)] = (uint16_t)s;
@@ -483,7 +535,7 @@ __global__ void __launch_bounds__(256) entries_sort_kernel(const __grid_constant
     run += c;
   }
   for (int j = J + lane; j < JP; j += 32) gst[j] = (uint16_t)tn;
-  __syncwarp();
+  if (bp.splits) write_splits(gst, h, J, tn, lane);
 #pragma unroll 4
   for (int s = lane; s < tn; s += 32) pb[atomicAdd(&h[col[s]], 1)] = (uint16_t)s;
   __syncwarp();
@@ -780,8 +832,8 @@ __global__ void __launch_bounds__(NT, kStateCtas)
         mb_wait(&pbar[b], (uint32_t)((item >> 1) & 1));
         const uint16_t* perm = permb + b * T;
         const uint16_t* st = startb + b * bp.jpad;
-        const int lo = (int)(((int64_t)warp * tn) / nwarps);
-        const int hi = (int)(((int64_t)(warp + 1) * tn) / nwarps);
+        const int lo = bp.splits ? (int)st[md.J + 1 + warp] : (int)(((int64_t)warp * tn) / nwarps);
+        const int hi = bp.splits ? (int)st[md.J + 2 + warp] : (int)(((int64_t)(warp + 1) * tn) / nwarps);
         if constexpr (R == 32) {
         int p = lo;
 #if TNB_STATE_MMA
@@ -2139,6 +2191,7 @@ int make_bplan(const ChainDev& ch, int64_t m, BPlan* bp, int* R_out, int* nt_out
   bp->wideL = N > 1 && ch.m[N - 1].J > 65535;
   bp->nw = bp->wide0 + bp->wideL;
   bp->crow0 = stream ? 1 : 0;
+  bp->splits = !stream && TNB_BALANCED && kComputeThreads / 32 == kSplitWarps;
   bp->ncrow = stream ? N - 1 - bp->wideL : N;
   for (int k = 0; k < ch.n; ++k) {
     const bool wide = (k == 0 && bp->wide0) || (k == N - 1 && bp->wideL);
@@ -2154,7 +2207,8 @@ int make_bplan(const ChainDev& ch, int64_t m, BPlan* bp, int* R_out, int* nt_out
   constexpr int NT = kComputeThreads;
   const int RP = R == 32 ? Geo<32>::RP : R + TNB_RPAD;
   const int idx_bytes = small ? 1 : 2;
-  const int jpad = ((jmax + 1) + 7) & ~7;
+  // starts, sentinel (+ the state kernel's warp splits)
+  const int jpad = ((jmax + 1 + (stream ? 0 : 1 + kSplitWarps)) + 7) & ~7;
   const size_t budget = ((size_t)233472 - 1024 * kStateCtas) / kStateCtas;
   // the prep kernel holds every slot's permutation and per-warp counts at once
   int jmin = 1 << 30;
@@ -2276,7 +2330,8 @@ int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m
               int32_t* err, unsigned char* ws, bool stream, cudaStream_t st, cudaEvent_t tables_done) {
   // prep: one CTA per tile; sort: one warp per (tile, sorted mode)
   const size_t psmem = prep_smem_bytes(bp.ncrow, bp.T, (int)sizeof(IdxT), bp.nw, bp.psort, bp.jpad);
-  auto pk = bp.psort ? entries_prep_kernel<IdxT, true> : entries_prep_kernel<IdxT, false>;
+  auto pk = bp.psort ? (bp.splits ? entries_prep_kernel<IdxT, true, true> : entries_prep_kernel<IdxT, true, false>)
+                     : entries_prep_kernel<IdxT, false, false>;
   int rc = check_cuda(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem),
                       "prep smem attr");
   if (rc) return rc;
