@@ -824,7 +824,15 @@ __global__ void __launch_bounds__(NT, kStateCtas)
             const int64_t ns0 = ntile * T;
             const int ntn = (int)((m - ns0) < T ? (m - ns0) : T);
             const uint32_t* nw = reinterpret_cast<const uint32_t*>(ws + ntile * bp.tile_bytes + bp.off_wide);
-            for (int s = tid; s < ntn; s += NT) prefetch_l2(ch.m[0].s + (int64_t)__ldg(nw + s) * ch.m[0].rr);
+            // the index loads first (independent, all in flight), then the prefetches
+            for (int base = tid; base < ntn; base += 4 * NT) {
+              uint32_t jj[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) jj[u] = base + u * NT < ntn ? __ldg(nw + base + u * NT) : 0u;
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (base + u * NT < ntn) prefetch_l2(ch.m[0].s + (int64_t)jj[u] * ch.m[0].rr);
+            }
           }
         }
 #endif
