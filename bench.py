@@ -428,8 +428,10 @@ def cpu_baseline_entries(t_nodes_fn, idx_host, out_dev, m_sample):
                       "(core.py:394-444), float64, OpenBLAS threads"}, err
 
 
-def bench_full(dev, steps, warmup, dist):
-    """K2 on cfg3: full() of a TT N=4, I=256, r=64 -> 17.18 GB fp32."""
+def bench_full(dev, steps, warmup, dist, ws=1, rank=0):
+    """K2 on cfg3: full() of a TT N=4, I=256, r=64 -> 17.18 GB fp32.  With N
+    ranks, rank r writes the leading-mode slab shard_bounds(256, N, r)
+    (SURVEY 8(e), strong scaling: the 17.18 GB are split across the GPUs)."""
     import torch
 
     import paper_2206_11128_b200 as tb
@@ -437,30 +439,33 @@ def bench_full(dev, steps, warmup, dist):
     shape, r = W.CONFIGS["cfg3"][1], W.CONFIGS["cfg3"][2]
     t = tb.TnTensor([tb.ModeNode("tt", c) for c in W.tt_cores(shape, r, W.base_seed())])
     t._packed()
-    out = torch.empty(shape, dtype=torch.float32, device=dev)
     from paper_2206_11128_b200 import _native as N
+    from paper_2206_11128_b200.shard import shard_bounds
     import ctypes
 
+    lo, hi = shard_bounds(shape[0], ws, rank)
+    out = torch.empty((hi - lo,) + tuple(shape[1:]), dtype=torch.float32, device=dev)
     p = t._packed()
     lib = N.load()
-    wsb = lib.tnb_full_workspace_bytes(ctypes.byref(p.chain), 0, shape[0])
+    wsb = lib.tnb_full_workspace_bytes(ctypes.byref(p.chain), lo, hi)
     wsbuf = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
     st = N.stream_ptr(dev)
 
     def step():
-        N.check(lib.tnb_full_f32(ctypes.byref(p.chain), 0, shape[0], out.data_ptr(),
+        N.check(lib.tnb_full_f32(ctypes.byref(p.chain), lo, hi, out.data_ptr(),
                                  wsbuf.data_ptr(), wsb, st), "full")
 
     ms = timed_steps(step, steps, warmup, torch.cuda.current_stream(dev), dist, kernel_timing=True) / steps
     g_ms, g_n = N.timing_read("full_gemm")
     N.timing_enable(False)
-    nbytes = out.numel() * 4
+    nbytes = out.numel() * 4  # this rank's slab
     del out
     peak, src = hbm_peak()
     k_ms = g_ms / g_n if g_n else ms
     traffic, tsrc = ncu_traffic("cfg3_full", "full_tc_gemm_kernel")
-    return {"op": "full", "workload": "cfg3", "ms_per_step": ms, "GB/s": nbytes / (ms * 1e-3) / 1e9,
-            "bytes_written": nbytes,
+    total = 4 * int(np.prod(shape))
+    return {"op": "full", "workload": "cfg3", "ms_per_step": ms, "GB/s": total / (ms * 1e-3) / 1e9,
+            "bytes_written": nbytes, "slab": [lo, hi],
             "roofline": {"bound": "hbm", "achieved": nbytes / (k_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": nbytes / (k_ms * 1e-3) / 1e9 / peak, "traffic": traffic,
                          "traffic_source": tsrc, "peak_source": src, "kernel": "full_gemm (tcgen05 3xTF32)",
@@ -468,9 +473,11 @@ def bench_full(dev, steps, warmup, dist):
                          "algorithmic": f"{nbytes} output bytes written per launch (4 B x 256^4)"}}
 
 
-def bench_dot(dev, steps, warmup, dist, is_norm=False):
+def bench_dot(dev, steps, warmup, dist, is_norm=False, ws=1, rank=0):
     """K3 on cfg4: 4096 pairs of TTs (N=16, I=64, r=16); cores drawn on the
-    device (torch, seeded) since only their shapes matter for timing."""
+    device (torch, seeded) since only their shapes matter for timing.  With N
+    ranks each rank holds and contracts its shard_bounds(4096, N, r) pairs
+    (SURVEY 8(e), strong scaling)."""
     import ctypes
 
     import torch
@@ -482,15 +489,19 @@ def bench_dot(dev, steps, warmup, dist, is_norm=False):
     g = torch.Generator(device=dev)
     g.manual_seed(W.base_seed())
     ranks = [1] + [r] * (len(shape) - 1) + [1]
+    from paper_2206_11128_b200.shard import shard_bounds
+
+    plo, phi = shard_bounds(4096, ws, rank)
+    npair = phi - plo
 
     def mk():
-        return tb.TnTensor([tb.ModeNode("tt", torch.randn((4096, ranks[k], s, ranks[k + 1]), device=dev,
+        return tb.TnTensor([tb.ModeNode("tt", torch.randn((npair, ranks[k], s, ranks[k + 1]), device=dev,
                                                           generator=g) * 0.25, batched=True)
-                            for k, s in enumerate(shape)], 4096)
+                            for k, s in enumerate(shape)], npair)
 
     a, b = mk(), mk()
     pa, pb = a._packed(), b._packed()
-    out = torch.empty(4096, dtype=torch.float32, device=dev)
+    out = torch.empty(npair, dtype=torch.float32, device=dev)
     lib = N.load()
     st = N.stream_ptr(dev)
 
@@ -505,12 +516,12 @@ def bench_dot(dev, steps, warmup, dist, is_norm=False):
     N.timing_enable(False)
     k_ms = d_ms / d_n if d_n else ms
     per_pair = sum(ranks[k] * s * ranks[k + 1] for k, s in enumerate(shape)) * 4
-    nbytes = 4096 * per_pair * (1 if is_norm else 2)
+    nbytes = npair * per_pair * (1 if is_norm else 2)
     peak, src = hbm_peak()
     traffic, tsrc = ncu_traffic("cfg4_dot", "dot_r16_kernel") if not is_norm else (None, None)
     # 2 * sum_k I_k (r_l r_l r_r + r_r r_l r_r) flop per pair
     # (Y = M B_j, then A_j^T Y), the same for norm
-    flop = 4096 * 2 * sum(s * (ranks[k] * ranks[k] * ranks[k + 1] + ranks[k + 1] * ranks[k] * ranks[k + 1])
+    flop = npair * 2 * sum(s * (ranks[k] * ranks[k] * ranks[k + 1] + ranks[k + 1] * ranks[k] * ranks[k + 1])
                           for k, s in enumerate(shape))
     hbm = {"bound": "hbm", "achieved": nbytes / (k_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
            "frac": nbytes / (k_ms * 1e-3) / 1e9 / peak, "traffic": traffic, "traffic_source": tsrc,
@@ -526,7 +537,8 @@ def bench_dot(dev, steps, warmup, dist, is_norm=False):
     roof, other = (fp, hbm) if is_norm else (hbm, fp)
     roof = dict(roof, other_roof=other)
     return {"op": "norm" if is_norm else "dot", "workload": "cfg4", "ms_per_step": ms,
-            "pairs/s": 4096 / (ms * 1e-3), "GB/s": nbytes / (ms * 1e-3) / 1e9, "roofline": roof}
+            "pairs/s": 4096 / (ms * 1e-3), "GB/s": nbytes * ws / (ms * 1e-3) / 1e9, "roofline": roof,
+            "pairs_this_rank": npair}
 
 
 def run_ours(args):
@@ -576,13 +588,15 @@ def run_ours(args):
                 torch.cuda.empty_cache()
             line["secondary"] = sec
     elif args.op == "full":
-        r = bench_full(dev, args.steps, args.warmup, dist)
-        line.update({"metric": "full() GB/s", "unit": "GB/s", "value": r["GB/s"] * ws,
+        r = bench_full(dev, args.steps, args.warmup, dist, ws, rank)
+        line.update({"metric": "full() GB/s", "unit": "GB/s", "value": r["GB/s"],
+                     "scaling": "strong" if ws > 1 else "weak",
                      "ms_per_step": r["ms_per_step"], "roofline": r["roofline"],
                      "config": {"workload": "cfg3", "l2": "17 GB output, larger than L2"}})
     else:
-        r = bench_dot(dev, args.steps, args.warmup, dist, args.op == "norm")
-        line.update({"metric": f"{args.op}s/sec", "unit": "pairs/s", "value": r["pairs/s"] * ws,
+        r = bench_dot(dev, args.steps, args.warmup, dist, args.op == "norm", ws, rank)
+        line.update({"metric": f"{args.op}s/sec", "unit": "pairs/s", "value": r["pairs/s"],
+                     "scaling": "strong" if ws > 1 else "weak",
                      "ms_per_step": r["ms_per_step"], "roofline": r["roofline"],
                      "config": {"workload": "cfg4", "l2": "4096 x 16 cores = 268 MB per operand, larger than L2"}})
     if rank == 0:
