@@ -345,6 +345,8 @@ def bench_entries(args, cfg, dev, dist, ws, rank):
                                           "compute_kernel", "tile")},
             "other_kernels_ms": {k: (v[0] / v[1] if v[1] else None) for k, v in kt.items()
                                  if k != "entries_compute"},
+            "other_kernels_note": ("entries_tables runs on a side stream concurrently with entries_prep / "
+                                   "entries_sort (joined before the compute kernel): its span overlaps theirs"),
             "step_tflops": algo_flops / (ms_step * 1e-3) / 1e12,
             "hbm_view": {"bytes_per_launch": (8 * len(shape) + 4) * m,
                          "achieved_gbs": (8 * len(shape) + 4) * m / (ms_step * 1e-3) / 1e9}}
