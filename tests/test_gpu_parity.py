@@ -490,3 +490,22 @@ def test_bucketed_r32_tensor_core_paths(lane_major, monkeypatch):
     bad[m // 2, 2] = 40
     with pytest.raises(tb.ContractViolationError, match="mode 2"):
         tb.entries(t, bad, algo=N.ALGO_BUCKETED)
+
+
+@pytest.mark.parametrize("three", [True, False])
+@pytest.mark.parametrize("m", [1, 17, 1000, 4099])
+def test_bucketed_stream_kernel_small_m(m, three):
+    # forced bucketed algorithm at tiny sizes: one ragged 256-row tile, warps
+    # with empty ranges, the producer's look-ahead past the last tile (the
+    # 3-mode chain runs the stream kernel at every m, the 4-mode one switches
+    # from the state kernel to the stream kernel once merging starts)
+    rng = np.random.default_rng(m)
+    nodes = _stream_nodes(rng, 24, jl=50)
+    mid = ("tt", (rng.standard_normal((24, 300, 24)) * 24 ** -0.5).astype(np.float32), None)
+    nodes = [nodes[0], mid, nodes[6]] if three else nodes[:2] + [mid, nodes[6]]
+    t = facade(nodes)
+    o = O.make_chain(nodes)
+    plan = N.entries_plan(t._packed().chain, m, N.ALGO_BUCKETED)
+    idx = O.uniform_indices(t.shape, m, 5)
+    got = tb.entries(t, idx, algo=N.ALGO_BUCKETED)
+    assert_close(got, O.entries(o, idx), what=f"stream m={m} plan={plan}")
