@@ -75,6 +75,12 @@
 #ifndef TNB_LAST_U
 #define TNB_LAST_U 4
 #endif
+#ifndef TNB_FFIRST_RING
+#define TNB_FFIRST_RING 1
+#endif
+#ifndef TNB_FRING_D
+#define TNB_FRING_D 3
+#endif
 #ifndef TNB_STATE_NEARPF
 #define TNB_STATE_NEARPF 0
 #endif
@@ -860,6 +866,38 @@ __global__ void __launch_bounds__(NT, kStateCtas)
                               mlast.rr == 1;
           const IdxT* colL = cidx + (size_t)(N - 1) * T;
           if (fclose) k2 = N - 1;
+          // fring: the first mode's table rows of this warp's positions are
+          // copied with 16-byte cp.async (LDGSTS, one commit group per 16
+          // positions, kFringD groups ahead) into the samples' own state rows,
+          // which mode 1 then reads as A fragments and overwrites in place --
+          // no CTA-wide gather barrier and no exposed load latency per step
+          const bool fring = TNB_FFIRST_RING && ffirst && k == 1;
+          int g_issued = 0;
+          auto issue_group = [&]() {
+            const int base = lo + 16 * g_issued;
+            const int rows = min(16, hi - base);
+            if (rows > 0) {
+              const uint32_t jr = lane < rows ? (bp.wide0 ? widx0[perm[base + lane]] : (uint32_t)cidx[perm[base + lane]])
+                                              : 0u;
+              const uint32_t sr = lane < rows ? (uint32_t)perm[base + lane] : 0u;
+#pragma unroll
+              for (int it = 0; it < 4; ++it) {  // 16 rows x 8 pieces of 16 bytes
+                const int i = lane + 32 * it;
+                const int row = i >> 3, piece = i & 7;
+                const uint32_t j = __shfl_sync(0xffffffffu, jr, row);
+                const uint32_t srow = __shfl_sync(0xffffffffu, sr, row);
+                if (row < rows)
+                  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s_state + srow * (RP * 4) + piece * 16),
+                               "l"(ch.m[0].s + (int64_t)j * R + piece * 4)
+                               : "memory");
+              }
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            ++g_issued;
+          };
+          constexpr int kFringD = TNB_FRING_D;
+          if (fring)
+            for (int i = 0; i < kFringD; ++i) issue_group();
           while (p < hi) {
             const int key = col[perm[p]];
             const int bend = min((int)st[key + 1], hi);
@@ -887,6 +925,15 @@ __global__ void __launch_bounds__(NT, kStateCtas)
             }
             while (p < bend) {
               const int n = min(16, bend - p);
+              if (fring) {  // the groups holding positions p .. p + n - 1 have landed
+                const int gneed = (p + n - 1 - lo) >> 4;
+                const int newer = g_issued - 1 - gneed;
+                if (newer >= 3) asm volatile("cp.async.wait_group 3;" ::: "memory");
+                else if (newer == 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
+                else if (newer == 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
+                else asm volatile("cp.async.wait_group 0;" ::: "memory");
+                __syncwarp();
+              }
               const int sa = perm[p + min(mg, n - 1)], sb = perm[p + min(mg + 8, n - 1)];
 #if TNB_STATE_NEARPF
               // L2 prefetch of the table rows this warp reads TNB_STATE_NEARPF
@@ -919,7 +966,7 @@ __global__ void __launch_bounds__(NT, kStateCtas)
 #pragma unroll
               for (int nt = 0; nt < 4; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
               float av[4][4];  // A values: rows g, g + 8 x columns 8kt + t, 8kt + t + 4
-              if (ffirst && k == 1) {
+              if (ffirst && k == 1 && !fring) {
                 const float* pa = ch.m[0].s + (int64_t)(bp.wide0 ? widx0[sa] : (uint32_t)cidx[sa]) * R + mt;
                 const float* pb = ch.m[0].s + (int64_t)(bp.wide0 ? widx0[sb] : (uint32_t)cidx[sb]) * R + mt;
 #pragma unroll
@@ -987,8 +1034,11 @@ __global__ void __launch_bounds__(NT, kStateCtas)
                 __syncwarp();
               }
               p += n;
+              if (fring)  // groups wholly consumed -> the next ones
+                while (g_issued < ((p - lo) >> 4) + kFringD && lo + 16 * g_issued < hi) issue_group();
             }
           }
+          if (fring) asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
 #endif
         while (p < hi) {
