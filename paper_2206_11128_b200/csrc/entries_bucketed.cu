@@ -68,10 +68,6 @@
 #ifndef TNB_FUSE_FIRST
 #define TNB_FUSE_FIRST 1
 #endif
-// ... with the last-mode rows loaded before the step's MMAs (1) or after (0)
-#ifndef TNB_FUSE_EARLY
-#define TNB_FUSE_EARLY 0
-#endif
 #ifndef TNB_LAST_U
 #define TNB_LAST_U 4
 #endif
@@ -81,20 +77,11 @@
 #ifndef TNB_FRING_D
 #define TNB_FRING_D 3
 #endif
-#ifndef TNB_STATE_NEARPF
-#define TNB_STATE_NEARPF 0
-#endif
-#ifndef TNB_STATE_PF_EARLY
-#define TNB_STATE_PF_EARLY 0
-#endif
 #ifndef TNB_STATE_PF
 #define TNB_STATE_PF 3
 #endif
 #ifndef TNB_STREAM_THREADS
 #define TNB_STREAM_THREADS 384
-#endif
-#ifndef TNB_STREAM_RS
-#define TNB_STREAM_RS 0
 #endif
 #ifndef TNB_STREAM_T
 #define TNB_STREAM_T 6144
@@ -821,7 +808,7 @@ __global__ void __launch_bounds__(NT, kStateCtas)
         // runs, of this tile's last-mode rows (bit 1) and of the NEXT tile's
         // first-mode rows (bit 2, indices from its record in global memory),
         // so neither gather waits on HBM latency
-        if (k == (TNB_STATE_PF_EARLY ? (int)bp.smode[0] : N - 2)) {
+        if (k == N - 2) {
           if ((TNB_STATE_PF & 1) && bp.wideL) {
             const ModeDev& ml = ch.m[N - 1];
             for (int s = tid; s < tn; s += NT) prefetch_l2(ml.s + (int64_t)widxL[s] * ml.rl);
@@ -935,33 +922,9 @@ __global__ void __launch_bounds__(NT, kStateCtas)
                 __syncwarp();
               }
               const int sa = perm[p + min(mg, n - 1)], sb = perm[p + min(mg + 8, n - 1)];
-#if TNB_STATE_NEARPF
-              // L2 prefetch of the table rows this warp reads TNB_STATE_NEARPF
-              // positions ahead (first-mode rows in mode 1, closing rows in
-              // the fused last sorted mode)
-              if (lane < 16 && ((ffirst && k == 1) || fclose)) {
-                const int pf = p + TNB_STATE_NEARPF + lane;
-                if (pf < hi) {
-                  const int sp = perm[pf];
-                  const float* a = (ffirst && k == 1)
-                                       ? ch.m[0].s + (int64_t)(bp.wide0 ? widx0[sp] : (uint32_t)cidx[sp]) * R
-                                       : mlast.s + (int64_t)(bp.wideL ? widxL[sp] : (uint32_t)colL[sp]) * R;
-                  prefetch_l2(a);
-                }
-              }
-#endif
               const uint32_t r0 = s_state + (uint32_t)sa * (RP * 4);
               const uint32_t r1 = s_state + (uint32_t)sb * (RP * 4);
-              float2 da[4], db[4];
-              if (fclose && TNB_FUSE_EARLY) {
-                const float* la = mlast.s + (int64_t)(bp.wideL ? widxL[sa] : (uint32_t)colL[sa]) * R + 2 * mt;
-                const float* lb = mlast.s + (int64_t)(bp.wideL ? widxL[sb] : (uint32_t)colL[sb]) * R + 2 * mt;
-#pragma unroll
-                for (int nt = 0; nt < 4; ++nt) {
-                  da[nt] = __ldg(reinterpret_cast<const float2*>(la + 8 * nt));
-                  db[nt] = __ldg(reinterpret_cast<const float2*>(lb + 8 * nt));
-                }
-              }
+              float2 da[4], db[4];  // closing rows, loaded after the MMAs (before them: spills)
               float acc[4][4];
 #pragma unroll
               for (int nt = 0; nt < 4; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
@@ -998,14 +961,12 @@ __global__ void __launch_bounds__(NT, kStateCtas)
                 }
               }
               if (fclose) {
-                if (!TNB_FUSE_EARLY) {
-                  const float* la = mlast.s + (int64_t)(bp.wideL ? widxL[sa] : (uint32_t)colL[sa]) * R + 2 * mt;
-                  const float* lb = mlast.s + (int64_t)(bp.wideL ? widxL[sb] : (uint32_t)colL[sb]) * R + 2 * mt;
+                const float* la = mlast.s + (int64_t)(bp.wideL ? widxL[sa] : (uint32_t)colL[sa]) * R + 2 * mt;
+                const float* lb = mlast.s + (int64_t)(bp.wideL ? widxL[sb] : (uint32_t)colL[sb]) * R + 2 * mt;
 #pragma unroll
-                  for (int nt = 0; nt < 4; ++nt) {
-                    da[nt] = __ldg(reinterpret_cast<const float2*>(la + 8 * nt));
-                    db[nt] = __ldg(reinterpret_cast<const float2*>(lb + 8 * nt));
-                  }
+                for (int nt = 0; nt < 4; ++nt) {
+                  da[nt] = __ldg(reinterpret_cast<const float2*>(la + 8 * nt));
+                  db[nt] = __ldg(reinterpret_cast<const float2*>(lb + 8 * nt));
                 }
                 float part0 = 0.f, part1 = 0.f;
 #pragma unroll
@@ -1640,27 +1601,15 @@ __global__ void __launch_bounds__(NT, 1)
           if constexpr (C1) a = fmaf(acc1[pi][0] + acc1[pi][1], ds[pi], a);
           part[pi] = a;
         }
-        if constexpr (P == 2 && TNB_STREAM_RS) {
-          // reduce-scatter over the group: the first exchange swaps halves
-          // (lanes q < L/2 finish sample 0, the others sample 1), so two
-          // samples cost log2(L) shuffles instead of 2 log2(L)
-          const bool up = (q & (L / 2)) != 0;
-          float keep = up ? part[1] : part[0];
-          keep += __shfl_xor_sync(0xffffffffu, up ? part[0] : part[1], L / 2);
 #pragma unroll
-          for (int o = L / 4; o > 0; o >>= 1) keep += __shfl_xor_sync(0xffffffffu, keep, o);
-          if ((q & (L / 2 - 1)) == 0 && (up ? G : 0) + gi < n) otile[sp[up ? 1 : 0]] = keep;
-        } else {
+        for (int o = L / 2; o > 0; o >>= 1) {
 #pragma unroll
-          for (int o = L / 2; o > 0; o >>= 1) {
+          for (int pi = 0; pi < P; ++pi) part[pi] += __shfl_xor_sync(0xffffffffu, part[pi], o);
+        }
+        if (q == 0) {
 #pragma unroll
-            for (int pi = 0; pi < P; ++pi) part[pi] += __shfl_xor_sync(0xffffffffu, part[pi], o);
-          }
-          if (q == 0) {
-#pragma unroll
-            for (int pi = 0; pi < P; ++pi)
-              if (pi * G + gi < n) otile[sp[pi]] = part[pi];
-          }
+          for (int pi = 0; pi < P; ++pi)
+            if (pi * G + gi < n) otile[sp[pi]] = part[pi];
         }
         }
         p += n;
