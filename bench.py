@@ -94,7 +94,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:  # noqa: BLE001
                 pass
-            self.stop_ev.wait(0.1)
+            self.stop_ev.wait(0.005)  # the timed regions are tens of ms
 
     def __enter__(self):
         if self.ok:
