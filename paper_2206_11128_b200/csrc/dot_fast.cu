@@ -159,15 +159,18 @@ __device__ __forceinline__ void slice_afrag(const float* S, int kc, int g, int t
   split_tf32(r0[16 + g], ah[2], al[2]);
   split_tf32(r0[16 + g + 8], ah[3], al[3]);
 }
+// SAME (norm: A_j == B_j): the slice's split fragments serve both products
+template <bool SAME>
 __device__ __forceinline__ void slice_mma(const float* Aj, const float* Bj, const uint32_t (&Mh)[2][4],
                                           const uint32_t (&Ml)[2][4], float (&Mw)[2][4], int g, int t) {
   float Y[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+  uint32_t sh[SAME ? 2 : 1][4], sl[SAME ? 2 : 1][4];  // B_j's fragments, kept for A_j^T Y when SAME
 #pragma unroll
   for (int kc = 0; kc < 2; ++kc) {
-    uint32_t ah[4], al[4];
-    slice_afrag(Bj, kc, g, t, ah, al);
-    mma3s(Y[0], ah, al, Mh[kc][0], Mh[kc][1], Ml[kc][0], Ml[kc][1]);
-    mma3s(Y[1], ah, al, Mh[kc][2], Mh[kc][3], Ml[kc][2], Ml[kc][3]);
+    const int ks = SAME ? kc : 0;
+    slice_afrag(Bj, kc, g, t, sh[ks], sl[ks]);
+    mma3s(Y[0], sh[ks], sl[ks], Mh[kc][0], Mh[kc][1], Ml[kc][0], Ml[kc][1]);
+    mma3s(Y[1], sh[ks], sl[ks], Mh[kc][2], Mh[kc][3], Ml[kc][2], Ml[kc][3]);
   }
   // this slice's A_j^T Y starts from zero and joins the running partial
   // with round-to-nearest FADDs: the MMA accumulator only ever sums the 6
@@ -176,7 +179,15 @@ __device__ __forceinline__ void slice_mma(const float* Aj, const float* Bj, cons
 #pragma unroll
   for (int kc = 0; kc < 2; ++kc) {
     uint32_t ah[4], al[4];
-    slice_afrag(Aj, kc, g, t, ah, al);
+    if constexpr (SAME) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        ah[i] = sh[SAME ? kc : 0][i];
+        al[i] = sl[SAME ? kc : 0][i];
+      }
+    } else {
+      slice_afrag(Aj, kc, g, t, ah, al);
+    }
     mma3(Z[0], ah, al, Y[kc][0], Y[kc][1]);
     mma3(Z[1], ah, al, Y[kc][2], Y[kc][3]);
   }
@@ -198,7 +209,7 @@ struct Walk {
   int k, c;
 };
 
-template <bool MMA>
+template <bool MMA, bool SAME>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm) dot_r16_kernel(const __grid_constant__ DotArgs args) {
   extern __shared__ __align__(128) unsigned char smem[];
   float* stA = reinterpret_cast<float*>(smem);                      // [kStages][CH*R*R]
@@ -216,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) dot_r16_kernel(const __g
   const int N = args.a.n, J = args.a.m[0].J;
   const int nch = (J + CH - 1) / CH;
   const int64_t B = args.a.batch;
-  const bool same = args.norm != 0;
+  constexpr bool same = SAME;  // norm: A == B (one operand streamed)
 
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -304,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) dot_r16_kernel(const __g
             lastacc = fmaf(a0, y0, lastacc);
             lastacc = fmaf(a1, y1, lastacc);
           } else if (MMA) {
-            slice_mma(A + jj * R * R, Bm + jj * R * R, Mh, Ml, Mw, fg, ft);
+            slice_mma<SAME>(A + jj * R * R, Bm + jj * R * R, Mh, Ml, Mw, fg, ft);
           } else if (jj < kWarps) {
             // two slices per warp (jj, jj + kWarps): 8 independent FFMA2 chains
             const int j2 = jj + kWarps;
@@ -460,7 +471,8 @@ int launch_dot_fast(const ChainDev& a, const ChainDev& b, float* out, bool is_no
   args.norm = is_norm ? 1 : 0;
   const size_t smem = dot_smem(is_norm);
   const char* e = getenv("TNB_DOT_SIMT");
-  auto kern = (e && e[0] == '1') ? dot_r16_kernel<false> : dot_r16_kernel<true>;
+  auto kern = (e && e[0] == '1') ? (is_norm ? dot_r16_kernel<false, true> : dot_r16_kernel<false, false>)
+                                 : (is_norm ? dot_r16_kernel<true, true> : dot_r16_kernel<true, false>);
   int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                       "dot smem attr");
   if (rc) return rc;
