@@ -102,7 +102,7 @@
 #define TNB_STREAM_NREC 2
 #endif
 #ifndef TNB_STREAM_PF
-#define TNB_STREAM_PF 2
+#define TNB_STREAM_PF 1
 #endif
 
 namespace tnb {
@@ -1188,8 +1188,14 @@ __global__ void __launch_bounds__(NT, kStateCtas)
 //     and a lane group evaluates a whole sample: w = v G on its columns,
 //     times the diagonal rows and the last row on those columns (direct L2
 //     loads), reduced over the group -> out[s].
-constexpr int kSC = 16;  // rows per ring chunk
-constexpr int kSD = 4;   // chunks per warp ring (ring row = sequence number & 63)
+#ifndef TNB_STREAM_SC
+#define TNB_STREAM_SC 32
+#endif
+#ifndef TNB_STREAM_SD
+#define TNB_STREAM_SD 2
+#endif
+constexpr int kSC = TNB_STREAM_SC;  // rows per ring chunk (16 or 32)
+constexpr int kSD = TNB_STREAM_SD;  // chunks per warp ring (power of two; ring row = sequence number % (kSC kSD))
 
 __device__ __forceinline__ bool mb_test(uint64_t* b, uint32_t parity) {
   uint32_t ok;
@@ -1339,6 +1345,7 @@ __global__ void __launch_bounds__(NT, 1)
         const uint32_t j = reinterpret_cast<const uint32_t*>(rec + bp.off_wide)[s];
         const float* a = ftab + (int64_t)j * R + (lane >= kSC ? R - 1 : 0);  // first and last line of the row
         asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+        if (kSC == 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(a + R - 1));
       }
     }
 #endif
