@@ -74,6 +74,9 @@
 #ifndef TNB_FFIRST_RING
 #define TNB_FFIRST_RING 1
 #endif
+#ifndef TNB_FRING_G
+#define TNB_FRING_G 16
+#endif
 #ifndef TNB_FRING_D
 #define TNB_FRING_D 3
 #endif
@@ -859,16 +862,17 @@ __global__ void __launch_bounds__(NT, kStateCtas)
           // which mode 1 then reads as A fragments and overwrites in place --
           // no CTA-wide gather barrier and no exposed load latency per step
           const bool fring = TNB_FFIRST_RING && ffirst && k == 1;
+          constexpr int kFringG = TNB_FRING_G;  // positions per cp.async group (16 or 32)
           int g_issued = 0;
           auto issue_group = [&]() {
-            const int base = lo + 16 * g_issued;
-            const int rows = min(16, hi - base);
+            const int base = lo + kFringG * g_issued;
+            const int rows = min(kFringG, hi - base);
             if (rows > 0) {
               const uint32_t jr = lane < rows ? (bp.wide0 ? widx0[perm[base + lane]] : (uint32_t)cidx[perm[base + lane]])
                                               : 0u;
               const uint32_t sr = lane < rows ? (uint32_t)perm[base + lane] : 0u;
 #pragma unroll
-              for (int it = 0; it < 4; ++it) {  // 16 rows x 8 pieces of 16 bytes
+              for (int it = 0; it < kFringG / 4; ++it) {  // kFringG rows x 8 pieces of 16 bytes
                 const int i = lane + 32 * it;
                 const int row = i >> 3, piece = i & 7;
                 const uint32_t j = __shfl_sync(0xffffffffu, jr, row);
@@ -913,7 +917,7 @@ __global__ void __launch_bounds__(NT, kStateCtas)
             while (p < bend) {
               const int n = min(16, bend - p);
               if (fring) {  // the groups holding positions p .. p + n - 1 have landed
-                const int gneed = (p + n - 1 - lo) >> 4;
+                const int gneed = (p + n - 1 - lo) / kFringG;
                 const int newer = g_issued - 1 - gneed;
                 if (newer >= 3) asm volatile("cp.async.wait_group 3;" ::: "memory");
                 else if (newer == 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
@@ -996,7 +1000,7 @@ __global__ void __launch_bounds__(NT, kStateCtas)
               }
               p += n;
               if (fring)  // groups wholly consumed -> the next ones
-                while (g_issued < ((p - lo) >> 4) + kFringD && lo + 16 * g_issued < hi) issue_group();
+                while (g_issued < (p - lo) / kFringG + kFringD && lo + kFringG * g_issued < hi) issue_group();
             }
           }
           if (fring) asm volatile("cp.async.wait_group 0;" ::: "memory");
