@@ -112,6 +112,9 @@ namespace tnb {
 namespace {
 
 constexpr int kMaxJ = 1024;          // bucket count limit for sorted modes
+#ifndef TNB_PREP_ILP2
+#define TNB_PREP_ILP2 1
+#endif
 #ifndef TNB_PREP_THREADS
 #define TNB_PREP_THREADS 512
 #endif
@@ -389,6 +392,55 @@ __global__ void __launch_bounds__(kPrepThreads, PSORT ? 1024 / kPrepThreads : 15
     const int N0 = bp.n0;
     const int64_t* src = idx + s0 * N0;
     const bool v2 = (N0 & 1) == 0 && (reinterpret_cast<uintptr_t>(idx) & 15) == 0;
+#if TNB_PREP_ILP2
+    // the sorting instance has registers to spare: rows of 8 indices (cfg5)
+    // go two per thread, all eight 16-byte loads issued before either row is
+    // combined
+    if (PSORT && v2 && N0 == 8) {
+      auto comb = [&](int s, const longlong2 (&r)[4]) {
+        int vk = 0;
+        uint32_t cur = 0;
+        auto put = [&](int o, int64_t raw) {
+          const int32_t J = bp.oJ[o];
+          const uint32_t v = (uint32_t)norm_index(raw, J, o, err);
+          const int tk = bp.vmap[o];
+          if (tk != vk) {
+            if (vk == 0 && bp.wide0) widx[s] = cur;
+            else if (vk == N - 1 && bp.wideL) widx[(size_t)bp.wide0 * T + s] = cur;
+            else idxs[(size_t)(vk - bp.crow0) * T + s] = (IdxT)cur;
+            vk = tk;
+            cur = 0;
+          }
+          cur = cur * (uint32_t)J + v;
+        };
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          put(2 * q, r[q].x);
+          put(2 * q + 1, r[q].y);
+        }
+        if (vk == 0 && bp.wide0) widx[s] = cur;
+        else if (vk == N - 1 && bp.wideL) widx[(size_t)bp.wide0 * T + s] = cur;
+        else idxs[(size_t)(vk - bp.crow0) * T + s] = (IdxT)cur;
+      };
+      for (int s = tid; s < tn; s += 2 * NT) {
+        const int sb = s + NT;
+        const bool hb = sb < tn;
+        const longlong2* ra = reinterpret_cast<const longlong2*>(src + (int64_t)s * 8);
+        const longlong2* rb = reinterpret_cast<const longlong2*>(src + (int64_t)(hb ? sb : s) * 8);
+        longlong2 a[4], b[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) a[q] = __ldg(ra + q);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) b[q] = __ldg(rb + q);
+        comb(s, a);
+        if (hb) comb(sb, b);
+      }
+      for (int s = tn + tid; s < T; s += NT) {  // tail rows: index 0
+        for (int k = 0; k < bp.ncrow; ++k) idxs[(size_t)k * T + s] = (IdxT)0;
+        for (int w = 0; w < bp.nw; ++w) widx[(size_t)w * T + s] = 0u;
+      }
+    } else
+#endif
     for (int s = tid; s < T; s += NT) {
       const int64_t* row = src + (int64_t)s * N0;
       if (s >= tn) {
