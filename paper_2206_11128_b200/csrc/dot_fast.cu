@@ -4,8 +4,9 @@
 // Reference: chain_dot (core.py:362-384) propagates an r_a x r_b transfer
 // matrix M mode by mode, M' = sum_j A_j^T M B_j, as numpy's einsum path
 // "xaic,xab->bcix" then "bcix,xbid->xcd".  Here:
-//   * one CTA per pair at a time (persistent, 4 CTAs per SM, 4 warps: measured
-//     against 8 and 2 warps per pair, 1.45 vs 1.55 / 1.63 ms at cfg4);
+//   * one CTA per pair at a time (persistent, 4 CTAs per SM, 4 compute warps:
+//     measured against 8 and 2 warps per pair, 1.45 vs 1.55 / 1.63 ms at cfg4)
+//     plus a producer warp that streams the chunks (1.44 ms);
 //   * core slices stream HBM -> shared memory with cp.async.bulk (TMA bulk
 //     copies) in chunks of 8 slices (8 KB per operand), double buffered
 //     behind an mbarrier full/empty pipeline -- each byte is read once;
@@ -30,7 +31,13 @@ namespace {
 #define TNB_DOT_CH 8
 #endif
 constexpr int kWarps = TNB_DOT_WARPS;
-constexpr int kThreads = kWarps * 32;
+// TNB_DOT_PRODUCER: one extra warp streams the chunks (thread 0 of the
+// compute warps no longer blocks on the slowest warp to refill a stage)
+#ifndef TNB_DOT_PRODUCER
+#define TNB_DOT_PRODUCER 1
+#endif
+constexpr int kCompute = kWarps * 32;                           // compute threads
+constexpr int kThreads = kCompute + (TNB_DOT_PRODUCER ? 32 : 0);
 constexpr int kCtasPerSm = 16 / kWarps;
 constexpr int R = 16;
 constexpr int CH = TNB_DOT_CH;         // slices per chunk
@@ -222,6 +229,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) dot_r16_kernel(const __g
   uint64_t* empty = bars + kStages;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // barrier of the compute warps only (the producer warp never joins)
+  auto csync = [&]() {
+    if (TNB_DOT_PRODUCER) asm volatile("bar.sync 1, %0;" ::"n"(kCompute) : "memory");
+    else __syncthreads();
+  };
   const int ap = lane >> 2, dq = lane & 3;  // rows/cols 2ap,2ap+1 ; 4dq..4dq+3
   const int fg = lane >> 2, ft = lane & 3;  // mma fragment coordinates (MMA path)
   const int N = args.a.n, J = args.a.m[0].J;
@@ -263,8 +275,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) dot_r16_kernel(const __g
       }
     }
   };
-  if (tid == 0)
+  if (TNB_DOT_PRODUCER) {
+    if (warp == kWarps) {  // the producer warp: every chunk of this CTA, in order
+      if (lane == 0)
+        while (pw.e < B) produce_one();
+      return;
+    }
+  } else if (tid == 0) {
     for (int s = 0; s < kStages; ++s) produce_one();
+  }
 
   uint32_t c_it = 0;
   for (int64_t e = blockIdx.x; e < B; e += gridDim.x) {
@@ -370,20 +389,20 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) dot_r16_kernel(const __g
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         ++c_it;
-        if (tid == 0) produce_one();
+        if (!TNB_DOT_PRODUCER && tid == 0) produce_one();
       }
       // ---- reduce the per-warp partial M over warps ----
       if (last) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) lastacc += __shfl_xor_sync(0xffffffffu, lastacc, o);
         if (lane == 0) red[warp] = lastacc;
-        __syncthreads();
+        csync();
         if (tid == 0) {
           float v = 0.f;
           for (int w = 0; w < kWarps; ++w) v += red[w];
           args.out[e] = args.norm ? sqrtf(fmaxf(v, 0.f)) : v;
         }
-        __syncthreads();
+        csync();
       } else {
         float* rw = red + warp * R * R;
         if (MMA && !first) {
@@ -406,14 +425,14 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) dot_r16_kernel(const __g
           x3 += z3;
           *reinterpret_cast<float4*>(rw + (2 * ap + i) * R + dq * 4) = make_float4(x0, x1, x2, x3);
         }
-        __syncthreads();
-        for (int e = tid; e < R * R; e += kThreads) {
+        csync();
+        for (int e = tid; e < R * R; e += kCompute) {
           float v = 0.f;
 #pragma unroll
           for (int w = 0; w < kWarps; ++w) v += red[w * R * R + e];
           msm[e] = v;
         }
-        __syncthreads();
+        csync();
         if (MMA) {
 #pragma unroll
           for (int nt = 0; nt < 2; ++nt) {
