@@ -104,6 +104,10 @@
 #ifndef TNB_STREAM_NREC
 #define TNB_STREAM_NREC 2
 #endif
+// XOR-swizzled (unpadded) ring rows at R = 24
+#ifndef TNB_STREAM_SWZ
+#define TNB_STREAM_SWZ 1
+#endif
 #ifndef TNB_STREAM_PF
 #define TNB_STREAM_PF 1
 #endif
@@ -1280,7 +1284,11 @@ __global__ void __launch_bounds__(NT, 1)
   constexpr int NW = NT / 32;
   constexpr int RING = kSC * kSD;
   constexpr int C1 = (C == 3) ? 1 : 0;
-  constexpr int RS = MMA ? R + 4 : R;  // ring row stride (floats): conflict-free A-fragment loads
+  // ring row stride (floats): R + 4 makes the A-fragment loads conflict-free;
+  // at R = 24 an XOR swizzle of the 16-byte pieces does the same without the
+  // padding (piece p of ring row q stored at p ^ ((q >> 2) & 1))
+  constexpr bool SWZ = MMA && R == 24 && TNB_STREAM_SWZ;
+  constexpr int RS = MMA ? (SWZ ? R : R + 4) : R;
   constexpr int KT = R / 8;            // MMA k- and n-tiles
   extern __shared__ __align__(128) unsigned char smem[];
   const int N = ch.n, T = bp.T;
@@ -1377,7 +1385,8 @@ __global__ void __launch_bounds__(NT, 1)
         const int row = i / (R / 4), piece = i - row * (R / 4);
         const uint32_t j = __shfl_sync(0xffffffffu, jr, row & 31);
         if (row < n)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst0 + (uint32_t)(row * RS * 4 + piece * 16)),
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst0 + (uint32_t)(row * RS * 4 +
+                                                                               (SWZ ? piece ^ (((slot * kSC + row) >> 2) & 1) : piece) * 16)),
                        "l"(ftab + (int64_t)j * R + piece * 4)
                        : "memory");
       }
@@ -1548,13 +1557,15 @@ __global__ void __launch_bounds__(NT, 1)
           // rows g, g + 8 of the step = sorted positions p + g, p + g + 8
           // (clamped into the bucket: padding rows recompute a real sample)
           int sr[2];
-          uint32_t vr[2];
+          uint32_t vr[2], vb16[2];
           float2 dcl[2][KT];
 #pragma unroll
           for (int r = 0; r < 2; ++r) {
             const int pos = p + min(mg + 8 * r, n - 1);
             sr[r] = perm[pos];
-            vr[r] = s_ring + ((sbase + (uint32_t)pos) % RING) * (RS * 4) + mt * 4;
+            const uint32_t q = (sbase + (uint32_t)pos) % RING;
+            vr[r] = s_ring + q * (RS * 4) + mt * 4;
+            vb16[r] = SWZ ? ((q >> 2) & 1) * 16 : 0;
 #pragma unroll
             for (int nt = 0; nt < KT; ++nt) {
               dcl[r][nt] = mlp[r][nt];
@@ -1571,10 +1582,10 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
           for (int kt = 0; kt < KT; ++kt) {
             uint32_t ah[4], al[4];
-            split_tf32_fast(lds32(vr[0] + kt * 32), ah[0], al[0]);
-            split_tf32_fast(lds32(vr[1] + kt * 32), ah[1], al[1]);
-            split_tf32_fast(lds32(vr[0] + kt * 32 + 16), ah[2], al[2]);
-            split_tf32_fast(lds32(vr[1] + kt * 32 + 16), ah[3], al[3]);
+            split_tf32_fast(lds32(vr[0] + kt * 32 + vb16[0]), ah[0], al[0]);
+            split_tf32_fast(lds32(vr[1] + kt * 32 + vb16[1]), ah[1], al[1]);
+            split_tf32_fast(lds32(vr[0] + kt * 32 + 16 - vb16[0]), ah[2], al[2]);
+            split_tf32_fast(lds32(vr[1] + kt * 32 + 16 - vb16[1]), ah[3], al[3]);
 #pragma unroll
             for (int nt = 0; nt < KT; ++nt) {
               mma_tf32(acc[nt], al, bh[kt][nt][0], bh[kt][nt][1]);
@@ -2333,7 +2344,7 @@ bool stream_shape_ok(const ChainDev& v, int R) {
 constexpr int kStreamThreads = TNB_STREAM_THREADS;
 constexpr bool kStreamMma = TNB_STREAM_MMA != 0;
 size_t stream_smem(const BPlan& bp, int R) {
-  const int rs = kStreamMma ? R + 4 : R;
+  const int rs = kStreamMma ? ((R == 24 && TNB_STREAM_SWZ) ? R : R + 4) : R;
   return TNB_STREAM_NREC * (size_t)bp.tile_bytes + (size_t)(kStreamThreads / 32) * kSD * kSC * rs * 4 + 128 +
          (size_t)(TNB_STREAM_NREC + (kStreamThreads / 32) * kSD) * 8 + 4 * TNB_STREAM_NREC + 16;
 }

@@ -199,7 +199,7 @@ def test_entries_plan_merges_cfg2_and_cfg5(lib, monkeypatch):
     assert info5["kernel_flops"] == (2 * 24 * 24 + 24 + 2 * 24) * float(1 << 26)
     # one sorted mode left: the stream kernel (4096-sample tiles); cfg2 keeps
     # the state kernel (two sorted modes)
-    assert (info5["compute_kernel"], info5["tile"]) == (1, 5632)
+    assert (info5["compute_kernel"], info5["tile"]) == (1, 6144)
     assert N.entries_plan(_chain(specs), 1 << 24)["compute_kernel"] == 0
     monkeypatch.setenv("TNB_ENTRIES_STREAM", "0")
     assert N.entries_plan(_chain(specs5), 1 << 26)["compute_kernel"] == 0
