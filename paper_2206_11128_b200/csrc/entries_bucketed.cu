@@ -108,6 +108,10 @@
 #ifndef TNB_STREAM_SWZ
 #define TNB_STREAM_SWZ 1
 #endif
+// stream plans: sorted-mode index packed into the first mode's uint32
+#ifndef TNB_STREAM_KPACK
+#define TNB_STREAM_KPACK 1
+#endif
 #ifndef TNB_STREAM_PF
 #define TNB_STREAM_PF 1
 #endif
@@ -309,6 +313,9 @@ struct BPlan {
   int crow0, ncrow;
   int psort;   // the prep kernel sorts (TNB_SORT_IN_PREP)
   int splits;  // balanced warp ranges are written after the bucket starts (state kernel)
+  // stream plans: the sorted mode's index is packed above the first mode's
+  // (uint32, bits kshift..) and its compact row dropped from the record
+  int kpack, kshift;
   int8_t slot[kMaxModes];  // mode -> sorted slot or -1
   // mode merging: the kernels run a VIRTUAL chain whose first / last modes
   // may be prefix / suffix tables over several original modes; the prep
@@ -484,10 +491,15 @@ __global__ void __launch_bounds__(kPrepThreads, PSORT ? 1024 / kPrepThreads : 15
   }
   __syncthreads();
   const size_t cbytes = (size_t)bp.ncrow * T * sizeof(IdxT) + (size_t)bp.nw * T * 4;
-  {  // compact block (+ wide rows) -> record (16-byte stores)
-    const int n16 = (int)(cbytes / 16);
-    for (int i = tid; i < n16; i += NT)
-      reinterpret_cast<uint4*>(rec)[i] = reinterpret_cast<const uint4*>(idxs)[i];
+  if (bp.kpack) {  // the sorted mode's index above the first mode's
+    for (int s = tid; s < T; s += NT) widx[s] |= (uint32_t)idxs[s] << bp.kshift;
+    __syncthreads();
+  }
+  {  // compact block (+ wide rows) -> record (16-byte stores), minus a packed row
+    const size_t skip = bp.kpack ? (size_t)T * sizeof(IdxT) : 0;
+    const int n16 = (int)((cbytes - skip) / 16);
+    const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const unsigned char*>(idxs) + skip);
+    for (int i = tid; i < n16; i += NT) reinterpret_cast<uint4*>(rec)[i] = src[i];
   }
   // counting sort of each sorted slot: histogram (shared atomics), warp-0
   // scan into the bucket starts, scatter into a staged permutation, 16-byte
@@ -1379,11 +1391,12 @@ __global__ void __launch_bounds__(NT, 1)
                                          reinterpret_cast<const uint16_t*>(rec + bp.off_perm)[plo + pcc * kSC + lane]]
                                    : 0u;
       const uint32_t dst0 = s_ring + (uint32_t)(slot * kSC * RS * 4);
+      const uint32_t kmask = bp.kpack ? (1u << bp.kshift) - 1u : ~0u;
 #pragma unroll
       for (int it = 0; it < (kSC * R / 4 + 31) / 32; ++it) {
         const int i = lane + 32 * it;
         const int row = i / (R / 4), piece = i - row * (R / 4);
-        const uint32_t j = __shfl_sync(0xffffffffu, jr, row & 31);
+        const uint32_t j = __shfl_sync(0xffffffffu, jr, row & 31) & kmask;
         if (row < n)
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst0 + (uint32_t)(row * RS * 4 +
                                                                                (SWZ ? piece ^ (((slot * kSC + row) >> 2) & 1) : piece) * 16)),
@@ -1407,7 +1420,7 @@ __global__ void __launch_bounds__(NT, 1)
       const int pf = plo + (pcc + TNB_STREAM_PF) * kSC + (lane & (kSC - 1));
       if (pf < phi) {
         const int s = reinterpret_cast<const uint16_t*>(rec + bp.off_perm)[pf];
-        const uint32_t j = reinterpret_cast<const uint32_t*>(rec + bp.off_wide)[s];
+        const uint32_t j = reinterpret_cast<const uint32_t*>(rec + bp.off_wide)[s] & (bp.kpack ? (1u << bp.kshift) - 1u : ~0u);
         const float* a = ftab + (int64_t)j * R + (lane >= kSC ? R - 1 : 0);  // first and last line of the row
         asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
         if (kSC == 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(a + R - 1));
@@ -1429,9 +1442,11 @@ __global__ void __launch_bounds__(NT, 1)
     // compact rows start at mode 1 (crow0 == 1): sorted mode 1, diagonal
     // mode 2, then the last mode unless it is wide (uint32 row after the
     // first mode's)
+    const int rfirst = 1 + bp.kpack;  // first mode with a compact row in the record
     const IdxT* ckey = reinterpret_cast<const IdxT*>(rec);
-    const IdxT* cdiag = reinterpret_cast<const IdxT*>(rec) + (size_t)T;
-    const IdxT* clastc = reinterpret_cast<const IdxT*>(rec) + (size_t)(N - 2) * T;
+    const uint32_t* cfirst = reinterpret_cast<const uint32_t*>(rec + bp.off_wide);
+    const IdxT* cdiag = reinterpret_cast<const IdxT*>(rec) + (size_t)(2 - rfirst) * T;
+    const IdxT* clastc = reinterpret_cast<const IdxT*>(rec) + (size_t)(N - 1 - rfirst) * T;
     const uint32_t* clastw = reinterpret_cast<const uint32_t*>(rec + bp.off_wide) + (size_t)T;
     const bool wl = bp.wideL != 0;
     const uint16_t* perm = reinterpret_cast<const uint16_t*>(rec + bp.off_perm);
@@ -1483,7 +1498,7 @@ __global__ void __launch_bounds__(NT, 1)
     }
     int p = lo;
     while (p < hi) {
-      const int key = ckey[perm[p]];
+      const int key = bp.kpack ? (int)(cfirst[perm[p]] >> bp.kshift) : (int)ckey[perm[p]];
       const int bend = min((int)st[key + 1], hi);
       uint64_t g2[MMA ? 1 : R];
       float g1[(C1 && !MMA) ? R : 1];
@@ -2313,7 +2328,15 @@ int make_bplan(const ChainDev& ch, int64_t m, BPlan* bp, int* R_out, int* nt_out
   bp->ntiles = (m + T - 1) / T;
   // [N][T] compact rows, [nw][T] uint32 wide rows (contiguous: N*T*idx_bytes
   // is a multiple of 32), then the sorted slots
-  bp->off_wide = (int64_t)bp->ncrow * T * idx_bytes;
+  {
+    int ks = 0;
+    while ((1LL << ks) < ch.m[0].J) ++ks;
+    int kb = 0;
+    while (nsort == 1 && (1LL << kb) < ch.m[bp->smode[0]].J) ++kb;
+    bp->kshift = ks;
+    bp->kpack = stream && TNB_STREAM_KPACK && bp->psort && nsort == 1 && bp->smode[0] == 1 && ks + kb <= 32;
+  }
+  bp->off_wide = (int64_t)(bp->ncrow - bp->kpack) * T * idx_bytes;
   const int64_t cidx_b = bp->off_wide + (int64_t)bp->nw * T * 4;
   bp->off_perm = cidx_b;
   bp->off_starts = cidx_b + (int64_t)nsort * T * 2;
