@@ -509,3 +509,25 @@ def test_bucketed_stream_kernel_small_m(m, three):
     idx = O.uniform_indices(t.shape, m, 5)
     got = tb.entries(t, idx, algo=N.ALGO_BUCKETED)
     assert_close(got, O.entries(o, idx), what=f"stream m={m} plan={plan}")
+
+
+def test_bucketed_stream_kernel_few_buckets():
+    # one sorted mode with only 40 buckets: the separate sort kernel (no sort
+    # in prep) and a record that keeps the sorted mode's compact row (no key
+    # packing) feed the stream kernel
+    rng = np.random.default_rng(40)
+    r = 24
+    s_ = r ** -0.5
+    nodes = [("tt", rng.standard_normal((1, 20000, r)).astype(np.float32), None),
+             ("tt", (rng.standard_normal((r, 40, r)) * s_).astype(np.float32), None),
+             ("tt", (rng.standard_normal((r, 5000, 1)) * s_).astype(np.float32), None)]
+    t = facade(nodes)
+    o = O.make_chain(nodes)
+    m = 300001
+    plan = N.entries_plan(t._packed().chain, m, N.ALGO_AUTO)
+    assert (plan["compute_kernel"], plan["n_virtual"]) == (1, 3), plan
+    idx = O.uniform_indices(t.shape, m, 6)
+    idx[::5] -= np.asarray(t.shape)
+    got = to_np(tb.entries(t, idx))
+    sel = np.concatenate([np.arange(0, 3000), np.arange(m - 3000, m), np.arange(3000, m - 3000, 17)])
+    assert_close(got[sel], O.entries(o, idx[sel]), what="stream few buckets")
