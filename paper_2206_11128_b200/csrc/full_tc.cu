@@ -32,17 +32,32 @@ namespace {
 constexpr int kThreads = 384;
 constexpr int BMT = 128;       // L rows per tile (UMMA N)
 constexpr int BNB = 128;       // R columns per n-block (UMMA M)
-constexpr int NB = 2;          // resident n-blocks per column block
+// TNB_FULL_NB3: 3 resident n-blocks (384 columns) and ONE accumulator,
+// released as soon as the epilogue has it in registers: each L tile then
+// serves 384 output columns instead of 256 (L2 reads of L: 2 -> 1.33 B per
+// output element)
+#ifndef TNB_FULL_NB3
+#define TNB_FULL_NB3 1  /* measured: 3.66-3.73 vs 3.71-3.82 ms (NB 2, two accumulators) at cfg3 */
+#endif
+constexpr int NB = TNB_FULL_NB3 ? 3 : 2;  // resident n-blocks per column block
+constexpr int kAccBufs = TNB_FULL_NB3 ? 1 : 2;
 constexpr int KMAX = 64;       // max contraction length
 constexpr int kTileBytes = 2 * 2 * BMT * 128;  // {hi,lo} x 2 K-blocks x 128 rows x 128 B = 64 KB
-constexpr int kStages = 3;
+// TNB_FULL_BULK (with NB3): the epilogue stages 64-row halves of each tile
+// in shared memory and writes them with 512-byte cp.async.bulk stores (one
+// per output row segment) instead of 128-byte st.global per warp
+#ifndef TNB_FULL_BULK
+#define TNB_FULL_BULK 0  /* measured: 5.18 vs 3.66 ms at cfg3 */
+#endif
+constexpr int kStages = TNB_FULL_BULK ? 2 : 3;
+static_assert(!TNB_FULL_BULK || TNB_FULL_NB3, "TNB_FULL_BULK needs TNB_FULL_NB3");
 // epilogue: 1 = each warp transposes a 32 x 32 block through shared memory
 // and writes 16-byte vectors (4 rows x 128 B per store instruction);
 // 0 = one 128-byte row segment per st.global (thread = output column)
 #ifndef TNB_FULL_V4
 #define TNB_FULL_V4 0  /* measured: 3.80 vs 3.73 ms at cfg3 */
 #endif
-constexpr int kEpiBytes = TNB_FULL_V4 ? 4 * 32 * 32 * 4 : 0;
+constexpr int kEpiBytes = TNB_FULL_BULK ? 2 * 64 * 128 * 4 : TNB_FULL_V4 ? 4 * 32 * 32 * 4 : 0;
 constexpr uint32_t kTmemCols = 512;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -208,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
   float* sEpi = reinterpret_cast<float*>(smem + kStages * kTileBytes);  // [4 warps][32][32]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kTileBytes + kEpiBytes);
   uint64_t* full = bars + 0;        // [kStages] tx
-  uint64_t* empty = bars + 3;       // [kStages] tcgen05.commit
+  uint64_t* empty = bars + 3;       // [kStages] tcgen05.commit (kStages <= 3)
   uint64_t* acc_full = bars + 6;    // [2] tcgen05.commit
   uint64_t* acc_empty = bars + 8;   // [2] 128 epilogue threads
   uint64_t* mma_idle = bars + 10;   // tcgen05.commit before an A reload
@@ -244,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tm_acc0 = tmem, tm_a0 = tmem + 2 * BMT;  // acc b at +b*128; A nb at +nb*128
+  const uint32_t tm_acc0 = tmem, tm_a0 = tmem + kAccBufs * BMT;  // acc b at +b*128; A nb at +nb*128
 
   if (warp == 0) {
     // ================= MMA issuer =================
@@ -272,8 +287,8 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
       tc_fence_after();
       const uint32_t bhi = sL0 + s * kTileBytes, blo = bhi + kTileBytes / 2;
       for (int nb = 0; nb < NB; ++nb) {
-        const int cbuf = s_it & 1;
-        mbar_wait(&acc_empty[cbuf], ((s_it >> 1) & 1) ^ 1);
+        const int cbuf = s_it % kAccBufs;
+        mbar_wait(&acc_empty[cbuf], ((s_it / kAccBufs) & 1) ^ 1);
         tc_fence_after();
         if (lane == 0) {
           const uint32_t d = tm_acc0 + cbuf * BMT;
@@ -316,13 +331,74 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
     const int q = warp & 3;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     uint32_t s_it = 0;
+    uint32_t bulk_it = 0;
+    (void)bulk_it;
     for (int64_t t = t0; t < t1; ++t) {
       const int64_t cb = t / n_mt, mt = t - cb * n_mt;
       for (int nb = 0; nb < NB; ++nb) {
-        const int cbuf = s_it & 1;
-        mbar_wait(&acc_full[cbuf], (s_it >> 1) & 1);
+        const int cbuf = s_it % kAccBufs;
+        mbar_wait(&acc_full[cbuf], (s_it / kAccBufs) & 1);
         tc_fence_after();
         const int64_t col = cb * NB * BNB + nb * BNB + q * 32 + lane;
+#if TNB_FULL_NB3
+        {
+          // whole 128-row accumulator column into registers, release it, store
+          const bool cok = col < N;
+          const int64_t rows_left = M - mt * BMT;
+          const int64_t ldc = args.ldc;
+          float* p = args.C + (mt * BMT) * ldc + col;
+          uint32_t v[BMT];
+#pragma unroll
+          for (int ch = 0; ch < BMT / 32; ++ch) TMEM_LD32(tm_acc0 + lane_base + ch * 32, (v + ch * 32));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          tc_fence_before();
+          mbar_arrive(&acc_empty[cbuf]);
+          ++s_it;
+#if TNB_FULL_BULK
+          {
+            const int64_t c0 = cb * NB * BNB + nb * BNB;  // first column of this n-block
+            const bool bulk_ok = rows_left >= BMT && c0 + BNB <= N && (ldc & 3) == 0 &&
+                                 (reinterpret_cast<uintptr_t>(args.C) & 15) == 0;
+            if (bulk_ok) {  // uniform over the 4 epilogue warps
+              const int e = tid - 128;  // 0..127; 0..63 issue the row stores
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                float* sb = sEpi + (size_t)(bulk_it & 1) * (64 * 128);
+                if (e < 64) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                named_sync(3, 128);
+#pragma unroll
+                for (int j = 0; j < 64; ++j) sb[j * 128 + q * 32 + lane] = __uint_as_float(v[h * 64 + j]);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                named_sync(3, 128);
+                if (e < 64) {
+                  float* dst = args.C + (mt * BMT + h * 64 + e) * ldc + c0;
+                  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 512;" ::"l"(dst),
+                               "r"(smem_u32(sb + e * 128))
+                               : "memory");
+                  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+                ++bulk_it;
+              }
+              continue;
+            }
+          }
+#endif
+          if (cok && rows_left >= BMT) {
+#pragma unroll
+            for (int j = 0; j < BMT; ++j) {
+              st_stream(p, v[j]);
+              p += ldc;
+            }
+          } else if (cok) {
+#pragma unroll
+            for (int j = 0; j < BMT; ++j) {
+              if (j < rows_left) st_stream(p, v[j]);
+              p += ldc;
+            }
+          }
+          continue;
+        }
+#endif
         const bool cok = col < N;
         const int64_t rows_left = M - mt * BMT;
         const bool full_rows = rows_left >= BMT;
@@ -373,6 +449,9 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
         ++s_it;
       }
     }
+#if TNB_FULL_BULK
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+#endif
   } else if (warp >= 8) {
     // ================= resident A: R^T block -> hi/lo -> TMEM =================
     const int q = warp & 3;
