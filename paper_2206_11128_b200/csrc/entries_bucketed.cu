@@ -1867,11 +1867,20 @@ __global__ void __launch_bounds__(256) table_gemm(ModeDev md, const float* __res
 // and walks the 8 row tiles of 16.  Large levels (cfg2: 2^20-row tables)
 // are write-bound instead of FFMA-bound.
 constexpr int kTcRows = 128, kTcZ = 8;
+// TNB_TABLE_STAGE: each 16-row tile of the CTA's 8 slices goes through
+// shared memory and leaves as float4 runs (1 KB per prefix row, 2 KB per
+// suffix slice) instead of 32-byte float2 pieces from the fragments
+#ifndef TNB_TABLE_STAGE
+#define TNB_TABLE_STAGE 0  /* measured: tables 0.187 vs 0.168 ms (serial, cfg2) */
+#endif
 template <int KT, int NTL, bool SUFFIX>
 __global__ void __launch_bounds__(256) table_gemm_tc(ModeDev md, const float* __restrict__ A, int64_t rows,
                                                      float* __restrict__ out) {
   constexpr int K = 8 * KT, Nn = 8 * NTL, AS = K + 4;
   __shared__ __align__(16) float As[kTcRows * AS];
+#if TNB_TABLE_STAGE
+  __shared__ __align__(16) float Os[16 * kTcZ * Nn];  // [row][slice][Nn], 8-column blocks rotated by row
+#endif
   const int J = md.J;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -1882,11 +1891,17 @@ __global__ void __launch_bounds__(256) table_gemm_tc(ModeDev md, const float* __
     As[r * AS + k] = r < nr ? __ldg(A + i0 * K + e) : 0.f;
   }
   __syncthreads();
-  const int j = blockIdx.y * kTcZ + warp;
+  const int z0 = blockIdx.y * kTcZ;
+  const int j = z0 + warp;
+#if TNB_TABLE_STAGE
+  const bool jok = j < J;  // every warp stays for the staging barriers
+#else
   if (j >= J) return;
+  constexpr bool jok = true;
+#endif
   // B(k, n) = G(j, k, n) (prefix) or G(j, n, k) (suffix); fragment (kt, nt):
   // b0 = B(8kt + t, 8nt + g), b1 = B(8kt + t + 4, 8nt + g)
-  const float* gj = md.s + (int64_t)j * md.rl * md.rr;
+  const float* gj = md.s + (int64_t)(jok ? j : 0) * md.rl * md.rr;
   uint32_t bh[KT][NTL][2], bl[KT][NTL][2];
 #pragma unroll
   for (int kt = 0; kt < KT; ++kt)
@@ -1895,7 +1910,7 @@ __global__ void __launch_bounds__(256) table_gemm_tc(ModeDev md, const float* __
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int k = 8 * kt + t + 4 * e, n = 8 * nt + g;
-        split_tf32(__ldg(gj + (SUFFIX ? n * K + k : k * Nn + n)), bh[kt][nt][e], bl[kt][nt][e]);
+        split_tf32(jok ? __ldg(gj + (SUFFIX ? n * K + k : k * Nn + n)) : 0.f, bh[kt][nt][e], bl[kt][nt][e]);
       }
   for (int mt = 0; mt < kTcRows / 16; ++mt) {
     if (mt * 16 >= nr) break;
@@ -1918,6 +1933,37 @@ __global__ void __launch_bounds__(256) table_gemm_tc(ModeDev md, const float* __
         mma_tf32(acc[nt], ah, bh[kt][nt][0], bh[kt][nt][1]);
       }
     }
+#if TNB_TABLE_STAGE
+    __syncthreads();  // the previous tile's reads of Os are done
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = g + 8 * h;
+      float* orow = Os + (r * kTcZ + warp) * Nn;
+#pragma unroll
+      for (int nt = 0; nt < NTL; ++nt)
+        *reinterpret_cast<float2*>(orow + 8 * ((nt + r) % NTL) + 2 * t) =
+            make_float2(acc[nt][2 * h], acc[nt][2 * h + 1]);
+    }
+    __syncthreads();
+    constexpr int F4 = Nn / 4;  // float4 per slice row
+    for (int f = tid; f < 16 * kTcZ * F4; f += 256) {
+      // prefix: row-major over (row, slice) -> 1 KB runs; suffix: slice-major -> 2 KB runs
+      int r, w;
+      if (SUFFIX) {
+        w = f / (16 * F4);
+        r = (f / F4) % 16;
+      } else {
+        r = f / (kTcZ * F4);
+        w = (f / F4) % kTcZ;
+      }
+      const int c4 = (f % F4) * 4;
+      if (mt * 16 + r >= nr || z0 + w >= J) continue;
+      const float4 v = *reinterpret_cast<const float4*>(Os + (r * kTcZ + w) * Nn + 8 * ((c4 / 8 + r) % NTL) + c4 % 8);
+      const int64_t i = i0 + mt * 16 + r;
+      float* dst = SUFFIX ? out + ((int64_t)(z0 + w) * rows + i) * Nn : out + (i * J + z0 + w) * Nn;
+      *reinterpret_cast<float4*>(dst + c4) = v;
+    }
+#else
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int r = mt * 16 + g + 8 * h;
@@ -1928,6 +1974,7 @@ __global__ void __launch_bounds__(256) table_gemm_tc(ModeDev md, const float* __
       for (int nt = 0; nt < NTL; ++nt)
         *reinterpret_cast<float2*>(dst + 8 * nt + 2 * t) = make_float2(acc[nt][2 * h], acc[nt][2 * h + 1]);
     }
+#endif
   }
 }
 
@@ -2571,7 +2618,15 @@ SideStream* side_stream() {
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
   SideStream& x = ss[dev];
   if (!x.s) {
-    if (cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking) != cudaSuccess ||
+    // high priority (TNB_TABLE_PRIO, default on): the block scheduler hands
+    // freed SMs to the short table kernels first, so the tables are ready
+    // before the prep / sort that fills the GPU has finished
+    int least = 0, greatest = 0;
+    const char* pe = getenv("TNB_TABLE_PRIO");
+    const bool prio = !(pe && pe[0] == '0');
+    if (!prio || cudaDeviceGetStreamPriorityRange(&least, &greatest) != cudaSuccess) greatest = 0;
+    cudaGetLastError();
+    if (cudaStreamCreateWithPriority(&x.s, cudaStreamNonBlocking, greatest) != cudaSuccess ||
         cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming) != cudaSuccess) {
       cudaGetLastError();
