@@ -23,7 +23,8 @@
  *     one thread-local side stream per device (created on first use) to build
  *     its tables concurrently with the index pass, and joins it back into the
  *     caller's stream before the per-entry kernel (TNB_TABLE_STREAM=0: no
- *     fork).
+ *     fork).  The side stream has the device's highest stream priority
+ *     (TNB_TABLE_PRIO=0: default priority).
  */
 #ifndef TNB_H_
 #define TNB_H_
