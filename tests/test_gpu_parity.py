@@ -531,3 +531,17 @@ def test_bucketed_stream_kernel_few_buckets():
     got = to_np(tb.entries(t, idx))
     sel = np.concatenate([np.arange(0, 3000), np.arange(m - 3000, m), np.arange(3000, m - 3000, 17)])
     assert_close(got[sel], O.entries(o, idx[sel]), what="stream few buckets")
+
+
+@pytest.mark.parametrize("rank,batch", [(8, None), (24, None), (64, None), (16, 2)])
+def test_full_tensor_core_gemm_ragged(rank, batch):
+    # the final L @ R of full() on the tcgen05 path (M * N >= 2^20, N >= 128,
+    # K <= 64) with neither M nor N a multiple of the 128-row tile or of the
+    # 384-column resident block: partial row tiles, a partial n-block and an
+    # n-block wholly past N (core.py:345-351)
+    shape = (40, 37, 53, 29)
+    cores = O.random_tt(shape, rank, seed=rank, batch_size=batch, scale=rank ** -0.5)
+    t = facade([("tt", c, None) for c in cores], batch)
+    o = O.make_chain([("tt", c) for c in cores], batch)
+    assert_close(tb.full(t), O.full(o), what=f"full r{rank} b{batch}")
+    assert_close(tb.full(t, lead=(3, 17)), O.full_slab(o, 3, 17), what=f"full slab r{rank} b{batch}")
