@@ -6,9 +6,10 @@
 // accumulated in fp32 in TMEM (the dropped lo*lo term is ~2^-22 relative).
 //
 // The kernel computes the TRANSPOSED product C^T = R^T L^T, so that
-//   * the operand that stays put (a 256-column block of R, i.e. 256 rows of
-//     R^T, split hi/lo) lives in TMEM as the MMA's A operand -- loaded once
-//     per column block by a helper warpgroup (tcgen05.st);
+//   * the operand that stays put (a 384-column block of R, i.e. 384 rows of
+//     R^T, split hi/lo; 256 with TNB_FULL_NB3=0) lives in TMEM as the MMA's A
+//     operand -- loaded once per column block by a helper warpgroup
+//     (tcgen05.st);
 //   * the streamed operand (128-row tiles of L) is the MMA's B operand in
 //     shared memory.  A tiny pre-pass writes L split into hi/lo AND already in
 //     the UMMA canonical K-major SWIZZLE_128B image, so one cp.async.bulk of
@@ -23,7 +24,8 @@
 //   warp 1      producer of L tiles (one lane)
 //   warps 4-7   epilogue (TMEM -> registers -> HBM)
 //   warps 8-11  resident-A loader (R^T block -> hi/lo -> TMEM)
-// TMEM: 512 columns = acc0 | acc1 | A(n-block 0) | A(n-block 1).
+// TMEM: 512 columns = acc | A(n-block 0) | A(n-block 1) | A(n-block 2)
+// (TNB_FULL_NB3=0: acc0 | acc1 | A(n-block 0) | A(n-block 1)).
 #include "common.cuh"
 
 namespace tnb {
