@@ -196,12 +196,16 @@ __global__ void full_right_step(ModeDev md, int64_t B, const T* __restrict__ in,
 // 128x128 tile, BK=8, 256 threads, 8x8 outputs per thread (two 4x4 quads per
 // axis so shared-memory reads and global stores are float4 and coalesced).
 constexpr int GBM = 128, GBN = 128, GBK = 8;
+#ifndef TNB_FULL_RIGHT_GEMM
+#define TNB_FULL_RIGHT_GEMM 1
+#endif
 template <typename T>
 __global__ void __launch_bounds__(256) gemm_kernel(const T* __restrict__ A, int64_t lda,
                                                    int64_t sA, const T* __restrict__ Bm,
                                                    int64_t ldb, int64_t sB,
                                                    T* __restrict__ C, int64_t ldc, int64_t sC,
-                                                   int64_t M, int64_t N, int K) {
+                                                   int64_t M, int64_t N, int K, int remap_rl,
+                                                   int64_t remap_J) {
   __shared__ __align__(16) T As[GBK][GBM];
   __shared__ __align__(16) T Bs[GBK][GBN];
   const int64_t e = blockIdx.z;
@@ -249,10 +253,12 @@ __global__ void __launch_bounds__(256) gemm_kernel(const T* __restrict__ A, int6
   for (int i = 0; i < 8; ++i) {
     const int64_t gm = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
     if (gm >= M) continue;
+    // remap_rl > 0: A's rows are (j, a) pairs, C's rows (a, j) (right step)
+    const int64_t om = remap_rl > 0 ? (gm % remap_rl) * remap_J + gm / remap_rl : gm;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int64_t gn = n0 + h * 64 + tx * 4;
-      T* dst = C + gm * ldc + gn;
+      T* dst = C + om * ldc + gn;
       if constexpr (std::is_same<T, float>::value) {
         if (vec && gn + 3 < N) {
           __stcs(reinterpret_cast<float4*>(dst),
@@ -303,7 +309,7 @@ int launch_gemm(const T* A, int64_t lda, int64_t sA, const T* B, int64_t ldb, in
   if (batch > 65535) return set_error(TNB_EINVAL, "gemm batch too large");
   dim3 grid((unsigned)ceil_div(N, GBN), (unsigned)ceil_div(M, GBM), (unsigned)batch);
   if (grid.y > 65535) return set_error(TNB_EINVAL, "gemm M too large");
-  gemm_kernel<T><<<grid, 256, 0, st>>>(A, lda, sA, B, ldb, sB, C, ldc, sC, M, N, K);
+  gemm_kernel<T><<<grid, 256, 0, st>>>(A, lda, sA, B, ldb, sB, C, ldc, sC, M, N, K, 0, 0);
   return check_launch("gemm");
 }
 
@@ -380,7 +386,15 @@ int full_t(const tnb_chain* c, int64_t lo, int64_t hi, T* out, void* ws, int64_t
     const ModeDev md = mode_dev(c, k);
     T* dst = rb[which ^ 1];
     const int64_t total = (int64_t)md.rl * md.J * cols * B;
-    if (total > 0)
+    const int64_t gm_rows = (int64_t)md.J * md.rl;
+    if (TNB_FULL_RIGHT_GEMM && total > 0 && md.layout == TNB_LAYOUT_DENSE && md.rr >= 8 && cols >= 64 &&
+        B <= 65535 && ceil_div(gm_rows, GBM) <= 65535) {
+      // dense right step as a GEMM over the (j, a) rows of the core: the same
+      // sequential sum over c per output, rows stored in (a, j) order
+      const dim3 grid((unsigned)ceil_div(cols, GBN), (unsigned)ceil_div(gm_rows, GBM), (unsigned)B);
+      gemm_kernel<T><<<grid, 256, 0, st>>>(reinterpret_cast<const T*>(md.s), md.rr, md.bstride, R, cols,
+                                           P.r_buf, dst, cols, P.r_buf, gm_rows, cols, md.rr, md.rl, md.J);
+    } else if (total > 0)
       full_right_step<T><<<grid_for(total), 256, 0, st>>>(md, B, R, P.r_buf, cols, dst, P.r_buf);
     rc = check_launch("full_right_step");
     if (rc) return rc;
