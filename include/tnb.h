@@ -143,6 +143,28 @@ int tnb_entries_f32(const tnb_chain* chain, const int64_t* idx, int64_t m,
                     float* out, int32_t* err_mode, int32_t algo,
                     void* workspace, int64_t workspace_bytes, void* stream);
 
+/*
+ * Index transport codec for HOST index matrices (the end-to-end path of
+ * entries: t[idx] with idx in host memory, core.py:394-416).  PCIe is the
+ * bound there (80 B per cfg2 sample), and every value of a typical index
+ * matrix fits in one byte.
+ *
+ * tnb_narrow_indices_host: HOST function.  Narrows count int64 values to
+ * int8 (width 1) or int16 (width 2) in out, using nthreads host threads
+ * (<= 0: all hardware threads).  *fits = 1 when every value lay in the
+ * narrow type's range, else 0 (out unspecified; send the int64 matrix).  A
+ * pure range check on the raw values: negative wrapping, the per-mode
+ * bounds check and the lowest-OOB-mode report stay in tnb_entries_f32, which
+ * sees exactly the caller's values after tnb_widen_indices.
+ * tnb_widen_indices: device, asynchronous on stream: out[i] = (int64) in[i];
+ * both buffers 16-byte aligned.
+ * tnb_host_threads: the hardware thread count the codec uses by default.
+ */
+int tnb_narrow_indices_host(const int64_t* idx, int64_t count, int32_t width, void* out,
+                            int32_t nthreads, int32_t* fits);
+int tnb_widen_indices(const void* in, int32_t width, int64_t count, int64_t* out, void* stream);
+int tnb_host_threads(void);
+
 /* --- K2: dense decompression  (core.py:337-359) -------------------------- */
 /*
  * Writes the C-order slab of full(t) whose leading (mode-0) index lies in

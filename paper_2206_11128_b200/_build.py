@@ -27,8 +27,12 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", 
          "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
 
 
+CXX = os.environ.get("CXX", "g++")
+CXXFLAGS = ["-O3", "-std=c++17", "-g", "-fPIC", "-pthread", "-Wall"]
+
+
 def _sources():
-    return sorted(CSRC.glob("*.cu"))
+    return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cpp"))
 
 
 def _headers():
@@ -36,11 +40,14 @@ def _headers():
 
 
 def _compile(src: Path, force: bool) -> Path:
-    obj = BUILD / (src.stem + ".o")
+    obj = BUILD / (src.stem + (".o" if src.suffix == ".cu" else ".cpp.o"))
     newest_dep = max([src.stat().st_mtime] + [h.stat().st_mtime for h in _headers()])
     if not force and obj.exists() and obj.stat().st_mtime >= newest_dep:
         return obj
-    cmd = [NVCC, *ARCH, *FLAGS, "-I", str(INCLUDE), "-I", str(CSRC), "-c", str(src), "-o", str(obj)]
+    if src.suffix == ".cpp":  # plain host code (the index transport codec)
+        cmd = [CXX, *CXXFLAGS, "-I", str(INCLUDE), "-c", str(src), "-o", str(obj)]
+    else:
+        cmd = [NVCC, *ARCH, *FLAGS, "-I", str(INCLUDE), "-I", str(CSRC), "-c", str(src), "-o", str(obj)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src.name}:\n{r.stdout}\n{r.stderr}")
@@ -55,7 +62,8 @@ def build(force: bool = False, verbose: bool = True) -> Path:
     with ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
         objs = list(ex.map(lambda s: _compile(s, force), srcs))
     if force or not LIB.exists() or LIB.stat().st_mtime < max(o.stat().st_mtime for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-cudart=static", "-o", str(LIB), *map(str, objs)]
+        cmd = [NVCC, *ARCH, "-shared", "-cudart=static", "-Xcompiler", "-pthread", "-o", str(LIB),
+               *map(str, objs)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -78,6 +78,9 @@ SIGNATURES = {
                              c_int64, c_void_p]),
     "tnb_dot_f64": (c_int, [POINTER(TnbChain), POINTER(TnbChain), c_void_p, c_void_p]),
     "tnb_norm_f64": (c_int, [POINTER(TnbChain), c_void_p, c_void_p]),
+    "tnb_narrow_indices_host": (c_int, [c_void_p, c_int64, c_int32, c_void_p, c_int32, POINTER(c_int32)]),
+    "tnb_widen_indices": (c_int, [c_void_p, c_int32, c_int64, c_void_p, c_void_p]),
+    "tnb_host_threads": (c_int, []),
     "tnb_entries_plan": (c_int, [POINTER(TnbChain), c_int64, c_int32, POINTER(TnbEntriesInfo)]),
     "tnb_timing_enable": (c_int, [c_int32]),
     "tnb_timing_read": (c_int, [c_char_p, POINTER(c_double), POINTER(c_int64)]),
@@ -148,6 +151,19 @@ def entries_plan(chain: TnbChain, m: int, algo: int = ALGO_AUTO) -> dict:
     info = TnbEntriesInfo()
     check(load().tnb_entries_plan(ctypes.byref(chain), m, algo, ctypes.byref(info)), "entries plan")
     return {f: getattr(info, f) for f, _ in TnbEntriesInfo._fields_}
+
+
+def narrow_indices(src, dst, width: int, nthreads: int = 0) -> bool:
+    """Host transport codec (tnb_narrow_indices_host): int64 host tensor
+    ``src`` -> int8/int16 host tensor ``dst`` of the same element count.
+    True when every value fit (``dst`` holds them), False otherwise.  Runs
+    on host threads with the GIL released (ctypes)."""
+    if src.numel() != dst.numel() or dst.element_size() != width:
+        raise ContractViolationError("narrow_indices: size / width mismatch")
+    fits = c_int32(0)
+    check(load().tnb_narrow_indices_host(src.data_ptr(), src.numel(), width, dst.data_ptr(), nthreads,
+                                         ctypes.byref(fits)), "narrow indices")
+    return bool(fits.value)
 
 
 def timing_enable(on: bool) -> None:

@@ -27,6 +27,7 @@ cache never goes stale.
 from __future__ import annotations
 
 import ctypes
+import os
 from typing import Iterable, Optional, Sequence
 
 import numpy as np
@@ -453,14 +454,34 @@ def _index_tensor(t: TnTensor, indices, device) -> torch.Tensor:
 _PIPELINE_ROWS = 1 << 21
 
 
+def _codec_width(t: TnTensor) -> int:
+    """Width of the index transport codec for this chain (include/tnb.h):
+    1 (int8) when every mode has <= 128 entries, 2 (int16) up to 32768, else
+    0 (no codec).  Valid indices lie in [-J, J); anything else either fails
+    the host range check (the chunk is then sent as int64) or is reported by
+    the device prep kernel exactly as without the codec."""
+    if os.environ.get("TNB_E2E_CODEC", "1") == "0":
+        return 0
+    jmax = max(t.shape)
+    return 1 if jmax <= 128 else (2 if jmax <= 32768 else 0)
+
+
 def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: int,
                        out_host: Optional[torch.Tensor] = None) -> torch.Tensor:
     """entries() for a large PINNED int64 host index matrix: chunked
     copy-stream H2D overlapped with the K1 launches on the compute stream;
     with a pinned host ``out_host`` each chunk's values are copied back on a
-    second copy stream (PCIe is full duplex) behind the next chunk's work."""
+    second copy stream (PCIe is full duplex) behind the next chunk's work.
+
+    PCIe is the bound of this path, so each chunk crosses it narrowed by the
+    index transport codec (int64 -> int8/int16 on host threads, a pure range
+    check; ``tnb_narrow_indices_host``) and is widened back on the device
+    (``tnb_widen_indices``) before the unchanged K1 launch; the host narrows
+    chunk i+1 while the GPU copies and evaluates chunk i.  A chunk with a
+    value outside the narrow range crosses as int64."""
     dev = p.device
     m = int(idx_host.shape[0])
+    n = t.ndim
     chunk = _PIPELINE_ROWS
     nch = (m + chunk - 1) // chunk
     # every launch sees exactly `chunk` rows (the short last chunk is padded
@@ -469,9 +490,16 @@ def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: in
     comp = torch.cuda.current_stream(dev)
     copy = torch.cuda.Stream(dev)
     errs = torch.empty(nch, dtype=torch.int32, device=dev)
-    bufs = [torch.empty((chunk, t.ndim), dtype=torch.int64, device=dev) for _ in range(2)]
+    bufs = [torch.empty((chunk, n), dtype=torch.int64, device=dev) for _ in range(2)]
     done = [torch.cuda.Event() for _ in range(2)]  # compute finished with buffer b
     back = torch.cuda.Stream(dev) if out_host is not None else None
+    width = _codec_width(t)
+    if width:
+        ndt = torch.int8 if width == 1 else torch.int16
+        stage = [torch.empty(chunk * n, dtype=ndt, pin_memory=True) for _ in range(2)]
+        dnar = [torch.empty(chunk * n, dtype=ndt, device=dev) for _ in range(2)]
+        landed = [None, None]  # H2D of staging buffer b finished (host may refill it)
+        lib = N.load()
     ws = None
     if algo == N.ALGO_AUTO and N.load().tnb_entries_workspace_bytes(
             ctypes.byref(p.chain), chunk, N.ALGO_BUCKETED) > 0:
@@ -481,16 +509,31 @@ def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: in
         lo, hi = c * chunk, min(m, (c + 1) * chunk)
         b = c & 1
         buf = bufs[b]
+        narrow = False
+        if width:
+            if landed[b] is not None:
+                landed[b].synchronize()  # the H2D of chunk c-2 has read stage[b]
+            cnt = (hi - lo) * n
+            narrow = N.narrow_indices(idx_host[lo:hi].view(-1), stage[b][:cnt], width)
         with torch.cuda.stream(copy):
             if c >= 2:
                 copy.wait_event(done[b])
-            buf[: hi - lo].copy_(idx_host[lo:hi], non_blocking=True)
+            if narrow:
+                dnar[b][:cnt].copy_(stage[b][:cnt], non_blocking=True)
+                landed[b] = torch.cuda.Event()
+                landed[b].record(copy)
+            else:
+                buf[: hi - lo].copy_(idx_host[lo:hi], non_blocking=True)
             if hi - lo < chunk:
                 buf[hi - lo:].zero_()
             ready = torch.cuda.Event()
             ready.record(copy)
         comp.wait_event(ready)
         buf.record_stream(comp)
+        if narrow:
+            dnar[b].record_stream(comp)
+            N.check(lib.tnb_widen_indices(dnar[b].data_ptr(), width, cnt, buf.data_ptr(),
+                                          N.stream_ptr(dev)), "widen indices")
         ws = launch_entries(p, buf, out[lo:lo + chunk], errs[c:c + 1], algo, ws)
         done[b].record(comp)
         if back is not None:

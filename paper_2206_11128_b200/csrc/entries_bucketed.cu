@@ -2098,6 +2098,11 @@ int wide_env() {
   return (e && e[0] == '0') ? 0 : 1;
 }
 
+int64_t env_rows(const char* name) {
+  const char* e = getenv(name);
+  return e ? atoll(e) : 0;
+}
+
 void plan_merge(const ChainDev& ch, int64_t m, MergePlan* mp) {
   const int N = ch.n;
   // uint16-indexed, L2-resident tables: up to min(m/16, 65535) rows.  A
@@ -2112,9 +2117,13 @@ void plan_merge(const ChainDev& ch, int64_t m, MergePlan* mp) {
   };
   int a = 1, b = 1;
   int64_t rows = ch.m[0].J, rs = ch.m[N - 1].J;
+  // plan-exploration caps on the prefix / suffix table rows (0 = planner's choice)
+  const int64_t pcap = env_rows("TNB_PREFIX_MAX_ROWS"), scap = env_rows("TNB_SUFFIX_MAX_ROWS");
   if (lim > 0) {
-    while (a < N - 1 && grow(rows * ch.m[a].J, ch.m[a], ch.m[a].rr)) rows *= ch.m[a++].J;
-    while (N - 1 - b >= a && grow(rs * ch.m[N - 1 - b].J, ch.m[N - 1 - b], ch.m[N - 1 - b].rl))
+    while (a < N - 1 && grow(rows * ch.m[a].J, ch.m[a], ch.m[a].rr) && (!pcap || rows * ch.m[a].J <= pcap))
+      rows *= ch.m[a++].J;
+    while (N - 1 - b >= a && grow(rs * ch.m[N - 1 - b].J, ch.m[N - 1 - b], ch.m[N - 1 - b].rl) &&
+           (!scap || rs * ch.m[N - 1 - b].J <= scap))
       rs *= ch.m[N - 1 - b++].J;
   }
   mp->table_bytes = 0;
@@ -2666,9 +2675,16 @@ int launch_entries_bucketed(const ChainDev& ch, const int64_t* idx, int64_t m, f
     if (ss) {
       rc = check_cuda(cudaEventRecord(ss->fork, st), "fork");
       if (!rc) rc = check_cuda(cudaStreamWaitEvent(ss->s, ss->fork, 0), "fork wait");
-      if (!rc) rc = build_tables(ch, mp, base, ss->s);
-      if (!rc) rc = check_cuda(cudaEventRecord(ss->join, ss->s), "join");
-      if (rc) return rc;
+      if (rc) return rc;  // nothing was queued on the side stream
+      rc = build_tables(ch, mp, base, ss->s);
+      const int rj = check_cuda(cudaEventRecord(ss->join, ss->s), "join");
+      if (rc || rj) {
+        // join on the error path too: the caller frees the workspace the
+        // side stream may still be writing
+        if (!rj) cudaStreamWaitEvent(st, ss->join, 0);
+        else cudaStreamSynchronize(ss->s);
+        return rc ? rc : rj;
+      }
       tables = ss->join;
     } else {
       rc = build_tables(ch, mp, base, st);
@@ -2683,18 +2699,25 @@ int launch_entries_bucketed(const ChainDev& ch, const int64_t* idx, int64_t m, f
   const bool small = bp.idx_bytes == 1;
   switch (R) {
     case 8:
-      return small ? launch_ri<8, uint8_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables)
-                   : launch_ri<8, uint16_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables);
+      rc = small ? launch_ri<8, uint8_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables)
+                 : launch_ri<8, uint16_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables);
+      break;
     case 16:
-      return small ? launch_ri<16, uint8_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables)
-                   : launch_ri<16, uint16_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables);
+      rc = small ? launch_ri<16, uint8_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables)
+                 : launch_ri<16, uint16_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables);
+      break;
     case 24:
-      return small ? launch_ri<24, uint8_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables)
-                   : launch_ri<24, uint16_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables);
+      rc = small ? launch_ri<24, uint8_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables)
+                 : launch_ri<24, uint16_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables);
+      break;
     default:
-      return small ? launch_ri<32, uint8_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables)
-                   : launch_ri<32, uint16_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables);
+      rc = small ? launch_ri<32, uint8_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables)
+                 : launch_ri<32, uint16_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables);
   }
+  // a failed launch may return before its own join: the side stream's table
+  // writes must still be ordered before anything the caller does with ws
+  if (rc && tables) cudaStreamWaitEvent(st, tables, 0);
+  return rc;
 }
 
 }  // namespace tnb

@@ -11,6 +11,7 @@
 // A slab [lo, hi) of the leading mode restricts L's rows, which is the
 // reference's own full(t[lo:hi]) (indexing.py:132-137); it is also how the
 // multi-GPU runner shards full() across devices.
+#include <cstdlib>
 #include <type_traits>
 #include <vector>
 
@@ -88,6 +89,11 @@ int make_plan(const tnb_chain* c, int64_t lo, int64_t hi, FullPlan* P, int elt) 
       best = score;
       P->p = p;
     }
+  }
+  // TNB_FULL_SPLIT=p pins the split edge (tests reach every step shape with it)
+  if (const char* e = getenv("TNB_FULL_SPLIT")) {
+    const int pin = atoi(e);
+    if (pin >= 1 && pin <= n) P->p = pin;
   }
   // buffer sizes for the chosen p
   const int p = P->p;
@@ -212,7 +218,8 @@ __global__ void __launch_bounds__(256) gemm_kernel(const T* __restrict__ A, int6
   A += e * sA;
   Bm += e * sB;
   C += e * sC;
-  const int64_t m0 = (int64_t)blockIdx.y * GBM, n0 = (int64_t)blockIdx.x * GBN;
+  // M tiles on grid.x (2^31 - 1 blocks), N tiles on grid.y
+  const int64_t m0 = (int64_t)blockIdx.x * GBM, n0 = (int64_t)blockIdx.y * GBN;
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   T acc[8][8];
 #pragma unroll
@@ -301,16 +308,34 @@ ModeDev mode_dev(const tnb_chain* c, int k) {
 
 }  // namespace
 
+// C[e] = A[e] @ B[e] (+ the right-step row remap), chunked so that any M,
+// any N and any batch fit the grid limits (x: 2^31 - 1, y / z: 65535).
+template <typename T>
+int launch_gemm_remap(const T* A, int64_t lda, int64_t sA, const T* B, int64_t ldb, int64_t sB,
+                      T* C, int64_t ldc, int64_t sC, int64_t M, int64_t N, int K, int64_t batch,
+                      int remap_rl, int64_t remap_J, cudaStream_t st) {
+  if (M == 0 || N == 0 || batch == 0) return TNB_OK;
+  if (ceil_div(M, GBM) > INT32_MAX) return set_error(TNB_EINVAL, "gemm M too large");
+  constexpr int64_t kMaxY = 65535, kMaxZ = 65535;
+  for (int64_t e0 = 0; e0 < batch; e0 += kMaxZ) {
+    const int64_t nb = batch - e0 < kMaxZ ? batch - e0 : kMaxZ;
+    for (int64_t c0 = 0; c0 < N; c0 += kMaxY * GBN) {
+      const int64_t nc = N - c0 < kMaxY * GBN ? N - c0 : kMaxY * GBN;
+      const dim3 grid((unsigned)ceil_div(M, GBM), (unsigned)ceil_div(nc, GBN), (unsigned)nb);
+      gemm_kernel<T><<<grid, 256, 0, st>>>(A + e0 * sA, lda, sA, B + e0 * sB + c0, ldb, sB,
+                                           C + e0 * sC + c0, ldc, sC, M, nc, K, remap_rl, remap_J);
+      const int rc = check_launch("gemm");
+      if (rc) return rc;
+    }
+  }
+  return TNB_OK;
+}
+
 template <typename T>
 int launch_gemm(const T* A, int64_t lda, int64_t sA, const T* B, int64_t ldb, int64_t sB,
                 T* C, int64_t ldc, int64_t sC, int64_t M, int64_t N, int K, int64_t batch,
                 cudaStream_t st) {
-  if (M == 0 || N == 0 || batch == 0) return TNB_OK;
-  if (batch > 65535) return set_error(TNB_EINVAL, "gemm batch too large");
-  dim3 grid((unsigned)ceil_div(N, GBN), (unsigned)ceil_div(M, GBM), (unsigned)batch);
-  if (grid.y > 65535) return set_error(TNB_EINVAL, "gemm M too large");
-  gemm_kernel<T><<<grid, 256, 0, st>>>(A, lda, sA, B, ldb, sB, C, ldc, sC, M, N, K, 0, 0);
-  return check_launch("gemm");
+  return launch_gemm_remap<T>(A, lda, sA, B, ldb, sB, C, ldc, sC, M, N, K, batch, 0, 0, st);
 }
 
 int64_t full_workspace(const tnb_chain* c, int64_t lo, int64_t hi, int elt) {
@@ -387,13 +412,12 @@ int full_t(const tnb_chain* c, int64_t lo, int64_t hi, T* out, void* ws, int64_t
     T* dst = rb[which ^ 1];
     const int64_t total = (int64_t)md.rl * md.J * cols * B;
     const int64_t gm_rows = (int64_t)md.J * md.rl;
-    if (TNB_FULL_RIGHT_GEMM && total > 0 && md.layout == TNB_LAYOUT_DENSE && md.rr >= 8 && cols >= 64 &&
-        B <= 65535 && ceil_div(gm_rows, GBM) <= 65535) {
+    if (TNB_FULL_RIGHT_GEMM && total > 0 && md.layout == TNB_LAYOUT_DENSE && md.rr >= 8 && cols >= 64) {
       // dense right step as a GEMM over the (j, a) rows of the core: the same
       // sequential sum over c per output, rows stored in (a, j) order
-      const dim3 grid((unsigned)ceil_div(cols, GBN), (unsigned)ceil_div(gm_rows, GBM), (unsigned)B);
-      gemm_kernel<T><<<grid, 256, 0, st>>>(reinterpret_cast<const T*>(md.s), md.rr, md.bstride, R, cols,
-                                           P.r_buf, dst, cols, P.r_buf, gm_rows, cols, md.rr, md.rl, md.J);
+      rc = launch_gemm_remap<T>(reinterpret_cast<const T*>(md.s), md.rr, md.bstride, R, cols, P.r_buf, dst,
+                                cols, P.r_buf, gm_rows, cols, md.rr, B, md.rl, md.J, st);
+      if (rc) return rc;
     } else if (total > 0)
       full_right_step<T><<<grid_for(total), 256, 0, st>>>(md, B, R, P.r_buf, cols, dst, P.r_buf);
     rc = check_launch("full_right_step");

@@ -19,6 +19,7 @@ from typing import Callable, Optional
 import torch
 
 from .core import TnTensor, chain_dot, entries, full, norm
+from .errors import ContractViolationError
 
 
 def shard_bounds(n: int, world: int, rank: int) -> tuple:
@@ -78,14 +79,31 @@ def batch_slice(t: TnTensor, lo: int, hi: int) -> TnTensor:
     return TnTensor(nodes, hi - lo)
 
 
+def _batch_of(t, op: str) -> int:
+    nb = getattr(t, "batch_size", None)
+    if nb is None:
+        raise ContractViolationError(f"{op} shards the batch axis: the tensor is not batched")
+    return int(nb)
+
+
+def _empty_result(t) -> torch.Tensor:
+    """The (0,) result of a rank whose pair shard is empty (batch < world):
+    it still joins the gather, so the other ranks do not wait forever."""
+    if isinstance(t, TnTensor):
+        return torch.empty(0, dtype=t.dtype, device=t.device)
+    return torch.empty(0, dtype=torch.float64)
+
+
 def dot_sharded(a: TnTensor, b: TnTensor, *, group=None, gather: bool = True,
                 compute: Optional[Callable] = None, slicer: Optional[Callable] = None):
     """Batched dot with the pairs split across ranks."""
     _, world, rank = _dist(group)
-    nb = a.batch_size
+    nb = _batch_of(a, "dot_sharded")
+    if _batch_of(b, "dot_sharded") != nb:
+        raise ContractViolationError("operands must agree on batching")
     lo, hi = shard_bounds(nb, world, rank)
     sl = slicer or batch_slice
-    local = (compute or chain_dot)(sl(a, lo, hi), sl(b, lo, hi))
+    local = (compute or chain_dot)(sl(a, lo, hi), sl(b, lo, hi)) if hi > lo else _empty_result(a)
     if not gather:
         return local, (lo, hi)
     return gather_rows(local, nb, group)
@@ -94,9 +112,9 @@ def dot_sharded(a: TnTensor, b: TnTensor, *, group=None, gather: bool = True,
 def norm_sharded(t: TnTensor, *, group=None, gather: bool = True,
                  compute: Optional[Callable] = None, slicer: Optional[Callable] = None):
     _, world, rank = _dist(group)
-    nb = t.batch_size
+    nb = _batch_of(t, "norm_sharded")
     lo, hi = shard_bounds(nb, world, rank)
-    local = (compute or norm)((slicer or batch_slice)(t, lo, hi))
+    local = (compute or norm)((slicer or batch_slice)(t, lo, hi)) if hi > lo else _empty_result(t)
     if not gather:
         return local, (lo, hi)
     return gather_rows(local, nb, group)

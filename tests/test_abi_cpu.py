@@ -230,3 +230,38 @@ def test_timing_is_opt_in(lib):
     N.timing_enable(True)
     assert N.timing_read("entries_compute") == (0.0, 0)
     N.timing_enable(False)
+
+
+@pytest.mark.parametrize("width", [1, 2])
+@pytest.mark.parametrize("nthreads", [1, 0])
+def test_host_narrow_codec(width, nthreads, lib):
+    # the host half of the index transport codec runs without a GPU
+    import torch
+
+    from paper_2206_11128_b200 import _native
+
+    lo, hi = (-128, 127) if width == 1 else (-32768, 32767)
+    nt = torch.int8 if width == 1 else torch.int16
+    rng = np.random.default_rng(width)
+    for n in (0, 1, 17, 1000, (3 << 20) + 5):
+        src = torch.from_numpy(rng.integers(lo, hi + 1, size=n, dtype=np.int64))
+        if n:
+            src[0], src[-1] = lo, hi
+        dst = torch.empty(n, dtype=nt)
+        assert _native.narrow_indices(src, dst, width, nthreads)
+        assert torch.equal(dst.to(torch.int64), src)
+        if n:
+            for bad in (hi + 1, lo - 1, 1 << 40, -(1 << 62)):
+                s2 = src.clone()
+                s2[n // 2] = bad
+                assert not _native.narrow_indices(s2, dst, width, nthreads)
+
+
+def test_host_narrow_codec_rejects_bad_width(lib):
+    import torch
+
+    from paper_2206_11128_b200 import _native
+    from paper_2206_11128_b200.errors import ContractViolationError
+
+    with pytest.raises(ContractViolationError):
+        _native.narrow_indices(torch.zeros(4, dtype=torch.int64), torch.zeros(4, dtype=torch.int32), 4)

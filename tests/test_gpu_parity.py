@@ -259,15 +259,21 @@ def test_dot_rank16_fast_and_generic(generic, monkeypatch):
     assert abs(tb.norm(t1) - O.norm(o1)) <= 1e-5 * O.norm(o1)
 
 
-def test_pipelined_host_indices_match_device_path():
-    # a large pinned int64 host matrix takes the chunked copy/compute pipeline;
-    # per-sample results do not depend on chunking or tiling (bitwise equal)
+@pytest.mark.parametrize("codec", ["1", "0"])
+def test_pipelined_host_indices_match_device_path(codec, monkeypatch):
+    # a large pinned int64 host matrix takes the chunked copy/compute pipeline
+    # (with and without the int8 index transport codec); per-sample results do
+    # not depend on chunking, tiling or the codec (bitwise equal)
     from paper_2206_11128_b200 import core as C
 
+    monkeypatch.setenv("TNB_E2E_CODEC", codec)
     cores = O.random_tt((32,) * 6, 16, seed=11, scale=0.25)
     t = facade([("tt", c, None) for c in cores])
+    assert C._codec_width(t) == (1 if codec == "1" else 0)
     m = 2 * C._PIPELINE_ROWS + 12345
-    idx = torch.from_numpy(O.uniform_indices((32,) * 6, m, 3)).pin_memory()
+    idx = torch.from_numpy(O.uniform_indices((32,) * 6, m, 3))
+    idx[::3] -= 32  # negative indices cross the codec as negatives and wrap on the device
+    idx = idx.pin_memory()
     got = tb.entries(t, idx)
     ref = tb.entries(t, idx.cuda())
     assert torch.equal(got, ref)
@@ -278,6 +284,17 @@ def test_pipelined_host_indices_match_device_path():
     bad[m - 5, 4] = 40
     with pytest.raises(tb.ContractViolationError, match="mode 4"):
         tb.entries(t, bad.pin_memory())
+    # values outside int8: that chunk crosses PCIe as int64, the other chunks
+    # narrowed; the lowest offending mode is still reported
+    bad = idx.clone()
+    bad[7, 5] = 1000
+    bad[C._PIPELINE_ROWS + 3, 2] = -33
+    bad[C._PIPELINE_ROWS + 4, 1] = -(1 << 40)
+    with pytest.raises(tb.ContractViolationError, match="mode 1"):
+        tb.entries(t, bad.pin_memory())
+    ok = idx.clone()
+    ok[C._PIPELINE_ROWS + 9, 3] = -32  # the most negative valid index
+    assert torch.equal(tb.entries(t, ok.pin_memory()), tb.entries(t, ok.cuda()))
 
 
 def test_bucketed_cfg5_structure():
@@ -545,3 +562,42 @@ def test_full_tensor_core_gemm_ragged(rank, batch):
     o = O.make_chain([("tt", c) for c in cores], batch)
     assert_close(tb.full(t), O.full(o), what=f"full r{rank} b{batch}")
     assert_close(tb.full(t, lead=(3, 17)), O.full_slab(o, 3, 17), what=f"full slab r{rank} b{batch}")
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("batch", [None, 3])
+def test_full_right_step_gemm_ragged(dtype, batch, monkeypatch):
+    # split pinned at p=1 so the whole chain but mode 0 is the right partial:
+    # mode 2's step (cols = 29 < 64) runs the per-output step kernel, mode 1's
+    # (r_r = 8, cols = 2030) the tiled GEMM with the (j, a) -> (a, j) row
+    # remap; gm_rows = 37 * 8 = 296 and cols = 2030 are not multiples of the
+    # 128 x 128 tile (core.py:345-351)
+    monkeypatch.setenv("TNB_FULL_SPLIT", "1")
+    shape = (9, 37, 70, 29)
+    cores = O.random_tt(shape, 8, seed=11, batch_size=batch, scale=8 ** -0.5)
+    o = O.make_chain([("tt", c) for c in cores], batch)
+    dt = torch.float64 if dtype == "f64" else torch.float32
+    t = tb.TnTensor([tb.ModeNode("tt", c, batched=batch is not None, dtype=dt) for c in cores], batch)
+    ref = O.full(o)
+    got = tb.full(t)
+    if dtype == "f64":
+        err = np.abs(to_np(got) - ref).max() / np.abs(ref).max()
+        assert err <= 1e-12, err
+    else:
+        assert_close(got, ref, what=f"right-step gemm b{batch}")
+    assert_close(tb.full(t, lead=(2, 7)), O.full_slab(o, 2, 7), what="right-step gemm slab")
+
+
+def test_full_tall_thin_generic_gemm(monkeypatch):
+    # an fp32 chain of shape (2^24, 2) split at p=1 has 2^24 rows
+    # of L and N=2 columns (no tensor-core GEMM), i.e. 131072 row tiles: more
+    # than the 65535 a grid's y axis holds
+    monkeypatch.setenv("TNB_FULL_SPLIT", "1")
+    rng = np.random.default_rng(5)
+    nodes = [("tt", rng.standard_normal((1, 1 << 24, 3)).astype(np.float32), None),
+             ("tt", rng.standard_normal((3, 2, 1)).astype(np.float32), None)]
+    t = facade(nodes)
+    got = to_np(tb.full(t))
+    a, b = nodes[0][1][0].astype(np.float64), nodes[1][1][:, :, 0].astype(np.float64)
+    sel = np.r_[0:4096, (1 << 24) - 4096:(1 << 24)]
+    assert_close(got[sel], a[sel] @ b, what="tall thin full")

@@ -48,6 +48,14 @@ def _worker(rank, world, port, q):
         res["dot"] = float(np.abs(dots.numpy() - O.chain_dot(a, b)).max())
         norms = S.norm_sharded(a, compute=lambda x: torch.from_numpy(O.norm(x)), slicer=O.batch_slice)
         res["norm"] = float(np.abs(norms.numpy() - O.norm(a)).max())
+        # batch < world: rank 1's pair shard is empty and must still join the gather
+        a1 = O.batch_slice(a, 0, 1)
+        b1 = O.batch_slice(b, 0, 1)
+        d1 = S.dot_sharded(a1, b1, compute=lambda x, y: torch.from_numpy(O.chain_dot(x, y)),
+                           slicer=O.batch_slice)
+        n1 = S.norm_sharded(a1, compute=lambda x: torch.from_numpy(O.norm(x)), slicer=O.batch_slice)
+        res["dot_small"] = float(np.abs(d1.numpy() - O.chain_dot(a1, b1)).max()) if d1.shape == (1,) else 1.0
+        res["norm_small"] = float(np.abs(n1.numpy() - O.norm(a1)).max()) if n1.shape == (1,) else 1.0
         slab, (lo, hi) = S.full_sharded(chain, compute=lambda c, l, h: torch.from_numpy(O.full_slab(c, l, h)))
         res["full"] = float(np.abs(slab.numpy() - O.full(chain)[lo:hi]).max())
         res["span"] = (lo, hi)
@@ -68,6 +76,16 @@ def test_two_rank_gloo_sharding():
         p.join(timeout=60)
         assert p.exitcode == 0
     for r in range(2):
-        for k in ("entries", "dot", "norm", "full"):
+        for k in ("entries", "dot", "norm", "full", "dot_small", "norm_small"):
             assert out[r][k] <= 1e-12, (r, k, out[r][k])
     assert out[0]["span"] == (0, 3) and out[1]["span"] == (3, 5)
+
+
+def test_sharded_dot_rejects_unbatched():
+    from paper_2206_11128_b200.errors import ContractViolationError
+
+    chain = O.make_chain([("tt", c) for c in O.random_tt((5, 4), 3, seed=3)])
+    with pytest.raises(ContractViolationError, match="not batched"):
+        S.dot_sharded(chain, chain, compute=lambda x, y: None, slicer=O.batch_slice)
+    with pytest.raises(ContractViolationError, match="not batched"):
+        S.norm_sharded(chain, compute=lambda x: None, slicer=O.batch_slice)

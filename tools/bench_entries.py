@@ -31,19 +31,29 @@ def one(cfg, algo=0, reps=5):
     idx = torch.randint(0, shape[0], (m, len(shape)), dtype=torch.int64, device="cuda")
     out = torch.empty(m, device="cuda")
     err = torch.empty(1, dtype=torch.int32, device="cuda")
-    for _ in range(2):
-        C.launch_entries(p, idx, out, err, algo)
+    from paper_2206_11128_b200 import _native as N
+
+    ws = None
+    for _ in range(3):
+        ws = C.launch_entries(p, idx, out, err, algo, ws)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    N.timing_enable(True)
     e0.record()
     for _ in range(reps):
-        C.launch_entries(p, idx, out, err, algo)
+        ws = C.launch_entries(p, idx, out, err, algo, ws)
     e1.record()
     torch.cuda.synchronize()
+    kt = {k: N.timing_read(k) for k in ("entries_prep", "entries_sort", "entries_compute", "entries_tables")}
+    N.timing_enable(False)
     ms = e0.elapsed_time(e1) / reps
     flops = W.entry_flops(modes) * m
+    plan = N.entries_plan(p.chain, m, algo)
     return {"cfg": cfg, "algo": algo, "ms": round(ms, 3), "Gentries/s": round(m / ms / 1e6, 3),
-            "TFLOP/s": round(flops / ms / 1e9, 2)}
+            "TFLOP/s": round(flops / ms / 1e9, 2),
+            "kernels_ms": {k: round(v[0] / v[1], 3) for k, v in kt.items() if v[1]},
+            "plan": {k: plan[k] for k in ("n_virtual", "prefix_modes", "suffix_modes", "prefix_rows",
+                                          "suffix_rows", "diag_tables", "compute_kernel", "tile")}}
 
 
 if __name__ == "__main__":
@@ -53,10 +63,16 @@ if __name__ == "__main__":
         print(json.dumps(one(cfg, algo)))
         sys.exit(0)
     variants = [{}, {"TNB_ENTRIES_MERGE": "0"}, {"TNB_LANE_MAJOR": "0"}]
+    cfgs = ("cfg2", "cfg5")
+    if "--sweep" in sys.argv:  # variants as JSON objects on the command line after --sweep
+        i = sys.argv.index("--sweep")
+        cfgs = (sys.argv[i + 1],)
+        variants = [json.loads(a) for a in sys.argv[i + 2:]]
     for v in variants:
-        for cfg in ("cfg2", "cfg5"):
+        for cfg in cfgs:
             env = dict(os.environ, **v)
             r = subprocess.run([sys.executable, __file__, "--one", cfg], env=env, capture_output=True, text=True)
             print(json.dumps(v), r.stdout.strip() or r.stderr[-500:], flush=True)
-    r = subprocess.run([sys.executable, __file__, "--one", "cfg5", "--algo", "2"], capture_output=True, text=True)
-    print("chain", r.stdout.strip() or r.stderr[-300:])
+    if "--sweep" not in sys.argv:
+        r = subprocess.run([sys.executable, __file__, "--one", "cfg5", "--algo", "2"], capture_output=True, text=True)
+        print("chain", r.stdout.strip() or r.stderr[-300:])
