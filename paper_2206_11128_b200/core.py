@@ -453,6 +453,10 @@ def _index_tensor(t: TnTensor, indices, device) -> torch.Tensor:
 # chunk i+1 overlaps the kernels of chunk i)
 _PIPELINE_ROWS = 1 << 21
 
+# what the last pipelined entries() call moved over PCIe (bench.py's e2e
+# byte counts): {"h2d_bytes", "d2h_bytes", "codec"}
+last_transfer: dict = {}
+
 
 def _codec_width(t: TnTensor) -> int:
     """Width of the index transport codec for this chain (include/tnb.h):
@@ -505,6 +509,8 @@ def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: in
             ctypes.byref(p.chain), chunk, N.ALGO_BUCKETED) > 0:
         algo = N.ALGO_BUCKETED  # one kernel for every chunk, even a short last one
     copy.wait_stream(comp)
+    h2d = 0
+    codecs = set()
     for c in range(nch):
         lo, hi = c * chunk, min(m, (c + 1) * chunk)
         b = c & 1
@@ -522,8 +528,12 @@ def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: in
                 dnar[b][:cnt].copy_(stage[b][:cnt], non_blocking=True)
                 landed[b] = torch.cuda.Event()
                 landed[b].record(copy)
+                h2d += cnt * width
+                codecs.add(f"int{8 * width}")
             else:
                 buf[: hi - lo].copy_(idx_host[lo:hi], non_blocking=True)
+                h2d += (hi - lo) * n * 8
+                codecs.add("int64")
             if hi - lo < chunk:
                 buf[hi - lo:].zero_()
             ready = torch.cuda.Event()
@@ -543,6 +553,9 @@ def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: in
     code = int(errs.min().item())
     if back is not None:
         back.synchronize()
+    last_transfer.clear()
+    last_transfer.update(h2d_bytes=h2d, d2h_bytes=m * 4 if back is not None else 0,
+                         codec="+".join(sorted(codecs)))
     if code < t.ndim:
         raise ContractViolationError(f"index out of bounds on mode {code}")
     return out_host if out_host is not None else out[:m]
