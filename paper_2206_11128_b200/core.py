@@ -449,9 +449,10 @@ def _index_tensor(t: TnTensor, indices, device) -> torch.Tensor:
     return idx.to(device=device, dtype=torch.int64).contiguous()
 
 
-# host index matrices at least this long are streamed in chunks (H2D of
-# chunk i+1 overlaps the kernels of chunk i)
+# host index matrices at least 2 * _PIPELINE_ROWS long are streamed in
+# chunks of _CHUNK_ROWS (H2D of chunk i+1 overlaps the kernels of chunk i)
 _PIPELINE_ROWS = 1 << 21
+_CHUNK_ROWS = 1 << 20
 
 # what the last pipelined entries() call moved over PCIe (bench.py's e2e
 # byte counts): {"h2d_bytes", "d2h_bytes", "codec"}
@@ -486,10 +487,10 @@ def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: in
     dev = p.device
     m = int(idx_host.shape[0])
     n = t.ndim
-    chunk = _PIPELINE_ROWS
+    chunk = _CHUNK_ROWS
     nch = (m + chunk - 1) // chunk
     # every launch sees exactly `chunk` rows (the short last chunk is padded
-    # with index 0), so all chunks run the same plan as one whole-array call
+    # with index 0), so all chunks run the same plan
     out = torch.empty(nch * chunk, dtype=torch.float32, device=dev)
     comp = torch.cuda.current_stream(dev)
     copy = torch.cuda.Stream(dev)
@@ -498,6 +499,18 @@ def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: in
     done = [torch.cuda.Event() for _ in range(2)]  # compute finished with buffer b
     back = torch.cuda.Stream(dev) if out_host is not None else None
     width = _codec_width(t)
+    # Two host resources feed the GPU: the DMA engine reading pinned memory
+    # over PCIe (~56 GB/s of int64) and the host cores narrowing (~80 GB/s of
+    # int64 read on 16 threads).  A fraction of the chunks crosses raw (no
+    # host work: the DMA reads them while the cores narrow the others), the
+    # rest narrowed; raw chunks are spread evenly, starting with chunk 0 so
+    # the copy engine starts at once.
+    raw_frac = float(os.environ.get("TNB_E2E_RAW_FRAC", "0.4")) if width else 1.0
+
+    def raw_chunk(c):
+        x = raw_frac
+        return int((c + 1) * x + 1 - x + 1e-9) > int(c * x + 1 - x + 1e-9)
+
     if width:
         ndt = torch.int8 if width == 1 else torch.int16
         stage = [torch.empty(chunk * n, dtype=ndt, pin_memory=True) for _ in range(2)]
@@ -516,7 +529,7 @@ def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: in
         b = c & 1
         buf = bufs[b]
         narrow = False
-        if width:
+        if width and not raw_chunk(c):
             if landed[b] is not None:
                 landed[b].synchronize()  # the H2D of chunk c-2 has read stage[b]
             cnt = (hi - lo) * n

@@ -94,6 +94,8 @@ def test_cfg3_whole_tensor_checksum():
 
 
 def test_cfg4_pairs():
+    # all 4096 pairs, in 16 chunks of 256 through batch-sliced oracle chains
+    # (SURVEY 8(d) parity sampling); dot and norm
     a = O.random_tt((64,) * 16, 16, seed=0, batch_size=4096, scale=0.25)
     b = O.random_tt((64,) * 16, 16, seed=1, batch_size=4096, scale=0.25)
     ta, oa = tt(a, 4096)
@@ -101,11 +103,42 @@ def test_cfg4_pairs():
     dots = to_np(tb.dot(ta, tb_))
     norms = to_np(tb.norm(ta))
     assert dots.shape == (4096,) and norms.shape == (4096,)
-    lo, hi = 0, 256
-    ref_d = O.chain_dot(O.batch_slice(oa, lo, hi), O.batch_slice(ob, lo, hi))
-    ref_n = O.norm(O.batch_slice(oa, lo, hi))
-    assert_close(dots[lo:hi], ref_d, what="cfg4 dot")
-    assert_close(norms[lo:hi], ref_n, what="cfg4 norm")
-    # the last chunk too (every shard of an 8-way split is covered by its ends)
-    ref_d = O.chain_dot(O.batch_slice(oa, 3840, 4096), O.batch_slice(ob, 3840, 4096))
-    assert_close(dots[3840:], ref_d, what="cfg4 dot tail")
+    for lo in range(0, 4096, 256):
+        hi = lo + 256
+        sa, sb = O.batch_slice(oa, lo, hi), O.batch_slice(ob, lo, hi)
+        ref_d = O.chain_dot(sa, sb)
+        ref_n = O.norm(sa)
+        assert_close(dots[lo:hi], ref_d, what=f"cfg4 dot [{lo}, {hi})")
+        assert_close(norms[lo:hi], ref_n, what=f"cfg4 norm [{lo}, {hi})")
+
+
+def test_cfg5_benchmarked_plan():
+    # cfg5 at the size bench.py times (2^26 tuples): the planner's HBM prefix
+    # table P012 (2^21 rows), the diagonal CP table and the stream kernel --
+    # the exact plan behind the benchmark line, checked on 2^20 oracle rows
+    # spread over the whole batch (core.py:394-444)
+    nodes = O.cfg5_nodes(seed=0)
+    t = facade(nodes)
+    o = O.make_chain(nodes)
+    m = 1 << 26
+    plan = N.entries_plan(t._packed().chain, m, N.ALGO_AUTO)
+    assert (plan["n_virtual"], plan["prefix_rows"], plan["compute_kernel"]) == (4, 1 << 21, 1), plan
+    idx = torch.from_numpy(O.uniform_indices((128,) * 8, m, 2)).cuda()
+    got = tb.entries(t, idx)
+    assert tuple(got.shape) == (m,)
+    sel = torch.from_numpy(np.linspace(0, m - 1, 1 << 20).astype(np.int64)).cuda()
+    sub = idx[sel].cpu().numpy()
+    g = got[sel].double().cpu().numpy()
+    del idx, got
+    assert_close(g, O.entries(o, sub), what="cfg5 at 2^26")
+
+
+def test_cfg2_benchmarked_plan():
+    # the plan behind the cfg2 headline: P0123 / S6789 HBM tables (2^20 rows
+    # each), two tensor-core sorted modes on the state kernel
+    cores = O.random_tt((32,) * 10, 32, seed=0, scale=32 ** -0.5)
+    t, _ = tt(cores)
+    plan = N.entries_plan(t._packed().chain, 1 << 24, N.ALGO_AUTO)
+    assert (plan["n_virtual"], plan["prefix_rows"], plan["suffix_rows"], plan["compute_kernel"]) == \
+        (4, 1 << 20, 1 << 20, 0), plan
+    assert plan["tensor_flops"] > 0

@@ -49,7 +49,10 @@ for nt in (1, 2, 4, 8, 16, 32, 0):
 print("widen kernel: %.3f ms" % wall(lambda: N.load().tnb_widen_indices(dnar.data_ptr(), 1, dnar.numel(),
                                                                         dev.data_ptr(), N.stream_ptr(dev.device))))
 print("entries(device idx): %.2f ms" % wall(lambda: tb.entries(t, dev)))
-for codec in ("0", "1"):
+from paper_2206_11128_b200 import core as C  # noqa: E402
+
+for codec, frac in (("0", "1"), ("1", "0"), ("1", "0.3"), ("1", "0.4"), ("1", "0.5")):
     os.environ["TNB_E2E_CODEC"] = codec
-    print("codec=%s entries(pinned host idx, out=pinned): %.2f ms" % (
-        codec, wall(lambda: tb.entries(t, idx_host, out=pin_out))))
+    os.environ["TNB_E2E_RAW_FRAC"] = frac
+    print("codec=%s raw_frac=%s entries(pinned host idx, out=pinned): %.2f ms %s" % (
+        codec, frac, wall(lambda: tb.entries(t, idx_host, out=pin_out)), C.last_transfer), flush=True)
