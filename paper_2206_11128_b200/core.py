@@ -513,9 +513,13 @@ def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: in
 
     if width:
         ndt = torch.int8 if width == 1 else torch.int16
-        stage = [torch.empty(chunk * n, dtype=ndt, pin_memory=True) for _ in range(2)]
+        # 4 pinned staging buffers: the host never waits for a narrowed
+        # chunk's H2D queued behind a raw chunk's (the copy stream is FIFO)
+        nst = 4
+        stage = [torch.empty(chunk * n, dtype=ndt, pin_memory=True) for _ in range(nst)]
         dnar = [torch.empty(chunk * n, dtype=ndt, device=dev) for _ in range(2)]
-        landed = [None, None]  # H2D of staging buffer b finished (host may refill it)
+        landed = [None] * nst  # H2D of staging buffer i finished (host may refill it)
+        n_narrow = 0
         lib = N.load()
     ws = None
     if algo == N.ALGO_AUTO and N.load().tnb_entries_workspace_bytes(
@@ -524,23 +528,33 @@ def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: in
     copy.wait_stream(comp)
     h2d = 0
     codecs = set()
+    trace = os.environ.get("TNB_E2E_TRACE") == "1"
+    tr = {"wait": 0.0, "narrow": 0.0, "enqueue": 0.0}
+    import time as _time
     for c in range(nch):
+        t_a = _time.perf_counter()
         lo, hi = c * chunk, min(m, (c + 1) * chunk)
         b = c & 1
         buf = bufs[b]
         narrow = False
         if width and not raw_chunk(c):
-            if landed[b] is not None:
-                landed[b].synchronize()  # the H2D of chunk c-2 has read stage[b]
+            si = n_narrow % nst
+            n_narrow += 1
+            if landed[si] is not None:
+                landed[si].synchronize()  # the H2D nst narrowed chunks ago has read stage[si]
+            t_b = _time.perf_counter()
             cnt = (hi - lo) * n
-            narrow = N.narrow_indices(idx_host[lo:hi].view(-1), stage[b][:cnt], width)
+            narrow = N.narrow_indices(idx_host[lo:hi].view(-1), stage[si][:cnt], width)
+            tr["wait"] += t_b - t_a
+            tr["narrow"] += _time.perf_counter() - t_b
+        t_c = _time.perf_counter()
         with torch.cuda.stream(copy):
             if c >= 2:
                 copy.wait_event(done[b])
             if narrow:
-                dnar[b][:cnt].copy_(stage[b][:cnt], non_blocking=True)
-                landed[b] = torch.cuda.Event()
-                landed[b].record(copy)
+                dnar[b][:cnt].copy_(stage[si][:cnt], non_blocking=True)
+                landed[si] = torch.cuda.Event()
+                landed[si].record(copy)
                 h2d += cnt * width
                 codecs.add(f"int{8 * width}")
             else:
@@ -563,12 +577,18 @@ def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: in
             back.wait_event(done[b])
             with torch.cuda.stream(back):
                 out_host[lo:hi].copy_(out[lo:hi], non_blocking=True)
+        tr["enqueue"] += _time.perf_counter() - t_c
+    t_d = _time.perf_counter()
     code = int(errs.min().item())
     if back is not None:
         back.synchronize()
     last_transfer.clear()
     last_transfer.update(h2d_bytes=h2d, d2h_bytes=m * 4 if back is not None else 0,
                          codec="+".join(sorted(codecs)))
+    if trace:
+        tr["drain"] = _time.perf_counter() - t_d
+        import sys as _sys
+        print("e2e trace (ms): " + " ".join(f"{k}={1e3 * v:.2f}" for k, v in tr.items()), file=_sys.stderr)
     if code < t.ndim:
         raise ContractViolationError(f"index out of bounds on mode {code}")
     return out_host if out_host is not None else out[:m]

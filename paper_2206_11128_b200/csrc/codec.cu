@@ -8,25 +8,26 @@
 namespace tnb {
 namespace {
 
-// each thread widens 16 consecutive values: one 16-byte (int8) or two
-// 16-byte (int16) loads, eight 16-byte stores
+// each thread widens 2 consecutive values per step: a 2 (4)-byte load and
+// one 16-byte store, so a warp's stores cover 512 contiguous bytes (the
+// 16-values-per-thread variant wrote 128-byte runs at a 128-byte lane
+// stride and ran at 1.1 TB/s)
 template <typename N>
 __global__ void __launch_bounds__(256) widen_kernel(const N* __restrict__ in, int64_t count,
                                                     int64_t* __restrict__ out) {
-  const int64_t groups = count / 16;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < groups;
+  const int64_t pairs = count / 2;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < pairs;
        g += (int64_t)gridDim.x * blockDim.x) {
-    N v[16];
-    const uint4* src = reinterpret_cast<const uint4*>(in + g * 16);
-#pragma unroll
-    for (int q = 0; q < (int)sizeof(N); ++q) reinterpret_cast<uint4*>(v)[q] = __ldcs(src + q);
-    longlong2* dst = reinterpret_cast<longlong2*>(out + g * 16);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) __stcs(dst + q, make_longlong2((long long)v[2 * q], (long long)v[2 * q + 1]));
+    N v[2];
+    if constexpr (sizeof(N) == 1)
+      *reinterpret_cast<uint16_t*>(v) = __ldcs(reinterpret_cast<const unsigned short*>(in) + g);
+    else
+      *reinterpret_cast<uint32_t*>(v) = __ldcs(reinterpret_cast<const unsigned int*>(in) + g);
+    __stcs(reinterpret_cast<longlong2*>(out) + g, make_longlong2((long long)v[0], (long long)v[1]));
   }
-  // ragged tail (count % 16 values)
-  const int64_t t = groups * 16 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (blockIdx.x == 0 && t < count) out[t] = (int64_t)in[t];
+  if (count & 1) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[count - 1] = (int64_t)in[count - 1];
+  }
 }
 
 }  // namespace
@@ -36,9 +37,9 @@ int launch_widen(const void* in, int width, int64_t count, int64_t* out, cudaStr
   if (!in || !out || (width != 1 && width != 2)) return set_error(TNB_EINVAL, "widen: bad arguments");
   if ((reinterpret_cast<uintptr_t>(in) & 15) || (reinterpret_cast<uintptr_t>(out) & 15))
     return set_error(TNB_EINVAL, "widen: buffers must be 16-byte aligned");
-  const int64_t groups = count / 16;
-  int64_t grid = (groups + 255) / 256;
-  const int64_t cap = (int64_t)num_sms() * 8;
+  const int64_t pairs = count / 2;
+  int64_t grid = (pairs + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 16;
   grid = grid < 1 ? 1 : (grid > cap ? cap : grid);
   if (width == 1)
     widen_kernel<int8_t><<<(unsigned)grid, 256, 0, st>>>(static_cast<const int8_t*>(in), count, out);

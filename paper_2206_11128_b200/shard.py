@@ -41,10 +41,15 @@ def _dist(group):
 
 
 def gather_rows(local: torch.Tensor, n_total: int, group=None) -> torch.Tensor:
-    """All-gather variable-size row blocks (rank order == row order)."""
+    """All-gather variable-size row blocks (rank order == row order).  NCCL
+    gathers device tensors in place; under gloo (the CPU test backend, or
+    ranks sharing one GPU) a device block is gathered through host memory
+    and the result moved back to the block's device."""
     dist, world, rank = _dist(group)
     if dist is None or world == 1:
         return local
+    if local.device.type == "cuda" and dist.get_backend(group) == "gloo":
+        return gather_rows(local.cpu(), n_total, group).to(local.device)
     base = n_total // world + (1 if n_total % world else 0)
     pad = torch.zeros((base,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
     pad[: local.shape[0]] = local
