@@ -471,6 +471,66 @@ def _codec_width(t: TnTensor) -> int:
     return 1 if jmax <= 128 else (2 if jmax <= 32768 else 0)
 
 
+class _Narrower:
+    """Background host thread of the index transport codec: narrows the
+    chunks the pipeline sends narrowed, in order, into a ring of pinned
+    staging buffers, while the calling thread enqueues copies and launches
+    (ctypes releases the GIL during tnb_narrow_indices_host).  A staging
+    buffer is refilled only after the H2D that read it has completed."""
+
+    def __init__(self, idx_host, spans, stage, width, nthreads):
+        import threading
+
+        self.idx, self.spans, self.stage, self.width, self.nt = idx_host, spans, stage, width, nthreads
+        k = len(spans)
+        self.ready = [threading.Event() for _ in range(k)]
+        self.recorded = [threading.Event() for _ in range(k)]
+        self.landed = [None] * k
+        self.fits = [False] * k
+        self.stop = False
+        self.error = None
+        self.th = threading.Thread(target=self._run, daemon=True)
+        self.th.start()
+
+    def _run(self):
+        nst = len(self.stage)
+        try:
+            for k, (lo, hi) in enumerate(self.spans):
+                if k >= nst:
+                    self.recorded[k - nst].wait()
+                    if self.landed[k - nst] is not None:
+                        self.landed[k - nst].synchronize()
+                if self.stop:
+                    return
+                cnt = (hi - lo) * self.idx.shape[1]
+                self.fits[k] = N.narrow_indices(self.idx[lo:hi].view(-1), self.stage[k % nst][:cnt], self.width,
+                                                self.nt)
+                self.ready[k].set()
+        except BaseException as e:  # noqa: BLE001  (re-raised by the caller)
+            self.error = e
+            for r in self.ready:
+                r.set()
+
+    def get(self, k):
+        """(staging buffer, fits) of narrowed chunk k, once narrowed."""
+        self.ready[k].wait()
+        if self.error is not None:
+            raise self.error
+        return self.stage[k % len(self.stage)], self.fits[k]
+
+    def released(self, k, event):
+        """The H2D of chunk k's staging buffer was enqueued; ``event`` marks
+        its completion (None: the buffer was not read)."""
+        self.landed[k] = event
+        self.recorded[k].set()
+
+    def close(self):
+        self.stop = True
+        for r in self.recorded:
+            r.set()
+        self.th.join()
+
+
 def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: int,
                        out_host: Optional[torch.Tensor] = None) -> torch.Tensor:
     """entries() for a large PINNED int64 host index matrix: chunked
@@ -478,12 +538,16 @@ def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: in
     with a pinned host ``out_host`` each chunk's values are copied back on a
     second copy stream (PCIe is full duplex) behind the next chunk's work.
 
-    PCIe is the bound of this path, so each chunk crosses it narrowed by the
+    PCIe is the bound of this path, so most chunks cross it narrowed by the
     index transport codec (int64 -> int8/int16 on host threads, a pure range
-    check; ``tnb_narrow_indices_host``) and is widened back on the device
-    (``tnb_widen_indices``) before the unchanged K1 launch; the host narrows
-    chunk i+1 while the GPU copies and evaluates chunk i.  A chunk with a
-    value outside the narrow range crosses as int64."""
+    check; ``tnb_narrow_indices_host``, run ahead by a background thread) and
+    are widened back on the device (``tnb_widen_indices``) before the
+    unchanged K1 launch.  Two host resources feed the GPU -- the DMA engine
+    reading pinned memory (~56 GB/s of int64) and the host cores narrowing
+    (~86 GB/s of int64 read on 16 threads) -- so a fraction of the chunks
+    (TNB_E2E_RAW_FRAC, default 0.35) crosses raw with no host work, spread
+    evenly and starting with chunk 0 so the copy engine starts at once.  A
+    chunk with a value outside the narrow range crosses as int64."""
     dev = p.device
     m = int(idx_host.shape[0])
     n = t.ndim
@@ -499,28 +563,29 @@ def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: in
     done = [torch.cuda.Event() for _ in range(2)]  # compute finished with buffer b
     back = torch.cuda.Stream(dev) if out_host is not None else None
     width = _codec_width(t)
-    # Two host resources feed the GPU: the DMA engine reading pinned memory
-    # over PCIe (~56 GB/s of int64) and the host cores narrowing (~80 GB/s of
-    # int64 read on 16 threads).  A fraction of the chunks crosses raw (no
-    # host work: the DMA reads them while the cores narrow the others), the
-    # rest narrowed; raw chunks are spread evenly, starting with chunk 0 so
-    # the copy engine starts at once.
-    raw_frac = float(os.environ.get("TNB_E2E_RAW_FRAC", "0.4")) if width else 1.0
+    raw_frac = float(os.environ.get("TNB_E2E_RAW_FRAC", "0.35")) if width else 1.0
 
     def raw_chunk(c):
         x = raw_frac
         return int((c + 1) * x + 1 - x + 1e-9) > int(c * x + 1 - x + 1e-9)
 
+    spans = [(c * chunk, min(m, (c + 1) * chunk)) for c in range(nch)]
+    narrow_k = {}  # chunk -> index among the narrowed chunks
+    nar = None
     if width:
+        for c in range(nch):
+            if not raw_chunk(c):
+                narrow_k[c] = len(narrow_k)
+    if narrow_k:
         ndt = torch.int8 if width == 1 else torch.int16
-        # 4 pinned staging buffers: the host never waits for a narrowed
+        # 4 pinned staging buffers: the narrowing thread never waits for a
         # chunk's H2D queued behind a raw chunk's (the copy stream is FIFO)
-        nst = 4
-        stage = [torch.empty(chunk * n, dtype=ndt, pin_memory=True) for _ in range(nst)]
+        stage = [torch.empty(chunk * n, dtype=ndt, pin_memory=True) for _ in range(4)]
         dnar = [torch.empty(chunk * n, dtype=ndt, device=dev) for _ in range(2)]
-        landed = [None] * nst  # H2D of staging buffer i finished (host may refill it)
-        n_narrow = 0
         lib = N.load()
+        # one hardware thread stays with this (enqueueing) thread
+        nthreads = int(os.environ.get("TNB_E2E_THREADS", "0")) or max(1, lib.tnb_host_threads() - 1)
+        nar = _Narrower(idx_host, [spans[c] for c in narrow_k], stage, width, nthreads)
     ws = None
     if algo == N.ALGO_AUTO and N.load().tnb_entries_workspace_bytes(
             ctypes.byref(p.chain), chunk, N.ALGO_BUCKETED) > 0:
@@ -528,67 +593,57 @@ def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: in
     copy.wait_stream(comp)
     h2d = 0
     codecs = set()
-    trace = os.environ.get("TNB_E2E_TRACE") == "1"
-    tr = {"wait": 0.0, "narrow": 0.0, "enqueue": 0.0}
-    import time as _time
-    for c in range(nch):
-        t_a = _time.perf_counter()
-        lo, hi = c * chunk, min(m, (c + 1) * chunk)
-        b = c & 1
-        buf = bufs[b]
-        narrow = False
-        if width and not raw_chunk(c):
-            si = n_narrow % nst
-            n_narrow += 1
-            if landed[si] is not None:
-                landed[si].synchronize()  # the H2D nst narrowed chunks ago has read stage[si]
-            t_b = _time.perf_counter()
-            cnt = (hi - lo) * n
-            narrow = N.narrow_indices(idx_host[lo:hi].view(-1), stage[si][:cnt], width)
-            tr["wait"] += t_b - t_a
-            tr["narrow"] += _time.perf_counter() - t_b
-        t_c = _time.perf_counter()
-        with torch.cuda.stream(copy):
-            if c >= 2:
-                copy.wait_event(done[b])
+    try:
+        for c in range(nch):
+            lo, hi = spans[c]
+            b = c & 1
+            buf = bufs[b]
+            narrow = False
+            if c in narrow_k:
+                k = narrow_k[c]
+                sbuf, narrow = nar.get(k)
+                cnt = (hi - lo) * n
+            with torch.cuda.stream(copy):
+                if c >= 2:
+                    copy.wait_event(done[b])
+                if narrow:
+                    dnar[b][:cnt].copy_(sbuf[:cnt], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(copy)
+                    nar.released(k, ev)
+                    h2d += cnt * width
+                    codecs.add(f"int{8 * width}")
+                else:
+                    if c in narrow_k:
+                        nar.released(narrow_k[c], None)  # did not fit: its staging buffer was not read
+                    buf[: hi - lo].copy_(idx_host[lo:hi], non_blocking=True)
+                    h2d += (hi - lo) * n * 8
+                    codecs.add("int64")
+                if hi - lo < chunk:
+                    buf[hi - lo:].zero_()
+                ready = torch.cuda.Event()
+                ready.record(copy)
+            comp.wait_event(ready)
+            buf.record_stream(comp)
             if narrow:
-                dnar[b][:cnt].copy_(stage[si][:cnt], non_blocking=True)
-                landed[si] = torch.cuda.Event()
-                landed[si].record(copy)
-                h2d += cnt * width
-                codecs.add(f"int{8 * width}")
-            else:
-                buf[: hi - lo].copy_(idx_host[lo:hi], non_blocking=True)
-                h2d += (hi - lo) * n * 8
-                codecs.add("int64")
-            if hi - lo < chunk:
-                buf[hi - lo:].zero_()
-            ready = torch.cuda.Event()
-            ready.record(copy)
-        comp.wait_event(ready)
-        buf.record_stream(comp)
-        if narrow:
-            dnar[b].record_stream(comp)
-            N.check(lib.tnb_widen_indices(dnar[b].data_ptr(), width, cnt, buf.data_ptr(),
-                                          N.stream_ptr(dev)), "widen indices")
-        ws = launch_entries(p, buf, out[lo:lo + chunk], errs[c:c + 1], algo, ws)
-        done[b].record(comp)
-        if back is not None:
-            back.wait_event(done[b])
-            with torch.cuda.stream(back):
-                out_host[lo:hi].copy_(out[lo:hi], non_blocking=True)
-        tr["enqueue"] += _time.perf_counter() - t_c
-    t_d = _time.perf_counter()
+                dnar[b].record_stream(comp)
+                N.check(lib.tnb_widen_indices(dnar[b].data_ptr(), width, cnt, buf.data_ptr(),
+                                              N.stream_ptr(dev)), "widen indices")
+            ws = launch_entries(p, buf, out[lo:lo + chunk], errs[c:c + 1], algo, ws)
+            done[b].record(comp)
+            if back is not None:
+                back.wait_event(done[b])
+                with torch.cuda.stream(back):
+                    out_host[lo:hi].copy_(out[lo:hi], non_blocking=True)
+    finally:
+        if nar is not None:
+            nar.close()
     code = int(errs.min().item())
     if back is not None:
         back.synchronize()
     last_transfer.clear()
     last_transfer.update(h2d_bytes=h2d, d2h_bytes=m * 4 if back is not None else 0,
                          codec="+".join(sorted(codecs)))
-    if trace:
-        tr["drain"] = _time.perf_counter() - t_d
-        import sys as _sys
-        print("e2e trace (ms): " + " ".join(f"{k}={1e3 * v:.2f}" for k, v in tr.items()), file=_sys.stderr)
     if code < t.ndim:
         raise ContractViolationError(f"index out of bounds on mode {code}")
     return out_host if out_host is not None else out[:m]
