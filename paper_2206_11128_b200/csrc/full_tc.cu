@@ -19,14 +19,12 @@
 //     output row m, so after tcgen05.ld (thread = n) every st.global of a
 //     warp writes 32 consecutive floats of one output row: whole 128-byte
 //     lines, no transpose.
-//   * the epilogue (TNB_FULL_TMA, default on) stages each warp's 32 x 32
-//     sub-tile of the output in shared memory and writes it with one TMA
-//     tensor store (cp.async.bulk.tensor.2d, 4 KB, double-buffered per warp):
-//     the st.global path it replaces issued one 128-byte store per row and
-//     topped out at ~34 GB/s per SM (outstanding-store bound, 5.1 TB/s), the
-//     TMA engine keeps KB-sized writes in flight with no LSU slots.  TMA
-//     clips rows / columns past the tensor bounds, so ragged tiles need no
-//     special case.
+//   * an alternative epilogue (TNB_FULL_TMA_STORE=1) stages each warp's
+//     32 x 32 sub-tile of the output in shared memory and writes it with one
+//     TMA tensor store (cp.async.bulk.tensor.2d, 4 KB, double-buffered per
+//     warp; TMA clips ragged tiles).  Measured slower (3.72 vs 3.45 ms): the
+//     store stream of one CTA per SM caps near 5.9 TB/s either way
+//     (tools/store_bench.cu), so the default stays st.global.
 // Roles (384 threads, one persistent CTA per SM):
 //   warp 0      MMA issuer (one lane) + TMEM allocator
 //   warp 1      producer of L tiles (one lane)
@@ -576,9 +574,14 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+// TNB_FULL_TMA_STORE=1 selects the TMA-store epilogue.  Off by default:
+// measured 3.72 vs 3.45 ms at cfg3 (profiles/r02_full_store_bench.txt: this
+// one-CTA-per-SM store stream tops out at 5.6-5.9 TB/s whichever way the
+// 128 x 128 tiles are written -- st.global.b32 / .v4, TMA 32x32 / 64x64 --
+// and the staging round trip costs more than it saves)
 bool tma_env() {
   const char* e = getenv("TNB_FULL_TMA_STORE");
-  return !(e && e[0] == '0');
+  return e && e[0] == '1';
 }
 
 // C [M][N] (row stride ldc floats) as a 2-D tensor map with 32 x 32 boxes;

@@ -103,6 +103,43 @@ __global__ void __launch_bounds__(W * 32, 1) store_kernel(const __grid_constant_
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// tile shape sweep: TR rows x TC cols per tile, st.global.cs.v4 by W warps
+// (each warp instruction: 512 contiguous bytes of one row); RIGHT: a CTA's
+// consecutive tiles go along the row (else down the column block)
+template <int TR, int TC, int W, bool RIGHT>
+__global__ void __launch_bounds__(W * 32, 1) shape_kernel(float* C) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n_mt = NN / TR, n_ct = NN / TC;
+  const int64_t nt = n_mt * n_ct;
+  const int64_t t0 = nt * blockIdx.x / gridDim.x, t1 = nt * (blockIdx.x + 1) / gridDim.x;
+  for (int64_t t = t0; t < t1; ++t) {
+    const int64_t ct = RIGHT ? t % n_ct : t / n_mt, mt = RIGHT ? t / n_ct : t - (t / n_mt) * n_mt;
+    const float base = (float)(t + lane);
+    constexpr int SEG = TC / 128;  // 512-byte segments per row
+    for (int e = warp; e < TR * SEG; e += W) {
+      const int r = e / SEG, sg = e % SEG;
+      float* p = C + (mt * TR + r) * NN + ct * TC + sg * 128 + lane * 4;
+      __stcs(reinterpret_cast<float4*>(p), make_float4(base, base + 1.f, base + 2.f, base + (float)e));
+    }
+  }
+}
+
+template <int TR, int TC, int W, bool RIGHT>
+float run_shape(float* C) {
+  auto k = shape_kernel<TR, TC, W, RIGHT>;
+  for (int i = 0; i < 2; ++i) k<<<148, W * 32>>>(C);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int i = 0; i < 5; ++i) k<<<148, W * 32>>>(C);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  return ms / 5;
+}
+
 template <int MODE, int W>
 float run(Args& a, int smem) {
   auto k = store_kernel<MODE, W>;
@@ -153,6 +190,17 @@ int main() {
   rep("tma 32x32 8 warps", run<1, 8>(a, 8 * 2 * 4096));
   rep("tma 32x32 16 warps", run<1, 16>(a, 16 * 2 * 4096));
   rep("tma 64x64 4 warps", run<3, 4>(a, 4 * 2 * 16384));
+  rep("v4 128x128 down 8w", run_shape<128, 128, 8, false>(a.C));
+  rep("v4 128x128 right 8w", run_shape<128, 128, 8, true>(a.C));
+  rep("v4 128x384 down 8w", run_shape<128, 384, 8, false>(a.C));
+  rep("v4 64x256 down 8w", run_shape<64, 256, 8, false>(a.C));
+  rep("v4 32x512 down 8w", run_shape<32, 512, 8, false>(a.C));
+  rep("v4 16x1024 down 8w", run_shape<16, 1024, 8, false>(a.C));
+  rep("v4 8x2048 down 8w", run_shape<8, 2048, 8, false>(a.C));
+  rep("v4 128x128 right 16w", run_shape<128, 128, 16, true>(a.C));
+  rep("v4 32x512 right 8w", run_shape<32, 512, 8, true>(a.C));
+  rep("v4 1x65536 (rows) 8w", run_shape<1, 65536, 8, false>(a.C));
+  rep("v4 1x65536 (rows) 32w", run_shape<1, 65536, 32, false>(a.C));
   cudaFree(a.C);
   return 0;
 }
