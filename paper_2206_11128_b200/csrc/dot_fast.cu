@@ -10,14 +10,29 @@
 //   * core slices stream HBM -> shared memory with cp.async.bulk (TMA bulk
 //     copies) in chunks of 8 slices (8 KB per operand), double buffered
 //     behind an mbarrier full/empty pipeline -- each byte is read once;
-//   * warp w takes slices j = w, w+4 of every chunk:
-//       Y_j = M B_j   (lane = 2 rows x 4 columns; M rows in registers)
-//       Mw += A_j^T Y_j  (Y_j bounced through a 1 KB per-warp smem tile)
-//     with packed FFMA2 (fma.rn.f32x2) throughout;
+//   * warp w takes slices j = w, w+4 of every chunk and, on tensor cores
+//     (mma.sync m16n8k8 TF32 in split form, x = hi + lo, three MMAs per
+//     product: lo*hi + hi*lo + hi*hi), computes
+//       Y_j^T = B_j^T M^T   then   Mw += A_j^T Y_j
+//     with the K slots of each 8-chunk permuted so that the accumulator
+//     fragment of the first product IS the B-operand fragment of the second:
+//     M and Y never leave registers; each slice's A_j^T Y_j starts from a
+//     zero fragment and joins the warp's running partial with a rounded FADD
+//     (long MMA accumulations drift: cfg4 relFro 2.5e-6 against float64);
 //   * at the end of each core the per-warp partial M's are summed through
-//     shared memory and the new M is broadcast back into registers.
-// The boundary cores (rank 1 outward) use the same pipeline with rank-1
-// special cases.  norm() streams only one operand (A == B).
+//     shared memory and reloaded (split once per mode) as fragments.
+// The boundary cores (rank 1 outward) use FFMA2 (fma.rn.f32x2) special
+// cases.  norm() streams only one operand (A == B) and splits each slice's
+// fragments once for both products (the SAME instantiation).
+// TNB_DOT_SIMT=1 selects the FFMA2 body (Y bounced through a per-warp smem
+// tile; 6e-7 relFro, 2.40 vs 1.44 ms).
+//
+// Why not tcgen05: per pair the products are 16 x 16 x 16.  UMMA needs
+// M >= 64 rows sharing ONE B operand; stacking 4-8 pairs' rows gives a
+// block-diagonal product (3/4 - 7/8 of the MMA work wasted), and the second
+// product M' = sum_j A_j^T Y_j is a 16 x 16 output with a 1024-long
+// reduction -- no UMMA shape fits it.  HBM is the binding roof for dot
+// (SURVEY 8(d)); the mma.sync path runs at 0.81 of it.
 #include "common.cuh"
 
 namespace tnb {

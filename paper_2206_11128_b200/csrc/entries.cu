@@ -16,7 +16,7 @@
 
 namespace tnb {
 int launch_entries_bucketed(const ChainDev& ch, const int64_t* idx, int64_t m, float* out,
-                            int32_t* err, void* ws, int64_t ws_bytes, cudaStream_t st);
+                            int32_t* err, void* ws, int64_t ws_bytes, cudaStream_t st, bool reuse_records = false);
 bool bucketed_supported(const ChainDev& ch);
 int64_t bucketed_workspace(const ChainDev& ch, int64_t m);
 void bucketed_info(const ChainDev& ch, int64_t m, tnb_entries_info* info);
@@ -134,11 +134,62 @@ int chain_rmax(const tnb_chain* c) {
   return r;
 }
 
+// Batched chains (core.py:425-429, _step_entries_batched core.py:447-460)
+// on the bucketed kernels: batch element b is the unbatched chain whose
+// modes point b * bstride into the repacked slices.  Every element shares
+// the index matrix, so the prep / sort tile records are built once (element
+// 0) and reused; each element builds its own tables and runs the compute
+// kernel into a [B][m] scratch, which one transpose kernel turns into the
+// reference's [m][B] output.
+ChainDev element_chain(const ChainDev& ch, int64_t b) {
+  ChainDev e = ch;
+  e.batch = 1;
+  for (int k = 0; k < ch.n; ++k) {
+    e.m[k].s = ch.m[k].s + b * ch.m[k].bstride;
+    e.m[k].bstride = 0;
+  }
+  return e;
+}
+
+// out[s][b] = tmp[b][s]: thread = sample, B consecutive floats per thread
+__global__ void batch_transpose_kernel(const float* __restrict__ tmp, int64_t m, int64_t B, float* __restrict__ out) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m; s += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t b = 0; b < B; ++b) out[s * B + b] = __ldcs(tmp + b * m + s);
+}
+
+int64_t batched_tmp_offset(const ChainDev& ch, int64_t m) {
+  return (bucketed_workspace(element_chain(ch, 0), m) + 255) & ~(int64_t)255;
+}
+
 }  // namespace
+
+bool bucketed_ok(const ChainDev& ch) {
+  return ch.batch > 1 ? bucketed_supported(element_chain(ch, 0)) : bucketed_supported(ch);
+}
 
 bool use_bucketed(const ChainDev& ch, int64_t m, int algo) {
   if (algo == TNB_ALGO_BUCKETED) return true;
-  return algo == TNB_ALGO_AUTO && m >= (1 << 16) && bucketed_supported(ch);
+  return algo == TNB_ALGO_AUTO && m >= (1 << 16) && bucketed_ok(ch);
+}
+
+int launch_bucketed_any(const ChainDev& ch, const int64_t* idx, int64_t m, float* out, int32_t* err, void* ws,
+                        int64_t ws_bytes, cudaStream_t st) {
+  if (!bucketed_ok(ch)) return set_error(TNB_EINVAL, "bucketed algorithm does not support this chain");
+  if (ch.batch <= 1) return launch_entries_bucketed(ch, idx, m, out, err, ws, ws_bytes, st);
+  const int64_t off = batched_tmp_offset(ch, m);
+  const int64_t need = off + ch.batch * m * (int64_t)sizeof(float);
+  if (!ws || ws_bytes < need)
+    return set_error(TNB_EWORKSPACE, "batched bucketed entries needs %lld workspace bytes, got %lld",
+                     (long long)need, (long long)ws_bytes);
+  float* tmp = reinterpret_cast<float*>(static_cast<unsigned char*>(ws) + off);
+  for (int64_t b = 0; b < ch.batch; ++b) {
+    const int rc = launch_entries_bucketed(element_chain(ch, b), idx, m, tmp + b * m, err, ws, off, st, b > 0);
+    if (rc) return rc;
+  }
+  int64_t g = (m + 255) / 256;
+  if (g > (int64_t)num_sms() * 16) g = (int64_t)num_sms() * 16;
+  batch_transpose_kernel<<<(unsigned)(g < 1 ? 1 : g), 256, 0, st>>>(tmp, m, ch.batch, out);
+  return check_launch("batch_transpose");
 }
 
 int64_t entries_workspace(const tnb_chain* c, int64_t m, int algo, int elt) {
@@ -151,8 +202,9 @@ int64_t entries_workspace(const tnb_chain* c, int64_t m, int algo, int elt) {
   }
   if (c->n_modes <= kMaxModes && (algo == TNB_ALGO_AUTO || algo == TNB_ALGO_BUCKETED)) {
     static thread_local ChainDev ch;
-    if (make_chain_dev(c, &ch, true) == TNB_OK && use_bucketed(ch, m, algo))
-      return bucketed_supported(ch) ? bucketed_workspace(ch, m) : 0;
+    if (make_chain_dev(c, &ch, true) == TNB_OK && use_bucketed(ch, m, algo) && bucketed_ok(ch))
+      return ch.batch > 1 ? batched_tmp_offset(ch, m) + ch.batch * m * (int64_t)sizeof(float)
+                          : bucketed_workspace(ch, m);
   }
   if (pick_algo(c, algo, rmax) != TNB_ALGO_LAYERED) return 0;
   const int64_t B = c->batch > 0 ? c->batch : 1;
@@ -185,9 +237,14 @@ int entries_plan(const tnb_chain* c, int64_t m, int algo, tnb_entries_info* info
   info->diag_tables = info->table_launches = 0;
   info->compute_kernel = info->tile = 0;
   info->tensor_flops = 0.0;
-  if (use_bucketed(ch, m, algo) && bucketed_supported(ch)) {
+  if (use_bucketed(ch, m, algo) && bucketed_ok(ch)) {
     info->algo = TNB_ALGO_BUCKETED;
-    bucketed_info(ch, m, info);
+    bucketed_info(ch.batch > 1 ? element_chain(ch, 0) : ch, m, info);
+    // batched: B elements, each its own tables and compute launch
+    info->kernel_flops *= (double)ch.batch;
+    info->tensor_flops *= (double)ch.batch;
+    info->table_flops *= (double)ch.batch;
+    info->table_launches *= (int32_t)ch.batch;
     return TNB_OK;
   }
   info->kernel_flops = chain_entry_flops(ch) * (double)m;
@@ -257,13 +314,8 @@ int launch_entries(const tnb_chain* c, const int64_t* idx, int64_t m, void* out_
     return entries_generic<double>(c, ch, use, idx, m, static_cast<double*>(out_v), err, ws, ws_bytes, st);
   }
   float* out = static_cast<float*>(out_v);
-  if (algo == TNB_ALGO_AUTO && use_bucketed(ch, m, algo))
-    return launch_entries_bucketed(ch, idx, m, out, err, ws, ws_bytes, st);
-  if (use == TNB_ALGO_BUCKETED) {
-    if (!bucketed_supported(ch))
-      return set_error(TNB_EINVAL, "bucketed algorithm does not support this chain");
-    return launch_entries_bucketed(ch, idx, m, out, err, ws, ws_bytes, st);
-  }
+  if ((algo == TNB_ALGO_AUTO && use_bucketed(ch, m, algo)) || use == TNB_ALGO_BUCKETED)
+    return launch_bucketed_any(ch, idx, m, out, err, ws, ws_bytes, st);
   return entries_generic<float>(c, ch, use, idx, m, out, err, ws, ws_bytes, st);
 }
 

@@ -2487,13 +2487,17 @@ int launch_stream(const ChainDev& ch, const BPlan& bp, const unsigned char* ws, 
 
 template <int R, typename IdxT, int NT, bool FOLD>
 int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m, float* out,
-              int32_t* err, unsigned char* ws, bool stream, cudaStream_t st, cudaEvent_t tables_done) {
+              int32_t* err, unsigned char* ws, bool stream, cudaStream_t st, cudaEvent_t tables_done,
+              bool reuse_records) {
+  int rc;
+  if (reuse_records) goto compute;  // batched chains: the tile records of element 0 serve every element
+  {
   // prep: one CTA per tile; sort: one warp per (tile, sorted mode)
   const size_t psmem = prep_smem_bytes(bp.ncrow, bp.T, (int)sizeof(IdxT), bp.nw, bp.psort, bp.jpad);
   auto pk = bp.psort ? (bp.splits ? entries_prep_kernel<IdxT, true, true> : entries_prep_kernel<IdxT, true, false>)
                      : entries_prep_kernel<IdxT, false, false>;
-  int rc = check_cuda(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem),
-                      "prep smem attr");
+  rc = check_cuda(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem),
+                  "prep smem attr");
   if (rc) return rc;
   {
     KTimer kt("entries_prep", st);
@@ -2517,6 +2521,8 @@ int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m
     rc = check_launch("entries_sort");
     if (rc) return rc;
   }
+  }
+compute:
   if (tables_done) {  // the tables were built on the side stream, concurrently with prep / sort
     rc = check_cuda(cudaStreamWaitEvent(st, tables_done, 0), "join tables");
     if (rc) return rc;
@@ -2541,13 +2547,15 @@ int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m
 
 template <int R, typename IdxT>
 int launch_ri(const ChainDev& ch, const BPlan& bp, int nt, const int64_t* idx, int64_t m, float* out,
-              int32_t* err, unsigned char* ws, bool stream, cudaStream_t st, cudaEvent_t tables_done) {
+              int32_t* err, unsigned char* ws, bool stream, cudaStream_t st, cudaEvent_t tables_done,
+              bool reuse) {
   const int N = ch.n;
   const bool fold = !stream && (R & 3) == 0 && N >= 3 && ch.m[N - 2].layout == TNB_LAYOUT_DIAG &&
                     ch.m[N - 1].rl == R && ch.m[N - 1].rr == 1;
   (void)nt;
-  if (fold) return launch_rt<R, IdxT, kComputeThreads, true>(ch, bp, idx, m, out, err, ws, stream, st, tables_done);
-  return launch_rt<R, IdxT, kComputeThreads, false>(ch, bp, idx, m, out, err, ws, stream, st, tables_done);
+  if (fold)
+    return launch_rt<R, IdxT, kComputeThreads, true>(ch, bp, idx, m, out, err, ws, stream, st, tables_done, reuse);
+  return launch_rt<R, IdxT, kComputeThreads, false>(ch, bp, idx, m, out, err, ws, stream, st, tables_done, reuse);
 }
 
 }  // namespace
@@ -2651,7 +2659,7 @@ int table_stream_env() {
 }
 
 int launch_entries_bucketed(const ChainDev& ch, const int64_t* idx, int64_t m, float* out,
-                            int32_t* err, void* ws, int64_t ws_bytes, cudaStream_t st) {
+                            int32_t* err, void* ws, int64_t ws_bytes, cudaStream_t st, bool reuse_records) {
   EPlan P;
   int rc = plan_entries(ch, m, &P);
   if (rc) return rc;
@@ -2699,20 +2707,20 @@ int launch_entries_bucketed(const ChainDev& ch, const int64_t* idx, int64_t m, f
   const bool small = bp.idx_bytes == 1;
   switch (R) {
     case 8:
-      rc = small ? launch_ri<8, uint8_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables)
-                 : launch_ri<8, uint16_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables);
+      rc = small ? launch_ri<8, uint8_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables, reuse_records)
+                 : launch_ri<8, uint16_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables, reuse_records);
       break;
     case 16:
-      rc = small ? launch_ri<16, uint8_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables)
-                 : launch_ri<16, uint16_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables);
+      rc = small ? launch_ri<16, uint8_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables, reuse_records)
+                 : launch_ri<16, uint16_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables, reuse_records);
       break;
     case 24:
-      rc = small ? launch_ri<24, uint8_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables)
-                 : launch_ri<24, uint16_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables);
+      rc = small ? launch_ri<24, uint8_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables, reuse_records)
+                 : launch_ri<24, uint16_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables, reuse_records);
       break;
     default:
-      rc = small ? launch_ri<32, uint8_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables)
-                 : launch_ri<32, uint16_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables);
+      rc = small ? launch_ri<32, uint8_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables, reuse_records)
+                 : launch_ri<32, uint16_t>(chv, bp, nt, idx, m, out, err, w, stream, st, tables, reuse_records);
   }
   // a failed launch may return before its own join: the side stream's table
   // writes must still be ordered before anything the caller does with ws

@@ -42,10 +42,8 @@ def test_golden_full_norm(name):
 def test_golden_entries(name, algo):
     c = G.case(name)
     t = facade(c["nodes"], c["batch"])
-    if algo == N.ALGO_BUCKETED and c["batch"] is not None:
-        with pytest.raises(tb.ContractViolationError, match="bucketed"):
-            tb.entries(t, c["out"]["idx"], algo=algo)
-        return
+    # batched chains run the bucketed kernels per batch element too
+    # (shared tile records, per-element tables, [m][B] transpose)
     got = tb.entries(t, c["out"]["idx"], algo=algo)
     assert_close(got, c["out"]["entries"], what=f"{name} entries algo={algo}")
 
@@ -603,3 +601,34 @@ def test_full_tall_thin_generic_gemm(monkeypatch):
     a, b = nodes[0][1][0].astype(np.float64), nodes[1][1][:, :, 0].astype(np.float64)
     sel = np.r_[0:4096, (1 << 24) - 4096:(1 << 24)]
     assert_close(got[sel], a[sel] @ b, what="tall thin full")
+
+
+@pytest.mark.parametrize("batch,shape,rank,m", [
+    (3, (32,) * 6, 32, (1 << 16) + 5),      # state kernel, r=32 tensor-core modes, merged tables
+    (5, (16,) * 7, 16, 70001),              # state kernel, R=16
+    (2, (2048, 40, 2048), 24, 1 << 17),     # stream kernel
+    (4, (32,) * 10, 32, 1 << 18),           # the cfg2 chain shape
+])
+def test_batched_bucketed_entries(batch, shape, rank, m):
+    # _step_entries_batched (core.py:447-460) on the bucketed path: output
+    # [m, B]; every element's column equals the unbatched chain of that
+    # element, bitwise (same kernels, same plan)
+    cores = O.random_tt(shape, rank, seed=rank + batch, batch_size=batch, scale=rank ** -0.5)
+    t = facade([("tt", c, None) for c in cores], batch)
+    o = O.make_chain([("tt", c) for c in cores], batch)
+    plan = N.entries_plan(t._packed().chain, m, N.ALGO_AUTO)
+    assert plan["algo"] == N.ALGO_BUCKETED, plan
+    idx = O.uniform_indices(shape, m, 21)
+    idx[::9] -= np.asarray(shape)
+    got = tb.entries(t, idx)
+    assert tuple(got.shape) == (m, batch)
+    sel = np.arange(0, m, max(1, m // 4000))
+    assert_close(to_np(got)[sel], O.entries(o, idx[sel]), what=f"batched bucketed B={batch}")
+    dev_idx = torch.from_numpy(idx).cuda()
+    for b in (0, batch - 1):
+        tb1 = facade([("tt", c[b], None) for c in cores])
+        assert torch.equal(got[:, b], tb.entries(tb1, dev_idx)), b
+    bad = idx.copy()
+    bad[m // 2, 1] = shape[1]
+    with pytest.raises(tb.ContractViolationError, match="mode 1"):
+        tb.entries(t, bad)

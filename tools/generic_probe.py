@@ -44,7 +44,7 @@ for algo, nm in ((N.ALGO_CHAIN, "chain"), (N.ALGO_LAYERED, "layered")):
     line(f"entries cfg2-shape B=4 algo={nm}", ev(lambda: tb.entries(t, idx, algo=algo)), m * 4, "entries")
 t64 = tt((256,) * 4, 64)
 i64 = torch.randint(0, 256, (m, 4), device="cuda")
-for algo, nm in ((N.ALGO_AUTO, "auto"), (N.ALGO_CHAIN, "chain"), (N.ALGO_LAYERED, "layered")):
+for algo, nm in ((N.ALGO_AUTO, "auto"), (N.ALGO_LAYERED, "layered")):
     line(f"entries cfg3 chain r=64 m=2^20 algo={nm}", ev(lambda: tb.entries(t64, i64, algo=algo)), m, "entries")
 for r in (8, 16, 24, 32):
     a, b = tt((64,) * 16, r, batch=1024, scale=0.25), tt((64,) * 16, r, batch=1024, scale=0.25, seed=1)
