@@ -6,6 +6,8 @@
 // the two-stage contraction numpy's einsum path picks for the reference
 // (Y = M B_j, then M' += A_j^T Y).  One CTA per pair; the
 // transfer matrices live in shared memory, core slices stream from HBM once.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace tnb {
@@ -78,6 +80,150 @@ __global__ void __launch_bounds__(256) dot_kernel(const __grid_constant__ ChainD
   }
 }
 
+// Chunked kernel for dense chains of any rank (the rank-16 mma.sync kernel
+// covers r = 16 fp32 only): per mode, CH slices of A and B at a time are
+// staged in shared memory with coalesced 16-byte loads, then
+//   Y_j[a][d] = sum_b M[a][b] B_j[b][d]          (all CH slices)
+//   M'[c][d] += sum_{j in chunk, a} A_j[a][c] Y_j[a][d]
+// each thread computing VW consecutive d (one 16-byte shared load of B / Y
+// per VW FMAs; A and M entries broadcast).  Three barriers per CH slices
+// instead of two per slice; persistent CTAs, several per SM.
+template <typename T>
+struct Vec;
+template <>
+struct Vec<float> {
+  using V = float4;
+  static constexpr int W = 4;
+  __device__ static void fma(const float s, const V& b, float* acc) {
+    acc[0] = fmaf(s, b.x, acc[0]);
+    acc[1] = fmaf(s, b.y, acc[1]);
+    acc[2] = fmaf(s, b.z, acc[2]);
+    acc[3] = fmaf(s, b.w, acc[3]);
+  }
+};
+template <>
+struct Vec<double> {
+  using V = double2;
+  static constexpr int W = 2;
+  __device__ static void fma(const double s, const V& b, double* acc) {
+    acc[0] = ::fma(s, b.x, acc[0]);
+    acc[1] = ::fma(s, b.y, acc[1]);
+  }
+};
+
+template <typename T>
+__device__ __forceinline__ void stage(T* dst, const T* __restrict__ src, int64_t count, int tid, int nt) {
+  // 16-byte pieces (both ends 16-byte aligned by construction), scalar tail
+  using V = typename Vec<T>::V;
+  constexpr int W = Vec<T>::W;
+  const int64_t nv = count / W;
+  for (int64_t i = tid; i < nv; i += nt) reinterpret_cast<V*>(dst)[i] = __ldg(reinterpret_cast<const V*>(src) + i);
+  for (int64_t i = nv * W + tid; i < count; i += nt) dst[i] = __ldg(src + i);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) dot_chunk_kernel(const __grid_constant__ ChainDev A,
+                                                        const __grid_constant__ ChainDev Bc, T* __restrict__ out,
+                                                        int is_norm, int mcap, int scap) {
+  using V = typename Vec<T>::V;
+  constexpr int W = Vec<T>::W;
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  T* M = reinterpret_cast<T*>(sm_raw);
+  T* Mn = M + mcap;
+  T* As = Mn + mcap;
+  T* Bs = As + scap;
+  T* Ys = Bs + scap;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int64_t e = blockIdx.x; e < A.batch; e += gridDim.x) {
+    if (tid == 0) M[0] = T(1);
+    __syncthreads();
+    for (int k = 0; k < A.n; ++k) {
+      const ModeDev& ma = A.m[k];
+      const ModeDev& mb = Bc.m[k];
+      const int ral = ma.rl, rar = ma.rr, rbl = mb.rl, rbr = mb.rr, J = ma.J;
+      const T* ga = reinterpret_cast<const T*>(ma.s) + e * ma.bstride;
+      const T* gb = reinterpret_cast<const T*>(mb.s) + e * mb.bstride;
+      const int sa = ral * rar, sb = rbl * rbr, sy = ral * rbr;
+      int CH = scap / (sa > sb ? (sa > sy ? sa : sy) : (sb > sy ? sb : sy));
+      CH = CH < 1 ? 1 : (CH > J ? J : CH);
+      const int dv = (rbr % W == 0) ? rbr / W : 0;  // vector groups per row (0: scalar rows)
+      for (int t = tid; t < rar * rbr; t += nt) Mn[t] = T(0);
+      for (int j0 = 0; j0 < J; j0 += CH) {
+        const int nj = J - j0 < CH ? J - j0 : CH;
+        __syncthreads();  // previous chunk done with As / Bs / Ys
+        stage(As, ga + (int64_t)j0 * sa, (int64_t)nj * sa, tid, nt);
+        stage(Bs, gb + (int64_t)j0 * sb, (int64_t)nj * sb, tid, nt);
+        __syncthreads();
+        if (dv) {
+          const int groups = nj * ral * dv;
+          for (int g = tid; g < groups; g += nt) {
+            const int j = g / (ral * dv), r = g - j * (ral * dv), a = r / dv, d0 = (r - a * dv) * W;
+            T acc[W];
+#pragma unroll
+            for (int q = 0; q < W; ++q) acc[q] = T(0);
+            const T* bj = Bs + j * sb + d0;
+            for (int b = 0; b < rbl; ++b)
+              Vec<T>::fma(M[a * rbl + b], *reinterpret_cast<const V*>(bj + b * rbr), acc);
+            *reinterpret_cast<V*>(Ys + j * sy + a * rbr + d0) = *reinterpret_cast<V*>(acc);
+          }
+        } else {
+          for (int t = tid; t < nj * sy; t += nt) {
+            const int j = t / sy, r = t - j * sy, a = r / rbr, d = r - a * rbr;
+            T acc = T(0);
+            for (int b = 0; b < rbl; ++b) acc = fmat(M[a * rbl + b], Bs[j * sb + b * rbr + d], acc);
+            Ys[j * sy + r] = acc;
+          }
+        }
+        __syncthreads();
+        if (dv) {
+          for (int g = tid; g < rar * dv; g += nt) {
+            const int c = g / dv, d0 = (g - c * dv) * W;
+            T acc[W];
+#pragma unroll
+            for (int q = 0; q < W; ++q) acc[q] = T(0);
+            for (int j = 0; j < nj; ++j) {
+              const T* aj = As + j * sa + c;
+              const T* yj = Ys + j * sy + d0;
+              for (int a = 0; a < ral; ++a) Vec<T>::fma(aj[a * rar], *reinterpret_cast<const V*>(yj + a * rbr), acc);
+            }
+#pragma unroll
+            for (int q = 0; q < W; ++q) Mn[c * rbr + d0 + q] += acc[q];
+          }
+        } else {
+          for (int t = tid; t < rar * rbr; t += nt) {
+            const int c = t / rbr, d = t - c * rbr;
+            T acc = T(0);
+            for (int j = 0; j < nj; ++j)
+              for (int a = 0; a < ral; ++a) acc = fmat(As[j * sa + a * rar + c], Ys[j * sy + a * rbr + d], acc);
+            Mn[t] += acc;
+          }
+        }
+      }
+      __syncthreads();
+      for (int t = tid; t < rar * rbr; t += nt) M[t] = Mn[t];
+      __syncthreads();
+    }
+    if (tid == 0) {
+      const T v = M[0];
+      out[e] = is_norm ? sqrt_pos(v) : v;
+    }
+    __syncthreads();
+  }
+}
+
+bool chunk_ok(const ChainDev& a, const ChainDev& b, int elt) {
+  for (int k = 0; k < a.n; ++k) {
+    const ModeDev &ma = a.m[k], &mb = b.m[k];
+    if (ma.layout != TNB_LAYOUT_DENSE || mb.layout != TNB_LAYOUT_DENSE) return false;
+    // 16-byte staging: slice runs, batch strides and chunk starts 16-byte aligned
+    if ((reinterpret_cast<uintptr_t>(ma.s) & 15) || (reinterpret_cast<uintptr_t>(mb.s) & 15)) return false;
+    if (((ma.bstride * elt) & 15) || ((mb.bstride * elt) & 15)) return false;
+    if (ma.J > 1 && (((int64_t)ma.rl * ma.rr * elt) & 15)) return false;
+    if (mb.J > 1 && (((int64_t)mb.rl * mb.rr * elt) & 15)) return false;
+  }
+  return true;
+}
+
 }  // namespace
 
 int launch_dot(const tnb_chain* a, const tnb_chain* b, void* out, bool is_norm, cudaStream_t st, int elt) {
@@ -97,6 +243,40 @@ int launch_dot(const tnb_chain* a, const tnb_chain* b, void* out, bool is_norm, 
   const char* gen = getenv("TNB_DOT_GENERIC");
   if (elt == 4 && !(gen && gen[0] == '1') && dot_fast_supported(ca, cb))
     return launch_dot_fast(ca, cb, static_cast<float*>(out), is_norm, st);
+  const char* chk = getenv("TNB_DOT_CHUNK");
+  if (!(chk && chk[0] == '0') && chunk_ok(ca, cb, elt)) {
+    int mcap = 1, scap_min = 1;
+    for (int k = 0; k < a->n_modes; ++k) {
+      const tnb_mode &x = a->modes[k], &y = b->modes[k];
+      const int s4[4] = {x.r_left * y.r_left, x.r_right * y.r_right, x.r_left * x.r_right, y.r_left * y.r_right};
+      mcap = std::max(mcap, std::max(s4[0], s4[1]));
+      scap_min = std::max(scap_min, std::max(std::max(s4[2], s4[3]), x.r_left * y.r_right));
+    }
+    mcap = (mcap + 3) & ~3;
+    // staged operand capacity: ~16 KB of fp32 (8 KB of fp64 values -- 16 KB) per operand, at least one slice
+    const int scap = ((std::max(scap_min, 16384 / 4) + 3) & ~3);
+    const size_t smem = ((size_t)2 * mcap + 3 * (size_t)scap) * (size_t)elt;
+    if (smem <= 200 * 1024) {
+      const int64_t B = ca.batch;
+      int per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / smem));
+      const int64_t slots = (int64_t)num_sms() * per_sm;
+      const int grid = (int)(B < slots ? B : slots);
+      if (elt == 8) {
+        rc = check_cuda(cudaFuncSetAttribute(dot_chunk_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem), "dot smem attr");
+        if (rc) return rc;
+        dot_chunk_kernel<double><<<grid, 256, smem, st>>>(ca, cb, static_cast<double*>(out), is_norm ? 1 : 0, mcap,
+                                                          scap);
+      } else {
+        rc = check_cuda(cudaFuncSetAttribute(dot_chunk_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem), "dot smem attr");
+        if (rc) return rc;
+        dot_chunk_kernel<float><<<grid, 256, smem, st>>>(ca, cb, static_cast<float*>(out), is_norm ? 1 : 0, mcap,
+                                                         scap);
+      }
+      return check_launch("dot_chunk");
+    }
+  }
   int cap = 1;
   for (int k = 0; k < a->n_modes; ++k) {
     const int ral = a->modes[k].r_left, rar = a->modes[k].r_right;

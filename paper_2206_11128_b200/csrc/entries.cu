@@ -21,6 +21,11 @@ bool bucketed_supported(const ChainDev& ch);
 int64_t bucketed_workspace(const ChainDev& ch, int64_t m);
 void bucketed_info(const ChainDev& ch, int64_t m, tnb_entries_info* info);
 double chain_entry_flops(const ChainDev& ch);
+bool two_table_ok(const ChainDev& ch, int64_t m);
+int64_t two_table_workspace(const ChainDev& ch, int64_t m);
+void two_table_info(const ChainDev& ch, int64_t m, tnb_entries_info* info);
+int launch_two_table(const ChainDev& ch, const int64_t* idx, int64_t m, float* out, int32_t* err, void* ws,
+                     int64_t ws_bytes, cudaStream_t st);
 
 namespace {
 
@@ -167,6 +172,12 @@ bool bucketed_ok(const ChainDev& ch) {
   return ch.batch > 1 ? bucketed_supported(element_chain(ch, 0)) : bucketed_supported(ch);
 }
 
+// AUTO: chains that merge into a prefix and a suffix table (any rank) run
+// the fused two-table kernel
+bool use_two_table(const tnb_chain* c, const ChainDev& ch, int64_t m, int algo) {
+  return algo == TNB_ALGO_AUTO && c->n_modes <= kMaxModes && m >= (1 << 12) && two_table_ok(ch, m);
+}
+
 bool use_bucketed(const ChainDev& ch, int64_t m, int algo) {
   if (algo == TNB_ALGO_BUCKETED) return true;
   return algo == TNB_ALGO_AUTO && m >= (1 << 16) && bucketed_ok(ch);
@@ -202,6 +213,7 @@ int64_t entries_workspace(const tnb_chain* c, int64_t m, int algo, int elt) {
   }
   if (c->n_modes <= kMaxModes && (algo == TNB_ALGO_AUTO || algo == TNB_ALGO_BUCKETED)) {
     static thread_local ChainDev ch;
+    if (make_chain_dev(c, &ch, true) == TNB_OK && use_two_table(c, ch, m, algo)) return two_table_workspace(ch, m);
     if (make_chain_dev(c, &ch, true) == TNB_OK && use_bucketed(ch, m, algo) && bucketed_ok(ch))
       return ch.batch > 1 ? batched_tmp_offset(ch, m) + ch.batch * m * (int64_t)sizeof(float)
                           : bucketed_workspace(ch, m);
@@ -237,6 +249,11 @@ int entries_plan(const tnb_chain* c, int64_t m, int algo, tnb_entries_info* info
   info->diag_tables = info->table_launches = 0;
   info->compute_kernel = info->tile = 0;
   info->tensor_flops = 0.0;
+  if (c->n_modes <= kMaxModes && use_two_table(c, ch, m, algo)) {
+    info->algo = TNB_ALGO_BUCKETED;
+    two_table_info(ch, m, info);
+    return TNB_OK;
+  }
   if (use_bucketed(ch, m, algo) && bucketed_ok(ch)) {
     info->algo = TNB_ALGO_BUCKETED;
     bucketed_info(ch.batch > 1 ? element_chain(ch, 0) : ch, m, info);
@@ -314,6 +331,7 @@ int launch_entries(const tnb_chain* c, const int64_t* idx, int64_t m, void* out_
     return entries_generic<double>(c, ch, use, idx, m, static_cast<double*>(out_v), err, ws, ws_bytes, st);
   }
   float* out = static_cast<float*>(out_v);
+  if (use_two_table(c, ch, m, algo)) return launch_two_table(ch, idx, m, out, err, ws, ws_bytes, st);
   if ((algo == TNB_ALGO_AUTO && use_bucketed(ch, m, algo)) || use == TNB_ALGO_BUCKETED)
     return launch_bucketed_any(ch, idx, m, out, err, ws, ws_bytes, st);
   return entries_generic<float>(c, ch, use, idx, m, out, err, ws, ws_bytes, st);

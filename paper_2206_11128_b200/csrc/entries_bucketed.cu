@@ -2728,4 +2728,162 @@ int launch_entries_bucketed(const ChainDev& ch, const int64_t* idx, int64_t m, f
   return rc;
 }
 
+
+// ---------------------------------------------------------------------------
+// Two-table chains.  When mode merging leaves a virtual chain of TWO modes
+// -- a prefix table P[(j_0..j_{a-1})][R] and a suffix table
+// S[(j_a..j_{n-1})][R] (either may be an original boundary mode) -- every
+// entry is one dot product of two gathered rows, for ANY rank R (the state /
+// stream kernels stop at R = 32; a rank-64 cfg3 chain of 4 modes lands here
+// with 65536-row tables).  One fused kernel per call after the tables:
+// thread = sample; it reads its int64 index row, wraps negatives, checks
+// every ORIGINAL mode (lowest OOB mode -> err, core.py:409-416), combines the
+// C-order row numbers and accumulates <P[p], S[q]> in 16-byte pieces.
+struct TwoTab {
+  const float* P;
+  const float* S;
+  int32_t n, a, R;
+  int32_t J[kMaxModes];
+  int64_t stride[kMaxModes];  // C-order weight of mode k inside its group
+};
+
+template <bool VEC>
+__global__ void __launch_bounds__(256) two_table_kernel(const __grid_constant__ TwoTab tt, const int64_t* __restrict__ idx,
+                                                        int64_t m, float* __restrict__ out, int32_t* __restrict__ err) {
+  const int n = tt.n, R = tt.R;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m; s += (int64_t)gridDim.x * blockDim.x) {
+    int64_t p = 0, q = 0;
+    int bad = n;
+    const int64_t* row = idx + s * n;
+    for (int k = 0; k < n; ++k) {
+      int64_t x = __ldcs(row + k);
+      const int64_t J = tt.J[k];
+      if (x < 0) x += J;
+      if ((x < 0 || x >= J) && bad == n) bad = k;
+      x = x < 0 ? 0 : (x >= J ? J - 1 : x);
+      if (k < tt.a) p += x * tt.stride[k];
+      else q += x * tt.stride[k];
+    }
+    if (bad < n) {
+      atomicMin(err, bad);
+      continue;
+    }
+    const float* pr = tt.P + p * R;
+    const float* qr = tt.S + q * R;
+    float acc0 = 0.f, acc1 = 0.f;
+    if (VEC) {
+      for (int c = 0; c < R; c += 4) {
+        const float4 u = __ldg(reinterpret_cast<const float4*>(pr + c));
+        const float4 v = __ldg(reinterpret_cast<const float4*>(qr + c));
+        acc0 = fmaf(u.x, v.x, acc0);
+        acc1 = fmaf(u.y, v.y, acc1);
+        acc0 = fmaf(u.z, v.z, acc0);
+        acc1 = fmaf(u.w, v.w, acc1);
+      }
+    } else {
+      for (int c = 0; c < R; ++c) acc0 = fmaf(__ldg(pr + c), __ldg(qr + c), acc0);
+    }
+    out[s] = acc0 + acc1;
+  }
+}
+
+namespace {
+bool two_table_plan(const ChainDev& ch, int64_t m, MergePlan* mp) {
+  if (ch.batch != 1 || ch.n < 2 || ch.n > kMaxModes) return false;
+  for (int k = 0; k < ch.n; ++k)
+    if (ch.m[k].bstride != 0 || ch.m[k].J <= 0) return false;
+  plan_merge(ch, m, mp);
+  if (mp->ng != 2) return false;
+  const int R = ch.m[mp->hi[0] - 1].rr;
+  return R >= 1 && R <= 4096 && ch.m[mp->lo[1]].rl == R;
+}
+}  // namespace
+
+bool two_table_ok(const ChainDev& ch, int64_t m) {
+  MergePlan mp;
+  return two_table_plan(ch, m, &mp);
+}
+
+int64_t two_table_workspace(const ChainDev& ch, int64_t m) {
+  MergePlan mp;
+  return two_table_plan(ch, m, &mp) ? mp.table_bytes : 0;
+}
+
+void two_table_info(const ChainDev& ch, int64_t m, tnb_entries_info* info) {
+  MergePlan mp;
+  two_table_plan(ch, m, &mp);
+  ChainDev v;
+  virtual_chain(ch, mp, nullptr, &v);
+  info->n_virtual = 2;
+  info->prefix_modes = mp.a();
+  info->suffix_modes = mp.b();
+  info->prefix_rows = mp.a() > 1 ? mp.rows[0] : 0;
+  info->suffix_rows = mp.b() > 1 ? mp.rows[1] : 0;
+  info->compute_kernel = 2;
+  info->tile = 0;
+  info->tensor_flops = 0.0;
+  info->diag_tables = 0;
+  info->table_launches = table_launches(mp);
+  info->kernel_flops = 2.0 * v.m[0].rr * (double)m;
+  double tf = 0.0;
+  if (mp.kind[0] == kPrefix) {
+    int64_t rows = ch.m[0].J;
+    for (int o = 1; o < mp.hi[0]; ++o) {
+      rows *= ch.m[o].J;
+      tf += (double)rows * ch.m[o].rr * (ch.m[o].layout == TNB_LAYOUT_DIAG ? 1.0 : 2.0 * ch.m[o].rl);
+    }
+  }
+  if (mp.kind[1] == kSuffix) {
+    int64_t rows = ch.m[ch.n - 1].J;
+    for (int o = ch.n - 2; o >= mp.lo[1]; --o) {
+      rows *= ch.m[o].J;
+      tf += (double)rows * ch.m[o].rl * (ch.m[o].layout == TNB_LAYOUT_DIAG ? 1.0 : 2.0 * ch.m[o].rr);
+    }
+  }
+  info->table_flops = tf;
+}
+
+int launch_two_table(const ChainDev& ch, const int64_t* idx, int64_t m, float* out, int32_t* err, void* ws,
+                     int64_t ws_bytes, cudaStream_t st) {
+  MergePlan mp;
+  if (!two_table_plan(ch, m, &mp)) return set_error(TNB_EINVAL, "chain does not reduce to two tables");
+  if (mp.table_bytes && (!ws || ws_bytes < mp.table_bytes))
+    return set_error(TNB_EWORKSPACE, "two-table entries needs %lld workspace bytes, got %lld",
+                     (long long)mp.table_bytes, (long long)ws_bytes);
+  unsigned char* base = static_cast<unsigned char*>(ws);
+  int rc = build_tables(ch, mp, base, st);
+  if (rc) return rc;
+  ChainDev v;
+  virtual_chain(ch, mp, base, &v);
+  TwoTab tt;
+  tt.P = v.m[0].s;
+  tt.S = v.m[1].s;
+  tt.n = ch.n;
+  tt.a = mp.hi[0];
+  tt.R = v.m[0].rr;
+  int64_t w = 1;
+  for (int k = tt.a - 1; k >= 0; --k) {
+    tt.stride[k] = w;
+    w *= ch.m[k].J;
+  }
+  w = 1;
+  for (int k = ch.n - 1; k >= tt.a; --k) {
+    tt.stride[k] = w;
+    w *= ch.m[k].J;
+  }
+  for (int k = 0; k < ch.n; ++k) tt.J[k] = ch.m[k].J;
+  int64_t g = ceil_div(m, 256);
+  if (g > (int64_t)num_sms() * 16) g = (int64_t)num_sms() * 16;
+  const bool vec = (tt.R & 3) == 0 && (reinterpret_cast<uintptr_t>(tt.P) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(tt.S) & 15) == 0;
+  {
+    KTimer kt("entries_compute", st);
+    if (vec)
+      two_table_kernel<true><<<(unsigned)(g < 1 ? 1 : g), 256, 0, st>>>(tt, idx, m, out, err);
+    else
+      two_table_kernel<false><<<(unsigned)(g < 1 ? 1 : g), 256, 0, st>>>(tt, idx, m, out, err);
+  }
+  return check_launch("two_table");
+}
+
 }  // namespace tnb

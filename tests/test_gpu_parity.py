@@ -632,3 +632,67 @@ def test_batched_bucketed_entries(batch, shape, rank, m):
     bad[m // 2, 1] = shape[1]
     with pytest.raises(tb.ContractViolationError, match="mode 1"):
         tb.entries(t, bad)
+
+
+@pytest.mark.parametrize("rank", [5, 8, 24, 32, 40])
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_dot_norm_rank_general(rank, dtype):
+    # chains of ranks other than 16 (the mma.sync kernel's) on the chunked
+    # kernel (16-byte staged slices; rank 5 takes the scalar rows, 40 the
+    # one-slice chunks); core.py:362-391
+    batch = 37
+    a = O.random_tt((24, 17, 33, 9, 20), rank, seed=rank, batch_size=batch, scale=rank ** -0.5)
+    b = O.random_tt((24, 17, 33, 9, 20), rank + 1, seed=rank + 1, batch_size=batch, scale=(rank + 1) ** -0.5)
+    dt = torch.float64 if dtype == "f64" else torch.float32
+    ta = tb.TnTensor([tb.ModeNode("tt", c, batched=True, dtype=dt) for c in a], batch)
+    tb_ = tb.TnTensor([tb.ModeNode("tt", c, batched=True, dtype=dt) for c in b], batch)
+    oa, ob = O.make_chain([("tt", c) for c in a], batch), O.make_chain([("tt", c) for c in b], batch)
+    tol = 1e-12 if dtype == "f64" else 1e-5
+    assert_dot_close(tb.dot(ta, tb_), O.chain_dot(oa, ob), O.norm(oa) * O.norm(ob), tol=tol, what=f"dot r{rank}")
+    assert_close(tb.norm(ta), O.norm(oa), tol=tol, what=f"norm r{rank}")
+    u = tb.TnTensor([tb.ModeNode("tt", c[3], dtype=dt) for c in a])
+    ou = O.make_chain([("tt", c[3]) for c in a])
+    assert abs(tb.norm(u) - O.norm(ou)) <= tol * O.norm(ou)
+
+
+@pytest.mark.parametrize("case", ["cfg3_r64", "two_modes", "cp_ends", "odd_rank", "negatives"])
+def test_two_table_entries(case):
+    # chains whose mode merging leaves a prefix and a suffix table: the fused
+    # two-table kernel, any rank (core.py:394-444)
+    rng = np.random.default_rng(31)
+    if case == "cfg3_r64":
+        cores = O.random_tt((256,) * 4, 64, seed=0, scale=64 ** -0.5)
+        nodes = [("tt", c, None) for c in cores]
+        m = 1 << 20
+    elif case == "two_modes":
+        nodes = [("tt", rng.standard_normal((1, 3000, 48)).astype(np.float32), None),
+                 ("tt", rng.standard_normal((48, 2500, 1)).astype(np.float32), None)]
+        m = 1 << 16
+    elif case == "cp_ends":
+        nodes = [("cp", rng.standard_normal((40, 12)).astype(np.float32), rng.standard_normal((70, 40)).astype(np.float32)),
+                 ("tt", (rng.standard_normal((12, 30, 12)) * 0.3).astype(np.float32), None),
+                 ("cp", rng.standard_normal((50, 12)).astype(np.float32), None)]
+        m = 100003
+    elif case == "odd_rank":
+        cores = O.random_tt((64, 30, 64), 37, seed=3, scale=37 ** -0.5)
+        nodes = [("tt", c, None) for c in cores]
+        m = 70001
+    else:
+        cores = O.random_tt((16,) * 6, 8, seed=4, scale=8 ** -0.5)
+        nodes = [("tt", c, None) for c in cores]
+        m = 1 << 17
+    t = facade(nodes)
+    o = O.make_chain(nodes)
+    plan = N.entries_plan(t._packed().chain, m, N.ALGO_AUTO)
+    assert (plan["compute_kernel"], plan["n_virtual"]) == (2, 2), plan
+    idx = O.uniform_indices(t.shape, m, 7)
+    idx[::3] -= np.asarray(t.shape)
+    got = to_np(tb.entries(t, idx))
+    sel = np.arange(0, m, max(1, m // 5000))
+    assert_close(got[sel], O.entries(o, idx[sel]), what=case)
+    for k in range(t.ndim):
+        bad = idx.copy()
+        bad[m // 2, k] = t.shape[k]
+        bad[m // 3, t.ndim - 1] = -t.shape[-1] - 1
+        with pytest.raises(tb.ContractViolationError, match=f"mode {min(k, t.ndim - 1)}"):
+            tb.entries(t, bad)
