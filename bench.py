@@ -399,8 +399,8 @@ def bench_entries(args, cfg, dev, dist, ws, rank, gate_rows=None):
     assert int(err.item()) >= t.ndim, "bench inputs must be in bounds"
     ms_step = ms / args.steps
     value = total / (ms_step * 1e-3)
-    stream_k = plan["compute_kernel"] == 1
-    kname = "entries_stream_kernel" if stream_k else "entries_compute_kernel"
+    kname = {0: "entries_compute_kernel", 1: "entries_stream_kernel", 2: "two_table_kernel"}.get(
+        plan["compute_kernel"], "entries_compute_kernel")
     kms, kn = kt["entries_compute"]
     if kn:  # bucketed: the per-entry compute kernel, timed on its own stream
         k_ms = kms / kn
@@ -532,6 +532,58 @@ def entries_secondary(args, dev, dist, ws, rank):
     if "parity_gate" in f:
         res["parity_gate"] = f["parity_gate"]
     return res
+
+
+def bench_entries_batched(dev, steps, warmup, B=16, m=1 << 20):
+    """Batched-chain entries (core.py:425-429, 447-460): a batch of B cfg2-shape
+    chains (N=10, I=32, r=32) on the same 2^20 tuples, output [m, B], on the
+    bucketed kernels (shared tile records, per-element tables / compute)."""
+    import torch
+
+    import paper_2206_11128_b200 as tb
+    from paper_2206_11128_b200 import _native as N
+    from paper_2206_11128_b200 import core as C
+
+    seed = W.base_seed()
+    shape = W.CONFIGS["cfg2"][1]
+    cores = W.tt_cores(shape, 32, seed + 7, batch_size=B)
+    t = tb.TnTensor([tb.ModeNode("tt", c, batched=True) for c in cores], B)
+    p = t._packed()
+    idx_np = W.indices(shape, m, seed + 8)
+    idx = torch.from_numpy(idx_np).to(dev)
+    out = torch.empty((m, B), dtype=torch.float32, device=dev)
+    err = torch.empty(1, dtype=torch.int32, device=dev)
+    plan = N.entries_plan(p.chain, m)
+    wsbuf = [None]
+
+    def step():
+        wsbuf[0] = C.launch_entries(p, idx, out, err, 0, wsbuf[0])
+
+    ms = timed_steps(step, steps, warmup, torch.cuda.current_stream(dev), False, kernel_timing=True) / steps
+    kt = {k: N.timing_read(k) for k in ("entries_prep", "entries_sort", "entries_compute", "entries_tables")}
+    N.timing_enable(False)
+    kms, kn = kt["entries_compute"]
+    k_ms = kms / steps if kn else ms  # the B compute launches of one step
+    fpk, fsrc = fp32_peak()
+    pipes = [{"bound": "tensor", "work": plan["tensor_flops"], "unit": "TFLOP/s", "peak": TC_TF32_PEAK,
+              "peak_source": "measured (profiles/peaks_r01.json, tools/peaks.cu mma.sync m16n8k8 tf32)",
+              "what": "split-TF32 mma.sync work of the sorted modes over the B compute launches"},
+             {"bound": "fp32", "work": plan["kernel_flops"] - plan["tensor_flops"] / 3, "unit": "TFLOP/s",
+              "peak": fpk, "peak_source": fsrc, "what": "FFMA work outside the tensor-core modes"}]
+    roof = pick_roof("entries_compute_kernel x B", k_ms, pipes,
+                     extra={"kernel_share_of_step": k_ms / ms,
+                            "plan": {k: plan[k] for k in ("algo", "n_virtual", "prefix_rows", "suffix_rows",
+                                                          "compute_kernel")}})
+    from oracle import tntz_oracle as O
+
+    sel = np.linspace(0, m - 1, 4096).astype(np.int64)
+    o = O.make_chain([("tt", c) for c in cores], B)
+    ref = O.entries(o, idx_np[sel])
+    pg = gate(O.rel_errors(out.double().cpu().numpy()[sel], ref))
+    return {"op": "entries_batched", "workload": f"B={B} cfg2-shape chains (N=10, I=32, r=32), {m} tuples, "
+                                                 f"output [m, B]", "ms_per_step": ms,
+            "entries/s": m * B / (ms * 1e-3), "roofline": roof,
+            "parity_gate": {"rows": len(sel), "what": "evenly spaced rows x all B", **pg}}
 
 
 def bench_full(dev, steps, warmup, dist, ws=1, rank=0, parity=True):
@@ -739,6 +791,7 @@ def run_ours(args):
         if not args.no_secondary and ws == 1:
             sec = []
             for fn in ((lambda: entries_secondary(args, dev, dist, ws, rank)) if cfg == "cfg2" else (lambda: None),
+                       lambda: bench_entries_batched(dev, 5, 3),
                        lambda: bench_full(dev, 3, 3, dist), lambda: bench_dot(dev, 5, 3, dist),
                        lambda: bench_dot(dev, 5, 3, dist, True)):
                 try:

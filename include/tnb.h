@@ -133,6 +133,12 @@ int tnb_promote_cp_f32(const tnb_node* node, int32_t position, int64_t batch,
 /*
  * idx: int64 [m][n_modes] row-major, raw user indices (negatives allowed);
  * out: fp32 [m] (unbatched) or [m][batch].
+ * TNB_ALGO_AUTO picks, for fp32: the fused two-table kernel when mode
+ * merging reduces the chain to a prefix and a suffix table (any rank), else
+ * the bucketed kernels for m >= 2^16 and ranks <= 32 -- batched chains too,
+ * one element at a time over shared tile records (_step_entries_batched,
+ * core.py:447-460) -- else the register chain (rank <= 32) or the layered
+ * algorithm.
  * err_mode: device int32; on completion it holds the LOWEST mode that had an
  * index outside [-J, J) (the ContractViolationError "index out of bounds on
  * mode k" of core.py:409-416), or a value >= n_modes when all were valid.
@@ -179,6 +185,10 @@ int tnb_full_f32(const tnb_chain* chain, int64_t lead_lo, int64_t lead_hi, float
 /* --- K3: inner products  (core.py:362-391) ------------------------------- */
 /*
  * out[e] = <a_e, b_e> for every batch element (one float when unbatched).
+ * Kernels: rank-16 TT chains (fp32) on the mma.sync split-TF32 kernel;
+ * other dense chains (any rank, fp32 and fp64) on the chunked kernel (slices
+ * staged in shared memory, 16-byte loads); chains with interior CP modes on
+ * the per-slice kernel.
  * Shapes and batching must agree (ContractViolationError in core.py:368-371).
  */
 int tnb_dot_f32(const tnb_chain* a, const tnb_chain* b, float* out, void* stream);
@@ -231,7 +241,9 @@ typedef struct {
   int32_t diag_tables;   /* runs of interior CP modes merged into product tables */
   int32_t table_launches;/* kernel launches that build the tables per call     */
   int32_t compute_kernel;/* bucketed: 0 = state kernel, 1 = stream kernel (one
-                            sorted mode; no per-sample state in shared memory) */
+                            sorted mode; no per-sample state in shared memory),
+                            2 = two-table kernel (the chain merges into a prefix
+                            and a suffix table: one fused gather-dot, any rank) */
   int32_t tile;          /* bucketed: samples per tile                          */
   double tensor_flops;   /* per call: tensor-core (split-TF32 mma.sync) flops
                             the compute kernel issues, 3 MMAs per product      */

@@ -1789,6 +1789,31 @@ __global__ void __launch_bounds__(256) table_suffix_step(ModeDev md, const float
   (void)J;
 }
 
+// suffix step for ranks above 32 (the staged kernel's 32 x 33 tile): slices
+// read through L1 / L2 (two-table chains of rank 64 and up)
+__global__ void __launch_bounds__(256) table_suffix_step_big(ModeDev md, const float* __restrict__ in, int64_t n,
+                                                              float* __restrict__ out) {
+  const int J = md.J, rl = md.rl, rr = md.rr;
+  const int64_t total = (int64_t)J * n * rl;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = t / rl;
+    const int a = (int)(t - row * rl);
+    const int j = (int)(row / n);
+    const int64_t x = row - (int64_t)j * n;
+    const float* y = in + x * rr;
+    float acc;
+    if (md.layout == TNB_LAYOUT_DIAG) {
+      acc = __ldg(md.s + (int64_t)j * rl + a) * y[a];
+    } else {
+      acc = 0.f;
+      const float* g = md.s + ((int64_t)j * rl + a) * rr;
+      for (int c = 0; c < rr; ++c) acc = fmaf(__ldg(g + c), y[c], acc);
+    }
+    out[t] = acc;
+  }
+}
+
 // Dense table steps as a tiled SIMT GEMM (the naive steps above re-read the
 // input row per output element and ran the FMA pipe at < 10%).  Per z = j:
 //   prefix: C_j[i][n] = sum_k A[i][k] G(j, k, n)  -> out[(i*J + j)*Nn + n]
@@ -2277,6 +2302,8 @@ int build_tables(const ChainDev& ch, const MergePlan& mp, unsigned char* base, c
         } else if ((int64_t)md.J * n * md.rl > 0 && table_gemm_ok(md, true)) {
           table_gemm<true><<<dim3((unsigned)ceil_div(n, kTRows), (unsigned)ceil_div(md.J, kTZ)), 256, 0, st>>>(
               md, in, n, out);
+        } else if ((int64_t)md.J * n * md.rl > 0 && (md.rl > 32 || md.rr > 32)) {
+          table_suffix_step_big<<<grid((int64_t)md.J * n * md.rl), 256, 0, st>>>(md, in, n, out);
         } else if ((int64_t)md.J * n * md.rl > 0) {
           const int per = 256 / md.rl;
           const int gx = (int)std::min<int64_t>(ceil_div(n, per), std::max<int64_t>(1, grid_cap / md.J));
