@@ -586,10 +586,7 @@ def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: in
         # one hardware thread stays with this (enqueueing) thread
         nthreads = int(os.environ.get("TNB_E2E_THREADS", "0")) or max(1, lib.tnb_host_threads() - 1)
         nar = _Narrower(idx_host, [spans[c] for c in narrow_k], stage, width, nthreads)
-    ws = None
-    if algo == N.ALGO_AUTO and N.load().tnb_entries_workspace_bytes(
-            ctypes.byref(p.chain), chunk, N.ALGO_BUCKETED) > 0:
-        algo = N.ALGO_BUCKETED  # one kernel for every chunk, even a short last one
+    ws = None  # every launch has exactly `chunk` rows: AUTO resolves to one plan for all chunks
     copy.wait_stream(comp)
     h2d = 0
     codecs = set()
