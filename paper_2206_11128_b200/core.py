@@ -551,7 +551,8 @@ def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: in
     dev = p.device
     m = int(idx_host.shape[0])
     n = t.ndim
-    chunk = _CHUNK_ROWS
+    chunk = 1 << int(os.environ.get("TNB_E2E_CHUNK_LOG2", "0")) if os.environ.get("TNB_E2E_CHUNK_LOG2") \
+        else _CHUNK_ROWS
     nch = (m + chunk - 1) // chunk
     # every launch sees exactly `chunk` rows (the short last chunk is padded
     # with index 0), so all chunks run the same plan
