@@ -117,6 +117,10 @@
 #endif
 
 namespace tnb {
+// full.cu: tiled SIMT GEMM (rank > 32 table levels)
+int gemm_f32(const float* A, int64_t lda, int64_t sA, const float* B, int64_t ldb, int64_t sB, float* C,
+             int64_t ldc, int64_t sC, int64_t M, int64_t N, int K, int64_t batch, cudaStream_t st);
+
 namespace {
 
 constexpr int kMaxJ = 1024;          // bucket count limit for sorted modes
@@ -2109,6 +2113,7 @@ struct MergePlan {
   int R = 0;                     // register geometry of the virtual chain
   int64_t table_bytes = 0;       // 256-aligned
   int8_t mma[kMaxModes];         // the copy is the tensor-core fragment layout (hi / lo, 2x size)
+  int64_t gemm_off = 0;          // scratch for the transposed core of a rank > 32 level (GEMM build)
   int a() const { return kind[0] == kPrefix ? hi[0] - lo[0] : 1; }
   int b() const { return kind[ng - 1] == kSuffix ? hi[ng - 1] - lo[ng - 1] : 1; }
 };
@@ -2121,6 +2126,26 @@ int merge_env() {
 int wide_env() {
   const char* e = getenv("TNB_MERGE_WIDE");
   return (e && e[0] == '0') ? 0 : 1;
+}
+
+bool gemm_level(const ModeDev& md) {
+  return md.layout == TNB_LAYOUT_DENSE && (md.rl > 32 || md.rr > 32);
+}
+
+// G[j][a][c] -> prefix: Bt[a][j][c] (B of C = IN * Bt, rows p, columns (j, c));
+//               suffix: GT[j][c][a] (per-j B of C_j = IN * G_j^T)
+template <bool SUFFIX>
+__global__ void core_transpose_kernel(ModeDev md, float* __restrict__ out) {
+  const int J = md.J, rl = md.rl, rr = md.rr;
+  const int64_t total = (int64_t)J * rl * rr;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = t / ((int64_t)rl * rr);
+    const int r = (int)(t - j * rl * rr), a = r / rr, c = r - (r / rr) * rr;
+    const float v = __ldg(md.s + t);
+    if (SUFFIX) out[(j * rr + c) * rl + a] = v;
+    else out[((int64_t)a * J + j) * rr + c] = v;
+  }
 }
 
 int64_t env_rows(const char* name) {
@@ -2223,6 +2248,18 @@ void plan_merge(const ChainDev& ch, int64_t m, MergePlan* mp) {
       off += ((int64_t)md.J * md.rl * md.rr * 4 * (mp->mma[v] ? 2 : 1) + 255) & ~(int64_t)255;
     }
   }
+  // table levels of rank > 32 are built as GEMMs against a transposed copy
+  // of the level's core (the staged / tensor-core table kernels stop at 32)
+  int64_t scratch = 0;
+  for (int v = 0; v < g; ++v) {
+    if (mp->kind[v] != kPrefix && mp->kind[v] != kSuffix) continue;
+    const int lo = mp->lo[v], hi = mp->hi[v];
+    const int o0 = mp->kind[v] == kPrefix ? lo + 1 : lo, o1 = mp->kind[v] == kPrefix ? hi : hi - 1;
+    for (int o = o0; o < o1; ++o)
+      if (gemm_level(ch.m[o])) scratch = std::max<int64_t>(scratch, (int64_t)ch.m[o].J * ch.m[o].rl * ch.m[o].rr * 4);
+  }
+  mp->gemm_off = off;
+  off += (scratch + 255) & ~(int64_t)255;
   mp->table_bytes = off;
 }
 
@@ -2271,7 +2308,14 @@ int build_tables(const ChainDev& ch, const MergePlan& mp, unsigned char* base, c
       for (int o = lo + 1; o < hi; ++o) {
         float* out = reinterpret_cast<float*>(base + mp.lvl[o]);
         const int64_t total = rows * ch.m[o].J * ch.m[o].rr;
-        if (total > 0 && launch_table_tc<false>(ch.m[o], in, rows, out, st)) {
+        if (total > 0 && gemm_level(ch.m[o])) {
+          const ModeDev& md = ch.m[o];
+          float* bt = reinterpret_cast<float*>(base + mp.gemm_off);
+          core_transpose_kernel<false><<<grid((int64_t)md.J * md.rl * md.rr), 256, 0, st>>>(md, bt);
+          int rc = gemm_f32(in, md.rl, 0, bt, (int64_t)md.J * md.rr, 0, out, (int64_t)md.J * md.rr, 0, rows,
+                            (int64_t)md.J * md.rr, md.rl, 1, st);
+          if (rc) return rc;
+        } else if (total > 0 && launch_table_tc<false>(ch.m[o], in, rows, out, st)) {
         } else if (total > 0 && table_gemm_ok(ch.m[o], false))
           table_gemm<false><<<dim3((unsigned)ceil_div(rows, kTRows), (unsigned)ceil_div(ch.m[o].J, kTZ)), 256, 0,
                               st>>>(ch.m[o], in, rows, out);
@@ -2298,7 +2342,13 @@ int build_tables(const ChainDev& ch, const MergePlan& mp, unsigned char* base, c
       for (int o = hi - 2; o >= lo; --o) {
         float* out = reinterpret_cast<float*>(base + mp.lvl[o]);
         const ModeDev& md = ch.m[o];
-        if ((int64_t)md.J * n * md.rl > 0 && launch_table_tc<true>(md, in, n, out, st)) {
+        if ((int64_t)md.J * n * md.rl > 0 && gemm_level(md)) {
+          float* gt = reinterpret_cast<float*>(base + mp.gemm_off);
+          core_transpose_kernel<true><<<grid((int64_t)md.J * md.rl * md.rr), 256, 0, st>>>(md, gt);
+          int rc = gemm_f32(in, md.rr, 0, gt, md.rl, (int64_t)md.rr * md.rl, out, md.rl, n * md.rl, n, md.rl, md.rr,
+                            md.J, st);
+          if (rc) return rc;
+        } else if ((int64_t)md.J * n * md.rl > 0 && launch_table_tc<true>(md, in, n, out, st)) {
         } else if ((int64_t)md.J * n * md.rl > 0 && table_gemm_ok(md, true)) {
           table_gemm<true><<<dim3((unsigned)ceil_div(n, kTRows), (unsigned)ceil_div(md.J, kTZ)), 256, 0, st>>>(
               md, in, n, out);

@@ -338,6 +338,13 @@ int launch_gemm(const T* A, int64_t lda, int64_t sA, const T* B, int64_t ldb, in
   return launch_gemm_remap<T>(A, lda, sA, B, ldb, sB, C, ldc, sC, M, N, K, batch, 0, 0, st);
 }
 
+// fp32 tiled SIMT GEMM for other translation units (the entries table
+// builder's rank > 32 levels)
+int gemm_f32(const float* A, int64_t lda, int64_t sA, const float* B, int64_t ldb, int64_t sB, float* C,
+             int64_t ldc, int64_t sC, int64_t M, int64_t N, int K, int64_t batch, cudaStream_t st) {
+  return launch_gemm<float>(A, lda, sA, B, ldb, sB, C, ldc, sC, M, N, K, batch, st);
+}
+
 int64_t full_workspace(const tnb_chain* c, int64_t lo, int64_t hi, int elt) {
   FullPlan P;
   if (make_plan(c, lo, hi, &P, elt)) return -1;
