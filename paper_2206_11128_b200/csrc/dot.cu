@@ -128,14 +128,16 @@ __global__ void __launch_bounds__(256) dot_chunk_kernel(const __grid_constant__ 
   using V = typename Vec<T>::V;
   constexpr int W = Vec<T>::W;
   extern __shared__ __align__(16) unsigned char sm_raw[];
-  T* M = reinterpret_cast<T*>(sm_raw);
-  T* Mn = M + mcap;
-  T* As = Mn + mcap;
+  T* M = reinterpret_cast<T*>(sm_raw);   // [ral][rbl]
+  T* Mt = M + mcap;                      // M transposed [rbl][ral] (W x W register tiles of Y)
+  T* Mn = Mt + mcap;                     // next M, [rar][rbr]
+  T* Ps = Mn + mcap;                     // per-thread W x W partials of M' (tiled modes), [nt][W][W]
+  T* As = Ps + 256 * W * W;
   T* Bs = As + scap;
   T* Ys = Bs + scap;
   const int tid = threadIdx.x, nt = blockDim.x;
   for (int64_t e = blockIdx.x; e < A.batch; e += gridDim.x) {
-    if (tid == 0) M[0] = T(1);
+    if (tid == 0) M[0] = Mt[0] = T(1);
     __syncthreads();
     for (int k = 0; k < A.n; ++k) {
       const ModeDev& ma = A.m[k];
@@ -146,25 +148,50 @@ __global__ void __launch_bounds__(256) dot_chunk_kernel(const __grid_constant__ 
       const int sa = ral * rar, sb = rbl * rbr, sy = ral * rbr;
       int CH = scap / (sa > sb ? (sa > sy ? sa : sy) : (sb > sy ? sb : sy));
       CH = CH < 1 ? 1 : (CH > J ? J : CH);
-      const int dv = (rbr % W == 0) ? rbr / W : 0;  // vector groups per row (0: scalar rows)
+      // W x W register tiles when every dimension they span is a multiple of
+      // W (interior modes); the rank-1 boundary modes take the scalar rows
+      const bool tiled = (ral % W == 0) && (rar % W == 0) && (rbr % W == 0);
+      const int ta = ral / W, td = rbr / W, tc = rar / W;
+      // M' reduction split: og output tiles x nsplit slices of the (j, a) pairs
+      const int og = tc * td;
+      const int nsplit = tiled ? (og >= nt ? 1 : nt / og) : 1;
       for (int t = tid; t < rar * rbr; t += nt) Mn[t] = T(0);
+      // tiled: this thread's M' tile (output tile o, reduction slice rs) in
+      // registers across the whole mode, reduced in a fixed order at its end
+      const int o = tiled ? tid % og : 0, rs = tiled ? tid / og : 0;
+      const int c0 = tiled ? (o / td) * W : 0, dd0 = tiled ? (o % td) * W : 0;
+      T macc[W][W];
+#pragma unroll
+      for (int i = 0; i < W; ++i)
+#pragma unroll
+        for (int q = 0; q < W; ++q) macc[i][q] = T(0);
       for (int j0 = 0; j0 < J; j0 += CH) {
         const int nj = J - j0 < CH ? J - j0 : CH;
-        __syncthreads();  // previous chunk done with As / Bs / Ys
+        __syncthreads();  // previous chunk done with As / Bs / Ys (and Mn zeroed)
         stage(As, ga + (int64_t)j0 * sa, (int64_t)nj * sa, tid, nt);
         stage(Bs, gb + (int64_t)j0 * sb, (int64_t)nj * sb, tid, nt);
         __syncthreads();
-        if (dv) {
-          const int groups = nj * ral * dv;
+        if (tiled) {
+          // Y_j[a0..a0+W)[d0..d0+W) = sum_b Mt[b][a0..] x B_j[b][d0..]
+          const int groups = nj * ta * td;
           for (int g = tid; g < groups; g += nt) {
-            const int j = g / (ral * dv), r = g - j * (ral * dv), a = r / dv, d0 = (r - a * dv) * W;
-            T acc[W];
+            const int j = g / (ta * td), r = g - j * (ta * td), a0 = (r / td) * W, d0 = (r % td) * W;
+            T acc[W][W];
 #pragma unroll
-            for (int q = 0; q < W; ++q) acc[q] = T(0);
+            for (int i = 0; i < W; ++i)
+#pragma unroll
+              for (int q = 0; q < W; ++q) acc[i][q] = T(0);
             const T* bj = Bs + j * sb + d0;
-            for (int b = 0; b < rbl; ++b)
-              Vec<T>::fma(M[a * rbl + b], *reinterpret_cast<const V*>(bj + b * rbr), acc);
-            *reinterpret_cast<V*>(Ys + j * sy + a * rbr + d0) = *reinterpret_cast<V*>(acc);
+            for (int b = 0; b < rbl; ++b) {
+              const V mv = *reinterpret_cast<const V*>(Mt + b * ral + a0);
+              const V bv = *reinterpret_cast<const V*>(bj + b * rbr);
+              const T* mp = reinterpret_cast<const T*>(&mv);
+#pragma unroll
+              for (int i = 0; i < W; ++i) Vec<T>::fma(mp[i], bv, acc[i]);
+            }
+#pragma unroll
+            for (int i = 0; i < W; ++i)
+              *reinterpret_cast<V*>(Ys + j * sy + (a0 + i) * rbr + d0) = *reinterpret_cast<V*>(acc[i]);
           }
         } else {
           for (int t = tid; t < nj * sy; t += nt) {
@@ -175,19 +202,17 @@ __global__ void __launch_bounds__(256) dot_chunk_kernel(const __grid_constant__ 
           }
         }
         __syncthreads();
-        if (dv) {
-          for (int g = tid; g < rar * dv; g += nt) {
-            const int c = g / dv, d0 = (g - c * dv) * W;
-            T acc[W];
+        if (tiled) {
+          // M'[c0..][d0..] += sum over this thread's slice of (j, a) of A_j[a][c0..] x Y_j[a][d0..]
+          if (tid < og * nsplit) {
+            for (int ja = rs; ja < nj * ral; ja += nsplit) {
+              const int j = ja / ral, a = ja - j * ral;
+              const V av = *reinterpret_cast<const V*>(As + j * sa + a * rar + c0);
+              const V yv = *reinterpret_cast<const V*>(Ys + j * sy + a * rbr + dd0);
+              const T* ap = reinterpret_cast<const T*>(&av);
 #pragma unroll
-            for (int q = 0; q < W; ++q) acc[q] = T(0);
-            for (int j = 0; j < nj; ++j) {
-              const T* aj = As + j * sa + c;
-              const T* yj = Ys + j * sy + d0;
-              for (int a = 0; a < ral; ++a) Vec<T>::fma(aj[a * rar], *reinterpret_cast<const V*>(yj + a * rbr), acc);
+              for (int i = 0; i < W; ++i) Vec<T>::fma(ap[i], yv, macc[i]);
             }
-#pragma unroll
-            for (int q = 0; q < W; ++q) Mn[c * rbr + d0 + q] += acc[q];
           }
         } else {
           for (int t = tid; t < rar * rbr; t += nt) {
@@ -199,8 +224,29 @@ __global__ void __launch_bounds__(256) dot_chunk_kernel(const __grid_constant__ 
           }
         }
       }
+      if (tiled) {
+        // fixed-order reduction of the nsplit partial tiles (deterministic)
+        if (tid < og * nsplit) {
+#pragma unroll
+          for (int i = 0; i < W; ++i)
+#pragma unroll
+            for (int q = 0; q < W; ++q) Ps[(tid * W + i) * W + q] = macc[i][q];
+        }
+        __syncthreads();
+        for (int t = tid; t < rar * rbr; t += nt) {
+          const int c = t / rbr, d = t - c * rbr;
+          const int oo = (c / W) * td + d / W, i = c % W, q = d % W;
+          T v = T(0);
+          for (int r2 = 0; r2 < nsplit; ++r2) v += Ps[((r2 * og + oo) * W + i) * W + q];
+          Mn[t] = v;
+        }
+      }
       __syncthreads();
-      for (int t = tid; t < rar * rbr; t += nt) M[t] = Mn[t];
+      for (int t = tid; t < rar * rbr; t += nt) {
+        const int c = t / rbr, d = t - c * rbr;
+        M[t] = Mn[t];
+        Mt[d * rar + c] = Mn[t];
+      }
       __syncthreads();
     }
     if (tid == 0) {
@@ -255,7 +301,7 @@ int launch_dot(const tnb_chain* a, const tnb_chain* b, void* out, bool is_norm, 
     mcap = (mcap + 3) & ~3;
     // staged operand capacity: ~16 KB of fp32 (8 KB of fp64 values -- 16 KB) per operand, at least one slice
     const int scap = ((std::max(scap_min, 16384 / 4) + 3) & ~3);
-    const size_t smem = ((size_t)2 * mcap + 3 * (size_t)scap) * (size_t)elt;
+    const size_t smem = ((size_t)3 * mcap + 256 * 16 / (elt / 4) + 3 * (size_t)scap) * (size_t)elt;
     if (smem <= 200 * 1024) {
       const int64_t B = ca.batch;
       int per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / smem));
