@@ -154,12 +154,15 @@ __global__ void __launch_bounds__(256) dot_chunk_kernel(const __grid_constant__ 
       const int ta = ral / W, td = rbr / W, tc = rar / W;
       // M' reduction split: og output tiles x nsplit slices of the (j, a) pairs
       const int og = tc * td;
-      const int nsplit = tiled ? (og >= nt ? 1 : nt / og) : 1;
+      // kept: the M' tiles fit one per thread (else each chunk's tiles are
+      // looped over and added into Mn)
+      const bool kept = tiled && og <= nt;
+      const int nsplit = kept ? nt / og : 1;
       for (int t = tid; t < rar * rbr; t += nt) Mn[t] = T(0);
       // tiled: this thread's M' tile (output tile o, reduction slice rs) in
       // registers across the whole mode, reduced in a fixed order at its end
-      const int o = tiled ? tid % og : 0, rs = tiled ? tid / og : 0;
-      const int c0 = tiled ? (o / td) * W : 0, dd0 = tiled ? (o % td) * W : 0;
+      const int o = kept ? tid % og : 0, rs = kept ? tid / og : 0;
+      const int c0 = kept ? (o / td) * W : 0, dd0 = kept ? (o % td) * W : 0;
       T macc[W][W];
 #pragma unroll
       for (int i = 0; i < W; ++i)
@@ -202,7 +205,28 @@ __global__ void __launch_bounds__(256) dot_chunk_kernel(const __grid_constant__ 
           }
         }
         __syncthreads();
-        if (tiled) {
+        if (tiled && !kept) {
+          for (int oo = tid; oo < og; oo += nt) {
+            const int cc = (oo / td) * W, d0 = (oo % td) * W;
+            T acc[W][W];
+#pragma unroll
+            for (int i = 0; i < W; ++i)
+#pragma unroll
+              for (int q = 0; q < W; ++q) acc[i][q] = T(0);
+            for (int ja = 0; ja < nj * ral; ++ja) {
+              const int j = ja / ral, a = ja - j * ral;
+              const V av = *reinterpret_cast<const V*>(As + j * sa + a * rar + cc);
+              const V yv = *reinterpret_cast<const V*>(Ys + j * sy + a * rbr + d0);
+              const T* ap = reinterpret_cast<const T*>(&av);
+#pragma unroll
+              for (int i = 0; i < W; ++i) Vec<T>::fma(ap[i], yv, acc[i]);
+            }
+#pragma unroll
+            for (int i = 0; i < W; ++i)
+#pragma unroll
+              for (int q = 0; q < W; ++q) Mn[(cc + i) * rbr + d0 + q] += acc[i][q];
+          }
+        } else if (tiled) {
           // M'[c0..][d0..] += sum over this thread's slice of (j, a) of A_j[a][c0..] x Y_j[a][d0..]
           if (tid < og * nsplit) {
             for (int ja = rs; ja < nj * ral; ja += nsplit) {
@@ -224,7 +248,7 @@ __global__ void __launch_bounds__(256) dot_chunk_kernel(const __grid_constant__ 
           }
         }
       }
-      if (tiled) {
+      if (kept) {
         // fixed-order reduction of the nsplit partial tiles (deterministic)
         if (tid < og * nsplit) {
 #pragma unroll
