@@ -121,6 +121,34 @@ __device__ __forceinline__ void stage(T* dst, const T* __restrict__ src, int64_t
   for (int64_t i = nv * W + tid; i < count; i += nt) dst[i] = __ldg(src + i);
 }
 
+// asynchronous staging (cp.async, 16-byte pieces + element tail), one commit
+// group per call; the caller waits with cp.async.wait_group
+template <typename T>
+__device__ __forceinline__ void stage_async(T* dst, const T* __restrict__ src, int64_t count, int tid, int nt) {
+  constexpr int W = 16 / (int)sizeof(T);
+  const int64_t nv = count / W;
+  for (int64_t i = tid; i < nv; i += nt)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst + i * W)),
+                 "l"(src + i * W)
+                 : "memory");
+  for (int64_t i = nv * W + tid; i < count; i += nt) {
+    if constexpr (sizeof(T) == 8)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst + i)),
+                   "l"(src + i)
+                   : "memory");
+    else
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst + i)),
+                   "l"(src + i)
+                   : "memory");
+  }
+}
+
+__device__ __forceinline__ int chunk_slices(int scap, int sa, int sb, int sy, int J) {
+  const int mx = sa > sb ? (sa > sy ? sa : sy) : (sb > sy ? sb : sy);
+  int ch = scap / mx;
+  return ch < 1 ? 1 : (ch > J ? J : ch);
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) dot_chunk_kernel(const __grid_constant__ ChainDev A,
                                                         const __grid_constant__ ChainDev Bc, T* __restrict__ out,
@@ -132,10 +160,28 @@ __global__ void __launch_bounds__(256) dot_chunk_kernel(const __grid_constant__ 
   T* Mt = M + mcap;                      // M transposed [rbl][ral] (W x W register tiles of Y)
   T* Mn = Mt + mcap;                     // next M, [rar][rbr]
   T* Ps = Mn + mcap;                     // per-thread W x W partials of M' (tiled modes), [nt][W][W]
-  T* As = Ps + 256 * W * W;
-  T* Bs = As + scap;
-  T* Ys = Bs + scap;
+  T* Asb[2] = {Ps + 256 * W * W, Ps + 256 * W * W + scap};  // double-buffered slice chunks
+  T* Bsb[2] = {Asb[1] + scap, Asb[1] + 2 * scap};
+  T* Ys = Bsb[1] + scap;
   const int tid = threadIdx.x, nt = blockDim.x;
+  // The next (pair, mode, chunk) item is staged with cp.async while the
+  // current one is computed: chunks run ahead across modes and pairs.
+  auto issue = [&](int64_t e, int k, int j0, int buf) {
+    if (e < A.batch) {
+      const ModeDev& ma = A.m[k];
+      const ModeDev& mb = Bc.m[k];
+      const int sa = ma.rl * ma.rr, sb = mb.rl * mb.rr, sy = ma.rl * mb.rr;
+      const int ch = chunk_slices(scap, sa, sb, sy, ma.J);
+      const int nj = ma.J - j0 < ch ? ma.J - j0 : ch;
+      stage_async(Asb[buf], reinterpret_cast<const T*>(ma.s) + e * ma.bstride + (int64_t)j0 * sa, (int64_t)nj * sa,
+                  tid, nt);
+      stage_async(Bsb[buf], reinterpret_cast<const T*>(mb.s) + e * mb.bstride + (int64_t)j0 * sb, (int64_t)nj * sb,
+                  tid, nt);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  int buf = 0;
+  issue(blockIdx.x, 0, 0, 0);
   for (int64_t e = blockIdx.x; e < A.batch; e += gridDim.x) {
     if (tid == 0) M[0] = Mt[0] = T(1);
     __syncthreads();
@@ -146,8 +192,7 @@ __global__ void __launch_bounds__(256) dot_chunk_kernel(const __grid_constant__ 
       const T* ga = reinterpret_cast<const T*>(ma.s) + e * ma.bstride;
       const T* gb = reinterpret_cast<const T*>(mb.s) + e * mb.bstride;
       const int sa = ral * rar, sb = rbl * rbr, sy = ral * rbr;
-      int CH = scap / (sa > sb ? (sa > sy ? sa : sy) : (sb > sy ? sb : sy));
-      CH = CH < 1 ? 1 : (CH > J ? J : CH);
+      const int CH = chunk_slices(scap, sa, sb, sy, J);
       // W x W register tiles when every dimension they span is a multiple of
       // W (interior modes); the rank-1 boundary modes take the scalar rows
       const bool tiled = (ral % W == 0) && (rar % W == 0) && (rbr % W == 0);
@@ -170,10 +215,15 @@ __global__ void __launch_bounds__(256) dot_chunk_kernel(const __grid_constant__ 
         for (int q = 0; q < W; ++q) macc[i][q] = T(0);
       for (int j0 = 0; j0 < J; j0 += CH) {
         const int nj = J - j0 < CH ? J - j0 : CH;
-        __syncthreads();  // previous chunk done with As / Bs / Ys (and Mn zeroed)
-        stage(As, ga + (int64_t)j0 * sa, (int64_t)nj * sa, tid, nt);
-        stage(Bs, gb + (int64_t)j0 * sb, (int64_t)nj * sb, tid, nt);
-        __syncthreads();
+        // stage the following item into the other buffer (its previous
+        // contents were consumed before the barrier that ended the last chunk)
+        if (j0 + CH < J) issue(e, k, j0 + CH, buf ^ 1);
+        else if (k + 1 < A.n) issue(e, k + 1, 0, buf ^ 1);
+        else issue(e + gridDim.x, 0, 0, buf ^ 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");  // this chunk's copies (this thread's) landed
+        __syncthreads();  // ... everyone's; previous chunk done with Ys (and Mn zeroed)
+        const T* As = Asb[buf];
+        const T* Bs = Bsb[buf];
         if (tiled) {
           // Y_j[a0..a0+W)[d0..d0+W) = sum_b Mt[b][a0..] x B_j[b][d0..]
           const int groups = nj * ta * td;
@@ -247,6 +297,8 @@ __global__ void __launch_bounds__(256) dot_chunk_kernel(const __grid_constant__ 
             Mn[t] += acc;
           }
         }
+        __syncthreads();  // As / Bs [buf] and Ys consumed: the next issue may refill them
+        buf ^= 1;
       }
       if (kept) {
         // fixed-order reduction of the nsplit partial tiles (deterministic)
@@ -325,10 +377,10 @@ int launch_dot(const tnb_chain* a, const tnb_chain* b, void* out, bool is_norm, 
     mcap = (mcap + 3) & ~3;
     // staged operand capacity: ~16 KB of fp32 (8 KB of fp64 values -- 16 KB) per operand, at least one slice
     const int scap = ((std::max(scap_min, 16384 / 4) + 3) & ~3);
-    const size_t smem = ((size_t)3 * mcap + 256 * 16 / (elt / 4) + 3 * (size_t)scap) * (size_t)elt;
+    const size_t smem = ((size_t)3 * mcap + 256 * 16 / (elt / 4) + 5 * (size_t)scap) * (size_t)elt;
     if (smem <= 200 * 1024) {
       const int64_t B = ca.batch;
-      int per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / smem));
+      int per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (size_t)(227 * 1024) / (smem + 1024)));
       const int64_t slots = (int64_t)num_sms() * per_sm;
       const int grid = (int)(B < slots ? B : slots);
       if (elt == 8) {
