@@ -83,6 +83,10 @@
 #ifndef TNB_STATE_PF
 #define TNB_STATE_PF 3
 #endif
+// state kernel, fused closing dot: L1 prefetch of the next step's closing rows
+#ifndef TNB_CLOSE_L1PF
+#define TNB_CLOSE_L1PF 1
+#endif
 #ifndef TNB_STREAM_THREADS
 #define TNB_STREAM_THREADS 384
 #endif
@@ -612,6 +616,9 @@ __global__ void __launch_bounds__(256) entries_sort_kernel(const __grid_constant
 }
 
 __device__ __forceinline__ uint32_t s32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
@@ -1000,6 +1007,18 @@ __global__ void __launch_bounds__(NT, kStateCtas)
               const int sa = perm[p + min(mg, n - 1)], sb = perm[p + min(mg + 8, n - 1)];
               const uint32_t r0 = s_state + (uint32_t)sa * (RP * 4);
               const uint32_t r1 = s_state + (uint32_t)sb * (RP * 4);
+#if TNB_CLOSE_L1PF
+              if (fclose && mt == 0) {
+                // the next step's closing rows (the warp's next 16 positions,
+                // wherever their bucket): into L1 now, read after its MMAs
+                const int pn = p + n;
+                if (pn + mg < hi)
+                  prefetch_l1(mlast.s + (int64_t)(bp.wideL ? widxL[perm[pn + mg]] : (uint32_t)colL[perm[pn + mg]]) * R);
+                if (pn + mg + 8 < hi)
+                  prefetch_l1(mlast.s +
+                              (int64_t)(bp.wideL ? widxL[perm[pn + mg + 8]] : (uint32_t)colL[perm[pn + mg + 8]]) * R);
+              }
+#endif
               float2 da[4], db[4];  // closing rows, loaded after the MMAs (before them: spills)
               float acc[4][4];
 #pragma unroll

@@ -20,9 +20,12 @@ def main():
     out.mkdir(parents=True, exist_ok=True)
 
     def comp(src):
-        obj = out / (src.stem + ".o")
-        cmd = [B.NVCC, *B.ARCH, *B.FLAGS, *defs, "-I", str(B.INCLUDE), "-I", str(B.CSRC), "-c", str(src), "-o",
-               str(obj)]
+        obj = out / (src.stem + (".o" if src.suffix == ".cu" else ".cpp.o"))
+        if src.suffix == ".cpp":
+            cmd = [B.CXX, *B.CXXFLAGS, *defs, "-I", str(B.INCLUDE), "-c", str(src), "-o", str(obj)]
+        else:
+            cmd = [B.NVCC, *B.ARCH, *B.FLAGS, *defs, "-I", str(B.INCLUDE), "-I", str(B.CSRC), "-c", str(src), "-o",
+                   str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode:
             raise RuntimeError(r.stderr)
@@ -31,7 +34,8 @@ def main():
     with ThreadPoolExecutor(8) as ex:
         objs = list(ex.map(comp, B._sources()))
     lib = out / "libtnb.so"
-    subprocess.run([B.NVCC, *B.ARCH, "-shared", "-cudart=static", "-o", str(lib), *map(str, objs)], check=True)
+    subprocess.run([B.NVCC, *B.ARCH, "-shared", "-cudart=static", "-Xcompiler", "-pthread", "-o", str(lib),
+                    *map(str, objs)], check=True)
     print(lib)
 
 
