@@ -449,15 +449,23 @@ def bench_entries(args, cfg, dev, dist, ws, rank, gate_rows=None):
         pad = torch.zeros(base, dtype=torch.float32, device=dev)
         gath = torch.empty(ws * base, dtype=torch.float32, device=dev)
 
+        gloo = torch.distributed.get_backend() == "gloo"
+
         def step_gather():
             step()
             pad[:m].copy_(out)
-            torch.distributed.all_gather_into_tensor(gath, pad)
+            if gloo:  # host round trip (gloo gathers CPU tensors)
+                g = gath.cpu()
+                torch.distributed.all_gather_into_tensor(g, pad.cpu())
+                gath.copy_(g)
+            else:
+                torch.distributed.all_gather_into_tensor(gath, pad)
 
         ms_g = timed_steps(step_gather, args.steps, 1, stream, dist) / args.steps
         fields["with_gather"] = {"ms_per_step": ms_g, "value": total / (ms_g * 1e-3), "unit": "entries/s",
                                  "gathered_bytes_per_rank": ws * base * 4,
-                                 "collective": "NCCL all_gather_into_tensor of the fp32 outputs"}
+                                 "collective": ("gloo (host) " if gloo else "NCCL ") +
+                                               "all_gather_into_tensor of the fp32 outputs"}
         del gath, pad
     # e2e through the public API from pinned host memory: H2D of the step's
     # indices + K1 + D2H of the step's output, every step
@@ -768,7 +776,9 @@ def run_ours(args):
     ws, rank, local = dist_env()
     dist = ws > 1
     if dist:
-        torch.distributed.init_process_group("nccl")
+        # TNB_BENCH_BACKEND=gloo: the same multi-rank path with ranks sharing
+        # one GPU (harness check on a one-GPU box; collectives via host memory)
+        torch.distributed.init_process_group(os.environ.get("TNB_BENCH_BACKEND", "nccl"))
     local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
