@@ -67,7 +67,7 @@ def report(tag, rep):
         d = dict(zip(hdr, row))
         u = dict(zip(hdr, units))
         name = d["Kernel Name"]
-        short = name.split("(")[0].split("::")[-1].split("<")[0]
+        short = name.split("(")[0].split("::")[-1].split("<")[0].replace("void ", "").strip()
         stalls = sorted(((float(v.replace(",", "")), h.replace("smsp__pcsamp_warps_issue_stalled_", ""))
                          for h, v in d.items()
                          if h.startswith("smsp__pcsamp_warps_issue_stalled") and not h.endswith("not_issued") and v),
