@@ -83,6 +83,17 @@
 #ifndef TNB_STATE_PF
 #define TNB_STATE_PF 3
 #endif
+// first-mode row rings (state and stream kernels): cp.async through L2 only
+// (.cg) or through L1 too (.ca: repeated rows -- every sample of a slice
+// query shares its prefix row -- are served by L1 instead of one hot L2 line)
+#ifndef TNB_RING_CA
+#define TNB_RING_CA 0
+#endif
+#if TNB_RING_CA
+#define TNB_RING_CP "cp.async.ca.shared.global"
+#else
+#define TNB_RING_CP "cp.async.cg.shared.global"
+#endif
 // state kernel, fused closing dot: L1 prefetch of the next step's closing
 // rows (measured: compute 2.39 vs 2.28 ms at cfg2 -- the extra perm / index
 // lookups cost more than the shorter closing-load latency saves)
@@ -959,7 +970,7 @@ __global__ void __launch_bounds__(NT, kStateCtas)
                 const uint32_t j = __shfl_sync(0xffffffffu, jr, row);
                 const uint32_t srow = __shfl_sync(0xffffffffu, sr, row);
                 if (row < rows)
-                  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s_state + srow * (RP * 4) + piece * 16),
+                  asm volatile(TNB_RING_CP " [%0], [%1], 16;" ::"r"(s_state + srow * (RP * 4) + piece * 16),
                                "l"(ch.m[0].s + (int64_t)j * R + piece * 4)
                                : "memory");
               }
@@ -1423,7 +1434,7 @@ __global__ void __launch_bounds__(NT, 1)
         const int row = i / (R / 4), piece = i - row * (R / 4);
         const uint32_t j = __shfl_sync(0xffffffffu, jr, row & 31) & kmask;
         if (row < n)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst0 + (uint32_t)(row * RS * 4 +
+          asm volatile(TNB_RING_CP " [%0], [%1], 16;" ::"r"(dst0 + (uint32_t)(row * RS * 4 +
                                                                                (SWZ ? piece ^ (((slot * kSC + row) >> 2) & 1) : piece) * 16)),
                        "l"(ftab + (int64_t)j * R + piece * 4)
                        : "memory");

@@ -43,6 +43,19 @@ cases = {
     "zipf_like": (torch.rand((m, n), device="cuda", generator=g) ** 4 * J).long().clamp_(0, J - 1),
 }
 cases["fibers_last_mode"][:, -1] = torch.arange(m, device="cuda") % J
+fixed = torch.randint(0, J, (m, n), device="cuda", generator=g)
+fixed[:, : n // 2] = torch.randint(0, J, (1, n // 2), device="cuda", generator=g)
+cases["slice_query_prefix_fixed"] = fixed
+fixed2 = torch.randint(0, J, (m, n), device="cuda", generator=g)
+fixed2[:, n // 2:] = torch.randint(0, J, (1, n - n // 2), device="cuda", generator=g)
+cases["slice_query_suffix_fixed"] = fixed2
+from paper_2206_11128_b200 import _native as N  # noqa: E402
+
 for name, idx in cases.items():
     ms = ev(lambda: tb.entries(t, idx))
-    print(f"{cfg} {name:20s} {ms:8.3f} ms  {m / ms / 1e6:8.3f} G entries/s", flush=True)
+    N.timing_enable(True)
+    tb.entries(t, idx)
+    torch.cuda.synchronize()
+    kt = {k: round(N.timing_read(k)[0], 3) for k in ("entries_prep", "entries_sort", "entries_compute", "entries_tables")}
+    N.timing_enable(False)
+    print(f"{cfg} {name:20s} {ms:8.3f} ms  {m / ms / 1e6:8.3f} G entries/s  {kt}", flush=True)
