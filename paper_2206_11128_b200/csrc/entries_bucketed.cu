@@ -83,16 +83,10 @@
 #ifndef TNB_STATE_PF
 #define TNB_STATE_PF 3
 #endif
-// first-mode row rings (state and stream kernels): cp.async through L2 only
-// (.cg) or through L1 too (.ca: repeated rows -- every sample of a slice
-// query shares its prefix row -- are served by L1 instead of one hot L2 line)
+// first-mode row rings (state and stream kernels): 1 = every group through
+// L1 (.ca); 0 = .ca only for groups whose rows repeat (ring_cp16 / hot_rows)
 #ifndef TNB_RING_CA
 #define TNB_RING_CA 0
-#endif
-#if TNB_RING_CA
-#define TNB_RING_CP "cp.async.ca.shared.global"
-#else
-#define TNB_RING_CP "cp.async.cg.shared.global"
 #endif
 // state kernel, fused closing dot: L1 prefetch of the next step's closing
 // rows (measured: compute 2.39 vs 2.28 ms at cfg2 -- the extra perm / index
@@ -629,6 +623,23 @@ __global__ void __launch_bounds__(256) entries_sort_kernel(const __grid_constant
 }
 
 __device__ __forceinline__ uint32_t s32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// 16-byte ring copies: through L2 only (.cg, streaming) or through L1 too
+// (.ca) when the group's rows repeat -- every sample of a slice query shares
+// its first-mode row, and 2^24 copies of one L2 line serialise on its slice
+// (cfg2 slice queries 14.0 -> 2.0 ms); random rows keep .cg (.ca for every
+// group measured 3% slower on uniform indices)
+__device__ __forceinline__ void ring_cp16(uint32_t dst, const void* src, bool hot) {
+  if (hot)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+  else
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+// majority of the group's rows equal to its first row (warp-uniform)
+__device__ __forceinline__ bool hot_rows(uint32_t jr, int rows, int lane) {
+  const uint32_t j0 = __shfl_sync(0xffffffffu, jr, 0);
+  const unsigned same = __ballot_sync(0xffffffffu, lane < rows && jr == j0);
+  return 2 * __popc(same) > rows;
+}
 __device__ __forceinline__ void prefetch_l1(const void* p) {
   asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
@@ -963,6 +974,7 @@ __global__ void __launch_bounds__(NT, kStateCtas)
               const uint32_t jr = lane < rows ? (bp.wide0 ? widx0[perm[base + lane]] : (uint32_t)cidx[perm[base + lane]])
                                               : 0u;
               const uint32_t sr = lane < rows ? (uint32_t)perm[base + lane] : 0u;
+              const bool hot = TNB_RING_CA || hot_rows(jr, rows, lane);
 #pragma unroll
               for (int it = 0; it < kFringG / 4; ++it) {  // kFringG rows x 8 pieces of 16 bytes
                 const int i = lane + 32 * it;
@@ -970,9 +982,7 @@ __global__ void __launch_bounds__(NT, kStateCtas)
                 const uint32_t j = __shfl_sync(0xffffffffu, jr, row);
                 const uint32_t srow = __shfl_sync(0xffffffffu, sr, row);
                 if (row < rows)
-                  asm volatile(TNB_RING_CP " [%0], [%1], 16;" ::"r"(s_state + srow * (RP * 4) + piece * 16),
-                               "l"(ch.m[0].s + (int64_t)j * R + piece * 4)
-                               : "memory");
+                  ring_cp16(s_state + srow * (RP * 4) + piece * 16, ch.m[0].s + (int64_t)j * R + piece * 4, hot);
               }
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
@@ -1428,16 +1438,15 @@ __global__ void __launch_bounds__(NT, 1)
                                    : 0u;
       const uint32_t dst0 = s_ring + (uint32_t)(slot * kSC * RS * 4);
       const uint32_t kmask = bp.kpack ? (1u << bp.kshift) - 1u : ~0u;
+      const bool hot = TNB_RING_CA || hot_rows(jr & kmask, n, lane);
 #pragma unroll
       for (int it = 0; it < (kSC * R / 4 + 31) / 32; ++it) {
         const int i = lane + 32 * it;
         const int row = i / (R / 4), piece = i - row * (R / 4);
         const uint32_t j = __shfl_sync(0xffffffffu, jr, row & 31) & kmask;
         if (row < n)
-          asm volatile(TNB_RING_CP " [%0], [%1], 16;" ::"r"(dst0 + (uint32_t)(row * RS * 4 +
-                                                                               (SWZ ? piece ^ (((slot * kSC + row) >> 2) & 1) : piece) * 16)),
-                       "l"(ftab + (int64_t)j * R + piece * 4)
-                       : "memory");
+          ring_cp16(dst0 + (uint32_t)(row * RS * 4 + (SWZ ? piece ^ (((slot * kSC + row) >> 2) & 1) : piece) * 16),
+                    ftab + (int64_t)j * R + piece * 4, hot);
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
