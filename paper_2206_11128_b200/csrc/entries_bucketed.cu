@@ -343,6 +343,9 @@ struct BPlan {
   int8_t smode[kMaxModes];  // sorted slot -> (virtual) mode
   int8_t lmaj[kMaxModes];   // sorted mode whose slices are in lane-major order
   int8_t mmal[kMaxModes];   // ... in the tensor-core fragment order (mma_slice_kernel)
+  // device word set by detect_hot_kernel when the first-mode rows repeat
+  // (slice queries): the compute kernels' rings then copy through L1
+  const int32_t* hot = nullptr;
 };
 
 // Balanced warp ranges for the state kernel's sorted modes, written by ONE
@@ -634,11 +637,32 @@ __device__ __forceinline__ void ring_cp16(uint32_t dst, const void* src, bool ho
   else
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
-// majority of the group's rows equal to its first row (warp-uniform)
-__device__ __forceinline__ bool hot_rows(uint32_t jr, int rows, int lane) {
-  const uint32_t j0 = __shfl_sync(0xffffffffu, jr, 0);
-  const unsigned same = __ballot_sync(0xffffffffu, lane < rows && jr == j0);
-  return 2 * __popc(same) > rows;
+// One warp per sampled tile: the first 32 samples' first-mode table rows;
+// a majority equal to sample 0's sets *hot (the caller zeroes it).  A
+// per-group vote inside the rings cost 2-8% on uniform indices; this is one
+// tiny launch per call and a kernel-uniform flag.
+template <typename IdxT>
+__global__ void detect_hot_kernel(const __grid_constant__ BPlan bp, const unsigned char* __restrict__ ws, int64_t m,
+                                  int32_t* __restrict__ hot) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (bp.ntiles + gridDim.x - 1) / gridDim.x;
+  const int64_t tile = (int64_t)blockIdx.x * stride;
+  if (tile >= bp.ntiles) return;
+  const int tn = (int)min((int64_t)bp.T, m - tile * bp.T);
+  const int rows = tn < 32 ? tn : 32;
+  const unsigned char* rec = ws + tile * bp.tile_bytes;
+  uint32_t j = 0;
+  if (lane < rows) {
+    if (bp.crow0 > 0 || bp.wide0) {  // first mode in the uint32 row (stream records: sorted index packed above)
+      const uint32_t kmask = bp.kpack ? (1u << bp.kshift) - 1u : ~0u;
+      j = reinterpret_cast<const uint32_t*>(rec + bp.off_wide)[lane] & kmask;
+    } else {
+      j = (uint32_t)reinterpret_cast<const IdxT*>(rec)[lane];
+    }
+  }
+  const uint32_t j0 = __shfl_sync(0xffffffffu, j, 0);
+  const unsigned same = __ballot_sync(0xffffffffu, lane < rows && j == j0);
+  if (lane == 0 && 2 * __popc(same) > rows) atomicOr(hot, 1);
 }
 __device__ __forceinline__ void prefetch_l1(const void* p) {
   asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
@@ -692,6 +716,7 @@ __global__ void __launch_bounds__(NT, kStateCtas)
 
   const uint32_t s_state = s32(state);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool hotk = bp.hot != nullptr && __ldg(bp.hot) != 0;  // repeated first-mode rows: rings via L1
   constexpr int nwarps = NT / 32;
   const int gi = lane / L;
   const int q = lane % L;
@@ -974,7 +999,7 @@ __global__ void __launch_bounds__(NT, kStateCtas)
               const uint32_t jr = lane < rows ? (bp.wide0 ? widx0[perm[base + lane]] : (uint32_t)cidx[perm[base + lane]])
                                               : 0u;
               const uint32_t sr = lane < rows ? (uint32_t)perm[base + lane] : 0u;
-              const bool hot = TNB_RING_CA || hot_rows(jr, rows, lane);
+              const bool hot = TNB_RING_CA || hotk;
 #pragma unroll
               for (int it = 0; it < kFringG / 4; ++it) {  // kFringG rows x 8 pieces of 16 bytes
                 const int i = lane + 32 * it;
@@ -1348,6 +1373,7 @@ __global__ void __launch_bounds__(NT, 1)
   constexpr bool SWZ = MMA && R == 24 && TNB_STREAM_SWZ;
   constexpr int RS = MMA ? (SWZ ? R : R + 4) : R;
   constexpr int KT = R / 8;            // MMA k- and n-tiles
+  const bool hotk = bp.hot != nullptr && __ldg(bp.hot) != 0;  // repeated first-mode rows: rings via L1
   extern __shared__ __align__(128) unsigned char smem[];
   const int N = ch.n, T = bp.T;
   const int64_t TB = bp.tile_bytes;
@@ -1438,7 +1464,7 @@ __global__ void __launch_bounds__(NT, 1)
                                    : 0u;
       const uint32_t dst0 = s_ring + (uint32_t)(slot * kSC * RS * 4);
       const uint32_t kmask = bp.kpack ? (1u << bp.kshift) - 1u : ~0u;
-      const bool hot = TNB_RING_CA || hot_rows(jr & kmask, n, lane);
+      const bool hot = TNB_RING_CA || hotk;
 #pragma unroll
       for (int it = 0; it < (kSC * R / 4 + 31) / 32; ++it) {
         const int i = lane + 32 * it;
@@ -2639,6 +2665,12 @@ int launch_rt(const ChainDev& ch, const BPlan& bp, const int64_t* idx, int64_t m
     rc = check_launch("entries_sort");
     if (rc) return rc;
   }
+  if (bp.hot) {
+    const int64_t g = bp.ntiles < 256 ? bp.ntiles : 256;
+    detect_hot_kernel<IdxT><<<(unsigned)g, 32, 0, st>>>(bp, ws, m, const_cast<int32_t*>(bp.hot));
+    rc = check_launch("detect_hot");
+    if (rc) return rc;
+  }
   }
 compute:
   if (tables_done) {  // the tables were built on the side stream, concurrently with prep / sort
@@ -2694,7 +2726,7 @@ int64_t bucketed_workspace(const ChainDev& ch, int64_t m) {
   if (m <= 0 || !bucketed_supported(ch)) return 0;
   EPlan P;
   if (plan_entries(ch, m, &P)) return 0;
-  return P.mp.table_bytes + P.bp.ntiles * P.bp.tile_bytes;
+  return P.mp.table_bytes + P.bp.ntiles * P.bp.tile_bytes + 256;
 }
 
 double chain_entry_flops(const ChainDev& ch);
@@ -2786,7 +2818,7 @@ int launch_entries_bucketed(const ChainDev& ch, const int64_t* idx, int64_t m, f
   BPlan& bp = P.bp;
   const int R = P.R, nt = P.nt;
   const bool stream = P.stream;
-  const int64_t need = mp.table_bytes + bp.ntiles * bp.tile_bytes;
+  const int64_t need = mp.table_bytes + bp.ntiles * bp.tile_bytes + 256;  // + the hot-rows flag
   if (!ws || ws_bytes < need)
     return set_error(TNB_EWORKSPACE, "bucketed entries needs %lld workspace bytes, got %lld",
                      (long long)need, (long long)ws_bytes);
@@ -2822,6 +2854,17 @@ int launch_entries_bucketed(const ChainDev& ch, const int64_t* idx, int64_t m, f
   ws = base + mp.table_bytes;
   const ChainDev& chv = v;
   unsigned char* w = static_cast<unsigned char*>(ws);
+  {
+    int32_t* hot = reinterpret_cast<int32_t*>(w + bp.ntiles * bp.tile_bytes);
+    bp.hot = hot;
+    if (!reuse_records) {  // batched elements reuse element 0's records and flag
+      rc = check_cuda(cudaMemsetAsync(hot, 0, sizeof(int32_t), st), "hot flag");
+      if (rc) {
+        if (tables) cudaStreamWaitEvent(st, tables, 0);
+        return rc;
+      }
+    }
+  }
   const bool small = bp.idx_bytes == 1;
   switch (R) {
     case 8:
