@@ -438,8 +438,11 @@ def bench_entries(args, cfg, dev, dist, ws, rank, gate_rows=None):
                               "step_gbs": (8 * len(shape) + 4) * m / (ms_step * 1e-3) / 1e9},
     }
     roof = pick_roof(kernel, k_ms, pipes, traffic, traffic_src, extra)
+    # event-timed launches (prep, sort, compute) + per step the table builds,
+    # detect_hot_kernel and the second (HOT) compute instantiation that
+    # returns at once when the flag does not match (the timer brackets both)
     launches = sum(n for k_, (_, n) in kt.items() if k_ != "entries_tables") + (
-        args.steps * plan["table_launches"] if kn else 0)
+        args.steps * (plan["table_launches"] + (2 if plan["compute_kernel"] in (0, 1) else 0)) if kn else 0)
     fields = {"value": value, "ms_per_step": ms_step, "roofline": roof, "clocks": clk.summary(),
               "gpu_launches": launches, "shard": [lo, hi]}
     if dist:

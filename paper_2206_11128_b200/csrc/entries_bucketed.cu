@@ -695,10 +695,11 @@ __device__ __forceinline__ void bulk(void* dst, const void* src, uint32_t bytes,
 // FOLD: the chain ends in interior CP modes followed by the last mode; that
 // run is folded into the last-mode dot product (separate instantiation so
 // chains without it keep the leaner register allocation)
-template <int R, typename IdxT, int NT, bool FOLD>
+template <int R, typename IdxT, int NT, bool FOLD, bool HOT>
 __global__ void __launch_bounds__(NT, kStateCtas)
     entries_compute_kernel(const __grid_constant__ ChainDev ch, const __grid_constant__ BPlan bp,
                            const unsigned char* __restrict__ ws, int64_t m, float* __restrict__ out) {
+  if ((bp.hot != nullptr && __ldg(bp.hot) != 0) != HOT) return;  // see entries_stream_kernel
   using Gm = Geo<R>;
   constexpr int C = Gm::C, L = Gm::L, G = Gm::G, P = Gm::P, RP = Gm::RP;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -716,7 +717,6 @@ __global__ void __launch_bounds__(NT, kStateCtas)
 
   const uint32_t s_state = s32(state);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const bool hotk = bp.hot != nullptr && __ldg(bp.hot) != 0;  // repeated first-mode rows: rings via L1
   constexpr int nwarps = NT / 32;
   const int gi = lane / L;
   const int q = lane % L;
@@ -999,7 +999,7 @@ __global__ void __launch_bounds__(NT, kStateCtas)
               const uint32_t jr = lane < rows ? (bp.wide0 ? widx0[perm[base + lane]] : (uint32_t)cidx[perm[base + lane]])
                                               : 0u;
               const uint32_t sr = lane < rows ? (uint32_t)perm[base + lane] : 0u;
-              const bool hot = TNB_RING_CA || hotk;
+              constexpr bool hot = TNB_RING_CA || HOT;
 #pragma unroll
               for (int it = 0; it < kFringG / 4; ++it) {  // kFringG rows x 8 pieces of 16 bytes
                 const int i = lane + 32 * it;
@@ -1358,10 +1358,15 @@ __device__ __forceinline__ bool mb_test(uint64_t* b, uint32_t parity) {
 // (mma.sync m16n8k8, split TF32, 16 samples per warp step) with the slice's
 // B fragments pre-split into hi / lo by the table build (mma_slice_kernel);
 // otherwise FFMA2 lane groups (Geo<R>).
-template <int R, typename IdxT, int NT, int ND, bool MMA>
+// HOT: the first-mode ring copies through L1 (repeated rows, see
+// detect_hot_kernel).  Both instantiations are launched back to back; the one
+// that does not match the device flag returns at once (~2 us), so each keeps
+// the code generation of a compile-time copy instruction.
+template <int R, typename IdxT, int NT, int ND, bool MMA, bool HOT>
 __global__ void __launch_bounds__(NT, 1)
     entries_stream_kernel(const __grid_constant__ ChainDev ch, const __grid_constant__ BPlan bp,
                           const unsigned char* __restrict__ ws, int64_t m, float* __restrict__ out) {
+  if ((bp.hot != nullptr && __ldg(bp.hot) != 0) != HOT) return;
   using Gm = Geo<R>;
   constexpr int C = Gm::C, L = Gm::L, G = Gm::G, P = Gm::P;
   constexpr int NW = NT / 32;
@@ -1373,7 +1378,6 @@ __global__ void __launch_bounds__(NT, 1)
   constexpr bool SWZ = MMA && R == 24 && TNB_STREAM_SWZ;
   constexpr int RS = MMA ? (SWZ ? R : R + 4) : R;
   constexpr int KT = R / 8;            // MMA k- and n-tiles
-  const bool hotk = bp.hot != nullptr && __ldg(bp.hot) != 0;  // repeated first-mode rows: rings via L1
   extern __shared__ __align__(128) unsigned char smem[];
   const int N = ch.n, T = bp.T;
   const int64_t TB = bp.tile_bytes;
@@ -1464,7 +1468,7 @@ __global__ void __launch_bounds__(NT, 1)
                                    : 0u;
       const uint32_t dst0 = s_ring + (uint32_t)(slot * kSC * RS * 4);
       const uint32_t kmask = bp.kpack ? (1u << bp.kshift) - 1u : ~0u;
-      const bool hot = TNB_RING_CA || hotk;
+      constexpr bool hot = TNB_RING_CA || HOT;
 #pragma unroll
       for (int it = 0; it < (kSC * R / 4 + 31) / 32; ++it) {
         const int i = lane + 32 * it;
@@ -2615,16 +2619,22 @@ template <int R, typename IdxT>
 int launch_stream(const ChainDev& ch, const BPlan& bp, const unsigned char* ws, int64_t m, float* out,
                   cudaStream_t st) {
   const size_t smem = stream_smem(bp, R);
-  auto k = ch.n == 4 ? entries_stream_kernel<R, IdxT, kStreamThreads, 1, kStreamMma>
-                     : entries_stream_kernel<R, IdxT, kStreamThreads, 0, kStreamMma>;
+  auto k = ch.n == 4 ? entries_stream_kernel<R, IdxT, kStreamThreads, 1, kStreamMma, false>
+                     : entries_stream_kernel<R, IdxT, kStreamThreads, 0, kStreamMma, false>;
+  auto kh = ch.n == 4 ? entries_stream_kernel<R, IdxT, kStreamThreads, 1, kStreamMma, true>
+                      : entries_stream_kernel<R, IdxT, kStreamThreads, 0, kStreamMma, true>;
   int rc = check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                       "stream smem attr");
+  if (!rc && bp.hot)
+    rc = check_cuda(cudaFuncSetAttribute(kh, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                    "stream smem attr");
   if (rc) return rc;
   const int64_t slots = (int64_t)num_sms();
   const int grid = (int)(bp.ntiles < slots ? bp.ntiles : slots);
   {
     KTimer kt("entries_compute", st);
     k<<<grid, kStreamThreads, smem, st>>>(ch, bp, ws, m, out);
+    if (bp.hot) kh<<<grid, kStreamThreads, smem, st>>>(ch, bp, ws, m, out);
   }
   return check_launch("entries_stream");
 }
@@ -2682,15 +2692,20 @@ compute:
     return set_error(TNB_EINVAL, "stream kernel: rank > 24");
   }
   const size_t csmem = compute_smem(bp.T, Geo<R>::RP, ch.n, (int)sizeof(IdxT), bp.jpad, bp.nw);
-  auto ck = entries_compute_kernel<R, IdxT, NT, FOLD>;
+  auto ck = entries_compute_kernel<R, IdxT, NT, FOLD, false>;
+  auto ckh = entries_compute_kernel<R, IdxT, NT, FOLD, true>;
   rc = check_cuda(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem),
                   "compute smem attr");
+  if (!rc && bp.hot)
+    rc = check_cuda(cudaFuncSetAttribute(ckh, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem),
+                    "compute smem attr");
   if (rc) return rc;
   const int64_t slots = (int64_t)num_sms() * kStateCtas;
   const int grid = (int)(bp.ntiles < slots ? bp.ntiles : slots);
   {
     KTimer kt("entries_compute", st);
     ck<<<grid, NT, csmem, st>>>(ch, bp, ws, m, out);
+    if (bp.hot) ckh<<<grid, NT, csmem, st>>>(ch, bp, ws, m, out);
   }
   return check_launch("entries_compute");
 }
