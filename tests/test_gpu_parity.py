@@ -696,3 +696,30 @@ def test_two_table_entries(case):
         bad[m // 3, t.ndim - 1] = -t.shape[-1] - 1
         with pytest.raises(tb.ContractViolationError, match=f"mode {min(k, t.ndim - 1)}"):
             tb.entries(t, bad)
+
+
+@pytest.mark.parametrize("case", ["state_r32", "stream_cfg5"])
+@pytest.mark.parametrize("pattern", ["prefix_fixed", "all_same", "half_same"])
+def test_bucketed_repeated_first_rows(case, pattern):
+    # slice queries: every sample shares its first-mode (prefix-table) row --
+    # detect_hot_kernel flags the call and the compute kernels' rings copy
+    # through L1; results identical in value to the oracle (core.py:394-444)
+    if case == "state_r32":
+        cores = O.random_tt((32,) * 6, 32, seed=2, scale=32 ** -0.5)
+        nodes = [("tt", c, None) for c in cores]
+        m = (1 << 17) + 3
+    else:
+        nodes = O.cfg5_nodes(seed=4)
+        m = 1 << 18
+    t = facade(nodes)
+    o = O.make_chain(nodes)
+    idx = O.uniform_indices(t.shape, m, 12)
+    if pattern == "prefix_fixed":
+        idx[:, : t.ndim // 2] = idx[0, : t.ndim // 2]
+    elif pattern == "all_same":
+        idx[:] = idx[5]
+    else:
+        idx[::2, :3] = idx[0, :3]
+    got = to_np(tb.entries(t, idx))
+    sel = np.arange(0, m, 61)
+    assert_close(got[sel], O.entries(o, idx[sel]), what=f"{case} {pattern}")
