@@ -74,6 +74,12 @@ static_assert(!TNB_FULL_BULK || TNB_FULL_NB3, "TNB_FULL_BULK needs TNB_FULL_NB3"
 #ifndef TNB_FULL_TMA
 #define TNB_FULL_TMA 1
 #endif
+// TNB_FULL_EPI8: 8 epilogue warps (the A-loader warps store the second half of
+// each tile's rows between A loads)
+#ifndef TNB_FULL_EPI8
+#define TNB_FULL_EPI8 0
+#endif
+static_assert(!(TNB_FULL_EPI8 && !TNB_FULL_NB3), "TNB_FULL_EPI8 needs TNB_FULL_NB3");
 constexpr int kTmaBox = 32;                                   // rows and columns per TMA store
 constexpr int kTmaBufBytes = kTmaBox * kTmaBox * 4;           // 4 KB
 constexpr int kTmaEpiBytes = TNB_FULL_TMA ? 4 * 2 * kTmaBufBytes : 0;
@@ -268,8 +274,8 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
     }
     mbar_init(&acc_full[0], 1);
     mbar_init(&acc_full[1], 1);
-    mbar_init(&acc_empty[0], 128);
-    mbar_init(&acc_empty[1], 128);
+    mbar_init(&acc_empty[0], TNB_FULL_EPI8 ? 256 : 128);
+    mbar_init(&acc_empty[1], TNB_FULL_EPI8 ? 256 : 128);
     mbar_init(mma_idle, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -349,6 +355,76 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
         ++it;
       }
     }
+#if TNB_FULL_EPI8
+  } else if (warp >= 4) {
+    // ===== epilogue on 8 warps (TNB_FULL_EPI8): warps 4-7 store the tile's
+    // first 64 rows, warps 8-11 its last 64 (TMEM lane quarter = warp % 4);
+    // warps 8-11 also load the resident A block when the column block changes
+    const int q = warp & 3, h = (warp >> 2) - 1;
+    const bool loader = warp >= 8;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    uint32_t s_it = 0;
+    int64_t cur_cb = -1;
+    for (int64_t t = t0; t < t1; ++t) {
+      const int64_t cb = t / n_mt, mt = t - cb * n_mt;
+      if (loader && cb != cur_cb) {
+        cur_cb = cb;
+        named_sync(1, 160);
+        for (int nb = 0; nb < NB; ++nb) {
+          const int64_t n = cb * NB * BNB + nb * BNB + q * 32 + lane;
+          const bool nok = n < N;
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            uint32_t hi[32], lo[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int k = half * 32 + j;
+              const float x = (nok && k < K) ? __ldg(args.B + (int64_t)k * args.ldb + n) : 0.f;
+              hi[j] = f2tf32(x);
+              lo[j] = __float_as_uint(x - __uint_as_float(hi[j]));
+            }
+            TMEM_ST32(tm_a0 + nb * BNB + lane_base + half * 32, hi);
+            TMEM_ST32(tm_a0 + nb * BNB + lane_base + KMAX + half * 32, lo);
+          }
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        named_sync(2, 160);
+      }
+      for (int nb = 0; nb < NB; ++nb) {
+        const int cbuf = s_it % kAccBufs;
+        mbar_wait(&acc_full[cbuf], (s_it / kAccBufs) & 1);
+        tc_fence_after();
+        const int64_t col = cb * NB * BNB + nb * BNB + q * 32 + lane;
+        uint32_t v[BMT / 2];
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) TMEM_LD32(tm_acc0 + cbuf * BMT + lane_base + (2 * h + ch) * 32, (v + ch * 32));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        mbar_arrive(&acc_empty[cbuf]);
+        ++s_it;
+        const int64_t r0 = mt * BMT + 64 * h;
+        const int64_t rows_left = M - r0;
+        if (col < N) {
+          float* p = args.C + r0 * args.ldc + col;
+          if (rows_left >= 64) {
+#pragma unroll
+            for (int j = 0; j < 64; ++j) {
+              st_stream(p, v[j]);
+              p += args.ldc;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 64; ++j) {
+              if (j < rows_left) st_stream(p, v[j]);
+              p += args.ldc;
+            }
+          }
+        }
+      }
+    }
+  }
+#else
   } else if (warp >= 4 && warp < 8) {
     // ================= epilogue: thread = output column =================
     const int q = warp & 3;
@@ -541,6 +617,7 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
       named_sync(2, 160);
     }
   }
+#endif
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
