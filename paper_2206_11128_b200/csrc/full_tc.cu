@@ -75,7 +75,8 @@ static_assert(!TNB_FULL_BULK || TNB_FULL_NB3, "TNB_FULL_BULK needs TNB_FULL_NB3"
 #define TNB_FULL_TMA 1
 #endif
 // TNB_FULL_EPI8: 8 epilogue warps (the A-loader warps store the second half of
-// each tile's rows between A loads)
+// each tile's rows between A loads).  Measured slower: 3.55-3.60 vs 3.37 ms
+// at cfg3 (round 1 saw the same with another 8-warp split)
 #ifndef TNB_FULL_EPI8
 #define TNB_FULL_EPI8 0
 #endif
