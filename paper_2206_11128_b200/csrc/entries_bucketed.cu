@@ -128,6 +128,11 @@
 #endif
 
 namespace tnb {
+// full_tc.cu: the tcgen05 3xTF32 GEMM (large dense prefix table levels)
+bool tc_gemm_supported(int64_t M, int64_t N, int K, int64_t lda, int64_t ldb, int64_t ldc);
+int64_t tc_gemm_workspace(int64_t M);
+int launch_tc_gemm(const float* A, int64_t lda, int64_t sA, const float* B, int64_t ldb, int64_t sB, float* C,
+                   int64_t ldc, int64_t sC, int64_t M, int64_t N, int K, int64_t batch, void* ws, cudaStream_t st);
 // full.cu: tiled SIMT GEMM (rank > 32 table levels)
 int gemm_f32(const float* A, int64_t lda, int64_t sA, const float* B, int64_t ldb, int64_t sB, float* C,
              int64_t ldc, int64_t sC, int64_t M, int64_t N, int K, int64_t batch, cudaStream_t st);
@@ -2203,6 +2208,18 @@ bool gemm_level(const ModeDev& md) {
   return md.layout == TNB_LAYOUT_DENSE && (md.rl > 32 || md.rr > 32);
 }
 
+// A dense PREFIX level is one row-major GEMM, C (P x J*rr) = IN (P x rl) *
+// Bt (rl x J*rr) with Bt[a][j][c] = G[j][a][c]: large ones run on the tcgen05
+// 3xTF32 GEMM of full() (TNB_TABLE_TCGEN05=0: the mma.sync table kernels)
+bool tc_prefix_level(const ModeDev& md, int64_t rows) {
+  static const bool on = [] {
+    const char* e = getenv("TNB_TABLE_TCGEN05");
+    return !(e && e[0] == '0');
+  }();
+  return on && md.layout == TNB_LAYOUT_DENSE && md.rl <= 64 &&
+         tc_gemm_supported(rows, (int64_t)md.J * md.rr, md.rl, md.rl, (int64_t)md.J * md.rr, (int64_t)md.J * md.rr);
+}
+
 // G[j][a][c] -> prefix: Bt[a][j][c] (B of C = IN * Bt, rows p, columns (j, c));
 //               suffix: GT[j][c][a] (per-j B of C_j = IN * G_j^T)
 template <bool SUFFIX>
@@ -2326,8 +2343,14 @@ void plan_merge(const ChainDev& ch, int64_t m, MergePlan* mp) {
     if (mp->kind[v] != kPrefix && mp->kind[v] != kSuffix) continue;
     const int lo = mp->lo[v], hi = mp->hi[v];
     const int o0 = mp->kind[v] == kPrefix ? lo + 1 : lo, o1 = mp->kind[v] == kPrefix ? hi : hi - 1;
-    for (int o = o0; o < o1; ++o)
-      if (gemm_level(ch.m[o])) scratch = std::max<int64_t>(scratch, (int64_t)ch.m[o].J * ch.m[o].rl * ch.m[o].rr * 4);
+    int64_t rows = ch.m[lo].J;  // prefix: input rows of level o
+    for (int o = o0; o < o1; ++o) {
+      const int64_t bt = ((int64_t)ch.m[o].J * ch.m[o].rl * ch.m[o].rr * 4 + 255) & ~(int64_t)255;
+      if (gemm_level(ch.m[o])) scratch = std::max<int64_t>(scratch, bt);
+      if (mp->kind[v] == kPrefix && tc_prefix_level(ch.m[o], rows))
+        scratch = std::max<int64_t>(scratch, bt + tc_gemm_workspace(rows));
+      if (mp->kind[v] == kPrefix) rows *= ch.m[o].J;
+    }
   }
   mp->gemm_off = off;
   off += (scratch + 255) & ~(int64_t)255;
@@ -2379,7 +2402,15 @@ int build_tables(const ChainDev& ch, const MergePlan& mp, unsigned char* base, c
       for (int o = lo + 1; o < hi; ++o) {
         float* out = reinterpret_cast<float*>(base + mp.lvl[o]);
         const int64_t total = rows * ch.m[o].J * ch.m[o].rr;
-        if (total > 0 && gemm_level(ch.m[o])) {
+        if (total > 0 && mp.kind[g] == kPrefix && tc_prefix_level(ch.m[o], rows)) {
+          const ModeDev& md = ch.m[o];
+          float* bt = reinterpret_cast<float*>(base + mp.gemm_off);
+          const int64_t btb = ((int64_t)md.J * md.rl * md.rr * 4 + 255) & ~(int64_t)255;
+          core_transpose_kernel<false><<<grid((int64_t)md.J * md.rl * md.rr), 256, 0, st>>>(md, bt);
+          int rc = launch_tc_gemm(in, md.rl, 0, bt, (int64_t)md.J * md.rr, 0, out, (int64_t)md.J * md.rr, 0, rows,
+                                  (int64_t)md.J * md.rr, md.rl, 1, base + mp.gemm_off + btb, st);
+          if (rc) return rc;
+        } else if (total > 0 && gemm_level(ch.m[o])) {
           const ModeDev& md = ch.m[o];
           float* bt = reinterpret_cast<float*>(base + mp.gemm_off);
           core_transpose_kernel<false><<<grid((int64_t)md.J * md.rl * md.rr), 256, 0, st>>>(md, bt);
