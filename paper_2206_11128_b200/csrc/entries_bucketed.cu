@@ -2189,7 +2189,8 @@ struct MergePlan {
   int R = 0;                     // register geometry of the virtual chain
   int64_t table_bytes = 0;       // 256-aligned
   int8_t mma[kMaxModes];         // the copy is the tensor-core fragment layout (hi / lo, 2x size)
-  int64_t gemm_off = 0;          // scratch for the transposed core of a rank > 32 level (GEMM build)
+  int64_t gemm_off = 0;          // scratch for GEMM-built table levels (transposed core + tcgen05 tiles)
+  int64_t gemm_bytes = 0;        // ... its size (the last region of the tables)
   int a() const { return kind[0] == kPrefix ? hi[0] - lo[0] : 1; }
   int b() const { return kind[ng - 1] == kSuffix ? hi[ng - 1] - lo[ng - 1] : 1; }
 };
@@ -2209,13 +2210,14 @@ bool gemm_level(const ModeDev& md) {
 }
 
 // A dense PREFIX level is one row-major GEMM, C (P x J*rr) = IN (P x rl) *
-// Bt (rl x J*rr) with Bt[a][j][c] = G[j][a][c]: large ones run on the tcgen05
-// 3xTF32 GEMM of full() (TNB_TABLE_TCGEN05=0: the mma.sync table kernels)
+// Bt (rl x J*rr) with Bt[a][j][c] = G[j][a][c]: large ones can run on the
+// tcgen05 3xTF32 GEMM of full() instead of the mma.sync table kernels.
+// Off by default: on the high-priority side stream its one-CTA-per-SM
+// persistent kernel takes whole SMs from the concurrent prep kernel (cfg2
+// step 2.95 vs 2.80 ms: prep 0.55 vs 0.41 ms; TNB_TABLE_TCGEN05=1 enables it)
 bool tc_prefix_level(const ModeDev& md, int64_t rows) {
-  static const bool on = [] {
-    const char* e = getenv("TNB_TABLE_TCGEN05");
-    return !(e && e[0] == '0');
-  }();
+  const char* e = getenv("TNB_TABLE_TCGEN05");
+  const bool on = e && e[0] == '1';
   return on && md.layout == TNB_LAYOUT_DENSE && md.rl <= 64 &&
          tc_gemm_supported(rows, (int64_t)md.J * md.rr, md.rl, md.rl, (int64_t)md.J * md.rr, (int64_t)md.J * md.rr);
 }
@@ -2353,7 +2355,8 @@ void plan_merge(const ChainDev& ch, int64_t m, MergePlan* mp) {
     }
   }
   mp->gemm_off = off;
-  off += (scratch + 255) & ~(int64_t)255;
+  mp->gemm_bytes = (scratch + 255) & ~(int64_t)255;
+  off += mp->gemm_bytes;
   mp->table_bytes = off;
 }
 
@@ -2636,7 +2639,9 @@ int plan_entries(const ChainDev& ch, int64_t m, EPlan* P) {
         if (kStreamMma) {  // the sorted mode's copy doubles (hi / lo fragments); it is the last table
           const ModeDev& g1 = ch.m[P->mp.lo[1]];
           P->mp.mma[1] = 1;
-          P->mp.table_bytes = P->mp.lm_off[1] + (((int64_t)g1.J * g1.rl * g1.rr * 2 * 4 + 255) & ~(int64_t)255);
+          // the GEMM scratch moves behind the doubled copy
+          P->mp.gemm_off = P->mp.lm_off[1] + (((int64_t)g1.J * g1.rl * g1.rr * 2 * 4 + 255) & ~(int64_t)255);
+          P->mp.table_bytes = P->mp.gemm_off + P->mp.gemm_bytes;
         }
         break;
       }

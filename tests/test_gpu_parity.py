@@ -723,3 +723,26 @@ def test_bucketed_repeated_first_rows(case, pattern):
     got = to_np(tb.entries(t, idx))
     sel = np.arange(0, m, 61)
     assert_close(got[sel], O.entries(o, idx[sel]), what=f"{case} {pattern}")
+
+
+@pytest.mark.parametrize("case", ["cfg2_like", "cfg5_structure"])
+def test_table_levels_on_tcgen05(case, monkeypatch):
+    # TNB_TABLE_TCGEN05=1: large dense prefix table levels as one tcgen05
+    # 3xTF32 GEMM against a transposed core (off by default: SM contention
+    # with the overlapped prep); values within the fp32 bar of the oracle
+    monkeypatch.setenv("TNB_TABLE_TCGEN05", "1")
+    if case == "cfg2_like":
+        cores = O.random_tt((32,) * 8, 32, seed=9, scale=32 ** -0.5)
+        nodes = [("tt", c, None) for c in cores]
+        m = 1 << 21
+    else:
+        nodes = O.cfg5_nodes(seed=6)
+        m = 1 << 23
+    t = facade(nodes)
+    o = O.make_chain(nodes)
+    plan = N.entries_plan(t._packed().chain, m, N.ALGO_AUTO)
+    assert plan["prefix_rows"] >= 1 << 15, plan
+    idx = O.uniform_indices(t.shape, m, 14)
+    got = to_np(tb.entries(t, torch.from_numpy(idx).cuda()))
+    sel = np.arange(0, m, m // 20000)
+    assert_close(got[sel], O.entries(o, idx[sel]), what=case)
