@@ -737,7 +737,7 @@ def test_table_levels_on_tcgen05(case, monkeypatch):
         m = 1 << 21
     else:
         nodes = O.cfg5_nodes(seed=6)
-        m = 1 << 23
+        m = 1 << 24  # the 2^21-row P012 table (its second level is a tcgen05 GEMM)
     t = facade(nodes)
     o = O.make_chain(nodes)
     plan = N.entries_plan(t._packed().chain, m, N.ALGO_AUTO)
