@@ -450,8 +450,9 @@ def _index_tensor(t: TnTensor, indices, device) -> torch.Tensor:
 
 
 # host index matrices at least 2 * _PIPELINE_ROWS long are streamed in
-# chunks of _CHUNK_ROWS (H2D of chunk i+1 overlaps the kernels of chunk i)
-_PIPELINE_ROWS = 1 << 21
+# chunks of _CHUNK_ROWS (H2D of chunk i+1 overlaps the kernels of chunk i);
+# 2^21 rows and up: an 8-way shard of the 2^24 cfg2 tuples still pipelines
+_PIPELINE_ROWS = 1 << 20
 _CHUNK_ROWS = 1 << 20
 
 # what the last pipelined entries() call moved over PCIe (bench.py's e2e
@@ -682,9 +683,14 @@ def entries(t: TnTensor, indices, *, algo: int = N.ALGO_AUTO,
             out.copy_(res)
             return out
         return res
+    host_in = isinstance(indices, torch.Tensor) and indices.device.type == "cpu" or \
+        not isinstance(indices, torch.Tensor)
     idx = _index_tensor(t, indices, p.device)
     m = int(idx.shape[0])
     b = t.batch_size
+    if host_in:
+        last_transfer.clear()
+        last_transfer.update(h2d_bytes=idx.numel() * 8, d2h_bytes=0, codec="int64")
     if out is not None:
         _check_out(t, p, out, m)
     dev_out = out if (out is not None and not host_out) else \
