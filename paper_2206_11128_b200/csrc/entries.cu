@@ -130,6 +130,14 @@ int pick_algo(const tnb_chain* c, int algo, int rmax) {
   return TNB_ALGO_CHAIN;
 }
 
+// float64 AUTO: the layered kernels beat the register chain once m is large
+// (cfg2 chain, 2^20 tuples: 7.7 vs 25.4 ms; cfg5: 3.0 vs 7.1 ms -- in double
+// the chain kernel's per-thread slice reads are L2-bound)
+int pick_algo_f64(const tnb_chain* c, int algo, int rmax, int64_t m) {
+  if (algo == TNB_ALGO_AUTO && m >= (1 << 12)) return TNB_ALGO_LAYERED;
+  return pick_algo(c, algo, rmax);
+}
+
 int chain_rmax(const tnb_chain* c) {
   int r = 1;
   for (int k = 0; k < c->n_modes; ++k) {
@@ -207,7 +215,7 @@ int64_t entries_workspace(const tnb_chain* c, int64_t m, int algo, int elt) {
   if (!c || !c->modes || c->n_modes < 1 || m < 0) return -1;
   const int rmax = chain_rmax(c);
   if (elt == 8) {
-    if (pick_algo(c, algo, rmax) != TNB_ALGO_LAYERED) return 0;
+    if (pick_algo_f64(c, algo, rmax, m) != TNB_ALGO_LAYERED) return 0;
     const int64_t B = c->batch > 0 ? c->batch : 1;
     return 2 * m * B * (int64_t)rmax * 8;
   }
@@ -328,7 +336,8 @@ int launch_entries(const tnb_chain* c, const int64_t* idx, int64_t m, void* out_
   if (rc || m == 0) return rc;
   if (elt == 8) {  // float64: the generic algorithms only
     if (use == TNB_ALGO_BUCKETED) return set_error(TNB_EINVAL, "the bucketed algorithm is fp32 only");
-    return entries_generic<double>(c, ch, use, idx, m, static_cast<double*>(out_v), err, ws, ws_bytes, st);
+    const int use64 = pick_algo_f64(c, algo, rmax0, m);
+    return entries_generic<double>(c, ch, use64, idx, m, static_cast<double*>(out_v), err, ws, ws_bytes, st);
   }
   float* out = static_cast<float*>(out_v);
   if (use_two_table(c, ch, m, algo)) return launch_two_table(ch, idx, m, out, err, ws, ws_bytes, st);

@@ -102,3 +102,18 @@ def test_f64_contracts():
     ta, tb_ = f64([("tt", x, None) for x in a], 64), f64([("tt", x, None) for x in b], 64)
     ref = O.chain_dot(O.make_chain([("tt", x) for x in a], 64), O.make_chain([("tt", x) for x in b], 64))
     close64(tb.dot(ta, tb_), ref, "batched dot", tol=1e-11)
+
+
+@pytest.mark.parametrize("batch", [None, 3])
+def test_f64_entries_layered_auto(batch):
+    # float64 AUTO picks the layered kernels from 2^12 rows up
+    cores = O.random_tt((32,) * 7, 16, seed=8, batch_size=batch, scale=0.25)
+    nodes = [("tt", c, None) for c in cores]
+    t, o = f64(nodes, batch), O.make_chain([("tt", c) for c in cores], batch)
+    idx = O.uniform_indices((32,) * 7, 9001, 4)
+    idx[::4] -= 32
+    close64(tb.entries(t, idx), O.entries(o, idx), "f64 layered entries")
+    bad = idx.copy()
+    bad[77, 3] = 32
+    with pytest.raises(tb.ContractViolationError, match="mode 3"):
+        tb.entries(t, bad)
