@@ -217,6 +217,20 @@ class TnTensor:
     def float(self) -> "TnTensor":
         return self.to(torch.float32)
 
+    # tntorch spellings (tntorch.Tensor): the per-mode cores and the Tucker
+    # factors (None where a mode has none); views of the nodes' tensors
+    @property
+    def cores(self) -> list:
+        return [n.core for n in self._nodes]
+
+    @property
+    def Us(self) -> list:
+        return [n.factor for n in self._nodes]
+
+    def numpy(self):
+        """The dense tensor as a float64 ndarray (tntorch ``Tensor.numpy``)."""
+        return full(self).cpu().double().numpy()
+
     @property
     def ndim(self) -> int:
         return len(self._nodes)

@@ -265,3 +265,18 @@ def test_host_narrow_codec_rejects_bad_width(lib):
 
     with pytest.raises(ContractViolationError):
         _native.narrow_indices(torch.zeros(4, dtype=torch.int64), torch.zeros(4, dtype=torch.int32), 4)
+
+
+def test_tntorch_attribute_aliases():
+    # tntorch.Tensor spellings over the tntz data model (no device work)
+    import paper_2206_11128_b200 as tb
+
+    rng = np.random.default_rng(0)
+    g0 = rng.standard_normal((1, 4, 3)).astype(np.float32)
+    u1 = rng.standard_normal((5, 3)).astype(np.float32)
+    f1 = rng.standard_normal((7, 5)).astype(np.float32)
+    t = tb.Tensor([tb.ModeNode("tt", g0), tb.ModeNode("cp", u1, f1)])
+    assert t.shape == (4, 7)
+    assert [tuple(c.shape) for c in t.cores] == [(1, 4, 3), (5, 3)]
+    assert t.Us[0] is None and tuple(t.Us[1].shape) == (7, 5)
+    assert np.array_equal(t.cores[1].cpu().numpy(), u1)
