@@ -13,6 +13,8 @@
 namespace tnb {
 bool dot_fast_supported(const ChainDev& a, const ChainDev& b);
 int launch_dot_fast(const ChainDev& a, const ChainDev& b, float* out, bool is_norm, cudaStream_t st);
+int dot_mma_rank(const ChainDev& a, const ChainDev& b);
+int launch_dot_mma(const ChainDev& a, const ChainDev& b, float* out, bool is_norm, cudaStream_t st);
 
 namespace {
 
@@ -365,6 +367,8 @@ int launch_dot(const tnb_chain* a, const tnb_chain* b, void* out, bool is_norm, 
   const char* gen = getenv("TNB_DOT_GENERIC");
   if (elt == 4 && !(gen && gen[0] == '1') && dot_fast_supported(ca, cb))
     return launch_dot_fast(ca, cb, static_cast<float*>(out), is_norm, st);
+  if (elt == 4 && !(gen && gen[0] == '1') && dot_mma_rank(ca, cb))
+    return launch_dot_mma(ca, cb, static_cast<float*>(out), is_norm, st);
   const char* chk = getenv("TNB_DOT_CHUNK");
   if (!(chk && chk[0] == '0') && chunk_ok(ca, cb, elt)) {
     int mcap = 1, scap_min = 1;

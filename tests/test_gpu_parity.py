@@ -746,3 +746,23 @@ def test_table_levels_on_tcgen05(case, monkeypatch):
     got = to_np(tb.entries(t, torch.from_numpy(idx).cuda()))
     sel = np.arange(0, m, m // 20000)
     assert_close(got[sel], O.entries(o, idx[sel]), what=case)
+
+
+@pytest.mark.parametrize("rank", [8, 24, 32, 48])
+@pytest.mark.parametrize("batch", [1, 37, 300])
+def test_dot_norm_tensor_core_ranks(rank, batch):
+    # uniform-rank TT chains of ranks 8 / 24 / 32 / 48 on the mma.sync
+    # split-TF32 kernel (dot_mma.cu): staged chunks, padded split rows, Y and
+    # A^T Y products on tensor cores (core.py:362-391)
+    shape = (24, 17, 33, 9, 20, 5)
+    a = O.random_tt(shape, rank, seed=rank, batch_size=batch, scale=rank ** -0.5)
+    b = O.random_tt(shape, rank, seed=rank + 100, batch_size=batch, scale=rank ** -0.5)
+    ta = tb.TnTensor([tb.ModeNode("tt", c, batched=True) for c in a], batch)
+    tb_ = tb.TnTensor([tb.ModeNode("tt", c, batched=True) for c in b], batch)
+    oa, ob = O.make_chain([("tt", c) for c in a], batch), O.make_chain([("tt", c) for c in b], batch)
+    assert_dot_close(tb.dot(ta, tb_), O.chain_dot(oa, ob), O.norm(oa) * O.norm(ob), what=f"dot r{rank}")
+    assert_close(tb.norm(ta), O.norm(oa), what=f"norm r{rank}")
+    # self-dot = norm^2 on the same kernel
+    d = to_np(tb.dot(ta, ta))
+    n = to_np(tb.norm(ta))
+    assert np.all(np.abs(d - n * n) <= 1e-5 * n * n)

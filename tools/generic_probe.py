@@ -50,6 +50,9 @@ for r in (8, 16, 24, 32):
     a, b = tt((64,) * 16, r, batch=1024, scale=0.25), tt((64,) * 16, r, batch=1024, scale=0.25, seed=1)
     line(f"dot cfg4-shape r={r} 1024 pairs", ev(lambda: tb.dot(a, b)), 1024, "pairs")
     line(f"norm cfg4-shape r={r} 1024 pairs", ev(lambda: tb.norm(a)), 1024, "pairs")
+    os.environ["TNB_DOT_MMA"] = "0"
+    line(f"dot cfg4-shape r={r} 1024 pairs (chunked SIMT)", ev(lambda: tb.dot(a, b)), 1024, "pairs")
+    os.environ.pop("TNB_DOT_MMA")
 t = tt((32,) * 10, 32, dtype=torch.float64)
 line("f64 entries cfg2 m=2^20", ev(lambda: tb.entries(t, idx)), m, "entries")
 t = tt((16,) * 6, 8, dtype=torch.float64)
