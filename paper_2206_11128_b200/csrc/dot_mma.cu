@@ -1,4 +1,4 @@
-// K3 on tensor cores for TT chains of uniform rank R in {8, 24, 32, 48} (the
+// K3 on tensor cores for TT chains of uniform rank R in {8, 32, 48} (the
 // rank-16 kernel, dot_fast.cu, covers R = 16; dot.cu's chunked SIMT kernel
 // covers everything else -- other ranks, CP modes, fp64).  Reference: chain_dot
 // (core.py:362-384) / norm (core.py:387-391): M' = sum_j A_j^T M B_j.
@@ -377,7 +377,9 @@ int env_dot_mma() {
 int dot_mma_rank(const ChainDev& a, const ChainDev& b) {
   if (!env_dot_mma() || a.n != b.n || a.batch != b.batch || a.n < 3) return 0;
   const int R = a.m[0].rr;
-  if (R != 8 && R != 24 && R != 32 && R != 48) return 0;
+  // R = 24 measured slower than the chunked SIMT kernel (its second 16-row
+  // tile is half padding): 4.48 vs 4.26 ms for 1024 cfg4-shape pairs
+  if (R != 8 && R != 32 && R != 48) return 0;
   return (mma_chain_ok(a, R) && mma_chain_ok(b, R)) ? R : 0;
 }
 

@@ -751,7 +751,7 @@ def test_table_levels_on_tcgen05(case, monkeypatch):
 @pytest.mark.parametrize("rank", [8, 24, 32, 48])
 @pytest.mark.parametrize("batch", [1, 37, 300])
 def test_dot_norm_tensor_core_ranks(rank, batch):
-    # uniform-rank TT chains of ranks 8 / 24 / 32 / 48 on the mma.sync
+    # uniform-rank TT chains of ranks 8 / 32 / 48 on the mma.sync (24: chunked)
     # split-TF32 kernel (dot_mma.cu): staged chunks, padded split rows, Y and
     # A^T Y products on tensor cores (core.py:362-391)
     shape = (24, 17, 33, 9, 20, 5)
