@@ -7,6 +7,6 @@ mkdir -p gpurun_out/prof
 export TNB_PREFIX_MAX_ROWS=32768 TNB_SUFFIX_MAX_ROWS=32768
 P="python tools/bench_entries.py --one cfg2"
 timeout 300 $P > gpurun_out/prof/l2plan_plain.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --kernel-name-base demangled -k "regex:entries_compute_kernel<[^>]*, (0|false)>" -s 1 -c 1 \
+  timeout 900 ncu --set full --clock-control none --kernel-name-base demangled -k "regex:entries_compute_kernel<.*\(bool\)0>" -s 1 -c 1 \
     -o gpurun_out/prof/cfg2_l2plan $P > gpurun_out/prof/ncu_l2plan.log 2>&1
 tail -2 gpurun_out/prof/ncu_l2plan.log; cat gpurun_out/prof/l2plan_plain.log | cut -c1-300
