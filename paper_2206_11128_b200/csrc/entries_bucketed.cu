@@ -88,6 +88,11 @@
 #ifndef TNB_RING_CA
 #define TNB_RING_CA 0
 #endif
+// state kernel, fused closing dot: L1 prefetch of this step's closing rows
+// before its MMAs
+#ifndef TNB_CLOSE_PF_EARLY
+#define TNB_CLOSE_PF_EARLY 0
+#endif
 // state kernel, fused closing dot: L1 prefetch of the next step's closing
 // rows (measured: compute 2.39 vs 2.28 ms at cfg2 -- the extra perm / index
 // lookups cost more than the shorter closing-load latency saves)
@@ -1073,6 +1078,13 @@ __global__ void __launch_bounds__(NT, kStateCtas)
               }
 #endif
               float2 da[4], db[4];  // closing rows, loaded after the MMAs (before them: spills)
+#if TNB_CLOSE_PF_EARLY
+              // this step's closing rows into L1 before the MMAs, read after them
+              if (fclose && mt == 0) {
+                prefetch_l1(mlast.s + (int64_t)(bp.wideL ? widxL[sa] : (uint32_t)colL[sa]) * R);
+                prefetch_l1(mlast.s + (int64_t)(bp.wideL ? widxL[sb] : (uint32_t)colL[sb]) * R);
+              }
+#endif
               float acc[4][4];
 #pragma unroll
               for (int nt = 0; nt < 4; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
