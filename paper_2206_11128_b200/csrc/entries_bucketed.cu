@@ -89,7 +89,7 @@
 #define TNB_RING_CA 0
 #endif
 // state kernel, fused closing dot: L1 prefetch of this step's closing rows
-// before its MMAs
+// before its MMAs (measured: compute 2.36 vs 2.29 ms at cfg2)
 #ifndef TNB_CLOSE_PF_EARLY
 #define TNB_CLOSE_PF_EARLY 0
 #endif

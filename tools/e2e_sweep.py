@@ -15,7 +15,10 @@ m, shape = 1 << 24, W.CONFIGS["cfg2"][1]
 t = tb.TnTensor([tb.ModeNode("tt", c) for c in W.tt_cores(shape, 32, 0)])
 ih = torch.from_numpy(W.indices(shape, m, 2)).pin_memory()
 po = torch.empty(m).pin_memory()
-for frac, thr, ch in itertools.product(("0.25", "0.35", "0.45"), ("12", "15", "16"), ("20", "21")):
+FRACS = sys.argv[1].split(",") if len(sys.argv) > 1 else ["0.25", "0.35", "0.45"]
+THREADS = sys.argv[2].split(",") if len(sys.argv) > 2 else ["12", "15", "16"]
+CHUNKS = sys.argv[3].split(",") if len(sys.argv) > 3 else ["20", "21"]
+for frac, thr, ch in itertools.product(FRACS, THREADS, CHUNKS):
     os.environ.update(TNB_E2E_RAW_FRAC=frac, TNB_E2E_THREADS=thr, TNB_E2E_CHUNK_LOG2=ch)
     tb.entries(t, ih, out=po)
     torch.cuda.synchronize()
