@@ -27,5 +27,5 @@ done
 X="python tools/prof_extra.py two_table"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:two_table -s 1 -c 1 -o $O/two_table $X > $O/ncu_tt.log 2>&1
 X="python tools/prof_extra.py dot_chunk"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:dot_chunk -s 1 -c 1 -o $O/dot_chunk $X > $O/ncu_dc.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:dot_mma -s 1 -c 1 -o $O/dot_mma $X > $O/ncu_dc.log 2>&1
 ls -la $O
