@@ -62,6 +62,7 @@ extern "C" {
 #define TNB_ALGO_LAYERED 1  /* one launch per mode over a global state buffer */
 #define TNB_ALGO_CHAIN 2    /* one thread per sample, cores via L1/L2          */
 #define TNB_ALGO_BUCKETED 3 /* per-CTA counting sort, warp-shared core slices  */
+#define TNB_ALGO_GSORT 4    /* one global sort by a merged interior mode, tcgen05 */
 
 /*
  * One node exactly as the reference stores it (ModeNode, core.py:41-99).
@@ -135,6 +136,9 @@ int tnb_promote_cp_f32(const tnb_node* node, int32_t position, int64_t batch,
  * out: fp32 [m] (unbatched) or [m][batch].
  * TNB_ALGO_AUTO picks, for fp32: the fused two-table kernel when mode
  * merging reduces the chain to a prefix and a suffix table (any rank), else
+ * the global-sort tcgen05 path (TNB_ALGO_GSORT) for unbatched chains with
+ * m >= 2^18 whose merged chain is first . dense . [diag] . last with ranks
+ * <= 32 that are multiples of 4, else
  * the bucketed kernels for m >= 2^16 and ranks <= 32 -- batched chains too,
  * one element at a time over shared tile records (_step_entries_batched,
  * core.py:447-460) -- else the register chain (rank <= 32) or the layered

@@ -22,7 +22,7 @@ TNB_OK, TNB_EINVAL, TNB_EINDEX, TNB_ECUDA, TNB_EWORKSPACE = 0, 1, 2, 3, 4
 KIND_TT, KIND_CP = 0, 1
 LAYOUT_DENSE, LAYOUT_DIAG = 0, 1
 POS_INTERIOR, POS_LEFT, POS_RIGHT, POS_SINGLE = 0, 1, 2, 3
-ALGO_AUTO, ALGO_LAYERED, ALGO_CHAIN, ALGO_BUCKETED = 0, 1, 2, 3
+ALGO_AUTO, ALGO_LAYERED, ALGO_CHAIN, ALGO_BUCKETED, ALGO_GSORT = 0, 1, 2, 3, 4
 
 
 class TnbNode(ctypes.Structure):

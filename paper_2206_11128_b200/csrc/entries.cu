@@ -22,6 +22,13 @@ int64_t bucketed_workspace(const ChainDev& ch, int64_t m);
 void bucketed_info(const ChainDev& ch, int64_t m, tnb_entries_info* info);
 double chain_entry_flops(const ChainDev& ch);
 bool two_table_ok(const ChainDev& ch, int64_t m);
+// entries_gsort.cuh: the global-sort tcgen05 path
+bool gsort_ok(const ChainDev& ch, int64_t m);
+bool gsort_auto(const ChainDev& ch, int64_t m);
+int64_t gsort_workspace(const ChainDev& ch, int64_t m);
+void gsort_info(const ChainDev& ch, int64_t m, tnb_entries_info* info);
+int launch_entries_gsort(const ChainDev& ch, const int64_t* idx, int64_t m, float* out, int32_t* err, void* ws,
+                         int64_t ws_bytes, cudaStream_t st);
 int64_t two_table_workspace(const ChainDev& ch, int64_t m);
 void two_table_info(const ChainDev& ch, int64_t m, tnb_entries_info* info);
 int launch_two_table(const ChainDev& ch, const int64_t* idx, int64_t m, float* out, int32_t* err, void* ws,
@@ -186,6 +193,13 @@ bool use_two_table(const tnb_chain* c, const ChainDev& ch, int64_t m, int algo) 
   return algo == TNB_ALGO_AUTO && c->n_modes <= kMaxModes && m >= (1 << 12) && two_table_ok(ch, m);
 }
 
+// AUTO: large unbatched calls whose merged chain is first . dense . [diag] . last
+// run the global-sort tcgen05 path (TNB_ENTRIES_GSORT=0 turns that off)
+bool use_gsort(const ChainDev& ch, int64_t m, int algo) {
+  if (algo == TNB_ALGO_GSORT) return true;
+  return algo == TNB_ALGO_AUTO && gsort_auto(ch, m);
+}
+
 bool use_bucketed(const ChainDev& ch, int64_t m, int algo) {
   if (algo == TNB_ALGO_BUCKETED) return true;
   return algo == TNB_ALGO_AUTO && m >= (1 << 16) && bucketed_ok(ch);
@@ -219,9 +233,10 @@ int64_t entries_workspace(const tnb_chain* c, int64_t m, int algo, int elt) {
     const int64_t B = c->batch > 0 ? c->batch : 1;
     return 2 * m * B * (int64_t)rmax * 8;
   }
-  if (c->n_modes <= kMaxModes && (algo == TNB_ALGO_AUTO || algo == TNB_ALGO_BUCKETED)) {
+  if (c->n_modes <= kMaxModes && (algo == TNB_ALGO_AUTO || algo == TNB_ALGO_BUCKETED || algo == TNB_ALGO_GSORT)) {
     static thread_local ChainDev ch;
     if (make_chain_dev(c, &ch, true) == TNB_OK && use_two_table(c, ch, m, algo)) return two_table_workspace(ch, m);
+    if (make_chain_dev(c, &ch, true) == TNB_OK && use_gsort(ch, m, algo)) return gsort_workspace(ch, m);
     if (make_chain_dev(c, &ch, true) == TNB_OK && use_bucketed(ch, m, algo) && bucketed_ok(ch))
       return ch.batch > 1 ? batched_tmp_offset(ch, m) + ch.batch * m * (int64_t)sizeof(float)
                           : bucketed_workspace(ch, m);
@@ -260,6 +275,12 @@ int entries_plan(const tnb_chain* c, int64_t m, int algo, tnb_entries_info* info
   if (c->n_modes <= kMaxModes && use_two_table(c, ch, m, algo)) {
     info->algo = TNB_ALGO_BUCKETED;
     two_table_info(ch, m, info);
+    return TNB_OK;
+  }
+  if (use_gsort(ch, m, algo)) {
+    if (!gsort_ok(ch, m)) return set_error(TNB_EINVAL, "the global-sort algorithm does not support this chain");
+    info->algo = TNB_ALGO_GSORT;
+    gsort_info(ch, m, info);
     return TNB_OK;
   }
   if (use_bucketed(ch, m, algo) && bucketed_ok(ch)) {
@@ -335,12 +356,17 @@ int launch_entries(const tnb_chain* c, const int64_t* idx, int64_t m, void* out_
   rc = check_cuda(cudaMemsetAsync(err, 0x7f, sizeof(int32_t), st), "memset err");
   if (rc || m == 0) return rc;
   if (elt == 8) {  // float64: the generic algorithms only
-    if (use == TNB_ALGO_BUCKETED) return set_error(TNB_EINVAL, "the bucketed algorithm is fp32 only");
+    if (use == TNB_ALGO_BUCKETED || use == TNB_ALGO_GSORT)
+      return set_error(TNB_EINVAL, "the bucketed / global-sort algorithms are fp32 only");
     const int use64 = pick_algo_f64(c, algo, rmax0, m);
     return entries_generic<double>(c, ch, use64, idx, m, static_cast<double*>(out_v), err, ws, ws_bytes, st);
   }
   float* out = static_cast<float*>(out_v);
   if (use_two_table(c, ch, m, algo)) return launch_two_table(ch, idx, m, out, err, ws, ws_bytes, st);
+  if (use_gsort(ch, m, algo)) {
+    if (!gsort_ok(ch, m)) return set_error(TNB_EINVAL, "the global-sort algorithm does not support this chain");
+    return launch_entries_gsort(ch, idx, m, out, err, ws, ws_bytes, st);
+  }
   if ((algo == TNB_ALGO_AUTO && use_bucketed(ch, m, algo)) || use == TNB_ALGO_BUCKETED)
     return launch_bucketed_any(ch, idx, m, out, err, ws, ws_bytes, st);
   return entries_generic<float>(c, ch, use, idx, m, out, err, ws, ws_bytes, st);

@@ -3110,4 +3110,8 @@ int launch_two_table(const ChainDev& ch, const int64_t* idx, int64_t m, float* o
   return check_launch("two_table");
 }
 
+
+// the global-sort tcgen05 path shares the planner and the table kernels above
+#include "entries_gsort.cuh"
+
 }  // namespace tnb

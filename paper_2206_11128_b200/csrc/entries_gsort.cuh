@@ -1,0 +1,1044 @@
+// K1, global-sort path (TNB_ALGO_GSORT): entry evaluation on tcgen05.
+//
+// Reference algorithm (core.py:432-444): per mode, argsort the samples by
+// their index so every group shares one core slice and the group's update is
+// a real GEMM.  The bucketed kernels (entries_bucketed.cu) group per tile,
+// on chip, which leaves ~45 samples per bucket: too few rows for a tcgen05
+// tile, so they run mma.sync.  This path sorts ONCE, globally, by the index
+// of a MERGED interior mode, so that every bucket is thousands of samples
+// that share one B operand and the per-entry work is ONE r x r product:
+//
+//   * mode merging (plan_merge) shortens the chain to
+//       first . [dense interior modes] . [diag table] . last
+//     and plan_gsort merges the dense interior modes into one table of
+//     K = prod J slices M[key] = G_a[j_a] ... G_b[j_b] (r0 x r1), each stored
+//     as the UMMA K-major SWIZZLE_128B image of its transpose, split into
+//     tf32 hi / lo (gs_mid_image_kernel).  cfg2: P0123 . G45 (1024 slices) .
+//     S6789;  cfg5: P012 . G3 (128 slices) . D45 . S67;
+//   * gs_prep_kernel: reads the int64 index rows once, wraps and validates
+//     every ORIGINAL mode (lowest bad mode -> *err, core.py:409-416), and
+//     writes one 16-byte record per sample {key, first row, last row, diag
+//     row} plus the global histogram of the keys;
+//   * gs_scan_kernel: bucket starts, and the start of every bucket in
+//     128-sample tiles (the compute kernel's work list);
+//   * gs_scatter_kernel: counting-sort scatter of the records by key (the
+//     order inside a bucket is not fixed, and need not be: a sample's
+//     arithmetic does not depend on its position);
+//   * entries_gsort_kernel (persistent, one 512-thread CTA per SM), per tile
+//     of 128 sorted samples of one bucket:
+//       producer warps   gather the samples' first-table rows into the A
+//                        operand tile (K-major SW128 layout) and their
+//                        closing rows (last / diag tables) into shared memory
+//                        with 16-byte cp.async, several tiles ahead;
+//       splitter warps   x -> tf32 hi (in place) and lo = x - hi (second tile);
+//       one MMA lane     D[128 x 32] = Ahi Bhi + Alo Bhi + Ahi Blo
+//                        (tcgen05.mma.kind::tf32, accumulators in TMEM);
+//       epilogue warps   tcgen05.ld the D row of their sample, dot it with the
+//                        closing rows, write out[orig].
+// The kernel is bound by the random row gathers (HBM / L2), not by the MMAs.
+#pragma once
+
+#define TMEM_LD32_GS(taddr, v)                                                                 \
+  asm volatile(                                                                                \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "   \
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "  \
+      "%28, %29, %30, %31}, [%32];"                                                            \
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),    \
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),             \
+        "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),          \
+        "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),          \
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),          \
+        "=r"(v[31])                                                                            \
+      : "r"(taddr))
+
+namespace {
+
+constexpr int kGsSmemK = 8192;           // up to here the histograms live in shared memory
+constexpr int kGsMaxK = 65536;           // buckets (above kGsSmemK: warp-aggregated global atomics)
+constexpr int kGsTile = 128;             // samples per tile (UMMA M)
+constexpr int kGsRow = 128;              // bytes per operand row (one SW128 atom row)
+constexpr int kGsTileBytes = kGsTile * kGsRow;  // 16 KB
+constexpr int kGsImgBytes = 2 * 32 * kGsRow;    // hi + lo image of one slice: 8 KB
+constexpr int kGsNA = 4;                 // TMEM accumulators (32 columns each)
+constexpr int kGsNB = 4;                 // slice images in flight
+constexpr int kGsThreads = 512;
+constexpr int kGsPrepThreads = 512;
+constexpr int kGsScatThreads = 512, kGsScatPer = 8;
+
+struct GPlan {
+  MergePlan mp;
+  int gdiag = -1;          // virtual group of the diagonal table, or -1
+  int omid_lo = 0, omid_hi = 0;  // original modes merged into the sorted mode
+  int r0 = 0, r1 = 0;      // its slices are r0 x r1
+  int64_t K = 0;           // ... and there are K of them
+  int64_t lvl_off[kMaxModes];  // mid level ending at original mode o (o > omid_lo)
+  int64_t img_off = 0, hist_off = 0, bstart_off = 0, tbase_off = 0, cursor_off = 0;
+  int64_t recu_off = 0, recs_off = 0, total_bytes = 0;
+};
+
+struct GsPrep {
+  int32_t n0;
+  uint32_t K;
+  int32_t oJ[kMaxModes];
+  int8_t grp[kMaxModes];  // 0 first, 1 sorted (mid), 2 diag, 3 last
+};
+
+int gsort_env() {
+  const char* e = getenv("TNB_ENTRIES_GSORT");
+  return (e && e[0] == '0') ? 0 : 1;
+}
+
+bool plan_gsort(const ChainDev& ch, int64_t m, GPlan* G) {
+  const int N = ch.n;
+  if (ch.batch != 1 || N < 3 || N > kMaxModes || m < 1 || m >= ((int64_t)1 << 31)) return false;
+  for (int k = 0; k < N; ++k)
+    if (ch.m[k].bstride != 0 || ch.m[k].J <= 0) return false;
+  MergePlan& mp = G->mp;
+  plan_merge(ch, m, &mp);
+  if (mp.ng < 3) return false;
+  // first: a [rows][r0] table
+  const ModeDev& f = ch.m[mp.hi[0] - 1];
+  if (mp.kind[0] == kOrig && (ch.m[0].layout != TNB_LAYOUT_DENSE || ch.m[0].rl != 1)) return false;
+  if (mp.kind[0] != kOrig && mp.kind[0] != kPrefix) return false;
+  const int r0 = f.rr;
+  // the dense interior modes right after it
+  int g = 1;
+  int64_t K = 1;
+  while (g < mp.ng - 1 && mp.kind[g] == kOrig && ch.m[mp.lo[g]].layout == TNB_LAYOUT_DENSE) {
+    K *= ch.m[mp.lo[g]].J;
+    if (K > kGsMaxK) return false;
+    ++g;
+  }
+  if (g == 1) return false;
+  G->omid_lo = mp.lo[1];
+  G->omid_hi = mp.hi[g - 1];
+  if (ch.m[G->omid_lo].rl != r0) return false;
+  const int r1 = ch.m[G->omid_hi - 1].rr;
+  for (int o = G->omid_lo; o < G->omid_hi; ++o)
+    if (ch.m[o].rl > 32 || ch.m[o].rr > 32) return false;
+  // at most one diagonal table
+  G->gdiag = -1;
+  if (g < mp.ng - 1) {
+    const ModeDev& d = ch.m[mp.lo[g]];
+    if (d.layout != TNB_LAYOUT_DIAG || d.rl != r1) return false;
+    G->gdiag = g;
+    ++g;
+  }
+  if (g != mp.ng - 1) return false;
+  // last: a [rows][r1] table
+  if (mp.kind[g] != kOrig && mp.kind[g] != kSuffix) return false;
+  const ModeDev& l = ch.m[mp.lo[g]];
+  if (mp.kind[g] == kOrig && (l.layout != TNB_LAYOUT_DENSE || l.rr != 1)) return false;
+  if (l.rl != r1) return false;
+  if (r0 < 4 || r0 > 32 || (r0 & 3) || r1 < 4 || r1 > 32 || (r1 & 3)) return false;
+  G->r0 = r0;
+  G->r1 = r1;
+  G->K = K;
+  // the bucketed kernels' slice copies are not needed here
+  for (int v = 0; v < mp.ng; ++v) mp.lm[v] = mp.mma[v] = 0;
+  int64_t off = mp.table_bytes;
+  auto take = [&](int64_t bytes) {
+    const int64_t o = off;
+    off += (bytes + 1023) & ~(int64_t)1023;
+    return o;
+  };
+  int64_t rows = (int64_t)ch.m[G->omid_lo].J * r0;
+  for (int o = G->omid_lo + 1; o < G->omid_hi; ++o) {
+    rows *= ch.m[o].J;
+    G->lvl_off[o] = take(rows * ch.m[o].rr * 4);
+  }
+  G->img_off = take(K * kGsImgBytes);
+  G->hist_off = take(K * 4);
+  G->bstart_off = take((K + 1) * 4);
+  G->tbase_off = take((K + 1) * 4);
+  G->cursor_off = take(K * 4);
+  G->recu_off = take(m * 16);
+  G->recs_off = take(m * 16);
+  G->total_bytes = off;
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// slice images: M (levels layout [j_lo][a][j_rest][c]) -> per key the K-major
+// SW128 image of M[key]^T (row n, 16-byte piece c at (c ^ (n & 7))), tf32 hi
+// then lo, zero padded to 32 x 32
+__global__ void gs_mid_image_kernel(const float* __restrict__ M, int64_t K, int64_t Jrest, int r0, int r1,
+                                    unsigned char* __restrict__ img) {
+  const int64_t total = K * 256;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = t >> 8;
+    const int n = (int)(t >> 3) & 31, c = (int)t & 7;
+    const int64_t jlo = k / Jrest, jr = k - jlo * Jrest;
+    float x[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int a = 4 * c + i;
+      x[i] = (n < r1 && a < r0) ? __ldg(M + ((jlo * r0 + a) * Jrest + jr) * r1 + n) : 0.f;
+    }
+    uint4 hi, lo;
+    uint32_t h, l;
+    split_tf32(x[0], h, l); hi.x = h; lo.x = l;
+    split_tf32(x[1], h, l); hi.y = h; lo.y = l;
+    split_tf32(x[2], h, l); hi.z = h; lo.z = l;
+    split_tf32(x[3], h, l); hi.w = h; lo.w = l;
+    unsigned char* dst = img + k * kGsImgBytes + n * kGsRow + ((c ^ (n & 7)) << 4);
+    *reinterpret_cast<uint4*>(dst) = hi;
+    *reinterpret_cast<uint4*>(dst + kGsImgBytes / 2) = lo;
+  }
+}
+
+// one prefix-style level: out[(p*J + j)*rr + c] = sum_a in[p*rl + a] G(j, a, c)
+int gs_prefix_level(const ModeDev& md, const float* in, int64_t rows, float* out, cudaStream_t st) {
+  const int64_t total = rows * md.J * md.rr;
+  if (total <= 0) return TNB_OK;
+  if (launch_table_tc<false>(md, in, rows, out, st)) {
+  } else if (table_gemm_ok(md, false)) {
+    table_gemm<false><<<dim3((unsigned)ceil_div(rows, kTRows), (unsigned)ceil_div(md.J, kTZ)), 256, 0, st>>>(md, in, rows,
+                                                                                                         out);
+  } else {
+    const int g = (int)std::min<int64_t>(ceil_div(total, 256), (int64_t)num_sms() * 8);
+    table_prefix_step<<<g, 256, 0, st>>>(md, in, rows, out);
+  }
+  return check_launch("gsort mid level");
+}
+
+int gs_build_mid(const ChainDev& ch, const GPlan& G, unsigned char* base, cudaStream_t st) {
+  KTimer kt("entries_mid", st);
+  const ModeDev& m0 = ch.m[G.omid_lo];
+  const float* in = m0.s;
+  int64_t rows = (int64_t)m0.J * G.r0, jrest = 1;
+  for (int o = G.omid_lo + 1; o < G.omid_hi; ++o) {
+    float* out = reinterpret_cast<float*>(base + G.lvl_off[o]);
+    int rc = gs_prefix_level(ch.m[o], in, rows, out, st);
+    if (rc) return rc;
+    in = out;
+    rows *= ch.m[o].J;
+    jrest *= ch.m[o].J;
+  }
+  const int g = (int)std::min<int64_t>(ceil_div(G.K * 256, 256), (int64_t)num_sms() * 8);
+  gs_mid_image_kernel<<<g, 256, 0, st>>>(in, G.K, jrest, G.r0, G.r1, base + G.img_off);
+  return check_launch("gsort mid image");
+}
+
+// ---------------------------------------------------------------------------
+// prep: thread = sample row; record {key, first row, last row, diag row}.
+// STAGE: each warp copies the 32 rows of its pass into shared memory with
+// coalesced 16-byte loads (all in flight at once) and every lane then reads
+// its own row back (row stride 8 N0 bytes: conflict-free for N0 = 8, 10);
+// otherwise each thread loads its row straight from global memory.
+constexpr int kGsStageN0 = 16;  // rows of up to 16 indices are staged
+template <bool SH, bool STAGE>
+__global__ void __launch_bounds__(kGsPrepThreads) gs_prep_kernel(const __grid_constant__ GsPrep gp,
+                                                                 const int64_t* __restrict__ idx, int64_t m,
+                                                                 int32_t* __restrict__ err, uint4* __restrict__ recu,
+                                                                 uint32_t* __restrict__ hist) {
+  extern __shared__ __align__(16) uint32_t gs_sh[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, N0 = gp.n0;
+  const uint32_t K = gp.K;
+  if (SH) {
+    for (uint32_t j = tid; j < K; j += kGsPrepThreads) gs_sh[j] = 0;
+    __syncthreads();
+  }
+  uint32_t f0, f1, f2, f3;
+  auto put = [&](int o, int64_t raw) {
+    const int32_t J = gp.oJ[o];
+    const uint32_t v = (uint32_t)norm_index(raw, J, o, err);
+    const int g = gp.grp[o];
+    if (g == 0) f0 = f0 * (uint32_t)J + v;
+    else if (g == 1) f1 = f1 * (uint32_t)J + v;
+    else if (g == 2) f2 = f2 * (uint32_t)J + v;
+    else f3 = f3 * (uint32_t)J + v;
+  };
+  auto emit = [&](int64_t s) {
+    recu[s] = make_uint4(f1, f0, f3, f2);
+    if (SH) {
+      atomicAdd(&gs_sh[f1], 1u);
+    } else {  // many buckets: one global atomic per distinct key of the warp
+      const unsigned mk = __match_any_sync(__activemask(), f1);
+      if (lane == __ffs(mk) - 1) atomicAdd(&hist[f1], (uint32_t)__popc(mk));
+    }
+  };
+  if (STAGE) {
+    const int h = N0 >> 1;  // 16-byte pieces per row
+    uint4* stage = reinterpret_cast<uint4*>(gs_sh + (SH ? ((K + 3) & ~3u) : 0)) + (size_t)warp * 32 * h;
+    constexpr int W = kGsPrepThreads / 32;
+    for (int64_t base = ((int64_t)blockIdx.x * W + warp) * 32; base < m; base += (int64_t)gridDim.x * W * 32) {
+      const int rows = (int)min((int64_t)32, m - base);
+      const int np = rows * h;
+      const uint4* src = reinterpret_cast<const uint4*>(idx + base * N0);
+      uint4 buf[kGsStageN0 / 2];
+#pragma unroll
+      for (int i = 0; i < kGsStageN0 / 2; ++i)
+        if (i < h && lane + 32 * i < np) buf[i] = __ldcs(src + lane + 32 * i);
+#pragma unroll
+      for (int i = 0; i < kGsStageN0 / 2; ++i)
+        if (i < h && lane + 32 * i < np) {
+          const int pi = lane + 32 * i;  // rows of 4 pieces (64 B) are XOR-swizzled against bank conflicts
+          stage[h == 4 ? (pi ^ ((pi >> 3) & 3)) : pi] = buf[i];
+        }
+      __syncwarp();
+      if (lane < rows) {
+        f0 = f1 = f2 = f3 = 0;
+        const longlong2* row = reinterpret_cast<const longlong2*>(stage + lane * h);
+        for (int o = 0; o < h; ++o) {
+          const longlong2 w = row[h == 4 ? (o ^ ((lane >> 1) & 3)) : o];
+          put(2 * o, w.x);
+          put(2 * o + 1, w.y);
+        }
+        emit(base + lane);
+      }
+      __syncwarp();
+    }
+  } else {
+    for (int64_t s = blockIdx.x * (int64_t)kGsPrepThreads + tid; s < m; s += (int64_t)gridDim.x * kGsPrepThreads) {
+      const int64_t* row = idx + s * N0;
+      f0 = f1 = f2 = f3 = 0;
+      for (int o = 0; o < N0; ++o) put(o, __ldg(row + o));
+      emit(s);
+    }
+  }
+  if (SH) {
+    __syncthreads();
+    for (uint32_t j = tid; j < K; j += kGsPrepThreads) {
+      const uint32_t c = gs_sh[j];
+      if (c) atomicAdd(&hist[j], c);
+    }
+  }
+}
+
+// scan (one CTA): bucket starts, tile starts, scatter cursors
+__global__ void __launch_bounds__(1024) gs_scan_kernel(const uint32_t* __restrict__ hist, uint32_t K,
+                                                       uint32_t* __restrict__ bstart, uint32_t* __restrict__ tbase,
+                                                       uint32_t* __restrict__ cursor) {
+  __shared__ uint32_t wc[32], wt[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t per = (K + 1023) / 1024;
+  const uint32_t j0 = min(K, tid * per), j1 = min(K, j0 + per);
+  uint32_t c = 0, t = 0;
+  for (uint32_t j = j0; j < j1; ++j) {
+    const uint32_t h = hist[j];
+    c += h;
+    t += (h + kGsTile - 1) / kGsTile;
+  }
+  uint32_t ic = c, it = t;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t yc = __shfl_up_sync(0xffffffffu, ic, o), yt = __shfl_up_sync(0xffffffffu, it, o);
+    if (lane >= o) {
+      ic += yc;
+      it += yt;
+    }
+  }
+  if (lane == 31) {
+    wc[warp] = ic;
+    wt[warp] = it;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t xc = wc[lane], xt = wt[lane];
+    uint32_t sc = xc, stt = xt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t yc = __shfl_up_sync(0xffffffffu, sc, o), yt = __shfl_up_sync(0xffffffffu, stt, o);
+      if (lane >= o) {
+        sc += yc;
+        stt += yt;
+      }
+    }
+    wc[lane] = sc - xc;
+    wt[lane] = stt - xt;
+    if (lane == 31) {
+      bstart[K] = sc;
+      tbase[K] = stt;
+    }
+  }
+  __syncthreads();
+  uint32_t rc = wc[warp] + ic - c, rt = wt[warp] + it - t;
+  for (uint32_t j = j0; j < j1; ++j) {
+    const uint32_t h = hist[j];
+    bstart[j] = rc;
+    cursor[j] = rc;
+    tbase[j] = rt;
+    rc += h;
+    rt += (h + kGsTile - 1) / kGsTile;
+  }
+}
+
+// scatter: each CTA takes 4096 records, counts its keys in shared memory
+// (the count a sample draws is its rank inside the CTA's share of the bucket),
+// reserves the CTA's range of every bucket with one atomicAdd, sorts the
+// records by key in shared memory and writes {orig, first row, last row, diag
+// row} runs to the sorted positions (a bucket's share is contiguous)
+__global__ void __launch_bounds__(kGsScatThreads) gs_scatter_kernel(const uint4* __restrict__ recu, int64_t m, uint32_t K,
+                                                                     uint32_t* __restrict__ cursor,
+                                                                     uint4* __restrict__ recs) {
+  extern __shared__ __align__(16) uint32_t gs_sh[];
+  constexpr int TS = kGsScatThreads * kGsScatPer;
+  uint4* stg = reinterpret_cast<uint4*>(gs_sh);               // [TS] records in key order
+  uint16_t* skey = reinterpret_cast<uint16_t*>(stg + TS);     // [TS] their keys
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(skey + TS);     // [K] counts, then local starts
+  uint32_t* bas = cnt + K;                                    // [K] global start of the CTA's share
+  __shared__ uint32_t wsum[kGsScatThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t per = (K + kGsScatThreads - 1) / kGsScatThreads;
+  for (int64_t tile = blockIdx.x; tile * TS < m; tile += gridDim.x) {
+    const int n = (int)min((int64_t)TS, m - tile * TS);
+    for (uint32_t j = tid; j < K; j += kGsScatThreads) cnt[j] = 0;
+    __syncthreads();
+    uint4 r[kGsScatPer];
+    uint32_t rk[kGsScatPer];
+#pragma unroll
+    for (int i = 0; i < kGsScatPer; ++i) {
+      const int l = i * kGsScatThreads + tid;
+      if (l < n) r[i] = __ldcs(recu + tile * TS + l);
+    }
+#pragma unroll
+    for (int i = 0; i < kGsScatPer; ++i) {
+      const int l = i * kGsScatThreads + tid;
+      if (l < n) rk[i] = atomicAdd(&cnt[r[i].x], 1u);
+    }
+    __syncthreads();
+    // reserve, and turn the counts into local starts (block exclusive scan)
+    const uint32_t j0 = min(K, tid * per), j1 = min(K, j0 + per);
+    uint32_t sum = 0;
+    for (uint32_t j = j0; j < j1; ++j) {
+      const uint32_t c = cnt[j];
+      if (c) bas[j] = atomicAdd(&cursor[j], c);
+      sum += c;
+    }
+    uint32_t inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t x = lane < kGsScatThreads / 32 ? wsum[lane] : 0;
+      uint32_t sc = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, sc, o);
+        if (lane >= o) sc += y;
+      }
+      if (lane < kGsScatThreads / 32) wsum[lane] = sc - x;
+    }
+    __syncthreads();
+    uint32_t run = wsum[warp] + inc - sum;
+    for (uint32_t j = j0; j < j1; ++j) {
+      const uint32_t c = cnt[j];
+      cnt[j] = run;
+      run += c;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kGsScatPer; ++i) {
+      const int l = i * kGsScatThreads + tid;
+      if (l < n) {
+        const uint32_t slot = cnt[r[i].x] + rk[i];
+        stg[slot] = make_uint4((uint32_t)(tile * TS + l), r[i].y, r[i].z, r[i].w);
+        skey[slot] = (uint16_t)r[i].x;
+      }
+    }
+    __syncthreads();
+    for (int l = tid; l < n; l += kGsScatThreads) {
+      const uint32_t k = skey[l];
+      recs[bas[k] + ((uint32_t)l - cnt[k])] = stg[l];
+    }
+    __syncthreads();
+  }
+}
+
+// scatter with many buckets: thread = record, the warp's records of one key
+// reserve their slots with one global atomicAdd
+__global__ void __launch_bounds__(256) gs_scatter_big_kernel(const uint4* __restrict__ recu, int64_t m,
+                                                             uint32_t* __restrict__ cursor, uint4* __restrict__ recs) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m; s += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 r = __ldcs(recu + s);
+    const unsigned mk = __match_any_sync(__activemask(), r.x);
+    const int leader = __ffs(mk) - 1;
+    uint32_t b = 0;
+    if (lane == leader) b = atomicAdd(&cursor[r.x], (uint32_t)__popc(mk));
+    b = __shfl_sync(mk, b, leader);
+    recs[b + __popc(mk & ((1u << lane) - 1u))] = make_uint4((uint32_t)s, r.y, r.z, r.w);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// compute kernel
+struct GsArgs {
+  const float* P;             // [rows][r0]
+  const float* S;             // [rows][r1]
+  const float* D;             // [rows][r1] or null
+  const unsigned char* img;   // [K][8 KB]
+  const uint4* recs;          // sorted records
+  const uint32_t* bstart;     // [K + 1]
+  const uint32_t* tbase;      // [K + 1]
+  uint32_t K, m;
+  int32_t r0, r1;
+  float* out;
+};
+
+__device__ __forceinline__ void gs_wait(uint64_t* b, uint32_t parity) {
+  const uint32_t a = s32(b);
+  uint32_t done;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(done)
+      : "r"(a), "r"(parity)
+      : "memory");
+  if (done) return;
+  const long long t0 = clock64();
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (clock64() - t0 > 8000000000LL) __trap();  // ~4 s: a protocol bug, not a slow tile
+  }
+}
+__device__ __forceinline__ void gs_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s32(b)) : "memory");
+}
+__device__ __forceinline__ void gs_cp_arrive(uint64_t* b) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(s32(b)) : "memory");
+}
+__device__ __forceinline__ void gs_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(s32(b)) : "memory");
+}
+__device__ __forceinline__ void gs_cp16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ uint64_t gs_desc(uint32_t saddr) {  // K-major SWIZZLE_128B, SBO 1024
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+__device__ __forceinline__ void gs_mma(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+// position of every role in the CTA's tile range: the bucket of tile t, and
+// how many bucket changes came before it (the slice-image ring slot)
+struct GsWalk {
+  const uint32_t* tb;
+  uint32_t b, t_cur, t_next, nb;
+  __device__ void init(const uint32_t* tbase, uint32_t K, uint32_t t0) {
+    tb = tbase;
+    uint32_t lo = 0, hi = K - 1;  // first b with tbase[b + 1] > t0 (exists: t0 < tbase[K])
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (__ldg(tb + mid + 1) > t0) hi = mid;
+      else lo = mid + 1;
+    }
+    b = lo;
+    t_cur = __ldg(tb + b);
+    t_next = __ldg(tb + b + 1);
+    nb = 0;
+  }
+  __device__ bool advance(uint32_t t) {
+    bool chg = false;
+    while (t >= t_next) {
+      ++b;
+      t_cur = t_next;
+      t_next = __ldg(tb + b + 1);
+      chg = true;
+    }
+    if (chg) ++nb;
+    return chg;
+  }
+};
+
+template <bool DIAG>
+struct GsSmem {
+  static constexpr int NS = DIAG ? 3 : 4;                                   // gather stages
+  static constexpr int kStage = (DIAG ? 3 : 2) * kGsTileBytes + 1024;       // A | S | (D) | orig[128]
+  static constexpr int kOrigOff = (DIAG ? 3 : 2) * kGsTileBytes;
+  static constexpr int kAlo = NS * kStage;                                  // 2 x 16 KB
+  static constexpr int kB = kAlo + 2 * kGsTileBytes;                        // kGsNB x 8 KB
+  static constexpr int kBars = kB + kGsNB * kGsImgBytes;
+  static constexpr int kNBars = 3 * NS + 2 + 2 * kGsNA + 2 * kGsNB;
+  static constexpr int kBytes = kBars + kNBars * 8 + 16;
+};
+
+template <bool DIAG>
+__global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __grid_constant__ GsArgs ga) {
+  using L = GsSmem<DIAG>;
+  constexpr int NS = L::NS;
+  extern __shared__ __align__(1024) unsigned char gs_raw[];
+  unsigned char* smem = gs_raw + ((1024 - (s32(gs_raw) & 1023)) & 1023);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBars);
+  uint64_t* full_raw = bars;                  // [NS] 128 cp.async arrivals + 128 plain (orig stores)
+  uint64_t* a_ready = bars + NS;              // [NS] 128 splitter threads
+  uint64_t* empty = bars + 2 * NS;            // [NS] 128 epilogue threads
+  uint64_t* alo_empty = bars + 3 * NS;        // [2] tcgen05.commit
+  uint64_t* acc_full = alo_empty + 2;         // [NA] tcgen05.commit
+  uint64_t* acc_empty = acc_full + kGsNA;     // [NA] 128 epilogue threads
+  uint64_t* b_full = acc_empty + kGsNA;       // [NB] tx
+  uint64_t* b_empty = b_full + kGsNB;         // [NB] tcgen05.commit
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(b_empty + kGsNB);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t Nt = __ldg(ga.tbase + ga.K);
+  const uint32_t t0 = (uint32_t)(((uint64_t)Nt * blockIdx.x) / gridDim.x);
+  const uint32_t t1 = (uint32_t)(((uint64_t)Nt * (blockIdx.x + 1)) / gridDim.x);
+  const int r0 = ga.r0, r1 = ga.r1;
+
+  // operand pad columns (r0 up to a multiple of 8 floats) must read as zero
+  for (int i = tid; i < L::kB / 16; i += kGsThreads) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mb_init(&full_raw[s], 256);
+      mb_init(&a_ready[s], 128);
+      mb_init(&empty[s], 128);
+    }
+    mb_init(&alo_empty[0], 1);
+    mb_init(&alo_empty[1], 1);
+    for (int a = 0; a < kGsNA; ++a) {
+      mb_init(&acc_full[a], 1);
+      mb_init(&acc_empty[a], 128);
+    }
+    for (int b = 0; b < kGsNB; ++b) {
+      mb_init(&b_full[b], 1);
+      mb_init(&b_empty[b], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s32(tmem_slot)),
+                 "r"((uint32_t)(kGsNA * 32)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sbase = s32(smem);
+
+  if (t0 < t1) {
+    if (warp == 0) {
+      // ================= MMA issuer =================
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(32 >> 3) << 17) |
+                             ((uint32_t)(kGsTile >> 4) << 24);
+      const int nk = (r0 + 7) >> 3;
+      GsWalk w;
+      w.init(ga.tbase, ga.K, t0);
+      uint32_t it = 0;
+      bool first = true;
+      uint32_t slot = 0;
+      for (uint32_t t = t0; t < t1; ++t, ++it) {
+        const bool chg = w.advance(t);
+        if (first || chg) {
+          if (!first) {
+            if (lane == 0) gs_commit(&b_empty[slot]);  // the previous bucket's MMAs are all issued
+            __syncwarp();
+          }
+          slot = w.nb % kGsNB;
+          gs_wait(&b_full[slot], (w.nb / kGsNB) & 1);
+          first = false;
+        }
+        const uint32_t s = it % NS, a = it % kGsNA;
+        gs_wait(&a_ready[s], (it / NS) & 1);
+        gs_wait(&acc_empty[a], ((it / kGsNA) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (lane == 0) {
+          const uint32_t ahi = sbase + s * L::kStage, alo = sbase + L::kAlo + (it & 1) * kGsTileBytes;
+          const uint32_t bhi = sbase + L::kB + slot * kGsImgBytes, blo = bhi + kGsImgBytes / 2;
+          const uint32_t d = tmem + a * 32;
+          uint32_t acc = 0;
+          for (int kk = 0; kk < nk; ++kk) {
+            const uint64_t dah = gs_desc(ahi + kk * 32), dal = gs_desc(alo + kk * 32);
+            const uint64_t dbh = gs_desc(bhi + kk * 32), dbl = gs_desc(blo + kk * 32);
+            gs_mma(d, dal, dbh, idesc, acc);
+            gs_mma(d, dah, dbl, idesc, 1);
+            gs_mma(d, dah, dbh, idesc, 1);
+            acc = 1;
+          }
+          gs_commit(&acc_full[a]);
+          gs_commit(&alo_empty[it & 1]);
+        }
+        __syncwarp();
+      }
+    } else if (warp == 1) {
+      // ================= slice images -> ring =================
+      if (lane == 0) {
+        GsWalk w;
+        w.init(ga.tbase, ga.K, t0);
+        bool first = true;
+        for (uint32_t t = t0; t < t1; ++t) {
+          const bool chg = w.advance(t);
+          if (first || chg) {
+            const uint32_t slot = w.nb % kGsNB;
+            gs_wait(&b_empty[slot], ((w.nb / kGsNB) & 1) ^ 1);
+            mb_expect(&b_full[slot], kGsImgBytes);
+            bulk(smem + L::kB + slot * kGsImgBytes, ga.img + (size_t)w.b * kGsImgBytes, kGsImgBytes, &b_full[slot]);
+            first = false;
+          }
+        }
+      }
+    } else if (warp >= 4 && warp < 8) {
+      // ================= epilogue: thread = sample row =================
+      const int q = warp & 3, row = q * 32 + lane;
+      const uint32_t swz = (uint32_t)(row & 7);
+      const int n4 = r1 >> 2;
+      uint32_t it = 0;
+      for (uint32_t t = t0; t < t1; ++t, ++it) {
+        const uint32_t s = it % NS, a = it % kGsNA;
+        gs_wait(&full_raw[s], (it / NS) & 1);
+        const unsigned char* st = smem + s * L::kStage;
+        const uint32_t orig = reinterpret_cast<const uint32_t*>(st + L::kOrigOff)[row];
+        float wv[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          if (c < n4) {
+            const uint32_t off = (uint32_t)row * kGsRow + (((uint32_t)c ^ swz) << 4);
+            float4 x = *reinterpret_cast<const float4*>(st + kGsTileBytes + off);
+            if (DIAG) {
+              const float4 y = *reinterpret_cast<const float4*>(st + 2 * kGsTileBytes + off);
+              x.x *= y.x;
+              x.y *= y.y;
+              x.z *= y.z;
+              x.w *= y.w;
+            }
+            wv[4 * c] = x.x;
+            wv[4 * c + 1] = x.y;
+            wv[4 * c + 2] = x.z;
+            wv[4 * c + 3] = x.w;
+          }
+        }
+        gs_wait(&acc_full[a], (it / kGsNA) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        uint32_t v[32];
+        TMEM_LD32_GS(tmem + ((uint32_t)(q * 32) << 16) + a * 32, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        gs_arrive(&acc_empty[a]);
+        float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          if (c < n4) {
+            acc0 = fmaf(__uint_as_float(v[4 * c]), wv[4 * c], acc0);
+            acc1 = fmaf(__uint_as_float(v[4 * c + 1]), wv[4 * c + 1], acc1);
+            acc0 = fmaf(__uint_as_float(v[4 * c + 2]), wv[4 * c + 2], acc0);
+            acc1 = fmaf(__uint_as_float(v[4 * c + 3]), wv[4 * c + 3], acc1);
+          }
+        }
+        if (orig != 0xffffffffu) ga.out[orig] = acc0 + acc1;
+        gs_arrive(&empty[s]);
+      }
+    } else if (warp >= 8 && warp < 12) {
+      // ================= producers: gathers =================
+      const int pw = warp - 8;
+      const int pa = r0 >> 2, ps = r1 >> 2;
+      GsWalk w;
+      w.init(ga.tbase, ga.K, t0);
+      uint32_t it = 0;
+      const int c = lane & 7;
+      const int row = pw * 32 + lane;
+      // the records of the CTA's tiles are one contiguous stream: the next
+      // tile's record is loaded one tile ahead, and the stream is prefetched
+      // into L2 eight tiles ahead
+      auto locate = [&](uint32_t t, uint32_t& p0, int& n) {
+        w.advance(t);
+        p0 = __ldg(ga.bstart + w.b) + (t - w.t_cur) * kGsTile;
+        const uint32_t left = __ldg(ga.bstart + w.b + 1) - p0;
+        n = left < (uint32_t)kGsTile ? (int)left : kGsTile;
+      };
+      uint32_t np0;
+      int nn;
+      locate(t0, np0, nn);
+      uint4 nrec = make_uint4(0xffffffffu, 0, 0, 0);
+      if (row < nn) nrec = __ldg(ga.recs + np0 + row);
+      for (uint32_t t = t0; t < t1; ++t, ++it) {
+        const uint4 rec = nrec;
+        const int n = nn;
+        if (t + 1 < t1) {
+          locate(t + 1, np0, nn);
+          nrec = make_uint4(0xffffffffu, 0, 0, 0);
+          if (row < nn) nrec = __ldg(ga.recs + np0 + row);
+          const uint32_t pf = np0 + (uint32_t)row + 8 * kGsTile;
+          if ((lane & 1) == 0 && pf < ga.m) prefetch_l2(ga.recs + pf);
+        }
+        const uint32_t s = it % NS;
+        gs_wait(&empty[s], ((it / NS) & 1) ^ 1);
+        unsigned char* st = smem + s * L::kStage;
+        reinterpret_cast<uint32_t*>(st + L::kOrigOff)[row] = rec.x;
+        const uint32_t sa = sbase + s * L::kStage;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int src = 4 * i + (lane >> 3);
+          const int r = pw * 32 + src;
+          const uint32_t pr = __shfl_sync(0xffffffffu, rec.y, src);
+          const uint32_t sr = __shfl_sync(0xffffffffu, rec.z, src);
+          const uint32_t dr = __shfl_sync(0xffffffffu, rec.w, src);
+          const uint32_t off = (uint32_t)r * kGsRow + (((uint32_t)c ^ (uint32_t)(r & 7)) << 4);
+          if (r < n) {
+            if (c < pa) gs_cp16(sa + off, ga.P + (size_t)pr * r0 + 4 * c);
+            if (c < ps) {
+              gs_cp16(sa + kGsTileBytes + off, ga.S + (size_t)sr * r1 + 4 * c);
+              if (DIAG) gs_cp16(sa + 2 * kGsTileBytes + off, ga.D + (size_t)dr * r1 + 4 * c);
+            }
+          }
+        }
+        gs_cp_arrive(&full_raw[s]);
+        gs_arrive(&full_raw[s]);
+      }
+    } else if (warp >= 12) {
+      // ================= splitters: x -> tf32 hi (in place), lo =================
+      const int row = (warp - 12) * 32 + lane;
+      const uint32_t swz = (uint32_t)(row & 7);
+      const int npc = ((r0 + 7) >> 3) * 2;
+      uint32_t it = 0;
+      for (uint32_t t = t0; t < t1; ++t, ++it) {
+        const uint32_t s = it % NS;
+        gs_wait(&full_raw[s], (it / NS) & 1);
+        gs_wait(&alo_empty[it & 1], ((it >> 1) & 1) ^ 1);
+        unsigned char* A = smem + s * L::kStage;
+        unsigned char* Alo = smem + L::kAlo + (it & 1) * kGsTileBytes;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          if (c < npc) {
+            const uint32_t off = (uint32_t)row * kGsRow + (((uint32_t)c ^ swz) << 4);
+            const float4 x = *reinterpret_cast<const float4*>(A + off);
+            uint4 hi, lo;
+            uint32_t h, l;
+            split_tf32_fast(x.x, h, l); hi.x = h; lo.x = l;
+            split_tf32_fast(x.y, h, l); hi.y = h; lo.y = l;
+            split_tf32_fast(x.z, h, l); hi.z = h; lo.z = l;
+            split_tf32_fast(x.w, h, l); hi.w = h; lo.w = l;
+            *reinterpret_cast<uint4*>(A + off) = hi;
+            *reinterpret_cast<uint4*>(Alo + off) = lo;
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        gs_arrive(&a_ready[s]);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)(kGsNA * 32)));
+  }
+}
+
+void gs_fill_prep(const ChainDev& ch, const GPlan& G, GsPrep* gp) {
+  const MergePlan& mp = G.mp;
+  gp->n0 = ch.n;
+  gp->K = (uint32_t)G.K;
+  for (int g = 0; g < mp.ng; ++g)
+    for (int o = mp.lo[g]; o < mp.hi[g]; ++o) {
+      gp->oJ[o] = ch.m[o].J;
+      gp->grp[o] = (int8_t)(g == 0 ? 0 : (g == mp.ng - 1 ? 3 : (g == G.gdiag ? 2 : 1)));
+    }
+}
+
+}  // namespace
+
+bool gsort_ok(const ChainDev& ch, int64_t m) {
+  static thread_local GPlan G;
+  if (!plan_gsort(ch, m, &G)) return false;
+  // 16-byte row pieces: original boundary modes must be 16-byte aligned
+  if (G.mp.kind[0] == kOrig && (reinterpret_cast<uintptr_t>(ch.m[0].s) & 15)) return false;
+  if (G.mp.kind[G.mp.ng - 1] == kOrig && (reinterpret_cast<uintptr_t>(ch.m[ch.n - 1].s) & 15)) return false;
+  if (G.gdiag >= 0 && G.mp.kind[G.gdiag] == kOrig && (reinterpret_cast<uintptr_t>(ch.m[G.mp.lo[G.gdiag]].s) & 15))
+    return false;
+  return true;
+}
+
+int64_t gsort_buckets(const ChainDev& ch, int64_t m);
+// AUTO: large calls whose buckets average at least 512 samples (4 tiles)
+bool gsort_auto(const ChainDev& ch, int64_t m) {
+  if (!gsort_env() || m < (1 << 18) || !gsort_ok(ch, m)) return false;
+  return gsort_buckets(ch, m) * 512 <= m;
+}
+
+int64_t gsort_buckets(const ChainDev& ch, int64_t m) {
+  static thread_local GPlan G;
+  return plan_gsort(ch, m, &G) ? G.K : 0;
+}
+
+int64_t gsort_workspace(const ChainDev& ch, int64_t m) {
+  static thread_local GPlan G;
+  return plan_gsort(ch, m, &G) ? G.total_bytes : 0;
+}
+
+void gsort_info(const ChainDev& ch, int64_t m, tnb_entries_info* info) {
+  static thread_local GPlan G;
+  if (!plan_gsort(ch, m, &G)) return;
+  const MergePlan& mp = G.mp;
+  info->compute_kernel = 3;
+  info->tile = kGsTile;
+  info->n_virtual = 3 + (G.gdiag >= 0 ? 1 : 0);
+  info->prefix_modes = mp.a();
+  info->suffix_modes = mp.b();
+  info->prefix_rows = mp.a() > 1 ? mp.rows[0] : 0;
+  info->suffix_rows = mp.b() > 1 ? mp.rows[mp.ng - 1] : 0;
+  info->diag_tables = 0;
+  info->table_launches = table_launches(mp) + (G.omid_hi - G.omid_lo);
+  // per entry: one r0 x r1 product (3 tf32 MMAs), the diagonal scale, the closing dot
+  info->tensor_flops = 3.0 * 2.0 * G.r0 * G.r1 * (double)m;
+  info->kernel_flops = (2.0 * G.r0 * G.r1 + (G.gdiag >= 0 ? G.r1 : 0) + 2.0 * G.r1) * (double)m;
+  double tf = 0.0;
+  for (int g = 0; g < mp.ng; ++g) {
+    const int lo = mp.lo[g], hi = mp.hi[g];
+    if (mp.kind[g] == kDiag) ++info->diag_tables;
+    if (mp.kind[g] == kPrefix || mp.kind[g] == kDiag) {
+      int64_t rows = ch.m[lo].J;
+      for (int o = lo + 1; o < hi; ++o) {
+        rows *= ch.m[o].J;
+        tf += (double)rows * ch.m[o].rr * (ch.m[o].layout == TNB_LAYOUT_DIAG ? 1.0 : 2.0 * ch.m[o].rl);
+      }
+    } else if (mp.kind[g] == kSuffix) {
+      int64_t rows = ch.m[hi - 1].J;
+      for (int o = hi - 2; o >= lo; --o) {
+        rows *= ch.m[o].J;
+        tf += (double)rows * ch.m[o].rl * (ch.m[o].layout == TNB_LAYOUT_DIAG ? 1.0 : 2.0 * ch.m[o].rr);
+      }
+    }
+  }
+  int64_t rows = (int64_t)ch.m[G.omid_lo].J * G.r0;
+  for (int o = G.omid_lo + 1; o < G.omid_hi; ++o) {
+    rows *= ch.m[o].J;
+    tf += (double)rows * ch.m[o].rr * 2.0 * ch.m[o].rl;
+  }
+  info->table_flops = tf;
+}
+
+int launch_entries_gsort(const ChainDev& ch, const int64_t* idx, int64_t m, float* out, int32_t* err, void* ws,
+                         int64_t ws_bytes, cudaStream_t st) {
+  static thread_local GPlan G;
+  if (!plan_gsort(ch, m, &G)) return set_error(TNB_EINVAL, "the global-sort algorithm does not support this chain");
+  if (!ws || ws_bytes < G.total_bytes)
+    return set_error(TNB_EWORKSPACE, "global-sort entries needs %lld workspace bytes, got %lld",
+                     (long long)G.total_bytes, (long long)ws_bytes);
+  unsigned char* base = static_cast<unsigned char*>(ws);
+  const MergePlan& mp = G.mp;
+  int rc;
+  // tables (first / last / diag) and the slice images depend only on the
+  // cores: side stream, concurrent with the index passes
+  cudaEvent_t tables = nullptr;
+  SideStream* ss = table_stream_env() ? side_stream() : nullptr;
+  if (ss) {
+    rc = check_cuda(cudaEventRecord(ss->fork, st), "fork");
+    if (!rc) rc = check_cuda(cudaStreamWaitEvent(ss->s, ss->fork, 0), "fork wait");
+    if (rc) return rc;
+    rc = build_tables(ch, mp, base, ss->s);
+    if (!rc) rc = gs_build_mid(ch, G, base, ss->s);
+    const int rj = check_cuda(cudaEventRecord(ss->join, ss->s), "join");
+    if (rc || rj) {
+      if (!rj) cudaStreamWaitEvent(st, ss->join, 0);
+      else cudaStreamSynchronize(ss->s);
+      return rc ? rc : rj;
+    }
+    tables = ss->join;
+  } else {
+    rc = build_tables(ch, mp, base, st);
+    if (!rc) rc = gs_build_mid(ch, G, base, st);
+    if (rc) return rc;
+  }
+  auto fail = [&](int code) {
+    if (tables) cudaStreamWaitEvent(st, tables, 0);
+    return code;
+  };
+  static thread_local ChainDev v;
+  virtual_chain(ch, mp, base, &v);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(base + G.hist_off);
+  uint32_t* bstart = reinterpret_cast<uint32_t*>(base + G.bstart_off);
+  uint32_t* tbase = reinterpret_cast<uint32_t*>(base + G.tbase_off);
+  uint32_t* cursor = reinterpret_cast<uint32_t*>(base + G.cursor_off);
+  uint4* recu = reinterpret_cast<uint4*>(base + G.recu_off);
+  uint4* recs = reinterpret_cast<uint4*>(base + G.recs_off);
+  const uint32_t K = (uint32_t)G.K;
+  rc = check_cuda(cudaMemsetAsync(hist, 0, (size_t)K * 4, st), "gsort hist");
+  if (rc) return fail(rc);
+  {
+    static thread_local GsPrep gp;
+    gs_fill_prep(ch, G, &gp);
+    const bool sh = K <= (uint32_t)kGsSmemK;
+    const bool stage = (ch.n & 1) == 0 && ch.n <= kGsStageN0 && (reinterpret_cast<uintptr_t>(idx) & 15) == 0;
+    const size_t sm = (sh ? (size_t)((K + 3) & ~3u) * 4 : 0) + (stage ? (size_t)kGsPrepThreads * (ch.n / 2) * 16 : 0);
+    auto pk = sh ? (stage ? gs_prep_kernel<true, true> : gs_prep_kernel<true, false>)
+                 : (stage ? gs_prep_kernel<false, true> : gs_prep_kernel<false, false>);
+    if (sm > 48 * 1024) {
+      rc = check_cuda(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "gsort prep smem");
+      if (rc) return fail(rc);
+    }
+    const int per_sm = sm > 56 * 1024 ? 2 : 4;
+    const int64_t g = std::min<int64_t>(ceil_div(m, kGsPrepThreads), (int64_t)num_sms() * per_sm);
+    KTimer kt("entries_prep", st);
+    pk<<<(unsigned)g, kGsPrepThreads, sm, st>>>(gp, idx, m, err, recu, hist);
+  }
+  rc = check_launch("gsort prep");
+  if (rc) return fail(rc);
+  {
+    KTimer kt("entries_sort", st);
+    gs_scan_kernel<<<1, 1024, 0, st>>>(hist, K, bstart, tbase, cursor);
+    const size_t sm = (size_t)kGsScatThreads * kGsScatPer * 18 + (size_t)K * 8;
+    if (K > (uint32_t)kGsSmemK) {
+      const int64_t g = std::min<int64_t>(ceil_div(m, 256), (int64_t)num_sms() * 16);
+      gs_scatter_big_kernel<<<(unsigned)g, 256, 0, st>>>(recu, m, cursor, recs);
+    } else {
+      if (sm > 48 * 1024)
+        rc = check_cuda(cudaFuncSetAttribute(gs_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
+                        "gsort scatter smem");
+      if (!rc) {
+        const int64_t g =
+            std::min<int64_t>(ceil_div(m, (int64_t)kGsScatThreads * kGsScatPer), (int64_t)num_sms() * 8);
+        gs_scatter_kernel<<<(unsigned)g, kGsScatThreads, sm, st>>>(recu, m, K, cursor, recs);
+      }
+    }
+  }
+  if (rc) return fail(rc);
+  rc = check_launch("gsort sort");
+  if (rc) return fail(rc);
+  if (tables) {
+    rc = check_cuda(cudaStreamWaitEvent(st, tables, 0), "join tables");
+    if (rc) return rc;
+  }
+  GsArgs ga;
+  ga.P = v.m[0].s;
+  ga.S = v.m[mp.ng - 1].s;
+  ga.D = G.gdiag >= 0 ? v.m[G.gdiag].s : nullptr;
+  ga.img = base + G.img_off;
+  ga.recs = recs;
+  ga.bstart = bstart;
+  ga.tbase = tbase;
+  ga.K = K;
+  ga.m = (uint32_t)m;
+  ga.r0 = G.r0;
+  ga.r1 = G.r1;
+  ga.out = out;
+  const bool diag = G.gdiag >= 0;
+  const size_t smem = 1024 + (diag ? GsSmem<true>::kBytes : GsSmem<false>::kBytes);
+  auto kfn = diag ? entries_gsort_kernel<true> : entries_gsort_kernel<false>;
+  rc = check_cuda(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "gsort smem attr");
+  if (rc) return rc;
+  const int64_t tiles_max = ceil_div(m, kGsTile) + (int64_t)K;
+  const int grid = (int)std::min<int64_t>(tiles_max, num_sms());
+  {
+    KTimer kt("entries_compute", st);
+    kfn<<<grid, kGsThreads, smem, st>>>(ga);
+  }
+  return check_launch("entries_gsort");
+}

@@ -44,7 +44,7 @@ def one(cfg, algo=0, reps=5):
         ws = C.launch_entries(p, idx, out, err, algo, ws)
     e1.record()
     torch.cuda.synchronize()
-    kt = {k: N.timing_read(k) for k in ("entries_prep", "entries_sort", "entries_compute", "entries_tables")}
+    kt = {k: N.timing_read(k) for k in ("entries_prep", "entries_sort", "entries_compute", "entries_tables", "entries_mid")}
     N.timing_enable(False)
     ms = e0.elapsed_time(e1) / reps
     flops = W.entry_flops(modes) * m
