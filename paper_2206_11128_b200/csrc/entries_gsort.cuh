@@ -51,6 +51,15 @@
         "=r"(v[31])                                                                            \
       : "r"(taddr))
 
+#define TMEM_LD16_GS(taddr, v)                                                                   \
+  asm volatile(                                                                                  \
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, " \
+      "%12, %13, %14, %15}, [%16];"                                                              \
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),      \
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), \
+        "=r"(v[14]), "=r"(v[15])                                                                 \
+      : "r"(taddr))
+
 namespace {
 
 constexpr int kGsSmemK = 8192;           // up to here the histograms live in shared memory
@@ -59,9 +68,25 @@ constexpr int kGsTile = 128;             // samples per tile (UMMA M)
 constexpr int kGsRow = 128;              // bytes per operand row (one SW128 atom row)
 constexpr int kGsTileBytes = kGsTile * kGsRow;  // 16 KB
 constexpr int kGsImgBytes = 2 * 32 * kGsRow;    // hi + lo image of one slice: 8 KB
-constexpr int kGsNA = 4;                 // TMEM accumulators (32 columns each)
-constexpr int kGsNB = 4;                 // slice images in flight
-constexpr int kGsThreads = 512;
+constexpr int kGsNA = 4;                 // TMEM accumulators (64 columns each: A Bhi | A Blo)
+constexpr int kGsNB = 2;                 // slice images in flight
+// warps: 0 MMA, 1 image loader, 2-3 idle, 4-7 epilogue, 8-11 splitters, 12-27 producers
+// (a warp holds at most ~8 LDGSTS in flight -- tools/gather_bench.cu -- so the
+// gather rate and a tile's gather latency are set by the number of producer warps)
+constexpr int kGsPW = 16;                // producer warps (8 rows of every tile each)
+constexpr int kGsThreads = (12 + kGsPW) * 32;
+#ifndef TNB_GS_PF
+#define TNB_GS_PF 8
+#endif
+#ifndef TNB_GS_PFROWS
+#define TNB_GS_PFROWS 6
+#endif
+#ifndef TNB_GS_PFL2
+#define TNB_GS_PFL2 32
+#endif
+constexpr int kGsPF = TNB_GS_PF;         // record loads in flight per producer lane (tiles)
+constexpr int kGsPFRows = TNB_GS_PFROWS;  // table rows are prefetched into L2 this many tiles ahead (< kGsPF)
+constexpr int kGsPFL2 = TNB_GS_PFL2;     // L2 prefetch distance of the record stream (tiles)
 constexpr int kGsPrepThreads = 512;
 constexpr int kGsScatThreads = 512, kGsScatPer = 8;
 
@@ -479,31 +504,32 @@ struct GsArgs {
   const uint32_t* tbase;      // [K + 1]
   uint32_t K, m;
   int32_t r0, r1;
+  int32_t pfP, pfS, pfD;      // tables too large for L2: their rows are streamed (evict_first)
+  int32_t keep_out;           // the result fits in L2: keep its lines there (evict_last)
   float* out;
+#ifdef TNB_GS_TRACE
+  unsigned long long* trace;  // [block][4 roles][6 phases] clock64 cycles
+#endif
 };
 
+// try_wait with a suspend-time hint: the waiting warp sleeps in hardware
+// until the phase completes instead of re-issuing the poll every ~20 cycles
+// (16 polling warps otherwise take most of the SM's issue slots from the few
+// working ones: the roles ran 2-3x slower)
 __device__ __forceinline__ void gs_wait(uint64_t* b, uint32_t parity) {
   const uint32_t a = s32(b);
   uint32_t done;
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, P1;\n\t}"
-      : "=r"(done)
-      : "r"(a), "r"(parity)
-      : "memory");
-  if (done) return;
-  const long long t0 = clock64();
+  int spins = 0;
   while (true) {
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, P1;\n\t}"
         : "=r"(done)
-        : "r"(a), "r"(parity)
+        : "r"(a), "r"(parity), "r"(1000000u)
         : "memory");
     if (done) return;
-    if (clock64() - t0 > 8000000000LL) __trap();  // ~4 s: a protocol bug, not a slow tile
+    if (++spins > 4000) __trap();  // ~4 s without progress: a protocol bug, not a slow tile
   }
 }
 __device__ __forceinline__ void gs_arrive(uint64_t* b) {
@@ -516,7 +542,17 @@ __device__ __forceinline__ void gs_commit(uint64_t* b) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(s32(b)) : "memory");
 }
 __device__ __forceinline__ void gs_cp16(uint32_t dst, const void* src) {
+#ifdef TNB_GS_CA
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+#else
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+#endif
+}
+// rows of a table too large for L2 are streamed (evict_first): they would
+// otherwise push out the result lines, whose scattered 4-byte writes only
+// merge into whole sectors while they stay in L2
+__device__ __forceinline__ void gs_cp16_stream(uint32_t dst, const void* src, uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(pol) : "memory");
 }
 __device__ __forceinline__ uint64_t gs_desc(uint32_t saddr) {  // K-major SWIZZLE_128B, SBO 1024
   uint64_t d = 0;
@@ -527,14 +563,61 @@ __device__ __forceinline__ uint64_t gs_desc(uint32_t saddr) {  // K-major SWIZZL
   d |= (uint64_t)2 << 61;
   return d;
 }
+// issued by the whole (converged) warp: one elected lane executes the MMA
 __device__ __forceinline__ void gs_mma(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\t"
+      "{\n\t.reg .pred p, q;\n\t"
+      "elect.sync _|q, 0xffffffff;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "@q tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
       : "memory");
 }
+__device__ __forceinline__ void gs_commit_elect(uint64_t* b) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\t"
+      "elect.sync _|q, 0xffffffff;\n\t"
+      "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(s32(b))
+      : "memory");
+}
+
+// TNB_GS_TRACE builds: every role's lane 0 accumulates the clock64 cycles it
+// spends in each phase of its loop and writes the sums at the end
+// (trace[block][role][phase]); tools/gs_trace.py prints the averages
+#ifdef TNB_GS_TRACE
+#define GS_TRACE_INIT() \
+  long long gs_acc_[6] = {0, 0, 0, 0, 0, 0}; \
+  long long gs_last_ = clock64()
+#define GS_TRACE(role, it, ev)              \
+  do {                                      \
+    const long long now_ = clock64();       \
+    gs_acc_[ev] += now_ - gs_last_;         \
+    gs_last_ = now_;                        \
+  } while (0)
+#define GS_STAMP(it, ev)                                                                 \
+  do {                                                                                   \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && (it) >= 256 && (it) < 288)         \
+      ga.trace[8192 + ((it) - 256) * 16 + (ev)] = (unsigned long long)clock64();         \
+  } while (0)
+#define GS_TRACE_END(role)                                                               \
+  do {                                                                                   \
+    if ((threadIdx.x & 31) == 0)                                                         \
+      for (int e_ = 0; e_ < 6; ++e_) ga.trace[(blockIdx.x * 4 + (role)) * 6 + e_] = (unsigned long long)gs_acc_[e_]; \
+  } while (0)
+#else
+#define GS_TRACE_INIT() \
+  do {                  \
+  } while (0)
+#define GS_TRACE(role, it, ev) \
+  do {                         \
+  } while (0)
+#define GS_TRACE_END(role) \
+  do {                     \
+  } while (0)
+#define GS_STAMP(it, ev) \
+  do {                   \
+  } while (0)
+#endif
 
 // position of every role in the CTA's tile range: the bucket of tile t, and
 // how many bucket changes came before it (the slice-image ring slot)
@@ -567,26 +650,33 @@ struct GsWalk {
   }
 };
 
-template <bool DIAG>
+// CSB: bytes between the closing rows (last / diag tables) of a stage: 128
+// (pieces XOR-swizzled like the operand tile) or 96 (compact rows of up to 24
+// floats: a fourth stage fits next to a diagonal table)
+template <bool DIAG, int CSB>
 struct GsSmem {
-  static constexpr int NS = DIAG ? 3 : 4;                                   // gather stages
-  static constexpr int kStage = (DIAG ? 3 : 2) * kGsTileBytes + 1024;       // A | S | (D) | orig[128]
-  static constexpr int kOrigOff = (DIAG ? 3 : 2) * kGsTileBytes;
-  static constexpr int kAlo = NS * kStage;                                  // 2 x 16 KB
-  static constexpr int kB = kAlo + 2 * kGsTileBytes;                        // kGsNB x 8 KB
-  static constexpr int kBars = kB + kGsNB * kGsImgBytes;
+  static constexpr int kClose = kGsTile * CSB;                               // one closing table's rows
+  static constexpr int kOrigOff = kGsTileBytes + (DIAG ? 2 : 1) * kClose;    // A | S | (D) | orig[128]
+  static constexpr int kStage = (kOrigOff + 512 + 1023) & ~1023;
+  static constexpr int NS = DIAG ? (CSB == 96 ? 4 : 3) : 5;                  // gather stages
+  static constexpr int kAlo = NS * kStage;                                   // 2 x 16 KB
+  static constexpr int kB = kAlo + 2 * kGsTileBytes;                         // kGsNB x 8 KB
+  static constexpr int RR = 4;                                               // record ring depth (tiles)
+  static constexpr int kRec = kB + kGsNB * kGsImgBytes;                      // kGsPW warps x RR x 8 records x 16 B
+  static constexpr int kBars = kRec + kGsPW * RR * 128;
   static constexpr int kNBars = 3 * NS + 2 + 2 * kGsNA + 2 * kGsNB;
   static constexpr int kBytes = kBars + kNBars * 8 + 16;
+  static_assert(kBytes + 1024 <= 232448, "shared memory");
 };
 
-template <bool DIAG>
+template <bool DIAG, int CSB>
 __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __grid_constant__ GsArgs ga) {
-  using L = GsSmem<DIAG>;
+  using L = GsSmem<DIAG, CSB>;
   constexpr int NS = L::NS;
   extern __shared__ __align__(1024) unsigned char gs_raw[];
   unsigned char* smem = gs_raw + ((1024 - (s32(gs_raw) & 1023)) & 1023);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBars);
-  uint64_t* full_raw = bars;                  // [NS] 128 cp.async arrivals + 128 plain (orig stores)
+  uint64_t* full_raw = bars;                  // [NS] every producer thread: one cp.async arrival + one plain (orig stores)
   uint64_t* a_ready = bars + NS;              // [NS] 128 splitter threads
   uint64_t* empty = bars + 2 * NS;            // [NS] 128 epilogue threads
   uint64_t* alo_empty = bars + 3 * NS;        // [2] tcgen05.commit
@@ -607,7 +697,7 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
-      mb_init(&full_raw[s], 256);
+      mb_init(&full_raw[s], 2 * 32 * kGsPW);
       mb_init(&a_ready[s], 128);
       mb_init(&empty[s], 128);
     }
@@ -625,7 +715,7 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s32(tmem_slot)),
-                 "r"((uint32_t)(kGsNA * 32)));
+                 "r"((uint32_t)(kGsNA * 64)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -637,20 +727,22 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
   if (t0 < t1) {
     if (warp == 0) {
       // ================= MMA issuer =================
-      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(32 >> 3) << 17) |
-                             ((uint32_t)(kGsTile >> 4) << 24);
+      const uint32_t idesc32 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(32 >> 3) << 17) |
+                               ((uint32_t)(kGsTile >> 4) << 24);
+      const uint32_t idesc64 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(64 >> 3) << 17) |
+                               ((uint32_t)(kGsTile >> 4) << 24);
       const int nk = (r0 + 7) >> 3;
       GsWalk w;
       w.init(ga.tbase, ga.K, t0);
       uint32_t it = 0;
       bool first = true;
       uint32_t slot = 0;
+      GS_TRACE_INIT();
       for (uint32_t t = t0; t < t1; ++t, ++it) {
         const bool chg = w.advance(t);
         if (first || chg) {
           if (!first) {
-            if (lane == 0) gs_commit(&b_empty[slot]);  // the previous bucket's MMAs are all issued
-            __syncwarp();
+            gs_commit_elect(&b_empty[slot]);  // the previous bucket's MMAs are all issued
           }
           slot = w.nb % kGsNB;
           gs_wait(&b_full[slot], (w.nb / kGsNB) & 1);
@@ -658,26 +750,37 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
         }
         const uint32_t s = it % NS, a = it % kGsNA;
         gs_wait(&a_ready[s], (it / NS) & 1);
+        GS_TRACE(0, it, 0);
+        GS_STAMP(it, 6);
         gs_wait(&acc_empty[a], ((it / kGsNA) & 1) ^ 1);
+        GS_TRACE(0, it, 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        if (lane == 0) {
-          const uint32_t ahi = sbase + s * L::kStage, alo = sbase + L::kAlo + (it & 1) * kGsTileBytes;
-          const uint32_t bhi = sbase + L::kB + slot * kGsImgBytes, blo = bhi + kGsImgBytes / 2;
-          const uint32_t d = tmem + a * 32;
-          uint32_t acc = 0;
-          for (int kk = 0; kk < nk; ++kk) {
-            const uint64_t dah = gs_desc(ahi + kk * 32), dal = gs_desc(alo + kk * 32);
-            const uint64_t dbh = gs_desc(bhi + kk * 32), dbl = gs_desc(blo + kk * 32);
-            gs_mma(d, dal, dbh, idesc, acc);
-            gs_mma(d, dah, dbl, idesc, 1);
-            gs_mma(d, dah, dbh, idesc, 1);
-            acc = 1;
+        {
+          // K-major SWIZZLE_128B descriptors: constant bits | (address >> 4); a
+          // k-step advances 32 bytes inside the 128-byte swizzle row.  Per
+          // k-step: Ahi x [Bhi | Blo] (N = 64: the image's hi and lo rows are
+          // contiguous) and Alo x Bhi (N = 32) -- the epilogue adds the halves
+          const uint64_t dc = ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+          const uint32_t ah = (sbase + s * L::kStage) >> 4, al = (sbase + L::kAlo + (it & 1) * kGsTileBytes) >> 4;
+          const uint32_t bh = (sbase + L::kB + slot * kGsImgBytes) >> 4;
+          const uint32_t d = tmem + a * 64;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            if (kk < nk) {
+              const uint64_t dah = dc | (uint64_t)(ah + 2 * kk), dal = dc | (uint64_t)(al + 2 * kk);
+              const uint64_t dbh = dc | (uint64_t)(bh + 2 * kk);
+              gs_mma(d, dah, dbh, idesc64, kk > 0);
+              gs_mma(d, dal, dbh, idesc32, 1);
+            }
           }
-          gs_commit(&acc_full[a]);
-          gs_commit(&alo_empty[it & 1]);
+          gs_commit_elect(&acc_full[a]);
+          gs_commit_elect(&alo_empty[it & 1]);
         }
+        GS_TRACE(0, it, 2);
+        GS_STAMP(it, 7);
         __syncwarp();
       }
+      GS_TRACE_END(0);
     } else if (warp == 1) {
       // ================= slice images -> ring =================
       if (lane == 0) {
@@ -701,144 +804,258 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
       const uint32_t swz = (uint32_t)(row & 7);
       const int n4 = r1 >> 2;
       uint32_t it = 0;
+      // the results land at random positions: their lines are kept in L2
+      // (evict_last) when the whole result fits, so the 4-byte writes merge
+      uint64_t keep;
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+      GS_TRACE_INIT();
       for (uint32_t t = t0; t < t1; ++t, ++it) {
         const uint32_t s = it % NS, a = it % kGsNA;
         gs_wait(&full_raw[s], (it / NS) & 1);
-        const unsigned char* st = smem + s * L::kStage;
-        const uint32_t orig = reinterpret_cast<const uint32_t*>(st + L::kOrigOff)[row];
-        float wv[32];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          if (c < n4) {
-            const uint32_t off = (uint32_t)row * kGsRow + (((uint32_t)c ^ swz) << 4);
-            float4 x = *reinterpret_cast<const float4*>(st + kGsTileBytes + off);
-            if (DIAG) {
-              const float4 y = *reinterpret_cast<const float4*>(st + 2 * kGsTileBytes + off);
-              x.x *= y.x;
-              x.y *= y.y;
-              x.z *= y.z;
-              x.w *= y.w;
-            }
-            wv[4 * c] = x.x;
-            wv[4 * c + 1] = x.y;
-            wv[4 * c + 2] = x.z;
-            wv[4 * c + 3] = x.w;
-          }
-        }
+        GS_TRACE(1, it, 0);
+        const uint32_t st = sbase + s * L::kStage;
+        uint32_t orig;
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(orig) : "r"(st + (uint32_t)L::kOrigOff + 4u * (uint32_t)row) : "memory");
+        const uint32_t srow = st + kGsTileBytes + (uint32_t)row * CSB;
         gs_wait(&acc_full[a], (it / kGsNA) & 1);
+        GS_TRACE(1, it, 1);
+        if (q == 0) GS_STAMP(it, 8);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        uint32_t v[32];
-        TMEM_LD32_GS(tmem + ((uint32_t)(q * 32) << 16) + a * 32, v);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        gs_arrive(&acc_empty[a]);
+        // D = (A Bhi + Alo Bhi)[0:32] + (A Blo)[32:64]: 16 columns of each half at a time
+        const uint32_t tacc = tmem + ((uint32_t)(q * 32) << 16) + a * 64;
         float acc0 = 0.f, acc1 = 0.f;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          if (c < n4) {
-            acc0 = fmaf(__uint_as_float(v[4 * c]), wv[4 * c], acc0);
-            acc1 = fmaf(__uint_as_float(v[4 * c + 1]), wv[4 * c + 1], acc1);
-            acc0 = fmaf(__uint_as_float(v[4 * c + 2]), wv[4 * c + 2], acc0);
-            acc1 = fmaf(__uint_as_float(v[4 * c + 3]), wv[4 * c + 3], acc1);
+        for (int h = 0; h < 2; ++h) {
+          if (4 * h < n4) {
+            uint32_t vh[16], vl[16];
+            TMEM_LD16_GS(tacc + 16 * h, vh);
+            TMEM_LD16_GS(tacc + 32 + 16 * h, vl);
+            float wv[16];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              if (4 * h + c < n4) {
+                const uint32_t off = (CSB == 128 ? ((uint32_t)(4 * h + c) ^ swz) : (uint32_t)(4 * h + c)) << 4;
+                float4 x = lds128(srow + off);
+                if (DIAG) {
+                  const float4 y = lds128(srow + L::kClose + off);
+                  x.x *= y.x;
+                  x.y *= y.y;
+                  x.z *= y.z;
+                  x.w *= y.w;
+                }
+                wv[4 * c] = x.x;
+                wv[4 * c + 1] = x.y;
+                wv[4 * c + 2] = x.z;
+                wv[4 * c + 3] = x.w;
+              }
+            }
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int c = 0; c < 16; c += 2) {
+              if (16 * h + c < r1) {
+                acc0 = fmaf(__uint_as_float(vh[c]) + __uint_as_float(vl[c]), wv[c], acc0);
+                acc1 = fmaf(__uint_as_float(vh[c + 1]) + __uint_as_float(vl[c + 1]), wv[c + 1], acc1);
+              }
+            }
           }
         }
-        if (orig != 0xffffffffu) ga.out[orig] = acc0 + acc1;
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        gs_arrive(&acc_empty[a]);
+#ifdef TNB_GS_OUTSEQ  // timing experiment: contiguous instead of scattered result writes (wrong results)
+        if (orig != 0xffffffffu) ga.out[(size_t)(blockIdx.x * 886 + it) * 128 % ga.m + row] = acc0 + acc1;
+#elif defined(TNB_GS_NOOUT)
+        if (orig == 0xfffffffeu) ga.out[orig] = acc0 + acc1;
+#else
+        if (orig != 0xffffffffu) {
+          if (ga.keep_out)
+            asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(ga.out + orig), "f"(acc0 + acc1), "l"(keep) : "memory");
+          else
+            ga.out[orig] = acc0 + acc1;
+        }
+#endif
         gs_arrive(&empty[s]);
+        GS_TRACE(1, it, 2);
+        if (q == 0) GS_STAMP(it, 9);
       }
-    } else if (warp >= 8 && warp < 12) {
-      // ================= producers: gathers =================
-      const int pw = warp - 8;
-      const int pa = r0 >> 2, ps = r1 >> 2;
+      if (q == 0) GS_TRACE_END(1);
+    } else if (warp >= 12) {
+      // ================= producers: gathers (kGsPW warps x 8 rows of every tile) =================
+      // lanes 8g..8g+7 copy the 16-byte pieces of one row (one 128-byte line
+      // per lane group and table); the warp's 8 rows take 2 passes.
+      const int pw = warp - 12;
+      const int c = lane & 7, rsub = lane >> 3;
+#ifdef TNB_GS_NOS  // timing experiment: no closing-row gathers (wrong results)
+      const bool okA = c < (r0 >> 2), okS = false;
+#else
+      const bool okA = c < (r0 >> 2), okS = c < (r1 >> 2);
+#endif
+      const unsigned char* Pc = reinterpret_cast<const unsigned char*>(ga.P) + 16 * c;
+      const unsigned char* Sc = reinterpret_cast<const unsigned char*>(ga.S) + 16 * c;
+      const unsigned char* Dc = reinterpret_cast<const unsigned char*>(ga.D) + 16 * c;
+      const uint32_t rbA = (uint32_t)r0 * 4, rbS = (uint32_t)r1 * 4;
+      uint32_t offA[2], offS[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const uint32_t r = (uint32_t)(pw * 8 + 4 * i + rsub);
+        offA[i] = r * kGsRow + (((uint32_t)c ^ (r & 7)) << 4);
+        offS[i] = kGsTileBytes + r * CSB + ((CSB == 128 ? ((uint32_t)c ^ (r & 7)) : (uint32_t)c) << 4);
+      }
+      uint64_t stream_pol;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(stream_pol));
+      const int row = pw * 8 + (lane & 7);  // lanes 0-7 hold the warp's records
       GsWalk w;
       w.init(ga.tbase, ga.K, t0);
-      uint32_t it = 0;
-      const int c = lane & 7;
-      const int row = pw * 32 + lane;
-      // the records of the CTA's tiles are one contiguous stream: the next
-      // tile's record is loaded one tile ahead, and the stream is prefetched
-      // into L2 eight tiles ahead
+      uint32_t bs_cur = __ldg(ga.bstart + w.b), bs_next = __ldg(ga.bstart + w.b + 1);
       auto locate = [&](uint32_t t, uint32_t& p0, int& n) {
-        w.advance(t);
-        p0 = __ldg(ga.bstart + w.b) + (t - w.t_cur) * kGsTile;
-        const uint32_t left = __ldg(ga.bstart + w.b + 1) - p0;
+        if (w.advance(t)) {
+          bs_cur = __ldg(ga.bstart + w.b);
+          bs_next = __ldg(ga.bstart + w.b + 1);
+        }
+        p0 = bs_cur + (t - w.t_cur) * kGsTile;
+        const uint32_t left = bs_next - p0;
         n = left < (uint32_t)kGsTile ? (int)left : kGsTile;
       };
-      uint32_t np0;
-      int nn;
-      locate(t0, np0, nn);
-      uint4 nrec = make_uint4(0xffffffffu, 0, 0, 0);
-      if (row < nn) nrec = __ldg(ga.recs + np0 + row);
-      for (uint32_t t = t0; t < t1; ++t, ++it) {
-        const uint4 rec = nrec;
-        const int n = nn;
-        if (t + 1 < t1) {
-          locate(t + 1, np0, nn);
-          nrec = make_uint4(0xffffffffu, 0, 0, 0);
-          if (row < nn) nrec = __ldg(ga.recs + np0 + row);
-          const uint32_t pf = np0 + (uint32_t)row + 8 * kGsTile;
+      // record ring in shared memory (per warp: RR tiles x 8 records), filled
+      // with cp.async RR tiles ahead: one commit group per tile, so
+      // wait_group RR-1 at the top of a tile means its record has landed
+      // (register prefetches of several tiles share a scoreboard: waiting for
+      // the oldest load also waited for the newest).  The CTA's records are
+      // one contiguous stream, prefetched into L2 further ahead.
+      constexpr int RR = L::RR;
+      const uint32_t ring = sbase + L::kRec + (uint32_t)pw * (RR * 128) + (uint32_t)(lane & 7) * 16;
+      auto issue_rec = [&](uint32_t t, uint32_t slot) {
+        uint32_t p0;
+        int n;
+        locate(t, p0, n);
+        if (lane < 8) {
+          const uint32_t dst = ring + slot * 128;
+          if (row < n) {
+            gs_cp16_stream(dst, ga.recs + p0 + row, stream_pol);
+          } else {
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %2, %2};" ::"r"(dst), "r"(0xffffffffu), "r"(0u) : "memory");
+          }
+          const uint32_t pf = p0 + (uint32_t)row + kGsPFL2 * kGsTile;
           if ((lane & 1) == 0 && pf < ga.m) prefetch_l2(ga.recs + pf);
         }
+      };
+#pragma unroll 1
+      for (int j = 0; j < RR; ++j) {
+        if (t0 + j < t1) issue_rec(t0 + j, (uint32_t)j);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      }
+      uint32_t it = 0;
+      GS_TRACE_INIT();
+      for (uint32_t t = t0; t < t1; ++t, ++it) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(RR - 1) : "memory");
+        const uint32_t slot = it % RR;
+        uint4 rec = make_uint4(0xffffffffu, 0, 0, 0);
+        if (lane < 8) {
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(rec.x), "=r"(rec.y), "=r"(rec.z), "=r"(rec.w)
+                       : "r"(ring + slot * 128)
+                       : "memory");
+        }
+        GS_TRACE(2, it, 5);
+        if (pw == 0) GS_STAMP(it, 0);
+        if (t + RR < t1) issue_rec(t + RR, slot);
+        GS_TRACE(2, it, 3);
         const uint32_t s = it % NS;
         gs_wait(&empty[s], ((it / NS) & 1) ^ 1);
-        unsigned char* st = smem + s * L::kStage;
-        reinterpret_cast<uint32_t*>(st + L::kOrigOff)[row] = rec.x;
+        GS_TRACE(2, it, 1);
+        if (pw == 0) GS_STAMP(it, 1);
         const uint32_t sa = sbase + s * L::kStage;
+        if (lane < 8) {
+          asm volatile("st.shared.b32 [%0], %1;" ::"r"(sa + (uint32_t)L::kOrigOff + 4u * (uint32_t)row), "r"(rec.x)
+                       : "memory");
+        }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int src = 4 * i + (lane >> 3);
-          const int r = pw * 32 + src;
+        for (int i = 0; i < 2; ++i) {
+          const int src = 4 * i + rsub;
+          const uint32_t og = __shfl_sync(0xffffffffu, rec.x, src);
           const uint32_t pr = __shfl_sync(0xffffffffu, rec.y, src);
           const uint32_t sr = __shfl_sync(0xffffffffu, rec.z, src);
-          const uint32_t dr = __shfl_sync(0xffffffffu, rec.w, src);
-          const uint32_t off = (uint32_t)r * kGsRow + (((uint32_t)c ^ (uint32_t)(r & 7)) << 4);
-          if (r < n) {
-            if (c < pa) gs_cp16(sa + off, ga.P + (size_t)pr * r0 + 4 * c);
-            if (c < ps) {
-              gs_cp16(sa + kGsTileBytes + off, ga.S + (size_t)sr * r1 + 4 * c);
-              if (DIAG) gs_cp16(sa + 2 * kGsTileBytes + off, ga.D + (size_t)dr * r1 + 4 * c);
+          uint32_t dr = 0;
+          if (DIAG) dr = __shfl_sync(0xffffffffu, rec.w, src);
+          if (og != 0xffffffffu) {
+            if (okA) {
+              if (ga.pfP) gs_cp16_stream(sa + offA[i], Pc + (uint64_t)pr * rbA, stream_pol);
+              else gs_cp16(sa + offA[i], Pc + (uint64_t)pr * rbA);
+            }
+            if (okS) {
+              if (ga.pfS) gs_cp16_stream(sa + offS[i], Sc + (uint64_t)sr * rbS, stream_pol);
+              else gs_cp16(sa + offS[i], Sc + (uint64_t)sr * rbS);
+              if (DIAG) {
+                if (ga.pfD) gs_cp16_stream(sa + offS[i] + L::kClose, Dc + (uint64_t)dr * rbS, stream_pol);
+                else gs_cp16(sa + offS[i] + L::kClose, Dc + (uint64_t)dr * rbS);
+              }
             }
           }
         }
         gs_cp_arrive(&full_raw[s]);
         gs_arrive(&full_raw[s]);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        GS_TRACE(2, it, 2);
+        if (pw == 0) GS_STAMP(it, 2);
       }
-    } else if (warp >= 12) {
+      if (pw == 0) GS_TRACE_END(2);
+    } else if (warp >= 8 && warp < 12) {
       // ================= splitters: x -> tf32 hi (in place), lo =================
-      const int row = (warp - 12) * 32 + lane;
+      const int row = (warp - 8) * 32 + lane;
       const uint32_t swz = (uint32_t)(row & 7);
-      const int npc = ((r0 + 7) >> 3) * 2;
+      const int nph = ((r0 + 7) >> 3) * 2;  // pieces (r0 padded to 8 floats)
+      const int c0 = 0;
+      const uint32_t rowoff = (uint32_t)row * kGsRow;
       uint32_t it = 0;
+      GS_TRACE_INIT();
       for (uint32_t t = t0; t < t1; ++t, ++it) {
         const uint32_t s = it % NS;
         gs_wait(&full_raw[s], (it / NS) & 1);
+        GS_TRACE(3, it, 0);
+        if (warp == 8) GS_STAMP(it, 3);
         gs_wait(&alo_empty[it & 1], ((it >> 1) & 1) ^ 1);
-        unsigned char* A = smem + s * L::kStage;
-        unsigned char* Alo = smem + L::kAlo + (it & 1) * kGsTileBytes;
+        GS_TRACE(3, it, 1);
+        const uint32_t A = sbase + s * L::kStage + rowoff;
+        const uint32_t Alo = sbase + L::kAlo + (it & 1) * kGsTileBytes + rowoff;
+        float4 x[8];  // all loads first: the in-place stores alias them
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          if (c < nph) x[c] = lds128(A + (((uint32_t)(c0 + c) ^ swz) << 4));
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          if (c < npc) {
-            const uint32_t off = (uint32_t)row * kGsRow + (((uint32_t)c ^ swz) << 4);
-            const float4 x = *reinterpret_cast<const float4*>(A + off);
-            uint4 hi, lo;
-            uint32_t h, l;
-            split_tf32_fast(x.x, h, l); hi.x = h; lo.x = l;
-            split_tf32_fast(x.y, h, l); hi.y = h; lo.y = l;
-            split_tf32_fast(x.z, h, l); hi.z = h; lo.z = l;
-            split_tf32_fast(x.w, h, l); hi.w = h; lo.w = l;
-            *reinterpret_cast<uint4*>(A + off) = hi;
-            *reinterpret_cast<uint4*>(Alo + off) = lo;
+          if (c < nph) {
+            const uint32_t off = ((uint32_t)(c0 + c) ^ swz) << 4;
+            // hi = x rounded to tf32 (nearest, ties away: add half an ulp of the
+            // 10-bit mantissa to the magnitude and truncate -- what cvt.rna does,
+            // on the full-rate integer pipe instead of the conversion pipe);
+            // lo = x - hi exact, truncated to tf32 by the tensor core
+            uint32_t h0, h1, h2, h3, l0, l1, l2, l3;
+            h0 = (__float_as_uint(x[c].x) + 0x1000u) & 0xffffe000u;
+            h1 = (__float_as_uint(x[c].y) + 0x1000u) & 0xffffe000u;
+            h2 = (__float_as_uint(x[c].z) + 0x1000u) & 0xffffe000u;
+            h3 = (__float_as_uint(x[c].w) + 0x1000u) & 0xffffe000u;
+            l0 = __float_as_uint(x[c].x - __uint_as_float(h0));
+            l1 = __float_as_uint(x[c].y - __uint_as_float(h1));
+            l2 = __float_as_uint(x[c].z - __uint_as_float(h2));
+            l3 = __float_as_uint(x[c].w - __uint_as_float(h3));
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(A + off), "r"(h0), "r"(h1), "r"(h2), "r"(h3)
+                         : "memory");
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(Alo + off), "r"(l0), "r"(l1), "r"(l2), "r"(l3)
+                         : "memory");
           }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         gs_arrive(&a_ready[s]);
+        GS_TRACE(3, it, 2);
+        if (warp == 8) GS_STAMP(it, 5);
       }
+      if (warp == 8) GS_TRACE_END(3);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)(kGsNA * 32)));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)(kGsNA * 64)));
   }
 }
 
@@ -1026,19 +1243,47 @@ int launch_entries_gsort(const ChainDev& ch, const int64_t* idx, int64_t m, floa
   ga.tbase = tbase;
   ga.K = K;
   ga.m = (uint32_t)m;
+  {  // L2 policies: big tables stream, a result that fits stays
+    const int64_t big = (int64_t)16 << 20;
+    const int gl = mp.ng - 1;
+    ga.pfP = (int64_t)v.m[0].J * G.r0 * 4 > big;
+    ga.pfS = (int64_t)v.m[gl].J * G.r1 * 4 > big;
+    ga.pfD = G.gdiag >= 0 && (int64_t)v.m[G.gdiag].J * G.r1 * 4 > big;
+    ga.keep_out = m * 4 <= ((int64_t)64 << 20);
+  }
   ga.r0 = G.r0;
   ga.r1 = G.r1;
   ga.out = out;
   const bool diag = G.gdiag >= 0;
-  const size_t smem = 1024 + (diag ? GsSmem<true>::kBytes : GsSmem<false>::kBytes);
-  auto kfn = diag ? entries_gsort_kernel<true> : entries_gsort_kernel<false>;
+  const bool compact = diag && G.r1 <= 24;  // 96-byte closing rows: a fourth stage
+  const size_t smem = 1024 + (compact ? GsSmem<true, 96>::kBytes
+                                      : (diag ? GsSmem<true, 128>::kBytes : GsSmem<false, 128>::kBytes));
+  auto kfn = compact ? entries_gsort_kernel<true, 96>
+                     : (diag ? entries_gsort_kernel<true, 128> : entries_gsort_kernel<false, 128>);
   rc = check_cuda(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "gsort smem attr");
   if (rc) return rc;
   const int64_t tiles_max = ceil_div(m, kGsTile) + (int64_t)K;
   const int grid = (int)std::min<int64_t>(tiles_max, num_sms());
+#ifdef TNB_GS_TRACE
+  static unsigned long long* tr = nullptr;
+  if (!tr) cudaMalloc(&tr, 16384 * 8);
+  cudaMemsetAsync(tr, 0, 16384 * 8, st);
+  ga.trace = tr;
+#endif
   {
     KTimer kt("entries_compute", st);
     kfn<<<grid, kGsThreads, smem, st>>>(ga);
   }
+#ifdef TNB_GS_TRACE
+  if (const char* tp = getenv("TNB_GS_TRACE_FILE")) {
+    static unsigned long long host[16384];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(host, tr, sizeof(host), cudaMemcpyDeviceToHost);
+    if (FILE* f = fopen(tp, "wb")) {
+      fwrite(host, 1, sizeof(host), f);
+      fclose(f);
+    }
+  }
+#endif
   return check_launch("entries_gsort");
 }
