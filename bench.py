@@ -394,13 +394,15 @@ def bench_entries(args, cfg, dev, dist, ws, rank, gate_rows=None):
 
     with ClockSampler(dev.index) as clk:
         ms = timed_steps(step, args.steps, args.warmup, stream, dist, kernel_timing=True)
-    kt = {k: N.timing_read(k) for k in ("entries_prep", "entries_sort", "entries_compute", "entries_tables")}
+    kt = {k: N.timing_read(k) for k in ("entries_prep", "entries_sort", "entries_compute", "entries_tables",
+                                        "entries_mid")}
     N.timing_enable(False)
     assert int(err.item()) >= t.ndim, "bench inputs must be in bounds"
     ms_step = ms / args.steps
     value = total / (ms_step * 1e-3)
-    kname = {0: "entries_compute_kernel", 1: "entries_stream_kernel", 2: "two_table_kernel"}.get(
-        plan["compute_kernel"], "entries_compute_kernel")
+    gsort = plan["compute_kernel"] == 3
+    kname = {0: "entries_compute_kernel", 1: "entries_stream_kernel", 2: "two_table_kernel",
+             3: "entries_gsort_kernel"}.get(plan["compute_kernel"], "entries_compute_kernel")
     kms, kn = kt["entries_compute"]
     if kn:  # bucketed: the per-entry compute kernel, timed on its own stream
         k_ms = kms / kn
@@ -416,7 +418,32 @@ def bench_entries(args, cfg, dev, dist, ws, rank, gate_rows=None):
               "peak_source": fsrc,
               "what": "FFMA work the kernel issues outside the tensor-core modes (first-mode copy, diagonal "
                       "modes, the closing dot), per launch"}]
-    if plan["tensor_flops"] > 0:
+    if gsort:
+        # global-sort kernel: per entry one gathered row of the first table,
+        # one of the last (and diag) table, its 16-byte record, a 4-byte result
+        r0 = p.modes[plan["prefix_modes"] - 1].r_right
+        r1 = p.modes[len(p.modes) - plan["suffix_modes"]].r_left
+        per_entry = 4 * r0 + 4 * r1 * (2 if plan["n_virtual"] == 4 else 1) + 16 + 4
+        hb, hsrc = hbm_peak()
+        gb = load_json("gather_bench_r02.json") or {}
+        pipes.append({"bound": "hbm", "work": float(per_entry) * m, "unit": "GB/s", "peak": hb, "peak_source": hsrc,
+                      "what": (f"gathered bytes the kernel requests per launch ({per_entry} B per entry: table rows, "
+                               "record, result); the measured ceiling of random 128-byte row gathers from HBM is "
+                               f"{gb.get('hbm_random_row_gather_gbs', 5320)} GB/s (tools/gather_bench.cu, "
+                               "profiles/gather_bench_r02.json)")})
+        bf = None
+        mp_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+        if os.path.exists(mp_path):
+            with open(mp_path) as f:
+                bf = json.load(f).get("bf16_tflops")
+        pipes.append({"bound": "tensor", "work": plan["tensor_flops"], "unit": "TFLOP/s",
+                      "peak": (bf or 2250.0) / 2.0,
+                      "peak_source": ("half the measured dense bf16 cuBLAS rate (MEASURED_PEAKS.json bf16_tflops): "
+                                      "tcgen05 kind::tf32 runs at half the bf16 rate" if bf else
+                                      "nominal dense tf32 (half of 2.25 PFLOP/s bf16)"),
+                      "what": "3xTF32 tcgen05.mma work of the merged sorted mode (2 MMAs per k-step: Ahi x [Bhi|Blo], "
+                              "Alo x Bhi; 3 * 2*r0*r1 flop per entry), per launch"})
+    elif plan["tensor_flops"] > 0:
         pipes.append({"bound": "tensor", "work": plan["tensor_flops"], "unit": "TFLOP/s", "peak": TC_TF32_PEAK,
                       "peak_source": "measured (profiles/peaks_r01.json, tools/peaks.cu mma.sync m16n8k8 tf32)",
                       "what": "split-TF32 mma.sync work of the sorted modes (3 MMAs per product, 2*r_l*r_r "
@@ -432,8 +459,9 @@ def bench_entries(args, cfg, dev, dist, ws, rank, gate_rows=None):
         "plan": {k: plan[k] for k in ("algo", "n_virtual", "prefix_modes", "suffix_modes", "prefix_rows",
                                       "suffix_rows", "diag_tables", "table_flops", "compute_kernel", "tile")},
         "other_kernels_ms": {k: (v[0] / v[1] if v[1] else None) for k, v in kt.items() if k != "entries_compute"},
-        "other_kernels_note": ("entries_tables runs on a side stream concurrently with entries_prep / "
-                               "entries_sort (joined before the compute kernel): its span overlaps theirs"),
+        "other_kernels_note": ("entries_tables (and entries_mid, the merged sorted mode's slice images) run on a side "
+                               "stream concurrently with entries_prep / entries_sort (joined before the compute "
+                               "kernel): their span overlaps those"),
         "algorithmic_bytes": {"per_entry": 8 * len(shape) + 4, "what": "int64 index row + fp32 output",
                               "step_gbs": (8 * len(shape) + 4) * m / (ms_step * 1e-3) / 1e9},
     }
@@ -441,8 +469,11 @@ def bench_entries(args, cfg, dev, dist, ws, rank, gate_rows=None):
     # event-timed launches (prep, sort, compute) + per step the table builds,
     # detect_hot_kernel and the second (HOT) compute instantiation that
     # returns at once when the flag does not match (the timer brackets both)
-    launches = sum(n for k_, (_, n) in kt.items() if k_ != "entries_tables") + (
-        args.steps * (plan["table_launches"] + (2 if plan["compute_kernel"] in (0, 1) else 0)) if kn else 0)
+    if gsort:  # prep, detect_hot, scan, scatter, compute + the table / slice-image builds
+        launches = args.steps * (5 + plan["table_launches"])
+    else:
+        launches = sum(n for k_, (_, n) in kt.items() if k_ not in ("entries_tables", "entries_mid")) + (
+            args.steps * (plan["table_launches"] + (2 if plan["compute_kernel"] in (0, 1) else 0)) if kn else 0)
     fields = {"value": value, "ms_per_step": ms_step, "roofline": roof, "clocks": clk.summary(),
               "gpu_launches": launches, "shard": [lo, hi]}
     if dist:

@@ -108,9 +108,11 @@ struct GsPrep {
   int8_t grp[kMaxModes];  // 0 first, 1 sorted (mid), 2 diag, 3 last
 };
 
+// TNB_ENTRIES_GSORT: 0 = AUTO never picks this path, 2 = AUTO picks it for
+// every chain it supports, default = when it merges at least two interior modes
 int gsort_env() {
   const char* e = getenv("TNB_ENTRIES_GSORT");
-  return (e && e[0] == '0') ? 0 : 1;
+  return (e && e[0] == '0') ? 0 : ((e && e[0] == '2') ? 2 : 1);
 }
 
 bool plan_gsort(const ChainDev& ch, int64_t m, GPlan* G) {
@@ -173,7 +175,7 @@ bool plan_gsort(const ChainDev& ch, int64_t m, GPlan* G) {
     G->lvl_off[o] = take(rows * ch.m[o].rr * 4);
   }
   G->img_off = take(K * kGsImgBytes);
-  G->hist_off = take(K * 4);
+  G->hist_off = take(K * 4 + 16);  // + 3 hot-row counters (gs_detect_hot_kernel)
   G->bstart_off = take((K + 1) * 4);
   G->tbase_off = take((K + 1) * 4);
   G->cursor_off = take(K * 4);
@@ -492,6 +494,33 @@ __global__ void __launch_bounds__(256) gs_scatter_big_kernel(const uint4* __rest
   }
 }
 
+// Repeated table rows (slice queries: every sample shares its leading or
+// trailing indices): all SMs would gather ONE L2 line, and 2^24 copies of it
+// serialise on its slice (cfg2 compute 0.84 -> 3.7 ms).  Each of kGsHotBlocks
+// warps looks at 32 consecutive records: a majority equal to the first one,
+// per table, counts a vote; the compute kernel copies a table's rows through
+// L1 (cp.async.ca) when most warps voted.
+constexpr int kGsHotBlocks = 64;
+__global__ void gs_detect_hot_kernel(const uint4* __restrict__ recu, int64_t m, uint32_t* __restrict__ hot) {
+  const int lane = threadIdx.x & 31;
+  const int64_t base = (m / kGsHotBlocks) * blockIdx.x;
+  const int64_t s = base + lane;
+  uint4 r = make_uint4(0, 0, 0, 0);
+  const bool ok = s < m;
+  if (ok) r = __ldg(recu + s);
+  const uint32_t y0 = __shfl_sync(0xffffffffu, r.y, 0), z0 = __shfl_sync(0xffffffffu, r.z, 0),
+                 w0 = __shfl_sync(0xffffffffu, r.w, 0);
+  const int n = __popc(__ballot_sync(0xffffffffu, ok));
+  const int ny = __popc(__ballot_sync(0xffffffffu, ok && r.y == y0));
+  const int nz = __popc(__ballot_sync(0xffffffffu, ok && r.z == z0));
+  const int nw = __popc(__ballot_sync(0xffffffffu, ok && r.w == w0));
+  if (lane == 0 && n >= 8) {
+    if (2 * ny > n) atomicAdd(hot + 0, 1u);
+    if (2 * nz > n) atomicAdd(hot + 1, 1u);
+    if (2 * nw > n) atomicAdd(hot + 2, 1u);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // compute kernel
 struct GsArgs {
@@ -506,6 +535,7 @@ struct GsArgs {
   int32_t r0, r1;
   int32_t pfP, pfS, pfD;      // tables too large for L2: their rows are streamed (evict_first)
   int32_t keep_out;           // the result fits in L2: keep its lines there (evict_last)
+  const uint32_t* hot;        // [3] gs_detect_hot_kernel votes: first / last / diag rows repeat
   float* out;
 #ifdef TNB_GS_TRACE
   unsigned long long* trace;  // [block][4 roles][6 phases] clock64 cycles
@@ -553,6 +583,15 @@ __device__ __forceinline__ void gs_cp16(uint32_t dst, const void* src) {
 // merge into whole sectors while they stay in L2
 __device__ __forceinline__ void gs_cp16_stream(uint32_t dst, const void* src, uint64_t pol) {
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void gs_cp16_l1(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+// mode 0: through L2 only; 1: streamed (evict_first); 2: through L1 (repeated rows)
+__device__ __forceinline__ void gs_cp16_mode(uint32_t dst, const void* src, int mode, uint64_t pol) {
+  if (mode == 2) gs_cp16_l1(dst, src);
+  else if (mode == 1) gs_cp16_stream(dst, src, pol);
+  else gs_cp16(dst, src);
 }
 __device__ __forceinline__ uint64_t gs_desc(uint32_t saddr) {  // K-major SWIZZLE_128B, SBO 1024
   uint64_t d = 0;
@@ -902,6 +941,9 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
       }
       uint64_t stream_pol;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(stream_pol));
+      const int modeP = 2 * __ldg(ga.hot + 0) > kGsHotBlocks ? 2 : (ga.pfP ? 1 : 0);
+      const int modeS = 2 * __ldg(ga.hot + 1) > kGsHotBlocks ? 2 : (ga.pfS ? 1 : 0);
+      const int modeD = DIAG && 2 * __ldg(ga.hot + 2) > kGsHotBlocks ? 2 : (ga.pfD ? 1 : 0);
       const int row = pw * 8 + (lane & 7);  // lanes 0-7 hold the warp's records
       GsWalk w;
       w.init(ga.tbase, ga.K, t0);
@@ -977,17 +1019,10 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
           uint32_t dr = 0;
           if (DIAG) dr = __shfl_sync(0xffffffffu, rec.w, src);
           if (og != 0xffffffffu) {
-            if (okA) {
-              if (ga.pfP) gs_cp16_stream(sa + offA[i], Pc + (uint64_t)pr * rbA, stream_pol);
-              else gs_cp16(sa + offA[i], Pc + (uint64_t)pr * rbA);
-            }
+            if (okA) gs_cp16_mode(sa + offA[i], Pc + (uint64_t)pr * rbA, modeP, stream_pol);
             if (okS) {
-              if (ga.pfS) gs_cp16_stream(sa + offS[i], Sc + (uint64_t)sr * rbS, stream_pol);
-              else gs_cp16(sa + offS[i], Sc + (uint64_t)sr * rbS);
-              if (DIAG) {
-                if (ga.pfD) gs_cp16_stream(sa + offS[i] + L::kClose, Dc + (uint64_t)dr * rbS, stream_pol);
-                else gs_cp16(sa + offS[i] + L::kClose, Dc + (uint64_t)dr * rbS);
-              }
+              gs_cp16_mode(sa + offS[i], Sc + (uint64_t)sr * rbS, modeS, stream_pol);
+              if (DIAG) gs_cp16_mode(sa + offS[i] + L::kClose, Dc + (uint64_t)dr * rbS, modeD, stream_pol);
             }
           }
         }
@@ -1083,16 +1118,18 @@ bool gsort_ok(const ChainDev& ch, int64_t m) {
   return true;
 }
 
-int64_t gsort_buckets(const ChainDev& ch, int64_t m);
-// AUTO: large calls whose buckets average at least 512 samples (4 tiles)
+// AUTO: large calls whose buckets average at least 512 samples (4 tiles) and
+// whose sorted mode is a product of at least two interior modes -- the global
+// sort then removes a whole r x r step per entry.  With a single interior
+// mode (cfg5: P012 . G3 . D45 . S67) the stream kernel's per-tile sort is
+// cheaper than the global one (4.6 vs 5.7 ms at 2^26 tuples).
 bool gsort_auto(const ChainDev& ch, int64_t m) {
-  if (!gsort_env() || m < (1 << 18) || !gsort_ok(ch, m)) return false;
-  return gsort_buckets(ch, m) * 512 <= m;
-}
-
-int64_t gsort_buckets(const ChainDev& ch, int64_t m) {
+  const int env = gsort_env();
+  if (!env || m < (1 << 18) || !gsort_ok(ch, m)) return false;
   static thread_local GPlan G;
-  return plan_gsort(ch, m, &G) ? G.K : 0;
+  plan_gsort(ch, m, &G);
+  if (G.K * 512 > m) return false;
+  return env == 2 || G.omid_hi - G.omid_lo >= 2;
 }
 
 int64_t gsort_workspace(const ChainDev& ch, int64_t m) {
@@ -1187,7 +1224,7 @@ int launch_entries_gsort(const ChainDev& ch, const int64_t* idx, int64_t m, floa
   uint4* recu = reinterpret_cast<uint4*>(base + G.recu_off);
   uint4* recs = reinterpret_cast<uint4*>(base + G.recs_off);
   const uint32_t K = (uint32_t)G.K;
-  rc = check_cuda(cudaMemsetAsync(hist, 0, (size_t)K * 4, st), "gsort hist");
+  rc = check_cuda(cudaMemsetAsync(hist, 0, (size_t)K * 4 + 16, st), "gsort hist");
   if (rc) return fail(rc);
   {
     static thread_local GsPrep gp;
@@ -1207,6 +1244,9 @@ int launch_entries_gsort(const ChainDev& ch, const int64_t* idx, int64_t m, floa
     pk<<<(unsigned)g, kGsPrepThreads, sm, st>>>(gp, idx, m, err, recu, hist);
   }
   rc = check_launch("gsort prep");
+  if (rc) return fail(rc);
+  gs_detect_hot_kernel<<<kGsHotBlocks, 32, 0, st>>>(recu, m, hist + K);
+  rc = check_launch("gsort detect hot");
   if (rc) return fail(rc);
   {
     KTimer kt("entries_sort", st);
@@ -1242,6 +1282,7 @@ int launch_entries_gsort(const ChainDev& ch, const int64_t* idx, int64_t m, floa
   ga.bstart = bstart;
   ga.tbase = tbase;
   ga.K = K;
+  ga.hot = hist + K;
   ga.m = (uint32_t)m;
   {  // L2 policies: big tables stream, a result that fits stays
     const int64_t big = (int64_t)16 << 20;

@@ -171,10 +171,30 @@ def test_entries_plan_merges_cfg2_and_cfg5(lib, monkeypatch):
     from paper_2206_11128_b200 import _native as N
 
     monkeypatch.delenv("TNB_ENTRIES_MERGE", raising=False)
-    # cfg2: 10 x TT, J=32, r=32, m=2^24 -> wide (HBM) prefix 0-3 and suffix
-    # 6-9 tables of 2^20 rows: two sorted modes remain
+    monkeypatch.delenv("TNB_ENTRIES_GSORT", raising=False)
     r = 32
     specs = [(0, 32, 1, r)] + [(0, 32, r, r)] * 8 + [(0, 32, r, 1)]
+    # cfg2 at 2^24 tuples, AUTO: the global-sort tcgen05 path -- prefix 0-3
+    # and suffix 6-9 tables, modes 4-5 merged into ONE sorted mode of 1024
+    # slices: one r x r product (3 tf32 MMAs) + the closing dot per entry
+    g = N.entries_plan(_chain(specs), 1 << 24)
+    assert (g["algo"], g["compute_kernel"], g["tile"], g["n_virtual"]) == (N.ALGO_GSORT, 3, 128, 3), g
+    assert (g["prefix_modes"], g["suffix_modes"]) == (4, 4) and g["prefix_rows"] == g["suffix_rows"] == 32 ** 4
+    assert g["kernel_flops"] == (2 * r * r + 2 * r) * float(1 << 24)
+    assert g["tensor_flops"] == 3 * 2 * r * r * float(1 << 24)
+    # tables P0123, S6789 and the merged level G4 G5 (32 * 32 rows of G4 against the 32 slices of G5)
+    assert g["table_flops"] == 2 * (32 ** 2 + 32 ** 3 + 32 ** 4) * r * 2 * r + (32 * r) * 32 * r * 2 * r
+    # below 2^23 tuples the tables stop at 2^15 rows and four interior modes
+    # (2^20 slices) do not merge: the bucketed kernels
+    assert N.entries_plan(_chain(specs), 1 << 22)["algo"] == N.ALGO_BUCKETED
+    # the explicit algorithm needs a supported chain (rank multiples of 4)
+    odd = [(0, 32, 1, 5), (0, 32, 5, 5), (0, 32, 5, 5), (0, 32, 5, 1)]
+    with pytest.raises(Exception):
+        N.entries_plan(_chain(odd), 1 << 20, N.ALGO_GSORT)
+    # TNB_ENTRIES_GSORT=0: the bucketed kernels, as before the global sort
+    monkeypatch.setenv("TNB_ENTRIES_GSORT", "0")
+    # cfg2: 10 x TT, J=32, r=32, m=2^24 -> wide (HBM) prefix 0-3 and suffix
+    # 6-9 tables of 2^20 rows: two sorted modes remain
     info = N.entries_plan(_chain(specs), 1 << 24)
     assert info["algo"] == N.ALGO_BUCKETED
     assert (info["prefix_modes"], info["suffix_modes"], info["n_virtual"]) == (4, 4, 4)
@@ -189,8 +209,15 @@ def test_entries_plan_merges_cfg2_and_cfg5(lib, monkeypatch):
     assert info["kernel_flops"] == (4 * 2 * r * r + 2 * r) * float(1 << 24)
     assert info["table_flops"] == 2 * (32 ** 2 * r * 2 * r + 32 ** 3 * r * 2 * r)
     monkeypatch.delenv("TNB_MERGE_WIDE")
-    # cfg5: TT 0-3 (r=24), CP 4-7 (diag interior, dense right end), J=128
+    # cfg5: TT 0-3 (r=24), CP 4-7 (diag interior, dense right end), J=128;
+    # a single interior mode is left after merging, so AUTO keeps the stream
+    # kernel with or without the global-sort path
     specs5 = [(0, 128, 1, 24)] + [(0, 128, 24, 24)] * 3 + [(1, 128, 24, 24)] * 3 + [(0, 128, 24, 1)]
+    monkeypatch.delenv("TNB_ENTRIES_GSORT")
+    assert N.entries_plan(_chain(specs5), 1 << 26)["compute_kernel"] == 1
+    g5 = N.entries_plan(_chain(specs5), 1 << 26, N.ALGO_GSORT)
+    assert (g5["compute_kernel"], g5["n_virtual"], g5["diag_tables"], g5["prefix_rows"]) == (3, 4, 1, 128 ** 3), g5
+    monkeypatch.setenv("TNB_ENTRIES_GSORT", "0")
     info5 = N.entries_plan(_chain(specs5), 1 << 26)
     # wide prefix 0-2 (2^21 rows), CP suffix 6-7 (16384 rows), CP 4-5 as one
     # diagonal product table: virtual chain P012, G3, D45, S67

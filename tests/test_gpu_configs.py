@@ -40,10 +40,15 @@ def test_cfg1_everything():
     assert_close(np.asarray(tb.norm(t)), np.asarray(O.norm(o)), what="cfg1 norm")
 
 
-def test_cfg2_subset():
+@pytest.mark.parametrize("gsort", ["1", "0"])
+def test_cfg2_subset(gsort, monkeypatch):
+    # AUTO at the benchmarked size: the global-sort tcgen05 path (default) and
+    # the bucketed state kernel (TNB_ENTRIES_GSORT=0)
+    monkeypatch.setenv("TNB_ENTRIES_GSORT", gsort)
     cores = O.random_tt((32,) * 10, 32, seed=0, scale=32 ** -0.5)
     t, o = tt(cores)
     m = 1 << 24
+    assert N.entries_plan(t._packed().chain, m, N.ALGO_AUTO)["compute_kernel"] == (3 if gsort == "1" else 0)
     idx = torch.from_numpy(O.uniform_indices((32,) * 10, m, 2)).cuda()
     got = tb.entries(t, idx)
     assert tuple(got.shape) == (m,)
@@ -133,11 +138,19 @@ def test_cfg5_benchmarked_plan():
     assert_close(g, O.entries(o, sub), what="cfg5 at 2^26")
 
 
-def test_cfg2_benchmarked_plan():
+def test_cfg2_benchmarked_plan(monkeypatch):
     # the plan behind the cfg2 headline: P0123 / S6789 HBM tables (2^20 rows
-    # each), two tensor-core sorted modes on the state kernel
+    # each), modes 4-5 merged into one sorted mode of 1024 slices, one global
+    # sort, tcgen05 tiles (test_cfg2_subset checks its values at 2^24 tuples)
+    monkeypatch.delenv("TNB_ENTRIES_GSORT", raising=False)
     cores = O.random_tt((32,) * 10, 32, seed=0, scale=32 ** -0.5)
     t, _ = tt(cores)
+    plan = N.entries_plan(t._packed().chain, 1 << 24, N.ALGO_AUTO)
+    assert (plan["algo"], plan["n_virtual"], plan["prefix_rows"], plan["suffix_rows"], plan["compute_kernel"]) == \
+        (N.ALGO_GSORT, 3, 1 << 20, 1 << 20, 3), plan
+    assert plan["tensor_flops"] == 3 * 2 * 32 * 32 * float(1 << 24)
+    # without the global sort: two tensor-core sorted modes on the state kernel
+    monkeypatch.setenv("TNB_ENTRIES_GSORT", "0")
     plan = N.entries_plan(t._packed().chain, 1 << 24, N.ALGO_AUTO)
     assert (plan["n_virtual"], plan["prefix_rows"], plan["suffix_rows"], plan["compute_kernel"]) == \
         (4, 1 << 20, 1 << 20, 0), plan

@@ -30,6 +30,13 @@ def _cuda():
         pytest.skip("no CUDA device")
 
 
+@pytest.fixture(autouse=True)
+def _bucketed_auto(monkeypatch):
+    # this module pins the bucketed / generic kernels: AUTO must not route
+    # large calls to the global-sort path (tests/test_gpu_gsort.py covers it)
+    monkeypatch.setenv("TNB_ENTRIES_GSORT", "0")
+
+
 class Guarded:
     """nbytes usable device bytes at a 256-byte aligned offset inside a
     buffer whose PAD-byte margins hold SENT."""
@@ -85,6 +92,22 @@ def test_guard_stream_kernel(m):
     t = tb.TnTensor([tb.ModeNode("tt", c) for c in cores])
     idx = O.uniform_indices(t.shape, m, 10)
     got = _entries_guarded(t, idx)
+    sel = np.arange(0, m, max(1, m // 3000))
+    assert_close(got.cpu().numpy()[sel], O.entries(O.make_chain([("tt", c) for c in cores]), idx[sel]))
+
+
+@pytest.mark.parametrize("m", [1, 129, 70001, (1 << 18) + 5])
+def test_guard_gsort_kernels(m, monkeypatch):
+    # global-sort path: prep / scan / scatter / tcgen05 compute with ragged
+    # bucket tails and empty buckets (P01 . G23 . S45 of an 8^6 chain, r = 16)
+    monkeypatch.setenv("TNB_PREFIX_MAX_ROWS", "64")
+    monkeypatch.setenv("TNB_SUFFIX_MAX_ROWS", "64")
+    cores = O.random_tt((8,) * 6, 16, seed=17, scale=0.25)
+    t = tb.TnTensor([tb.ModeNode("tt", c) for c in cores])
+    idx = O.uniform_indices(t.shape, m, 4)
+    idx[::5] -= 8
+    assert N.entries_plan(t._packed().chain, m, N.ALGO_GSORT)["compute_kernel"] == 3
+    got = _entries_guarded(t, idx, N.ALGO_GSORT)
     sel = np.arange(0, m, max(1, m // 3000))
     assert_close(got.cpu().numpy()[sel], O.entries(O.make_chain([("tt", c) for c in cores]), idx[sel]))
 

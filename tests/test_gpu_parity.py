@@ -23,6 +23,13 @@ def _cuda():
         pytest.skip("no CUDA device")
 
 
+@pytest.fixture(autouse=True)
+def _bucketed_auto(monkeypatch):
+    # this module pins the bucketed / generic kernels: AUTO must not route
+    # large calls to the global-sort path (tests/test_gpu_gsort.py covers it)
+    monkeypatch.setenv("TNB_ENTRIES_GSORT", "0")
+
+
 @pytest.mark.parametrize("name", G.CASE_NAMES)
 def test_golden_full_norm(name):
     c = G.case(name)
