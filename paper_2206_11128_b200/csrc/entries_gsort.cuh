@@ -559,7 +559,7 @@ __device__ __forceinline__ void gs_wait(uint64_t* b, uint32_t parity) {
         : "r"(a), "r"(parity), "r"(1000000u)
         : "memory");
     if (done) return;
-    if (++spins > 4000) __trap();  // ~4 s without progress: a protocol bug, not a slow tile
+    if (++spins > 30000) __trap();  // ~30 s without progress: a protocol bug, not a slow tile
   }
 }
 __device__ __forceinline__ void gs_arrive(uint64_t* b) {

@@ -158,3 +158,18 @@ def test_gsort_rejects_unsupported_chains():
     with pytest.raises(tb.ContractViolationError):
         tb.entries(t, idx, algo=N.ALGO_GSORT)
     assert_close(tb.entries(t, idx), O.entries(o, idx))
+
+
+def test_gsort_is_bitwise_reproducible(monkeypatch):
+    # the scatter's order inside a bucket is not fixed, the values must not depend on it
+    monkeypatch.setenv("TNB_PREFIX_MAX_ROWS", "512")
+    monkeypatch.setenv("TNB_SUFFIX_MAX_ROWS", "512")
+    nodes = [("tt", c, None) for c in O.random_tt((8,) * 8, 32, seed=21, scale=32 ** -0.5)]
+    t = facade(nodes)
+    idx = torch.from_numpy(O.uniform_indices(t.shape, 400000, 7)).cuda()
+    a = tb.entries(t, idx, algo=N.ALGO_GSORT)
+    b = tb.entries(t, idx, algo=N.ALGO_GSORT)
+    perm = torch.randperm(idx.shape[0], device="cuda")
+    c = tb.entries(t, idx[perm], algo=N.ALGO_GSORT)
+    assert torch.equal(a, b)
+    assert torch.equal(a[perm], c)
