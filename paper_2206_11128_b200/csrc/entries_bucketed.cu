@@ -2001,21 +2001,9 @@ __global__ void __launch_bounds__(256) table_gemm_tc(ModeDev md, const float* __
   const int J = md.J;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int64_t i0 = (int64_t)blockIdx.x * kTcRows;
-  const int nr = (int)(rows - i0 < kTcRows ? rows - i0 : kTcRows);
-  for (int e = tid; e < kTcRows * K; e += 256) {
-    const int r = e / K, k = e - r * K;
-    As[r * AS + k] = r < nr ? __ldg(A + i0 * K + e) : 0.f;
-  }
-  __syncthreads();
   const int z0 = blockIdx.y * kTcZ;
   const int j = z0 + warp;
-#if TNB_TABLE_STAGE
   const bool jok = j < J;  // every warp stays for the staging barriers
-#else
-  if (j >= J) return;
-  constexpr bool jok = true;
-#endif
   // B(k, n) = G(j, k, n) (prefix) or G(j, n, k) (suffix); fragment (kt, nt):
   // b0 = B(8kt + t, 8nt + g), b1 = B(8kt + t + 4, 8nt + g)
   const float* gj = md.s + (int64_t)(jok ? j : 0) * md.rl * md.rr;
@@ -2029,8 +2017,26 @@ __global__ void __launch_bounds__(256) table_gemm_tc(ModeDev md, const float* __
         const int k = 8 * kt + t + 4 * e, n = 8 * nt + g;
         split_tf32(jok ? __ldg(gj + (SUFFIX ? n * K + k : k * Nn + n)) : 0.f, bh[kt][nt][e], bl[kt][nt][e]);
       }
+  // the CTA's row chunks (the slice fragments above are loaded once)
+  const bool a16 = (reinterpret_cast<uintptr_t>(A) & 15) == 0;
+  for (int64_t i0 = (int64_t)blockIdx.x * kTcRows; i0 < rows; i0 += (int64_t)gridDim.x * kTcRows) {
+  const int nr = (int)(rows - i0 < kTcRows ? rows - i0 : kTcRows);
+  __syncthreads();  // the previous chunk's fragment loads are done
+  if (a16) {  // K % 4 == 0: 16-byte loads of the chunk's contiguous rows
+    for (int e = tid; e < kTcRows * (K / 4); e += 256) {
+      const int r = e / (K / 4), k4 = e - r * (K / 4);
+      const float4 v = r < nr ? __ldg(reinterpret_cast<const float4*>(A + i0 * K) + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+      *reinterpret_cast<float4*>(As + r * AS + 4 * k4) = v;
+    }
+  } else {
+    for (int e = tid; e < kTcRows * K; e += 256) {
+      const int r = e / K, k = e - r * K;
+      As[r * AS + k] = r < nr ? __ldg(A + i0 * K + e) : 0.f;
+    }
+  }
+  __syncthreads();
   for (int mt = 0; mt < kTcRows / 16; ++mt) {
-    if (mt * 16 >= nr) break;
+    if (mt * 16 >= nr || !jok) break;
     float acc[NTL][4];
 #pragma unroll
     for (int nt = 0; nt < NTL; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
@@ -2093,13 +2099,17 @@ __global__ void __launch_bounds__(256) table_gemm_tc(ModeDev md, const float* __
     }
 #endif
   }
+  }
 }
 
 template <bool SUFFIX>
 bool launch_table_tc(const ModeDev& md, const float* in, int64_t rows, float* out, cudaStream_t st) {
   const int K = SUFFIX ? md.rr : md.rl, Nn = SUFFIX ? md.rl : md.rr;
   if (!TNB_TABLE_TC || md.layout != TNB_LAYOUT_DENSE || K != Nn || (K & 7) || K < 8 || K > 32) return false;
-  const dim3 grid((unsigned)ceil_div(rows, kTcRows), (unsigned)ceil_div(md.J, kTcZ));
+  // ~4 CTAs per SM in all; a CTA walks its row chunks with the slice fragments loaded once
+  const int64_t gy = ceil_div(md.J, kTcZ);
+  const int64_t gx = std::min<int64_t>(ceil_div(rows, kTcRows), std::max<int64_t>(1, ((int64_t)num_sms() * 4) / gy));
+  const dim3 grid((unsigned)gx, (unsigned)gy);
   switch (K) {
     case 8: table_gemm_tc<1, 1, SUFFIX><<<grid, 256, 0, st>>>(md, in, rows, out); break;
     case 16: table_gemm_tc<2, 2, SUFFIX><<<grid, 256, 0, st>>>(md, in, rows, out); break;

@@ -88,14 +88,24 @@ constexpr int kGsPF = TNB_GS_PF;         // record loads in flight per producer 
 constexpr int kGsPFRows = TNB_GS_PFROWS;  // table rows are prefetched into L2 this many tiles ahead (< kGsPF)
 constexpr int kGsPFL2 = TNB_GS_PFL2;     // L2 prefetch distance of the record stream (tiles)
 constexpr int kGsPrepThreads = 512;
-constexpr int kGsScatThreads = 512, kGsScatPer = 8;
+#ifndef TNB_GS_SCAT_T
+#define TNB_GS_SCAT_T 512
+#endif
+#ifndef TNB_GS_SCAT_PER
+#define TNB_GS_SCAT_PER 8
+#endif
+constexpr int kGsScatThreads = TNB_GS_SCAT_T, kGsScatPer = TNB_GS_SCAT_PER;
 
 struct GPlan {
   MergePlan mp;
   int gdiag = -1;          // virtual group of the diagonal table, or -1
   int omid_lo = 0, omid_hi = 0;  // original modes merged into the sorted mode
   int r0 = 0, r1 = 0;      // its slices are r0 x r1
-  int64_t K = 0;           // ... and there are K of them
+  int64_t K = 0;           // sort buckets: Kmid slices x nsub row ranges of the first table
+  int64_t Kmid = 0;        // slices of the merged sorted mode
+  int nsub = 1;            // row ranges of the first table in the sort key (L2 locality)
+  int64_t sub_rows = 0;    // rows per range (0: none)
+  int64_t tinfo_off = 0;   // per-tile {first sorted position, bucket, rows}
   int64_t lvl_off[kMaxModes];  // mid level ending at original mode o (o > omid_lo)
   int64_t img_off = 0, hist_off = 0, bstart_off = 0, tbase_off = 0, cursor_off = 0;
   int64_t recu_off = 0, recs_off = 0, total_bytes = 0;
@@ -104,8 +114,11 @@ struct GPlan {
 struct GsPrep {
   int32_t n0;
   uint32_t K;
+  uint32_t Kmid, sub_rows;  // key = (first row / sub_rows) * Kmid + merged index (sub_rows 0: no row ranges)
   int32_t oJ[kMaxModes];
-  int8_t grp[kMaxModes];  // 0 first, 1 sorted (mid), 2 diag, 3 last
+  // C-order weight of mode o inside its group, in the group's field (first /
+  // sorted / diag / last) and zero in the other three: no branches per mode
+  uint32_t w0[kMaxModes], w1[kMaxModes], w2[kMaxModes], w3[kMaxModes];
 };
 
 // TNB_ENTRIES_GSORT: 0 = AUTO never picks this path, 2 = AUTO picks it for
@@ -160,6 +173,28 @@ bool plan_gsort(const ChainDev& ch, int64_t m, GPlan* G) {
   if (r0 < 4 || r0 > 32 || (r0 & 3) || r1 < 4 || r1 > 32 || (r1 & 3)) return false;
   G->r0 = r0;
   G->r1 = r1;
+  G->Kmid = K;
+  // A first table too large for L2 is gathered one row range at a time: the
+  // range index leads the sort key and the compute kernel's CTAs sweep the
+  // sorted tiles together (interleaved), so at any time the gathers fall into
+  // one range (<= 16 MB, L2-resident: every row is fetched from HBM once per
+  // call instead of once per sample).  Limits: shared-memory histograms
+  // (kGsSmemK buckets) and buckets of >= 512 samples on average.
+  G->nsub = 1;
+  G->sub_rows = 0;
+  {
+    const int64_t rowsP = mp.rows[0];
+    const int64_t bytesP = rowsP * r0 * 4;
+    const char* e = getenv("TNB_GS_SUBRANGES");
+    const int want = e ? atoi(e) : 1;  // measured: no gain at cfg2 (the kernel is issue-bound, not DRAM-bound) and a slower 8192-bucket scatter
+    int ns = 1;
+    while (bytesP / ns > ((int64_t)16 << 20) && ns * 2 <= want && K * ns * 2 <= kGsSmemK && K * ns * 2 * 512 <= m) ns *= 2;
+    if (ns > 1) {
+      G->nsub = ns;
+      G->sub_rows = (rowsP + ns - 1) / ns;
+    }
+  }
+  K *= G->nsub;
   G->K = K;
   // the bucketed kernels' slice copies are not needed here
   for (int v = 0; v < mp.ng; ++v) mp.lm[v] = mp.mma[v] = 0;
@@ -179,6 +214,7 @@ bool plan_gsort(const ChainDev& ch, int64_t m, GPlan* G) {
   G->bstart_off = take((K + 1) * 4);
   G->tbase_off = take((K + 1) * 4);
   G->cursor_off = take(K * 4);
+  G->tinfo_off = take(((m + kGsTile - 1) / kGsTile + K + 1) * 8);
   G->recu_off = take(m * 16);
   G->recs_off = take(m * 16);
   G->total_bytes = off;
@@ -268,16 +304,25 @@ __global__ void __launch_bounds__(kGsPrepThreads) gs_prep_kernel(const __grid_co
     __syncthreads();
   }
   uint32_t f0, f1, f2, f3;
+  int badm;
+  // wrap and check one index on 32-bit halves: valid raw values have a high
+  // word of 0 (then lo < J) or -1 (then lo + J wraps below J); core.py:409-416
   auto put = [&](int o, int64_t raw) {
-    const int32_t J = gp.oJ[o];
-    const uint32_t v = (uint32_t)norm_index(raw, J, o, err);
-    const int g = gp.grp[o];
-    if (g == 0) f0 = f0 * (uint32_t)J + v;
-    else if (g == 1) f1 = f1 * (uint32_t)J + v;
-    else if (g == 2) f2 = f2 * (uint32_t)J + v;
-    else f3 = f3 * (uint32_t)J + v;
+    const uint32_t J = (uint32_t)gp.oJ[o];
+    const uint32_t lo = (uint32_t)raw;
+    const int32_t hi = (int32_t)(raw >> 32);
+    uint32_t v = lo + ((uint32_t)hi & J);
+    const bool bad = v >= J || (uint32_t)(hi + 1) > 1u;
+    badm = (bad && o < badm) ? o : badm;
+    v = bad ? 0u : v;
+    f0 += v * gp.w0[o];
+    f1 += v * gp.w1[o];
+    f2 += v * gp.w2[o];
+    f3 += v * gp.w3[o];
   };
   auto emit = [&](int64_t s) {
+    if (badm < N0) atomicMin(err, badm);
+    if (gp.sub_rows) f1 += (f0 / gp.sub_rows) * gp.Kmid;
     recu[s] = make_uint4(f1, f0, f3, f2);
     if (SH) {
       atomicAdd(&gs_sh[f1], 1u);
@@ -307,6 +352,7 @@ __global__ void __launch_bounds__(kGsPrepThreads) gs_prep_kernel(const __grid_co
       __syncwarp();
       if (lane < rows) {
         f0 = f1 = f2 = f3 = 0;
+        badm = N0;
         const longlong2* row = reinterpret_cast<const longlong2*>(stage + lane * h);
         for (int o = 0; o < h; ++o) {
           const longlong2 w = row[h == 4 ? (o ^ ((lane >> 1) & 3)) : o];
@@ -321,6 +367,7 @@ __global__ void __launch_bounds__(kGsPrepThreads) gs_prep_kernel(const __grid_co
     for (int64_t s = blockIdx.x * (int64_t)kGsPrepThreads + tid; s < m; s += (int64_t)gridDim.x * kGsPrepThreads) {
       const int64_t* row = idx + s * N0;
       f0 = f1 = f2 = f3 = 0;
+      badm = N0;
       for (int o = 0; o < N0; ++o) put(o, __ldg(row + o));
       emit(s);
     }
@@ -392,12 +439,32 @@ __global__ void __launch_bounds__(1024) gs_scan_kernel(const uint32_t* __restric
   }
 }
 
+// tile map: for every 128-sample tile of the sorted order its first position,
+// its bucket and its number of rows (the last tile of a bucket is ragged) --
+// one 8-byte load per tile and role in the compute kernel
+__global__ void __launch_bounds__(256) gs_tilemap_kernel(const uint32_t* __restrict__ bstart,
+                                                        const uint32_t* __restrict__ tbase, uint32_t K,
+                                                        uint2* __restrict__ tinfo) {
+  const uint32_t Nt = __ldg(tbase + K);
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < Nt; t += gridDim.x * blockDim.x) {
+    uint32_t lo = 0, hi = K - 1;  // first b with tbase[b + 1] > t
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (__ldg(tbase + mid + 1) > t) hi = mid;
+      else lo = mid + 1;
+    }
+    const uint32_t p0 = __ldg(bstart + lo) + (t - __ldg(tbase + lo)) * kGsTile;
+    const uint32_t left = __ldg(bstart + lo + 1) - p0;
+    tinfo[t] = make_uint2(p0, (lo << 8) | ((left < (uint32_t)kGsTile ? left : (uint32_t)kGsTile) - 1));
+  }
+}
+
 // scatter: each CTA takes 4096 records, counts its keys in shared memory
 // (the count a sample draws is its rank inside the CTA's share of the bucket),
 // reserves the CTA's range of every bucket with one atomicAdd, sorts the
 // records by key in shared memory and writes {orig, first row, last row, diag
 // row} runs to the sorted positions (a bucket's share is contiguous)
-__global__ void __launch_bounds__(kGsScatThreads) gs_scatter_kernel(const uint4* __restrict__ recu, int64_t m, uint32_t K,
+__global__ void __launch_bounds__(kGsScatThreads, 2048 / kGsScatThreads > 2 ? 2 : 2048 / kGsScatThreads) gs_scatter_kernel(const uint4* __restrict__ recu, int64_t m, uint32_t K,
                                                                      uint32_t* __restrict__ cursor,
                                                                      uint4* __restrict__ recs) {
   extern __shared__ __align__(16) uint32_t gs_sh[];
@@ -529,9 +596,10 @@ struct GsArgs {
   const float* D;             // [rows][r1] or null
   const unsigned char* img;   // [K][8 KB]
   const uint4* recs;          // sorted records
-  const uint32_t* bstart;     // [K + 1]
-  const uint32_t* tbase;      // [K + 1]
-  uint32_t K, m;
+  const uint2* tinfo;         // [tiles] {first sorted position, bucket << 8 | rows - 1}
+  const uint32_t* tbase;      // [K + 1] (tbase[K] = number of tiles)
+  uint32_t K, Kmid, m;
+  int32_t interleave;         // CTAs take runs of kGsRun tiles round-robin instead of one contiguous range
   int32_t r0, r1;
   int32_t pfP, pfS, pfD;      // tables too large for L2: their rows are streamed (evict_first)
   int32_t keep_out;           // the result fits in L2: keep its lines there (evict_last)
@@ -560,6 +628,25 @@ __device__ __forceinline__ void gs_wait(uint64_t* b, uint32_t parity) {
         : "memory");
     if (done) return;
     if (++spins > 30000) __trap();  // ~30 s without progress: a protocol bug, not a slow tile
+  }
+}
+// producers waiting for a free stage are not on the critical path: they
+// sleep between polls instead of taking issue slots from the working warps
+__device__ __forceinline__ void gs_wait_relaxed(uint64_t* b, uint32_t parity) {
+  const uint32_t a = s32(b);
+  uint32_t done;
+  int spins = 0;
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity), "r"(1000000u)
+        : "memory");
+    if (done) return;
+    __nanosleep(128);
+    if (++spins > 100000000) __trap();
   }
 }
 __device__ __forceinline__ void gs_arrive(uint64_t* b) {
@@ -658,34 +745,28 @@ __device__ __forceinline__ void gs_commit_elect(uint64_t* b) {
   } while (0)
 #endif
 
-// position of every role in the CTA's tile range: the bucket of tile t, and
-// how many bucket changes came before it (the slice-image ring slot)
-struct GsWalk {
-  const uint32_t* tb;
-  uint32_t b, t_cur, t_next, nb;
-  __device__ void init(const uint32_t* tbase, uint32_t K, uint32_t t0) {
-    tb = tbase;
-    uint32_t lo = 0, hi = K - 1;  // first b with tbase[b + 1] > t0 (exists: t0 < tbase[K])
-    while (lo < hi) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (__ldg(tb + mid + 1) > t0) hi = mid;
-      else lo = mid + 1;
+// The CTA's tile sequence.  Contiguous: tiles [Nt b / G, Nt (b + 1) / G).
+// Interleaved (row ranges in the sort key): runs of kGsRun consecutive tiles
+// dealt round-robin, so all CTAs work in the same part of the sorted order.
+constexpr uint32_t kGsRun = 4;
+struct GsSeq {
+  uint32_t first, cnt, G, inter;
+  __device__ void init(uint32_t Nt, uint32_t bid, uint32_t grid, int interleave) {
+    G = grid;
+    inter = (uint32_t)interleave;
+    if (!inter) {
+      first = (uint32_t)(((uint64_t)Nt * bid) / grid);
+      cnt = (uint32_t)(((uint64_t)Nt * (bid + 1)) / grid) - first;
+    } else {
+      first = bid;
+      const uint32_t NR = (Nt + kGsRun - 1) / kGsRun;  // runs
+      const uint32_t nr = bid < NR ? (NR - bid + grid - 1) / grid : 0;
+      cnt = nr * kGsRun;
+      if (nr && (NR - 1) % grid == bid) cnt -= NR * kGsRun - Nt;  // the last run is short
     }
-    b = lo;
-    t_cur = __ldg(tb + b);
-    t_next = __ldg(tb + b + 1);
-    nb = 0;
   }
-  __device__ bool advance(uint32_t t) {
-    bool chg = false;
-    while (t >= t_next) {
-      ++b;
-      t_cur = t_next;
-      t_next = __ldg(tb + b + 1);
-      chg = true;
-    }
-    if (chg) ++nb;
-    return chg;
+  __device__ __forceinline__ uint32_t tile(uint32_t i) const {
+    return inter ? ((i / kGsRun) * G + first) * kGsRun + (i % kGsRun) : first + i;
   }
 };
 
@@ -726,9 +807,9 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(b_empty + kGsNB);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t Nt = __ldg(ga.tbase + ga.K);
-  const uint32_t t0 = (uint32_t)(((uint64_t)Nt * blockIdx.x) / gridDim.x);
-  const uint32_t t1 = (uint32_t)(((uint64_t)Nt * (blockIdx.x + 1)) / gridDim.x);
+  GsSeq seq;
+  seq.init(__ldg(ga.tbase + ga.K), blockIdx.x, gridDim.x, ga.interleave);
+  const uint32_t ntile = seq.cnt;
   const int r0 = ga.r0, r1 = ga.r1;
 
   // operand pad columns (r0 up to a multiple of 8 floats) must read as zero
@@ -763,7 +844,7 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
   const uint32_t tmem = *tmem_slot;
   const uint32_t sbase = s32(smem);
 
-  if (t0 < t1) {
+  if (ntile > 0) {
     if (warp == 0) {
       // ================= MMA issuer =================
       const uint32_t idesc32 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(32 >> 3) << 17) |
@@ -771,21 +852,20 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
       const uint32_t idesc64 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(64 >> 3) << 17) |
                                ((uint32_t)(kGsTile >> 4) << 24);
       const int nk = (r0 + 7) >> 3;
-      GsWalk w;
-      w.init(ga.tbase, ga.K, t0);
-      uint32_t it = 0;
-      bool first = true;
-      uint32_t slot = 0;
+      uint32_t nb = 0, slot = 0, prev_b = 0xffffffffu;  // bucket changes so far: the slice-image ring position
+      uint32_t nxt = __ldg(&ga.tinfo[seq.tile(0)].y);
       GS_TRACE_INIT();
-      for (uint32_t t = t0; t < t1; ++t, ++it) {
-        const bool chg = w.advance(t);
-        if (first || chg) {
-          if (!first) {
+      for (uint32_t it = 0; it < ntile; ++it) {
+        const uint32_t b = nxt >> 8;
+        if (it + 1 < ntile) nxt = __ldg(&ga.tinfo[seq.tile(it + 1)].y);
+        if (b != prev_b) {
+          if (prev_b != 0xffffffffu) {
             gs_commit_elect(&b_empty[slot]);  // the previous bucket's MMAs are all issued
+            ++nb;
           }
-          slot = w.nb % kGsNB;
-          gs_wait(&b_full[slot], (w.nb / kGsNB) & 1);
-          first = false;
+          prev_b = b;
+          slot = nb % kGsNB;
+          gs_wait(&b_full[slot], (nb / kGsNB) & 1);
         }
         const uint32_t s = it % NS, a = it % kGsNA;
         gs_wait(&a_ready[s], (it / NS) & 1);
@@ -823,17 +903,19 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
     } else if (warp == 1) {
       // ================= slice images -> ring =================
       if (lane == 0) {
-        GsWalk w;
-        w.init(ga.tbase, ga.K, t0);
-        bool first = true;
-        for (uint32_t t = t0; t < t1; ++t) {
-          const bool chg = w.advance(t);
-          if (first || chg) {
-            const uint32_t slot = w.nb % kGsNB;
-            gs_wait(&b_empty[slot], ((w.nb / kGsNB) & 1) ^ 1);
+        uint32_t nb = 0, prev_b = 0xffffffffu;
+        uint32_t nxt = __ldg(&ga.tinfo[seq.tile(0)].y);
+        for (uint32_t it = 0; it < ntile; ++it) {
+          const uint32_t b = nxt >> 8;
+          if (it + 1 < ntile) nxt = __ldg(&ga.tinfo[seq.tile(it + 1)].y);
+          if (b != prev_b) {
+            if (prev_b != 0xffffffffu) ++nb;
+            prev_b = b;
+            const uint32_t slot = nb % kGsNB;
+            gs_wait(&b_empty[slot], ((nb / kGsNB) & 1) ^ 1);
             mb_expect(&b_full[slot], kGsImgBytes);
-            bulk(smem + L::kB + slot * kGsImgBytes, ga.img + (size_t)w.b * kGsImgBytes, kGsImgBytes, &b_full[slot]);
-            first = false;
+            bulk(smem + L::kB + slot * kGsImgBytes, ga.img + (size_t)(b % ga.Kmid) * kGsImgBytes, kGsImgBytes,
+                 &b_full[slot]);
           }
         }
       }
@@ -848,7 +930,7 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
       uint64_t keep;
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
       GS_TRACE_INIT();
-      for (uint32_t t = t0; t < t1; ++t, ++it) {
+      for (; it < ntile; ++it) {
         const uint32_t s = it % NS, a = it % kGsNA;
         gs_wait(&full_raw[s], (it / NS) & 1);
         GS_TRACE(1, it, 0);
@@ -941,53 +1023,45 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
       }
       uint64_t stream_pol;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(stream_pol));
-      const int modeP = 2 * __ldg(ga.hot + 0) > kGsHotBlocks ? 2 : (ga.pfP ? 1 : 0);
+      const int modeP = 2 * __ldg(ga.hot + 0) > kGsHotBlocks ? 2 : (ga.pfP && !ga.interleave ? 1 : 0);
       const int modeS = 2 * __ldg(ga.hot + 1) > kGsHotBlocks ? 2 : (ga.pfS ? 1 : 0);
       const int modeD = DIAG && 2 * __ldg(ga.hot + 2) > kGsHotBlocks ? 2 : (ga.pfD ? 1 : 0);
+      uint64_t normal_pol;
+      asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(normal_pol));
+      const bool anyhot = modeP == 2 || modeS == 2 || modeD == 2;
+      const uint64_t polP = modeP == 1 ? stream_pol : normal_pol, polS = modeS == 1 ? stream_pol : normal_pol,
+                     polD = modeD == 1 ? stream_pol : normal_pol;
       const int row = pw * 8 + (lane & 7);  // lanes 0-7 hold the warp's records
-      GsWalk w;
-      w.init(ga.tbase, ga.K, t0);
-      uint32_t bs_cur = __ldg(ga.bstart + w.b), bs_next = __ldg(ga.bstart + w.b + 1);
-      auto locate = [&](uint32_t t, uint32_t& p0, int& n) {
-        if (w.advance(t)) {
-          bs_cur = __ldg(ga.bstart + w.b);
-          bs_next = __ldg(ga.bstart + w.b + 1);
-        }
-        p0 = bs_cur + (t - w.t_cur) * kGsTile;
-        const uint32_t left = bs_next - p0;
-        n = left < (uint32_t)kGsTile ? (int)left : kGsTile;
-      };
       // record ring in shared memory (per warp: RR tiles x 8 records), filled
       // with cp.async RR tiles ahead: one commit group per tile, so
       // wait_group RR-1 at the top of a tile means its record has landed
       // (register prefetches of several tiles share a scoreboard: waiting for
-      // the oldest load also waited for the newest).  The CTA's records are
-      // one contiguous stream, prefetched into L2 further ahead.
+      // the oldest load also waited for the newest).  The tile map entry of
+      // the tile after the one being requested is loaded one step ahead.
       constexpr int RR = L::RR;
       const uint32_t ring = sbase + L::kRec + (uint32_t)pw * (RR * 128) + (uint32_t)(lane & 7) * 16;
-      auto issue_rec = [&](uint32_t t, uint32_t slot) {
-        uint32_t p0;
-        int n;
-        locate(t, p0, n);
+      uint2 tnext = __ldg(ga.tinfo + seq.tile(0));
+      uint32_t jreq = 0;  // next tile (sequence index) whose records are requested
+      auto issue_rec = [&](uint32_t slot) {
+        const uint2 ti = tnext;
+        ++jreq;
+        if (jreq < ntile) tnext = __ldg(ga.tinfo + seq.tile(jreq));
         if (lane < 8) {
           const uint32_t dst = ring + slot * 128;
-          if (row < n) {
-            gs_cp16_stream(dst, ga.recs + p0 + row, stream_pol);
+          if (row <= (int)(ti.y & 0xff)) {
+            gs_cp16_stream(dst, ga.recs + ti.x + row, stream_pol);
           } else {
             asm volatile("st.shared.v4.b32 [%0], {%1, %2, %2, %2};" ::"r"(dst), "r"(0xffffffffu), "r"(0u) : "memory");
           }
-          const uint32_t pf = p0 + (uint32_t)row + kGsPFL2 * kGsTile;
-          if ((lane & 1) == 0 && pf < ga.m) prefetch_l2(ga.recs + pf);
         }
       };
 #pragma unroll 1
       for (int j = 0; j < RR; ++j) {
-        if (t0 + j < t1) issue_rec(t0 + j, (uint32_t)j);
+        if ((uint32_t)j < ntile) issue_rec((uint32_t)j);
         asm volatile("cp.async.commit_group;" ::: "memory");
       }
-      uint32_t it = 0;
       GS_TRACE_INIT();
-      for (uint32_t t = t0; t < t1; ++t, ++it) {
+      for (uint32_t it = 0; it < ntile; ++it) {
         asm volatile("cp.async.wait_group %0;" ::"n"(RR - 1) : "memory");
         const uint32_t slot = it % RR;
         uint4 rec = make_uint4(0xffffffffu, 0, 0, 0);
@@ -999,10 +1073,10 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
         }
         GS_TRACE(2, it, 5);
         if (pw == 0) GS_STAMP(it, 0);
-        if (t + RR < t1) issue_rec(t + RR, slot);
+        if (jreq < ntile) issue_rec(slot);
         GS_TRACE(2, it, 3);
         const uint32_t s = it % NS;
-        gs_wait(&empty[s], ((it / NS) & 1) ^ 1);
+        gs_wait_relaxed(&empty[s], ((it / NS) & 1) ^ 1);
         GS_TRACE(2, it, 1);
         if (pw == 0) GS_STAMP(it, 1);
         const uint32_t sa = sbase + s * L::kStage;
@@ -1010,19 +1084,38 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
           asm volatile("st.shared.b32 [%0], %1;" ::"r"(sa + (uint32_t)L::kOrigOff + 4u * (uint32_t)row), "r"(rec.x)
                        : "memory");
         }
+        if (!anyhot) {  // the usual case: one copy instruction per piece, the L2 policy in a register
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int src = 4 * i + rsub;
-          const uint32_t og = __shfl_sync(0xffffffffu, rec.x, src);
-          const uint32_t pr = __shfl_sync(0xffffffffu, rec.y, src);
-          const uint32_t sr = __shfl_sync(0xffffffffu, rec.z, src);
-          uint32_t dr = 0;
-          if (DIAG) dr = __shfl_sync(0xffffffffu, rec.w, src);
-          if (og != 0xffffffffu) {
-            if (okA) gs_cp16_mode(sa + offA[i], Pc + (uint64_t)pr * rbA, modeP, stream_pol);
-            if (okS) {
-              gs_cp16_mode(sa + offS[i], Sc + (uint64_t)sr * rbS, modeS, stream_pol);
-              if (DIAG) gs_cp16_mode(sa + offS[i] + L::kClose, Dc + (uint64_t)dr * rbS, modeD, stream_pol);
+          for (int i = 0; i < 2; ++i) {
+            const int src = 4 * i + rsub;
+            const uint32_t og = __shfl_sync(0xffffffffu, rec.x, src);
+            const uint32_t pr = __shfl_sync(0xffffffffu, rec.y, src);
+            const uint32_t sr = __shfl_sync(0xffffffffu, rec.z, src);
+            uint32_t dr = 0;
+            if (DIAG) dr = __shfl_sync(0xffffffffu, rec.w, src);
+            if (og != 0xffffffffu) {
+              if (okA) gs_cp16_stream(sa + offA[i], Pc + (uint64_t)pr * rbA, polP);
+              if (okS) {
+                gs_cp16_stream(sa + offS[i], Sc + (uint64_t)sr * rbS, polS);
+                if (DIAG) gs_cp16_stream(sa + offS[i] + L::kClose, Dc + (uint64_t)dr * rbS, polD);
+              }
+            }
+          }
+        } else {  // some table's rows repeat: those go through L1
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int src = 4 * i + rsub;
+            const uint32_t og = __shfl_sync(0xffffffffu, rec.x, src);
+            const uint32_t pr = __shfl_sync(0xffffffffu, rec.y, src);
+            const uint32_t sr = __shfl_sync(0xffffffffu, rec.z, src);
+            uint32_t dr = 0;
+            if (DIAG) dr = __shfl_sync(0xffffffffu, rec.w, src);
+            if (og != 0xffffffffu) {
+              if (okA) gs_cp16_mode(sa + offA[i], Pc + (uint64_t)pr * rbA, modeP, stream_pol);
+              if (okS) {
+                gs_cp16_mode(sa + offS[i], Sc + (uint64_t)sr * rbS, modeS, stream_pol);
+                if (DIAG) gs_cp16_mode(sa + offS[i] + L::kClose, Dc + (uint64_t)dr * rbS, modeD, stream_pol);
+              }
             }
           }
         }
@@ -1042,7 +1135,7 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
       const uint32_t rowoff = (uint32_t)row * kGsRow;
       uint32_t it = 0;
       GS_TRACE_INIT();
-      for (uint32_t t = t0; t < t1; ++t, ++it) {
+      for (; it < ntile; ++it) {
         const uint32_t s = it % NS;
         gs_wait(&full_raw[s], (it / NS) & 1);
         GS_TRACE(3, it, 0);
@@ -1098,11 +1191,21 @@ void gs_fill_prep(const ChainDev& ch, const GPlan& G, GsPrep* gp) {
   const MergePlan& mp = G.mp;
   gp->n0 = ch.n;
   gp->K = (uint32_t)G.K;
-  for (int g = 0; g < mp.ng; ++g)
-    for (int o = mp.lo[g]; o < mp.hi[g]; ++o) {
+  gp->Kmid = (uint32_t)G.Kmid;
+  gp->sub_rows = (uint32_t)G.sub_rows;
+  for (int g = 0; g < mp.ng; ++g) {
+    const int f = g == 0 ? 0 : (g == mp.ng - 1 ? 3 : (g == G.gdiag ? 2 : 1));
+    // the sorted field runs over ALL merged interior groups (one original mode each)
+    uint32_t w = 1;
+    if (f == 1)
+      for (int o = mp.hi[g]; o < G.omid_hi; ++o) w *= (uint32_t)ch.m[o].J;
+    for (int o = mp.hi[g] - 1; o >= mp.lo[g]; --o) {
       gp->oJ[o] = ch.m[o].J;
-      gp->grp[o] = (int8_t)(g == 0 ? 0 : (g == mp.ng - 1 ? 3 : (g == G.gdiag ? 2 : 1)));
+      gp->w0[o] = gp->w1[o] = gp->w2[o] = gp->w3[o] = 0;
+      (f == 0 ? gp->w0 : f == 1 ? gp->w1 : f == 2 ? gp->w2 : gp->w3)[o] = w;
+      w *= (uint32_t)ch.m[o].J;
     }
+  }
 }
 
 }  // namespace
@@ -1221,6 +1324,7 @@ int launch_entries_gsort(const ChainDev& ch, const int64_t* idx, int64_t m, floa
   uint32_t* bstart = reinterpret_cast<uint32_t*>(base + G.bstart_off);
   uint32_t* tbase = reinterpret_cast<uint32_t*>(base + G.tbase_off);
   uint32_t* cursor = reinterpret_cast<uint32_t*>(base + G.cursor_off);
+  uint2* tinfo = reinterpret_cast<uint2*>(base + G.tinfo_off);
   uint4* recu = reinterpret_cast<uint4*>(base + G.recu_off);
   uint4* recs = reinterpret_cast<uint4*>(base + G.recs_off);
   const uint32_t K = (uint32_t)G.K;
@@ -1251,6 +1355,8 @@ int launch_entries_gsort(const ChainDev& ch, const int64_t* idx, int64_t m, floa
   {
     KTimer kt("entries_sort", st);
     gs_scan_kernel<<<1, 1024, 0, st>>>(hist, K, bstart, tbase, cursor);
+    gs_tilemap_kernel<<<(unsigned)std::min<int64_t>(ceil_div(ceil_div(m, kGsTile) + K, 256), (int64_t)num_sms() * 8), 256, 0,
+                        st>>>(bstart, tbase, K, tinfo);
     const size_t sm = (size_t)kGsScatThreads * kGsScatPer * 18 + (size_t)K * 8;
     if (K > (uint32_t)kGsSmemK) {
       const int64_t g = std::min<int64_t>(ceil_div(m, 256), (int64_t)num_sms() * 16);
@@ -1279,9 +1385,11 @@ int launch_entries_gsort(const ChainDev& ch, const int64_t* idx, int64_t m, floa
   ga.D = G.gdiag >= 0 ? v.m[G.gdiag].s : nullptr;
   ga.img = base + G.img_off;
   ga.recs = recs;
-  ga.bstart = bstart;
+  ga.tinfo = tinfo;
   ga.tbase = tbase;
   ga.K = K;
+  ga.Kmid = (uint32_t)G.Kmid;
+  ga.interleave = G.nsub > 1;
   ga.hot = hist + K;
   ga.m = (uint32_t)m;
   {  // L2 policies: big tables stream, a result that fits stays
