@@ -73,7 +73,18 @@ constexpr int kGsNB = 2;                 // slice images in flight
 // warps: 0 MMA, 1 image loader, 2-3 idle, 4-7 epilogue, 8-11 splitters, 12-27 producers
 // (a warp holds at most ~8 LDGSTS in flight -- tools/gather_bench.cu -- so the
 // gather rate and a tile's gather latency are set by the number of producer warps)
-constexpr int kGsPW = 16;                // producer warps (8 rows of every tile each)
+#ifndef TNB_GS_PW
+#define TNB_GS_PW 16
+#endif
+// splitter: 1 = the MMA reads the gathered tile itself (hi = truncation by the
+// tensor core), only lo is written; 0 = hi rounded to nearest, stored in place
+#ifndef TNB_GS_TRUNC_HI
+#define TNB_GS_TRUNC_HI 1
+#endif
+constexpr int kGsPW = TNB_GS_PW;         // producer warps (128 / kGsPW rows of every tile each)
+constexpr int kGsRW = kGsTile / kGsPW;   // rows per producer warp
+constexpr int kGsPasses = kGsRW / 4;     // 4 rows per copy instruction
+static_assert(kGsRW * kGsPW == kGsTile && kGsPasses * 4 == kGsRW && kGsRW <= 32, "producer geometry");
 constexpr int kGsThreads = (12 + kGsPW) * 32;
 #ifndef TNB_GS_PF
 #define TNB_GS_PF 8
@@ -782,8 +793,8 @@ struct GsSmem {
   static constexpr int kAlo = NS * kStage;                                   // 2 x 16 KB
   static constexpr int kB = kAlo + 2 * kGsTileBytes;                         // kGsNB x 8 KB
   static constexpr int RR = 4;                                               // record ring depth (tiles)
-  static constexpr int kRec = kB + kGsNB * kGsImgBytes;                      // kGsPW warps x RR x 8 records x 16 B
-  static constexpr int kBars = kRec + kGsPW * RR * 128;
+  static constexpr int kRec = kB + kGsNB * kGsImgBytes;                      // kGsPW warps x RR x kGsRW records x 16 B
+  static constexpr int kBars = kRec + kGsPW * RR * kGsRW * 16;
   static constexpr int kNBars = 3 * NS + 2 + 2 * kGsNA + 2 * kGsNB;
   static constexpr int kBytes = kBars + kNBars * 8 + 16;
   static_assert(kBytes + 1024 <= 232448, "shared memory");
@@ -932,7 +943,11 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
       GS_TRACE_INIT();
       for (; it < ntile; ++it) {
         const uint32_t s = it % NS, a = it % kGsNA;
+#ifdef TNB_GS_RELAX_ALL
+        gs_wait_relaxed(&full_raw[s], (it / NS) & 1);
+#else
         gs_wait(&full_raw[s], (it / NS) & 1);
+#endif
         GS_TRACE(1, it, 0);
         const uint32_t st = sbase + s * L::kStage;
         uint32_t orig;
@@ -1014,10 +1029,10 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
       const unsigned char* Sc = reinterpret_cast<const unsigned char*>(ga.S) + 16 * c;
       const unsigned char* Dc = reinterpret_cast<const unsigned char*>(ga.D) + 16 * c;
       const uint32_t rbA = (uint32_t)r0 * 4, rbS = (uint32_t)r1 * 4;
-      uint32_t offA[2], offS[2];
+      uint32_t offA[kGsPasses], offS[kGsPasses];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const uint32_t r = (uint32_t)(pw * 8 + 4 * i + rsub);
+      for (int i = 0; i < kGsPasses; ++i) {
+        const uint32_t r = (uint32_t)(pw * kGsRW + 4 * i + rsub);
         offA[i] = r * kGsRow + (((uint32_t)c ^ (r & 7)) << 4);
         offS[i] = kGsTileBytes + r * CSB + ((CSB == 128 ? ((uint32_t)c ^ (r & 7)) : (uint32_t)c) << 4);
       }
@@ -1031,7 +1046,7 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
       const bool anyhot = modeP == 2 || modeS == 2 || modeD == 2;
       const uint64_t polP = modeP == 1 ? stream_pol : normal_pol, polS = modeS == 1 ? stream_pol : normal_pol,
                      polD = modeD == 1 ? stream_pol : normal_pol;
-      const int row = pw * 8 + (lane & 7);  // lanes 0-7 hold the warp's records
+      const int row = pw * kGsRW + (lane % kGsRW);  // lanes 0 .. kGsRW-1 hold the warp's records
       // record ring in shared memory (per warp: RR tiles x 8 records), filled
       // with cp.async RR tiles ahead: one commit group per tile, so
       // wait_group RR-1 at the top of a tile means its record has landed
@@ -1039,15 +1054,15 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
       // the oldest load also waited for the newest).  The tile map entry of
       // the tile after the one being requested is loaded one step ahead.
       constexpr int RR = L::RR;
-      const uint32_t ring = sbase + L::kRec + (uint32_t)pw * (RR * 128) + (uint32_t)(lane & 7) * 16;
+      const uint32_t ring = sbase + L::kRec + (uint32_t)pw * (RR * kGsRW * 16) + (uint32_t)(lane % kGsRW) * 16;
       uint2 tnext = __ldg(ga.tinfo + seq.tile(0));
       uint32_t jreq = 0;  // next tile (sequence index) whose records are requested
       auto issue_rec = [&](uint32_t slot) {
         const uint2 ti = tnext;
         ++jreq;
         if (jreq < ntile) tnext = __ldg(ga.tinfo + seq.tile(jreq));
-        if (lane < 8) {
-          const uint32_t dst = ring + slot * 128;
+        if (lane < kGsRW) {
+          const uint32_t dst = ring + slot * (kGsRW * 16);
           if (row <= (int)(ti.y & 0xff)) {
             gs_cp16_stream(dst, ga.recs + ti.x + row, stream_pol);
           } else {
@@ -1065,10 +1080,10 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
         asm volatile("cp.async.wait_group %0;" ::"n"(RR - 1) : "memory");
         const uint32_t slot = it % RR;
         uint4 rec = make_uint4(0xffffffffu, 0, 0, 0);
-        if (lane < 8) {
+        if (lane < kGsRW) {
           asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                        : "=r"(rec.x), "=r"(rec.y), "=r"(rec.z), "=r"(rec.w)
-                       : "r"(ring + slot * 128)
+                       : "r"(ring + slot * (kGsRW * 16))
                        : "memory");
         }
         GS_TRACE(2, it, 5);
@@ -1080,13 +1095,13 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
         GS_TRACE(2, it, 1);
         if (pw == 0) GS_STAMP(it, 1);
         const uint32_t sa = sbase + s * L::kStage;
-        if (lane < 8) {
+        if (lane < kGsRW) {
           asm volatile("st.shared.b32 [%0], %1;" ::"r"(sa + (uint32_t)L::kOrigOff + 4u * (uint32_t)row), "r"(rec.x)
                        : "memory");
         }
         if (!anyhot) {  // the usual case: one copy instruction per piece, the L2 policy in a register
 #pragma unroll
-          for (int i = 0; i < 2; ++i) {
+          for (int i = 0; i < kGsPasses; ++i) {
             const int src = 4 * i + rsub;
             const uint32_t og = __shfl_sync(0xffffffffu, rec.x, src);
             const uint32_t pr = __shfl_sync(0xffffffffu, rec.y, src);
@@ -1103,7 +1118,7 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
           }
         } else {  // some table's rows repeat: those go through L1
 #pragma unroll
-          for (int i = 0; i < 2; ++i) {
+          for (int i = 0; i < kGsPasses; ++i) {
             const int src = 4 * i + rsub;
             const uint32_t og = __shfl_sync(0xffffffffu, rec.x, src);
             const uint32_t pr = __shfl_sync(0xffffffffu, rec.y, src);
@@ -1137,7 +1152,11 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
       GS_TRACE_INIT();
       for (; it < ntile; ++it) {
         const uint32_t s = it % NS;
+#ifdef TNB_GS_RELAX_ALL
+        gs_wait_relaxed(&full_raw[s], (it / NS) & 1);
+#else
         gs_wait(&full_raw[s], (it / NS) & 1);
+#endif
         GS_TRACE(3, it, 0);
         if (warp == 8) GS_STAMP(it, 3);
         gs_wait(&alo_empty[it & 1], ((it >> 1) & 1) ^ 1);
@@ -1152,6 +1171,15 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
         for (int c = 0; c < 8; ++c) {
           if (c < nph) {
             const uint32_t off = ((uint32_t)(c0 + c) ^ swz) << 4;
+#if TNB_GS_TRUNC_HI
+            // The MMA reads the gathered tile as it is: the tensor core ignores
+            // the low 13 mantissa bits, i.e. hi = x truncated to tf32.  Only
+            // lo = x - hi (exact) is written -- no in-place store of hi.
+            const uint32_t l0 = __float_as_uint(x[c].x - __uint_as_float(__float_as_uint(x[c].x) & 0xffffe000u));
+            const uint32_t l1 = __float_as_uint(x[c].y - __uint_as_float(__float_as_uint(x[c].y) & 0xffffe000u));
+            const uint32_t l2 = __float_as_uint(x[c].z - __uint_as_float(__float_as_uint(x[c].z) & 0xffffe000u));
+            const uint32_t l3 = __float_as_uint(x[c].w - __uint_as_float(__float_as_uint(x[c].w) & 0xffffe000u));
+#else
             // hi = x rounded to tf32 (nearest, ties away: add half an ulp of the
             // 10-bit mantissa to the magnitude and truncate -- what cvt.rna does,
             // on the full-rate integer pipe instead of the conversion pipe);
@@ -1167,6 +1195,7 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
             l3 = __float_as_uint(x[c].w - __uint_as_float(h3));
             asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(A + off), "r"(h0), "r"(h1), "r"(h2), "r"(h3)
                          : "memory");
+#endif
             asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(Alo + off), "r"(l0), "r"(l1), "r"(l2), "r"(l3)
                          : "memory");
           }
