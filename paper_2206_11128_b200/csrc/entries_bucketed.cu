@@ -225,6 +225,21 @@ __device__ __forceinline__ void split_tf32_fast(float x, uint32_t& hi, uint32_t&
   split_tf32(x, hi, lo);
 #endif
 }
+// the A-fragment split of the per-entry kernels: hi = the fp32 bits as they
+// are (the tensor core ignores the low 13 mantissa bits: truncation), lo =
+// x - trunc(x) exact -- no conversion-pipe instruction per element
+// (TNB_SPLIT_TRUNC=0: cvt.rna as above)
+#ifndef TNB_SPLIT_TRUNC
+#define TNB_SPLIT_TRUNC 1
+#endif
+__device__ __forceinline__ void split_tf32_step(float x, uint32_t& hi, uint32_t& lo) {
+#if TNB_SPLIT_TRUNC
+  hi = __float_as_uint(x);
+  lo = __float_as_uint(x - __uint_as_float(hi & 0xffffe000u));
+#else
+  split_tf32_fast(x, hi, lo);
+#endif
+}
 __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
       "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
@@ -1112,7 +1127,7 @@ __global__ void __launch_bounds__(NT, kStateCtas)
               for (int kt = 0; kt < 4; ++kt) {
                 uint32_t ah[4], al[4];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) split_tf32_fast(av[kt][i], ah[i], al[i]);
+                for (int i = 0; i < 4; ++i) split_tf32_step(av[kt][i], ah[i], al[i]);
 #pragma unroll
                 for (int nt = 0; nt < 4; ++nt) {
                   mma_tf32(acc[nt], al, bh[kt][nt][0], bh[kt][nt][1]);
@@ -1689,10 +1704,10 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
           for (int kt = 0; kt < KT; ++kt) {
             uint32_t ah[4], al[4];
-            split_tf32_fast(lds32(vr[0] + kt * 32 + vb16[0]), ah[0], al[0]);
-            split_tf32_fast(lds32(vr[1] + kt * 32 + vb16[1]), ah[1], al[1]);
-            split_tf32_fast(lds32(vr[0] + kt * 32 + 16 - vb16[0]), ah[2], al[2]);
-            split_tf32_fast(lds32(vr[1] + kt * 32 + 16 - vb16[1]), ah[3], al[3]);
+            split_tf32_step(lds32(vr[0] + kt * 32 + vb16[0]), ah[0], al[0]);
+            split_tf32_step(lds32(vr[1] + kt * 32 + vb16[1]), ah[1], al[1]);
+            split_tf32_step(lds32(vr[0] + kt * 32 + 16 - vb16[0]), ah[2], al[2]);
+            split_tf32_step(lds32(vr[1] + kt * 32 + 16 - vb16[1]), ah[3], al[3]);
 #pragma unroll
             for (int nt = 0; nt < KT; ++nt) {
               mma_tf32(acc[nt], al, bh[kt][nt][0], bh[kt][nt][1]);
