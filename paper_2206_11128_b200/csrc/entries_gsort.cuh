@@ -86,26 +86,8 @@ constexpr int kGsRW = kGsTile / kGsPW;   // rows per producer warp
 constexpr int kGsPasses = kGsRW / 4;     // 4 rows per copy instruction
 static_assert(kGsRW * kGsPW == kGsTile && kGsPasses * 4 == kGsRW && kGsRW <= 32, "producer geometry");
 constexpr int kGsThreads = (12 + kGsPW) * 32;
-#ifndef TNB_GS_PF
-#define TNB_GS_PF 8
-#endif
-#ifndef TNB_GS_PFROWS
-#define TNB_GS_PFROWS 6
-#endif
-#ifndef TNB_GS_PFL2
-#define TNB_GS_PFL2 32
-#endif
-constexpr int kGsPF = TNB_GS_PF;         // record loads in flight per producer lane (tiles)
-constexpr int kGsPFRows = TNB_GS_PFROWS;  // table rows are prefetched into L2 this many tiles ahead (< kGsPF)
-constexpr int kGsPFL2 = TNB_GS_PFL2;     // L2 prefetch distance of the record stream (tiles)
 constexpr int kGsPrepThreads = 512;
-#ifndef TNB_GS_SCAT_T
-#define TNB_GS_SCAT_T 512
-#endif
-#ifndef TNB_GS_SCAT_PER
-#define TNB_GS_SCAT_PER 8
-#endif
-constexpr int kGsScatThreads = TNB_GS_SCAT_T, kGsScatPer = TNB_GS_SCAT_PER;
+constexpr int kGsScatThreads = 512, kGsScatPer = 8;  // 1024 x 4 and 256 x 8 measured equal / slower
 
 struct GPlan {
   MergePlan mp;
@@ -475,7 +457,7 @@ __global__ void __launch_bounds__(256) gs_tilemap_kernel(const uint32_t* __restr
 // reserves the CTA's range of every bucket with one atomicAdd, sorts the
 // records by key in shared memory and writes {orig, first row, last row, diag
 // row} runs to the sorted positions (a bucket's share is contiguous)
-__global__ void __launch_bounds__(kGsScatThreads, 2048 / kGsScatThreads > 2 ? 2 : 2048 / kGsScatThreads) gs_scatter_kernel(const uint4* __restrict__ recu, int64_t m, uint32_t K,
+__global__ void __launch_bounds__(kGsScatThreads, 2) gs_scatter_kernel(const uint4* __restrict__ recu, int64_t m, uint32_t K,
                                                                      uint32_t* __restrict__ cursor,
                                                                      uint4* __restrict__ recs) {
   extern __shared__ __align__(16) uint32_t gs_sh[];
@@ -670,11 +652,7 @@ __device__ __forceinline__ void gs_commit(uint64_t* b) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(s32(b)) : "memory");
 }
 __device__ __forceinline__ void gs_cp16(uint32_t dst, const void* src) {
-#ifdef TNB_GS_CA
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-#else
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-#endif
 }
 // rows of a table too large for L2 are streamed (evict_first): they would
 // otherwise push out the result lines, whose scattered 4-byte writes only
@@ -943,11 +921,7 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
       GS_TRACE_INIT();
       for (; it < ntile; ++it) {
         const uint32_t s = it % NS, a = it % kGsNA;
-#ifdef TNB_GS_RELAX_ALL
-        gs_wait_relaxed(&full_raw[s], (it / NS) & 1);
-#else
         gs_wait(&full_raw[s], (it / NS) & 1);
-#endif
         GS_TRACE(1, it, 0);
         const uint32_t st = sbase + s * L::kStage;
         uint32_t orig;
@@ -997,18 +971,12 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
         }
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         gs_arrive(&acc_empty[a]);
-#ifdef TNB_GS_OUTSEQ  // timing experiment: contiguous instead of scattered result writes (wrong results)
-        if (orig != 0xffffffffu) ga.out[(size_t)(blockIdx.x * 886 + it) * 128 % ga.m + row] = acc0 + acc1;
-#elif defined(TNB_GS_NOOUT)
-        if (orig == 0xfffffffeu) ga.out[orig] = acc0 + acc1;
-#else
         if (orig != 0xffffffffu) {
           if (ga.keep_out)
             asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(ga.out + orig), "f"(acc0 + acc1), "l"(keep) : "memory");
           else
             ga.out[orig] = acc0 + acc1;
         }
-#endif
         gs_arrive(&empty[s]);
         GS_TRACE(1, it, 2);
         if (q == 0) GS_STAMP(it, 9);
@@ -1020,11 +988,7 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
       // per lane group and table); the warp's 8 rows take 2 passes.
       const int pw = warp - 12;
       const int c = lane & 7, rsub = lane >> 3;
-#ifdef TNB_GS_NOS  // timing experiment: no closing-row gathers (wrong results)
-      const bool okA = c < (r0 >> 2), okS = false;
-#else
       const bool okA = c < (r0 >> 2), okS = c < (r1 >> 2);
-#endif
       const unsigned char* Pc = reinterpret_cast<const unsigned char*>(ga.P) + 16 * c;
       const unsigned char* Sc = reinterpret_cast<const unsigned char*>(ga.S) + 16 * c;
       const unsigned char* Dc = reinterpret_cast<const unsigned char*>(ga.D) + 16 * c;
@@ -1152,11 +1116,7 @@ __global__ void __launch_bounds__(kGsThreads, 1) entries_gsort_kernel(const __gr
       GS_TRACE_INIT();
       for (; it < ntile; ++it) {
         const uint32_t s = it % NS;
-#ifdef TNB_GS_RELAX_ALL
-        gs_wait_relaxed(&full_raw[s], (it / NS) & 1);
-#else
         gs_wait(&full_raw[s], (it / NS) & 1);
-#endif
         GS_TRACE(3, it, 0);
         if (warp == 8) GS_STAMP(it, 3);
         gs_wait(&alo_empty[it & 1], ((it >> 1) & 1) ^ 1);
