@@ -2280,14 +2280,15 @@ int64_t env_rows(const char* name) {
   return e ? atoll(e) : 0;
 }
 
-void plan_merge(const ChainDev& ch, int64_t m, MergePlan* mp) {
+// wide_rows: row limit of the wide (HBM) prefix / suffix tables (0: m / 8)
+void plan_merge(const ChainDev& ch, int64_t m, MergePlan* mp, int64_t wide_rows = 0) {
   const int N = ch.n;
   // uint16-indexed, L2-resident tables: up to min(m/16, 65535) rows.  A
   // prefix / suffix may grow further ("wide": uint32 indices, HBM-resident,
   // up to m/8 rows and 1.5 GB) but only by absorbing DENSE modes -- each
   // one removes a sorted r x r step per entry for one gathered row.
   const int64_t lim = (merge_env() && N >= 3) ? (m / 16 < 65535 ? m / 16 : 65535) : 0;
-  const int64_t limw = (lim > 0 && wide_env()) ? std::min<int64_t>(m / 8, (int64_t)1 << 30) : lim;
+  const int64_t limw = (lim > 0 && wide_env()) ? std::min<int64_t>(wide_rows > 0 ? wide_rows : m / 8, (int64_t)1 << 30) : lim;
   const double max_table = 1.5e9;
   auto grow = [&](int64_t nr, const ModeDev& md, int width) {
     return nr <= lim || (nr <= limw && md.layout == TNB_LAYOUT_DENSE && (double)nr * width * 4 <= max_table);
