@@ -173,3 +173,21 @@ def test_gsort_is_bitwise_reproducible(monkeypatch):
     c = tb.entries(t, idx[perm], algo=N.ALGO_GSORT)
     assert torch.equal(a, b)
     assert torch.equal(a[perm], c)
+
+
+def test_gsort_mid_size_uses_wider_tables():
+    # cfg2 chain at 2^21 tuples (a rank's shard of the headline at 8 GPUs): the
+    # usual merge (tables of up to m / 8 rows) leaves four interior modes, so
+    # the planner retries with tables of up to m / 2 rows: P0123 . G45 . S6789
+    cores = O.random_tt((32,) * 10, 32, seed=0, scale=32 ** -0.5)
+    nodes = [("tt", c, None) for c in cores]
+    t, o = facade(nodes), O.make_chain(nodes)
+    m = 1 << 21
+    plan = _plan(t, m, N.ALGO_AUTO)
+    assert (plan["algo"], plan["n_virtual"], plan["prefix_rows"], plan["suffix_rows"]) == \
+        (N.ALGO_GSORT, 3, 1 << 20, 1 << 20), plan
+    idx = O.uniform_indices(t.shape, m, 5)
+    idx[3::11] -= 32
+    got = tb.entries(t, idx)
+    sel = np.arange(0, m, 37)
+    assert_close(got[torch.as_tensor(sel, device=got.device)], O.entries(o, idx[sel]))
