@@ -6,6 +6,10 @@
 // Modes: 0 = 16-byte cp.async (LDGSTS), 8 lanes per row, per-warp ring with wait_group
 //        1 = LDG.128 into registers, 8 lanes per row, UNROLL rows in flight per lane group
 //        2 = cp.async.bulk (TMA) 128 B per row, one mbarrier per batch of 32 rows per warp
+//        3 = TMA tile::gather4 (UTMALDG.2D.GATHER4): 4 rows per instruction, SWIZZLE_128B tensor map;
+//            checked against the table (row r holds the value r in every column)
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -137,13 +141,79 @@ __global__ void __launch_bounds__(256) k_bulk(const float* __restrict__ tab, con
   if (acc == 12345.f) out[0] = acc;
 }
 
+// mode 3: TMA gather4: lanes 0..7 of a warp issue one gather4 each per batch of 32 rows
+template <int DEPTH>
+__global__ void __launch_bounds__(256) k_gather4(const __grid_constant__ CUtensorMap tm, const uint32_t* __restrict__ idx,
+                                                 int64_t m, float* __restrict__ out, unsigned long long* __restrict__ bad) {
+  extern __shared__ __align__(1024) unsigned char sm_raw[];
+  unsigned char* sm = sm_raw + ((1024 - (s32(sm_raw) & 1023)) & 1023);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned char* ring = sm + (size_t)warp * DEPTH * 4096;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + (size_t)8 * DEPTH * 4096) + warp * DEPTH;
+  if (lane == 0)
+    for (int d = 0; d < DEPTH; ++d) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s32(bars + d)));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  const int64_t nb = m / 32;
+  const int64_t gw = blockIdx.x * 8 + warp, nw = (int64_t)gridDim.x * 8;
+  float acc = 0.f;
+  unsigned long long nbad = 0;
+  auto issue = [&](int64_t b, int slot) {
+    const uint32_t row = __ldg(idx + b * 32 + lane);
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s32(bars + slot)), "r"(4096u) : "memory");
+    const int r0 = __shfl_sync(0xffffffffu, (int)row, (4 * lane) & 31), r1 = __shfl_sync(0xffffffffu, (int)row, (4 * lane + 1) & 31),
+              r2 = __shfl_sync(0xffffffffu, (int)row, (4 * lane + 2) & 31), r3 = __shfl_sync(0xffffffffu, (int)row, (4 * lane + 3) & 31);
+    __syncwarp();
+    if (lane < 8)
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+          "%6}], [%7];" ::"r"(s32(ring + slot * 4096 + lane * 512)),
+          "l"(&tm), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(s32(bars + slot))
+          : "memory");
+  };
+  int64_t b = gw;
+  for (int d = 0; d < DEPTH; ++d)
+    if (b + (int64_t)d * nw < nb) issue(b + (int64_t)d * nw, d);
+  int slot = 0;
+  uint32_t ph = 0;
+  for (; b < nb; b += nw) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra W_%=;\n\t}" ::"r"(s32(bars + slot)),
+        "r"(ph)
+        : "memory");
+    // row `lane` of the batch, column 4 * (lane & 7): SWIZZLE_128B puts 16-byte piece c at c ^ (row & 7)
+    const float v = *reinterpret_cast<const float*>(ring + slot * 4096 + lane * 128 + ((0 ^ (lane & 7)) << 4));
+    const float w = *reinterpret_cast<const float*>(ring + slot * 4096 + lane * 128 + ((3 ^ (lane & 7)) << 4) + 4);
+    const uint32_t want = __ldg(idx + b * 32 + lane);
+    if (v != (float)(want & 0xffff) || w != (float)(want & 0xffff) + 13.f) ++nbad;
+    acc += v;
+    __syncwarp();
+    const int64_t nxt = b + (int64_t)DEPTH * nw;
+    if (nxt < nb) issue(nxt, slot);
+    if (++slot == DEPTH) {
+      slot = 0;
+      ph ^= 1;
+    }
+  }
+  if (nbad) atomicAdd(bad, nbad);
+  if (acc == 12345.f) out[0] = acc;
+}
+
 int main(int argc, char** argv) {
   const int lr = argc > 1 ? atoi(argv[1]) : 20, lm = argc > 2 ? atoi(argv[2]) : 24;
   const int64_t rows = (int64_t)1 << lr, m = (int64_t)1 << lm;
   float *tab, *out;
   uint32_t* idx;
   CK(cudaMalloc(&tab, rows * 128));
-  CK(cudaMemset(tab, 0, rows * 128));
+  {  // row r: column c holds (r & 0xffff) + c (exact in fp32)
+    std::vector<float> ht((size_t)rows * 32);
+    for (int64_t r = 0; r < rows; ++r)
+      for (int c = 0; c < 32; ++c) ht[(size_t)r * 32 + c] = (float)(r & 0xffff) + (float)c;
+    CK(cudaMemcpy(tab, ht.data(), (size_t)rows * 128, cudaMemcpyHostToDevice));
+  }
   CK(cudaMalloc(&out, 4));
   CK(cudaMalloc(&idx, m * 4));
   std::vector<uint32_t> h(m);
@@ -197,5 +267,38 @@ int main(int argc, char** argv) {
   BULK(4, 1)
   BULK(6, 1)
   BULK(3, 2)
+  {  // mode 3: TMA gather4 through a SWIZZLE_128B tensor map, box height 1 and 4
+    void* fp = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q));
+    auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fp);
+    unsigned long long* bad;
+    CK(cudaMalloc(&bad, 8));
+    for (int bh : {1}) {  // box height 4 is rejected at run time (illegal instruction)
+      CUtensorMap tm;
+      const cuuint64_t dims[2] = {32, (cuuint64_t)rows};
+      const cuuint64_t strides[1] = {128};
+      const cuuint32_t box[2] = {32, (cuuint32_t)bh};
+      const cuuint32_t estr[2] = {1, 1};
+      const CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, tab, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      printf("tensor map box height %d: encode rc %d\n", bh, (int)r);
+      if (r != CUDA_SUCCESS) continue;
+#define G4(D, CTAS)                                                                                              \
+  {                                                                                                              \
+    const int smb = 8 * D * 4096 + 8 * D * 8 + 1024;                                                             \
+    CK(cudaFuncSetAttribute(k_gather4<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smb));                    \
+    CK(cudaMemset(bad, 0, 8));                                                                                   \
+    run("gather4 depth " #D " x " #CTAS " CTA/SM", [&] { k_gather4<D><<<148 * CTAS, 256, smb>>>(tm, idx, m, out, bad); }); \
+    unsigned long long hb = 0;                                                                                   \
+    CK(cudaMemcpy(&hb, bad, 8, cudaMemcpyDeviceToHost));                                                         \
+    printf("    mismatching rows: %llu of %lld\n", hb, (long long)(6 * m));                                      \
+  }
+      G4(2, 1)
+      G4(4, 1)
+      G4(4, 2)
+      G4(2, 4)
+    }
+  }
   return 0;
 }
