@@ -20,36 +20,33 @@
 //     writes one 16-byte record per sample {key, first row, last row, diag
 //     row} plus the global histogram of the keys;
 //   * gs_scan_kernel: bucket starts, and the start of every bucket in
-//     128-sample tiles (the compute kernel's work list);
+//     128-sample tiles (the compute kernel's work list, balanced by tiles
+//     whatever the skew); gs_tilemap_kernel: per tile {first sorted position,
+//     bucket, rows};
 //   * gs_scatter_kernel: counting-sort scatter of the records by key (the
 //     order inside a bucket is not fixed, and need not be: a sample's
 //     arithmetic does not depend on its position);
-//   * entries_gsort_kernel (persistent, one 512-thread CTA per SM), per tile
+//   * entries_gsort_kernel (persistent, one 896-thread CTA per SM), per tile
 //     of 128 sorted samples of one bucket:
-//       producer warps   gather the samples' first-table rows into the A
+//       16 producer warps gather the samples' first-table rows into the A
 //                        operand tile (K-major SW128 layout) and their
 //                        closing rows (last / diag tables) into shared memory
-//                        with 16-byte cp.async, several tiles ahead;
-//       splitter warps   x -> tf32 hi (in place) and lo = x - hi (second tile);
-//       one MMA lane     D[128 x 32] = Ahi Bhi + Alo Bhi + Ahi Blo
-//                        (tcgen05.mma.kind::tf32, accumulators in TMEM);
-//       epilogue warps   tcgen05.ld the D row of their sample, dot it with the
-//                        closing rows, write out[orig].
-// The kernel is bound by the random row gathers (HBM / L2), not by the MMAs.
+//                        with 16-byte cp.async, several tiles ahead (records
+//                        through a per-warp cp.async ring; L2 policies:
+//                        big tables stream, results stay; repeated rows go
+//                        through L1);
+//       4 splitter warps  lo = x - trunc_tf32(x) into a second tile (the MMA
+//                        reads the gathered tile itself as hi: the tensor
+//                        core ignores the low 13 mantissa bits);
+//       one MMA warp     D[128 x 64] = A [Bhi | Blo], D[:, :32] += Alo Bhi
+//                        (tcgen05.mma.kind::tf32, accumulators in TMEM, issued
+//                        by one elected lane);
+//       4 epilogue warps tcgen05.ld the D row of their sample, add the halves,
+//                        dot it with the closing rows, write out[orig].
+// The kernel runs at the rate the SM can keep random row gathers in flight
+// (DESIGN 3 K1 2c, tools/gather_bench.cu); the MMAs take 13% of the tensor pipe.
+// Results are bitwise reproducible and independent of the input order.
 #pragma once
-
-#define TMEM_LD32_GS(taddr, v)                                                                 \
-  asm volatile(                                                                                \
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "   \
-      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "  \
-      "%28, %29, %30, %31}, [%32];"                                                            \
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),    \
-        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),             \
-        "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),          \
-        "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),          \
-        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),          \
-        "=r"(v[31])                                                                            \
-      : "r"(taddr))
 
 #define TMEM_LD16_GS(taddr, v)                                                                   \
   asm volatile(                                                                                  \
