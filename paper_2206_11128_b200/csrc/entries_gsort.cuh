@@ -1222,16 +1222,20 @@ bool gsort_ok(const ChainDev& ch, int64_t m) {
 
 // AUTO: large calls whose buckets average at least 512 samples (4 tiles) and
 // whose sorted mode is a product of at least two interior modes -- the global
-// sort then removes a whole r x r step per entry.  With a single interior
-// mode (cfg5: P012 . G3 . D45 . S67) the stream kernel's per-tile sort is
-// cheaper than the global one (4.6 vs 5.7 ms at 2^26 tuples).
+// sort then removes a whole r x r step per entry -- or is a single interior
+// mode that the bucketed path would run on the state kernel (48^7, r = 32 at
+// 2^22 tuples: 0.34 against 0.47 ms; r = 20: against 1.08 ms).  A single
+// interior mode that fits the stream kernel stays there: its per-tile sort is
+// cheaper than the global one (cfg5: 4.6 against 5.5 ms at 2^26 tuples).
 bool gsort_auto(const ChainDev& ch, int64_t m) {
   const int env = gsort_env();
   if (!env || m < (1 << 18) || !gsort_ok(ch, m)) return false;
   static thread_local GPlan G;
   plan_gsort(ch, m, &G);
   if (G.K * 512 > m) return false;
-  return env == 2 || G.omid_hi - G.omid_lo >= 2;
+  if (env == 2 || G.omid_hi - G.omid_lo >= 2) return true;
+  static thread_local EPlan P;
+  return bucketed_supported(ch) && plan_entries(ch, m, &P) == TNB_OK && !P.stream;
 }
 
 int64_t gsort_workspace(const ChainDev& ch, int64_t m) {
