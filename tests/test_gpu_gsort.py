@@ -6,17 +6,20 @@ negative wrap and the lowest-bad-mode report, all through the C ABI."""
 import numpy as np
 import pytest
 
-torch = pytest.importorskip("torch")
-if not torch.cuda.is_available():  # pragma: no cover
-    pytest.skip("needs a GPU", allow_module_level=True)
-
-import paper_2206_11128_b200 as tb
 from oracle import tntz_oracle as O
-from paper_2206_11128_b200 import _native as N
-
-from .helpers import assert_close, facade
+from tests.helpers import assert_close, facade
 
 pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+tb = pytest.importorskip("paper_2206_11128_b200")
+from paper_2206_11128_b200 import _native as N  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
 
 
 def _plan(t, m, algo=N.ALGO_GSORT):
