@@ -579,7 +579,8 @@ def entries_secondary(args, dev, dist, ws, rank):
 def bench_entries_batched(dev, steps, warmup, B=16, m=1 << 20):
     """Batched-chain entries (core.py:425-429, 447-460): a batch of B cfg2-shape
     chains (N=10, I=32, r=32) on the same 2^20 tuples, output [m, B], on the
-    bucketed kernels (shared tile records, per-element tables / compute)."""
+    global-sort kernels when the merge allows (records sorted once, per-element
+    tables / compute), else the bucketed kernels (shared tile records)."""
     import torch
 
     import paper_2206_11128_b200 as tb
@@ -602,20 +603,33 @@ def bench_entries_batched(dev, steps, warmup, B=16, m=1 << 20):
         wsbuf[0] = C.launch_entries(p, idx, out, err, 0, wsbuf[0])
 
     ms = timed_steps(step, steps, warmup, torch.cuda.current_stream(dev), False, kernel_timing=True) / steps
-    kt = {k: N.timing_read(k) for k in ("entries_prep", "entries_sort", "entries_compute", "entries_tables")}
+    kt = {k: N.timing_read(k) for k in ("entries_prep", "entries_sort", "entries_compute", "entries_tables",
+                                        "entries_mid")}
     N.timing_enable(False)
     kms, kn = kt["entries_compute"]
     k_ms = kms / steps if kn else ms  # the B compute launches of one step
     fpk, fsrc = fp32_peak()
-    pipes = [{"bound": "tensor", "work": plan["tensor_flops"], "unit": "TFLOP/s", "peak": TC_TF32_PEAK,
-              "peak_source": "measured (profiles/peaks_r01.json, tools/peaks.cu mma.sync m16n8k8 tf32)",
-              "what": "split-TF32 mma.sync work of the sorted modes over the B compute launches"},
-             {"bound": "fp32", "work": plan["kernel_flops"] - plan["tensor_flops"] / 3, "unit": "TFLOP/s",
-              "peak": fpk, "peak_source": fsrc, "what": "FFMA work outside the tensor-core modes"}]
-    roof = pick_roof("entries_compute_kernel x B", k_ms, pipes,
+    gsort = plan["compute_kernel"] == 3
+    if gsort:
+        # global-sort kernel per element over records sorted once: per entry and
+        # element one row of each table (128 B each), the 16-byte record, a result
+        hb, hsrc = hbm_peak()
+        pipes = [{"bound": "hbm", "work": float(2 * 128 + 16 + 4) * m * B, "unit": "GB/s", "peak": hb,
+                  "peak_source": hsrc,
+                  "what": "gathered bytes the B compute launches request (two 128-byte table rows, record, result "
+                          "per entry and element); the step is dominated by the per-element table builds, which "
+                          "cannot overlap the persistent compute kernel (both fill the GPU)"}]
+    else:
+        pipes = [{"bound": "tensor", "work": plan["tensor_flops"], "unit": "TFLOP/s", "peak": TC_TF32_PEAK,
+                  "peak_source": "measured (profiles/peaks_r01.json, tools/peaks.cu mma.sync m16n8k8 tf32)",
+                  "what": "split-TF32 mma.sync work of the sorted modes over the B compute launches"},
+                 {"bound": "fp32", "work": plan["kernel_flops"] - plan["tensor_flops"] / 3, "unit": "TFLOP/s",
+                  "peak": fpk, "peak_source": fsrc, "what": "FFMA work outside the tensor-core modes"}]
+    roof = pick_roof(("entries_gsort_kernel" if gsort else "entries_compute_kernel") + " x B", k_ms, pipes,
                      extra={"kernel_share_of_step": k_ms / ms,
                             "plan": {k: plan[k] for k in ("algo", "n_virtual", "prefix_rows", "suffix_rows",
-                                                          "compute_kernel")}})
+                                                          "compute_kernel")},
+                            "tables_ms_per_step": (kt["entries_tables"][0] + kt["entries_mid"][0]) / steps})
     from oracle import tntz_oracle as O
 
     sel = np.linspace(0, m - 1, 4096).astype(np.int64)

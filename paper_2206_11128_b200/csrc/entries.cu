@@ -23,12 +23,18 @@ void bucketed_info(const ChainDev& ch, int64_t m, tnb_entries_info* info);
 double chain_entry_flops(const ChainDev& ch);
 bool two_table_ok(const ChainDev& ch, int64_t m);
 // entries_gsort.cuh: the global-sort tcgen05 path
-bool gsort_ok(const ChainDev& ch, int64_t m);
-bool gsort_auto(const ChainDev& ch, int64_t m);
-int64_t gsort_workspace(const ChainDev& ch, int64_t m);
-void gsort_info(const ChainDev& ch, int64_t m, tnb_entries_info* info);
+bool gsort_ok(const ChainDev& ch, int64_t m, bool batched);
+bool gsort_auto(const ChainDev& ch, int64_t m, bool batched);
+int64_t gsort_workspace(const ChainDev& ch, int64_t m, bool batched);
+void gsort_info(const ChainDev& ch, int64_t m, tnb_entries_info* info, bool batched);
 int launch_entries_gsort(const ChainDev& ch, const int64_t* idx, int64_t m, float* out, int32_t* err, void* ws,
                          int64_t ws_bytes, cudaStream_t st);
+int64_t gsort_table_bytes(const ChainDev& ch, int64_t m, bool batched);
+int gsort_tables(const ChainDev& ch, int64_t m, bool batched, void* table_ws, cudaStream_t st, int slot,
+                 cudaEvent_t* done);
+int gsort_compute(const ChainDev& ch, const int64_t* idx, int64_t m, float* out, int32_t* err, void* ws,
+                  int64_t ws_bytes, void* table_ws, cudaStream_t st, bool batched, bool reuse_records,
+                  cudaEvent_t tables);
 int64_t two_table_workspace(const ChainDev& ch, int64_t m);
 void two_table_info(const ChainDev& ch, int64_t m, tnb_entries_info* info);
 int launch_two_table(const ChainDev& ch, const int64_t* idx, int64_t m, float* out, int32_t* err, void* ws,
@@ -195,9 +201,62 @@ bool use_two_table(const tnb_chain* c, const ChainDev& ch, int64_t m, int algo) 
 
 // AUTO: large unbatched calls whose merged chain is first . dense . [diag] . last
 // run the global-sort tcgen05 path (TNB_ENTRIES_GSORT=0 turns that off)
+// (batched chains: one element at a time over the records sorted once)
 bool use_gsort(const ChainDev& ch, int64_t m, int algo) {
   if (algo == TNB_ALGO_GSORT) return true;
-  return algo == TNB_ALGO_AUTO && gsort_auto(ch, m);
+  if (algo != TNB_ALGO_AUTO) return false;
+  return ch.batch > 1 ? gsort_auto(element_chain(ch, 0), m, true) : gsort_auto(ch, m, false);
+}
+
+bool gsort_ok_any(const ChainDev& ch, int64_t m) {
+  return ch.batch > 1 ? gsort_ok(element_chain(ch, 0), m, true) : gsort_ok(ch, m, false);
+}
+
+// batched workspace: [element workspace (its head holds the tables of the even
+// elements)] [a second table region for the odd elements] [tmp: B x m results]
+int64_t gsort_tab2_offset(const ChainDev& ch, int64_t m) {
+  return (gsort_workspace(element_chain(ch, 0), m, true) + 255) & ~(int64_t)255;
+}
+
+int64_t gsort_tmp_offset(const ChainDev& ch, int64_t m) {
+  return gsort_tab2_offset(ch, m) + ((gsort_table_bytes(element_chain(ch, 0), m, true) + 255) & ~(int64_t)255);
+}
+
+int64_t gsort_workspace_any(const ChainDev& ch, int64_t m) {
+  if (ch.batch <= 1) return gsort_workspace(ch, m, false);
+  return gsort_tmp_offset(ch, m) + ch.batch * m * (int64_t)sizeof(float);
+}
+
+int launch_gsort_any(const ChainDev& ch, const int64_t* idx, int64_t m, float* out, int32_t* err, void* ws,
+                     int64_t ws_bytes, cudaStream_t st) {
+  if (ch.batch <= 1) return launch_entries_gsort(ch, idx, m, out, err, ws, ws_bytes, st);
+  const int64_t off2 = gsort_tab2_offset(ch, m), off = gsort_tmp_offset(ch, m);
+  const int64_t need = off + ch.batch * m * (int64_t)sizeof(float);
+  if (!ws || ws_bytes < need)
+    return set_error(TNB_EWORKSPACE, "batched global-sort entries needs %lld workspace bytes, got %lld",
+                     (long long)need, (long long)ws_bytes);
+  unsigned char* w = static_cast<unsigned char*>(ws);
+  float* tmp = reinterpret_cast<float*>(w + off);
+  // element b's tables live in region b & 1; element b + 1's are built (side
+  // stream) while element b's index passes / compute kernel run: the fork
+  // waits for what is queued on st, i.e. compute b - 1, the region's last reader
+  auto region = [&](int64_t b) { return (b & 1) ? w + off2 : w; };
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  int rc = gsort_tables(element_chain(ch, 0), m, true, region(0), st, 0, &ev[0]);
+  for (int64_t b = 0; b < ch.batch && !rc; ++b) {
+    if (b + 1 < ch.batch) rc = gsort_tables(element_chain(ch, b + 1), m, true, region(b + 1), st, (b + 1) & 1, &ev[(b + 1) & 1]);
+    if (rc) {
+      if (ev[b & 1]) cudaStreamWaitEvent(st, ev[b & 1], 0);
+      break;
+    }
+    rc = gsort_compute(element_chain(ch, b), idx, m, tmp + b * m, err, ws, off2, region(b), st, true, b > 0, ev[b & 1]);
+    if (rc && b + 1 < ch.batch && ev[(b + 1) & 1]) cudaStreamWaitEvent(st, ev[(b + 1) & 1], 0);
+  }
+  if (rc) return rc;
+  int64_t g = (m + 255) / 256;
+  if (g > (int64_t)num_sms() * 16) g = (int64_t)num_sms() * 16;
+  batch_transpose_kernel<<<(unsigned)(g < 1 ? 1 : g), 256, 0, st>>>(tmp, m, ch.batch, out);
+  return check_launch("batch_transpose");
 }
 
 bool use_bucketed(const ChainDev& ch, int64_t m, int algo) {
@@ -236,7 +295,7 @@ int64_t entries_workspace(const tnb_chain* c, int64_t m, int algo, int elt) {
   if (c->n_modes <= kMaxModes && (algo == TNB_ALGO_AUTO || algo == TNB_ALGO_BUCKETED || algo == TNB_ALGO_GSORT)) {
     static thread_local ChainDev ch;
     if (make_chain_dev(c, &ch, true) == TNB_OK && use_two_table(c, ch, m, algo)) return two_table_workspace(ch, m);
-    if (make_chain_dev(c, &ch, true) == TNB_OK && use_gsort(ch, m, algo)) return gsort_workspace(ch, m);
+    if (make_chain_dev(c, &ch, true) == TNB_OK && use_gsort(ch, m, algo)) return gsort_workspace_any(ch, m);
     if (make_chain_dev(c, &ch, true) == TNB_OK && use_bucketed(ch, m, algo) && bucketed_ok(ch))
       return ch.batch > 1 ? batched_tmp_offset(ch, m) + ch.batch * m * (int64_t)sizeof(float)
                           : bucketed_workspace(ch, m);
@@ -278,9 +337,14 @@ int entries_plan(const tnb_chain* c, int64_t m, int algo, tnb_entries_info* info
     return TNB_OK;
   }
   if (use_gsort(ch, m, algo)) {
-    if (!gsort_ok(ch, m)) return set_error(TNB_EINVAL, "the global-sort algorithm does not support this chain");
+    if (!gsort_ok_any(ch, m)) return set_error(TNB_EINVAL, "the global-sort algorithm does not support this chain");
     info->algo = TNB_ALGO_GSORT;
-    gsort_info(ch, m, info);
+    gsort_info(ch.batch > 1 ? element_chain(ch, 0) : ch, m, info, ch.batch > 1);
+    // batched: B elements, each its own tables and compute launch
+    info->kernel_flops *= (double)ch.batch;
+    info->tensor_flops *= (double)ch.batch;
+    info->table_flops *= (double)ch.batch;
+    info->table_launches *= (int32_t)ch.batch;
     return TNB_OK;
   }
   if (use_bucketed(ch, m, algo) && bucketed_ok(ch)) {
@@ -364,8 +428,8 @@ int launch_entries(const tnb_chain* c, const int64_t* idx, int64_t m, void* out_
   float* out = static_cast<float*>(out_v);
   if (use_two_table(c, ch, m, algo)) return launch_two_table(ch, idx, m, out, err, ws, ws_bytes, st);
   if (use_gsort(ch, m, algo)) {
-    if (!gsort_ok(ch, m)) return set_error(TNB_EINVAL, "the global-sort algorithm does not support this chain");
-    return launch_entries_gsort(ch, idx, m, out, err, ws, ws_bytes, st);
+    if (!gsort_ok_any(ch, m)) return set_error(TNB_EINVAL, "the global-sort algorithm does not support this chain");
+    return launch_gsort_any(ch, idx, m, out, err, ws, ws_bytes, st);
   }
   if ((algo == TNB_ALGO_AUTO && use_bucketed(ch, m, algo)) || use == TNB_ALGO_BUCKETED)
     return launch_bucketed_any(ch, idx, m, out, err, ws, ws_bytes, st);

@@ -2867,6 +2867,7 @@ void bucketed_info(const ChainDev& ch, int64_t m, tnb_entries_info* info) {
 struct SideStream {
   cudaStream_t s = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
+  cudaEvent_t join2 = nullptr;  // second join: batched global-sort calls build the next element's tables ahead
 };
 SideStream* side_stream() {
   static thread_local SideStream ss[64];
@@ -2884,7 +2885,8 @@ SideStream* side_stream() {
     cudaGetLastError();
     if (cudaStreamCreateWithPriority(&x.s, cudaStreamNonBlocking, greatest) != cudaSuccess ||
         cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.join2, cudaEventDisableTiming) != cudaSuccess) {
       cudaGetLastError();
       x = SideStream{};
       return nullptr;

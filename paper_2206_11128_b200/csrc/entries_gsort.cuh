@@ -125,9 +125,12 @@ bool plan_gsort_with(const ChainDev& ch, int64_t m, GPlan* G, int64_t wide_rows)
 // sorted step of one sample, and every absorbed mode removes that step from
 // all m samples (cfg2 chain at 2^22 tuples: P0123 . G45 . S6789, 0.45 ms,
 // instead of six modes on the state kernel, 1.0 ms).
-bool plan_gsort(const ChainDev& ch, int64_t m, GPlan* G) {
+// batched: the chain is one element of a batched chain -- the index passes
+// are shared by all elements, so tables of up to m rows still pay.
+bool plan_gsort(const ChainDev& ch, int64_t m, GPlan* G, bool batched = false) {
   if (plan_gsort_with(ch, m, G, 0) && G->K * 512 <= m) return true;
   if (plan_gsort_with(ch, m, G, m / 2) && G->K * 512 <= m) return true;
+  if (batched && plan_gsort_with(ch, m, G, m) && G->K * 512 <= m) return true;
   return plan_gsort_with(ch, m, G, 0);
 }
 
@@ -1209,9 +1212,9 @@ void gs_fill_prep(const ChainDev& ch, const GPlan& G, GsPrep* gp) {
 
 }  // namespace
 
-bool gsort_ok(const ChainDev& ch, int64_t m) {
+bool gsort_ok(const ChainDev& ch, int64_t m, bool batched) {
   static thread_local GPlan G;
-  if (!plan_gsort(ch, m, &G)) return false;
+  if (!plan_gsort(ch, m, &G, batched)) return false;
   // 16-byte row pieces: original boundary modes must be 16-byte aligned
   if (G.mp.kind[0] == kOrig && (reinterpret_cast<uintptr_t>(ch.m[0].s) & 15)) return false;
   if (G.mp.kind[G.mp.ng - 1] == kOrig && (reinterpret_cast<uintptr_t>(ch.m[ch.n - 1].s) & 15)) return false;
@@ -1227,25 +1230,25 @@ bool gsort_ok(const ChainDev& ch, int64_t m) {
 // 2^22 tuples: 0.34 against 0.47 ms; r = 20: against 1.08 ms).  A single
 // interior mode that fits the stream kernel stays there: its per-tile sort is
 // cheaper than the global one (cfg5: 4.6 against 5.5 ms at 2^26 tuples).
-bool gsort_auto(const ChainDev& ch, int64_t m) {
+bool gsort_auto(const ChainDev& ch, int64_t m, bool batched) {
   const int env = gsort_env();
-  if (!env || m < (1 << 18) || !gsort_ok(ch, m)) return false;
+  if (!env || m < (1 << 18) || !gsort_ok(ch, m, batched)) return false;
   static thread_local GPlan G;
-  plan_gsort(ch, m, &G);
+  plan_gsort(ch, m, &G, batched);
   if (G.K * 512 > m) return false;
   if (env == 2 || G.omid_hi - G.omid_lo >= 2) return true;
   static thread_local EPlan P;
   return bucketed_supported(ch) && plan_entries(ch, m, &P) == TNB_OK && !P.stream;
 }
 
-int64_t gsort_workspace(const ChainDev& ch, int64_t m) {
+int64_t gsort_workspace(const ChainDev& ch, int64_t m, bool batched) {
   static thread_local GPlan G;
-  return plan_gsort(ch, m, &G) ? G.total_bytes : 0;
+  return plan_gsort(ch, m, &G, batched) ? G.total_bytes : 0;
 }
 
-void gsort_info(const ChainDev& ch, int64_t m, tnb_entries_info* info) {
+void gsort_info(const ChainDev& ch, int64_t m, tnb_entries_info* info, bool batched) {
   static thread_local GPlan G;
-  if (!plan_gsort(ch, m, &G)) return;
+  if (!plan_gsort(ch, m, &G, batched)) return;
   const MergePlan& mp = G.mp;
   info->compute_kernel = 3;
   info->tile = kGsTile;
@@ -1285,44 +1288,78 @@ void gsort_info(const ChainDev& ch, int64_t m, tnb_entries_info* info) {
   info->table_flops = tf;
 }
 
-int launch_entries_gsort(const ChainDev& ch, const int64_t* idx, int64_t m, float* out, int32_t* err, void* ws,
-                         int64_t ws_bytes, cudaStream_t st) {
+// Bytes of the core-dependent head of the workspace: tables, levels of the
+// merged mode and its slice images.  Batched calls keep two of them and
+// build element b + 1's while element b's compute kernel runs.
+int64_t gsort_table_bytes(const ChainDev& ch, int64_t m, bool batched) {
   static thread_local GPlan G;
-  if (!plan_gsort(ch, m, &G)) return set_error(TNB_EINVAL, "the global-sort algorithm does not support this chain");
-  if (!ws || ws_bytes < G.total_bytes)
-    return set_error(TNB_EWORKSPACE, "global-sort entries needs %lld workspace bytes, got %lld",
-                     (long long)G.total_bytes, (long long)ws_bytes);
-  unsigned char* base = static_cast<unsigned char*>(ws);
-  const MergePlan& mp = G.mp;
+  return plan_gsort(ch, m, &G, batched) ? G.hist_off : 0;
+}
+
+// Phase 1 of a call: tables (first / last / diag) and the slice images of the
+// chain `ch` into table_ws.  They depend only on the cores: side stream
+// (forked from st: after everything queued there), concurrent with whatever
+// st runs next; *done = the event the compute kernel has to wait for (null
+// when they were built on st itself).  slot picks one of the two join events.
+int gsort_tables(const ChainDev& ch, int64_t m, bool batched, void* table_ws, cudaStream_t st, int slot,
+                 cudaEvent_t* done) {
+  static thread_local GPlan G;
+  if (!plan_gsort(ch, m, &G, batched))
+    return set_error(TNB_EINVAL, "the global-sort algorithm does not support this chain");
+  unsigned char* tb = static_cast<unsigned char*>(table_ws);
+  *done = nullptr;
   int rc;
-  // tables (first / last / diag) and the slice images depend only on the
-  // cores: side stream, concurrent with the index passes
-  cudaEvent_t tables = nullptr;
   SideStream* ss = table_stream_env() ? side_stream() : nullptr;
   if (ss) {
+    cudaEvent_t join = slot ? ss->join2 : ss->join;
     rc = check_cuda(cudaEventRecord(ss->fork, st), "fork");
     if (!rc) rc = check_cuda(cudaStreamWaitEvent(ss->s, ss->fork, 0), "fork wait");
     if (rc) return rc;
-    rc = build_tables(ch, mp, base, ss->s);
-    if (!rc) rc = gs_build_mid(ch, G, base, ss->s);
-    const int rj = check_cuda(cudaEventRecord(ss->join, ss->s), "join");
+    rc = build_tables(ch, G.mp, tb, ss->s);
+    if (!rc) rc = gs_build_mid(ch, G, tb, ss->s);
+    const int rj = check_cuda(cudaEventRecord(join, ss->s), "join");
     if (rc || rj) {
-      if (!rj) cudaStreamWaitEvent(st, ss->join, 0);
+      // join on the error path too: the caller frees the workspace the side stream may still be writing
+      if (!rj) cudaStreamWaitEvent(st, join, 0);
       else cudaStreamSynchronize(ss->s);
       return rc ? rc : rj;
     }
-    tables = ss->join;
-  } else {
-    rc = build_tables(ch, mp, base, st);
-    if (!rc) rc = gs_build_mid(ch, G, base, st);
-    if (rc) return rc;
+    *done = join;
+    return TNB_OK;
   }
+  rc = build_tables(ch, G.mp, tb, st);
+  if (!rc) rc = gs_build_mid(ch, G, tb, st);
+  return rc;
+}
+
+// Phase 2: the index passes (unless the records of a previous element of the
+// batch are reused) and the compute kernel, which waits for `tables`.
+// batched / reuse_records: the chain is one element of a batched chain; every
+// element shares the index matrix, so the sorted records, the tile map and the
+// hot-row votes of element 0 serve the others.
+int gsort_compute(const ChainDev& ch, const int64_t* idx, int64_t m, float* out, int32_t* err, void* ws,
+                  int64_t ws_bytes, void* table_ws, cudaStream_t st, bool batched, bool reuse_records,
+                  cudaEvent_t tables) {
+  static thread_local GPlan G;
+  auto fail0 = [&](int code) {
+    if (tables) cudaStreamWaitEvent(st, tables, 0);
+    return code;
+  };
+  if (!plan_gsort(ch, m, &G, batched))
+    return fail0(set_error(TNB_EINVAL, "the global-sort algorithm does not support this chain"));
+  if (!ws || ws_bytes < G.total_bytes)
+    return fail0(set_error(TNB_EWORKSPACE, "global-sort entries needs %lld workspace bytes, got %lld",
+                           (long long)G.total_bytes, (long long)ws_bytes));
+  unsigned char* base = static_cast<unsigned char*>(ws);
+  unsigned char* tb = static_cast<unsigned char*>(table_ws);
+  const MergePlan& mp = G.mp;
+  int rc;
   auto fail = [&](int code) {
     if (tables) cudaStreamWaitEvent(st, tables, 0);
     return code;
   };
   static thread_local ChainDev v;
-  virtual_chain(ch, mp, base, &v);
+  virtual_chain(ch, mp, tb, &v);
   uint32_t* hist = reinterpret_cast<uint32_t*>(base + G.hist_off);
   uint32_t* bstart = reinterpret_cast<uint32_t*>(base + G.bstart_off);
   uint32_t* tbase = reinterpret_cast<uint32_t*>(base + G.tbase_off);
@@ -1331,53 +1368,55 @@ int launch_entries_gsort(const ChainDev& ch, const int64_t* idx, int64_t m, floa
   uint4* recu = reinterpret_cast<uint4*>(base + G.recu_off);
   uint4* recs = reinterpret_cast<uint4*>(base + G.recs_off);
   const uint32_t K = (uint32_t)G.K;
-  rc = check_cuda(cudaMemsetAsync(hist, 0, (size_t)K * 4 + 16, st), "gsort hist");
-  if (rc) return fail(rc);
-  {
-    static thread_local GsPrep gp;
-    gs_fill_prep(ch, G, &gp);
-    const bool sh = K <= (uint32_t)kGsSmemK;
-    const bool stage = (ch.n & 1) == 0 && ch.n <= kGsStageN0 && (reinterpret_cast<uintptr_t>(idx) & 15) == 0;
-    const size_t sm = (sh ? (size_t)((K + 3) & ~3u) * 4 : 0) + (stage ? (size_t)kGsPrepThreads * (ch.n / 2) * 16 : 0);
-    auto pk = sh ? (stage ? gs_prep_kernel<true, true> : gs_prep_kernel<true, false>)
-                 : (stage ? gs_prep_kernel<false, true> : gs_prep_kernel<false, false>);
-    if (sm > 48 * 1024) {
-      rc = check_cuda(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "gsort prep smem");
-      if (rc) return fail(rc);
+  if (!reuse_records) {
+    rc = check_cuda(cudaMemsetAsync(hist, 0, (size_t)K * 4 + 16, st), "gsort hist");
+    if (rc) return fail(rc);
+    {
+      static thread_local GsPrep gp;
+      gs_fill_prep(ch, G, &gp);
+      const bool sh = K <= (uint32_t)kGsSmemK;
+      const bool stage = (ch.n & 1) == 0 && ch.n <= kGsStageN0 && (reinterpret_cast<uintptr_t>(idx) & 15) == 0;
+      const size_t sm = (sh ? (size_t)((K + 3) & ~3u) * 4 : 0) + (stage ? (size_t)kGsPrepThreads * (ch.n / 2) * 16 : 0);
+      auto pk = sh ? (stage ? gs_prep_kernel<true, true> : gs_prep_kernel<true, false>)
+                   : (stage ? gs_prep_kernel<false, true> : gs_prep_kernel<false, false>);
+      if (sm > 48 * 1024) {
+        rc = check_cuda(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "gsort prep smem");
+        if (rc) return fail(rc);
+      }
+      const int per_sm = sm > 56 * 1024 ? 2 : 4;
+      const int64_t g = std::min<int64_t>(ceil_div(m, kGsPrepThreads), (int64_t)num_sms() * per_sm);
+      KTimer kt("entries_prep", st);
+      pk<<<(unsigned)g, kGsPrepThreads, sm, st>>>(gp, idx, m, err, recu, hist);
     }
-    const int per_sm = sm > 56 * 1024 ? 2 : 4;
-    const int64_t g = std::min<int64_t>(ceil_div(m, kGsPrepThreads), (int64_t)num_sms() * per_sm);
-    KTimer kt("entries_prep", st);
-    pk<<<(unsigned)g, kGsPrepThreads, sm, st>>>(gp, idx, m, err, recu, hist);
-  }
-  rc = check_launch("gsort prep");
-  if (rc) return fail(rc);
-  gs_detect_hot_kernel<<<kGsHotBlocks, 32, 0, st>>>(recu, m, hist + K);
-  rc = check_launch("gsort detect hot");
-  if (rc) return fail(rc);
-  {
-    KTimer kt("entries_sort", st);
-    gs_scan_kernel<<<1, 1024, 0, st>>>(hist, K, bstart, tbase, cursor);
-    gs_tilemap_kernel<<<(unsigned)std::min<int64_t>(ceil_div(ceil_div(m, kGsTile) + K, 256), (int64_t)num_sms() * 8), 256, 0,
-                        st>>>(bstart, tbase, K, tinfo);
-    const size_t sm = (size_t)kGsScatThreads * kGsScatPer * 18 + (size_t)K * 8;
-    if (K > (uint32_t)kGsSmemK) {
-      const int64_t g = std::min<int64_t>(ceil_div(m, 256), (int64_t)num_sms() * 16);
-      gs_scatter_big_kernel<<<(unsigned)g, 256, 0, st>>>(recu, m, cursor, recs);
-    } else {
-      if (sm > 48 * 1024)
-        rc = check_cuda(cudaFuncSetAttribute(gs_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
-                        "gsort scatter smem");
-      if (!rc) {
-        const int64_t g =
-            std::min<int64_t>(ceil_div(m, (int64_t)kGsScatThreads * kGsScatPer), (int64_t)num_sms() * 8);
-        gs_scatter_kernel<<<(unsigned)g, kGsScatThreads, sm, st>>>(recu, m, K, cursor, recs);
+    rc = check_launch("gsort prep");
+    if (rc) return fail(rc);
+    gs_detect_hot_kernel<<<kGsHotBlocks, 32, 0, st>>>(recu, m, hist + K);
+    rc = check_launch("gsort detect hot");
+    if (rc) return fail(rc);
+    {
+      KTimer kt("entries_sort", st);
+      gs_scan_kernel<<<1, 1024, 0, st>>>(hist, K, bstart, tbase, cursor);
+      gs_tilemap_kernel<<<(unsigned)std::min<int64_t>(ceil_div(ceil_div(m, kGsTile) + K, 256), (int64_t)num_sms() * 8), 256, 0,
+                          st>>>(bstart, tbase, K, tinfo);
+      const size_t sm = (size_t)kGsScatThreads * kGsScatPer * 18 + (size_t)K * 8;
+      if (K > (uint32_t)kGsSmemK) {
+        const int64_t g = std::min<int64_t>(ceil_div(m, 256), (int64_t)num_sms() * 16);
+        gs_scatter_big_kernel<<<(unsigned)g, 256, 0, st>>>(recu, m, cursor, recs);
+      } else {
+        if (sm > 48 * 1024)
+          rc = check_cuda(cudaFuncSetAttribute(gs_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
+                          "gsort scatter smem");
+        if (!rc) {
+          const int64_t g =
+              std::min<int64_t>(ceil_div(m, (int64_t)kGsScatThreads * kGsScatPer), (int64_t)num_sms() * 8);
+          gs_scatter_kernel<<<(unsigned)g, kGsScatThreads, sm, st>>>(recu, m, K, cursor, recs);
+        }
       }
     }
+    if (rc) return fail(rc);
+    rc = check_launch("gsort sort");
+    if (rc) return fail(rc);
   }
-  if (rc) return fail(rc);
-  rc = check_launch("gsort sort");
-  if (rc) return fail(rc);
   if (tables) {
     rc = check_cuda(cudaStreamWaitEvent(st, tables, 0), "join tables");
     if (rc) return rc;
@@ -1386,7 +1425,7 @@ int launch_entries_gsort(const ChainDev& ch, const int64_t* idx, int64_t m, floa
   ga.P = v.m[0].s;
   ga.S = v.m[mp.ng - 1].s;
   ga.D = G.gdiag >= 0 ? v.m[G.gdiag].s : nullptr;
-  ga.img = base + G.img_off;
+  ga.img = tb + G.img_off;
   ga.recs = recs;
   ga.tinfo = tinfo;
   ga.tbase = tbase;
@@ -1438,4 +1477,15 @@ int launch_entries_gsort(const ChainDev& ch, const int64_t* idx, int64_t m, floa
   }
 #endif
   return check_launch("entries_gsort");
+}
+
+int launch_entries_gsort(const ChainDev& ch, const int64_t* idx, int64_t m, float* out, int32_t* err, void* ws,
+                         int64_t ws_bytes, cudaStream_t st) {
+  if (!ws || ws_bytes < gsort_workspace(ch, m, false))
+    return set_error(TNB_EWORKSPACE, "global-sort entries needs %lld workspace bytes, got %lld",
+                     (long long)gsort_workspace(ch, m, false), (long long)ws_bytes);
+  cudaEvent_t tables = nullptr;
+  const int rc = gsort_tables(ch, m, false, ws, st, 0, &tables);
+  if (rc) return rc;
+  return gsort_compute(ch, idx, m, out, err, ws, ws_bytes, ws, st, false, false, tables);
 }

@@ -194,3 +194,44 @@ def test_gsort_mid_size_uses_wider_tables():
     got = tb.entries(t, idx)
     sel = np.arange(0, m, 37)
     assert_close(got[torch.as_tensor(sel, device=got.device)], O.entries(o, idx[sel]))
+
+
+def test_gsort_batched_chains():
+    # batched chains (core.py:425-429, 447-460): the records are sorted once and
+    # every element runs its own tables and compute launch; each column equals
+    # the unbatched element bitwise
+    B, m = 3, 1 << 20
+    cores = O.random_tt((32,) * 8, 32, seed=31, batch_size=B, scale=32 ** -0.5)
+    t = tb.TnTensor([tb.ModeNode("tt", c, batched=True) for c in cores], B)
+    plan = _plan(t, m, N.ALGO_AUTO)
+    assert (plan["algo"], plan["compute_kernel"], plan["n_virtual"]) == (N.ALGO_GSORT, 3, 3), plan
+    idx = O.uniform_indices((32,) * 8, m, 9)
+    idx[5::13] -= 32
+    got = tb.entries(t, idx)
+    assert tuple(got.shape) == (m, B)
+    sel = np.arange(0, m, 257)
+    o = O.make_chain([("tt", c) for c in cores], B)
+    assert_close(got[torch.as_tensor(sel, device=got.device)], O.entries(o, idx[sel]))
+    for b in range(B):
+        tb_b = t.batch_element(b)
+        assert torch.equal(got[:, b], tb.entries(tb_b, idx))
+    bad = idx.copy()
+    bad[4242, 6] = 32
+    with pytest.raises(tb.ContractViolationError, match="mode 6"):
+        tb.entries(t, bad)
+
+
+def test_gsort_batched_cfg2_shape_plan():
+    # B cfg2-shape chains on 2^20 tuples (bench.py's batched line): tables of up
+    # to m rows pay because the index passes are shared -- P0123 . G45 . S6789
+    B, m = 2, 1 << 20
+    cores = O.random_tt((32,) * 10, 32, seed=33, batch_size=B, scale=32 ** -0.5)
+    t = tb.TnTensor([tb.ModeNode("tt", c, batched=True) for c in cores], B)
+    plan = _plan(t, m, N.ALGO_AUTO)
+    assert (plan["algo"], plan["n_virtual"], plan["prefix_rows"], plan["suffix_rows"]) == \
+        (N.ALGO_GSORT, 3, 1 << 20, 1 << 20), plan
+    idx = O.uniform_indices((32,) * 10, m, 10)
+    got = tb.entries(t, idx)
+    sel = np.arange(0, m, 509)
+    o = O.make_chain([("tt", c) for c in cores], B)
+    assert_close(got[torch.as_tensor(sel, device=got.device)], O.entries(o, idx[sel]))
