@@ -2060,10 +2060,10 @@ __global__ void __launch_bounds__(256) table_gemm_tc(ModeDev md, const float* __
 #pragma unroll
     for (int kt = 0; kt < KT; ++kt) {
       uint32_t ah[4], al[4];
-      split_tf32_fast(a0[8 * kt], ah[0], al[0]);
-      split_tf32_fast(a1[8 * kt], ah[1], al[1]);
-      split_tf32_fast(a0[8 * kt + 4], ah[2], al[2]);
-      split_tf32_fast(a1[8 * kt + 4], ah[3], al[3]);
+      split_tf32_step(a0[8 * kt], ah[0], al[0]);
+      split_tf32_step(a1[8 * kt], ah[1], al[1]);
+      split_tf32_step(a0[8 * kt + 4], ah[2], al[2]);
+      split_tf32_step(a1[8 * kt + 4], ah[3], al[3]);
 #pragma unroll
       for (int nt = 0; nt < NTL; ++nt) {
         mma_tf32(acc[nt], al, bh[kt][nt][0], bh[kt][nt][1]);
