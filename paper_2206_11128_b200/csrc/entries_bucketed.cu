@@ -1836,6 +1836,9 @@ __global__ void __launch_bounds__(NT, 1)
   }
 }
 
+// large dense table levels on tcgen05
+#include "table_tc5.cuh"
+
 // ---- prefix / suffix tables for mode merging -------------------------------
 // prefix step (rows in C order of the merged indices):
 //   out[(p*J + j)*rr + c] = sum_a in[p*rl + a] * G(j, a, c)      (dense)
@@ -2389,7 +2392,16 @@ void plan_merge(const ChainDev& ch, int64_t m, MergePlan* mp, int64_t wide_rows 
       if (gemm_level(ch.m[o])) scratch = std::max<int64_t>(scratch, bt);
       if (mp->kind[v] == kPrefix && tc_prefix_level(ch.m[o], rows))
         scratch = std::max<int64_t>(scratch, bt + tc_gemm_workspace(rows));
+      if (mp->kind[v] == kPrefix && t5_level_ok(ch.m[o], rows, false))
+        scratch = std::max<int64_t>(scratch, t5_image_bytes(ch.m[o]));
       if (mp->kind[v] == kPrefix) rows *= ch.m[o].J;
+    }
+    if (mp->kind[v] == kSuffix) {  // suffix levels run from the last mode down: input rows = prod J of the modes above
+      int64_t n = ch.m[hi - 1].J;
+      for (int o = hi - 2; o >= lo; --o) {
+        if (t5_level_ok(ch.m[o], n, true)) scratch = std::max<int64_t>(scratch, t5_image_bytes(ch.m[o]));
+        n *= ch.m[o].J;
+      }
     }
   }
   mp->gemm_off = off;
@@ -2458,6 +2470,10 @@ int build_tables(const ChainDev& ch, const MergePlan& mp, unsigned char* base, c
           int rc = gemm_f32(in, md.rl, 0, bt, (int64_t)md.J * md.rr, 0, out, (int64_t)md.J * md.rr, 0, rows,
                             (int64_t)md.J * md.rr, md.rl, 1, st);
           if (rc) return rc;
+        } else if (total > 0 && mp.kind[g] == kPrefix && t5_level_ok(ch.m[o], rows, false) &&
+                   (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
+          int rc = launch_t5_level<false>(ch.m[o], in, rows, out, base + mp.gemm_off, st);
+          if (rc) return rc;
         } else if (total > 0 && launch_table_tc<false>(ch.m[o], in, rows, out, st)) {
         } else if (total > 0 && table_gemm_ok(ch.m[o], false))
           table_gemm<false><<<dim3((unsigned)ceil_div(rows, kTRows), (unsigned)ceil_div(ch.m[o].J, kTZ)), 256, 0,
@@ -2490,6 +2506,9 @@ int build_tables(const ChainDev& ch, const MergePlan& mp, unsigned char* base, c
           core_transpose_kernel<true><<<grid((int64_t)md.J * md.rl * md.rr), 256, 0, st>>>(md, gt);
           int rc = gemm_f32(in, md.rr, 0, gt, md.rl, (int64_t)md.rr * md.rl, out, md.rl, n * md.rl, n, md.rl, md.rr,
                             md.J, st);
+          if (rc) return rc;
+        } else if ((int64_t)md.J * n * md.rl > 0 && t5_level_ok(md, n, true) && (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
+          int rc = launch_t5_level<true>(md, in, n, out, base + mp.gemm_off, st);
           if (rc) return rc;
         } else if ((int64_t)md.J * n * md.rl > 0 && launch_table_tc<true>(md, in, n, out, st)) {
         } else if ((int64_t)md.J * n * md.rl > 0 && table_gemm_ok(md, true)) {
