@@ -2405,7 +2405,8 @@ void plan_merge(const ChainDev& ch, int64_t m, MergePlan* mp, int64_t wide_rows 
     }
   }
   mp->gemm_off = off;
-  mp->gemm_bytes = (scratch + 255) & ~(int64_t)255;
+  // two halves: the prefix and the suffix chains may run concurrently (build_tables)
+  mp->gemm_bytes = 2 * ((scratch + 255) & ~(int64_t)255);
   off += mp->gemm_bytes;
   mp->table_bytes = off;
 }
@@ -2441,9 +2442,32 @@ void virtual_chain(const ChainDev& ch, const MergePlan& mp, unsigned char* base,
   v->rmax = rmax;
 }
 
-int build_tables(const ChainDev& ch, const MergePlan& mp, unsigned char* base, cudaStream_t st) {
+// st2 (with the events ea / eb): the suffix table's levels run there,
+// concurrently with the prefix / diagonal ones on st -- the two chains are
+// independent and their small first levels are launch-latency bound; st waits
+// for st2 before build_tables returns.
+int build_tables(const ChainDev& ch, const MergePlan& mp, unsigned char* base, cudaStream_t st,
+                 cudaStream_t st2 = nullptr, cudaEvent_t ea = nullptr, cudaEvent_t eb = nullptr) {
   if (!mp.table_bytes) return TNB_OK;
   KTimer kt("entries_tables", st);
+  bool forked = false;
+  if (st2 && ea && eb && mp.ng > 1 && mp.kind[mp.ng - 1] == kSuffix && mp.kind[0] == kPrefix) {
+    if (cudaEventRecord(ea, st) == cudaSuccess && cudaStreamWaitEvent(st2, ea, 0) == cudaSuccess) forked = true;
+    else cudaGetLastError();
+  }
+  cudaStream_t sfx = forked ? st2 : st;
+  struct Join {  // st waits for the suffix stream on every exit path
+    bool on;
+    cudaStream_t st, st2;
+    cudaEvent_t eb;
+    ~Join() {
+      if (on) {
+        if (cudaEventRecord(eb, st2) == cudaSuccess) cudaStreamWaitEvent(st, eb, 0);
+        else cudaStreamSynchronize(st2);
+      }
+    }
+  } join{forked, st, st2, eb};
+  unsigned char* scratch2 = base + mp.gemm_off + mp.gemm_bytes / 2;  // the suffix chain's half
   const int grid_cap = num_sms() * 8;
   auto grid = [&](int64_t total) { return (int)std::min<int64_t>(ceil_div(total, 256), grid_cap); };
   for (int g = 0; g < mp.ng; ++g) {
@@ -2502,24 +2526,24 @@ int build_tables(const ChainDev& ch, const MergePlan& mp, unsigned char* base, c
         float* out = reinterpret_cast<float*>(base + mp.lvl[o]);
         const ModeDev& md = ch.m[o];
         if ((int64_t)md.J * n * md.rl > 0 && gemm_level(md)) {
-          float* gt = reinterpret_cast<float*>(base + mp.gemm_off);
-          core_transpose_kernel<true><<<grid((int64_t)md.J * md.rl * md.rr), 256, 0, st>>>(md, gt);
+          float* gt = reinterpret_cast<float*>(scratch2);
+          core_transpose_kernel<true><<<grid((int64_t)md.J * md.rl * md.rr), 256, 0, sfx>>>(md, gt);
           int rc = gemm_f32(in, md.rr, 0, gt, md.rl, (int64_t)md.rr * md.rl, out, md.rl, n * md.rl, n, md.rl, md.rr,
-                            md.J, st);
+                            md.J, sfx);
           if (rc) return rc;
         } else if ((int64_t)md.J * n * md.rl > 0 && t5_level_ok(md, n, true) && (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
-          int rc = launch_t5_level<true>(md, in, n, out, base + mp.gemm_off, st);
+          int rc = launch_t5_level<true>(md, in, n, out, scratch2, sfx);
           if (rc) return rc;
-        } else if ((int64_t)md.J * n * md.rl > 0 && launch_table_tc<true>(md, in, n, out, st)) {
+        } else if ((int64_t)md.J * n * md.rl > 0 && launch_table_tc<true>(md, in, n, out, sfx)) {
         } else if ((int64_t)md.J * n * md.rl > 0 && table_gemm_ok(md, true)) {
-          table_gemm<true><<<dim3((unsigned)ceil_div(n, kTRows), (unsigned)ceil_div(md.J, kTZ)), 256, 0, st>>>(
+          table_gemm<true><<<dim3((unsigned)ceil_div(n, kTRows), (unsigned)ceil_div(md.J, kTZ)), 256, 0, sfx>>>(
               md, in, n, out);
         } else if ((int64_t)md.J * n * md.rl > 0 && (md.rl > 32 || md.rr > 32)) {
-          table_suffix_step_big<<<grid((int64_t)md.J * n * md.rl), 256, 0, st>>>(md, in, n, out);
+          table_suffix_step_big<<<grid((int64_t)md.J * n * md.rl), 256, 0, sfx>>>(md, in, n, out);
         } else if ((int64_t)md.J * n * md.rl > 0) {
           const int per = 256 / md.rl;
           const int gx = (int)std::min<int64_t>(ceil_div(n, per), std::max<int64_t>(1, grid_cap / md.J));
-          table_suffix_step<<<dim3(gx, md.J), 256, 0, st>>>(md, in, n, out);
+          table_suffix_step<<<dim3(gx, md.J), 256, 0, sfx>>>(md, in, n, out);
         }
         int rc = check_launch("table_suffix_step");
         if (rc) return rc;
@@ -2887,6 +2911,8 @@ struct SideStream {
   cudaStream_t s = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
   cudaEvent_t join2 = nullptr;  // second join: batched global-sort calls build the next element's tables ahead
+  cudaStream_t s2 = nullptr;    // the suffix table's levels, concurrent with the prefix's (build_tables)
+  cudaEvent_t ea = nullptr, eb = nullptr;
 };
 SideStream* side_stream() {
   static thread_local SideStream ss[64];
@@ -2905,7 +2931,10 @@ SideStream* side_stream() {
     if (cudaStreamCreateWithPriority(&x.s, cudaStreamNonBlocking, greatest) != cudaSuccess ||
         cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&x.join2, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&x.join2, cudaEventDisableTiming) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&x.s2, cudaStreamNonBlocking, greatest) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.ea, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.eb, cudaEventDisableTiming) != cudaSuccess) {
       cudaGetLastError();
       x = SideStream{};
       return nullptr;
@@ -2944,7 +2973,8 @@ int launch_entries_bucketed(const ChainDev& ch, const int64_t* idx, int64_t m, f
       rc = check_cuda(cudaEventRecord(ss->fork, st), "fork");
       if (!rc) rc = check_cuda(cudaStreamWaitEvent(ss->s, ss->fork, 0), "fork wait");
       if (rc) return rc;  // nothing was queued on the side stream
-      rc = build_tables(ch, mp, base, ss->s);
+      const bool conc = reuse_records || 4 * (mp.rows[0] + mp.rows[mp.ng - 1]) >= m;  // tables on the critical path
+      rc = build_tables(ch, mp, base, ss->s, conc ? ss->s2 : nullptr, ss->ea, ss->eb);
       const int rj = check_cuda(cudaEventRecord(ss->join, ss->s), "join");
       if (rc || rj) {
         // join on the error path too: the caller frees the workspace the

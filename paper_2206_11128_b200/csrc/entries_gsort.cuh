@@ -1315,7 +1315,11 @@ int gsort_tables(const ChainDev& ch, int64_t m, bool batched, void* table_ws, cu
     rc = check_cuda(cudaEventRecord(ss->fork, st), "fork");
     if (!rc) rc = check_cuda(cudaStreamWaitEvent(ss->s, ss->fork, 0), "fork wait");
     if (rc) return rc;
-    rc = build_tables(ch, G.mp, tb, ss->s);
+    // prefix and suffix chains side by side when the tables are on the critical path (batched elements
+    // after the first have no index passes to hide behind; else when the tables are large against m:
+    // next to the index passes of a 2^24-tuple call the second stream only takes bandwidth from them)
+    const bool conc = batched || 4 * (G.mp.rows[0] + G.mp.rows[G.mp.ng - 1]) >= m;
+    rc = build_tables(ch, G.mp, tb, ss->s, conc ? ss->s2 : nullptr, ss->ea, ss->eb);
     if (!rc) rc = gs_build_mid(ch, G, tb, ss->s);
     const int rj = check_cuda(cudaEventRecord(join, ss->s), "join");
     if (rc || rj) {
