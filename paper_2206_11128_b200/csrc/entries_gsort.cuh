@@ -121,16 +121,17 @@ int gsort_env() {
 bool plan_gsort_with(const ChainDev& ch, int64_t m, GPlan* G, int64_t wide_rows);
 // The merge the bucketed kernels use (wide tables of up to m / 8 rows), or --
 // when that leaves too many interior modes for one sort (K > m / 512) -- the
-// same with tables of up to m / 2 rows: a table row costs as much as one
-// sorted step of one sample, and every absorbed mode removes that step from
-// all m samples (cfg2 chain at 2^22 tuples: P0123 . G45 . S6789, 0.45 ms,
-// instead of six modes on the state kernel, 1.0 ms).
-// batched: the chain is one element of a batched chain -- the index passes
-// are shared by all elements, so tables of up to m rows still pay.
+// same with tables of up to m / 2, then m rows: a table row costs as much as
+// one sorted step of one sample, and every absorbed mode removes that step
+// from all m samples (cfg2 chain: P0123 . G45 . S6789 instead of six modes on
+// the state kernel -- 0.38 against 1.0 ms at 2^22 tuples, 0.18 against 0.30 ms
+// at 2^20).
+// (batched: the chain is one element of a batched chain; same plan.)
 bool plan_gsort(const ChainDev& ch, int64_t m, GPlan* G, bool batched = false) {
   if (plan_gsort_with(ch, m, G, 0) && G->K * 512 <= m) return true;
-  if (plan_gsort_with(ch, m, G, m / 2) && G->K * 512 <= m) return true;
-  if (batched && plan_gsort_with(ch, m, G, m) && G->K * 512 <= m) return true;
+  // (small ranks stay with the first plan: 40^9, r = 8 at 2^22 tuples ran 0.41 against 0.39 ms)
+  if (plan_gsort_with(ch, m, G, m / 2) && G->K * 512 <= m && G->r0 * G->r1 >= 256) return true;
+  if (plan_gsort_with(ch, m, G, m) && G->K * 512 <= m && G->r0 * G->r1 >= 256) return true;
   return plan_gsort_with(ch, m, G, 0);
 }
 
