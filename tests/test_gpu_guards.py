@@ -112,6 +112,25 @@ def test_guard_gsort_kernels(m, monkeypatch):
     assert_close(got.cpu().numpy()[sel], O.entries(O.make_chain([("tt", c) for c in cores]), idx[sel]))
 
 
+@pytest.mark.parametrize("t5", ["1", "0"])
+def test_guard_table_levels(t5, monkeypatch):
+    # table levels with 4913 input rows (ragged against the 128-row tiles), 17
+    # slices (groups of 8, 8, 1) and rank 12 (zero-padded k-steps): the tcgen05
+    # level kernel (TNB_TABLE_T5=1) and the mma.sync / SIMT kernels it replaces
+    monkeypatch.delenv("TNB_ENTRIES_GSORT", raising=False)
+    monkeypatch.setenv("TNB_TABLE_T5", t5)
+    cores = O.random_tt((17,) * 9, 12, seed=23, scale=12 ** -0.5)
+    t = tb.TnTensor([tb.ModeNode("tt", c) for c in cores])
+    m = 1 << 20
+    plan = N.entries_plan(t._packed().chain, m, N.ALGO_AUTO)
+    assert (plan["prefix_rows"], plan["suffix_rows"]) == (17 ** 4, 17 ** 4), plan
+    idx = O.uniform_indices(t.shape, m, 6)
+    idx[::9] -= 17
+    got = _entries_guarded(t, idx)
+    sel = np.arange(0, m, 331)
+    assert_close(got.cpu().numpy()[sel], O.entries(O.make_chain([("tt", c) for c in cores]), idx[sel]))
+
+
 def test_guard_cfg5_structure():
     nodes = O.cfg5_nodes(seed=2)
     t = tb.TnTensor([tb.ModeNode(k, c, f) for k, c, f in nodes])
