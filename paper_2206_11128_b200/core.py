@@ -28,6 +28,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import time
 from typing import Iterable, Optional, Sequence
 
 import numpy as np
@@ -546,6 +547,198 @@ class _Narrower:
         self.th.join()
 
 
+def _entries_pipelined_dyn(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: int,
+                           out_host: Optional[torch.Tensor], width: int, chunk: int) -> torch.Tensor:
+    """The self-balancing form of the pipelined host path (default when the
+    index codec applies).  The two host resources that feed the GPU -- the DMA
+    engine reading pinned int64 chunks and the host cores narrowing chunks to
+    int8/int16 -- each take the next chunk they can: the calling thread sends
+    RAW chunks from the front of the matrix whenever fewer than two raw copies
+    are queued, the narrowing thread works from the BACK, and finished
+    narrowed chunks are sent as they appear, until the two meet.  No chunk
+    waits for the slower resource and the split adapts to the machine (a
+    fixed raw fraction, TNB_E2E_DYNAMIC=0, has to be tuned per host: 0.35
+    here, 0.5 on a box with slower cores).  Chunks are independent, so their
+    order on the GPU does not matter; every launch sees `chunk` rows."""
+    import queue
+    import threading
+
+    dev = p.device
+    m = int(idx_host.shape[0])
+    n = t.ndim
+    nch = (m + chunk - 1) // chunk
+    out = torch.empty(nch * chunk, dtype=torch.float32, device=dev)
+    comp = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    back = torch.cuda.Stream(dev) if out_host is not None else None
+    errs = torch.empty(nch, dtype=torch.int32, device=dev)
+    bufs = [torch.empty((chunk, n), dtype=torch.int64, device=dev) for _ in range(2)]
+    done = [torch.cuda.Event() for _ in range(2)]  # compute finished with buffer b
+    ndt = torch.int8 if width == 1 else torch.int16
+    nstage = 4
+    stage = [torch.empty(chunk * n, dtype=ndt, pin_memory=True) for _ in range(nstage)]
+    dnar = [torch.empty(chunk * n, dtype=ndt, device=dev) for _ in range(2)]
+    lib = N.load()
+    # the enqueueing thread polls here and the CUDA driver has its own: leaving
+    # them a few hardware threads measured steadier than using all but one
+    nthreads = int(os.environ.get("TNB_E2E_THREADS", "0")) or max(1, lib.tnb_host_threads() * 3 // 4)
+    spans = [(c * chunk, min(m, (c + 1) * chunk)) for c in range(nch)]
+
+    lock = threading.Lock()
+    ends = [0, nch - 1]  # next raw chunk (front), next chunk to narrow (back)
+    ready: "queue.Queue" = queue.Queue()
+    free = [threading.Event() for _ in range(nstage)]  # staging buffer may be refilled ...
+    landed = [None] * nstage                              # ... once this H2D event has completed
+    for f in free:
+        f.set()
+    state = {"stop": False, "error": None, "wait_ms": 0.0, "narrow_ms": 0.0}
+
+    def claim(front: bool):
+        with lock:
+            if ends[0] > ends[1]:
+                return None
+            if front:
+                ends[0] += 1
+                return ends[0] - 1
+            ends[1] -= 1
+            return ends[1] + 1
+
+    def narrower():
+        k = 0
+        try:
+            while not state["stop"]:
+                sb = k % nstage
+                t0 = time.perf_counter()
+                free[sb].wait()
+                if state["stop"]:
+                    return
+                if landed[sb] is not None:
+                    landed[sb].synchronize()
+                c = claim(False)
+                if c is None:
+                    return
+                free[sb].clear()
+                lo, hi = spans[c]
+                cnt = (hi - lo) * n
+                t1 = time.perf_counter()
+                fits = N.narrow_indices(idx_host[lo:hi].view(-1), stage[sb][:cnt], width, nthreads)
+                t2 = time.perf_counter()
+                state["wait_ms"] += (t1 - t0) * 1e3
+                state["narrow_ms"] += (t2 - t1) * 1e3
+                ready.put((c, sb, fits))
+                k += 1
+        except BaseException as e:  # noqa: BLE001  (re-raised by the caller)
+            state["error"] = e
+        finally:
+            ready.put(None)  # the narrower is done
+
+    th = threading.Thread(target=narrower, daemon=True)
+    th.start()
+    ws = None
+    copy.wait_stream(comp)
+    h2d = 0
+    codecs = set()
+    raw_events: list = []
+    sent = 0
+    narrower_done = False
+
+    def dispatch(c, sb, narrow):
+        nonlocal ws, h2d, sent
+        lo, hi = spans[c]
+        b = sent & 1
+        buf = bufs[b]
+        cnt = (hi - lo) * n
+        with torch.cuda.stream(copy):
+            if sent >= 2:
+                copy.wait_event(done[b])
+            if narrow:
+                dnar[b][:cnt].copy_(stage[sb][:cnt], non_blocking=True)
+                h2d += cnt * width
+                codecs.add(f"int{8 * width}")
+            else:
+                buf[: hi - lo].copy_(idx_host[lo:hi], non_blocking=True)
+                h2d += cnt * 8
+                codecs.add("int64")
+            ev = torch.cuda.Event()
+            ev.record(copy)
+            if hi - lo < chunk:
+                buf[hi - lo:].zero_()
+            ready_ev = torch.cuda.Event()
+            ready_ev.record(copy)
+        if sb is not None:  # the staging buffer is free once this copy (if any) has read it
+            landed[sb] = ev if narrow else None
+            free[sb].set()
+        if not narrow:
+            raw_events.append(ev)
+        comp.wait_event(ready_ev)
+        buf.record_stream(comp)
+        if narrow:
+            dnar[b].record_stream(comp)
+            N.check(lib.tnb_widen_indices(dnar[b].data_ptr(), width, cnt, buf.data_ptr(), N.stream_ptr(dev)),
+                    "widen indices")
+        ws = launch_entries(p, buf, out[lo:lo + chunk], errs[c:c + 1], algo, ws)
+        done[b].record(comp)
+        if back is not None:
+            back.wait_event(done[b])
+            with torch.cuda.stream(back):
+                out_host[lo:hi].copy_(out[lo:hi], non_blocking=True)
+        sent += 1
+
+    try:
+        while sent < nch:
+            item = None
+            if not narrower_done:
+                try:
+                    item = ready.get_nowait()
+                except queue.Empty:
+                    item = False
+                if item is None:
+                    narrower_done = True
+                    if state["error"] is not None:
+                        raise state["error"]
+                    continue
+            if item:
+                c, sb, fits = item
+                dispatch(c, sb, fits)  # a chunk with a value outside the narrow range crosses as int64
+                continue
+            raw_events[:] = [e for e in raw_events if not e.query()]
+            if len(raw_events) < 2:
+                c = claim(True)
+                if c is not None:
+                    dispatch(c, None, False)
+                    continue
+                if narrower_done:
+                    break  # nothing left to claim: every chunk was dispatched
+            if not narrower_done:
+                try:
+                    item = ready.get(timeout=0.0002)
+                except queue.Empty:
+                    continue
+                if item is None:
+                    narrower_done = True
+                    if state["error"] is not None:
+                        raise state["error"]
+                else:
+                    dispatch(*item)
+            else:
+                time.sleep(0.0001)
+    finally:
+        state["stop"] = True
+        for f in free:
+            f.set()
+        th.join()
+    code = int(errs.min().item())
+    if back is not None:
+        back.synchronize()
+    last_transfer.clear()
+    last_transfer.update(h2d_bytes=h2d, d2h_bytes=m * 4 if back is not None else 0,
+                         codec="+".join(sorted(codecs)), narrow_ms=round(state["narrow_ms"], 2),
+                         narrow_wait_ms=round(state["wait_ms"], 2))
+    if code < t.ndim:
+        raise ContractViolationError(f"index out of bounds on mode {code}")
+    return out_host if out_host is not None else out[:m]
+
+
 def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: int,
                        out_host: Optional[torch.Tensor] = None) -> torch.Tensor:
     """entries() for a large PINNED int64 host index matrix: chunked
@@ -568,6 +761,9 @@ def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: in
     n = t.ndim
     chunk = 1 << int(os.environ.get("TNB_E2E_CHUNK_LOG2", "0")) if os.environ.get("TNB_E2E_CHUNK_LOG2") \
         else _CHUNK_ROWS
+    width = _codec_width(t)
+    if width and os.environ.get("TNB_E2E_DYNAMIC", "1") != "0" and "TNB_E2E_RAW_FRAC" not in os.environ:
+        return _entries_pipelined_dyn(t, p, idx_host, algo, out_host, width, chunk)
     nch = (m + chunk - 1) // chunk
     # every launch sees exactly `chunk` rows (the short last chunk is padded
     # with index 0), so all chunks run the same plan
@@ -578,7 +774,6 @@ def _entries_pipelined(t: TnTensor, p: _Packed, idx_host: torch.Tensor, algo: in
     bufs = [torch.empty((chunk, n), dtype=torch.int64, device=dev) for _ in range(2)]
     done = [torch.cuda.Event() for _ in range(2)]  # compute finished with buffer b
     back = torch.cuda.Stream(dev) if out_host is not None else None
-    width = _codec_width(t)
     raw_frac = float(os.environ.get("TNB_E2E_RAW_FRAC", "0.35")) if width else 1.0
 
     def raw_chunk(c):

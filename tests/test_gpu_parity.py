@@ -264,16 +264,19 @@ def test_dot_rank16_fast_and_generic(generic, monkeypatch):
     assert abs(tb.norm(t1) - O.norm(o1)) <= 1e-5 * O.norm(o1)
 
 
-@pytest.mark.parametrize("codec,raw_frac", [("1", "0.35"), ("1", "0"), ("0", "0.35")])
+@pytest.mark.parametrize("codec,raw_frac", [("1", None), ("1", "0.35"), ("1", "0"), ("0", "0.35")])
 def test_pipelined_host_indices_match_device_path(codec, raw_frac, monkeypatch):
     # a large pinned int64 host matrix takes the chunked copy/compute pipeline
     # (with and without the int8 index transport codec, some chunks raw or all
     # narrowed); per-sample results do not depend on chunking, tiling or the
-    # codec (bitwise equal)
+    # codec (bitwise equal); raw_frac None = the self-balancing chunk order
     from paper_2206_11128_b200 import core as C
 
     monkeypatch.setenv("TNB_E2E_CODEC", codec)
-    monkeypatch.setenv("TNB_E2E_RAW_FRAC", raw_frac)
+    if raw_frac is None:  # the self-balancing pipeline (the default)
+        monkeypatch.delenv("TNB_E2E_RAW_FRAC", raising=False)
+    else:
+        monkeypatch.setenv("TNB_E2E_RAW_FRAC", raw_frac)
     cores = O.random_tt((32,) * 6, 16, seed=11, scale=0.25)
     t = facade([("tt", c, None) for c in cores])
     assert C._codec_width(t) == (1 if codec == "1" else 0)

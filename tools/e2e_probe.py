@@ -56,3 +56,14 @@ for codec, frac in (("0", "1"), ("1", "0"), ("1", "0.3"), ("1", "0.4"), ("1", "0
     os.environ["TNB_E2E_RAW_FRAC"] = frac
     print("codec=%s raw_frac=%s entries(pinned host idx, out=pinned): %.2f ms %s" % (
         codec, frac, wall(lambda: tb.entries(t, idx_host, out=pin_out)), C.last_transfer), flush=True)
+os.environ["TNB_E2E_CODEC"] = "1"
+os.environ.pop("TNB_E2E_RAW_FRAC", None)
+for rep in range(3):
+    print("codec=1 dynamic entries(pinned host idx, out=pinned): %.2f ms %s" % (
+        wall(lambda: tb.entries(t, idx_host, out=pin_out)), C.last_transfer), flush=True)
+got = pin_out.clone()
+os.environ["TNB_E2E_RAW_FRAC"] = "0.35"
+tb.entries(t, idx_host, out=pin_out)
+torch.cuda.synchronize()
+assert torch.equal(pin_out, got), "the self-balancing pipeline differs from the static one"
+print("dynamic == static pipeline (bitwise)")
