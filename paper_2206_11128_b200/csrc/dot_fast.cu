@@ -123,13 +123,20 @@ __device__ __forceinline__ void sts128x2(uint32_t a, uint64_t p0, uint64_t p1) {
 //      measured cfg4 error equals the fully rounded split's.
 //   0: hi = rna(x), lo = rna(x - hi).
 #ifndef TNB_DOT_TRUNC_SPLIT
-#define TNB_DOT_TRUNC_SPLIT 2  /* 1: cfg4 dot 1.32 ms but relFro 1.06e-5, over the 1e-5 bar;
-                                  2: 1.54 ms at relFro 2.5e-6 (= the fully rounded split's) */
+#define TNB_DOT_TRUNC_SPLIT 3  /* 1: cfg4 dot 1.32 ms but relFro 1.06e-5, over the 1e-5 bar;
+                                  2: 1.43 ms at relFro 2.5e-6 (= the fully rounded split's);
+                                  3: the same bits as 2 in 3 instead of 5 instructions: 1.27 ms */
 #endif
 __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
 #if TNB_DOT_TRUNC_SPLIT == 1
   hi = __float_as_uint(x);
   lo = __float_as_uint(x - __uint_as_float(hi & 0xffffe000u));
+#elif TNB_DOT_TRUNC_SPLIT == 3
+  // as 2, with the round-to-nearest-away done on the bit pattern: cvt.rna
+  // compiles to add / NaN test / select / mask, this to add / mask (the same
+  // hi for every finite x; a NaN still reaches the products through lo)
+  hi = (__float_as_uint(x) + 0x1000u) & 0xffffe000u;
+  lo = __float_as_uint(x - __uint_as_float(hi));
 #elif TNB_DOT_TRUNC_SPLIT == 2
   // hi rounded, lo = x - hi exact but left for the tensor core to truncate
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
@@ -138,6 +145,41 @@ __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) 
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
   const float r = x - __uint_as_float(hi);
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo) : "f"(r));
+#endif
+}
+// TNB_DOT_PAIR: two values per split with one packed fp32x2 subtract (FADD2)
+// for the two lo parts, and packed adds for the running partial
+#ifndef TNB_DOT_PAIR
+#define TNB_DOT_PAIR 1
+#endif
+__device__ __forceinline__ void split2_tf32(float x0, float x1, uint32_t& h0, uint32_t& h1, uint32_t& l0,
+                                            uint32_t& l1) {
+#if TNB_DOT_PAIR && TNB_DOT_TRUNC_SPLIT == 3
+  h0 = (__float_as_uint(x0) + 0x1000u) & 0xffffe000u;
+  h1 = (__float_as_uint(x1) + 0x1000u) & 0xffffe000u;
+  uint64_t X, H, L;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(X) : "f"(x0), "f"(x1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(H) : "r"(h0), "r"(h1));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(L) : "l"(X), "l"(H));
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(l0), "=r"(l1) : "l"(L));
+#else
+  split_tf32(x0, h0, l0);
+  split_tf32(x1, h1, l1);
+#endif
+}
+__device__ __forceinline__ void add4(float (&d)[4], const float (&z)[4]) {
+#if TNB_DOT_PAIR
+#pragma unroll
+  for (int i = 0; i < 4; i += 2) {
+    uint64_t D, Z;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(D) : "f"(d[i]), "f"(d[i + 1]));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(Z) : "f"(z[i]), "f"(z[i + 1]));
+    asm("add.rn.f32x2 %0, %0, %1;" : "+l"(D) : "l"(Z));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(d[i]), "=f"(d[i + 1]) : "l"(D));
+  }
+#else
+#pragma unroll
+  for (int i = 0; i < 4; ++i) d[i] += z[i];
 #endif
 }
 __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
@@ -156,14 +198,38 @@ __device__ __forceinline__ void mma3s(float (&d)[4], const uint32_t (&ah)[4], co
 __device__ __forceinline__ void mma3(float (&d)[4], const uint32_t (&ah)[4], const uint32_t (&al)[4], float b0,
                                      float b1) {
   uint32_t h0, l0, h1, l1;
-  split_tf32(b0, h0, l0);
-  split_tf32(b1, h1, l1);
+  split2_tf32(b0, b1, h0, h1, l0, l1);
 #if TNB_DOT_4TERM
   mma_tf32(d, al, l0, l1);
 #endif
   mma_tf32(d, al, h0, h1);
   mma_tf32(d, ah, l0, l1);
   mma_tf32(d, ah, h0, h1);
+}
+
+// TNB_DOT_ILV: issue order of a slice's MMAs.  0: each accumulator's three
+// split products back to back (a dependent chain of 6 per accumulator);
+// 1: the two n-tiles' chains interleaved; 2: also one accumulator per k-chunk
+// (four chains of 3, joined with fp32 adds).
+#ifndef TNB_DOT_ILV
+#define TNB_DOT_ILV 0
+#endif
+__device__ __forceinline__ void mma3s_pair(float (&d0)[4], float (&d1)[4], const uint32_t (&ah)[4],
+                                           const uint32_t (&al)[4], const uint32_t (&Bh)[4],
+                                           const uint32_t (&Bl)[4]) {
+  mma_tf32(d0, al, Bh[0], Bh[1]);
+  mma_tf32(d1, al, Bh[2], Bh[3]);
+  mma_tf32(d0, ah, Bl[0], Bl[1]);
+  mma_tf32(d1, ah, Bl[2], Bl[3]);
+  mma_tf32(d0, ah, Bh[0], Bh[1]);
+  mma_tf32(d1, ah, Bh[2], Bh[3]);
+}
+__device__ __forceinline__ void mma3_pair(float (&d0)[4], float (&d1)[4], const uint32_t (&ah)[4],
+                                          const uint32_t (&al)[4], const float (&y)[4]) {
+  uint32_t Bh[4], Bl[4];
+#pragma unroll
+  for (int i = 0; i < 4; i += 2) split2_tf32(y[i], y[i + 1], Bh[i], Bh[i + 1], Bl[i], Bl[i + 1]);
+  mma3s_pair(d0, d1, ah, al, Bh, Bl);
 }
 
 // One interior slice on tensor cores.  Fragments (m16n8k8 tf32, g = lane/4,
@@ -176,10 +242,8 @@ __device__ __forceinline__ void mma3(float (&d)[4], const uint32_t (&ah)[4], con
 __device__ __forceinline__ void slice_afrag(const float* S, int kc, int g, int t, uint32_t (&ah)[4],
                                             uint32_t (&al)[4]) {
   const float* r0 = S + (8 * kc + 2 * t) * 16;
-  split_tf32(r0[g], ah[0], al[0]);
-  split_tf32(r0[g + 8], ah[1], al[1]);
-  split_tf32(r0[16 + g], ah[2], al[2]);
-  split_tf32(r0[16 + g + 8], ah[3], al[3]);
+  split2_tf32(r0[g], r0[g + 8], ah[0], ah[1], al[0], al[1]);
+  split2_tf32(r0[16 + g], r0[16 + g + 8], ah[2], ah[3], al[2], al[3]);
 }
 // SAME (norm: A_j == B_j): the slice's split fragments serve both products
 template <bool SAME>
@@ -187,17 +251,58 @@ __device__ __forceinline__ void slice_mma(const float* Aj, const float* Bj, cons
                                           const uint32_t (&Ml)[2][4], float (&Mw)[2][4], int g, int t) {
   float Y[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
   uint32_t sh[SAME ? 2 : 1][4], sl[SAME ? 2 : 1][4];  // B_j's fragments, kept for A_j^T Y when SAME
+#if TNB_DOT_ILV == 2
+  {
+    float Y2[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    uint32_t th[2][4], tl[2][4];
+    slice_afrag(Bj, 0, g, t, th[0], tl[0]);
+    slice_afrag(Bj, 1, g, t, th[1], tl[1]);
+    mma_tf32(Y[0], tl[0], Mh[0][0], Mh[0][1]);
+    mma_tf32(Y[1], tl[0], Mh[0][2], Mh[0][3]);
+    mma_tf32(Y2[0], tl[1], Mh[1][0], Mh[1][1]);
+    mma_tf32(Y2[1], tl[1], Mh[1][2], Mh[1][3]);
+    mma_tf32(Y[0], th[0], Ml[0][0], Ml[0][1]);
+    mma_tf32(Y[1], th[0], Ml[0][2], Ml[0][3]);
+    mma_tf32(Y2[0], th[1], Ml[1][0], Ml[1][1]);
+    mma_tf32(Y2[1], th[1], Ml[1][2], Ml[1][3]);
+    mma_tf32(Y[0], th[0], Mh[0][0], Mh[0][1]);
+    mma_tf32(Y[1], th[0], Mh[0][2], Mh[0][3]);
+    mma_tf32(Y2[0], th[1], Mh[1][0], Mh[1][1]);
+    mma_tf32(Y2[1], th[1], Mh[1][2], Mh[1][3]);
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) Y[nt][i] += Y2[nt][i];
+    if constexpr (SAME) {
+#pragma unroll
+      for (int kc = 0; kc < 2; ++kc)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          sh[SAME ? kc : 0][i] = th[kc][i];
+          sl[SAME ? kc : 0][i] = tl[kc][i];
+        }
+    }
+  }
+#else
 #pragma unroll
   for (int kc = 0; kc < 2; ++kc) {
     const int ks = SAME ? kc : 0;
     slice_afrag(Bj, kc, g, t, sh[ks], sl[ks]);
+#if TNB_DOT_ILV == 1
+    mma3s_pair(Y[0], Y[1], sh[ks], sl[ks], Mh[kc], Ml[kc]);
+#else
     mma3s(Y[0], sh[ks], sl[ks], Mh[kc][0], Mh[kc][1], Ml[kc][0], Ml[kc][1]);
     mma3s(Y[1], sh[ks], sl[ks], Mh[kc][2], Mh[kc][3], Ml[kc][2], Ml[kc][3]);
+#endif
   }
+#endif
   // this slice's A_j^T Y starts from zero and joins the running partial
   // with round-to-nearest FADDs: the MMA accumulator only ever sums the 6
   // products of one slice
   float Z[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#if TNB_DOT_ILV == 2
+  float Z2[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#endif
 #pragma unroll
   for (int kc = 0; kc < 2; ++kc) {
     uint32_t ah[4], al[4];
@@ -210,13 +315,34 @@ __device__ __forceinline__ void slice_mma(const float* Aj, const float* Bj, cons
     } else {
       slice_afrag(Aj, kc, g, t, ah, al);
     }
+#if TNB_DOT_ILV == 2
+    if (kc == 1) {  // the second k-chunk has its own accumulators (joined below)
+      mma3_pair(Z2[0], Z2[1], ah, al, Y[kc]);
+      continue;
+    }
+#endif
+#if TNB_DOT_ILV >= 1
+    mma3_pair(Z[0], Z[1], ah, al, Y[kc]);
+#else
     mma3(Z[0], ah, al, Y[kc][0], Y[kc][1]);
     mma3(Z[1], ah, al, Y[kc][2], Y[kc][3]);
+#endif
   }
 #pragma unroll
   for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-    for (int i = 0; i < 4; ++i) Mw[nt][i] += Z[nt][i];
+    for (int i = 0; i < 4; ++i) {
+#if TNB_DOT_ILV == 2
+      Z[nt][i] += Z2[nt][i];
+#endif
+#if !TNB_DOT_PAIR
+      Mw[nt][i] += Z[nt][i];
+#endif
+    }
+#if TNB_DOT_PAIR
+  add4(Mw[0], Z[0]);
+  add4(Mw[1], Z[1]);
+#endif
 }
 
 struct DotArgs {
@@ -321,6 +447,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) dot_r16_kernel(const __g
         const float* A = stA + s * CH * R * R;
         const float* Bm = same ? A : stB + s * CH * R * R;
         const int nj = min(CH, J - c * CH);
+        if (MMA && !first && !last) {  // interior slices on tensor cores (the loop the kernel lives in)
+#pragma unroll 1
+          for (int jj = warp; jj < nj; jj += kWarps)
+            slice_mma<SAME>(A + jj * R * R, Bm + jj * R * R, Mh, Ml, Mw, fg, ft);
+        } else
         for (int jj = warp; jj < nj; jj += kWarps) {
           if (first) {  // 1 x R slices: M' += A_j^T B_j
             const uint32_t a_row = su32(A + jj * R), b_row = su32(Bm + jj * R);
@@ -349,7 +480,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) dot_r16_kernel(const __g
             lastacc = fmaf(a0, y0, lastacc);
             lastacc = fmaf(a1, y1, lastacc);
           } else if (MMA) {
-            slice_mma<SAME>(A + jj * R * R, Bm + jj * R * R, Mh, Ml, Mw, fg, ft);
+            // (taken by the loop above)
           } else if (jj < kWarps) {
             // two slices per warp (jj, jj + kWarps): 8 independent FFMA2 chains
             const int j2 = jj + kWarps;

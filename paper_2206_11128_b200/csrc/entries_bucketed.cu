@@ -209,17 +209,19 @@ __device__ __forceinline__ void sts32(uint32_t a, float x) {
 
 // split-TF32 on mma.sync m16n8k8: x = hi + lo, both rounded to tf32; the
 // three products lo*hi + hi*lo + hi*hi keep fp32-level accuracy
+// (rna on the bit pattern: cvt.rna.tf32.f32's value for every finite x in
+// add + mask instead of add / NaN test / select / mask)
+__device__ __forceinline__ uint32_t rna_tf32(float x) { return (__float_as_uint(x) + 0x1000u) & 0xffffe000u; }
 __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
-  const float r = x - __uint_as_float(hi);
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo) : "f"(r));
+  hi = rna_tf32(x);
+  lo = rna_tf32(x - __uint_as_float(hi));
 }
 // the per-step A-fragment split: lo = x - rna(x) exact, passed unrounded (the
 // tensor core truncates it; the dropped bits are below 2^-21 |x|) -- one
 // instruction less than split_tf32
 __device__ __forceinline__ void split_tf32_fast(float x, uint32_t& hi, uint32_t& lo) {
 #if TNB_FAST_SPLIT
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
+  hi = rna_tf32(x);
   lo = __float_as_uint(x - __uint_as_float(hi));
 #else
   split_tf32(x, hi, lo);
