@@ -53,7 +53,10 @@ constexpr int kWarps = TNB_DOT_WARPS;
 #endif
 constexpr int kCompute = kWarps * 32;                           // compute threads
 constexpr int kThreads = kCompute + (TNB_DOT_PRODUCER ? 32 : 0);
-constexpr int kCtasPerSm = 16 / kWarps;
+#ifndef TNB_DOT_CTAS
+#define TNB_DOT_CTAS (16 / TNB_DOT_WARPS)
+#endif
+constexpr int kCtasPerSm = TNB_DOT_CTAS;
 constexpr int R = 16;
 constexpr int CH = TNB_DOT_CH;         // slices per chunk
 static_assert(CH == 2 * kWarps, "the FFMA path takes two slices per warp and chunk");
@@ -80,6 +83,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "@!P1 bra WAIT_%=;\n\t}" ::"r"(su32(b)),
       "r"(parity)
       : "memory");
+}
+// the producer lane's wait for a free stage: try_wait with a suspend-time
+// hint, so the lane sleeps in the barrier unit instead of re-issuing the test
+// every ~30 cycles beside the compute warps of its scheduler
+#ifndef TNB_DOT_PSUSP
+#define TNB_DOT_PSUSP 1
+#endif
+__device__ __forceinline__ void mbar_wait_suspend(uint64_t* b, uint32_t parity) {
+#if TNB_DOT_PSUSP
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(su32(b)),
+      "r"(parity), "r"(20000u)
+      : "memory");
+#else
+  mbar_wait(b, parity);
+#endif
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -210,9 +231,10 @@ __device__ __forceinline__ void mma3(float (&d)[4], const uint32_t (&ah)[4], con
 // TNB_DOT_ILV: issue order of a slice's MMAs.  0: each accumulator's three
 // split products back to back (a dependent chain of 6 per accumulator);
 // 1: the two n-tiles' chains interleaved; 2: also one accumulator per k-chunk
-// (four chains of 3, joined with fp32 adds).
+// (four chains of 3, joined with fp32 adds: half the error, 4-7% slower).
+// Two slices per warp at a time (four chains) measured no faster than 1.
 #ifndef TNB_DOT_ILV
-#define TNB_DOT_ILV 0
+#define TNB_DOT_ILV 1
 #endif
 __device__ __forceinline__ void mma3s_pair(float (&d0)[4], float (&d1)[4], const uint32_t (&ah)[4],
                                            const uint32_t (&al)[4], const uint32_t (&Bh)[4],
@@ -397,7 +419,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) dot_r16_kernel(const __g
   auto produce_one = [&]() {
     if (pw.e >= B) return;
     const int s = p_it % kStages;
-    mbar_wait(&empty[s], ((p_it / kStages) & 1) ^ 1);
+    mbar_wait_suspend(&empty[s], ((p_it / kStages) & 1) ^ 1);
     const ModeDev& ma = args.a.m[pw.k];
     const ModeDev& mb = args.b.m[pw.k];
     const int j0 = pw.c * CH, nj = min(CH, J - j0);
