@@ -81,6 +81,15 @@ static_assert(!TNB_FULL_BULK || TNB_FULL_NB3, "TNB_FULL_BULK needs TNB_FULL_NB3"
 #define TNB_FULL_EPI8 0
 #endif
 static_assert(!(TNB_FULL_EPI8 && !TNB_FULL_NB3), "TNB_FULL_EPI8 needs TNB_FULL_NB3");
+// TNB_FULL_ALT: two epilogue warpgroups (warps 4-7 and the A-loader warps
+// 8-11) take ALTERNATE 128 x 128 sub-tiles: while one group is still storing
+// its sub-tile, the other waits for the next MMA, drains the accumulator and
+// starts storing, so the store stream has no gap at every tcgen05.ld.  Still
+// one TMEM accumulator; acc_full / acc_empty [g] belong to group g.
+#ifndef TNB_FULL_ALT
+#define TNB_FULL_ALT 0
+#endif
+static_assert(!(TNB_FULL_ALT && (!TNB_FULL_NB3 || TNB_FULL_EPI8)), "TNB_FULL_ALT needs TNB_FULL_NB3 without EPI8");
 constexpr int kTmaBox = 32;                                   // rows and columns per TMA store
 constexpr int kTmaBufBytes = kTmaBox * kTmaBox * 4;           // 4 KB
 constexpr int kTmaEpiBytes = TNB_FULL_TMA ? 4 * 2 * kTmaBufBytes : 0;
@@ -317,8 +326,13 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
       tc_fence_after();
       const uint32_t bhi = sL0 + s * kTileBytes, blo = bhi + kTileBytes / 2;
       for (int nb = 0; nb < NB; ++nb) {
+#if TNB_FULL_ALT
+        const int cbuf = 0;  // one accumulator; the barriers alternate with the epilogue groups
+        if (s_it > 0) mbar_wait(&acc_empty[(s_it - 1) & 1], ((s_it - 1) >> 1) & 1);
+#else
         const int cbuf = s_it % kAccBufs;
         mbar_wait(&acc_empty[cbuf], ((s_it / kAccBufs) & 1) ^ 1);
+#endif
         tc_fence_after();
         if (lane == 0) {
           const uint32_t d = tm_acc0 + cbuf * BMT;
@@ -332,7 +346,7 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
             mma_tf32_ts(d, ah + kk * 8, dl, idesc, 1);
             mma_tf32_ts(d, al + kk * 8, dh, idesc, 1);
           }
-          tc_commit(&acc_full[cbuf]);
+          tc_commit(&acc_full[TNB_FULL_ALT ? (int)(s_it & 1) : cbuf]);
         }
         __syncwarp();
         ++s_it;
@@ -356,7 +370,73 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
         ++it;
       }
     }
-#if TNB_FULL_EPI8
+#if TNB_FULL_ALT
+  } else if (warp >= 4) {
+    // ===== two epilogue groups on alternate sub-tiles (TNB_FULL_ALT); group 1
+    // (warps 8-11) also loads the resident A block when the column block changes
+    const int q = warp & 3, g = (warp >> 2) - 1;
+    const bool loader = warp >= 8;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    uint32_t s_it = 0;
+    int64_t cur_cb = -1;
+    for (int64_t t = t0; t < t1; ++t) {
+      const int64_t cb = t / n_mt, mt = t - cb * n_mt;
+      if (loader && cb != cur_cb) {
+        cur_cb = cb;
+        named_sync(1, 160);
+        for (int nb = 0; nb < NB; ++nb) {
+          const int64_t n = cb * NB * BNB + nb * BNB + q * 32 + lane;
+          const bool nok = n < N;
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            uint32_t hi[32], lo[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int k = half * 32 + j;
+              const float x = (nok && k < K) ? __ldg(args.B + (int64_t)k * args.ldb + n) : 0.f;
+              hi[j] = f2tf32(x);
+              lo[j] = __float_as_uint(x - __uint_as_float(hi[j]));
+            }
+            TMEM_ST32(tm_a0 + nb * BNB + lane_base + half * 32, hi);
+            TMEM_ST32(tm_a0 + nb * BNB + lane_base + KMAX + half * 32, lo);
+          }
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        named_sync(2, 160);
+      }
+      for (int nb = 0; nb < NB; ++nb, ++s_it) {
+        if ((int)(s_it & 1) != g) continue;
+        mbar_wait(&acc_full[g], (s_it >> 1) & 1);
+        tc_fence_after();
+        const int64_t col = cb * NB * BNB + nb * BNB + q * 32 + lane;
+        uint32_t v[BMT];
+#pragma unroll
+        for (int ch = 0; ch < BMT / 32; ++ch) TMEM_LD32(tm_acc0 + lane_base + ch * 32, (v + ch * 32));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        mbar_arrive(&acc_empty[g]);
+        const int64_t rows_left = M - mt * BMT;
+        if (col < N) {
+          float* p = args.C + (mt * BMT) * args.ldc + col;
+          if (rows_left >= BMT) {
+#pragma unroll
+            for (int j = 0; j < BMT; ++j) {
+              st_stream(p, v[j]);
+              p += args.ldc;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < BMT; ++j) {
+              if (j < rows_left) st_stream(p, v[j]);
+              p += args.ldc;
+            }
+          }
+        }
+      }
+    }
+  }
+#elif TNB_FULL_EPI8
   } else if (warp >= 4) {
     // ===== epilogue on 8 warps (TNB_FULL_EPI8): warps 4-7 store the tile's
     // first 64 rows, warps 8-11 its last 64 (TMEM lane quarter = warp % 4);
