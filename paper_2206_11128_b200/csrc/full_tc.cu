@@ -253,6 +253,7 @@ struct alignas(64) TcArgs {
   int64_t ldc;
   int64_t M, N;
   int K;
+  int lockstep;             // tile order, see tile_at in the kernel
 };
 
 __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_constant__ TcArgs args) {
@@ -273,9 +274,26 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
   const int K = args.K;
   const int nk = (K + 7) >> 3;
   const int64_t n_mt = (M + BMT - 1) / BMT, n_cb = (N + NB * BNB - 1) / (NB * BNB);
-  const int64_t n_tiles = n_mt * n_cb;
-  const int64_t t0 = (n_tiles * blockIdx.x) / gridDim.x;
-  const int64_t t1 = (n_tiles * (blockIdx.x + 1)) / gridDim.x;
+  // Tile order.  lockstep: CTA b owns column block b + G w for a whole pass
+  // down the row tiles (w = 0 .. n_cb / G - 1, G = grid size), so at any time
+  // every CTA writes the SAME 128-row band of C, each its own 1.5 KB of every
+  // row -- the order DRAM likes (tools/store_bench.cu: 6.7 vs 5.5 TB/s for the
+  // same stores) and every CTA reads the same L tile from L2 at the same
+  // time.  The column blocks left over (n_cb mod G) are split evenly by
+  // tiles, as everything is without lockstep.
+  const int64_t G = gridDim.x, n_lock_cb = args.lockstep ? (n_cb / G) * G : 0;
+  const int64_t lock_cnt = (n_lock_cb / G) * n_mt;
+  const int64_t tail_tiles = (n_cb - n_lock_cb) * n_mt;
+  const int64_t tail0 = n_lock_cb * n_mt + (tail_tiles * blockIdx.x) / G;
+  const int64_t tail1 = n_lock_cb * n_mt + (tail_tiles * (blockIdx.x + 1)) / G;
+  const int64_t t_cnt = lock_cnt + (tail1 - tail0);
+  auto tile_at = [&](int64_t i) -> int64_t {  // i-th tile of this CTA as t = cb * n_mt + mt
+    if (i < lock_cnt) {
+      const int64_t w = i / n_mt;
+      return (w * G + blockIdx.x) * n_mt + (i - w * n_mt);
+    }
+    return tail0 + (i - lock_cnt);
+  };
 
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -307,7 +325,8 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
     const uint32_t sL0 = smem_u32(sL);
     int64_t cur_cb = -1;
     uint32_t idle_phase = 0, it = 0, s_it = 0;
-    for (int64_t t = t0; t < t1; ++t) {
+    for (int64_t ti = 0; ti < t_cnt; ++ti) {
+      const int64_t t = tile_at(ti);
       const int64_t cb = t / n_mt;
       if (cb != cur_cb) {
         if (cur_cb >= 0) {  // MMAs reading the old A must be done
@@ -361,7 +380,8 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
       uint64_t keep;
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
       uint32_t it = 0;
-      for (int64_t t = t0; t < t1; ++t) {
+      for (int64_t ti = 0; ti < t_cnt; ++ti) {
+      const int64_t t = tile_at(ti);
         const int64_t mt = t % n_mt;
         const int s = it % kStages;
         mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
@@ -379,7 +399,8 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     uint32_t s_it = 0;
     int64_t cur_cb = -1;
-    for (int64_t t = t0; t < t1; ++t) {
+    for (int64_t ti = 0; ti < t_cnt; ++ti) {
+      const int64_t t = tile_at(ti);
       const int64_t cb = t / n_mt, mt = t - cb * n_mt;
       if (loader && cb != cur_cb) {
         cur_cb = cb;
@@ -446,7 +467,8 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     uint32_t s_it = 0;
     int64_t cur_cb = -1;
-    for (int64_t t = t0; t < t1; ++t) {
+    for (int64_t ti = 0; ti < t_cnt; ++ti) {
+      const int64_t t = tile_at(ti);
       const int64_t cb = t / n_mt, mt = t - cb * n_mt;
       if (loader && cb != cur_cb) {
         cur_cb = cb;
@@ -515,7 +537,8 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
     uint32_t tma_it = 0;  // TMA stores this warp issued (staging buffer = tma_it & 1)
     (void)bulk_it;
     (void)tma_it;
-    for (int64_t t = t0; t < t1; ++t) {
+    for (int64_t ti = 0; ti < t_cnt; ++ti) {
+      const int64_t t = tile_at(ti);
       const int64_t cb = t / n_mt, mt = t - cb * n_mt;
       for (int nb = 0; nb < NB; ++nb) {
         const int cbuf = s_it % kAccBufs;
@@ -671,7 +694,8 @@ __global__ void __launch_bounds__(kThreads, 1) full_tc_gemm_kernel(const __grid_
     const int q = warp & 3;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     int64_t cur_cb = -1;
-    for (int64_t t = t0; t < t1; ++t) {
+    for (int64_t ti = 0; ti < t_cnt; ++ti) {
+      const int64_t t = tile_at(ti);
       const int64_t cb = t / n_mt;
       if (cb == cur_cb) continue;
       cur_cb = cb;
@@ -798,6 +822,10 @@ int launch_tc_gemm(const float* A, int64_t lda, int64_t sA, const float* B, int6
     a.M = M;
     a.N = N;
     a.K = K;
+    {
+      const char* ev = getenv("TNB_FULL_LOCKSTEP");
+      a.lockstep = !(ev && ev[0] == '0');
+    }
     full_tc_gemm_kernel<<<grid, kThreads, kSmemBytes, st>>>(a);
     rc = check_launch("full_tc_gemm");
     if (rc) return rc;

@@ -32,11 +32,41 @@ __global__ void __launch_bounds__(W * 32, 1) store_kernel(const __grid_constant_
   const int64_t nt = n_mt * n_cb;
   const int64_t t0 = nt * blockIdx.x / gridDim.x, t1 = nt * (blockIdx.x + 1) / gridDim.x;
   uint32_t it = 0;
-  for (int64_t t = t0; t < t1; ++t) {
-    const int64_t cb = t / n_mt, mt = t - cb * n_mt;
+  // MODE 4 / 5: the b32 stores of mode 0 with the CTAs in lockstep on one 128-row
+  // band: 4 = tiles in row-major order, grid-strided (adjacent CTAs write
+  // adjacent column tiles); 5 = CTA b keeps column tile b + 148 w for a whole
+  // pass down the rows (what a resident-operand GEMM needs), all CTAs at the
+  // same row band
+  const int64_t t_lo = MODE >= 4 ? 0 : t0, t_hi = MODE == 6 ? 2 * 3 * n_mt : MODE >= 4 ? (nt + gridDim.x - 1) / gridDim.x : t1;
+  for (int64_t tt = t_lo; tt < t_hi; ++tt) {
+    int64_t t = tt, cb, mt;
+    if (MODE == 4) {
+      t = tt * gridDim.x + blockIdx.x;
+      if (t >= nt) break;
+      mt = t / n_cb;
+      cb = t - mt * n_cb;
+    } else if (MODE == 5) {
+      const int64_t w = tt / n_mt;
+      mt = tt - w * n_mt;
+      cb = w * gridDim.x + blockIdx.x;
+      if (cb >= n_cb) break;
+    } else if (MODE == 6) {
+      // the GEMM's order: CTA b owns 384 columns (3 column tiles) of wave w; per
+      // row tile it writes the three 128 x 128 sub-tiles one after the other
+      const int64_t per = 3 * n_mt, w = tt / per, r = tt - w * per;
+      mt = r / 3;
+      cb = (w * gridDim.x + blockIdx.x) * 3 + (r - mt * 3);
+      if (cb >= n_cb) {
+        if (r - mt * 3 == 0 && (w * gridDim.x + blockIdx.x) * 3 >= n_cb) break;
+        continue;
+      }
+    } else {
+      cb = t / n_mt;
+      mt = t - cb * n_mt;
+    }
     const float base = (float)(t + lane);
 #define V(j) (base + (float)(j))
-    if (MODE == 0) {
+    if (MODE == 0 || MODE >= 4) {
       // W warps split the 128 columns x 128 rows: warp w: column group w % 4, rows half
       constexpr int RG = W / 4;  // row groups
       const int cg = warp & 3, rg = warp >> 2;
@@ -181,6 +211,10 @@ int main() {
     printf("%-34s %8.3f ms %8.1f GB/s\n", name, ms, bytes / (ms * 1e-3) / 1e9);
   };
   rep("st.b32 4 warps (current)", run<0, 4>(a, 0));
+  rep("st.b32 4 warps lockstep row-major", run<4, 4>(a, 0));
+  rep("st.b32 4 warps lockstep col-block", run<5, 4>(a, 0));
+  rep("st.b32 4 warps lockstep 384-col block", run<6, 4>(a, 0));
+  rep("st.b32 8 warps lockstep row-major", run<4, 8>(a, 0));
   rep("st.b32 8 warps", run<0, 8>(a, 0));
   rep("st.b32 16 warps", run<0, 16>(a, 0));
   rep("st.v4 4 warps", run<2, 4>(a, 0));
