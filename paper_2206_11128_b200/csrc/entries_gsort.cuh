@@ -95,6 +95,7 @@ struct GPlan {
   int64_t Kmid = 0;        // slices of the merged sorted mode
   int nsub = 1;            // row ranges of the first table in the sort key (L2 locality)
   int64_t sub_rows = 0;    // rows per range (0: none)
+  int chunk_shift = 0;     // > 0: the sample index >> chunk_shift leads the sort key (result windows, below)
   int64_t tinfo_off = 0;   // per-tile {first sorted position, bucket, rows}
   int64_t lvl_off[kMaxModes];  // mid level ending at original mode o (o > omid_lo)
   int64_t img_off = 0, hist_off = 0, bstart_off = 0, tbase_off = 0, cursor_off = 0;
@@ -105,6 +106,7 @@ struct GsPrep {
   int32_t n0;
   uint32_t K;
   uint32_t Kmid, sub_rows;  // key = (first row / sub_rows) * Kmid + merged index (sub_rows 0: no row ranges)
+  uint32_t chunk_shift;     // or key = (sample >> chunk_shift) * Kmid + merged index (0: none)
   int32_t oJ[kMaxModes];
   // C-order weight of mode o inside its group, in the group's field (first /
   // sorted / diag / last) and zero in the other three: no branches per mode
@@ -201,6 +203,30 @@ bool plan_gsort_with(const ChainDev& ch, int64_t m, GPlan* G, int64_t wide_rows)
       G->sub_rows = (rowsP + ns - 1) / ns;
     }
   }
+  // A result too large for L2 is written one window of samples at a time: the
+  // compute kernel stores every value at its sample's position (4 scattered
+  // bytes), which the memory system retires at ~16 G stores/s once the result
+  // no longer fits in L2 (2^26 samples: 4.2 ms of stores alone).  With the
+  // sample index's high bits leading the sort key, the CTAs (interleaved)
+  // sweep one 2^23-sample window at a time and its 32 MB of results fill
+  // whole lines in L2 before they are written back (cfg2 chain, 2^26 tuples:
+  // 7.7 -> 6.2 ms; 2^25: 3.76 -> 2.90 ms, 3.22 with 2^22-sample windows and
+  // their 8192 buckets).
+  G->chunk_shift = 0;
+  {
+    const char* e = getenv("TNB_GS_CHUNK_LOG2");  // 0: off; n: 2^n-sample windows whatever the result size (tests)
+    int sh = e ? atoi(e) : 23;
+    if (G->nsub == 1 && sh > 0 && sh < 31 && (e || m * 4 > ((int64_t)64 << 20))) {
+      auto nchunk = [&](int b) { return (m + ((int64_t)1 << b) - 1) >> b; };
+      // windows of up to 64 MB when the bucket count would outgrow the shared-memory histograms
+      while (!e && sh < 24 && K * nchunk(sh) > kGsSmemK) ++sh;
+      const int64_t nc = nchunk(sh);
+      if (nc > 1 && K * nc <= kGsSmemK && K * nc * 512 <= m) {
+        G->chunk_shift = sh;
+        G->nsub = (int)nc;  // the windows take the row ranges' place in the key
+      }
+    }
+  }
   K *= G->nsub;
   G->K = K;
   // the bucketed kernels' slice copies are not needed here
@@ -216,7 +242,7 @@ bool plan_gsort_with(const ChainDev& ch, int64_t m, GPlan* G, int64_t wide_rows)
     rows *= ch.m[o].J;
     G->lvl_off[o] = take(rows * ch.m[o].rr * 4);
   }
-  G->img_off = take(K * kGsImgBytes);
+  G->img_off = take(G->Kmid * kGsImgBytes);
   G->hist_off = take(K * 4 + 16);  // + 3 hot-row counters (gs_detect_hot_kernel)
   G->bstart_off = take((K + 1) * 4);
   G->tbase_off = take((K + 1) * 4);
@@ -286,8 +312,9 @@ int gs_build_mid(const ChainDev& ch, const GPlan& G, unsigned char* base, cudaSt
     rows *= ch.m[o].J;
     jrest *= ch.m[o].J;
   }
-  const int g = (int)std::min<int64_t>(ceil_div(G.K * 256, 256), (int64_t)num_sms() * 8);
-  gs_mid_image_kernel<<<g, 256, 0, st>>>(in, G.K, jrest, G.r0, G.r1, base + G.img_off);
+  // one image per slice of the merged mode (the kernel maps bucket -> bucket % Kmid)
+  const int g = (int)std::min<int64_t>(ceil_div(G.Kmid * 256, 256), (int64_t)num_sms() * 8);
+  gs_mid_image_kernel<<<g, 256, 0, st>>>(in, G.Kmid, jrest, G.r0, G.r1, base + G.img_off);
   return check_launch("gsort mid image");
 }
 
@@ -330,6 +357,7 @@ __global__ void __launch_bounds__(kGsPrepThreads) gs_prep_kernel(const __grid_co
   auto emit = [&](int64_t s) {
     if (badm < N0) atomicMin(err, badm);
     if (gp.sub_rows) f1 += (f0 / gp.sub_rows) * gp.Kmid;
+    if (gp.chunk_shift) f1 += (uint32_t)(s >> gp.chunk_shift) * gp.Kmid;
     recu[s] = make_uint4(f1, f0, f3, f2);
     if (SH) {
       atomicAdd(&gs_sh[f1], 1u);
@@ -1196,6 +1224,7 @@ void gs_fill_prep(const ChainDev& ch, const GPlan& G, GsPrep* gp) {
   gp->K = (uint32_t)G.K;
   gp->Kmid = (uint32_t)G.Kmid;
   gp->sub_rows = (uint32_t)G.sub_rows;
+  gp->chunk_shift = (uint32_t)G.chunk_shift;
   for (int g = 0; g < mp.ng; ++g) {
     const int f = g == 0 ? 0 : (g == mp.ng - 1 ? 3 : (g == G.gdiag ? 2 : 1));
     // the sorted field runs over ALL merged interior groups (one original mode each)

@@ -235,3 +235,29 @@ def test_gsort_batched_cfg2_shape_plan():
     sel = np.arange(0, m, 509)
     o = O.make_chain([("tt", c) for c in cores], B)
     assert_close(got[torch.as_tensor(sel, device=got.device)], O.entries(o, idx[sel]))
+
+
+@pytest.mark.parametrize("log2", ["16", "18"])
+def test_gsort_result_windows(log2, monkeypatch):
+    # results too large for L2 are written one window of samples at a time
+    # (the sample index's high bits lead the sort key, CTAs interleaved);
+    # TNB_GS_CHUNK_LOG2 forces small windows here.  Per-sample values do not
+    # depend on the sort order: bitwise equal to the unwindowed call.
+    monkeypatch.setenv("TNB_PREFIX_MAX_ROWS", "512")
+    monkeypatch.setenv("TNB_SUFFIX_MAX_ROWS", "512")
+    nodes = [("tt", c, None) for c in O.random_tt((8,) * 8, 16, seed=9, scale=0.25)]
+    t, o = facade(nodes), O.make_chain(nodes)
+    m = 700001  # ragged last window
+    idx = O.uniform_indices(t.shape, m, 5)
+    idx[::5] -= np.asarray(t.shape)
+    monkeypatch.setenv("TNB_GS_CHUNK_LOG2", "0")
+    ref = tb.entries(t, idx, algo=N.ALGO_GSORT)
+    monkeypatch.setenv("TNB_GS_CHUNK_LOG2", log2)
+    got = tb.entries(t, idx, algo=N.ALGO_GSORT)
+    assert torch.equal(got, ref)
+    sel = np.arange(0, m, 53)
+    assert_close(got[torch.from_numpy(sel).cuda()], O.entries(o, idx[sel]))
+    bad = idx.copy()
+    bad[m - 3, 6] = 8
+    with pytest.raises(tb.ContractViolationError, match="mode 6"):
+        tb.entries(t, bad, algo=N.ALGO_GSORT)
