@@ -38,7 +38,8 @@ print("%s m=2^%s windows=%s: %.3f ms/step  checksum %.6e" % (cfg, sys.argv[2], o
 '''
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 for lg in (sys.argv[2:] or ["26"]):
-    for w in ("0", None, "23"):
+    for w in (os.environ.get("BIG_M_WINDOWS", "0,auto,23").split(",")):
+        w = None if w == "auto" else w
         env = dict(os.environ)
         if w is None:
             env.pop("TNB_GS_CHUNK_LOG2", None)
