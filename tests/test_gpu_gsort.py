@@ -261,3 +261,24 @@ def test_gsort_result_windows(log2, monkeypatch):
     bad[m - 3, 6] = 8
     with pytest.raises(tb.ContractViolationError, match="mode 6"):
         tb.entries(t, bad, algo=N.ALGO_GSORT)
+
+
+@pytest.mark.slow
+def test_gsort_result_windows_default_above_64mb(monkeypatch):
+    # a result above 64 MB takes the windowed sort key by default; same bits as
+    # the unwindowed call, values against the oracle on a subsample
+    monkeypatch.setenv("TNB_PREFIX_MAX_ROWS", "512")
+    monkeypatch.setenv("TNB_SUFFIX_MAX_ROWS", "512")
+    nodes = [("tt", c, None) for c in O.random_tt((8,) * 8, 16, seed=13, scale=0.25)]
+    t, o = facade(nodes), O.make_chain(nodes)
+    m = (1 << 24) + (1 << 21) + 77
+    g = torch.Generator(device="cuda")
+    g.manual_seed(17)
+    idx = torch.randint(0, 8, (m, 8), device="cuda", generator=g)
+    monkeypatch.delenv("TNB_GS_CHUNK_LOG2", raising=False)
+    got = tb.entries(t, idx, algo=N.ALGO_GSORT)
+    monkeypatch.setenv("TNB_GS_CHUNK_LOG2", "0")
+    ref = tb.entries(t, idx, algo=N.ALGO_GSORT)
+    assert torch.equal(got, ref)
+    sel = torch.arange(0, m, 4099, device="cuda")
+    assert_close(got[sel], O.entries(o, idx[sel].cpu().numpy()))
